@@ -1,0 +1,241 @@
+/*
+ * pipeboost.h — C ABI of the B200-native PipeBoost layer-sharded cold start.
+ *
+ * Method (PAPER.md = "P:L<line>"; SURVEY.md §8 is the scope contract):
+ *   plan    — which GPU loads which layers, in which order
+ *   load    — each GPU DMAs its own disjoint slice over PCIe    P:L235-236 ("GPU 0 reads A-0 while GPU 1 reads A-1")
+ *   merge   — W' = W + (alpha/r) * B * A on the loader          P:L111-114, P:L267-270 (merged LoRA, §4.3.2)
+ *   gather  — merged slices all-gathered over NVLink            P:L239, P:L247 (progressive loading of the rest)
+ *   prefill — pipeline-parallel first token as layers arrive    P:L259-264 (§4.3.1)
+ *
+ * Conventions for every entry point:
+ *   - Returns pb_status: 0 (PB_OK) or a negative error; never throws, never aborts.
+ *     pb_last_error() returns a thread-local, human-readable message for the
+ *     last failing call on the calling thread.
+ *   - Preconditions (null pointers, ranges, call order) are checked synchronously.
+ *     Asynchronous CUDA failures surface at the next blocking call
+ *     (pb_sync, pb_prefill_wait, pb_prefill_first_token).
+ *   - Pointers: "host" = CPU memory, "device" = memory of the rank's CUDA device.
+ *     The caller owns every buffer and every stream; the library BORROWS them
+ *     for the lifetime of the object it hands them to. The library owns only
+ *     pb_plan, pb_ctx, and the CUDA events / tensor maps / IPC mappings inside a ctx.
+ *   - One process (or one logical rank) per GPU. A pb_ctx belongs to one rank;
+ *     calls on distinct contexts may run concurrently from different host threads
+ *     (the paper coordinates GPUs with threads); calls on the same ctx
+ *     must not.
+ *   - Data type: weights and LoRA factors are bf16 (north star; the paper never
+ *     states its dtype). Residual stream and logits are fp32.
+ */
+#ifndef PIPEBOOST_H
+#define PIPEBOOST_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define PB_API __attribute__((visibility("default")))
+#else
+#define PB_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    PB_OK = 0,
+    PB_EINVAL = -1,        /* bad argument: null pointer, out-of-range value, buffer too small for the plan */
+    PB_EPARTITION = -2,    /* n_gpus > n_layers: no balanced contiguous partition */
+    PB_EPROTOCOL = -3,     /* call order violated (per rank: trial_begin -> load -> merge -> gather -> prefill) */
+    PB_ECUDA = -4,         /* a CUDA runtime/driver call failed (message has the CUDA error string) */
+    PB_ENOMEM = -6,        /* caller-provided capacity smaller than required (see pb_plan_sizes) */
+    PB_ENUMERIC = -7,      /* non-finite logits */
+    PB_EUNSUPPORTED = -8   /* valid request this build does not implement (message says which) */
+} pb_status;
+
+typedef enum { PB_ARCH_OPT = 0, PB_ARCH_LLAMA = 1 } pb_arch;
+
+/* Decoder description (HF conventions). */
+typedef struct {
+    int32_t arch;          /* pb_arch */
+    int32_t n_layers;
+    int32_t d_model;
+    int32_t n_heads;
+    int32_t n_kv_heads;    /* == n_heads for OPT; GQA for Llama */
+    int32_t d_ffn;
+    int32_t vocab;
+    int32_t max_pos;       /* OPT learned positions: table has max_pos + 2 rows; ignored for Llama */
+    int32_t tied;          /* OPT: LM head tied to the token embedding */
+    float norm_eps;        /* 1e-5 */
+    float rope_theta;      /* 1e4 (Llama) */
+} pb_model_desc;
+
+/* LoRA targets (bit mask). OPT: Q,K,V,O,FC1,FC2. Llama: Q,K,V,O,GATE,UP,DOWN. */
+enum {
+    PB_T_Q = 1, PB_T_K = 2, PB_T_V = 4, PB_T_O = 8, PB_T_FC1 = 16, PB_T_FC2 = 32,
+    PB_T_GATE = 64, PB_T_UP = 128, PB_T_DOWN = 256
+};
+
+/* One adapter: B is [out x rank], A is [rank x in]; delta W = (alpha/rank) * B * A
+ * (Hu et al. naming; the paper's P:L113 swaps the names). */
+typedef struct {
+    int32_t rank;          /* 1..64 */
+    float alpha;
+    uint32_t targets;      /* PB_T_* mask */
+} pb_adapter_desc;
+
+typedef enum {
+    PB_LOAD_STAGE = 0,       /* GPU g loads its own stage's layers (paper, fig:ftpp_loading(c)) */
+    PB_LOAD_INTERLEAVE = 1   /* layer l loaded by GPU l mod N; stage owners receive the rest over NVLink */
+} pb_load_policy;
+
+typedef struct {
+    int32_t policy;            /* pb_load_policy */
+    int32_t vocab_sliced;      /* 1: embedding / LM head split into N balanced row slices, one per GPU (G5) */
+    int64_t chunk_bytes;       /* DMA chunk size (rows per chunk = chunk_bytes / row_bytes, rounded down to x128) */
+    int32_t prefill_chunks;    /* k >= 1 prompt chunks pipelined through the stages */
+    int32_t host_alias_layers; /* 0: host image holds every layer; K>0: layer l reads host image of layer l mod K */
+} pb_plan_opts;
+
+typedef struct pb_plan pb_plan;   /* opaque, immutable after creation, safe to share between threads */
+typedef struct pb_ctx pb_ctx;     /* opaque, one per rank */
+
+/* ------------------------------------------------------------------------ */
+/* a1 — plan (host only, pure, deterministic)                                 */
+/* ------------------------------------------------------------------------ */
+
+/* Build the plan for `n_gpus` GPUs. Layer stages are contiguous and balanced,
+ * the first (L mod N) stages one layer longer (remainder rule S:L130).
+ * Errors: PB_EINVAL (null, n_gpus < 1, bad model/adapter field), PB_EPARTITION (n_gpus > n_layers),
+ * PB_EUNSUPPORTED (rank > 64). *out receives a plan to release with pb_plan_free. */
+PB_API pb_status pb_plan_create(const pb_model_desc* model, const pb_adapter_desc* adapters, int32_t n_adapters,
+                         int32_t n_gpus, const pb_plan_opts* opts, pb_plan** out);
+
+/* Canonical text dump of the plan (stages, tensor table, chunks, per-GPU load and
+ * receive lists, adapter ownership, sizes). Writes at most cap bytes including the
+ * terminating NUL; *needed = full length + 1. PB_ENOMEM if cap is too small
+ * (buf then holds a truncated, NUL-terminated prefix). */
+PB_API pb_status pb_plan_dump(const pb_plan* plan, char* buf, size_t cap, size_t* needed);
+
+typedef struct {
+    int64_t host_base_bytes;     /* pinned host image of the base model (canonical layout) */
+    int64_t host_adapter_bytes;  /* pinned host image of all adapters */
+    int64_t dev_weight_bytes;    /* per-GPU device buffer: the whole model, same offsets on every GPU */
+    int64_t dev_adapter_bytes;   /* per-GPU device buffer for adapter factors (same layout as host) */
+    int32_t n_tensors, n_atensors, n_chunks, n_gpus;
+} pb_plan_sizes_t;
+PB_API pb_status pb_plan_sizes(const pb_plan* plan, pb_plan_sizes_t* out);
+
+/* Device workspace bytes a rank needs to prefill `batch` sequences of `seq` tokens. */
+PB_API pb_status pb_plan_workspace_bytes(const pb_plan* plan, int32_t batch, int32_t seq, int64_t* out);
+
+/* Base tensor i (0 <= i < n_tensors) of the canonical table. name is owned by the plan. */
+typedef struct {
+    const char* name;
+    int32_t rows, cols, layer;   /* layer = -1 for embed / pos / final norm / lm_head */
+    int64_t host_off, dev_off, bytes;
+} pb_tensor_info;
+PB_API pb_status pb_plan_tensor(const pb_plan* plan, int32_t i, pb_tensor_info* out);
+
+/* Adapter factor i (0 <= i < n_atensors): A ([rank x in]) or B ([out x rank]) of one target. */
+typedef struct {
+    const char* name;
+    int32_t rows, cols, layer, adapter, target_bit, is_B, base_tensor, base_row0;
+    int64_t off, bytes;          /* same offset in the host and device adapter buffers */
+} pb_atensor_info;
+PB_API pb_status pb_plan_atensor(const pb_plan* plan, int32_t i, pb_atensor_info* out);
+
+PB_API void pb_plan_free(pb_plan* plan);
+
+/* ------------------------------------------------------------------------ */
+/* Per-rank context                                                           */
+/* ------------------------------------------------------------------------ */
+
+typedef struct {
+    void* weights;        int64_t weights_cap;    /* device, >= dev_weight_bytes */
+    void* adapters;       int64_t adapters_cap;   /* device, >= dev_adapter_bytes (may be NULL if no adapters) */
+    void* workspace;      int64_t workspace_cap;  /* device, >= pb_plan_workspace_bytes(max_batch, max_seq) */
+    int32_t max_batch, max_seq;
+    void* stream_h2d[2];  /* cudaStream_t: copy-engine H2D lanes */
+    void* stream_merge;   /* cudaStream_t: merge kernels + per-layer readiness */
+    void* stream_nvlink;  /* cudaStream_t: peer (NVLink) receive copies */
+    void* stream_compute; /* cudaStream_t: prefill kernels */
+} pb_rank_bufs;
+
+/* Create rank `rank`'s context on the current CUDA device. host_base / host_adapters
+ * are PINNED host images in the canonical layout (cudaHostAlloc / torch pin_memory);
+ * host_adapters may be NULL when the plan has no adapters. Precomputes TMA tensor maps
+ * and events; enqueues nothing. Errors: PB_EINVAL, PB_ENOMEM (capacity), PB_ECUDA. */
+PB_API pb_status pb_ctx_create(const pb_plan* plan, int32_t rank, const void* host_base, const void* host_adapters,
+                        const pb_rank_bufs* bufs, pb_ctx** out);
+
+/* Cross-rank wiring (N > 1). Each rank exports an opaque blob of CUDA IPC handles
+ * (weights, workspace, flag words); every other rank imports it. Blobs are
+ * exchanged by the caller (e.g. torch.distributed all_gather_object).
+ * pb_ctx_export: *needed = blob size; PB_ENOMEM if cap too small. */
+PB_API pb_status pb_ctx_export(pb_ctx* ctx, void* blob, size_t cap, size_t* needed);
+PB_API pb_status pb_ctx_import_peer(pb_ctx* ctx, int32_t peer, const void* blob, size_t len);
+/* Same-process wiring (several ranks driven by one process, e.g. logical ranks on
+ * one GPU in tests, or one process driving N devices): peer pointers taken directly. */
+PB_API pb_status pb_ctx_link_local(pb_ctx* ctx, int32_t peer, pb_ctx* peer_ctx);
+
+/* Start cold-start trial `epoch` (>= 1, strictly increasing, identical on all ranks).
+ * Records t0 on stream_h2d[0]. Cross-rank readiness words are compared against the
+ * epoch, so device flags never need resetting. */
+PB_API pb_status pb_trial_begin(pb_ctx* ctx, uint32_t epoch);
+
+/* a2 — enqueue this rank's load list: chunked cudaMemcpyAsync pinned host -> HBM,
+ * alternating the two H2D streams; a `landed` event per chunk. Async. */
+PB_API pb_status pb_load_shard(pb_ctx* ctx);
+
+/* a3 — enqueue the LoRA merge of every adapted row range this rank loaded
+ * (tcgen05 kernel, in place, W <- RNE_bf16(W + s * B * A), fp32 accumulate), each
+ * after its chunks land; then per-layer readiness and peer signals. Must be called
+ * (even without adapters) after pb_load_shard. Async. adapter_id: which adapter to
+ * merge into the base weights (the single-adapter case; -1 = none). */
+PB_API pb_status pb_merge_lora(pb_ctx* ctx, int32_t adapter_id);
+
+/* a4 — enqueue this rank's receive list: for each chunk, wait for the loader's
+ * ready word (merged or landed), then copy peer HBM -> local HBM over NVLink
+ * (copy engine). Stage-needed chunks first, then rotation (g+i) mod N. Async. */
+PB_API pb_status pb_gather_layers(pb_ctx* ctx);
+
+/* a5 — pipelined first-token prefill. Every rank calls it (SPMD). tokens: host
+ * [batch][seq] int32 (read on rank 0 only; other ranks may pass NULL); the
+ * stages run layers as they become resident (no wait for the full model).
+ * Rank 0 receives the first tokens (host [batch], lowest index wins exact ties)
+ * and optionally the fp32 logits (host [batch][vocab] or NULL).
+ * pb_prefill_enqueue only enqueues; pb_prefill_wait blocks until this rank's work
+ * (and on rank 0 the token D2H) is complete; pb_prefill_first_token = both.
+ * Errors: PB_EINVAL (batch/seq out of range), PB_EPROTOCOL, PB_ECUDA, PB_ENUMERIC. */
+PB_API pb_status pb_prefill_enqueue(pb_ctx* ctx, const int32_t* tokens, int32_t batch, int32_t seq);
+PB_API pb_status pb_prefill_wait(pb_ctx* ctx, float* logits_out, int32_t* tokens_out);
+PB_API pb_status pb_prefill_first_token(pb_ctx* ctx, const int32_t* tokens, int32_t batch, int32_t seq,
+                                 float* logits_out, int32_t* tokens_out);
+
+/* Block until every stream of this rank is idle; surfaces async CUDA errors. */
+PB_API pb_status pb_sync(pb_ctx* ctx);
+
+/* Timeline of the last trial (valid after pb_sync / pb_prefill_wait), ms since t0
+ * on this rank's device clock. Arrays are owned by the ctx; valid until the next trial. */
+typedef struct {
+    double t_ready_ms;       /* every layer of this rank's stage resident and merged ("ready to serve") */
+    double t_full_ms;        /* this rank holds the whole merged model (strategy-switch point) */
+    double ttft_ms;          /* device time of the first-token D2H completion (rank 0), else last prefill op */
+    double load_done_ms;     /* last own chunk landed */
+    int64_t load_bytes;      /* bytes this rank moved over PCIe in the trial */
+    int64_t recv_bytes;      /* bytes this rank received over NVLink */
+    int32_t n_chunks;
+    const double* chunk_landed_ms;   /* [n_chunks], -1 where not loaded by this rank */
+    const double* chunk_gathered_ms; /* [n_chunks], -1 where not received by this rank */
+    int32_t n_launches;      /* kernels this rank launched in the trial */
+} pb_timeline_t;
+PB_API pb_status pb_timeline(pb_ctx* ctx, pb_timeline_t* out);
+
+PB_API const char* pb_last_error(void);
+PB_API void pb_ctx_free(pb_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PIPEBOOST_H */

@@ -1,0 +1,65 @@
+/*
+ * pipeboost_ops.h — the individual device kernels of the cold-start path, exposed for parity tests
+ * and micro-benchmarks. These are the SAME kernels pb_merge_lora / pb_prefill_* launch.
+ *
+ * All pointers are DEVICE pointers on the current CUDA device unless stated; `stream` is a
+ * cudaStream_t (NULL = legacy default stream). Calls are asynchronous; tensor maps are encoded on the
+ * host per call (so these entry points cost a few microseconds of host time more than the path).
+ * Returns PB_OK, PB_EINVAL (shape/alignment not supported) or PB_ECUDA (launch failed).
+ * Layouts are row-major; bf16 = IEEE bfloat16 bits (uint16).
+ */
+#ifndef PIPEBOOST_OPS_H
+#define PIPEBOOST_OPS_H
+
+#include "pipeboost.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* a3 merge: W[rows x cols] (row pitch ldw elems) <- RNE_bf16(W + scale * B * A),
+ * B [rows x rank] (pitch rank), A [rank x cols] (pitch cols); rank % 8 == 0, rank <= 64, cols % 8 == 0,
+ * 16-byte aligned bases. tcgen05.mma with fp32 TMEM accumulation. */
+PB_API pb_status pb_op_merge(void* W, int64_t ldw, int32_t rows, int32_t cols, const void* B, const void* A,
+                             int32_t rank, float scale, void* stream);
+
+/* Prefill GEMM: X [*, K] bf16 (rows [m_begin, m_end) used; the map spans x_rows rows), W [n_rows x K] bf16.
+ * epi 0: out bf16 [*, ldo] = (X W^T + bias) * (col < scale_cols ? scale : 1), ReLU if relu;
+ * epi 1: out fp32 [*, ldo] += X W^T + bias;
+ * epi 2: W = [gate; up] with N = d_ffn outputs: out bf16 = silu(X gate^T) * (X up^T).
+ * K % 64 == 0. bias may be NULL. */
+PB_API pb_status pb_op_gemm(const void* X, int32_t x_rows, int32_t m_begin, int32_t m_end, int32_t K, const void* W,
+                            int32_t n_rows, int32_t N, int32_t epi, const void* bias, int32_t relu, float scale,
+                            int32_t scale_cols, void* out, int32_t ldo, void* stream);
+
+/* LayerNorm (beta != NULL) or RMSNorm (beta == NULL): fp32 h [rows x d] -> bf16 out [rows x d]. */
+PB_API pb_status pb_op_norm(const float* h, int32_t rows, int32_t d, const void* gamma, const void* beta, float eps,
+                            void* out, void* stream);
+
+/* Causal attention (token-major rows t*B+b of qkv, row pitch ld): queries [t0, t1) of every sequence.
+ * q at col h*hd, k at k_col0 + kvh*hd, v at v_col0 + kvh*hd; out bf16 [*, ldo] at col h*hd. */
+PB_API pb_status pb_op_attention(const void* qkv, int32_t ld, void* out, int32_t ldo, int32_t t0, int32_t t1,
+                                 int32_t B, int32_t n_heads, int32_t n_kv_heads, int32_t hd, int32_t k_col0,
+                                 int32_t v_col0, float score_scale, void* stream);
+
+/* RoPE (rotate_half, theta) in place on q heads [0, n_q) at col 0 and k heads at k_col0, rows [r0, r1).
+ * table: device scratch of T*hd/2*8 bytes (filled here). */
+PB_API pb_status pb_op_rope(void* qkv, int32_t ld, int32_t r0, int32_t r1, int32_t B, int32_t T, int32_t n_q,
+                            int32_t n_k, int32_t hd, int32_t k_col0, float theta, void* table, void* stream);
+
+/* logits[b, v] (fp32, pitch ldl) = y[b] . E[v] for v in [v0, v1); y bf16 [B x d], B <= 8. */
+PB_API pb_status pb_op_logits(const void* y, int32_t B, int32_t d, const void* E, int32_t v0, int32_t v1,
+                              float* logits, int32_t ldl, void* stream);
+
+/* tokens[b] = argmax_v logits[b, v], lowest index on ties; nan_flag |= 1 on non-finite logits. */
+PB_API pb_status pb_op_argmax(const float* logits, int32_t B, int32_t V, int32_t ldl, int32_t* tokens,
+                              int32_t* nan_flag, void* stream);
+
+/* Embedding: h[row] = E[tok[row]] (+ pos[t + 2] when pos != NULL), rows [r0, r1), t = row / B. */
+PB_API pb_status pb_op_embed(const void* E, const void* pos, const int32_t* tok, float* h, int32_t d, int32_t r0,
+                             int32_t r1, int32_t B, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,188 @@
+"""Public Python API of the cold-start engine (thin: buffers, streams and wiring via torch; every
+step of the method runs in libpipeboost.so through the C ABI in _binding).
+
+    plan   = Plan(model, adapters, n_gpus, policy="stage", vocab_sliced=0, chunk_bytes=32 << 20)
+    eng    = RankEngine(plan, rank, host_base, host_adapters, max_batch=1, max_seq=128)
+    eng.wire_local([...]) | eng.wire_ipc(blobs)          # N > 1
+    toks   = eng.cold_start(epoch, tokens, adapter_id=0)  # a1..a5 for this rank; rank 0 gets the tokens
+
+One process per GPU (torch.distributed for the handle exchange), or several ranks driven from one
+process (logical ranks on one device for tests, or one process driving N devices).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import List, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _binding as B
+
+
+class Plan:
+    """pb_plan: immutable layer-to-GPU assignment, load and receive orders."""
+
+    def __init__(self, model, adapters: Sequence, n_gpus: int, policy: str = "stage", vocab_sliced: int = 0,
+                 chunk_bytes: int = 32 << 20, prefill_chunks: int = 1, host_alias_layers: int = 0):
+        self.model = model
+        self.adapters = tuple(adapters)
+        self.n_gpus = n_gpus
+        self.opts = B.plan_opts(policy, vocab_sliced, chunk_bytes, prefill_chunks, host_alias_layers)
+        self.handle = B.pb_plan_create(model, self.adapters, n_gpus, self.opts)
+        self.sizes = B.pb_plan_sizes(self.handle)
+
+    def dump(self) -> str:
+        return B.pb_plan_dump(self.handle)
+
+    def tensors(self):
+        out = []
+        for i in range(self.sizes.n_tensors):
+            t = B.pb_plan_tensor(self.handle, i)
+            out.append((t.name.decode(), t.rows, t.cols, t.host_off, t.layer, t.dev_off))
+        return out
+
+    def atensors(self):
+        out = []
+        for i in range(self.sizes.n_atensors):
+            t = B.pb_plan_atensor(self.handle, i)
+            out.append((t.name.decode(), t.rows, t.cols, t.off, t.adapter, t.is_B, t.base_tensor, t.base_row0))
+        return out
+
+    def workspace_bytes(self, batch: int, seq: int) -> int:
+        return B.pb_plan_workspace_bytes(self.handle, batch, seq)
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            B.pb_plan_free(h)
+            self.handle = None
+
+
+class RankEngine:
+    """One rank's pb_ctx plus the device buffers and streams it borrows."""
+
+    def __init__(self, plan: Plan, rank: int, host_base: torch.Tensor, host_adapters: Optional[torch.Tensor],
+                 max_batch: int = 1, max_seq: int = 128, device: Optional[torch.device] = None):
+        self.plan = plan
+        self.rank = rank
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        assert host_base.is_pinned(), "host_base must be pinned"
+        self.host_base = host_base
+        self.host_adapters = host_adapters
+        s = plan.sizes
+        with torch.cuda.device(self.device):
+            self.weights = torch.empty(s.dev_weight_bytes, dtype=torch.uint8, device=self.device)
+            self.adapters = torch.empty(max(s.dev_adapter_bytes, 1), dtype=torch.uint8, device=self.device)
+            ws = plan.workspace_bytes(max_batch, max_seq)
+            self.workspace = torch.empty(ws, dtype=torch.uint8, device=self.device)
+            self.streams = [torch.cuda.Stream(self.device) for _ in range(5)]
+        self.bufs = B.pb_rank_bufs()
+        self.bufs.weights = self.weights.data_ptr()
+        self.bufs.weights_cap = self.weights.numel()
+        self.bufs.adapters = self.adapters.data_ptr() if s.dev_adapter_bytes else None
+        self.bufs.adapters_cap = s.dev_adapter_bytes
+        self.bufs.workspace = self.workspace.data_ptr()
+        self.bufs.workspace_cap = self.workspace.numel()
+        self.bufs.max_batch = max_batch
+        self.bufs.max_seq = max_seq
+        self.bufs.stream_h2d[0] = self.streams[0].cuda_stream
+        self.bufs.stream_h2d[1] = self.streams[1].cuda_stream
+        self.bufs.stream_merge = self.streams[2].cuda_stream
+        self.bufs.stream_nvlink = self.streams[3].cuda_stream
+        self.bufs.stream_compute = self.streams[4].cuda_stream
+        ha = host_adapters.data_ptr() if (host_adapters is not None and s.host_adapter_bytes) else None
+        with torch.cuda.device(self.device):
+            self.ctx = B.pb_ctx_create(plan.handle, rank, host_base.data_ptr(), ha, self.bufs)
+        self._out_tokens = np.zeros(max_batch, dtype=np.int32)
+
+    # ---- wiring
+    def export(self) -> bytes:
+        with torch.cuda.device(self.device):
+            return B.pb_ctx_export(self.ctx)
+
+    def wire_ipc(self, blobs: List[bytes]):
+        with torch.cuda.device(self.device):
+            for r, blob in enumerate(blobs):
+                if r != self.rank:
+                    B.pb_ctx_import_peer(self.ctx, r, blob)
+
+    def wire_local(self, engines: List["RankEngine"]):
+        with torch.cuda.device(self.device):
+            for e in engines:
+                if e.rank != self.rank:
+                    B.pb_ctx_link_local(self.ctx, e.rank, e.ctx)
+
+    # ---- the method
+    def invalidate(self):
+        """Put the weights buffer in an explicit cold state (0xFF) — not part of a trial."""
+        with torch.cuda.device(self.device):
+            self.weights.fill_(0xFF)
+            self.adapters.fill_(0xFF)
+            torch.cuda.synchronize(self.device)
+
+    def enqueue(self, epoch: int, tokens: Optional[np.ndarray], batch: int, seq: int, adapter_id: int = 0):
+        """Enqueue a1..a5 for this rank (non-blocking). tokens [batch, seq] int32 (needed on rank 0)."""
+        self._batch = batch
+        with torch.cuda.device(self.device):
+            B.pb_trial_begin(self.ctx, epoch)
+            B.pb_load_shard(self.ctx)
+            B.pb_merge_lora(self.ctx, adapter_id)
+            B.pb_gather_layers(self.ctx)
+            tp = None
+            if tokens is not None:
+                self._tok = np.ascontiguousarray(tokens, dtype=np.int32)
+                assert self._tok.shape == (batch, seq)
+                tp = self._tok.ctypes.data
+            B.pb_prefill_enqueue(self.ctx, tp, batch, seq)
+
+    def wait(self, want_logits: bool = False):
+        """Block until this rank's trial is done; rank 0 returns (tokens[B], logits[B, V] | None)."""
+        with torch.cuda.device(self.device):
+            logits, lp, tp = None, None, None
+            if self.rank == 0:
+                tp = self._out_tokens.ctypes.data
+                if want_logits:
+                    logits = np.empty((self._batch, self.plan.model.vocab), dtype=np.float32)
+                    lp = logits.ctypes.data
+            B.pb_prefill_wait(self.ctx, lp, tp)
+            B.pb_sync(self.ctx)
+            if self.rank == 0:
+                return self._out_tokens[:self._batch].copy(), logits
+            return None, None
+
+    def cold_start(self, epoch: int, tokens: Optional[np.ndarray], batch: int = None, seq: int = None,
+                   adapter_id: int = 0, want_logits: bool = False):
+        """One cold start on this rank (blocking). With several ranks in ONE process use enqueue() on
+        every rank first, then wait() — a rank's device work may wait on its peers' readiness words."""
+        if tokens is not None:
+            batch, seq = np.asarray(tokens).shape
+        self.enqueue(epoch, tokens, batch, seq, adapter_id)
+        return self.wait(want_logits)
+
+    def timeline(self) -> dict:
+        t = B.pb_timeline(self.ctx)
+        n = t.n_chunks
+        return {"t_ready_ms": t.t_ready_ms, "t_full_ms": t.t_full_ms, "ttft_ms": t.ttft_ms,
+                "load_done_ms": t.load_done_ms, "load_bytes": t.load_bytes, "recv_bytes": t.recv_bytes,
+                "n_launches": t.n_launches,
+                "chunk_landed_ms": np.ctypeslib.as_array(t.chunk_landed_ms, shape=(n,)).copy() if n else np.zeros(0),
+                "chunk_gathered_ms": np.ctypeslib.as_array(t.chunk_gathered_ms, shape=(n,)).copy() if n else np.zeros(0)}
+
+    def weights_bytes(self) -> np.ndarray:
+        return self.weights.cpu().numpy()
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            B.pb_ctx_free(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def pinned_host(nbytes: int) -> torch.Tensor:
+    return torch.empty(max(nbytes, 1), dtype=torch.uint8, pin_memory=True)

@@ -1,0 +1,94 @@
+// kernels.hpp — launchers of the device kernels (host-callable, asynchronous on `stream`).
+// Every launcher returns cudaError_t of the launch; kernels never allocate.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace pb {
+
+// ---------------------------------------------------------------- tensor maps (TMA)
+// Resolved once from the driver (cudaGetDriverEntryPoint), no libcuda link dependency.
+bool driver_init(char* err, size_t errlen);
+// 2-D bf16 tensor map: rows x cols row-major with row pitch `ld_elems`, box {box_cols, box_rows},
+// swizzle in bytes (0, 32, 64, 128). Returns false and fills err on failure.
+bool make_map_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld_elems,
+                   uint32_t box_rows, uint32_t box_cols, int swizzle_bytes, char* err, size_t errlen);
+
+// Stream memory operations / cross-rank readiness words.
+cudaError_t stream_wait_geq(cudaStream_t s, const uint32_t* dev_addr, uint32_t value);
+struct SignalTargets {
+    uint32_t* addr[8];
+    int n;
+};
+cudaError_t launch_signal(const SignalTargets& t, uint32_t value, cudaStream_t s);
+
+// ---------------------------------------------------------------- a3: LoRA merge (tcgen05)
+// W[rows x cols] (row pitch ldw) <- RNE_bf16(W + scale * B[rows x r] * A[r x cols]), fp32 accumulate in TMEM.
+// Maps: mapW box {64 cols, 128 rows} SW128; mapB box {rk, 128} with swizzle rk*2 bytes; mapA box {64, rk} SW128,
+// rk = r rounded up to 16 / 32 / 64 (zero-filled by TMA out of bounds).
+struct MergeMaps {
+    CUtensorMap W, B, A;
+};
+int merge_rk(int rank);  // padded K of the merge MMA (16, 32 or 64)
+bool make_merge_maps(MergeMaps* m, void* W, int64_t ldw, int rows, int cols, const void* B, const void* A, int rank,
+                     char* err, size_t errlen);
+cudaError_t launch_merge(const MergeMaps& maps, int rows, int cols, int rank, float scale, cudaStream_t s);
+
+// ---------------------------------------------------------------- prefill GEMM (tcgen05)
+// out = X[M x K] * W[N x K]^T with a fused epilogue. X rows [m_begin, m_end) are computed.
+enum GemmEpi : int {
+    EPI_BF16 = 0,      // out_bf16[m, n] = bf16((acc + bias[n]) * (n < scale_cols ? scale : 1)), optional ReLU
+    EPI_RESID = 1,     // h_f32[m, n] += acc + bias[n]
+    EPI_SILU_MUL = 2,  // W is [gate; up] (2*N_out x K); out_bf16[m, n] = bf16(silu(gate_n) * up_n), n < N_out
+};
+struct GemmArgs {
+    int M_begin, M_end;   // rows of X / out computed
+    int N, K;             // N = output columns (EPI_SILU_MUL: N_out), K = reduction length (multiple of 64)
+    int epi;
+    int relu;
+    int scale_cols;
+    float scale;
+    const __nv_bfloat16* bias;  // [N] or null
+    void* out;                  // bf16 [*, ldo] or fp32 [*, ldo]
+    int ldo;
+    int up_row0;                // EPI_SILU_MUL: first row of `up` in W (= N_out)
+};
+// Maps: X box {64, 128} SW128 over [max_rows x K]; W box {64, 128} (EPI_SILU_MUL: {64, 64}) SW128 over [rows x K].
+cudaError_t launch_gemm(const CUtensorMap& mapX, const CUtensorMap& mapW, const GemmArgs& a, cudaStream_t s);
+
+// ---------------------------------------------------------------- SIMT kernels
+// Row norm over d of fp32 rows -> bf16: LayerNorm (beta != null) or RMSNorm (beta == null).
+cudaError_t launch_norm(const float* h, int ldh, __nv_bfloat16* out, int ldo, int rows, int d, const __nv_bfloat16* gamma,
+                        const __nv_bfloat16* beta, float eps, cudaStream_t s);
+
+struct EmbedSrc {
+    const __nv_bfloat16* base[8];  // embedding table of each owner (peer pointers allowed)
+    int slice_begin[9];            // vocab rows [slice_begin[i], slice_begin[i+1]) live on owner i
+    int n;
+};
+// h[row, :] = E[tok[row]] (+ P[pos(row) + 2]) as fp32, rows [r0, r1), row = t * B + b.
+cudaError_t launch_embed(const EmbedSrc& E, const __nv_bfloat16* pos, const int32_t* tok, float* h, int d, int r0,
+                         int r1, int B, cudaStream_t s);
+
+// RoPE cos/sin table [T x hd/2] (float2), angles t * theta^(-2i/hd) computed in fp64.
+cudaError_t launch_rope_table(float2* table, int T, int hd, double theta, cudaStream_t s);
+// In-place rotate_half RoPE on q (n_q heads at col 0) and k (n_k heads at col q_cols) of rows [r0, r1).
+cudaError_t launch_rope(__nv_bfloat16* qkv, int ld, int r0, int r1, int B, int n_q, int n_k, int hd, int k_col0,
+                        const float2* table, cudaStream_t s);
+
+// Causal attention for query rows [t0, t1) (token-major rows t*B+b) against keys [0, t] of the same
+// sequence; q at col h*hd, k at k_col0 + (h/group)*hd, v at v_col0 + (h/group)*hd of `qkv`.
+cudaError_t launch_attention(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int ldo, int t0, int t1, int B,
+                             int n_heads, int n_kv_heads, int hd, int k_col0, int v_col0, float score_scale,
+                             cudaStream_t s);
+
+// logits[b, v] = sum_c y[b, c] * E[v, c] for v in [v0, v1) (fp32 out, row pitch ldl).
+cudaError_t launch_logits(const __nv_bfloat16* y, int B, int d, const __nv_bfloat16* E, int v0, int v1, float* logits,
+                          int ldl, cudaStream_t s);
+// tokens[b] = argmax_v logits[b, v] (lowest index on ties); *nan_flag |= 1 if any logit is not finite.
+cudaError_t launch_argmax(const float* logits, int B, int V, int ldl, int32_t* tokens, int32_t* nan_flag,
+                          cudaStream_t s);
+
+}  // namespace pb

@@ -1,0 +1,112 @@
+// ops.cpp — pb_op_*: the path's kernels behind the C ABI, one call = one kernel (for parity tests).
+#include <cuda_runtime.h>
+
+#include "../../include/pipeboost_ops.h"
+#include "errors.hpp"
+#include "kernels.hpp"
+
+using namespace pb;
+
+static pb_status cuda_status(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return PB_OK;
+    return fail(PB_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+extern "C" pb_status pb_op_merge(void* W, int64_t ldw, int32_t rows, int32_t cols, const void* B, const void* A,
+                                 int32_t rank, float scale, void* stream) {
+    if (!W || !B || !A) return fail(PB_EINVAL, "pb_op_merge: null pointer");
+    if (rank < 8 || rank > 64 || rank % 8 || cols % 8 || ldw % 8 || rows < 0 || cols < 0)
+        return fail(PB_EINVAL, "pb_op_merge: need rank%%8==0, rank<=64, cols%%8==0 (rank=%d cols=%d)", rank, cols);
+    if (!aligned16(W) || !aligned16(B) || !aligned16(A)) return fail(PB_EINVAL, "pb_op_merge: bases must be 16-B aligned");
+    if (rows == 0 || cols == 0) return PB_OK;
+    MergeMaps m;
+    char err[512];
+    if (!make_merge_maps(&m, W, ldw, rows, cols, B, A, rank, err, sizeof err)) return fail(PB_EINVAL, "%s", err);
+    return cuda_status(launch_merge(m, rows, cols, rank, scale, (cudaStream_t)stream), "merge");
+}
+
+extern "C" pb_status pb_op_gemm(const void* X, int32_t x_rows, int32_t m_begin, int32_t m_end, int32_t K,
+                                const void* W, int32_t n_rows, int32_t N, int32_t epi, const void* bias, int32_t relu,
+                                float scale, int32_t scale_cols, void* out, int32_t ldo, void* stream) {
+    if (!X || !W || !out) return fail(PB_EINVAL, "pb_op_gemm: null pointer");
+    if (K % 8 || K <= 0 || epi < 0 || epi > 2 || m_begin < 0 || m_end > x_rows)
+        return fail(PB_EINVAL, "pb_op_gemm: bad shape (K=%d epi=%d)", K, epi);
+    CUtensorMap mx, mw;
+    char err[512];
+    if (!make_map_bf16(&mx, X, x_rows, K, K, 128, 64, 128, err, sizeof err) ||
+        !make_map_bf16(&mw, W, n_rows, K, K, epi == EPI_SILU_MUL ? 64 : 128, 64, 128, err, sizeof err))
+        return fail(PB_EINVAL, "%s", err);
+    GemmArgs a{};
+    a.M_begin = m_begin;
+    a.M_end = m_end;
+    a.N = N;
+    a.K = K;
+    a.epi = epi;
+    a.relu = relu;
+    a.scale = scale;
+    a.scale_cols = scale_cols;
+    a.bias = static_cast<const __nv_bfloat16*>(bias);
+    a.out = out;
+    a.ldo = ldo;
+    a.up_row0 = N;
+    return cuda_status(launch_gemm(mx, mw, a, (cudaStream_t)stream), "gemm");
+}
+
+extern "C" pb_status pb_op_norm(const float* h, int32_t rows, int32_t d, const void* gamma, const void* beta, float eps,
+                                void* out, void* stream) {
+    if (!h || !gamma || !out) return fail(PB_EINVAL, "pb_op_norm: null pointer");
+    return cuda_status(launch_norm(h, d, static_cast<__nv_bfloat16*>(out), d, rows, d,
+                                   static_cast<const __nv_bfloat16*>(gamma), static_cast<const __nv_bfloat16*>(beta),
+                                   eps, (cudaStream_t)stream),
+                       "norm");
+}
+
+extern "C" pb_status pb_op_attention(const void* qkv, int32_t ld, void* out, int32_t ldo, int32_t t0, int32_t t1,
+                                     int32_t B, int32_t n_heads, int32_t n_kv_heads, int32_t hd, int32_t k_col0,
+                                     int32_t v_col0, float score_scale, void* stream) {
+    if (!qkv || !out) return fail(PB_EINVAL, "pb_op_attention: null pointer");
+    if (n_kv_heads <= 0 || n_heads % n_kv_heads) return fail(PB_EINVAL, "pb_op_attention: bad heads");
+    return cuda_status(launch_attention(static_cast<const __nv_bfloat16*>(qkv), ld, static_cast<__nv_bfloat16*>(out),
+                                        ldo, t0, t1, B, n_heads, n_kv_heads, hd, k_col0, v_col0, score_scale,
+                                        (cudaStream_t)stream),
+                       "attention");
+}
+
+extern "C" pb_status pb_op_rope(void* qkv, int32_t ld, int32_t r0, int32_t r1, int32_t B, int32_t T, int32_t n_q,
+                                int32_t n_k, int32_t hd, int32_t k_col0, float theta, void* table, void* stream) {
+    if (!qkv || !table) return fail(PB_EINVAL, "pb_op_rope: null pointer");
+    cudaError_t e = launch_rope_table(static_cast<float2*>(table), T, hd, theta, (cudaStream_t)stream);
+    if (e == cudaSuccess)
+        e = launch_rope(static_cast<__nv_bfloat16*>(qkv), ld, r0, r1, B, n_q, n_k, hd, k_col0,
+                        static_cast<const float2*>(table), (cudaStream_t)stream);
+    return cuda_status(e, "rope");
+}
+
+extern "C" pb_status pb_op_logits(const void* y, int32_t B, int32_t d, const void* E, int32_t v0, int32_t v1,
+                                  float* logits, int32_t ldl, void* stream) {
+    if (!y || !E || !logits) return fail(PB_EINVAL, "pb_op_logits: null pointer");
+    return cuda_status(launch_logits(static_cast<const __nv_bfloat16*>(y), B, d, static_cast<const __nv_bfloat16*>(E),
+                                     v0, v1, logits, ldl, (cudaStream_t)stream),
+                       "logits");
+}
+
+extern "C" pb_status pb_op_argmax(const float* logits, int32_t B, int32_t V, int32_t ldl, int32_t* tokens,
+                                  int32_t* nan_flag, void* stream) {
+    if (!logits || !tokens || !nan_flag) return fail(PB_EINVAL, "pb_op_argmax: null pointer");
+    return cuda_status(launch_argmax(logits, B, V, ldl, tokens, nan_flag, (cudaStream_t)stream), "argmax");
+}
+
+extern "C" pb_status pb_op_embed(const void* E, const void* pos, const int32_t* tok, float* h, int32_t d, int32_t r0,
+                                 int32_t r1, int32_t B, void* stream) {
+    if (!E || !tok || !h) return fail(PB_EINVAL, "pb_op_embed: null pointer");
+    EmbedSrc src{};
+    src.base[0] = static_cast<const __nv_bfloat16*>(E);
+    src.slice_begin[0] = 0;
+    src.slice_begin[1] = 0x7fffffff;
+    src.n = 1;
+    return cuda_status(launch_embed(src, static_cast<const __nv_bfloat16*>(pos), tok, h, d, r0, r1, B,
+                                    (cudaStream_t)stream),
+                       "embed");
+}

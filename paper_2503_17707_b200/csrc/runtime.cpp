@@ -1,0 +1,780 @@
+// runtime.cpp — pb_ctx: the per-rank cold-start engine.
+//
+//   pb_load_shard    (a2)  chunked cudaMemcpyAsync pinned host -> HBM over this GPU's own PCIe link,
+//                          alternating two copy-engine streams; a `landed` event per chunk
+//   pb_merge_lora    (a3)  per own chunk in load order: wait landed, tcgen05 merge of every adapted row
+//                          range (after its adapter factors land), then publish the chunk to the peers
+//                          (readiness word = epoch) and record per-tensor readiness
+//   pb_gather_layers (a4)  receive list: wait the loader's readiness word (cuStreamWaitValue32 on local
+//                          memory), copy peer HBM -> local HBM over NVLink (copy engine)
+//   pb_prefill_*     (a5)  pipelined first-token prefill: each stage runs its layers as they become ready,
+//                          hands the fp32 residual to the next stage (peer copy + readiness word),
+//                          vocab-parallel logits, argmax on rank 0, token D2H
+// Cross-rank dependencies are device-side (readiness words compared with the trial epoch), so the host
+// threads / processes of different ranks never wait for each other inside a trial.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <unistd.h>
+
+#include "errors.hpp"
+#include "runtime.hpp"
+
+using namespace pb;
+
+#define CU(call)                                                                                         \
+    do {                                                                                                 \
+        cudaError_t e_ = (call);                                                                         \
+        if (e_ != cudaSuccess) return fail(PB_ECUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+namespace {
+
+int64_t al(int64_t x, int64_t a = 256) { return (x + a - 1) / a * a; }
+
+int max_stage_layers(const pb_plan* p) {
+    int m = 0;
+    for (auto& s : p->stages) m = std::max(m, s.second - s.first);
+    return m;
+}
+
+int32_t qkv_dim(const pb_plan* p) { return (p->model.n_heads + 2 * p->model.n_kv_heads) * p->head_dim(); }
+
+// Head tensor: tied OPT -> embed, otherwise lm_head.
+int32_t head_tensor(const pb_plan* p) {
+    return p->model.arch == PB_ARCH_OPT && p->model.tied ? p->find_tensor("embed") : p->find_tensor("lm_head");
+}
+
+bool is_head_owner(const pb_plan* p, int32_t g) {
+    const int32_t ht = head_tensor(p);
+    for (auto& c : p->chunks)
+        if (!c.is_adapter && c.tensor == ht && c.loader == g) return true;
+    return false;
+}
+
+// Vocab rows [v0, v1) of the head this rank owns (contiguous by construction).
+void head_slice(const pb_plan* p, int32_t g, int32_t* v0, int32_t* v1) {
+    const int32_t ht = head_tensor(p);
+    *v0 = INT32_MAX;
+    *v1 = -1;
+    for (auto& c : p->chunks)
+        if (!c.is_adapter && c.tensor == ht && c.loader == g) {
+            *v0 = std::min(*v0, c.r0);
+            *v1 = std::max(*v1, c.r1);
+        }
+    if (*v1 < 0) *v0 = *v1 = 0;
+}
+
+pb_status check_ctx(pb_ctx* c, const char* fn) {
+    if (!c) return fail(PB_EINVAL, "%s: null ctx", fn);
+    cudaError_t e = cudaSetDevice(c->device);
+    if (e != cudaSuccess) return fail(PB_ECUDA, "%s: cudaSetDevice: %s", fn, cudaGetErrorString(e));
+    return PB_OK;
+}
+
+struct IpcBlob {
+    uint32_t magic;
+    int32_t rank;
+    int32_t device;
+    int32_t pid;
+    cudaIpcMemHandle_t wh, sh;
+    int64_t w_off, s_off;
+};
+constexpr uint32_t kMagic = 0x50424950;  // "PBIP"
+
+}  // namespace
+
+WsLayout pb::ws_layout(const pb_plan* p, int32_t batch, int32_t seq) {
+    WsLayout L;
+    const auto& m = p->model;
+    const int64_t rows = (int64_t)batch * seq;
+    const int64_t d = m.d_model, hd = p->head_dim(), qd = (int64_t)m.n_heads * hd, f = m.d_ffn;
+    const int k = std::max(1, p->opts.prefill_chunks);
+    L.max_rows = (int32_t)rows;
+    L.max_batch = batch;
+    L.max_seq = seq;
+    L.f_chunk = 0;
+    L.f_act = (int32_t)p->chunks.size();
+    L.f_y = L.f_act + k;
+    L.f_logit = L.f_y + 1;
+    L.n_words = L.f_logit + p->n_gpus;
+    int64_t o = 0;
+    L.flags = o;   o = al(o + 4 * (int64_t)L.n_words);
+    L.tokens = o;  o = al(o + 4 * rows);
+    L.h = o;       o = al(o + 4 * rows * d);
+    L.x = o;       o = al(o + 2 * rows * d);
+    L.n_qkv = k > 1 ? max_stage_layers(p) : 1;
+    L.qkv_stride = al(2 * rows * qkv_dim(p));
+    L.qkv = o;     o += L.qkv_stride * L.n_qkv;
+    L.attn = o;    o = al(o + 2 * rows * qd);
+    L.mlp = o;     o = al(o + 2 * rows * f);
+    L.y = o;       o = al(o + 2 * (int64_t)batch * d);
+    L.logits = o;  o = al(o + 4 * (int64_t)batch * m.vocab);
+    L.tok_out = o; o = al(o + 4 * (int64_t)batch);
+    L.nan = o;     o = al(o + 4);
+    L.rope = o;    o = al(o + (m.arch == PB_ARCH_LLAMA ? 8 * (int64_t)seq * (hd / 2) : 0));
+    L.total = al(o, 4096);
+    return L;
+}
+
+extern "C" pb_status pb_plan_workspace_bytes(const pb_plan* p, int32_t batch, int32_t seq, int64_t* out) {
+    if (!p || !out) return fail(PB_EINVAL, "pb_plan_workspace_bytes: null argument");
+    if (batch < 1 || batch > 8 || seq < 1) return fail(PB_EINVAL, "batch must be in [1, 8] and seq >= 1");
+    if (p->model.arch == PB_ARCH_OPT && seq > p->model.max_pos) return fail(PB_EINVAL, "seq > max_pos");
+    *out = ws_layout(p, batch, seq).total;
+    return PB_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+// context creation
+// ------------------------------------------------------------------------------------------------
+
+static pb_status build_merge_jobs(pb_ctx* c) {
+    const pb_plan* p = c->plan;
+    c->jobs_of_chunk.assign(p->chunks.size(), {});
+    char err[512];
+    // adapter chunks of each atensor
+    std::vector<std::vector<int32_t>> achunks(p->atensors.size());
+    for (auto& ch : p->chunks)
+        if (ch.is_adapter) achunks[ch.tensor].push_back(ch.id);
+    for (auto& mr : p->merges) {
+        const auto& bt = p->tensors[mr.base];
+        const auto& A = p->atensors[mr.a_tensor];
+        const auto& Bf = p->atensors[mr.b_tensor];
+        const int rank = p->adapters[mr.adapter].rank;
+        for (auto& ch : p->chunks) {
+            if (ch.is_adapter || ch.tensor != mr.base || ch.loader != c->rank) continue;
+            const int32_t ra = std::max(ch.r0, mr.row0), rb = std::min(ch.r1, mr.row0 + mr.rows);
+            if (rb <= ra) continue;
+            if (rank % 8 != 0)
+                return fail(PB_EUNSUPPORTED, "merge needs rank %% 8 == 0 (TMA 16-byte row pitch), got %d", rank);
+            MergeJob j;
+            j.chunk = ch.id;
+            j.adapter = mr.adapter;
+            j.rows = rb - ra;
+            j.cols = mr.cols;
+            j.rank = rank;
+            j.scale = p->adapters[mr.adapter].alpha / (float)rank;
+            j.need = achunks[mr.a_tensor];
+            j.need.insert(j.need.end(), achunks[mr.b_tensor].begin(), achunks[mr.b_tensor].end());
+            char* W = c->weights + bt.dev_off + (int64_t)ra * bt.row_bytes();
+            const char* Bp = c->adapters + Bf.off + (int64_t)(ra - mr.row0) * Bf.row_bytes();
+            const char* Ap = c->adapters + A.off;
+            if (!make_merge_maps(&j.maps, W, bt.cols, j.rows, j.cols, Bp, Ap, rank, err, sizeof err))
+                return fail(PB_EINVAL, "merge map: %s", err);
+            c->jobs_of_chunk[ch.id].push_back((int32_t)c->jobs.size());
+            c->jobs.push_back(j);
+        }
+    }
+    return PB_OK;
+}
+
+static pb_status build_prefill_maps(pb_ctx* c) {
+    const pb_plan* p = c->plan;
+    const auto& m = p->model;
+    const int64_t d = m.d_model, qd = (int64_t)m.n_heads * p->head_dim(), f = m.d_ffn;
+    const int64_t R = c->L.max_rows;
+    char err[512];
+    if (!make_map_bf16(&c->map_x, c->ws + c->L.x, R, d, d, 128, 64, 128, err, sizeof err) ||
+        !make_map_bf16(&c->map_attn, c->ws + c->L.attn, R, qd, qd, 128, 64, 128, err, sizeof err) ||
+        !make_map_bf16(&c->map_mlp, c->ws + c->L.mlp, R, f, f, 128, 64, 128, err, sizeof err))
+        return fail(PB_EINVAL, "activation map: %s", err);
+    c->lmaps.assign(m.n_layers, LayerMaps{});
+    const auto st = p->stages[c->rank];
+    for (int l = st.first; l < st.second; ++l) {
+        auto T = [&](const char* s) -> const TensorRec& {
+            return p->tensors[p->find_tensor("L" + std::to_string(l) + "." + s)];
+        };
+        const bool opt = m.arch == PB_ARCH_OPT;
+        const TensorRec& q = T("qkv");
+        const TensorRec& o = T("o");
+        const TensorRec& up = T(opt ? "fc1" : "gate_up");
+        const TensorRec& dn = T(opt ? "fc2" : "down");
+        LayerMaps& lm = c->lmaps[l];
+        if (!make_map_bf16(&lm.qkv, c->weights + q.dev_off, q.rows, q.cols, q.cols, 128, 64, 128, err, sizeof err) ||
+            !make_map_bf16(&lm.o, c->weights + o.dev_off, o.rows, o.cols, o.cols, 128, 64, 128, err, sizeof err) ||
+            !make_map_bf16(&lm.up, c->weights + up.dev_off, up.rows, up.cols, up.cols, opt ? 128 : 64, 64, 128, err,
+                           sizeof err) ||
+            !make_map_bf16(&lm.down, c->weights + dn.dev_off, dn.rows, dn.cols, dn.cols, 128, 64, 128, err, sizeof err))
+            return fail(PB_EINVAL, "weight map layer %d: %s", l, err);
+    }
+    return PB_OK;
+}
+
+extern "C" pb_status pb_ctx_create(const pb_plan* plan, int32_t rank, const void* host_base, const void* host_adapters,
+                                   const pb_rank_bufs* bufs, pb_ctx** out) {
+    PB_TRY_BEGIN
+    if (!plan || !host_base || !bufs || !out) return fail(PB_EINVAL, "pb_ctx_create: null argument");
+    *out = nullptr;
+    if (rank < 0 || rank >= plan->n_gpus) return fail(PB_EINVAL, "rank %d out of [0, %d)", rank, plan->n_gpus);
+    if (!bufs->weights || bufs->weights_cap < plan->dev_weight_bytes)
+        return fail(PB_ENOMEM, "weights buffer: need %lld bytes", (long long)plan->dev_weight_bytes);
+    if (!plan->adapters.empty() && (!bufs->adapters || bufs->adapters_cap < plan->host_adapter_bytes || !host_adapters))
+        return fail(PB_ENOMEM, "adapters buffer: need %lld bytes (and a host image)", (long long)plan->host_adapter_bytes);
+    if (bufs->max_batch < 1 || bufs->max_batch > 8 || bufs->max_seq < 1)
+        return fail(PB_EINVAL, "max_batch must be in [1, 8], max_seq >= 1");
+    if (plan->model.arch == PB_ARCH_OPT && bufs->max_seq > plan->model.max_pos)
+        return fail(PB_EINVAL, "max_seq %d > max_pos %d", bufs->max_seq, plan->model.max_pos);
+    const int hd = plan->head_dim();
+    if (hd != 32 && hd != 64 && hd != 128) return fail(PB_EUNSUPPORTED, "head_dim %d (supported: 32, 64, 128)", hd);
+    if (plan->model.d_model % 64 || plan->model.d_ffn % 8 || plan->model.d_model > 256 * 40)
+        return fail(PB_EUNSUPPORTED, "d_model must be a multiple of 64 (<= 10240), d_ffn of 8");
+    WsLayout L = ws_layout(plan, bufs->max_batch, bufs->max_seq);
+    if (!bufs->workspace || bufs->workspace_cap < L.total)
+        return fail(PB_ENOMEM, "workspace: need %lld bytes", (long long)L.total);
+    char err[256];
+    if (!driver_init(err, sizeof err)) return fail(PB_ECUDA, "%s", err);
+
+    auto* c = new pb_ctx();
+    c->plan = plan;
+    c->rank = rank;
+    c->n = plan->n_gpus;
+    cudaGetDevice(&c->device);
+    c->weights = static_cast<char*>(bufs->weights);
+    c->adapters = static_cast<char*>(bufs->adapters);
+    c->ws = static_cast<char*>(bufs->workspace);
+    c->bufs = *bufs;
+    c->h2d[0] = (cudaStream_t)bufs->stream_h2d[0];
+    c->h2d[1] = (cudaStream_t)bufs->stream_h2d[1];
+    c->merge = (cudaStream_t)bufs->stream_merge;
+    c->nv = (cudaStream_t)bufs->stream_nvlink;
+    c->comp = (cudaStream_t)bufs->stream_compute;
+    c->L = L;
+    c->host_base = host_base;
+    c->host_adapters = host_adapters;
+    c->peers.assign(c->n, Peer{});
+    c->peers[rank].weights = c->weights;
+    c->peers[rank].ws = c->ws;
+    c->peers[rank].linked = true;
+
+    auto cleanup = [&](pb_status st) { pb_ctx_free(c); return st; };
+    const size_t NC = plan->chunks.size(), NT = plan->tensors.size();
+    c->landed.assign(NC, nullptr);
+    c->gathered.assign(NC, nullptr);
+    c->tensor_ready.assign(NT, nullptr);
+    c->tl_landed.assign(NC, -1.0);
+    c->tl_gathered.assign(NC, -1.0);
+    auto mk = [&](cudaEvent_t* e) { return cudaEventCreate(e); };
+    if (mk(&c->t0) || mk(&c->merge_done) || mk(&c->gather_done) || mk(&c->done))
+        return cleanup(fail(PB_ECUDA, "cudaEventCreate failed"));
+    for (int32_t id : plan->load[rank])
+        if (mk(&c->landed[id])) return cleanup(fail(PB_ECUDA, "cudaEventCreate failed"));
+    for (int32_t id : plan->recv[rank])
+        if (mk(&c->gathered[id])) return cleanup(fail(PB_ECUDA, "cudaEventCreate failed"));
+    for (size_t t = 0; t < NT; ++t)
+        if (mk(&c->tensor_ready[t])) return cleanup(fail(PB_ECUDA, "cudaEventCreate failed"));
+    // per-tensor last own / received chunk
+    c->last_own_chunk.assign(NT, -1);
+    c->last_recv_chunk.assign(NT, -1);
+    for (int32_t id : plan->load[rank])
+        if (!plan->chunks[id].is_adapter) c->last_own_chunk[plan->chunks[id].tensor] = id;
+    for (int32_t id : plan->recv[rank]) c->last_recv_chunk[plan->chunks[id].tensor] = id;
+
+    pb_status st = build_merge_jobs(c);
+    if (st != PB_OK) return cleanup(st);
+    st = build_prefill_maps(c);
+    if (st != PB_OK) return cleanup(st);
+    if (cudaHostAlloc((void**)&c->h_tokens, sizeof(int32_t) * L.max_rows, cudaHostAllocPortable) != cudaSuccess ||
+        cudaHostAlloc((void**)&c->h_out, sizeof(int32_t) * (L.max_batch + 1), cudaHostAllocPortable) != cudaSuccess)
+        return cleanup(fail(PB_ECUDA, "cudaHostAlloc failed"));
+    // readiness words start at 0 (epochs are >= 1)
+    if (cudaMemset(c->ws + L.flags, 0, 4 * (size_t)L.n_words) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
+        return cleanup(fail(PB_ECUDA, "flag init failed"));
+    *out = c;
+    return PB_OK;
+    PB_TRY_END
+}
+
+extern "C" void pb_ctx_free(pb_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    auto d = [](cudaEvent_t e) { if (e) cudaEventDestroy(e); };
+    d(c->t0); d(c->merge_done); d(c->gather_done); d(c->done);
+    for (auto e : c->landed) d(e);
+    for (auto e : c->gathered) d(e);
+    for (auto e : c->tensor_ready) d(e);
+    for (auto& p : c->peers)
+        for (void* b : p.ipc_bases) cudaIpcCloseMemHandle(b);
+    if (c->h_tokens) cudaFreeHost(c->h_tokens);
+    if (c->h_out) cudaFreeHost(c->h_out);
+    delete c;
+}
+
+// ------------------------------------------------------------------------------------------------
+// cross-rank wiring
+// ------------------------------------------------------------------------------------------------
+
+extern "C" pb_status pb_ctx_export(pb_ctx* c, void* blob, size_t cap, size_t* needed) {
+    pb_status st = check_ctx(c, "pb_ctx_export");
+    if (st) return st;
+    if (!needed) return fail(PB_EINVAL, "pb_ctx_export: null needed");
+    *needed = sizeof(IpcBlob);
+    if (!blob || cap < sizeof(IpcBlob)) return fail(PB_ENOMEM, "pb_ctx_export: need %zu bytes", sizeof(IpcBlob));
+    IpcBlob b{};
+    b.magic = kMagic;
+    b.rank = c->rank;
+    b.device = c->device;
+    b.pid = (int32_t)getpid();
+    void* base = nullptr;
+    size_t size = 0;
+    CU(cudaIpcGetMemHandle(&b.wh, c->weights));
+    {
+        CUdeviceptr bp;
+        size_t sz;
+        // offset of our pointer inside its allocation
+        using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+        static GetRange fn = nullptr;
+        if (!fn) {
+            cudaDriverEntryPointQueryResult q;
+            cudaGetDriverEntryPoint("cuMemGetAddressRange", (void**)&fn, cudaEnableDefault, &q);
+        }
+        if (!fn) return fail(PB_ECUDA, "cuMemGetAddressRange unavailable");
+        if (fn(&bp, &sz, (CUdeviceptr)c->weights) != CUDA_SUCCESS) return fail(PB_ECUDA, "cuMemGetAddressRange(weights)");
+        b.w_off = (int64_t)((CUdeviceptr)c->weights - bp);
+        if (fn(&bp, &sz, (CUdeviceptr)c->ws) != CUDA_SUCCESS) return fail(PB_ECUDA, "cuMemGetAddressRange(ws)");
+        b.s_off = (int64_t)((CUdeviceptr)c->ws - bp);
+    }
+    (void)base;
+    (void)size;
+    CU(cudaIpcGetMemHandle(&b.sh, c->ws));
+    memcpy(blob, &b, sizeof b);
+    return PB_OK;
+}
+
+extern "C" pb_status pb_ctx_import_peer(pb_ctx* c, int32_t peer, const void* blob, size_t len) {
+    pb_status st = check_ctx(c, "pb_ctx_import_peer");
+    if (st) return st;
+    if (!blob || len < sizeof(IpcBlob)) return fail(PB_EINVAL, "pb_ctx_import_peer: bad blob");
+    if (peer < 0 || peer >= c->n || peer == c->rank) return fail(PB_EINVAL, "bad peer %d", peer);
+    IpcBlob b;
+    memcpy(&b, blob, sizeof b);
+    if (b.magic != kMagic || b.rank != peer) return fail(PB_EINVAL, "blob is not rank %d's", peer);
+    Peer& P = c->peers[peer];
+    void* wb = nullptr;
+    CU(cudaIpcOpenMemHandle(&wb, b.wh, cudaIpcMemLazyEnablePeerAccess));
+    P.ipc_bases.push_back(wb);
+    void* sb = nullptr;
+    if (memcmp(&b.wh, &b.sh, sizeof b.wh) == 0) {
+        sb = wb;   // same allocation
+    } else {
+        CU(cudaIpcOpenMemHandle(&sb, b.sh, cudaIpcMemLazyEnablePeerAccess));
+        P.ipc_bases.push_back(sb);
+    }
+    P.weights = static_cast<char*>(wb) + b.w_off;
+    P.ws = static_cast<char*>(sb) + b.s_off;
+    P.linked = true;
+    return PB_OK;
+}
+
+extern "C" pb_status pb_ctx_link_local(pb_ctx* c, int32_t peer, pb_ctx* pc) {
+    pb_status st = check_ctx(c, "pb_ctx_link_local");
+    if (st) return st;
+    if (!pc || peer < 0 || peer >= c->n || peer == c->rank || pc->rank != peer || pc->plan->n_gpus != c->n)
+        return fail(PB_EINVAL, "pb_ctx_link_local: bad peer");
+    if (pc->device != c->device) {
+        cudaError_t e = cudaDeviceEnablePeerAccess(pc->device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+            return fail(PB_ECUDA, "cudaDeviceEnablePeerAccess: %s", cudaGetErrorString(e));
+        cudaGetLastError();
+    }
+    c->peers[peer].weights = pc->weights;
+    c->peers[peer].ws = pc->ws;
+    c->peers[peer].linked = true;
+    return PB_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+// trial
+// ------------------------------------------------------------------------------------------------
+
+static uint32_t* flag_ptr(char* ws, const WsLayout& L, int32_t word) {
+    return reinterpret_cast<uint32_t*>(ws + L.flags) + word;
+}
+
+// Publish readiness word `word` (= epoch) on the given ranks.
+static cudaError_t signal_ranks(pb_ctx* c, int32_t word, const std::vector<int32_t>& ranks, cudaStream_t s) {
+    SignalTargets t{};
+    for (int32_t r : ranks) t.addr[t.n++] = flag_ptr(c->peers[r].ws, c->L, word);
+    if (t.n == 0) return cudaSuccess;
+    ++c->n_launches;
+    return launch_signal(t, c->epoch, s);
+}
+
+static cudaError_t wait_word(pb_ctx* c, int32_t word, cudaStream_t s) {
+    return stream_wait_geq(s, flag_ptr(c->ws, c->L, word), c->epoch);
+}
+
+extern "C" pb_status pb_trial_begin(pb_ctx* c, uint32_t epoch) {
+    pb_status st = check_ctx(c, "pb_trial_begin");
+    if (st) return st;
+    if (epoch <= c->epoch) return fail(PB_EINVAL, "epoch %u must exceed the previous %u", epoch, c->epoch);
+    for (int r = 0; r < c->n; ++r)
+        if (!c->peers[r].linked) return fail(PB_EPROTOCOL, "peer %d not wired (import/link)", r);
+    c->epoch = epoch;
+    c->n_launches = 0;
+    c->load_bytes = c->recv_bytes = 0;
+    std::fill(c->tl_landed.begin(), c->tl_landed.end(), -1.0);
+    std::fill(c->tl_gathered.begin(), c->tl_gathered.end(), -1.0);
+    CU(cudaEventRecord(c->t0, c->h2d[0]));
+    cudaStream_t others[] = {c->h2d[1], c->merge, c->nv, c->comp};
+    for (auto s : others) CU(cudaStreamWaitEvent(s, c->t0, 0));
+    c->phase = Phase::Begun;
+    return PB_OK;
+}
+
+extern "C" pb_status pb_load_shard(pb_ctx* c) {
+    pb_status st = check_ctx(c, "pb_load_shard");
+    if (st) return st;
+    if (c->phase != Phase::Begun) return fail(PB_EPROTOCOL, "pb_load_shard: call pb_trial_begin first");
+    const pb_plan* p = c->plan;
+    int i = 0;
+    for (int32_t id : p->load[c->rank]) {
+        const ChunkRec& ch = p->chunks[id];
+        cudaStream_t s = c->h2d[i++ & 1];
+        char* dst = (ch.is_adapter ? c->adapters : c->weights) + ch.dev_off;
+        const char* src = static_cast<const char*>(ch.is_adapter ? c->host_adapters : c->host_base) + ch.host_off;
+        CU(cudaMemcpyAsync(dst, src, ch.bytes, cudaMemcpyHostToDevice, s));
+        CU(cudaEventRecord(c->landed[id], s));
+        c->load_bytes += ch.bytes;
+    }
+    c->phase = Phase::Loaded;
+    return PB_OK;
+}
+
+extern "C" pb_status pb_merge_lora(pb_ctx* c, int32_t adapter_id) {
+    pb_status st = check_ctx(c, "pb_merge_lora");
+    if (st) return st;
+    if (c->phase != Phase::Loaded) return fail(PB_EPROTOCOL, "pb_merge_lora: call pb_load_shard first");
+    const pb_plan* p = c->plan;
+    if (adapter_id < -1 || adapter_id >= (int32_t)p->adapters.size())
+        return fail(PB_EINVAL, "adapter_id %d out of range", adapter_id);
+    std::vector<int32_t> others;
+    for (int r = 0; r < c->n; ++r)
+        if (r != c->rank) others.push_back(r);
+    std::vector<char> waited(p->chunks.size(), 0);
+    for (int32_t id : p->load[c->rank]) {
+        const ChunkRec& ch = p->chunks[id];
+        if (ch.is_adapter) continue;
+        CU(cudaStreamWaitEvent(c->merge, c->landed[id], 0));
+        for (int32_t j : c->jobs_of_chunk[id]) {
+            const MergeJob& job = c->jobs[j];
+            if (job.adapter != adapter_id) continue;
+            for (int32_t a : job.need)
+                if (!waited[a]) {
+                    CU(cudaStreamWaitEvent(c->merge, c->landed[a], 0));
+                    waited[a] = 1;
+                }
+            CU(launch_merge(job.maps, job.rows, job.cols, job.rank, job.scale, c->merge));
+            ++c->n_launches;
+        }
+        if (!others.empty()) CU(signal_ranks(c, c->L.f_chunk + id, others, c->merge));
+        if (c->last_own_chunk[ch.tensor] == id) CU(cudaEventRecord(c->tensor_ready[ch.tensor], c->merge));
+    }
+    CU(cudaEventRecord(c->merge_done, c->merge));
+    c->phase = Phase::Merged;
+    return PB_OK;
+}
+
+extern "C" pb_status pb_gather_layers(pb_ctx* c) {
+    pb_status st = check_ctx(c, "pb_gather_layers");
+    if (st) return st;
+    if (c->phase != Phase::Merged) return fail(PB_EPROTOCOL, "pb_gather_layers: call pb_merge_lora first");
+    const pb_plan* p = c->plan;
+    for (int32_t id : p->recv[c->rank]) {
+        const ChunkRec& ch = p->chunks[id];
+        CU(wait_word(c, c->L.f_chunk + id, c->nv));
+        CU(cudaMemcpyAsync(c->weights + ch.dev_off, c->peers[ch.loader].weights + ch.dev_off, ch.bytes,
+                           cudaMemcpyDeviceToDevice, c->nv));
+        CU(cudaEventRecord(c->gathered[id], c->nv));
+        c->recv_bytes += ch.bytes;
+        if (c->last_recv_chunk[ch.tensor] == id) CU(cudaEventRecord(c->tensor_ready[ch.tensor], c->nv));
+    }
+    CU(cudaEventRecord(c->gather_done, c->nv));
+    c->phase = Phase::Gathered;
+    return PB_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+// prefill
+// ------------------------------------------------------------------------------------------------
+
+namespace {
+
+const __nv_bfloat16* wt(pb_ctx* c, int l, const char* sfx) {
+    const pb_plan* p = c->plan;
+    const int32_t t = p->find_tensor(l >= 0 ? "L" + std::to_string(l) + "." + sfx : std::string(sfx));
+    return t < 0 ? nullptr : reinterpret_cast<const __nv_bfloat16*>(c->weights + p->tensors[t].dev_off);
+}
+
+cudaEvent_t layer_ready(pb_ctx* c, int l) {
+    const pb_plan* p = c->plan;
+    int32_t last = -1;
+    for (size_t t = 0; t < p->tensors.size(); ++t)
+        if (p->tensors[t].layer == l) last = (int32_t)t;
+    return c->tensor_ready[last];
+}
+
+pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B) {
+    const pb_plan* p = c->plan;
+    const auto& m = p->model;
+    const bool opt = m.arch == PB_ARCH_OPT;
+    const int d = m.d_model, hd = p->head_dim(), H = m.n_heads, KVH = m.n_kv_heads, qd = H * hd, kvd = KVH * hd;
+    const int f = m.d_ffn, qdim = qkv_dim(p);
+    const WsLayout& L = c->L;
+    float* h = reinterpret_cast<float*>(c->ws + L.h);
+    __nv_bfloat16* x = reinterpret_cast<__nv_bfloat16*>(c->ws + L.x);
+    const int li = L.n_qkv > 1 ? l - p->stages[c->rank].first : 0;
+    __nv_bfloat16* qkv = reinterpret_cast<__nv_bfloat16*>(c->ws + L.qkv + L.qkv_stride * li);
+    __nv_bfloat16* attn = reinterpret_cast<__nv_bfloat16*>(c->ws + L.attn);
+    __nv_bfloat16* mlp = reinterpret_cast<__nv_bfloat16*>(c->ws + L.mlp);
+    const LayerMaps& lm = c->lmaps[l];
+    cudaStream_t s = c->comp;
+    const int rows = r1 - r0;
+    auto G = [&](int M_begin, int N, int K, int epi, const __nv_bfloat16* bias, int relu, float scale, int scale_cols,
+                 void* out, int ldo) {
+        GemmArgs a{};
+        a.M_begin = M_begin;
+        a.M_end = r1;
+        a.N = N;
+        a.K = K;
+        a.epi = epi;
+        a.relu = relu;
+        a.scale = scale;
+        a.scale_cols = scale_cols;
+        a.bias = bias;
+        a.out = out;
+        a.ldo = ldo;
+        a.up_row0 = f;
+        return a;
+    };
+    // --- attention block
+    CU(launch_norm(h + (size_t)r0 * d, d, x + (size_t)r0 * d, d, rows, d, wt(c, l, "ln1_g"),
+                   opt ? wt(c, l, "ln1_b") : nullptr, m.norm_eps, s));
+    GemmArgs a = G(r0, qdim, d, EPI_BF16, opt ? wt(c, l, "qkv_b") : nullptr, 0, opt ? 1.0f / sqrtf((float)hd) : 1.0f,
+                   opt ? d : 0, qkv, qdim);
+    CU(launch_gemm(c->map_x, lm.qkv, a, s));
+    if (!opt)
+        CU(launch_rope(qkv, qdim, r0, r1, B, H, KVH, hd, qd, reinterpret_cast<const float2*>(c->ws + L.rope), s));
+    CU(launch_attention(qkv, qdim, attn, qd, ta, tb, B, H, KVH, hd, qd, qd + kvd, opt ? 1.0f : 1.0f / sqrtf((float)hd),
+                        s));
+    a = G(r0, d, qd, EPI_RESID, opt ? wt(c, l, "o_b") : nullptr, 0, 1.f, 0, h, d);
+    CU(launch_gemm(c->map_attn, lm.o, a, s));
+    // --- MLP block
+    CU(launch_norm(h + (size_t)r0 * d, d, x + (size_t)r0 * d, d, rows, d, wt(c, l, "ln2_g"),
+                   opt ? wt(c, l, "ln2_b") : nullptr, m.norm_eps, s));
+    if (opt) {
+        a = G(r0, f, d, EPI_BF16, wt(c, l, "fc1_b"), 1, 1.f, 0, mlp, f);
+        CU(launch_gemm(c->map_x, lm.up, a, s));
+        a = G(r0, d, f, EPI_RESID, wt(c, l, "fc2_b"), 0, 1.f, 0, h, d);
+        CU(launch_gemm(c->map_mlp, lm.down, a, s));
+    } else {
+        a = G(r0, f, d, EPI_SILU_MUL, nullptr, 0, 1.f, 0, mlp, f);
+        CU(launch_gemm(c->map_x, lm.up, a, s));
+        a = G(r0, d, f, EPI_RESID, nullptr, 0, 1.f, 0, h, d);
+        CU(launch_gemm(c->map_mlp, lm.down, a, s));
+    }
+    c->n_launches += opt ? 7 : 8;
+    return PB_OK;
+}
+
+}  // namespace
+
+extern "C" pb_status pb_prefill_enqueue(pb_ctx* c, const int32_t* tokens, int32_t B, int32_t T) {
+    pb_status st = check_ctx(c, "pb_prefill_enqueue");
+    if (st) return st;
+    if (c->phase != Phase::Gathered) return fail(PB_EPROTOCOL, "pb_prefill_enqueue: call pb_gather_layers first");
+    if (B < 1 || T < 1 || B > c->L.max_batch || T > c->L.max_seq || (int64_t)B * T > c->L.max_rows)
+        return fail(PB_EINVAL, "batch %d x seq %d exceeds the workspace (%d x %d)", B, T, c->L.max_batch, c->L.max_seq);
+    if (c->rank == 0 && !tokens) return fail(PB_EINVAL, "rank 0 needs tokens");
+    const pb_plan* p = c->plan;
+    const auto& m = p->model;
+    const bool opt = m.arch == PB_ARCH_OPT;
+    const int g = c->rank, N = c->n, d = m.d_model, hd = p->head_dim();
+    const WsLayout& L = c->L;
+    cudaStream_t s = c->comp;
+    c->cur_batch = B;
+    c->cur_seq = T;
+    const int k = std::max(1, std::min(p->opts.prefill_chunks, T));
+    std::vector<int> tb(k + 1);   // token chunk boundaries, remainder to lower chunks
+    for (int j = 0, t = 0; j <= k; ++j) {
+        tb[j] = t;
+        if (j < k) t += T / k + (j < T % k ? 1 : 0);
+    }
+    float* h = reinterpret_cast<float*>(c->ws + L.h);
+    if (!opt) {
+        CU(launch_rope_table(reinterpret_cast<float2*>(c->ws + L.rope), T, hd, m.rope_theta, s));
+        ++c->n_launches;
+    }
+    if (g == 0) {
+        for (int b = 0; b < B; ++b)   // token-major rows: row = t * B + b
+            for (int t = 0; t < T; ++t) c->h_tokens[t * B + b] = tokens[(size_t)b * T + t];
+        CU(cudaMemcpyAsync(c->ws + L.tokens, c->h_tokens, sizeof(int32_t) * B * T, cudaMemcpyHostToDevice, s));
+        CU(cudaMemsetAsync(c->ws + L.nan, 0, 4, s));
+    }
+    const auto stage = p->stages[g];
+    for (int j = 0; j < k; ++j) {
+        const int r0 = tb[j] * B, r1 = tb[j + 1] * B;
+        if (g == 0) {
+            if (j == 0) {
+                // embedding rows may live on every rank (vocab slices): wait for each piece
+                const int32_t et = p->find_tensor("embed");
+                for (auto& ch : p->chunks) {
+                    if (ch.is_adapter || ch.tensor != et) continue;
+                    if (ch.loader == g) continue;
+                    CU(wait_word(c, L.f_chunk + ch.id, s));
+                }
+                if (c->last_own_chunk[et] >= 0) CU(cudaStreamWaitEvent(s, c->tensor_ready[et], 0));
+                if (opt) CU(cudaStreamWaitEvent(s, c->tensor_ready[p->find_tensor("pos")], 0));
+            }
+            EmbedSrc E{};
+            const int32_t et = p->find_tensor("embed");
+            if (p->opts.vocab_sliced) {
+                auto sl = std::vector<int32_t>(N + 1, 0);
+                for (auto& ch : p->chunks)
+                    if (!ch.is_adapter && ch.tensor == et) sl[ch.loader + 1] = std::max(sl[ch.loader + 1], ch.r1);
+                for (int r = 0; r < N; ++r) {
+                    E.base[r] = reinterpret_cast<const __nv_bfloat16*>(c->peers[r].weights + p->tensors[et].dev_off);
+                    E.slice_begin[r] = r == 0 ? 0 : sl[r];
+                }
+                E.slice_begin[N] = INT32_MAX;
+                E.n = N;
+            } else {
+                E.base[0] = wt(c, -1, "embed");
+                E.slice_begin[0] = 0;
+                E.slice_begin[1] = INT32_MAX;
+                E.n = 1;
+            }
+            CU(launch_embed(E, opt ? wt(c, -1, "pos") : nullptr, reinterpret_cast<const int32_t*>(c->ws + L.tokens), h, d,
+                            r0, r1, B, s));
+            ++c->n_launches;
+        } else {
+            CU(wait_word(c, L.f_act + j, s));
+        }
+        for (int l = stage.first; l < stage.second; ++l) {
+            if (j == 0) CU(cudaStreamWaitEvent(s, layer_ready(c, l), 0));
+            st = run_layer(c, l, r0, r1, tb[j], tb[j + 1], B);
+            if (st) return st;
+        }
+        if (g < N - 1) {
+            CU(cudaMemcpyAsync(c->peers[g + 1].ws + L.h + (size_t)r0 * d * 4, h + (size_t)r0 * d, (size_t)(r1 - r0) * d * 4,
+                               cudaMemcpyDeviceToDevice, s));
+            CU(signal_ranks(c, L.f_act + j, {g + 1}, s));
+        }
+    }
+    // final norm of the last position (last stage), broadcast y to the head owners
+    __nv_bfloat16* y = reinterpret_cast<__nv_bfloat16*>(c->ws + L.y);
+    std::vector<int32_t> owners;
+    for (int r = 0; r < N; ++r)
+        if (is_head_owner(p, r)) owners.push_back(r);
+    if (g == N - 1) {
+        CU(cudaStreamWaitEvent(s, c->tensor_ready[p->find_tensor("final_g")], 0));
+        if (opt) CU(cudaStreamWaitEvent(s, c->tensor_ready[p->find_tensor("final_b")], 0));
+        CU(launch_norm(h + (size_t)(T - 1) * B * d, d, y, d, B, d, wt(c, -1, "final_g"), opt ? wt(c, -1, "final_b") : nullptr,
+                       m.norm_eps, s));
+        ++c->n_launches;
+        std::vector<int32_t> remote;
+        for (int32_t r : owners)
+            if (r != g) {
+                CU(cudaMemcpyAsync(c->peers[r].ws + L.y, y, (size_t)B * d * 2, cudaMemcpyDeviceToDevice, s));
+                remote.push_back(r);
+            }
+        CU(signal_ranks(c, L.f_y, remote, s));
+    }
+    float* logits = reinterpret_cast<float*>(c->ws + L.logits);
+    const int V = m.vocab;
+    if (is_head_owner(p, g)) {
+        if (g != N - 1) CU(wait_word(c, L.f_y, s));
+        const int32_t ht = head_tensor(p);
+        CU(cudaStreamWaitEvent(s, c->tensor_ready[ht], 0));
+        int32_t v0, v1;
+        head_slice(p, g, &v0, &v1);
+        const __nv_bfloat16* E = reinterpret_cast<const __nv_bfloat16*>(c->weights + p->tensors[ht].dev_off);
+        CU(launch_logits(y, B, d, E, v0, v1, logits, V, s));
+        ++c->n_launches;
+        if (g != 0) {
+            CU(cudaMemcpy2DAsync(c->peers[0].ws + L.logits + (size_t)v0 * 4, (size_t)V * 4, logits + v0, (size_t)V * 4,
+                                 (size_t)(v1 - v0) * 4, B, cudaMemcpyDeviceToDevice, s));
+            CU(signal_ranks(c, L.f_logit + g, {0}, s));
+        }
+    }
+    if (g == 0) {
+        for (int32_t r : owners)
+            if (r != 0) CU(wait_word(c, L.f_logit + r, s));
+        CU(launch_argmax(logits, B, V, V, reinterpret_cast<int32_t*>(c->ws + L.tok_out),
+                         reinterpret_cast<int32_t*>(c->ws + L.nan), s));
+        ++c->n_launches;
+        CU(cudaMemcpyAsync(c->h_out, c->ws + L.tok_out, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, s));
+        CU(cudaMemcpyAsync(c->h_out + B, c->ws + L.nan, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    }
+    CU(cudaEventRecord(c->done, s));
+    c->phase = Phase::Prefilled;
+    return PB_OK;
+}
+
+extern "C" pb_status pb_prefill_wait(pb_ctx* c, float* logits_out, int32_t* tokens_out) {
+    pb_status st = check_ctx(c, "pb_prefill_wait");
+    if (st) return st;
+    if (c->phase != Phase::Prefilled) return fail(PB_EPROTOCOL, "pb_prefill_wait: nothing enqueued");
+    CU(cudaEventSynchronize(c->done));
+    CU(cudaGetLastError());
+    if (c->rank == 0) {
+        const int B = c->cur_batch;
+        if (tokens_out) memcpy(tokens_out, c->h_out, sizeof(int32_t) * B);
+        if (logits_out)
+            CU(cudaMemcpy(logits_out, c->ws + c->L.logits, sizeof(float) * B * c->plan->model.vocab,
+                          cudaMemcpyDeviceToHost));
+        if (c->h_out[B]) return fail(PB_ENUMERIC, "non-finite logits");
+    }
+    return PB_OK;
+}
+
+extern "C" pb_status pb_prefill_first_token(pb_ctx* c, const int32_t* tokens, int32_t B, int32_t T, float* logits_out,
+                                            int32_t* tokens_out) {
+    pb_status st = pb_prefill_enqueue(c, tokens, B, T);
+    if (st) return st;
+    return pb_prefill_wait(c, logits_out, tokens_out);
+}
+
+extern "C" pb_status pb_sync(pb_ctx* c) {
+    pb_status st = check_ctx(c, "pb_sync");
+    if (st) return st;
+    cudaStream_t ss[] = {c->h2d[0], c->h2d[1], c->merge, c->nv, c->comp};
+    for (auto s : ss) CU(cudaStreamSynchronize(s));
+    CU(cudaGetLastError());
+    return PB_OK;
+}
+
+extern "C" pb_status pb_timeline(pb_ctx* c, pb_timeline_t* out) {
+    pb_status st = check_ctx(c, "pb_timeline");
+    if (st) return st;
+    if (!out) return fail(PB_EINVAL, "pb_timeline: null out");
+    if (c->phase == Phase::Idle) return fail(PB_EPROTOCOL, "pb_timeline: no trial");
+    const pb_plan* p = c->plan;
+    auto ms = [&](cudaEvent_t e) -> double {
+        float v = 0;
+        if (!e || cudaEventElapsedTime(&v, c->t0, e) != cudaSuccess) { cudaGetLastError(); return -1; }
+        return v;
+    };
+    double load_done = 0;
+    for (int32_t id : p->load[c->rank]) {
+        c->tl_landed[id] = ms(c->landed[id]);
+        load_done = std::max(load_done, c->tl_landed[id]);
+    }
+    for (int32_t id : p->recv[c->rank]) c->tl_gathered[id] = ms(c->gathered[id]);
+    double ready = 0;
+    for (int l = p->stages[c->rank].first; l < p->stages[c->rank].second; ++l) ready = std::max(ready, ms(layer_ready(c, l)));
+    out->t_ready_ms = ready;
+    out->t_full_ms = std::max(ms(c->merge_done), ms(c->gather_done));
+    out->ttft_ms = c->phase == Phase::Prefilled ? ms(c->done) : -1;
+    out->load_done_ms = load_done;
+    out->load_bytes = c->load_bytes;
+    out->recv_bytes = c->recv_bytes;
+    out->n_chunks = (int32_t)p->chunks.size();
+    out->chunk_landed_ms = c->tl_landed.data();
+    out->chunk_gathered_ms = c->tl_gathered.data();
+    out->n_launches = c->n_launches;
+    return PB_OK;
+}

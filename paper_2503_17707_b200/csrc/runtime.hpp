@@ -1,0 +1,90 @@
+// runtime.hpp — per-rank context (pb_ctx) internals.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "kernels.hpp"
+#include "plan.hpp"
+
+namespace pb {
+
+// Workspace layout (byte offsets inside the caller's workspace buffer), identical on every rank so a
+// peer can address it: flags | tokens | h | x | qkv[n_qkv] | attn | mlp | y | logits | tok_out | nan | rope.
+struct WsLayout {
+    int64_t flags = 0, tokens = 0, h = 0, x = 0, qkv = 0, qkv_stride = 0, attn = 0, mlp = 0, y = 0, logits = 0,
+            tok_out = 0, nan = 0, rope = 0, total = 0;
+    int32_t n_qkv = 1;
+    int32_t max_rows = 0, max_batch = 0, max_seq = 0;
+    // readiness words (uint32) inside `flags`
+    int32_t f_chunk = 0, f_act = 0, f_y = 0, f_logit = 0, n_words = 0;
+};
+WsLayout ws_layout(const pb_plan* p, int32_t batch, int32_t seq);
+
+struct MergeJob {
+    int32_t chunk;       // base chunk whose rows it updates
+    int32_t adapter;
+    int32_t rows, cols, rank;
+    float scale;
+    std::vector<int32_t> need;   // adapter chunks that must have landed
+    MergeMaps maps;
+};
+
+struct LayerMaps {
+    CUtensorMap qkv, o, up, down;   // up = fc1 (OPT) or [gate; up] with 64-row boxes (Llama)
+};
+
+struct Peer {
+    char* weights = nullptr;
+    char* ws = nullptr;
+    bool linked = false;
+    std::vector<void*> ipc_bases;   // cudaIpcOpenMemHandle results to close
+};
+
+enum class Phase { Idle, Begun, Loaded, Merged, Gathered, Prefilled };
+
+}  // namespace pb
+
+struct pb_ctx {
+    const pb_plan* plan;
+    int32_t rank, n;
+    int device;
+    char* weights;
+    char* adapters;
+    char* ws;
+    pb_rank_bufs bufs;
+    cudaStream_t h2d[2], merge, nv, comp;
+    pb::WsLayout L;
+    const void* host_base;
+    const void* host_adapters;
+    std::vector<pb::Peer> peers;
+
+    // events
+    cudaEvent_t t0 = nullptr, merge_done = nullptr, gather_done = nullptr, done = nullptr;
+    std::vector<cudaEvent_t> landed, gathered, tensor_ready;
+    std::vector<char> tensor_own;        // this rank loads every piece of the tensor
+    std::vector<int32_t> last_own_chunk; // per base tensor: last own chunk in load order (-1 if none)
+    std::vector<int32_t> last_recv_chunk;
+
+    // merges: per chunk, indices into jobs
+    std::vector<pb::MergeJob> jobs;
+    std::vector<std::vector<int32_t>> jobs_of_chunk;
+
+    // prefill tensor maps
+    CUtensorMap map_x, map_attn, map_mlp;
+    std::vector<pb::LayerMaps> lmaps;   // indexed by layer (only this rank's stage is encoded)
+
+    // pinned staging
+    int32_t* h_tokens = nullptr;   // [max_rows]
+    int32_t* h_out = nullptr;      // [max_batch + 1] tokens + nan flag
+
+    // trial state
+    uint32_t epoch = 0;
+    pb::Phase phase = pb::Phase::Idle;
+    int32_t cur_batch = 0, cur_seq = 0;
+    int32_t n_launches = 0;
+    int64_t load_bytes = 0, recv_bytes = 0;
+    std::vector<double> tl_landed, tl_gathered;
+    bool use_wait_value = true;
+};

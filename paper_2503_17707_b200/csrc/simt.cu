@@ -1,0 +1,377 @@
+// simt.cu — the non-GEMM prefill kernels (CUDA cores): norms, embedding gather, RoPE, causal attention,
+// vocab-parallel logits, argmax, and the cross-rank readiness signal.
+//
+// All are memory- or latency-bound row kernels: coalesced 16-byte accesses, fp32 statistics with
+// warp-shuffle reductions, one CTA (or one warp) per row.
+#include <cuda_bf16.h>
+#include <math_constants.h>
+
+#include "kernels.hpp"
+
+namespace pb {
+
+namespace {
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+template <int NT>
+__device__ __forceinline__ float block_sum(float v, float* red) {
+    v = warp_sum(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    float t = (l < NT / 32) ? red[l] : 0.f;
+    return warp_sum(t);
+}
+
+// ------------------------------------------------------------------ LayerNorm / RMSNorm
+// One CTA per row; the row is held in registers (d <= 256 * 40). Two-pass fp32 statistics.
+template <int NT, int PER>
+__global__ void __launch_bounds__(NT) norm_kernel(const float* __restrict__ h, int ldh, __nv_bfloat16* __restrict__ out,
+                                                  int ldo, int d, const __nv_bfloat16* __restrict__ gamma,
+                                                  const __nv_bfloat16* __restrict__ beta, float eps) {
+    __shared__ float red[32];
+    const float* x = h + (size_t)blockIdx.x * ldh;
+    float v[PER];
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int c = threadIdx.x + i * NT;
+        v[i] = c < d ? x[c] : 0.f;
+        s += v[i];
+    }
+    float mean = 0.f;
+    if (beta) mean = block_sum<NT>(s, red) / d;
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int c = threadIdx.x + i * NT;
+        const float t = c < d ? v[i] - mean : 0.f;
+        q += t * t;
+    }
+    const float var = block_sum<NT>(q, red) / d;
+    const float rstd = rsqrtf(var + eps);
+    __nv_bfloat16* o = out + (size_t)blockIdx.x * ldo;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int c = threadIdx.x + i * NT;
+        if (c < d) {
+            float y = (v[i] - mean) * rstd * __bfloat162float(gamma[c]);
+            if (beta) y += __bfloat162float(beta[c]);
+            o[c] = __float2bfloat16_rn(y);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ embedding (+ OPT learned positions)
+__global__ void embed_kernel(EmbedSrc E, const __nv_bfloat16* __restrict__ pos, const int32_t* __restrict__ tok,
+                             float* __restrict__ h, int d, int r0, int B) {
+    const int row = r0 + blockIdx.x;
+    const int t = row / B;
+    const int id = tok[row];
+    int owner = 0;
+    while (owner + 1 < E.n && id >= E.slice_begin[owner + 1]) ++owner;
+    const __nv_bfloat16* e = E.base[owner] + (size_t)id * d;
+    const __nv_bfloat16* p = pos ? pos + (size_t)(t + 2) * d : nullptr;   // HF OPT position offset 2
+    float* o = h + (size_t)row * d;
+    for (int c = threadIdx.x * 8; c < d; c += blockDim.x * 8) {
+        uint4 ev = *reinterpret_cast<const uint4*>(e + c);
+        const __nv_bfloat16* eb = reinterpret_cast<const __nv_bfloat16*>(&ev);
+        float f[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) f[i] = __bfloat162float(eb[i]);
+        if (p) {
+            uint4 pv = *reinterpret_cast<const uint4*>(p + c);
+            const __nv_bfloat16* pb = reinterpret_cast<const __nv_bfloat16*>(&pv);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) f[i] += __bfloat162float(pb[i]);
+        }
+        reinterpret_cast<float4*>(o + c)[0] = make_float4(f[0], f[1], f[2], f[3]);
+        reinterpret_cast<float4*>(o + c)[1] = make_float4(f[4], f[5], f[6], f[7]);
+    }
+}
+
+// ------------------------------------------------------------------ RoPE
+__global__ void rope_table_kernel(float2* table, int T, int hd, double theta) {
+    const int half = hd / 2;
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= T * half) return;
+    const int t = idx / half, i = idx % half;
+    const double inv_freq = pow(theta, -2.0 * i / (double)hd);
+    double sv, cv;
+    sincos((double)t * inv_freq, &sv, &cv);
+    table[idx] = make_float2((float)cv, (float)sv);
+}
+
+// x'_i = x_i cos - x_{i+hd/2} sin ; x'_{i+hd/2} = x_{i+hd/2} cos + x_i sin   (HF rotate_half)
+__global__ void rope_kernel(__nv_bfloat16* qkv, int ld, int r0, int B, int n_q, int n_k, int hd, int k_col0,
+                            const float2* __restrict__ table) {
+    const int row = r0 + blockIdx.x;
+    const int t = row / B;
+    const int half = hd / 2;
+    const int total = (n_q + n_k) * half;
+    __nv_bfloat16* base = qkv + (size_t)row * ld;
+    for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+        const int head = idx / half, i = idx % half;
+        __nv_bfloat16* x = head < n_q ? base + head * hd : base + k_col0 + (head - n_q) * hd;
+        const float2 cs = table[t * half + i];
+        const float a = __bfloat162float(x[i]), b = __bfloat162float(x[i + half]);
+        x[i] = __float2bfloat16_rn(a * cs.x - b * cs.y);
+        x[i + half] = __float2bfloat16_rn(b * cs.x + a * cs.y);
+    }
+}
+
+// ------------------------------------------------------------------ causal attention (flash-style, SIMT)
+// CTA = (32 query positions, head, sequence); 8 warps x 4 queries. Keys/values streamed through shared
+// memory 32 at a time (K transposed for conflict-free lane-per-key dot products); online softmax in fp32.
+template <int HD>
+__global__ void __launch_bounds__(256) attention_kernel(const __nv_bfloat16* __restrict__ qkv, int ld,
+                                                        __nv_bfloat16* __restrict__ out, int ldo, int t0, int t1,
+                                                        int B, int group, int k_col0, int v_col0,
+                                                        float score_scale) {
+    constexpr int KT = 32, QT = 32, DPL = HD / 32;   // dims per lane
+    extern __shared__ float attn_smem[];
+    float (*sQ)[HD] = reinterpret_cast<float (*)[HD]>(attn_smem);
+    float (*sKt)[KT + 1] = reinterpret_cast<float (*)[KT + 1]>(attn_smem + QT * HD);
+    float (*sV)[HD] = reinterpret_cast<float (*)[HD]>(attn_smem + QT * HD + HD * (KT + 1));
+    const int b = blockIdx.z, h = blockIdx.y, kvh = h / group;
+    const int q0 = t0 + blockIdx.x * QT;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int q_hi = min(q0 + QT, t1);   // exclusive
+    // load Q tile
+    for (int i = threadIdx.x; i < QT * HD; i += 256) {
+        const int qi = i / HD, c = i % HD;
+        const int t = q0 + qi;
+        sQ[qi][c] = t < t1 ? __bfloat162float(qkv[(size_t)(t * B + b) * ld + h * HD + c]) * score_scale : 0.f;
+    }
+    float m[4], l[4], acc[4][DPL];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        m[i] = -CUDART_INF_F;
+        l[i] = 0.f;
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) acc[i][e] = 0.f;
+    }
+    const int n_keys = q_hi;   // keys [0, q_hi) cover every query in the tile
+    for (int k0 = 0; k0 < n_keys; k0 += KT) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < KT * HD; i += 256) {
+            const int kj = i / HD, c = i % HD;
+            const int t = k0 + kj;
+            float kv = 0.f, vv = 0.f;
+            if (t < n_keys) {
+                const __nv_bfloat16* r = qkv + (size_t)(t * B + b) * ld;
+                kv = __bfloat162float(r[k_col0 + kvh * HD + c]);
+                vv = __bfloat162float(r[v_col0 + kvh * HD + c]);
+            }
+            sKt[c][kj] = kv;
+            sV[kj][c] = vv;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int qi = warp * 4 + i;
+            const int t = q0 + qi;
+            if (t >= q_hi) continue;
+            const int key = k0 + lane;
+            float s = 0.f;
+#pragma unroll 16
+            for (int c = 0; c < HD; ++c) s = fmaf(sQ[qi][c], sKt[c][lane], s);
+            if (key > t) s = -CUDART_INF_F;
+            const float mx = warp_max(s);
+            const float m_new = fmaxf(m[i], mx);
+            if (m_new == -CUDART_INF_F) continue;   // whole tile masked for this query
+            const float p = __expf(s - m_new);
+            const float corr = __expf(m[i] - m_new);
+            l[i] = l[i] * corr + warp_sum(p);
+            m[i] = m_new;
+#pragma unroll
+            for (int e = 0; e < DPL; ++e) acc[i][e] *= corr;
+#pragma unroll 8
+            for (int j = 0; j < KT; ++j) {
+                const float pj = __shfl_sync(0xffffffffu, p, j);
+#pragma unroll
+                for (int e = 0; e < DPL; ++e) acc[i][e] = fmaf(pj, sV[j][lane + 32 * e], acc[i][e]);
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int t = q0 + warp * 4 + i;
+        if (t >= q_hi) continue;
+        const float inv = 1.f / l[i];
+        __nv_bfloat16* o = out + (size_t)(t * B + b) * ldo + h * HD;
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) o[lane + 32 * e] = __float2bfloat16_rn(acc[i][e] * inv);
+    }
+}
+
+// ------------------------------------------------------------------ vocab-parallel logits
+// One warp per vocabulary row; y (B <= 8 rows) staged in shared memory as fp32.
+__global__ void __launch_bounds__(256) logits_kernel(const __nv_bfloat16* __restrict__ y, int B, int d,
+                                                     const __nv_bfloat16* __restrict__ E, int v0, int v1,
+                                                     float* __restrict__ logits, int ldl) {
+    extern __shared__ float sy[];
+    for (int i = threadIdx.x; i < B * d; i += blockDim.x) sy[i] = __bfloat162float(y[i]);
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int v = v0 + blockIdx.x * 8 + warp;
+    if (v >= v1) return;
+    const __nv_bfloat16* e = E + (size_t)v * d;
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int c = lane * 8; c < d; c += 256) {
+        uint4 ev = __ldg(reinterpret_cast<const uint4*>(e + c));
+        const __nv_bfloat16* eb = reinterpret_cast<const __nv_bfloat16*>(&ev);
+        float f[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) f[i] = __bfloat162float(eb[i]);
+        for (int b = 0; b < B; ++b) {
+            const float* yb = sy + b * d + c;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[b] = fmaf(f[i], yb[i], acc[b]);
+        }
+    }
+    for (int b = 0; b < B; ++b) {
+        const float s = warp_sum(acc[b]);
+        if (lane == 0) logits[(size_t)b * ldl + v] = s;
+    }
+}
+
+// ------------------------------------------------------------------ argmax (lowest index wins ties)
+__global__ void __launch_bounds__(1024) argmax_kernel(const float* __restrict__ logits, int V, int ldl,
+                                                      int32_t* tokens, int32_t* nan_flag) {
+    __shared__ float sv[32];
+    __shared__ int si[32];
+    const float* x = logits + (size_t)blockIdx.x * ldl;
+    float best = -CUDART_INF_F;
+    int bi = 0x7fffffff;
+    bool bad = false;
+    for (int v = threadIdx.x; v < V; v += blockDim.x) {
+        const float f = x[v];
+        if (!isfinite(f)) bad = true;
+        if (f > best || (f == best && v < bi)) { best = f; bi = v; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) { sv[w] = best; si[w] = bi; }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nan_flag, 1);
+    if (w == 0) {
+        best = l < (blockDim.x >> 5) ? sv[l] : -CUDART_INF_F;
+        bi = l < (blockDim.x >> 5) ? si[l] : 0x7fffffff;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+        }
+        if (l == 0) tokens[blockIdx.x] = bi == 0x7fffffff ? 0 : bi;
+    }
+}
+
+// ------------------------------------------------------------------ cross-rank readiness words
+__global__ void signal_kernel(SignalTargets t, uint32_t value) {
+    const int i = threadIdx.x;
+    if (i < t.n) {
+        __threadfence_system();
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(t.addr[i]), "r"(value) : "memory");
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_norm(const float* h, int ldh, __nv_bfloat16* out, int ldo, int rows, int d,
+                        const __nv_bfloat16* gamma, const __nv_bfloat16* beta, float eps, cudaStream_t s) {
+    if (rows <= 0) return cudaSuccess;
+    if (d <= 256 * 8) norm_kernel<256, 8><<<rows, 256, 0, s>>>(h, ldh, out, ldo, d, gamma, beta, eps);
+    else if (d <= 256 * 40) norm_kernel<256, 40><<<rows, 256, 0, s>>>(h, ldh, out, ldo, d, gamma, beta, eps);
+    else return cudaErrorInvalidValue;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_embed(const EmbedSrc& E, const __nv_bfloat16* pos, const int32_t* tok, float* h, int d, int r0,
+                         int r1, int B, cudaStream_t s) {
+    if (r1 <= r0) return cudaSuccess;
+    if (d % 8) return cudaErrorInvalidValue;
+    embed_kernel<<<r1 - r0, 128, 0, s>>>(E, pos, tok, h, d, r0, B);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rope_table(float2* table, int T, int hd, double theta, cudaStream_t s) {
+    const int n = T * (hd / 2);
+    if (n <= 0) return cudaSuccess;
+    rope_table_kernel<<<(n + 255) / 256, 256, 0, s>>>(table, T, hd, theta);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rope(__nv_bfloat16* qkv, int ld, int r0, int r1, int B, int n_q, int n_k, int hd, int k_col0,
+                        const float2* table, cudaStream_t s) {
+    if (r1 <= r0) return cudaSuccess;
+    rope_kernel<<<r1 - r0, 256, 0, s>>>(qkv, ld, r0, B, n_q, n_k, hd, k_col0, table);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_attention(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int ldo, int t0, int t1, int B,
+                             int n_heads, int n_kv_heads, int hd, int k_col0, int v_col0, float score_scale,
+                             cudaStream_t s) {
+    if (t1 <= t0) return cudaSuccess;
+    dim3 grid((t1 - t0 + 31) / 32, n_heads, B);
+    const int group = n_heads / n_kv_heads;
+    const int sm = (32 * hd + hd * 33 + 32 * hd) * (int)sizeof(float);
+#define PB_ATTN(HD)                                                                                        \
+    case HD: {                                                                                             \
+        cudaError_t e = cudaFuncSetAttribute(attention_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm); \
+        if (e != cudaSuccess) return e;                                                                    \
+        attention_kernel<HD><<<grid, 256, sm, s>>>(qkv, ld, out, ldo, t0, t1, B, group, k_col0, v_col0, score_scale); \
+        break;                                                                                             \
+    }
+    switch (hd) {
+        PB_ATTN(32)
+        PB_ATTN(64)
+        PB_ATTN(128)
+        default: return cudaErrorInvalidValue;
+    }
+#undef PB_ATTN
+    return cudaGetLastError();
+}
+
+cudaError_t launch_logits(const __nv_bfloat16* y, int B, int d, const __nv_bfloat16* E, int v0, int v1, float* logits,
+                          int ldl, cudaStream_t s) {
+    if (v1 <= v0) return cudaSuccess;
+    if (B > 8 || d % 8) return cudaErrorInvalidValue;
+    const size_t sm = (size_t)B * d * sizeof(float);
+    if (sm > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(logits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e != cudaSuccess) return e;
+    }
+    logits_kernel<<<(v1 - v0 + 7) / 8, 256, sm, s>>>(y, B, d, E, v0, v1, logits, ldl);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_argmax(const float* logits, int B, int V, int ldl, int32_t* tokens, int32_t* nan_flag,
+                          cudaStream_t s) {
+    argmax_kernel<<<B, 1024, 0, s>>>(logits, V, ldl, tokens, nan_flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_signal(const SignalTargets& t, uint32_t value, cudaStream_t s) {
+    if (t.n <= 0) return cudaSuccess;
+    signal_kernel<<<1, 32, 0, s>>>(t, value);
+    return cudaGetLastError();
+}
+
+}  // namespace pb

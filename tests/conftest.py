@@ -9,3 +9,7 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) and the built CUDA library")
     config.addinivalue_line("markers", "slow: long-running CPU test")
+
+# Several logical ranks share one GPU in the multi-rank tests; every rank has 5 streams and some of
+# them block on device-side readiness waits, so give each stream its own hardware queue.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")

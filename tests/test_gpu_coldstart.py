@@ -1,0 +1,170 @@
+"""End-to-end parity of the cold-start path on the B200, through the C ABI (pb_* via api.RankEngine).
+
+Checks, per the north star:
+  * first-token logits within 1e-2 relative of the oracle (bf16 storage contract), same argmax (G10 rule);
+  * plan bit-exact with the oracle (tests/test_plan_parity.py) and gathered weight bytes bit-exact:
+    after the trial every rank holds, byte for byte, what the loader produced (unadapted tensors = host
+    bytes, adapted ranges = the loader's merge, within the merge bound of the oracle);
+  * pipelined prefill equals sequential: logits bit-identical across N, load policy, vocab slicing and
+    prompt chunking (P:L259-264 — stages only change where layers run).
+Multi-rank cases run N logical ranks on one GPU in one process (device-side readiness words make the
+cross-rank waits independent of host order).
+"""
+import numpy as np
+import pytest
+import torch
+
+import harness
+import oracle
+import synth
+from oracle.numerics import bf16_bits_to_f64, bf16_ulp
+from paper_2503_17707_b200.api import Plan, RankEngine
+from synth.configs import TINY_LLAMA, TINY_OPT, WORKLOADS, lora
+from gpu_util import need_gpu
+
+pytestmark = pytest.mark.gpu
+
+_ORACLE_CACHE = {}
+
+
+def oracle_logits(model, adapters, toks):
+    key = (model, adapters, toks.tobytes())
+    if key not in _ORACLE_CACHE:
+        _ORACLE_CACHE[key] = oracle.first_token_logits(model, adapters, toks, mode="bf16")
+    return _ORACLE_CACHE[key]
+
+
+def run(model, adapters, n, toks, policy="stage", sliced=0, k=1, chunk_bytes=32 << 20, trials=1, alias=0):
+    plan = Plan(model, adapters, n, policy=policy, vocab_sliced=sliced, chunk_bytes=chunk_bytes, prefill_chunks=k,
+                host_alias_layers=alias)
+    base, ada = harness.build_host_images(plan)
+    B, T = toks.shape
+    engs = [RankEngine(plan, r, base, ada, max_batch=B, max_seq=T) for r in range(n)]
+    for e in engs:
+        e.wire_local(engs)
+    out = None
+    for ep in range(1, trials + 1):
+        for e in engs:
+            e.invalidate()
+        for e in engs:
+            e.enqueue(ep, toks if e.rank == 0 else None, B, T, adapter_id=0 if adapters else -1)
+        res = [e.wait(want_logits=True) for e in engs]
+        out = res[0]
+    return plan, engs, out, base
+
+
+def check_against_oracle(model, adapters, toks, logits, tokens):
+    ol, ot = oracle_logits(model, adapters, toks)
+    for b in range(toks.shape[0]):
+        err = np.abs(logits[b].astype(np.float64) - ol[b]).max()
+        rel = err / np.abs(ol[b]).max()
+        assert rel <= 1e-2, rel
+        srt = np.sort(ol[b])
+        margin = srt[-1] - srt[-2]
+        if margin > 2 * err:
+            assert tokens[b] == ot[b]
+        else:   # near tie: the GPU's token must be within the error of the max
+            assert ol[b][tokens[b]] >= srt[-1] - 2 * err
+    return rel
+
+
+@pytest.mark.parametrize("model", [TINY_OPT, TINY_LLAMA], ids=["opt", "llama"])
+def test_single_gpu_matches_oracle(model):
+    need_gpu()
+    toks = synth.tokens(1, 16, model.vocab)
+    plan, engs, (tokens, logits), base = run(model, (lora(8),), 1, toks)
+    check_against_oracle(model, (lora(8),), toks, logits, tokens)
+
+
+def test_batch_and_ragged_prompt():
+    need_gpu()
+    toks = synth.tokens(3, 37, TINY_OPT.vocab)
+    plan, engs, (tokens, logits), base = run(TINY_OPT, (lora(8),), 1, toks)
+    check_against_oracle(TINY_OPT, (lora(8),), toks, logits, tokens)
+
+
+def test_no_adapter_and_trials_repeat():
+    need_gpu()
+    toks = synth.tokens(1, 16, TINY_OPT.vocab)
+    plan, engs, (tokens, logits), base = run(TINY_OPT, (), 1, toks, trials=3)
+    check_against_oracle(TINY_OPT, (), toks, logits, tokens)
+
+
+@pytest.mark.parametrize("model", [TINY_OPT, TINY_LLAMA], ids=["opt", "llama"])
+def test_pipelined_equals_sequential_bitwise(model):
+    """Logits bit-identical across N, load policy, vocab slicing, prompt chunking (north star)."""
+    need_gpu()
+    ads = (lora(8),)
+    toks = synth.tokens(2, 24, model.vocab)
+    _, _, (t1, ref), _ = run(model, ads, 1, toks)
+    check_against_oracle(model, ads, toks, ref, t1)
+    for n, policy, sliced, k in [(2, "stage", 0, 1), (2, "interleave", 1, 1), (4, "stage", 1, 3),
+                                 (4, "interleave", 0, 2), (2, "stage", 0, 4), (3, "interleave", 1, 1)]:
+        _, _, (tn, ln), _ = run(model, ads, n, toks, policy=policy, sliced=sliced, k=k, chunk_bytes=64 << 10)
+        assert np.array_equal(ln.view(np.uint32), ref.view(np.uint32)), (n, policy, sliced, k)
+        assert np.array_equal(tn, t1)
+
+
+def test_gathered_bytes_exact():
+    """After the trial every rank's weights equal the loader's bytes; unadapted = host image,
+    adapted ranges = oracle merge within the merge bound."""
+    need_gpu()
+    model, ads = TINY_OPT, (lora(8),)
+    toks = synth.tokens(1, 16, model.vocab)
+    plan, engs, _, base = run(model, ads, 4, toks, policy="interleave", sliced=1, chunk_bytes=32 << 10)
+    host = base.numpy()
+    w = [e.weights_bytes() for e in engs]
+    for r in range(1, 4):
+        assert np.array_equal(w[r], w[0])   # every rank holds the same merged model
+    ow = oracle.OracleWeights(model, ads)
+    adapted = {(at[6]) for at in plan.atensors()}
+    for (name, rows, cols, host_off, layer, dev_off) in plan.tensors():
+        nb = rows * cols * 2
+        got = w[0][dev_off:dev_off + nb]
+        tid = [t[0] for t in plan.tensors()].index(name)
+        if tid not in adapted:
+            assert np.array_equal(got, host[host_off:host_off + nb]), name
+        else:
+            g = bf16_bits_to_f64(got.view(np.uint16).reshape(rows, cols))
+            o = bf16_bits_to_f64(ow.merged_bits(name, 0))
+            assert np.all(np.abs(g - o) <= 2 * bf16_ulp(o) + 1e-6), name
+            assert (g == o).mean() > 0.95
+
+
+def test_host_alias_layers():
+    need_gpu()
+    from synth.configs import ModelDesc
+    model = ModelDesc("opt", 6, 256, 4, 4, 1024, 1024, 128, 1)
+    toks = synth.tokens(1, 16, model.vocab)
+    plan, engs, (tokens, logits), base = run(model, (lora(8),), 2, toks, alias=2)
+    ol, ot = oracle.first_token_logits(model, (lora(8),), toks, mode="bf16", host_alias_layers=2)
+    rel = np.abs(logits[0] - ol[0]).max() / np.abs(ol[0]).max()
+    assert rel <= 1e-2
+
+
+def test_timeline_and_protocol():
+    need_gpu()
+    toks = synth.tokens(1, 16, TINY_OPT.vocab)
+    plan, engs, _, _ = run(TINY_OPT, (lora(8),), 2, toks)
+    for e in engs:
+        tl = e.timeline()
+        assert tl["load_bytes"] > 0 and tl["t_full_ms"] >= tl["t_ready_ms"] >= 0
+        assert tl["n_launches"] > 0
+    assert engs[0].timeline()["ttft_ms"] > 0
+    from paper_2503_17707_b200 import _binding as B
+    with pytest.raises(B.PBError) as ei:
+        B.pb_load_shard(engs[0].ctx)          # no trial begun
+    assert ei.value.status == B.PB_EPROTOCOL
+    with pytest.raises(B.PBError):
+        B.pb_trial_begin(engs[0].ctx, 1)      # epoch must increase
+
+
+@pytest.mark.slow
+def test_c2_full_size_single_gpu():
+    """BASELINE configs[1] at full size on one GPU — the bench workload — against the oracle."""
+    need_gpu()
+    w = WORKLOADS["C2"]
+    toks = synth.tokens(1, w.seq, w.model.vocab)
+    plan, engs, (tokens, logits), _ = run(w.model, w.adapters, 1, toks, chunk_bytes=32 << 20)
+    rel = check_against_oracle(w.model, w.adapters, toks, logits, tokens)
+    print("C2 rel err", rel)

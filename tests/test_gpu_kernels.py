@@ -1,0 +1,220 @@
+"""Kernel-level parity on the B200: each pb_op_* (the path's own kernels, through the C ABI)
+against the oracle's definitions on seeded inputs, including ragged tails."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import forward as OF
+from oracle.merge import merge_bf16_bits
+from oracle.numerics import bf16_bits_to_f64, bf16_ulp, f64_to_bf16_bits, rne_bf16
+from paper_2503_17707_b200 import _binding as B
+from gpu_util import dev_bf16, dev_f32, host_bits, need_gpu, ptr, stream
+
+pytestmark = pytest.mark.gpu
+
+
+def rbits(rng, shape, a):
+    return f64_to_bf16_bits(rng.uniform(-a, a, size=shape))
+
+
+@pytest.mark.parametrize("rows,cols,rank", [(256, 256, 8), (384, 640, 16), (200, 328, 16), (512, 512, 64),
+                                            (128, 1024, 32), (1000, 136, 16), (2048, 2048, 16)])
+def test_merge_within_one_ulp_of_correct_rounding(rows, cols, rank):
+    need_gpu()
+    rng = np.random.default_rng(rows * 7 + cols + rank)
+    guard = 3
+    full = rbits(rng, (rows + 2 * guard, cols), 0.035)
+    Bm = rbits(rng, (rows, rank), 0.08)
+    Am = rbits(rng, (rank, cols), 1 / np.sqrt(cols))
+    s = 2.0
+    W = dev_bf16(full)
+    Bd, Ad = dev_bf16(Bm), dev_bf16(Am)
+    region = ptr(W) + guard * cols * 2
+    B.pb_op_merge(region, cols, rows, cols, ptr(Bd), ptr(Ad), rank, s, stream())
+    torch.cuda.synchronize()
+    got = host_bits(W)
+    want = merge_bf16_bits(full[guard:guard + rows], Bm, Am, s)
+    # rows outside the region are untouched (bit exact)
+    assert np.array_equal(got[:guard], full[:guard]) and np.array_equal(got[guard + rows:], full[guard + rows:])
+    g = bf16_bits_to_f64(got[guard:guard + rows])
+    w = bf16_bits_to_f64(want)
+    # Bound: 1 bf16 ulp of the correctly rounded value (final rounding) + the fp32 accumulation error of
+    # W + s*sum_k B A, (r + 2) * 2^-24 * (|W| + s * sum_k |B||A|) — the latter only matters under
+    # cancellation (W ~ -s*BA), where the result is tiny and its ulp finer than fp32's error on the terms.
+    Wf = bf16_bits_to_f64(full[guard:guard + rows])
+    mag = np.abs(Wf) + s * (np.abs(bf16_bits_to_f64(Bm)) @ np.abs(bf16_bits_to_f64(Am)))
+    bound = bf16_ulp(w) + (rank + 2) * 2.0 ** -24 * mag
+    assert np.all(np.abs(g - w) <= bound), (np.abs(g - w) / bound).max()
+    assert (g == w).mean() > 0.95
+
+
+def test_merge_zero_B_is_identity():
+    need_gpu()
+    rng = np.random.default_rng(5)
+    Wb = rbits(rng, (256, 384), 0.05)
+    W = dev_bf16(Wb)
+    Bd = dev_bf16(np.zeros((256, 16), np.uint16))
+    Ad = dev_bf16(rbits(rng, (16, 384), 0.1))
+    B.pb_op_merge(ptr(W), 384, 256, 384, ptr(Bd), ptr(Ad), 16, 2.0, stream())
+    torch.cuda.synchronize()
+    assert np.array_equal(host_bits(W), Wb)
+
+
+def _gemm_case(rng, M, K, N):
+    X = rbits(rng, (M, K), 1.0)
+    W = rbits(rng, (N, K), 0.05)
+    bias = rbits(rng, (N,), 0.05)
+    return X, W, bias
+
+
+@pytest.mark.parametrize("M,K,N,m0,m1", [(128, 256, 768, 0, 128), (16, 256, 1024, 0, 16), (300, 512, 384, 0, 300),
+                                         (256, 2048, 640, 128, 256), (200, 192, 136, 40, 170), (130, 688, 256, 0, 130)])
+def test_gemm_bf16_epilogue(M, K, N, m0, m1):
+    need_gpu()
+    rng = np.random.default_rng(M + K + N)
+    X, W, bias = _gemm_case(rng, M, K, N)
+    out = torch.zeros((M, N), dtype=torch.bfloat16, device="cuda")
+    sc_cols = N // 3
+    B.pb_op_gemm(ptr(dev_bf16(X)), M, m0, m1, K, ptr(dev_bf16(W)), N, N, 0, ptr(dev_bf16(bias)), 0, 0.125, sc_cols,
+                 ptr(out), N, stream())
+    torch.cuda.synchronize()
+    ref = bf16_bits_to_f64(X) @ bf16_bits_to_f64(W).T + bf16_bits_to_f64(bias)
+    ref[:, :sc_cols] *= 0.125
+    got = bf16_bits_to_f64(host_bits(out))
+    assert np.all(got[:m0] == 0) and np.all(got[m1:] == 0)
+    r = ref[m0:m1]
+    err = np.abs(got[m0:m1] - r)
+    assert np.all(err <= bf16_ulp(r) + 1e-6 * np.abs(r).max()), err.max()
+
+
+def test_gemm_relu_and_resid_and_silu():
+    need_gpu()
+    rng = np.random.default_rng(11)
+    M, K, N = 192, 320, 256
+    X, W, bias = _gemm_case(rng, M, K, N)
+    Xd, Wd, bd = dev_bf16(X), dev_bf16(W), dev_bf16(bias)
+    ref = bf16_bits_to_f64(X) @ bf16_bits_to_f64(W).T + bf16_bits_to_f64(bias)
+    # ReLU
+    out = torch.zeros((M, N), dtype=torch.bfloat16, device="cuda")
+    B.pb_op_gemm(ptr(Xd), M, 0, M, K, ptr(Wd), N, N, 0, ptr(bd), 1, 1.0, 0, ptr(out), N, stream())
+    torch.cuda.synchronize()
+    r = np.maximum(ref, 0)
+    assert np.all(np.abs(bf16_bits_to_f64(host_bits(out)) - r) <= bf16_ulp(r) + 1e-6)
+    # residual fp32
+    h0 = rng.standard_normal((M, N)).astype(np.float32)
+    h = dev_f32(h0)
+    B.pb_op_gemm(ptr(Xd), M, 0, M, K, ptr(Wd), N, N, 1, ptr(bd), 0, 1.0, 0, ptr(h), N, stream())
+    torch.cuda.synchronize()
+    assert np.allclose(h.cpu().numpy(), h0 + ref, rtol=1e-5, atol=1e-5)
+    # SiLU(gate) * up with W = [gate; up]
+    f = 136
+    Wgu = rbits(rng, (2 * f, K), 0.05)
+    out2 = torch.zeros((M, f), dtype=torch.bfloat16, device="cuda")
+    B.pb_op_gemm(ptr(Xd), M, 0, M, K, ptr(dev_bf16(Wgu)), 2 * f, f, 2, 0, 0, 1.0, 0, ptr(out2), f, stream())
+    torch.cuda.synchronize()
+    gu = bf16_bits_to_f64(X) @ bf16_bits_to_f64(Wgu).T
+    g, u = gu[:, :f], gu[:, f:]
+    r2 = g / (1 + np.exp(-g)) * u
+    err = np.abs(bf16_bits_to_f64(host_bits(out2)) - r2)
+    assert np.all(err <= 2 * bf16_ulp(r2) + 1e-5), err.max()
+
+
+@pytest.mark.parametrize("rms", [False, True])
+@pytest.mark.parametrize("d", [256, 2048, 5120, 9216])
+def test_norm(rms, d):
+    need_gpu()
+    rng = np.random.default_rng(d + rms)
+    rows = 37
+    h = (rng.standard_normal((rows, d)) * 3 + 0.5).astype(np.float32)
+    g = rbits(rng, (d,), 0.1) if False else f64_to_bf16_bits(1 + rng.uniform(-0.1, 0.1, d))
+    b = f64_to_bf16_bits(rng.uniform(-0.02, 0.02, d))
+    out = torch.zeros((rows, d), dtype=torch.bfloat16, device="cuda")
+    B.pb_op_norm(ptr(dev_f32(h)), rows, d, ptr(dev_bf16(g)), 0 if rms else ptr(dev_bf16(b)), 1e-5, ptr(out), stream())
+    torch.cuda.synchronize()
+    hf = h.astype(np.float64)
+    ref = OF.rms_norm(hf, bf16_bits_to_f64(g), 1e-5) if rms else \
+        OF.layer_norm(hf, bf16_bits_to_f64(g), bf16_bits_to_f64(b), 1e-5)
+    err = np.abs(bf16_bits_to_f64(host_bits(out)) - ref)
+    assert np.all(err <= bf16_ulp(ref) + 1e-6), err.max()
+
+
+@pytest.mark.parametrize("T,Bsz,H,KVH,hd,t0,t1", [(16, 1, 4, 4, 64, 0, 16), (77, 2, 4, 2, 128, 0, 77),
+                                                  (128, 1, 2, 2, 64, 64, 128), (40, 3, 2, 1, 32, 17, 40)])
+def test_attention(T, Bsz, H, KVH, hd, t0, t1):
+    need_gpu()
+    rng = np.random.default_rng(T + H + hd)
+    qd, kvd = H * hd, KVH * hd
+    ld = qd + 2 * kvd
+    qkv = rbits(rng, (T * Bsz, ld), 1.0)
+    out = torch.zeros((T * Bsz, qd), dtype=torch.bfloat16, device="cuda")
+    scale = hd ** -0.5
+    B.pb_op_attention(ptr(dev_bf16(qkv)), ld, ptr(out), qd, t0, t1, Bsz, H, KVH, hd, qd, qd + kvd, scale, stream())
+    torch.cuda.synchronize()
+    got = bf16_bits_to_f64(host_bits(out))
+    x = bf16_bits_to_f64(qkv)
+    for b in range(Bsz):
+        rows = np.arange(T) * Bsz + b
+        q, k, v = x[rows, :qd], x[rows, qd:qd + kvd], x[rows, qd + kvd:]
+        ref = OF.causal_attention(q, k, v, H, KVH, hd, scale, lambda z: z)
+        g = got[rows]
+        assert np.all(g[:t0] == 0)
+        err = np.abs(g[t0:t1] - ref[t0:t1])
+        assert np.all(err <= 2 * bf16_ulp(ref[t0:t1]) + 1e-4), err.max()
+
+
+def test_rope():
+    need_gpu()
+    rng = np.random.default_rng(3)
+    T, Bsz, H, KVH, hd = 50, 2, 4, 2, 128
+    qd, kvd = H * hd, KVH * hd
+    ld = qd + 2 * kvd
+    x = rbits(rng, (T * Bsz, ld), 1.0)
+    xd = dev_bf16(x)
+    table = torch.empty(T * hd // 2 * 2, dtype=torch.float32, device="cuda")
+    B.pb_op_rope(ptr(xd), ld, 0, T * Bsz, Bsz, T, H, KVH, hd, qd, 1e4, ptr(table), stream())
+    torch.cuda.synchronize()
+    got = bf16_bits_to_f64(host_bits(xd))
+    xf = bf16_bits_to_f64(x)
+    for b in range(Bsz):
+        rows = np.arange(T) * Bsz + b
+        rq = OF.rope(xf[rows, :qd], H, hd, 1e4)
+        rk = OF.rope(xf[rows, qd:qd + kvd], KVH, hd, 1e4)
+        for g, r in ((got[rows, :qd], rq), (got[rows, qd:qd + kvd], rk)):
+            assert np.all(np.abs(g - r) <= bf16_ulp(r) + 1e-6)
+        assert np.array_equal(got[rows, qd + kvd:], xf[rows, qd + kvd:])
+
+
+def test_logits_argmax_embed():
+    need_gpu()
+    rng = np.random.default_rng(9)
+    Bsz, d, V = 3, 512, 1000
+    y = rbits(rng, (Bsz, d), 1.0)
+    E = rbits(rng, (V, d), 0.035)
+    logits = torch.full((Bsz, V), float("nan"), device="cuda")
+    Ed = dev_bf16(E)
+    B.pb_op_logits(ptr(dev_bf16(y)), Bsz, d, ptr(Ed), 100, 1000, ptr(logits), V, stream())
+    B.pb_op_logits(ptr(dev_bf16(y)), Bsz, d, ptr(Ed), 0, 100, ptr(logits), V, stream())
+    torch.cuda.synchronize()
+    ref = bf16_bits_to_f64(y) @ bf16_bits_to_f64(E).T
+    assert np.allclose(logits.cpu().numpy(), ref, rtol=1e-5, atol=1e-5)
+    # argmax with an exact tie: lowest index wins
+    lg = np.asarray(ref, dtype=np.float32)
+    lg[1, 10] = lg[1, 900] = lg[1].max() + 1
+    toks = torch.zeros(Bsz, dtype=torch.int32, device="cuda")
+    nan = torch.zeros(1, dtype=torch.int32, device="cuda")
+    B.pb_op_argmax(ptr(dev_f32(lg)), Bsz, V, V, ptr(toks), ptr(nan), stream())
+    torch.cuda.synchronize()
+    assert toks.cpu().tolist() == [int(np.argmax(r)) for r in lg] and nan.item() == 0
+    lg[2, 5] = np.nan
+    B.pb_op_argmax(ptr(dev_f32(lg)), Bsz, V, V, ptr(toks), ptr(nan), stream())
+    torch.cuda.synchronize()
+    assert nan.item() == 1
+    # embedding (+ OPT positions, offset 2), token-major rows
+    T = 7
+    P = rbits(rng, (T + 2, d), 0.035)
+    tok = rng.integers(0, V, size=T * Bsz).astype(np.int32)
+    h = torch.zeros((T * Bsz, d), device="cuda")
+    B.pb_op_embed(ptr(Ed), ptr(dev_bf16(P)), ptr(torch.from_numpy(tok).cuda()), ptr(h), d, 0, T * Bsz, Bsz, stream())
+    torch.cuda.synchronize()
+    want = bf16_bits_to_f64(E)[tok] + bf16_bits_to_f64(P)[np.arange(T * Bsz) // Bsz + 2]
+    assert np.array_equal(h.cpu().numpy(), want.astype(np.float32))
