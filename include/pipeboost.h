@@ -232,6 +232,19 @@ typedef struct {
 } pb_timeline_t;
 PB_API pb_status pb_timeline(pb_ctx* ctx, pb_timeline_t* out);
 
+/* Optional per-launch kernel timing (CUDA events around every kernel this rank launches, recorded on
+ * the launching stream). Off by default. pb_kernel_stats aggregates the LAST trial per kernel class:
+ * launches, summed device duration, and the algorithmic flops / bytes of those launches (the work the
+ * method must do: GEMM 2MNK, merge 4 bytes per weight element + operands, ...). Classes: "merge",
+ * "gemm", "attention", "norm", "rope", "embed", "logits", "argmax", "signal". */
+typedef struct {
+    const char* name;
+    int32_t launches;
+    double total_ms, flops, bytes;
+} pb_kernel_stat;
+PB_API pb_status pb_ctx_set_profiling(pb_ctx* ctx, int32_t enable);
+PB_API pb_status pb_kernel_stats(pb_ctx* ctx, pb_kernel_stat* out, int32_t cap, int32_t* n);
+
 PB_API const char* pb_last_error(void);
 PB_API void pb_ctx_free(pb_ctx* ctx);
 

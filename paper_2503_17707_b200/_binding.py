@@ -72,6 +72,11 @@ class pb_timeline_t(C.Structure):
                 ("chunk_gathered_ms", C.POINTER(C.c_double)), ("n_launches", C.c_int32)]
 
 
+class pb_kernel_stat(C.Structure):
+    _fields_ = [("name", C.c_char_p), ("launches", C.c_int32), ("total_ms", C.c_double), ("flops", C.c_double),
+                ("bytes", C.c_double)]
+
+
 _P = C.c_void_p
 _SIGS = {
     "pb_plan_create": [C.POINTER(pb_model_desc), C.POINTER(pb_adapter_desc), C.c_int32, C.c_int32,
@@ -96,6 +101,8 @@ _SIGS = {
     "pb_sync": [_P],
     "pb_timeline": [_P, C.POINTER(pb_timeline_t)],
     "pb_ctx_free": [_P],
+    "pb_ctx_set_profiling": [_P, C.c_int32],
+    "pb_kernel_stats": [_P, C.POINTER(pb_kernel_stat), C.c_int32, C.POINTER(C.c_int32)],
     "pb_last_error": [],
     # include/pipeboost_ops.h
     "pb_op_merge": [_P, C.c_int64, C.c_int32, C.c_int32, _P, _P, C.c_int32, C.c_float, _P],
@@ -261,6 +268,18 @@ def pb_timeline(ctx) -> pb_timeline_t:
     t = pb_timeline_t()
     check(lib().pb_timeline(ctx, C.byref(t)))
     return t
+
+
+def pb_ctx_set_profiling(ctx, enable):
+    check(lib().pb_ctx_set_profiling(ctx, 1 if enable else 0))
+
+
+def pb_kernel_stats(ctx):
+    n = C.c_int32(0)
+    arr = (pb_kernel_stat * 16)()
+    check(lib().pb_kernel_stats(ctx, arr, 16, C.byref(n)))
+    return {arr[i].name.decode(): {"launches": arr[i].launches, "total_ms": arr[i].total_ms, "flops": arr[i].flops,
+                                   "bytes": arr[i].bytes} for i in range(n.value)}
 
 
 def pb_ctx_free(ctx):

@@ -296,6 +296,7 @@ extern "C" void pb_ctx_free(pb_ctx* c) {
     for (auto e : c->landed) d(e);
     for (auto e : c->gathered) d(e);
     for (auto e : c->tensor_ready) d(e);
+    for (auto& r : c->prof) { d(r.a); d(r.b); }
     for (auto& p : c->peers)
         for (void* b : p.ipc_bases) cudaIpcCloseMemHandle(b);
     if (c->h_tokens) cudaFreeHost(c->h_tokens);
@@ -394,17 +395,72 @@ static uint32_t* flag_ptr(char* ws, const WsLayout& L, int32_t word) {
     return reinterpret_cast<uint32_t*>(ws + L.flags) + word;
 }
 
+static int prof_begin(pb_ctx* c, int cls, cudaStream_t s) {
+    if (!c->profiling) return -1;
+    if (c->prof_n == c->prof.size()) {
+        ProfRec r{};
+        if (cudaEventCreate(&r.a) != cudaSuccess || cudaEventCreate(&r.b) != cudaSuccess) return -1;
+        c->prof.push_back(r);
+    }
+    ProfRec& r = c->prof[c->prof_n];
+    r.cls = cls;
+    r.flops = r.bytes = 0;
+    if (cudaEventRecord(r.a, s) != cudaSuccess) return -1;
+    return (int)c->prof_n++;
+}
+
+static void prof_end(pb_ctx* c, int i, cudaStream_t s, double flops, double bytes) {
+    if (i < 0) return;
+    ProfRec& r = c->prof[i];
+    r.flops = flops;
+    r.bytes = bytes;
+    cudaEventRecord(r.b, s);
+}
+
 // Publish readiness word `word` (= epoch) on the given ranks.
 static cudaError_t signal_ranks(pb_ctx* c, int32_t word, const std::vector<int32_t>& ranks, cudaStream_t s) {
     SignalTargets t{};
     for (int32_t r : ranks) t.addr[t.n++] = flag_ptr(c->peers[r].ws, c->L, word);
     if (t.n == 0) return cudaSuccess;
     ++c->n_launches;
-    return launch_signal(t, c->epoch, s);
+    const int pi = prof_begin(c, K_SIGNAL, s);
+    cudaError_t e = launch_signal(t, c->epoch, s);
+    prof_end(c, pi, s, 0, 4.0 * t.n);
+    return e;
 }
 
 static cudaError_t wait_word(pb_ctx* c, int32_t word, cudaStream_t s) {
     return stream_wait_geq(s, flag_ptr(c->ws, c->L, word), c->epoch);
+}
+
+extern "C" pb_status pb_ctx_set_profiling(pb_ctx* c, int32_t enable) {
+    pb_status st = check_ctx(c, "pb_ctx_set_profiling");
+    if (st) return st;
+    c->profiling = enable != 0;
+    return PB_OK;
+}
+
+extern "C" pb_status pb_kernel_stats(pb_ctx* c, pb_kernel_stat* out, int32_t cap, int32_t* n) {
+    pb_status st = check_ctx(c, "pb_kernel_stats");
+    if (st) return st;
+    if (!n) return fail(PB_EINVAL, "pb_kernel_stats: null n");
+    static const char* names[K_NCLASS] = {"merge", "gemm", "attention", "norm", "rope", "embed", "logits", "argmax", "signal"};
+    pb_kernel_stat agg[K_NCLASS];
+    for (int k = 0; k < K_NCLASS; ++k) agg[k] = {names[k], 0, 0.0, 0.0, 0.0};
+    for (size_t i = 0; i < c->prof_n; ++i) {
+        const ProfRec& r = c->prof[i];
+        float ms = 0;
+        CU(cudaEventElapsedTime(&ms, r.a, r.b));
+        pb_kernel_stat& a = agg[r.cls];
+        a.launches++;
+        a.total_ms += ms;
+        a.flops += r.flops;
+        a.bytes += r.bytes;
+    }
+    *n = K_NCLASS;
+    if (!out || cap < K_NCLASS) return fail(PB_ENOMEM, "pb_kernel_stats: need %d entries", (int)K_NCLASS);
+    for (int k = 0; k < K_NCLASS; ++k) out[k] = agg[k];
+    return PB_OK;
 }
 
 extern "C" pb_status pb_trial_begin(pb_ctx* c, uint32_t epoch) {
@@ -415,6 +471,7 @@ extern "C" pb_status pb_trial_begin(pb_ctx* c, uint32_t epoch) {
         if (!c->peers[r].linked) return fail(PB_EPROTOCOL, "peer %d not wired (import/link)", r);
     c->epoch = epoch;
     c->n_launches = 0;
+    c->prof_n = 0;
     c->load_bytes = c->recv_bytes = 0;
     std::fill(c->tl_landed.begin(), c->tl_landed.end(), -1.0);
     std::fill(c->tl_gathered.begin(), c->tl_gathered.end(), -1.0);
@@ -467,7 +524,10 @@ extern "C" pb_status pb_merge_lora(pb_ctx* c, int32_t adapter_id) {
                     CU(cudaStreamWaitEvent(c->merge, c->landed[a], 0));
                     waited[a] = 1;
                 }
+            const int pi = prof_begin(c, K_MERGE, c->merge);
             CU(launch_merge(job.maps, job.rows, job.cols, job.rank, job.scale, c->merge));
+            prof_end(c, pi, c->merge, 2.0 * job.rows * job.cols * job.rank,
+                     4.0 * job.rows * job.cols + 2.0 * job.rank * (job.rows + job.cols));
             ++c->n_launches;
         }
         if (!others.empty()) CU(signal_ranks(c, c->L.f_chunk + id, others, c->merge));
@@ -550,31 +610,54 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B) {
         a.up_row0 = f;
         return a;
     };
+    // Algorithmic work of a GEMM launch: 2MNK flops; bytes = X + W + output (fp32 residual read + write).
+    auto gemm = [&](const CUtensorMap& mx, const CUtensorMap& mw, const GemmArgs& a, int n_w_rows) -> cudaError_t {
+        const int pi = prof_begin(c, K_GEMM, s);
+        cudaError_t e = launch_gemm(mx, mw, a, s);
+        const double M = rows, N = a.N, K = a.K;
+        const double out_b = a.epi == EPI_RESID ? 8.0 * M * N : 2.0 * M * N;
+        prof_end(c, pi, s, 2.0 * M * n_w_rows * K, 2.0 * M * K + 2.0 * n_w_rows * K + out_b);
+        return e;
+    };
+    auto norm = [&](const char* g_name, const char* b_name) -> cudaError_t {
+        const int pi = prof_begin(c, K_NORM, s);
+        cudaError_t e = launch_norm(h + (size_t)r0 * d, d, x + (size_t)r0 * d, d, rows, d, wt(c, l, g_name),
+                                    opt ? wt(c, l, b_name) : nullptr, m.norm_eps, s);
+        prof_end(c, pi, s, 8.0 * rows * d, 6.0 * rows * d);
+        return e;
+    };
     // --- attention block
-    CU(launch_norm(h + (size_t)r0 * d, d, x + (size_t)r0 * d, d, rows, d, wt(c, l, "ln1_g"),
-                   opt ? wt(c, l, "ln1_b") : nullptr, m.norm_eps, s));
+    CU(norm("ln1_g", "ln1_b"));
     GemmArgs a = G(r0, qdim, d, EPI_BF16, opt ? wt(c, l, "qkv_b") : nullptr, 0, opt ? 1.0f / sqrtf((float)hd) : 1.0f,
                    opt ? d : 0, qkv, qdim);
-    CU(launch_gemm(c->map_x, lm.qkv, a, s));
-    if (!opt)
+    CU(gemm(c->map_x, lm.qkv, a, qdim));
+    if (!opt) {
+        const int pi = prof_begin(c, K_ROPE, s);
         CU(launch_rope(qkv, qdim, r0, r1, B, H, KVH, hd, qd, reinterpret_cast<const float2*>(c->ws + L.rope), s));
-    CU(launch_attention(qkv, qdim, attn, qd, ta, tb, B, H, KVH, hd, qd, qd + kvd, opt ? 1.0f : 1.0f / sqrtf((float)hd),
-                        s));
+        prof_end(c, pi, s, 6.0 * rows * (qd + kvd) / 2, 4.0 * rows * (qd + kvd));
+    }
+    {
+        const int pi = prof_begin(c, K_ATTN, s);
+        CU(launch_attention(qkv, qdim, attn, qd, ta, tb, B, H, KVH, hd, qd, qd + kvd,
+                            opt ? 1.0f : 1.0f / sqrtf((float)hd), s));
+        // causal pairs: sum over queries t in [ta, tb) of (t + 1) keys
+        const double pairs = (double)B * ((double)tb * (tb + 1) / 2 - (double)ta * (ta + 1) / 2);
+        prof_end(c, pi, s, 4.0 * pairs * H * hd, 2.0 * rows * qd * 2 + 2.0 * B * tb * 2 * kvd);
+    }
     a = G(r0, d, qd, EPI_RESID, opt ? wt(c, l, "o_b") : nullptr, 0, 1.f, 0, h, d);
-    CU(launch_gemm(c->map_attn, lm.o, a, s));
+    CU(gemm(c->map_attn, lm.o, a, d));
     // --- MLP block
-    CU(launch_norm(h + (size_t)r0 * d, d, x + (size_t)r0 * d, d, rows, d, wt(c, l, "ln2_g"),
-                   opt ? wt(c, l, "ln2_b") : nullptr, m.norm_eps, s));
+    CU(norm("ln2_g", "ln2_b"));
     if (opt) {
         a = G(r0, f, d, EPI_BF16, wt(c, l, "fc1_b"), 1, 1.f, 0, mlp, f);
-        CU(launch_gemm(c->map_x, lm.up, a, s));
+        CU(gemm(c->map_x, lm.up, a, f));
         a = G(r0, d, f, EPI_RESID, wt(c, l, "fc2_b"), 0, 1.f, 0, h, d);
-        CU(launch_gemm(c->map_mlp, lm.down, a, s));
+        CU(gemm(c->map_mlp, lm.down, a, d));
     } else {
         a = G(r0, f, d, EPI_SILU_MUL, nullptr, 0, 1.f, 0, mlp, f);
-        CU(launch_gemm(c->map_x, lm.up, a, s));
+        CU(gemm(c->map_x, lm.up, a, 2 * f));
         a = G(r0, d, f, EPI_RESID, nullptr, 0, 1.f, 0, h, d);
-        CU(launch_gemm(c->map_mlp, lm.down, a, s));
+        CU(gemm(c->map_mlp, lm.down, a, d));
     }
     c->n_launches += opt ? 7 : 8;
     return PB_OK;
@@ -647,8 +730,10 @@ extern "C" pb_status pb_prefill_enqueue(pb_ctx* c, const int32_t* tokens, int32_
                 E.slice_begin[1] = INT32_MAX;
                 E.n = 1;
             }
+            const int pi = prof_begin(c, K_EMBED, s);
             CU(launch_embed(E, opt ? wt(c, -1, "pos") : nullptr, reinterpret_cast<const int32_t*>(c->ws + L.tokens), h, d,
                             r0, r1, B, s));
+            prof_end(c, pi, s, (opt ? 1.0 : 0.0) * (r1 - r0) * d, (r1 - r0) * d * (opt ? 8.0 : 6.0));
             ++c->n_launches;
         } else {
             CU(wait_word(c, L.f_act + j, s));
@@ -672,8 +757,10 @@ extern "C" pb_status pb_prefill_enqueue(pb_ctx* c, const int32_t* tokens, int32_
     if (g == N - 1) {
         CU(cudaStreamWaitEvent(s, c->tensor_ready[p->find_tensor("final_g")], 0));
         if (opt) CU(cudaStreamWaitEvent(s, c->tensor_ready[p->find_tensor("final_b")], 0));
+        const int pi = prof_begin(c, K_NORM, s);
         CU(launch_norm(h + (size_t)(T - 1) * B * d, d, y, d, B, d, wt(c, -1, "final_g"), opt ? wt(c, -1, "final_b") : nullptr,
                        m.norm_eps, s));
+        prof_end(c, pi, s, 8.0 * B * d, 6.0 * B * d);
         ++c->n_launches;
         std::vector<int32_t> remote;
         for (int32_t r : owners)
@@ -692,7 +779,9 @@ extern "C" pb_status pb_prefill_enqueue(pb_ctx* c, const int32_t* tokens, int32_
         int32_t v0, v1;
         head_slice(p, g, &v0, &v1);
         const __nv_bfloat16* E = reinterpret_cast<const __nv_bfloat16*>(c->weights + p->tensors[ht].dev_off);
+        const int pi = prof_begin(c, K_LOGITS, s);
         CU(launch_logits(y, B, d, E, v0, v1, logits, V, s));
+        prof_end(c, pi, s, 2.0 * B * (v1 - v0) * d, 2.0 * (double)(v1 - v0) * d + 4.0 * B * (v1 - v0));
         ++c->n_launches;
         if (g != 0) {
             CU(cudaMemcpy2DAsync(c->peers[0].ws + L.logits + (size_t)v0 * 4, (size_t)V * 4, logits + v0, (size_t)V * 4,
@@ -703,8 +792,10 @@ extern "C" pb_status pb_prefill_enqueue(pb_ctx* c, const int32_t* tokens, int32_
     if (g == 0) {
         for (int32_t r : owners)
             if (r != 0) CU(wait_word(c, L.f_logit + r, s));
+        const int pi = prof_begin(c, K_ARGMAX, s);
         CU(launch_argmax(logits, B, V, V, reinterpret_cast<int32_t*>(c->ws + L.tok_out),
                          reinterpret_cast<int32_t*>(c->ws + L.nan), s));
+        prof_end(c, pi, s, 0, 4.0 * B * V);
         ++c->n_launches;
         CU(cudaMemcpyAsync(c->h_out, c->ws + L.tok_out, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, s));
         CU(cudaMemcpyAsync(c->h_out + B, c->ws + L.nan, sizeof(int32_t), cudaMemcpyDeviceToHost, s));

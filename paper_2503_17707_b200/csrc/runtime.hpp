@@ -44,6 +44,14 @@ struct Peer {
 
 enum class Phase { Idle, Begun, Loaded, Merged, Gathered, Prefilled };
 
+// Kernel classes timed by the optional per-launch profiler (pb_ctx_set_profiling).
+enum KClass : int { K_MERGE = 0, K_GEMM, K_ATTN, K_NORM, K_ROPE, K_EMBED, K_LOGITS, K_ARGMAX, K_SIGNAL, K_NCLASS };
+struct ProfRec {
+    int cls;
+    cudaEvent_t a, b;
+    double flops, bytes;
+};
+
 }  // namespace pb
 
 struct pb_ctx {
@@ -87,4 +95,7 @@ struct pb_ctx {
     int64_t load_bytes = 0, recv_bytes = 0;
     std::vector<double> tl_landed, tl_gathered;
     bool use_wait_value = true;
+    bool profiling = false;
+    std::vector<pb::ProfRec> prof;
+    size_t prof_n = 0;
 };

@@ -75,8 +75,8 @@ def test_gemm_bf16_epilogue(M, K, N, m0, m1):
     X, W, bias = _gemm_case(rng, M, K, N)
     out = torch.zeros((M, N), dtype=torch.bfloat16, device="cuda")
     sc_cols = N // 3
-    B.pb_op_gemm(ptr(dev_bf16(X)), M, m0, m1, K, ptr(dev_bf16(W)), N, N, 0, ptr(dev_bf16(bias)), 0, 0.125, sc_cols,
-                 ptr(out), N, stream())
+    Xd, Wd, bd = dev_bf16(X), dev_bf16(W), dev_bf16(bias)   # keep references alive across the async launch
+    B.pb_op_gemm(ptr(Xd), M, m0, m1, K, ptr(Wd), N, N, 0, ptr(bd), 0, 0.125, sc_cols, ptr(out), N, stream())
     torch.cuda.synchronize()
     ref = bf16_bits_to_f64(X) @ bf16_bits_to_f64(W).T + bf16_bits_to_f64(bias)
     ref[:, :sc_cols] *= 0.125
@@ -110,7 +110,8 @@ def test_gemm_relu_and_resid_and_silu():
     f = 136
     Wgu = rbits(rng, (2 * f, K), 0.05)
     out2 = torch.zeros((M, f), dtype=torch.bfloat16, device="cuda")
-    B.pb_op_gemm(ptr(Xd), M, 0, M, K, ptr(dev_bf16(Wgu)), 2 * f, f, 2, 0, 0, 1.0, 0, ptr(out2), f, stream())
+    Wgud = dev_bf16(Wgu)
+    B.pb_op_gemm(ptr(Xd), M, 0, M, K, ptr(Wgud), 2 * f, f, 2, 0, 0, 1.0, 0, ptr(out2), f, stream())
     torch.cuda.synchronize()
     gu = bf16_bits_to_f64(X) @ bf16_bits_to_f64(Wgu).T
     g, u = gu[:, :f], gu[:, f:]
@@ -129,7 +130,8 @@ def test_norm(rms, d):
     g = rbits(rng, (d,), 0.1) if False else f64_to_bf16_bits(1 + rng.uniform(-0.1, 0.1, d))
     b = f64_to_bf16_bits(rng.uniform(-0.02, 0.02, d))
     out = torch.zeros((rows, d), dtype=torch.bfloat16, device="cuda")
-    B.pb_op_norm(ptr(dev_f32(h)), rows, d, ptr(dev_bf16(g)), 0 if rms else ptr(dev_bf16(b)), 1e-5, ptr(out), stream())
+    hd_, gd, bd = dev_f32(h), dev_bf16(g), dev_bf16(b)
+    B.pb_op_norm(ptr(hd_), rows, d, ptr(gd), 0 if rms else ptr(bd), 1e-5, ptr(out), stream())
     torch.cuda.synchronize()
     hf = h.astype(np.float64)
     ref = OF.rms_norm(hf, bf16_bits_to_f64(g), 1e-5) if rms else \
@@ -148,7 +150,8 @@ def test_attention(T, Bsz, H, KVH, hd, t0, t1):
     qkv = rbits(rng, (T * Bsz, ld), 1.0)
     out = torch.zeros((T * Bsz, qd), dtype=torch.bfloat16, device="cuda")
     scale = hd ** -0.5
-    B.pb_op_attention(ptr(dev_bf16(qkv)), ld, ptr(out), qd, t0, t1, Bsz, H, KVH, hd, qd, qd + kvd, scale, stream())
+    qkvd = dev_bf16(qkv)
+    B.pb_op_attention(ptr(qkvd), ld, ptr(out), qd, t0, t1, Bsz, H, KVH, hd, qd, qd + kvd, scale, stream())
     torch.cuda.synchronize()
     got = bf16_bits_to_f64(host_bits(out))
     x = bf16_bits_to_f64(qkv)
@@ -191,9 +194,9 @@ def test_logits_argmax_embed():
     y = rbits(rng, (Bsz, d), 1.0)
     E = rbits(rng, (V, d), 0.035)
     logits = torch.full((Bsz, V), float("nan"), device="cuda")
-    Ed = dev_bf16(E)
-    B.pb_op_logits(ptr(dev_bf16(y)), Bsz, d, ptr(Ed), 100, 1000, ptr(logits), V, stream())
-    B.pb_op_logits(ptr(dev_bf16(y)), Bsz, d, ptr(Ed), 0, 100, ptr(logits), V, stream())
+    Ed, yd = dev_bf16(E), dev_bf16(y)
+    B.pb_op_logits(ptr(yd), Bsz, d, ptr(Ed), 100, 1000, ptr(logits), V, stream())
+    B.pb_op_logits(ptr(yd), Bsz, d, ptr(Ed), 0, 100, ptr(logits), V, stream())
     torch.cuda.synchronize()
     ref = bf16_bits_to_f64(y) @ bf16_bits_to_f64(E).T
     assert np.allclose(logits.cpu().numpy(), ref, rtol=1e-5, atol=1e-5)
@@ -202,11 +205,13 @@ def test_logits_argmax_embed():
     lg[1, 10] = lg[1, 900] = lg[1].max() + 1
     toks = torch.zeros(Bsz, dtype=torch.int32, device="cuda")
     nan = torch.zeros(1, dtype=torch.int32, device="cuda")
-    B.pb_op_argmax(ptr(dev_f32(lg)), Bsz, V, V, ptr(toks), ptr(nan), stream())
+    lgd = dev_f32(lg)
+    B.pb_op_argmax(ptr(lgd), Bsz, V, V, ptr(toks), ptr(nan), stream())
     torch.cuda.synchronize()
     assert toks.cpu().tolist() == [int(np.argmax(r)) for r in lg] and nan.item() == 0
     lg[2, 5] = np.nan
-    B.pb_op_argmax(ptr(dev_f32(lg)), Bsz, V, V, ptr(toks), ptr(nan), stream())
+    lgd2 = dev_f32(lg)
+    B.pb_op_argmax(ptr(lgd2), Bsz, V, V, ptr(toks), ptr(nan), stream())
     torch.cuda.synchronize()
     assert nan.item() == 1
     # embedding (+ OPT positions, offset 2), token-major rows
@@ -214,7 +219,8 @@ def test_logits_argmax_embed():
     P = rbits(rng, (T + 2, d), 0.035)
     tok = rng.integers(0, V, size=T * Bsz).astype(np.int32)
     h = torch.zeros((T * Bsz, d), device="cuda")
-    B.pb_op_embed(ptr(Ed), ptr(dev_bf16(P)), ptr(torch.from_numpy(tok).cuda()), ptr(h), d, 0, T * Bsz, Bsz, stream())
+    Pd, tokd = dev_bf16(P), torch.from_numpy(tok).cuda()
+    B.pb_op_embed(ptr(Ed), ptr(Pd), ptr(tokd), ptr(h), d, 0, T * Bsz, Bsz, stream())
     torch.cuda.synchronize()
     want = bf16_bits_to_f64(E)[tok] + bf16_bits_to_f64(P)[np.arange(T * Bsz) // Bsz + 2]
     assert np.array_equal(h.cpu().numpy(), want.astype(np.float32))
