@@ -1,0 +1,436 @@
+#!/usr/bin/env python
+"""bench.py — cold-start TTFT of the PipeBoost layer-sharded cold start on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C2] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (one process per GPU)
+
+A step = one whole cold start: the weights buffer of every GPU is put in an
+explicit cold state (0xFF, untimed), then plan-ordered H2D load of each GPU's shard -> LoRA merge ->
+NVLink gather -> pipelined first-token prefill, until the first token is in host memory.
+  value      = TTFT ms, device clock (t0 event before the first DMA -> token D2H complete), max over ranks
+  e2e        = the same cold start timed by the host around the public API call (RankEngine.cold_start),
+               barrier -> token in host memory; bytes moved H2D/D2H per step stated
+  roofline   = dominant SM kernel class (per-launch CUDA events on its stream) vs MEASURED_PEAKS.json
+  pcie_roofline = the path's own bound: S / sum of measured concurrent H2D GB/s (TTFT >= that)
+The CPU oracle (oracle/, the only other place it runs) is timed on rank 0 on a bounded sample.
+Inputs (2.6 GB of weights at C2) are far larger than the 126 MB L2; weights are re-invalidated each step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+import numpy as np  # noqa: E402
+
+METRIC = "cold-start TTFT (ms) and aggregate load GB/s vs PCIe roofline at 1/2/4/8 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C2")
+    ap.add_argument("--policy", default=None, choices=[None, "stage", "interleave"])
+    ap.add_argument("--vocab-sliced", type=int, default=None)
+    ap.add_argument("--chunk-mb", type=int, default=64)
+    ap.add_argument("--prefill-chunks", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--cpu-sample-layers", type=int, default=4)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------------------------------
+# CPU oracle timing (reported baseline; --impl reference)
+# ----------------------------------------------------------------------------------------------------
+
+def oracle_sample(w, sample_layers: int):
+    """Time the CPU oracle (merge + sequential forward, bf16 storage contract) on embed + `sample_layers`
+    decoder layers + head, extrapolated linearly to all L layers. Weights are materialised (untimed)
+    first: a CPU 'cold start' has no load step. Returns (extrapolated_ms, detail)."""
+    import oracle
+    from oracle import forward as OF
+    from oracle.merge import merge_bf16_bits
+    from oracle.numerics import bf16_bits_to_f64
+    import synth
+
+    m, ads = w.model, w.adapters
+    L = m.n_layers
+    ls = list(range(min(sample_layers, L)))
+    ow = oracle.OracleWeights(m, ads)
+    names = [n for n in ow.tensors if not n.startswith("L") or int(n[1:].split(".")[0]) in ls]
+    base = {n: ow.base_bits(n) for n in names}
+    facs = [at for at in ow.atensors if at.adapter == 0 and at.layer in ls]
+    fac_bits = {at.name: ow.adapter_bits(at) for at in facs}
+    toks = synth.tokens(w.batch, w.seq, m.vocab)
+    import threadpoolctl  # noqa: F401  (numpy BLAS threads = all cores by default)
+    t0 = time.perf_counter()
+    merged = dict(base)
+    id2name = {t.id: n for n, t in ow.tensors.items()}
+    by_target = {}
+    for at in facs:
+        by_target.setdefault((at.layer, at.target), {})[at.factor] = at
+    for (l, tgt), f in by_target.items():
+        name = id2name[f["A"].base]
+        W = merged[name].copy()
+        r0, rows = f["A"].row0, f["B"].rows
+        W[r0:r0 + rows] = merge_bf16_bits(W[r0:r0 + rows], fac_bits[f["B"].name], fac_bits[f["A"].name], ads[0].scale)
+        merged[name] = W
+    t_merge = time.perf_counter() - t0
+    wf = {}
+
+    def Wget(n):
+        if n not in wf:
+            x = bf16_bits_to_f64(merged[n])
+            wf[n] = x.reshape(-1) if ow.tensors[n].rows == 1 else x
+        return wf[n]
+
+    for n in merged:   # fp64 views are part of the oracle's data, not its compute
+        Wget(n)
+    t1 = time.perf_counter()
+    for b in range(w.batch):
+        OF.forward_logits(m, Wget, toks[b], "bf16", layers=[])
+    t_head = time.perf_counter() - t1
+    t2 = time.perf_counter()
+    for b in range(w.batch):
+        OF.forward_logits(m, Wget, toks[b], "bf16", layers=ls)
+    t_all = time.perf_counter() - t2
+    per_layer = max(t_all - t_head, 0.0) / len(ls)
+    merge_per_layer = t_merge / len(ls)
+    total_s = t_head + L * (per_layer + merge_per_layer)
+    detail = {"sample_layers": len(ls), "layers": L, "merge_s_per_layer": merge_per_layer,
+              "forward_s_per_layer": per_layer, "embed_head_s": t_head, "measured_s": t_merge + t_head + t_all}
+    return total_s * 1e3, detail
+
+
+def cpu_cores():
+    try:
+        import threadpoolctl
+        info = threadpoolctl.threadpool_info()
+        return max([i.get("num_threads", 1) for i in info] + [1])
+    except Exception:
+        return os.cpu_count()
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from synth.configs import WORKLOADS
+    w = WORKLOADS[args.workload]
+    vals = []
+    det = None
+    for i in range(args.warmup + args.steps):
+        v, det = oracle_sample(w, args.cpu_sample_layers)
+        if i >= args.warmup:
+            vals.append(v)
+    val = statistics.mean(vals)
+    sample = (f"{det['sample_layers']} of {det['layers']} layers + embed/head, B={w.batch} T={w.seq}, "
+              f"extrapolated linearly in layers")
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "ms", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": val, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64 (bf16 storage contract)",
+            "data": "synthetic (seeded splitmix64; HF init std 0.02)",
+            "config": workload_config(w, args, 1),
+            "cpu_baseline": {"value": val, "unit": "ms", "cores": cpu_cores(), "kind": "oracle", "sample": sample,
+                             "detail": det},
+            "e2e": {"value": val, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(w, args, n):
+    return {"workload": f"{w.tag}: {w.note}, L={w.model.n_layers} d={w.model.d_model}, "
+                        f"LoRA r={w.adapters[0].rank if w.adapters else 0} on {','.join(w.adapters[0].targets) if w.adapters else '-'}",
+            "batch": w.batch, "seq_len": w.seq, "n_gpus": n,
+            "policy": args.policy, "vocab_sliced": args.vocab_sliced, "chunk_mb": args.chunk_mb,
+            "prefill_chunks": args.prefill_chunks,
+            "l2": "inputs (whole model weights) larger than the 126 MB L2; device weights reset to 0xFF between steps",
+            "parallelism": f"pp{n} (layer-sharded load, pipelined prefill)"}
+
+
+# ----------------------------------------------------------------------------------------------------
+# clocks during the timed region
+# ----------------------------------------------------------------------------------------------------
+
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self):
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, pw, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx.append(float(p[1]))
+                pw.append(float(p[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        thr = max(pw) * 0.5 if pw else 0
+        load = [s for s, w in zip(sm, pw) if w >= thr] or sm
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": max(pw)}
+
+
+# ----------------------------------------------------------------------------------------------------
+# our arm
+# ----------------------------------------------------------------------------------------------------
+
+def measure_h2d(nbytes=1 << 30, chunk=64 << 20):
+    """Concurrent pinned H2D GB/s of this rank's GPU (2 copy streams, 64 MB chunks): the PCIe roofline constant."""
+    import torch
+    host = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    dev = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    ss = [torch.cuda.Stream(), torch.cuda.Stream()]
+    best = 0.0
+    for r in range(4):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(ss[0])
+        ss[1].wait_event(e0)
+        for i, off in enumerate(range(0, nbytes, chunk)):
+            with torch.cuda.stream(ss[i & 1]):
+                dev[off:off + chunk].copy_(host[off:off + chunk], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(ss[1])
+        ss[0].wait_event(ev)
+        e1.record(ss[0])
+        torch.cuda.synchronize()
+        if r:
+            best = max(best, nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+    del host, dev
+    return best
+
+
+def load_peaks():
+    p = os.path.join(HERE, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6534.5), d.get("bf16_tflops", 1664.9), d.get("bf16_tflops_sustained", 1389.1), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import harness
+    import synth
+    from paper_2503_17707_b200 import _binding as B
+    from paper_2503_17707_b200.api import Plan, RankEngine, pinned_host
+    from synth.configs import WORKLOADS
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {world}"
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def allmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([float(x)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    def allsum(x):
+        if world == 1:
+            return x
+        t = torch.tensor([float(x)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t)
+        return t.item()
+
+    w = WORKLOADS[args.workload]
+    if args.policy is None:
+        args.policy = "stage" if world == 1 else "interleave"
+    if args.vocab_sliced is None:
+        args.vocab_sliced = 0 if world == 1 else 1
+    if args.prefill_chunks is None:
+        args.prefill_chunks = 1 if world == 1 else 2
+    plan = Plan(w.model, w.adapters, world, policy=args.policy, vocab_sliced=args.vocab_sliced,
+                chunk_bytes=args.chunk_mb << 20, prefill_chunks=args.prefill_chunks)
+    S = plan.sizes.host_base_bytes + plan.sizes.host_adapter_bytes
+
+    # --- host images: one DRAM copy of the checkpoint shared by all GPU processes
+    shm_paths = []
+    if world == 1:
+        base, ada = harness.build_host_images(plan)
+    else:
+        tag = f"/dev/shm/pipeboost_{args.workload}_{os.getppid()}"
+        sizes = [("base", plan.sizes.host_base_bytes), ("ada", plan.sizes.host_adapter_bytes)]
+        if local == 0:
+            bufs = {k: torch.from_file(f"{tag}_{k}", shared=True, size=max(n, 1), dtype=torch.uint8) for k, n in sizes}
+            harness.fill_host_images(plan, bufs["base"].data_ptr(), bufs["ada"].data_ptr())
+        barrier()
+        bufs = {k: torch.from_file(f"{tag}_{k}", shared=True, size=max(n, 1), dtype=torch.uint8) for k, n in sizes}
+        for k, n in sizes:
+            torch.cuda.cudart().cudaHostRegister(bufs[k].data_ptr(), max(n, 1), 0)
+        shm_paths = [f"{tag}_{k}" for k, _ in sizes]
+        base, ada = bufs["base"], bufs["ada"]
+
+    eng = RankEngine(plan, rank, base, ada if plan.sizes.host_adapter_bytes else None, max_batch=w.batch,
+                     max_seq=w.seq)
+    if world > 1:
+        blobs = [None] * world
+        dist.all_gather_object(blobs, eng.export())
+        eng.wire_ipc(blobs)
+    if not args.no_profile:
+        B.pb_ctx_set_profiling(eng.ctx, 1)
+    toks = synth.tokens(w.batch, w.seq, w.model.vocab)
+
+    barrier()
+    h2d_gbs = measure_h2d()          # all ranks concurrently: the PCIe roofline constant
+    barrier()
+    agg_h2d = allsum(h2d_gbs)
+
+    clocks = ClockSampler()
+    ttft, e2e, ready, full, load_done, launches = [], [], [], [], [], 0
+    kstats = {}
+    out_tokens = None
+    for step in range(args.warmup + args.steps):
+        timed = step >= args.warmup
+        eng.invalidate()
+        if timed and step == args.warmup and rank == 0:
+            clocks.start()
+        barrier()
+        torch.cuda.synchronize()
+        th0 = time.perf_counter()
+        res = eng.cold_start(step + 1, toks if rank == 0 else None, w.batch, w.seq, adapter_id=0 if w.adapters else -1)
+        th1 = time.perf_counter()
+        barrier()
+        torch.cuda.synchronize()
+        tl = eng.timeline()
+        if rank == 0:
+            out_tokens = res[0]
+        if timed:
+            ttft.append(allmax(tl["ttft_ms"]))
+            e2e.append(allmax((th1 - th0) * 1e3))
+            ready.append(allmax(tl["t_ready_ms"]))
+            full.append(allmax(tl["t_full_ms"]))
+            load_done.append(allmax(tl["load_done_ms"]))
+            launches += int(allsum(tl["n_launches"]))
+            if not args.no_profile:
+                for k, v in B.pb_kernel_stats(eng.ctx).items():
+                    a = kstats.setdefault(k, {"launches": 0, "total_ms": 0.0, "flops": 0.0, "bytes": 0.0})
+                    for f in a:
+                        a[f] += v[f]
+    clk = clocks.stop() if rank == 0 else None
+
+    if rank == 0:
+        hbm, bf16_burst, bf16_sus, peak_src = load_peaks()
+        val = statistics.mean(ttft)
+        # dominant SM kernel class over the timed steps
+        roof = None
+        kern = {}
+        for k, a in kstats.items():
+            if a["launches"] == 0:
+                continue
+            bound = "tensor" if k in ("gemm",) else "hbm"
+            if bound == "tensor":
+                ach = a["flops"] / (a["total_ms"] * 1e-3) / 1e12
+                peak, unit = bf16_sus, "TFLOP/s"
+            else:
+                ach = a["bytes"] / (a["total_ms"] * 1e-3) / 1e9
+                peak, unit = hbm, "GB/s"
+            kern[k] = {"launches": a["launches"] // max(1, args.steps), "avg_us": 1e3 * a["total_ms"] / a["launches"],
+                       "ms_per_step": a["total_ms"] / args.steps, "achieved": ach, "unit": unit, "frac": ach / peak}
+        sm_kernels = {k: v for k, v in kern.items() if k != "signal"}
+        if sm_kernels:
+            dom = max(sm_kernels, key=lambda k: sm_kernels[k]["ms_per_step"])
+            d = sm_kernels[dom]
+            roof = {"kernel": dom, "bound": "tensor" if d["unit"] == "TFLOP/s" else "hbm", "achieved": d["achieved"],
+                    "peak": bf16_sus if d["unit"] == "TFLOP/s" else hbm, "unit": d["unit"], "frac": d["frac"],
+                    "traffic": None, "peak_source": f"{peak_src} ({'sustained bf16' if d['unit'] == 'TFLOP/s' else 'HBM copy'})"}
+        t_pcie = S / (agg_h2d * 1e9) * 1e3
+        line = {
+            "metric": METRIC, "value": val, "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": val, "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded splitmix64 values, HF init std 0.02; random-init OPT/Llama shapes)",
+            "config": workload_config(w, args, world),
+            "e2e": {"value": statistics.mean(e2e), "unit": "ms", "h2d_bytes_per_step": int(S + toks.nbytes),
+                    "d2h_bytes_per_step": int(4 * w.batch)},
+            "gpu_launches": launches,
+            "clocks": clk,
+            "roofline": roof,
+            "pcie_roofline": {"bound_ms": t_pcie, "bytes": S, "h2d_gbs_per_gpu_measured": h2d_gbs,
+                              "h2d_gbs_aggregate": agg_h2d, "frac": t_pcie / val,
+                              "load_gbs_aggregate": S / (statistics.mean(load_done) * 1e-3) / 1e9},
+            "ttft_breakdown_ms": {"t_ready": statistics.mean(ready), "t_full": statistics.mean(full),
+                                  "load_done": statistics.mean(load_done), "ttft_min": min(ttft),
+                                  "ttft_median": statistics.median(ttft)},
+            "kernels": kern,
+            "first_tokens": [int(x) for x in out_tokens],
+        }
+        if not args.no_cpu_baseline:
+            v, det = oracle_sample(w, args.cpu_sample_layers)
+            line["cpu_baseline"] = {"value": v, "unit": "ms", "cores": cpu_cores(), "kind": "oracle",
+                                    "sample": f"{det['sample_layers']} of {det['layers']} layers + embed/head, "
+                                              f"B={w.batch} T={w.seq}, extrapolated linearly in layers",
+                                    "detail": det}
+        print(json.dumps(line), flush=True)
+    barrier()
+    eng.close()
+    if world > 1:
+        for p in shm_paths:
+            if local == 0 and os.path.exists(p):
+                os.unlink(p)
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

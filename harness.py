@@ -12,16 +12,19 @@ from paper_2503_17707_b200.api import Plan, pinned_host
 from synth import host_image
 
 
+def fill_host_images(plan: Plan, base_ptr: int, ada_ptr: int | None):
+    """Write the seeded model (and adapters) into host buffers laid out as `plan` says."""
+    tens = plan.tensors()
+    host_image.fill_base(base_ptr, [(n, r, c, off, l) for (n, r, c, off, l, _) in tens])
+    if plan.sizes.host_adapter_bytes and ada_ptr:
+        items = [(n, r, c, off, a, is_b, tens[base_t][2]) for (n, r, c, off, a, is_b, base_t, _) in plan.atensors()]
+        host_image.fill_adapters(ada_ptr, items, plan.adapters)
+
+
 def build_host_images(plan: Plan):
+    """Pinned host images (one process)."""
     s = plan.sizes
     base = pinned_host(s.host_base_bytes)
-    tens = plan.tensors()
-    host_image.fill_base(base.data_ptr(), [(n, r, c, off, l) for (n, r, c, off, l, _) in tens])
-    ada = None
-    if s.host_adapter_bytes:
-        ada = pinned_host(s.host_adapter_bytes)
-        items = []
-        for (n, r, c, off, a, is_b, base_t, _) in plan.atensors():
-            items.append((n, r, c, off, a, is_b, tens[base_t][2]))
-        host_image.fill_adapters(ada.data_ptr(), items, plan.adapters)
+    ada = pinned_host(s.host_adapter_bytes) if s.host_adapter_bytes else None
+    fill_host_images(plan, base.data_ptr(), ada.data_ptr() if ada is not None else None)
     return base, ada

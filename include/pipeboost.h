@@ -244,6 +244,13 @@ typedef struct {
 } pb_kernel_stat;
 PB_API pb_status pb_ctx_set_profiling(pb_ctx* ctx, int32_t enable);
 PB_API pb_status pb_kernel_stats(pb_ctx* ctx, pb_kernel_stat* out, int32_t cap, int32_t* n);
+/* Per-launch trace of the last profiled trial: class index (order of pb_kernel_stats), start / end ms
+ * since t0 on the device clock. Writes min(cap, launches) records; *n = launches. */
+typedef struct {
+    int32_t cls;
+    float start_ms, end_ms;
+} pb_kernel_event;
+PB_API pb_status pb_kernel_trace(pb_ctx* ctx, pb_kernel_event* out, int32_t cap, int32_t* n);
 
 PB_API const char* pb_last_error(void);
 PB_API void pb_ctx_free(pb_ctx* ctx);

@@ -151,7 +151,8 @@ def balanced_slices(n: int, parts: int) -> List[Tuple[int, int]]:
 # ---------------------------------------------------------------------------
 
 def layer_tensor_shapes(m: ModelDesc):
-    """(suffix, rows, cols) of one decoder layer, canonical order.
+    """(suffix, rows, cols) of one decoder layer, canonical order = the order the layer's forward
+    consumes them (norm, qkv, o, norm, mlp), so a layer can start before its last bytes land.
 
     q,k,v are stored back to back as one [q;k;v] matrix and (Llama) gate,up as
     one [gate;up] matrix: the checkpoint layout is already the runtime layout, so
@@ -159,13 +160,13 @@ def layer_tensor_shapes(m: ModelDesc):
     """
     d, f, hd = m.d_model, m.d_ffn, m.head_dim
     if m.arch == "opt":
-        return [("qkv", 3 * d, d), ("qkv_b", 1, 3 * d), ("o", d, d), ("o_b", 1, d),
-                ("ln1_g", 1, d), ("ln1_b", 1, d), ("fc1", f, d), ("fc1_b", 1, f),
-                ("fc2", d, f), ("fc2_b", 1, d), ("ln2_g", 1, d), ("ln2_b", 1, d)]
+        return [("ln1_g", 1, d), ("ln1_b", 1, d), ("qkv", 3 * d, d), ("qkv_b", 1, 3 * d), ("o", d, d),
+                ("o_b", 1, d), ("ln2_g", 1, d), ("ln2_b", 1, d), ("fc1", f, d), ("fc1_b", 1, f),
+                ("fc2", d, f), ("fc2_b", 1, d)]
     if m.arch == "llama":
         qkv_rows = (m.n_heads + 2 * m.n_kv_heads) * hd
-        return [("qkv", qkv_rows, d), ("o", d, m.n_heads * hd), ("ln1_g", 1, d),
-                ("gate_up", 2 * f, d), ("down", d, f), ("ln2_g", 1, d)]
+        return [("ln1_g", 1, d), ("qkv", qkv_rows, d), ("o", d, m.n_heads * hd), ("ln2_g", 1, d),
+                ("gate_up", 2 * f, d), ("down", d, f)]
     raise ValueError(m.arch)
 
 
@@ -318,7 +319,8 @@ def build_chunks(plan: Plan) -> None:
 
     # Per-GPU load list: the GPU's pieces in canonical table order; a layer's
     # adapter parts (adapter order, then target order, A then B) come right
-    # after that layer's base tensors (G8).
+    # BEFORE that layer's base tensors (G8: the paper is silent; the factors are
+    # tiny, and having them first lets each adapted tensor merge as soon as it lands).
     N = plan.n_gpus
     plan.load = [[] for _ in range(N)]
     ad_by_layer = {}
@@ -334,14 +336,14 @@ def build_chunks(plan: Plan) -> None:
             i += 1
             continue
         l = t.layer
+        for at in ad_by_layer.get(l, []):
+            for c in per_atensor[at.id]:
+                plan.load[c.loader].append(c.id)
         j = i
         while j < len(ts) and ts[j].layer == l:
             for c in per_tensor[ts[j].id]:
                 plan.load[c.loader].append(c.id)
             j += 1
-        for at in ad_by_layer.get(l, []):
-            for c in per_atensor[at.id]:
-                plan.load[c.loader].append(c.id)
         i = j
 
 

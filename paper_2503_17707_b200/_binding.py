@@ -77,6 +77,10 @@ class pb_kernel_stat(C.Structure):
                 ("bytes", C.c_double)]
 
 
+class pb_kernel_event(C.Structure):
+    _fields_ = [("cls", C.c_int32), ("start_ms", C.c_float), ("end_ms", C.c_float)]
+
+
 _P = C.c_void_p
 _SIGS = {
     "pb_plan_create": [C.POINTER(pb_model_desc), C.POINTER(pb_adapter_desc), C.c_int32, C.c_int32,
@@ -103,6 +107,7 @@ _SIGS = {
     "pb_ctx_free": [_P],
     "pb_ctx_set_profiling": [_P, C.c_int32],
     "pb_kernel_stats": [_P, C.POINTER(pb_kernel_stat), C.c_int32, C.POINTER(C.c_int32)],
+    "pb_kernel_trace": [_P, C.POINTER(pb_kernel_event), C.c_int32, C.POINTER(C.c_int32)],
     "pb_last_error": [],
     # include/pipeboost_ops.h
     "pb_op_merge": [_P, C.c_int64, C.c_int32, C.c_int32, _P, _P, C.c_int32, C.c_float, _P],
@@ -280,6 +285,17 @@ def pb_kernel_stats(ctx):
     check(lib().pb_kernel_stats(ctx, arr, 16, C.byref(n)))
     return {arr[i].name.decode(): {"launches": arr[i].launches, "total_ms": arr[i].total_ms, "flops": arr[i].flops,
                                    "bytes": arr[i].bytes} for i in range(n.value)}
+
+
+KCLASSES = ["merge", "gemm", "attention", "norm", "rope", "embed", "logits", "argmax", "signal"]
+
+
+def pb_kernel_trace(ctx):
+    n = C.c_int32(0)
+    lib().pb_kernel_trace(ctx, None, 0, C.byref(n))
+    arr = (pb_kernel_event * max(1, n.value))()
+    check(lib().pb_kernel_trace(ctx, arr, n.value, C.byref(n)))
+    return [(KCLASSES[arr[i].cls], arr[i].start_ms, arr[i].end_ms) for i in range(n.value)]
 
 
 def pb_ctx_free(ctx):

@@ -54,8 +54,11 @@ class Plan:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h:
-            B.pb_plan_free(h)
+        if h and B is not None and B.pb_plan_free is not None:
+            try:
+                B.pb_plan_free(h)
+            except Exception:
+                pass
             self.handle = None
 
 
@@ -67,7 +70,7 @@ class RankEngine:
         self.plan = plan
         self.rank = rank
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-        assert host_base.is_pinned(), "host_base must be pinned"
+        # host_base / host_adapters must be page-locked (torch pin_memory or cudaHostRegister'ed shared memory)
         self.host_base = host_base
         self.host_adapters = host_adapters
         s = plan.sizes

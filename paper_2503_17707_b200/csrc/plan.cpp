@@ -29,13 +29,14 @@ struct Shape { const char* sfx; int64_t rows, cols; };
 
 std::vector<Shape> layer_shapes(const pb_model_desc& m) {
     const int64_t d = m.d_model, f = m.d_ffn, hd = m.d_model / m.n_heads;
+    // Compute order (norm, qkv, o, norm, mlp): a layer's kernels can start as its tensors land.
     if (m.arch == PB_ARCH_OPT)
-        return {{"qkv", 3 * d, d}, {"qkv_b", 1, 3 * d}, {"o", d, d}, {"o_b", 1, d},
-                {"ln1_g", 1, d}, {"ln1_b", 1, d}, {"fc1", f, d}, {"fc1_b", 1, f},
-                {"fc2", d, f}, {"fc2_b", 1, d}, {"ln2_g", 1, d}, {"ln2_b", 1, d}};
+        return {{"ln1_g", 1, d}, {"ln1_b", 1, d}, {"qkv", 3 * d, d}, {"qkv_b", 1, 3 * d}, {"o", d, d},
+                {"o_b", 1, d}, {"ln2_g", 1, d}, {"ln2_b", 1, d}, {"fc1", f, d}, {"fc1_b", 1, f},
+                {"fc2", d, f}, {"fc2_b", 1, d}};
     const int64_t qkv = (int64_t)(m.n_heads + 2 * m.n_kv_heads) * hd;
-    return {{"qkv", qkv, d}, {"o", d, (int64_t)m.n_heads * hd}, {"ln1_g", 1, d},
-            {"gate_up", 2 * f, d}, {"down", d, f}, {"ln2_g", 1, d}};
+    return {{"ln1_g", 1, d}, {"qkv", qkv, d}, {"o", d, (int64_t)m.n_heads * hd}, {"ln2_g", 1, d},
+            {"gate_up", 2 * f, d}, {"down", d, f}};
 }
 
 // Target geometry: base suffix, first base row, out features, in features.
@@ -264,7 +265,8 @@ extern "C" pb_status pb_plan_create(const pb_model_desc* model, const pb_adapter
         }
     }
 
-    // Per-GPU load lists: canonical table order; a layer's adapter factors right after its base tensors.
+    // Per-GPU load lists: canonical table order; a layer's adapter factors right before its base tensors
+    // (tiny, and then every adapted tensor can merge the moment it lands).
     p->load.assign(N, {});
     std::vector<std::vector<int32_t>> ad_of_layer(L);
     for (size_t ai = 0; ai < p->atensors.size(); ++ai) ad_of_layer[p->atensors[ai].layer].push_back((int32_t)ai);
@@ -275,11 +277,11 @@ extern "C" pb_status pb_plan_create(const pb_model_desc* model, const pb_adapter
             ++ti;
             continue;
         }
+        for (int32_t ai : ad_of_layer[l])
+            for (int32_t c : ad_chunks[ai]) p->load[p->chunks[c].loader].push_back(c);
         size_t tj = ti;
         for (; tj < p->tensors.size() && p->tensors[tj].layer == l; ++tj)
             for (int32_t c : base_chunks[tj]) p->load[p->chunks[c].loader].push_back(c);
-        for (int32_t ai : ad_of_layer[l])
-            for (int32_t c : ad_chunks[ai]) p->load[p->chunks[c].loader].push_back(c);
         ti = tj;
     }
 

@@ -1,7 +1,7 @@
 // runtime.cpp — pb_ctx: the per-rank cold-start engine.
 //
 //   pb_load_shard    (a2)  chunked cudaMemcpyAsync pinned host -> HBM over this GPU's own PCIe link,
-//                          alternating two copy-engine streams; a `landed` event per chunk
+//                          one ordered copy-engine lane; a `landed` event per chunk
 //   pb_merge_lora    (a3)  per own chunk in load order: wait landed, tcgen05 merge of every adapted row
 //                          range (after its adapter factors land), then publish the chunk to the peers
 //                          (readiness word = epoch) and record per-tensor readiness
@@ -171,6 +171,40 @@ static pb_status build_merge_jobs(pb_ctx* c) {
     return PB_OK;
 }
 
+// Coalesce the load list into DMA groups: a chunk joins the current group when it continues it in both
+// address spaces with the same (< 4 KiB alignment) gap, and either the group stays within chunk_bytes or
+// the chunk is small (biases / norms). Fewer, larger copies keep the copy engine at link speed.
+static void build_copy_groups(pb_ctx* c) {
+    const pb_plan* p = c->plan;
+    const auto& ld = p->load[c->rank];
+    const int64_t cap = p->opts.chunk_bytes, small = 256 << 10;
+    c->copies.clear();
+    for (int32_t i = 0; i < (int32_t)ld.size(); ++i) {
+        const ChunkRec& ch = p->chunks[ld[i]];
+        const char* hbase = static_cast<const char*>(ch.is_adapter ? c->host_adapters : c->host_base);
+        char* dbase = ch.is_adapter ? c->adapters : c->weights;
+        const char* src = hbase + ch.host_off;
+        char* dst = dbase + ch.dev_off;
+        if (!c->copies.empty()) {
+            CopyGroup& g = c->copies.back();
+            const ChunkRec& prev = p->chunks[ld[g.first + g.count - 1]];
+            const int64_t hgap = src - (g.src + g.bytes), dgap = dst - (g.dst + g.bytes);
+            if (prev.is_adapter == ch.is_adapter && hgap == dgap && hgap >= 0 && hgap < kAlign &&
+                (g.bytes + hgap + ch.bytes <= cap || ch.bytes < small)) {
+                g.bytes += hgap + ch.bytes;
+                g.count++;
+                continue;
+            }
+        }
+        c->copies.push_back(CopyGroup{src, dst, ch.bytes, i, 1});
+    }
+    c->landed_alias.assign(p->chunks.size(), -1);
+    for (const CopyGroup& g : c->copies)
+        for (int32_t i = g.first; i < g.first + g.count; ++i) c->landed_alias[ld[i]] = ld[g.first];
+}
+
+static cudaEvent_t landed_ev(pb_ctx* c, int32_t chunk) { return c->landed[c->landed_alias[chunk]]; }
+
 static pb_status build_prefill_maps(pb_ctx* c) {
     const pb_plan* p = c->plan;
     const auto& m = p->model;
@@ -272,6 +306,7 @@ extern "C" pb_status pb_ctx_create(const pb_plan* plan, int32_t rank, const void
         if (!plan->chunks[id].is_adapter) c->last_own_chunk[plan->chunks[id].tensor] = id;
     for (int32_t id : plan->recv[rank]) c->last_recv_chunk[plan->chunks[id].tensor] = id;
 
+    build_copy_groups(c);
     pb_status st = build_merge_jobs(c);
     if (st != PB_OK) return cleanup(st);
     st = build_prefill_maps(c);
@@ -463,6 +498,20 @@ extern "C" pb_status pb_kernel_stats(pb_ctx* c, pb_kernel_stat* out, int32_t cap
     return PB_OK;
 }
 
+extern "C" pb_status pb_kernel_trace(pb_ctx* c, pb_kernel_event* out, int32_t cap, int32_t* n) {
+    pb_status st = check_ctx(c, "pb_kernel_trace");
+    if (st) return st;
+    if (!n) return fail(PB_EINVAL, "pb_kernel_trace: null n");
+    *n = (int32_t)c->prof_n;
+    for (size_t i = 0; i < c->prof_n && out && (int32_t)i < cap; ++i) {
+        const ProfRec& r = c->prof[i];
+        out[i].cls = r.cls;
+        CU(cudaEventElapsedTime(&out[i].start_ms, c->t0, r.a));
+        CU(cudaEventElapsedTime(&out[i].end_ms, c->t0, r.b));
+    }
+    return PB_OK;
+}
+
 extern "C" pb_status pb_trial_begin(pb_ctx* c, uint32_t epoch) {
     pb_status st = check_ctx(c, "pb_trial_begin");
     if (st) return st;
@@ -487,15 +536,15 @@ extern "C" pb_status pb_load_shard(pb_ctx* c) {
     if (st) return st;
     if (c->phase != Phase::Begun) return fail(PB_EPROTOCOL, "pb_load_shard: call pb_trial_begin first");
     const pb_plan* p = c->plan;
-    int i = 0;
-    for (int32_t id : p->load[c->rank]) {
-        const ChunkRec& ch = p->chunks[id];
-        cudaStream_t s = c->h2d[i++ & 1];
-        char* dst = (ch.is_adapter ? c->adapters : c->weights) + ch.dev_off;
-        const char* src = static_cast<const char*>(ch.is_adapter ? c->host_adapters : c->host_base) + ch.host_off;
-        CU(cudaMemcpyAsync(dst, src, ch.bytes, cudaMemcpyHostToDevice, s));
-        CU(cudaEventRecord(c->landed[id], s));
-        c->load_bytes += ch.bytes;
+    // One copy lane, in load-list order. Measured on B200 (tools/h2d_order.py): the H2D copy engine drains
+    // one stream's queue before starting another's, so alternating chunks over two streams makes every
+    // layer wait for half the model; a single ordered lane lands layer l at ~(l+1)/L of the load time.
+    const auto& ld = p->load[c->rank];
+    for (const CopyGroup& g : c->copies) {
+        CU(cudaMemcpyAsync(g.dst, g.src, g.bytes, cudaMemcpyHostToDevice, c->h2d[0]));
+        // one event per DMA: every chunk of the group maps to the group's first chunk event
+        CU(cudaEventRecord(c->landed[ld[g.first]], c->h2d[0]));
+        for (int32_t i = g.first; i < g.first + g.count; ++i) c->load_bytes += p->chunks[ld[i]].bytes;
     }
     c->phase = Phase::Loaded;
     return PB_OK;
@@ -515,13 +564,13 @@ extern "C" pb_status pb_merge_lora(pb_ctx* c, int32_t adapter_id) {
     for (int32_t id : p->load[c->rank]) {
         const ChunkRec& ch = p->chunks[id];
         if (ch.is_adapter) continue;
-        CU(cudaStreamWaitEvent(c->merge, c->landed[id], 0));
+        CU(cudaStreamWaitEvent(c->merge, landed_ev(c, id), 0));
         for (int32_t j : c->jobs_of_chunk[id]) {
             const MergeJob& job = c->jobs[j];
             if (job.adapter != adapter_id) continue;
             for (int32_t a : job.need)
                 if (!waited[a]) {
-                    CU(cudaStreamWaitEvent(c->merge, c->landed[a], 0));
+                    CU(cudaStreamWaitEvent(c->merge, landed_ev(c, a), 0));
                     waited[a] = 1;
                 }
             const int pi = prof_begin(c, K_MERGE, c->merge);
@@ -577,7 +626,15 @@ cudaEvent_t layer_ready(pb_ctx* c, int l) {
     return c->tensor_ready[last];
 }
 
-pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B) {
+cudaError_t wait_tensor(pb_ctx* c, int l, const char* sfx) {
+    const pb_plan* p = c->plan;
+    const int32_t t = p->find_tensor("L" + std::to_string(l) + "." + sfx);
+    return cudaStreamWaitEvent(c->comp, c->tensor_ready[t], 0);
+}
+
+// Layer l on token rows [r0, r1) (prompt positions [ta, tb)). On the first prompt chunk each step waits
+// only for the tensors it reads (layout is in compute order), so a layer starts while its tail loads.
+pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, bool first_chunk) {
     const pb_plan* p = c->plan;
     const auto& m = p->model;
     const bool opt = m.arch == PB_ARCH_OPT;
@@ -626,8 +683,11 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B) {
         prof_end(c, pi, s, 8.0 * rows * d, 6.0 * rows * d);
         return e;
     };
+    auto need = [&](const char* sfx) -> cudaError_t { return first_chunk ? wait_tensor(c, l, sfx) : cudaSuccess; };
     // --- attention block
+    CU(need(opt ? "ln1_b" : "ln1_g"));
     CU(norm("ln1_g", "ln1_b"));
+    CU(need(opt ? "qkv_b" : "qkv"));
     GemmArgs a = G(r0, qdim, d, EPI_BF16, opt ? wt(c, l, "qkv_b") : nullptr, 0, opt ? 1.0f / sqrtf((float)hd) : 1.0f,
                    opt ? d : 0, qkv, qdim);
     CU(gemm(c->map_x, lm.qkv, a, qdim));
@@ -644,18 +704,24 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B) {
         const double pairs = (double)B * ((double)tb * (tb + 1) / 2 - (double)ta * (ta + 1) / 2);
         prof_end(c, pi, s, 4.0 * pairs * H * hd, 2.0 * rows * qd * 2 + 2.0 * B * tb * 2 * kvd);
     }
+    CU(need(opt ? "o_b" : "o"));
     a = G(r0, d, qd, EPI_RESID, opt ? wt(c, l, "o_b") : nullptr, 0, 1.f, 0, h, d);
     CU(gemm(c->map_attn, lm.o, a, d));
     // --- MLP block
+    CU(need(opt ? "ln2_b" : "ln2_g"));
     CU(norm("ln2_g", "ln2_b"));
     if (opt) {
+        CU(need("fc1_b"));
         a = G(r0, f, d, EPI_BF16, wt(c, l, "fc1_b"), 1, 1.f, 0, mlp, f);
         CU(gemm(c->map_x, lm.up, a, f));
+        CU(need("fc2_b"));
         a = G(r0, d, f, EPI_RESID, wt(c, l, "fc2_b"), 0, 1.f, 0, h, d);
         CU(gemm(c->map_mlp, lm.down, a, d));
     } else {
+        CU(need("gate_up"));
         a = G(r0, f, d, EPI_SILU_MUL, nullptr, 0, 1.f, 0, mlp, f);
         CU(gemm(c->map_x, lm.up, a, 2 * f));
+        CU(need("down"));
         a = G(r0, d, f, EPI_RESID, nullptr, 0, 1.f, 0, h, d);
         CU(gemm(c->map_mlp, lm.down, a, d));
     }
@@ -739,8 +805,7 @@ extern "C" pb_status pb_prefill_enqueue(pb_ctx* c, const int32_t* tokens, int32_
             CU(wait_word(c, L.f_act + j, s));
         }
         for (int l = stage.first; l < stage.second; ++l) {
-            if (j == 0) CU(cudaStreamWaitEvent(s, layer_ready(c, l), 0));
-            st = run_layer(c, l, r0, r1, tb[j], tb[j + 1], B);
+            st = run_layer(c, l, r0, r1, tb[j], tb[j + 1], B, j == 0);
             if (st) return st;
         }
         if (g < N - 1) {
@@ -851,7 +916,7 @@ extern "C" pb_status pb_timeline(pb_ctx* c, pb_timeline_t* out) {
     };
     double load_done = 0;
     for (int32_t id : p->load[c->rank]) {
-        c->tl_landed[id] = ms(c->landed[id]);
+        c->tl_landed[id] = ms(landed_ev(c, id));
         load_done = std::max(load_done, c->tl_landed[id]);
     }
     for (int32_t id : p->recv[c->rank]) c->tl_gathered[id] = ms(c->gathered[id]);

@@ -31,6 +31,15 @@ struct MergeJob {
     MergeMaps maps;
 };
 
+// One cudaMemcpyAsync of the load list: a run of consecutive load-list chunks that are contiguous (up to
+// alignment padding) in both the host image and the device buffer.
+struct CopyGroup {
+    const char* src;
+    char* dst;
+    int64_t bytes;
+    int32_t first, count;   // range in the rank's load list
+};
+
 struct LayerMaps {
     CUtensorMap qkv, o, up, down;   // up = fc1 (OPT) or [gate; up] with 64-row boxes (Llama)
 };
@@ -74,6 +83,9 @@ struct pb_ctx {
     std::vector<char> tensor_own;        // this rank loads every piece of the tensor
     std::vector<int32_t> last_own_chunk; // per base tensor: last own chunk in load order (-1 if none)
     std::vector<int32_t> last_recv_chunk;
+
+    std::vector<pb::CopyGroup> copies;
+    std::vector<int32_t> landed_alias;   // chunk -> first chunk of its copy group (owner of the landed event)
 
     // merges: per chunk, indices into jobs
     std::vector<pb::MergeJob> jobs;

@@ -114,8 +114,10 @@ def test_gathered_bytes_exact():
     plan, engs, _, base = run(model, ads, 4, toks, policy="interleave", sliced=1, chunk_bytes=32 << 10)
     host = base.numpy()
     w = [e.weights_bytes() for e in engs]
-    for r in range(1, 4):
-        assert np.array_equal(w[r], w[0])   # every rank holds the same merged model
+    for (name, rows, cols, host_off, layer, dev_off) in plan.tensors():   # every rank: same merged model
+        nb = rows * cols * 2
+        for r in range(1, 4):
+            assert np.array_equal(w[r][dev_off:dev_off + nb], w[0][dev_off:dev_off + nb]), (name, r)
     ow = oracle.OracleWeights(model, ads)
     adapted = {(at[6]) for at in plan.atensors()}
     for (name, rows, cols, host_off, layer, dev_off) in plan.tensors():
