@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--cpu-sample-layers", type=int, default=4)
+    ap.add_argument("--dist-backend", default="nccl", help="torch.distributed backend for barriers/handle exchange")
+    ap.add_argument("--same-gpu", action="store_true", help="all ranks on cuda:0 (testing the N>1 path on one GPU)")
     return ap.parse_args()
 
 
@@ -247,6 +249,15 @@ def measure_h2d(nbytes=1 << 30, chunk=64 << 20):
     return best
 
 
+def ncu_traffic(kernel_class):
+    """dram bytes (read + write) per launch of the kernel class, from the committed ncu --set full capture."""
+    p = os.path.join(HERE, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    return d.get(kernel_class)
+
+
 def load_peaks():
     p = os.path.join(HERE, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -273,25 +284,31 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {world}"
-    torch.cuda.set_device(local)
+    dev = 0 if args.same_gpu else local
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(args.dist_backend)
 
     def barrier():
         if world > 1:
             dist.barrier()
 
+    red_dev = "cuda" if args.dist_backend == "nccl" else "cpu"
+
     def allmax(x):
         if world == 1:
             return x
-        t = torch.tensor([float(x)], device="cuda", dtype=torch.float64)
+        t = torch.tensor([float(x)], device=red_dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.item()
 
     def allsum(x):
         if world == 1:
             return x
-        t = torch.tensor([float(x)], device="cuda", dtype=torch.float64)
+        t = torch.tensor([float(x)], device=red_dev, dtype=torch.float64)
         dist.all_reduce(t)
         return t.item()
 
@@ -329,8 +346,6 @@ def main():
         blobs = [None] * world
         dist.all_gather_object(blobs, eng.export())
         eng.wire_ipc(blobs)
-    if not args.no_profile:
-        B.pb_ctx_set_profiling(eng.ctx, 1)
     toks = synth.tokens(w.batch, w.seq, w.model.vocab)
 
     barrier()
@@ -350,7 +365,8 @@ def main():
         barrier()
         torch.cuda.synchronize()
         th0 = time.perf_counter()
-        res = eng.cold_start(step + 1, toks if rank == 0 else None, w.batch, w.seq, adapter_id=0 if w.adapters else -1)
+        res = eng.cold_start(2 * step + 1, toks if rank == 0 else None, w.batch, w.seq,
+                             adapter_id=0 if w.adapters else -1)
         th1 = time.perf_counter()
         barrier()
         torch.cuda.synchronize()
@@ -365,6 +381,15 @@ def main():
             load_done.append(allmax(tl["load_done_ms"]))
             launches += int(allsum(tl["n_launches"]))
             if not args.no_profile:
+                # Kernel timing: the same prefill kernels re-run on the now-resident weights, each bracketed by
+                # CUDA events on its launching stream. (Inside the cold start the PCIe link is saturated and a
+                # timing-event record costs ~20 us, which would swamp 5-50 us kernels.)
+                B.pb_ctx_set_profiling(eng.ctx, 1)
+                barrier()
+                eng.replay_enqueue(2 * step + 2, toks if rank == 0 else None, w.batch, w.seq)
+                eng.wait()
+                B.pb_ctx_set_profiling(eng.ctx, 0)
+                barrier()
                 for k, v in B.pb_kernel_stats(eng.ctx).items():
                     a = kstats.setdefault(k, {"launches": 0, "total_ms": 0.0, "flops": 0.0, "bytes": 0.0})
                     for f in a:
@@ -380,22 +405,26 @@ def main():
         for k, a in kstats.items():
             if a["launches"] == 0:
                 continue
-            bound = "tensor" if k in ("gemm",) else "hbm"
-            if bound == "tensor":
-                ach = a["flops"] / (a["total_ms"] * 1e-3) / 1e12
-                peak, unit = bf16_sus, "TFLOP/s"
+            t = a["total_ms"] * 1e-3
+            # binding resource = the larger of (flops / tensor peak) and (bytes / HBM peak)
+            tensor_bound = k in ("gemm",) and a["flops"] / (bf16_sus * 1e12) > a["bytes"] / (hbm * 1e9)
+            if tensor_bound:
+                ach, peak, unit = a["flops"] / t / 1e12, bf16_sus, "TFLOP/s"
             else:
-                ach = a["bytes"] / (a["total_ms"] * 1e-3) / 1e9
-                peak, unit = hbm, "GB/s"
+                ach, peak, unit = a["bytes"] / t / 1e9, hbm, "GB/s"
             kern[k] = {"launches": a["launches"] // max(1, args.steps), "avg_us": 1e3 * a["total_ms"] / a["launches"],
-                       "ms_per_step": a["total_ms"] / args.steps, "achieved": ach, "unit": unit, "frac": ach / peak}
+                       "ms_per_step": a["total_ms"] / args.steps, "achieved": ach, "unit": unit, "frac": ach / peak,
+                       "tflops": a["flops"] / t / 1e12, "gbs": a["bytes"] / t / 1e9}
         sm_kernels = {k: v for k, v in kern.items() if k != "signal"}
         if sm_kernels:
             dom = max(sm_kernels, key=lambda k: sm_kernels[k]["ms_per_step"])
             d = sm_kernels[dom]
             roof = {"kernel": dom, "bound": "tensor" if d["unit"] == "TFLOP/s" else "hbm", "achieved": d["achieved"],
                     "peak": bf16_sus if d["unit"] == "TFLOP/s" else hbm, "unit": d["unit"], "frac": d["frac"],
-                    "traffic": None, "peak_source": f"{peak_src} ({'sustained bf16' if d['unit'] == 'TFLOP/s' else 'HBM copy'})"}
+                    "traffic": ncu_traffic(dom),
+                    "peak_source": f"{peak_src} ({'sustained bf16' if d['unit'] == 'TFLOP/s' else 'HBM copy'})",
+                    "timing": "CUDA events per launch on the launching stream, warm re-run of the step's prefill "
+                              "(pb_prefill_replay) after each timed cold start"}
         t_pcie = S / (agg_h2d * 1e9) * 1e3
         line = {
             "metric": METRIC, "value": val, "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,

@@ -213,6 +213,12 @@ PB_API pb_status pb_prefill_wait(pb_ctx* ctx, float* logits_out, int32_t* tokens
 PB_API pb_status pb_prefill_first_token(pb_ctx* ctx, const int32_t* tokens, int32_t batch, int32_t seq,
                                  float* logits_out, int32_t* tokens_out);
 
+/* Warm re-run of the last trial's prefill on the now-resident merged weights (no load / merge / gather,
+ * no readiness waits on weights): the single-GPU-resident regime after T_full. Used by bench.py
+ * to time every prefill kernel with CUDA events away from the PCIe-saturated cold-start window. Every
+ * rank calls it with the same new epoch; complete it with pb_prefill_wait. */
+PB_API pb_status pb_prefill_replay(pb_ctx* ctx, uint32_t epoch, const int32_t* tokens, int32_t batch, int32_t seq);
+
 /* Block until every stream of this rank is idle; surfaces async CUDA errors. */
 PB_API pb_status pb_sync(pb_ctx* ctx);
 

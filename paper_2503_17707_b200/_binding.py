@@ -101,6 +101,7 @@ _SIGS = {
     "pb_gather_layers": [_P],
     "pb_prefill_enqueue": [_P, _P, C.c_int32, C.c_int32],
     "pb_prefill_wait": [_P, _P, _P],
+    "pb_prefill_replay": [_P, C.c_uint32, _P, C.c_int32, C.c_int32],
     "pb_prefill_first_token": [_P, _P, C.c_int32, C.c_int32, _P, _P],
     "pb_sync": [_P],
     "pb_timeline": [_P, C.POINTER(pb_timeline_t)],
@@ -113,6 +114,8 @@ _SIGS = {
     "pb_op_merge": [_P, C.c_int64, C.c_int32, C.c_int32, _P, _P, C.c_int32, C.c_float, _P],
     "pb_op_gemm": [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int32, C.c_int32, C.c_int32, _P,
                    C.c_int32, C.c_float, C.c_int32, _P, C.c_int32, _P],
+    "pb_op_gemm_split": [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int32, C.c_int32, C.c_int32, _P,
+                         C.c_int32, C.c_float, C.c_int32, _P, C.c_int32, C.c_int32, _P],
     "pb_op_norm": [_P, C.c_int32, C.c_int32, _P, _P, C.c_float, _P, _P],
     "pb_op_attention": [_P, C.c_int32, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                         C.c_int32, C.c_int32, C.c_int32, C.c_float, _P],
@@ -257,6 +260,10 @@ def pb_prefill_enqueue(ctx, tokens_ptr, batch, seq):
     check(lib().pb_prefill_enqueue(ctx, tokens_ptr, batch, seq))
 
 
+def pb_prefill_replay(ctx, epoch, tokens_ptr, batch, seq):
+    check(lib().pb_prefill_replay(ctx, epoch, tokens_ptr, batch, seq))
+
+
 def pb_prefill_wait(ctx, logits_ptr, tokens_ptr):
     check(lib().pb_prefill_wait(ctx, logits_ptr, tokens_ptr))
 
@@ -313,6 +320,12 @@ def pb_op_merge(W, ldw, rows, cols, B, A, rank, scale, stream=0):
 def pb_op_gemm(X, x_rows, m_begin, m_end, K, W, n_rows, N, epi, bias, relu, scale, scale_cols, out, ldo, stream=0):
     check(lib().pb_op_gemm(X, x_rows, m_begin, m_end, K, W, n_rows, N, epi, bias, relu, scale, scale_cols, out, ldo,
                            stream))
+
+
+def pb_op_gemm_split(X, x_rows, m_begin, m_end, K, W, n_rows, N, epi, bias, relu, scale, scale_cols, out, ldo,
+                     split_k, stream=0):
+    check(lib().pb_op_gemm_split(X, x_rows, m_begin, m_end, K, W, n_rows, N, epi, bias, relu, scale, scale_cols, out,
+                                 ldo, split_k, stream))
 
 
 def pb_op_norm(h, rows, d, gamma, beta, eps, out, stream=0):

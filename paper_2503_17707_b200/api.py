@@ -163,6 +163,16 @@ class RankEngine:
         self.enqueue(epoch, tokens, batch, seq, adapter_id)
         return self.wait(want_logits)
 
+    def replay_enqueue(self, epoch: int, tokens: Optional[np.ndarray], batch: int, seq: int):
+        """Warm prefill re-run on the resident weights (pb_prefill_replay); complete with wait()."""
+        self._batch = batch
+        with torch.cuda.device(self.device):
+            tp = None
+            if tokens is not None:
+                self._tok = np.ascontiguousarray(tokens, dtype=np.int32)
+                tp = self._tok.ctypes.data
+            B.pb_prefill_replay(self.ctx, epoch, tp, batch, seq)
+
     def timeline(self) -> dict:
         t = B.pb_timeline(self.ctx)
         n = t.n_chunks

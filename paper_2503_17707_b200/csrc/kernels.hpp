@@ -54,7 +54,9 @@ struct GemmArgs {
     void* out;                  // bf16 [*, ldo] or fp32 [*, ldo]
     int ldo;
     int up_row0;                // EPI_SILU_MUL: first row of `up` in W (= N_out)
+    int split_k;                // 0 = automatic (gemm_split_k), else the cluster split-K factor (1..8)
 };
+int gemm_split_k(int N, int K, int epi);
 // Maps: X box {64, 128} SW128 over [max_rows x K]; W box {64, 128} (EPI_SILU_MUL: {64, 64}) SW128 over [rows x K].
 cudaError_t launch_gemm(const CUtensorMap& mapX, const CUtensorMap& mapW, const GemmArgs& a, cudaStream_t s);
 

@@ -290,21 +290,38 @@ extern "C" pb_status pb_ctx_create(const pb_plan* plan, int32_t rank, const void
     c->tensor_ready.assign(NT, nullptr);
     c->tl_landed.assign(NC, -1.0);
     c->tl_gathered.assign(NC, -1.0);
+    // Timing events only where the timeline needs a timestamp; dependency events are created with
+    // cudaEventDisableTiming (measured on B200: a timing-event record costs ~20 us while the PCIe link
+    // is saturated by the load).
     auto mk = [&](cudaEvent_t* e) { return cudaEventCreate(e); };
-    if (mk(&c->t0) || mk(&c->merge_done) || mk(&c->gather_done) || mk(&c->done))
+    auto mk_dep = [&](cudaEvent_t* e) { return cudaEventCreateWithFlags(e, cudaEventDisableTiming); };
+    if (mk(&c->t0) || mk(&c->merge_done) || mk(&c->gather_done) || mk(&c->done) || mk(&c->ready_merge) ||
+        mk(&c->ready_recv))
         return cleanup(fail(PB_ECUDA, "cudaEventCreate failed"));
     for (int32_t id : plan->load[rank])
         if (mk(&c->landed[id])) return cleanup(fail(PB_ECUDA, "cudaEventCreate failed"));
     for (int32_t id : plan->recv[rank])
         if (mk(&c->gathered[id])) return cleanup(fail(PB_ECUDA, "cudaEventCreate failed"));
     for (size_t t = 0; t < NT; ++t)
-        if (mk(&c->tensor_ready[t])) return cleanup(fail(PB_ECUDA, "cudaEventCreate failed"));
+        if (mk_dep(&c->tensor_ready[t])) return cleanup(fail(PB_ECUDA, "cudaEventCreate failed"));
     // per-tensor last own / received chunk
     c->last_own_chunk.assign(NT, -1);
     c->last_recv_chunk.assign(NT, -1);
     for (int32_t id : plan->load[rank])
         if (!plan->chunks[id].is_adapter) c->last_own_chunk[plan->chunks[id].tensor] = id;
     for (int32_t id : plan->recv[rank]) c->last_recv_chunk[plan->chunks[id].tensor] = id;
+    {
+        const auto st = plan->stages[rank];
+        auto in_stage = [&](int32_t id) {
+            const auto& ch = plan->chunks[id];
+            const int32_t l = ch.is_adapter ? -1 : plan->tensors[ch.tensor].layer;
+            return l >= st.first && l < st.second;
+        };
+        for (int32_t id : plan->load[rank])
+            if (in_stage(id)) c->last_own_stage_chunk = id;
+        for (int32_t id : plan->recv[rank])
+            if (in_stage(id)) c->last_recv_stage_chunk = id;
+    }
 
     build_copy_groups(c);
     pb_status st = build_merge_jobs(c);
@@ -327,7 +344,7 @@ extern "C" void pb_ctx_free(pb_ctx* c) {
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     auto d = [](cudaEvent_t e) { if (e) cudaEventDestroy(e); };
-    d(c->t0); d(c->merge_done); d(c->gather_done); d(c->done);
+    d(c->t0); d(c->merge_done); d(c->gather_done); d(c->done); d(c->ready_merge); d(c->ready_recv);
     for (auto e : c->landed) d(e);
     for (auto e : c->gathered) d(e);
     for (auto e : c->tensor_ready) d(e);
@@ -581,6 +598,7 @@ extern "C" pb_status pb_merge_lora(pb_ctx* c, int32_t adapter_id) {
         }
         if (!others.empty()) CU(signal_ranks(c, c->L.f_chunk + id, others, c->merge));
         if (c->last_own_chunk[ch.tensor] == id) CU(cudaEventRecord(c->tensor_ready[ch.tensor], c->merge));
+        if (id == c->last_own_stage_chunk) CU(cudaEventRecord(c->ready_merge, c->merge));
     }
     CU(cudaEventRecord(c->merge_done, c->merge));
     c->phase = Phase::Merged;
@@ -600,6 +618,7 @@ extern "C" pb_status pb_gather_layers(pb_ctx* c) {
         CU(cudaEventRecord(c->gathered[id], c->nv));
         c->recv_bytes += ch.bytes;
         if (c->last_recv_chunk[ch.tensor] == id) CU(cudaEventRecord(c->tensor_ready[ch.tensor], c->nv));
+        if (id == c->last_recv_stage_chunk) CU(cudaEventRecord(c->ready_recv, c->nv));
     }
     CU(cudaEventRecord(c->gather_done, c->nv));
     c->phase = Phase::Gathered;
@@ -618,13 +637,6 @@ const __nv_bfloat16* wt(pb_ctx* c, int l, const char* sfx) {
     return t < 0 ? nullptr : reinterpret_cast<const __nv_bfloat16*>(c->weights + p->tensors[t].dev_off);
 }
 
-cudaEvent_t layer_ready(pb_ctx* c, int l) {
-    const pb_plan* p = c->plan;
-    int32_t last = -1;
-    for (size_t t = 0; t < p->tensors.size(); ++t)
-        if (p->tensors[t].layer == l) last = (int32_t)t;
-    return c->tensor_ready[last];
-}
 
 cudaError_t wait_tensor(pb_ctx* c, int l, const char* sfx) {
     const pb_plan* p = c->plan;
@@ -731,10 +743,30 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, boo
 
 }  // namespace
 
+static pb_status enqueue_prefill(pb_ctx* c, const int32_t* tokens, int32_t B, int32_t T, bool replay);
+
 extern "C" pb_status pb_prefill_enqueue(pb_ctx* c, const int32_t* tokens, int32_t B, int32_t T) {
     pb_status st = check_ctx(c, "pb_prefill_enqueue");
     if (st) return st;
     if (c->phase != Phase::Gathered) return fail(PB_EPROTOCOL, "pb_prefill_enqueue: call pb_gather_layers first");
+    return enqueue_prefill(c, tokens, B, T, false);
+}
+
+extern "C" pb_status pb_prefill_replay(pb_ctx* c, uint32_t epoch, const int32_t* tokens, int32_t B, int32_t T) {
+    pb_status st = check_ctx(c, "pb_prefill_replay");
+    if (st) return st;
+    if (c->phase != Phase::Prefilled) return fail(PB_EPROTOCOL, "pb_prefill_replay: needs a completed cold start");
+    if (epoch <= c->epoch) return fail(PB_EINVAL, "epoch %u must exceed the previous %u", epoch, c->epoch);
+    CU(cudaStreamSynchronize(c->comp));
+    c->epoch = epoch;
+    c->n_launches = 0;
+    c->prof_n = 0;
+    CU(cudaEventRecord(c->t0, c->comp));
+    return enqueue_prefill(c, tokens, B, T, true);
+}
+
+static pb_status enqueue_prefill(pb_ctx* c, const int32_t* tokens, int32_t B, int32_t T, bool replay) {
+    pb_status st = PB_OK;
     if (B < 1 || T < 1 || B > c->L.max_batch || T > c->L.max_seq || (int64_t)B * T > c->L.max_rows)
         return fail(PB_EINVAL, "batch %d x seq %d exceeds the workspace (%d x %d)", B, T, c->L.max_batch, c->L.max_seq);
     if (c->rank == 0 && !tokens) return fail(PB_EINVAL, "rank 0 needs tokens");
@@ -767,7 +799,7 @@ extern "C" pb_status pb_prefill_enqueue(pb_ctx* c, const int32_t* tokens, int32_
     for (int j = 0; j < k; ++j) {
         const int r0 = tb[j] * B, r1 = tb[j + 1] * B;
         if (g == 0) {
-            if (j == 0) {
+            if (j == 0 && !replay) {
                 // embedding rows may live on every rank (vocab slices): wait for each piece
                 const int32_t et = p->find_tensor("embed");
                 for (auto& ch : p->chunks) {
@@ -805,7 +837,7 @@ extern "C" pb_status pb_prefill_enqueue(pb_ctx* c, const int32_t* tokens, int32_
             CU(wait_word(c, L.f_act + j, s));
         }
         for (int l = stage.first; l < stage.second; ++l) {
-            st = run_layer(c, l, r0, r1, tb[j], tb[j + 1], B, j == 0);
+            st = run_layer(c, l, r0, r1, tb[j], tb[j + 1], B, j == 0 && !replay);
             if (st) return st;
         }
         if (g < N - 1) {
@@ -820,8 +852,10 @@ extern "C" pb_status pb_prefill_enqueue(pb_ctx* c, const int32_t* tokens, int32_
     for (int r = 0; r < N; ++r)
         if (is_head_owner(p, r)) owners.push_back(r);
     if (g == N - 1) {
-        CU(cudaStreamWaitEvent(s, c->tensor_ready[p->find_tensor("final_g")], 0));
-        if (opt) CU(cudaStreamWaitEvent(s, c->tensor_ready[p->find_tensor("final_b")], 0));
+        if (!replay) {
+            CU(cudaStreamWaitEvent(s, c->tensor_ready[p->find_tensor("final_g")], 0));
+            if (opt) CU(cudaStreamWaitEvent(s, c->tensor_ready[p->find_tensor("final_b")], 0));
+        }
         const int pi = prof_begin(c, K_NORM, s);
         CU(launch_norm(h + (size_t)(T - 1) * B * d, d, y, d, B, d, wt(c, -1, "final_g"), opt ? wt(c, -1, "final_b") : nullptr,
                        m.norm_eps, s));
@@ -840,7 +874,7 @@ extern "C" pb_status pb_prefill_enqueue(pb_ctx* c, const int32_t* tokens, int32_
     if (is_head_owner(p, g)) {
         if (g != N - 1) CU(wait_word(c, L.f_y, s));
         const int32_t ht = head_tensor(p);
-        CU(cudaStreamWaitEvent(s, c->tensor_ready[ht], 0));
+        if (!replay) CU(cudaStreamWaitEvent(s, c->tensor_ready[ht], 0));
         int32_t v0, v1;
         head_slice(p, g, &v0, &v1);
         const __nv_bfloat16* E = reinterpret_cast<const __nv_bfloat16*>(c->weights + p->tensors[ht].dev_off);
@@ -921,7 +955,8 @@ extern "C" pb_status pb_timeline(pb_ctx* c, pb_timeline_t* out) {
     }
     for (int32_t id : p->recv[c->rank]) c->tl_gathered[id] = ms(c->gathered[id]);
     double ready = 0;
-    for (int l = p->stages[c->rank].first; l < p->stages[c->rank].second; ++l) ready = std::max(ready, ms(layer_ready(c, l)));
+    if (c->last_own_stage_chunk >= 0) ready = std::max(ready, ms(c->ready_merge));
+    if (c->last_recv_stage_chunk >= 0) ready = std::max(ready, ms(c->ready_recv));
     out->t_ready_ms = ready;
     out->t_full_ms = std::max(ms(c->merge_done), ms(c->gather_done));
     out->ttft_ms = c->phase == Phase::Prefilled ? ms(c->done) : -1;

@@ -79,6 +79,8 @@ struct pb_ctx {
 
     // events
     cudaEvent_t t0 = nullptr, merge_done = nullptr, gather_done = nullptr, done = nullptr;
+    cudaEvent_t ready_merge = nullptr, ready_recv = nullptr;   // timing: last stage chunk merged / received
+    int32_t last_own_stage_chunk = -1, last_recv_stage_chunk = -1;
     std::vector<cudaEvent_t> landed, gathered, tensor_ready;
     std::vector<char> tensor_own;        // this rank loads every piece of the tensor
     std::vector<int32_t> last_own_chunk; // per base tensor: last own chunk in load order (-1 if none)

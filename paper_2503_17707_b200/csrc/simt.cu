@@ -135,7 +135,7 @@ __global__ void rope_kernel(__nv_bfloat16* qkv, int ld, int r0, int B, int n_q, 
 // CTA = (32 query positions, head, sequence); 8 warps x 4 queries. Keys/values streamed through shared
 // memory 32 at a time (K transposed for conflict-free lane-per-key dot products); online softmax in fp32.
 template <int HD>
-__global__ void __launch_bounds__(256) attention_kernel(const __nv_bfloat16* __restrict__ qkv, int ld,
+__global__ void __launch_bounds__(256, 2) attention_kernel(const __nv_bfloat16* __restrict__ qkv, int ld,
                                                         __nv_bfloat16* __restrict__ out, int ldo, int t0, int t1,
                                                         int B, int group, int k_col0, int v_col0,
                                                         float score_scale) {
@@ -163,6 +163,7 @@ __global__ void __launch_bounds__(256) attention_kernel(const __nv_bfloat16* __r
         for (int e = 0; e < DPL; ++e) acc[i][e] = 0.f;
     }
     const int n_keys = q_hi;   // keys [0, q_hi) cover every query in the tile
+    const int qw0 = q0 + warp * 4;   // this warp's 4 queries (independent FMA chains -> ILP)
     for (int k0 = 0; k0 < n_keys; k0 += KT) {
         __syncthreads();
         for (int i = threadIdx.x; i < KT * HD; i += 256) {
@@ -178,30 +179,43 @@ __global__ void __launch_bounds__(256) attention_kernel(const __nv_bfloat16* __r
             sV[kj][c] = vv;
         }
         __syncthreads();
+        if (qw0 >= q_hi || k0 > qw0 + 3) continue;   // warp-uniform: no live query or keys all in the future
+        const int key = k0 + lane;
+        float sc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 8
+        for (int c = 0; c < HD; ++c) {
+            const float kt = sKt[c][lane];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) sc[i] = fmaf(sQ[warp * 4 + i][c], kt, sc[i]);
+        }
+        float p[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const int qi = warp * 4 + i;
-            const int t = q0 + qi;
-            if (t >= q_hi) continue;
-            const int key = k0 + lane;
-            float s = 0.f;
-#pragma unroll 16
-            for (int c = 0; c < HD; ++c) s = fmaf(sQ[qi][c], sKt[c][lane], s);
-            if (key > t) s = -CUDART_INF_F;
-            const float mx = warp_max(s);
+            const int t = qw0 + i;
+            float sv = (key > t || t >= q_hi) ? -CUDART_INF_F : sc[i];
+            const float mx = warp_max(sv);
             const float m_new = fmaxf(m[i], mx);
-            if (m_new == -CUDART_INF_F) continue;   // whole tile masked for this query
-            const float p = __expf(s - m_new);
+            if (m_new == -CUDART_INF_F) {   // nothing visible yet for this query
+                p[i] = 0.f;
+                continue;
+            }
+            p[i] = __expf(sv - m_new);
             const float corr = __expf(m[i] - m_new);
-            l[i] = l[i] * corr + warp_sum(p);
+            l[i] = l[i] * corr + warp_sum(p[i]);
             m[i] = m_new;
 #pragma unroll
             for (int e = 0; e < DPL; ++e) acc[i][e] *= corr;
-#pragma unroll 8
-            for (int j = 0; j < KT; ++j) {
-                const float pj = __shfl_sync(0xffffffffu, p, j);
+        }
+#pragma unroll 4
+        for (int j = 0; j < KT; ++j) {
+            float vj[DPL];
 #pragma unroll
-                for (int e = 0; e < DPL; ++e) acc[i][e] = fmaf(pj, sV[j][lane + 32 * e], acc[i][e]);
+            for (int e = 0; e < DPL; ++e) vj[e] = sV[j][lane + 32 * e];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float pj = __shfl_sync(0xffffffffu, p[i], j);
+#pragma unroll
+                for (int e = 0; e < DPL; ++e) acc[i][e] = fmaf(pj, vj[e], acc[i][e]);
             }
         }
     }

@@ -170,3 +170,16 @@ def test_c2_full_size_single_gpu():
     plan, engs, (tokens, logits), _ = run(w.model, w.adapters, 1, toks, chunk_bytes=32 << 20)
     rel = check_against_oracle(w.model, w.adapters, toks, logits, tokens)
     print("C2 rel err", rel)
+
+
+def test_replay_bitwise_equals_cold_start():
+    """pb_prefill_replay (warm re-run on resident weights) reproduces the cold start's logits exactly,
+    single and multi-rank."""
+    need_gpu()
+    for n in (1, 2):
+        toks = synth.tokens(1, 16, TINY_OPT.vocab)
+        plan, engs, (t1, l1), _ = run(TINY_OPT, (lora(8),), n, toks, policy="interleave", sliced=1, k=2)
+        for e in engs:
+            e.replay_enqueue(2, toks if e.rank == 0 else None, 1, 16)
+        res = [e.wait(want_logits=True) for e in engs]
+        assert np.array_equal(res[0][1].view(np.uint32), l1.view(np.uint32)) and np.array_equal(res[0][0], t1)
