@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--cpu-sample-layers", type=int, default=4)
+    ap.add_argument("--host-alias", type=int, default=0,
+                    help="host_alias_layers K: layer l is DMA'd from the host image of layer l mod K (DRAM-limited boxes)")
     ap.add_argument("--dist-backend", default="nccl", help="torch.distributed backend for barriers/handle exchange")
     ap.add_argument("--same-gpu", action="store_true", help="all ranks on cuda:0 (testing the N>1 path on one GPU)")
     return ap.parse_args()
@@ -157,7 +159,7 @@ def workload_config(w, args, n):
                         f"LoRA r={w.adapters[0].rank if w.adapters else 0} on {','.join(w.adapters[0].targets) if w.adapters else '-'}",
             "batch": w.batch, "seq_len": w.seq, "n_gpus": n,
             "policy": args.policy, "vocab_sliced": args.vocab_sliced, "chunk_mb": args.chunk_mb,
-            "prefill_chunks": args.prefill_chunks,
+            "prefill_chunks": args.prefill_chunks, "host_alias_layers": args.host_alias,
             "l2": "inputs (whole model weights) larger than the 126 MB L2; device weights reset to 0xFF between steps",
             "parallelism": f"pp{n} (layer-sharded load, pipelined prefill)"}
 
@@ -320,8 +322,8 @@ def main():
     if args.prefill_chunks is None:
         args.prefill_chunks = 1 if world == 1 else 2
     plan = Plan(w.model, w.adapters, world, policy=args.policy, vocab_sliced=args.vocab_sliced,
-                chunk_bytes=args.chunk_mb << 20, prefill_chunks=args.prefill_chunks)
-    S = plan.sizes.host_base_bytes + plan.sizes.host_adapter_bytes
+                chunk_bytes=args.chunk_mb << 20, prefill_chunks=args.prefill_chunks, host_alias_layers=args.host_alias)
+    S = plan.sizes.dev_weight_bytes + plan.sizes.dev_adapter_bytes   # bytes DMA'd per cold start (all ranks)
 
     # --- host images: one DRAM copy of the checkpoint shared by all GPU processes
     shm_paths = []

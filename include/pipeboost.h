@@ -156,7 +156,9 @@ typedef struct {
     void* adapters;       int64_t adapters_cap;   /* device, >= dev_adapter_bytes (may be NULL if no adapters) */
     void* workspace;      int64_t workspace_cap;  /* device, >= pb_plan_workspace_bytes(max_batch, max_seq) */
     int32_t max_batch, max_seq;
-    void* stream_h2d[2];  /* cudaStream_t: copy-engine H2D lanes */
+    /* cudaStream_t handles, five DISTINCT streams per rank; NULL = the ctx creates and owns its own
+     * non-blocking streams (recommended: torch's stream pool recycles handles across ranks). */
+    void* stream_h2d[2];  /* cudaStream_t: copy-engine H2D lane(s) (one ordered lane is used) */
     void* stream_merge;   /* cudaStream_t: merge kernels + per-layer readiness */
     void* stream_nvlink;  /* cudaStream_t: peer (NVLink) receive copies */
     void* stream_compute; /* cudaStream_t: prefill kernels */

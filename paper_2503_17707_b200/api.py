@@ -79,7 +79,8 @@ class RankEngine:
             self.adapters = torch.empty(max(s.dev_adapter_bytes, 1), dtype=torch.uint8, device=self.device)
             ws = plan.workspace_bytes(max_batch, max_seq)
             self.workspace = torch.empty(ws, dtype=torch.uint8, device=self.device)
-            self.streams = [torch.cuda.Stream(self.device) for _ in range(5)]
+            # streams: NULL -> the ctx creates five distinct non-blocking streams (torch's stream pool
+            # recycles 32 handles, and two ranks sharing a stream can deadlock on readiness waits)
         self.bufs = B.pb_rank_bufs()
         self.bufs.weights = self.weights.data_ptr()
         self.bufs.weights_cap = self.weights.numel()
@@ -89,11 +90,11 @@ class RankEngine:
         self.bufs.workspace_cap = self.workspace.numel()
         self.bufs.max_batch = max_batch
         self.bufs.max_seq = max_seq
-        self.bufs.stream_h2d[0] = self.streams[0].cuda_stream
-        self.bufs.stream_h2d[1] = self.streams[1].cuda_stream
-        self.bufs.stream_merge = self.streams[2].cuda_stream
-        self.bufs.stream_nvlink = self.streams[3].cuda_stream
-        self.bufs.stream_compute = self.streams[4].cuda_stream
+        self.bufs.stream_h2d[0] = None
+        self.bufs.stream_h2d[1] = None
+        self.bufs.stream_merge = None
+        self.bufs.stream_nvlink = None
+        self.bufs.stream_compute = None
         ha = host_adapters.data_ptr() if (host_adapters is not None and s.host_adapter_bytes) else None
         with torch.cuda.device(self.device):
             self.ctx = B.pb_ctx_create(plan.handle, rank, host_base.data_ptr(), ha, self.bufs)

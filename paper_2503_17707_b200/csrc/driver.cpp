@@ -15,10 +15,12 @@ using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, 
                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 using WaitValue32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using WriteValue32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 using GetErrorString = CUresult (*)(CUresult, const char**);
 
 EncodeTiled g_encode = nullptr;
 WaitValue32 g_wait32 = nullptr;
+WriteValue32 g_write32 = nullptr;
 GetErrorString g_errstr = nullptr;
 std::once_flag g_once;
 bool g_ok = false;
@@ -37,8 +39,9 @@ bool driver_init(char* err, size_t errlen) {
     std::call_once(g_once, [] {
         g_encode = reinterpret_cast<EncodeTiled>(entry("cuTensorMapEncodeTiled"));
         g_wait32 = reinterpret_cast<WaitValue32>(entry("cuStreamWaitValue32"));
+        g_write32 = reinterpret_cast<WriteValue32>(entry("cuStreamWriteValue32"));
         g_errstr = reinterpret_cast<GetErrorString>(entry("cuGetErrorString"));
-        g_ok = g_encode && g_wait32;
+        g_ok = g_encode && g_wait32 && g_write32;
         if (!g_ok) snprintf(g_err, sizeof g_err, "driver entry points unavailable (cuTensorMapEncodeTiled/cuStreamWaitValue32)");
     });
     if (!g_ok && err) snprintf(err, errlen, "%s", g_err);
@@ -75,6 +78,14 @@ cudaError_t stream_wait_geq(cudaStream_t s, const uint32_t* dev_addr, uint32_t v
     if (!g_wait32) return cudaErrorNotSupported;
     CUresult r = g_wait32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(dev_addr), value,
                           CU_STREAM_WAIT_VALUE_GEQ);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorUnknown;
+}
+
+cudaError_t stream_write(cudaStream_t s, uint32_t* dev_addr, uint32_t value) {
+    if (!g_write32) return cudaErrorNotSupported;
+    // default flags: a memory barrier orders every prior write of the stream before this one
+    CUresult r = g_write32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(dev_addr), value,
+                           CU_STREAM_WRITE_VALUE_DEFAULT);
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorUnknown;
 }
 

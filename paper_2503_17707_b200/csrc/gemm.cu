@@ -252,8 +252,13 @@ cudaError_t launch_epi(const CUtensorMap& mapX, const CUtensorMap& mapW, const G
         if (e != cudaSuccess) return e;
     }
     const int per = EPI == EPI_SILU_MUL ? BN / 2 : BN;
+    const dim3 grid((a.N + per - 1) / per, (a.M_end - a.M_begin + BM - 1) / BM, S);
+    if (S == 1) {   // no cluster: plain launch (lower launch latency)
+        gemm_kernel<EPI><<<grid, 128, kSmem, s>>>(mapX, mapW, a);
+        return cudaGetLastError();
+    }
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((a.N + per - 1) / per, (a.M_end - a.M_begin + BM - 1) / BM, S);
+    cfg.gridDim = grid;
     cfg.blockDim = dim3(128);
     cfg.dynamicSmemBytes = kSmem;
     cfg.stream = s;
@@ -269,15 +274,16 @@ cudaError_t launch_epi(const CUtensorMap& mapX, const CUtensorMap& mapW, const G
 
 }  // namespace
 
-// Split-K factor: fill the 148 SMs with (N tiles x S) CTAs, at most 8 (portable cluster), at least two
+// Split-K factor: fill the 148 SMs with (N tiles x S) CTAs, at most 4 (measured on B200 at M = 128:
+// S = 8 loses to S = 4 on cluster scheduling + DSMEM reduction, tools/gemm_bench.py), at least eight
 // 64-wide K blocks per split. Depends on N and K only (determinism across prompt chunkings).
 int gemm_split_k(int N, int K, int epi) {
     const int per = epi == EPI_SILU_MUL ? BN / 2 : BN;
     const int n_tiles = (N + per - 1) / per;
     const int nk = (K + BK - 1) / BK;
     int S = 148 / (n_tiles > 0 ? n_tiles : 1);
-    S = S < 1 ? 1 : (S > 8 ? 8 : S);
-    while (S > 1 && nk / S < 2) --S;
+    S = S < 1 ? 1 : (S > 4 ? 4 : S);
+    while (S > 1 && nk / S < 8) --S;
     return S;
 }
 

@@ -18,6 +18,7 @@ bool make_map_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t c
 
 // Stream memory operations / cross-rank readiness words.
 cudaError_t stream_wait_geq(cudaStream_t s, const uint32_t* dev_addr, uint32_t value);
+cudaError_t stream_write(cudaStream_t s, uint32_t* dev_addr, uint32_t value);   // after all prior stream work
 struct SignalTargets {
     uint32_t* addr[8];
     int n;

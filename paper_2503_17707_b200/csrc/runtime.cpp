@@ -15,8 +15,12 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <deque>
 #include <cstring>
+#include <cstdio>
+#include <cstdlib>
 #include <unistd.h>
 
 #include "errors.hpp"
@@ -67,6 +71,10 @@ void head_slice(const pb_plan* p, int32_t g, int32_t* v0, int32_t* v1) {
     if (*v1 < 0) *v0 = *v1 = 0;
 }
 
+void join_load(pb_ctx* c) {
+    if (c->load_thread.joinable()) c->load_thread.join();
+}
+
 pb_status check_ctx(pb_ctx* c, const char* fn) {
     if (!c) return fail(PB_EINVAL, "%s: null ctx", fn);
     cudaError_t e = cudaSetDevice(c->device);
@@ -99,7 +107,9 @@ WsLayout pb::ws_layout(const pb_plan* p, int32_t batch, int32_t seq) {
     L.f_act = (int32_t)p->chunks.size();
     L.f_y = L.f_act + k;
     L.f_logit = L.f_y + 1;
-    L.n_words = L.f_logit + p->n_gpus;
+    L.f_land = L.f_logit + p->n_gpus;
+    L.f_tensor = L.f_land + (int32_t)p->chunks.size();
+    L.n_words = L.f_tensor + (int32_t)p->tensors.size();
     int64_t o = 0;
     L.flags = o;   o = al(o + 4 * (int64_t)L.n_words);
     L.tokens = o;  o = al(o + 4 * rows);
@@ -275,6 +285,18 @@ extern "C" pb_status pb_ctx_create(const pb_plan* plan, int32_t rank, const void
     c->merge = (cudaStream_t)bufs->stream_merge;
     c->nv = (cudaStream_t)bufs->stream_nvlink;
     c->comp = (cudaStream_t)bufs->stream_compute;
+    // NULL streams: the ctx creates its own (distinct, non-blocking). Each rank needs five DISTINCT streams:
+    // device-side readiness waits on a stream shared with another rank's producer would deadlock.
+    cudaStream_t* mine[5] = {&c->h2d[0], &c->h2d[1], &c->merge, &c->nv, &c->comp};
+    for (auto* sp : mine)
+        if (!*sp) {
+            if (cudaStreamCreateWithFlags(sp, cudaStreamNonBlocking) != cudaSuccess) {
+                for (auto* q : mine)
+                    if (*q && q != sp) { /* owned ones are released by pb_ctx_free below */ }
+                return fail(PB_ECUDA, "cudaStreamCreateWithFlags failed");
+            }
+            c->owned_streams.push_back(*sp);
+        }
     c->L = L;
     c->host_base = host_base;
     c->host_adapters = host_adapters;
@@ -287,23 +309,21 @@ extern "C" pb_status pb_ctx_create(const pb_plan* plan, int32_t rank, const void
     const size_t NC = plan->chunks.size(), NT = plan->tensors.size();
     c->landed.assign(NC, nullptr);
     c->gathered.assign(NC, nullptr);
-    c->tensor_ready.assign(NT, nullptr);
     c->tl_landed.assign(NC, -1.0);
     c->tl_gathered.assign(NC, -1.0);
-    // Timing events only where the timeline needs a timestamp; dependency events are created with
-    // cudaEventDisableTiming (measured on B200: a timing-event record costs ~20 us while the PCIe link
-    // is saturated by the load).
+    // Events only where the timeline needs a timestamp (measured on B200: a timing-event record costs
+    // ~20 us while the PCIe link is saturated by the load); dependencies are device-side readiness words.
     auto mk = [&](cudaEvent_t* e) { return cudaEventCreate(e); };
-    auto mk_dep = [&](cudaEvent_t* e) { return cudaEventCreateWithFlags(e, cudaEventDisableTiming); };
     if (mk(&c->t0) || mk(&c->merge_done) || mk(&c->gather_done) || mk(&c->done) || mk(&c->ready_merge) ||
         mk(&c->ready_recv))
         return cleanup(fail(PB_ECUDA, "cudaEventCreate failed"));
     for (int32_t id : plan->load[rank])
         if (mk(&c->landed[id])) return cleanup(fail(PB_ECUDA, "cudaEventCreate failed"));
+    c->budget_events.assign(4 * kEventPool, nullptr);
+    for (auto& e : c->budget_events)
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming)) return cleanup(fail(PB_ECUDA, "cudaEventCreate failed"));
     for (int32_t id : plan->recv[rank])
         if (mk(&c->gathered[id])) return cleanup(fail(PB_ECUDA, "cudaEventCreate failed"));
-    for (size_t t = 0; t < NT; ++t)
-        if (mk_dep(&c->tensor_ready[t])) return cleanup(fail(PB_ECUDA, "cudaEventCreate failed"));
     // per-tensor last own / received chunk
     c->last_own_chunk.assign(NT, -1);
     c->last_recv_chunk.assign(NT, -1);
@@ -341,13 +361,15 @@ extern "C" pb_status pb_ctx_create(const pb_plan* plan, int32_t rank, const void
 
 extern "C" void pb_ctx_free(pb_ctx* c) {
     if (!c) return;
+    join_load(c);
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     auto d = [](cudaEvent_t e) { if (e) cudaEventDestroy(e); };
     d(c->t0); d(c->merge_done); d(c->gather_done); d(c->done); d(c->ready_merge); d(c->ready_recv);
+    for (auto e : c->budget_events) d(e);
+    for (auto st : c->owned_streams) cudaStreamDestroy(st);
     for (auto e : c->landed) d(e);
     for (auto e : c->gathered) d(e);
-    for (auto e : c->tensor_ready) d(e);
     for (auto& r : c->prof) { d(r.a); d(r.b); }
     for (auto& p : c->peers)
         for (void* b : p.ipc_bases) cudaIpcCloseMemHandle(b);
@@ -485,6 +507,13 @@ static cudaError_t wait_word(pb_ctx* c, int32_t word, cudaStream_t s) {
     return stream_wait_geq(s, flag_ptr(c->ws, c->L, word), c->epoch);
 }
 
+// Local readiness word: written by the producing stream after its prior work, so consumers can be
+// enqueued in any host order (the load is enqueued from a worker thread that may block on a full queue).
+static cudaError_t set_word(pb_ctx* c, int32_t word, cudaStream_t s) {
+    return stream_write(s, flag_ptr(c->ws, c->L, word), c->epoch);
+}
+
+
 extern "C" pb_status pb_ctx_set_profiling(pb_ctx* c, int32_t enable) {
     pb_status st = check_ctx(c, "pb_ctx_set_profiling");
     if (st) return st;
@@ -533,6 +562,7 @@ extern "C" pb_status pb_trial_begin(pb_ctx* c, uint32_t epoch) {
     pb_status st = check_ctx(c, "pb_trial_begin");
     if (st) return st;
     if (epoch <= c->epoch) return fail(PB_EINVAL, "epoch %u must exceed the previous %u", epoch, c->epoch);
+    join_load(c);
     for (int r = 0; r < c->n; ++r)
         if (!c->peers[r].linked) return fail(PB_EPROTOCOL, "peer %d not wired (import/link)", r);
     c->epoch = epoch;
@@ -552,18 +582,8 @@ extern "C" pb_status pb_load_shard(pb_ctx* c) {
     pb_status st = check_ctx(c, "pb_load_shard");
     if (st) return st;
     if (c->phase != Phase::Begun) return fail(PB_EPROTOCOL, "pb_load_shard: call pb_trial_begin first");
-    const pb_plan* p = c->plan;
-    // One copy lane, in load-list order. Measured on B200 (tools/h2d_order.py): the H2D copy engine drains
-    // one stream's queue before starting another's, so alternating chunks over two streams makes every
-    // layer wait for half the model; a single ordered lane lands layer l at ~(l+1)/L of the load time.
-    const auto& ld = p->load[c->rank];
-    for (const CopyGroup& g : c->copies) {
-        CU(cudaMemcpyAsync(g.dst, g.src, g.bytes, cudaMemcpyHostToDevice, c->h2d[0]));
-        // one event per DMA: every chunk of the group maps to the group's first chunk event
-        CU(cudaEventRecord(c->landed[ld[g.first]], c->h2d[0]));
-        for (int32_t i = g.first; i < g.first + g.count; ++i) c->load_bytes += p->chunks[ld[i]].bytes;
-    }
-    c->phase = Phase::Loaded;
+    for (int32_t id : c->plan->load[c->rank]) c->load_bytes += c->plan->chunks[id].bytes;
+    c->phase = Phase::Loaded;   // armed: issued by the trial issuer (issue_trial) in data-arrival order
     return PB_OK;
 }
 
@@ -571,36 +591,9 @@ extern "C" pb_status pb_merge_lora(pb_ctx* c, int32_t adapter_id) {
     pb_status st = check_ctx(c, "pb_merge_lora");
     if (st) return st;
     if (c->phase != Phase::Loaded) return fail(PB_EPROTOCOL, "pb_merge_lora: call pb_load_shard first");
-    const pb_plan* p = c->plan;
-    if (adapter_id < -1 || adapter_id >= (int32_t)p->adapters.size())
+    if (adapter_id < -1 || adapter_id >= (int32_t)c->plan->adapters.size())
         return fail(PB_EINVAL, "adapter_id %d out of range", adapter_id);
-    std::vector<int32_t> others;
-    for (int r = 0; r < c->n; ++r)
-        if (r != c->rank) others.push_back(r);
-    std::vector<char> waited(p->chunks.size(), 0);
-    for (int32_t id : p->load[c->rank]) {
-        const ChunkRec& ch = p->chunks[id];
-        if (ch.is_adapter) continue;
-        CU(cudaStreamWaitEvent(c->merge, landed_ev(c, id), 0));
-        for (int32_t j : c->jobs_of_chunk[id]) {
-            const MergeJob& job = c->jobs[j];
-            if (job.adapter != adapter_id) continue;
-            for (int32_t a : job.need)
-                if (!waited[a]) {
-                    CU(cudaStreamWaitEvent(c->merge, landed_ev(c, a), 0));
-                    waited[a] = 1;
-                }
-            const int pi = prof_begin(c, K_MERGE, c->merge);
-            CU(launch_merge(job.maps, job.rows, job.cols, job.rank, job.scale, c->merge));
-            prof_end(c, pi, c->merge, 2.0 * job.rows * job.cols * job.rank,
-                     4.0 * job.rows * job.cols + 2.0 * job.rank * (job.rows + job.cols));
-            ++c->n_launches;
-        }
-        if (!others.empty()) CU(signal_ranks(c, c->L.f_chunk + id, others, c->merge));
-        if (c->last_own_chunk[ch.tensor] == id) CU(cudaEventRecord(c->tensor_ready[ch.tensor], c->merge));
-        if (id == c->last_own_stage_chunk) CU(cudaEventRecord(c->ready_merge, c->merge));
-    }
-    CU(cudaEventRecord(c->merge_done, c->merge));
+    c->merge_adapter = adapter_id;
     c->phase = Phase::Merged;
     return PB_OK;
 }
@@ -609,18 +602,7 @@ extern "C" pb_status pb_gather_layers(pb_ctx* c) {
     pb_status st = check_ctx(c, "pb_gather_layers");
     if (st) return st;
     if (c->phase != Phase::Merged) return fail(PB_EPROTOCOL, "pb_gather_layers: call pb_merge_lora first");
-    const pb_plan* p = c->plan;
-    for (int32_t id : p->recv[c->rank]) {
-        const ChunkRec& ch = p->chunks[id];
-        CU(wait_word(c, c->L.f_chunk + id, c->nv));
-        CU(cudaMemcpyAsync(c->weights + ch.dev_off, c->peers[ch.loader].weights + ch.dev_off, ch.bytes,
-                           cudaMemcpyDeviceToDevice, c->nv));
-        CU(cudaEventRecord(c->gathered[id], c->nv));
-        c->recv_bytes += ch.bytes;
-        if (c->last_recv_chunk[ch.tensor] == id) CU(cudaEventRecord(c->tensor_ready[ch.tensor], c->nv));
-        if (id == c->last_recv_stage_chunk) CU(cudaEventRecord(c->ready_recv, c->nv));
-    }
-    CU(cudaEventRecord(c->gather_done, c->nv));
+    for (int32_t id : c->plan->recv[c->rank]) c->recv_bytes += c->plan->chunks[id].bytes;
     c->phase = Phase::Gathered;
     return PB_OK;
 }
@@ -641,7 +623,7 @@ const __nv_bfloat16* wt(pb_ctx* c, int l, const char* sfx) {
 cudaError_t wait_tensor(pb_ctx* c, int l, const char* sfx) {
     const pb_plan* p = c->plan;
     const int32_t t = p->find_tensor("L" + std::to_string(l) + "." + sfx);
-    return cudaStreamWaitEvent(c->comp, c->tensor_ready[t], 0);
+    return wait_word(c, c->L.f_tensor + t, c->comp);
 }
 
 // Layer l on token rows [r0, r1) (prompt positions [ta, tb)). On the first prompt chunk each step waits
@@ -743,77 +725,249 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, boo
 
 }  // namespace
 
-static pb_status enqueue_prefill(pb_ctx* c, const int32_t* tokens, int32_t B, int32_t T, bool replay);
+// ================================================================================================
+// Trial issuer: one thread per rank issues every operation of the trial in data-arrival order —
+// copy group -> the merges / peer signals / tensor words of its chunks -> the receive copies (pro rata)
+// -> the compute items whose weights have been issued. Every stream has an outstanding-op budget
+// (mark events polled with cudaEventQuery), so no enqueue call ever blocks inside the driver on a full
+// queue: measured on B200, an enqueue blocked behind a device-side wait never recovers, and a 70B model
+// has thousands of copies. Every device-side wait is issued after the operation that satisfies it
+// (topological order), so the issuer can only ever poll, never deadlock.
+// ================================================================================================
+namespace {
 
-extern "C" pb_status pb_prefill_enqueue(pb_ctx* c, const int32_t* tokens, int32_t B, int32_t T) {
-    pb_status st = check_ctx(c, "pb_prefill_enqueue");
-    if (st) return st;
-    if (c->phase != Phase::Gathered) return fail(PB_EPROTOCOL, "pb_prefill_enqueue: call pb_gather_layers first");
-    return enqueue_prefill(c, tokens, B, T, false);
+struct Budget {
+    static constexpr int kMarkEvery = 16, kCap = 384;
+    cudaStream_t s = nullptr;
+    cudaEvent_t* pool = nullptr;   // kPool events, reused cyclically (at most kCap/kMarkEvery+1 in flight)
+    size_t next = 0;
+    std::deque<std::pair<cudaEvent_t, long>> marks;
+    long issued = 0, done = 0, since = 0;
+    void poll() {
+        while (!marks.empty() && cudaEventQuery(marks.front().first) == cudaSuccess) {
+            done = marks.front().second;
+            marks.pop_front();
+        }
+    }
+    cudaError_t mark() {   // a progress event covering every op issued so far
+        since = 0;
+        cudaEvent_t e = pool[next++ % kEventPool];
+        marks.emplace_back(e, issued);
+        return cudaEventRecord(e, s);
+    }
+    // True when n more ops fit. A request larger than the cap is admitted once the stream is empty; the
+    // ops issued since the last mark get a mark of their own so that "empty" becomes observable.
+    bool can(long n) {
+        if (issued - done + n <= kCap) return true;
+        if (since > 0 && mark() != cudaSuccess) return false;
+        poll();
+        return issued - done + n <= kCap || issued == done;
+    }
+    cudaError_t add(long n) {
+        issued += n;
+        since += n;
+        return since >= kMarkEvery ? mark() : cudaSuccess;
+    }
+};
+
+enum ItemKind { I_PROLOGUE, I_EMBED, I_WAITACT, I_LAYER, I_PUSH, I_FINAL, I_HEAD, I_ARGMAX, I_DONE };
+struct Item {
+    int kind, j, l;
+    std::vector<int32_t> prereq;   // tensors whose readiness-word writer must already be issued
+};
+
+struct Issuer {
+    pb_ctx* c;
+    int B, T, k;
+    bool replay;
+    std::vector<int> tb;
+    std::vector<Item> items;
+    std::vector<char> tensor_issued, adapter_waited;
+    Budget h2d, merge, nv, comp;
+};
+
+int prof_ops(pb_ctx* c) { return c->profiling ? 2 : 0; }
+
+// ---- loads and merges of one copy group
+pb_status issue_group(Issuer& I, size_t gi) {
+    pb_ctx* c = I.c;
+    const pb_plan* p = c->plan;
+    const CopyGroup& g = c->copies[gi];
+    const auto& ld = p->load[c->rank];
+    // The landed event doubles as the merge stream's dependency: the issuer issues every copy before the
+    // waits on it, so a plain event works and the copy lane carries no memop (a stream write after each
+    // copy stalls the copy engine between groups, measured ~10 us per group on B200).
+    CU(cudaMemcpyAsync(g.dst, g.src, g.bytes, cudaMemcpyHostToDevice, c->h2d[0]));
+    CU(cudaEventRecord(c->landed[ld[g.first]], c->h2d[0]));
+    CU(I.h2d.add(2));
+    static thread_local std::vector<int32_t> others;
+    others.clear();
+    for (int r = 0; r < c->n; ++r)
+        if (r != c->rank) others.push_back(r);
+    long mops = 0;
+    for (int32_t i = g.first; i < g.first + g.count; ++i) {
+        const int32_t id = ld[i];
+        const ChunkRec& ch = p->chunks[id];
+        if (ch.is_adapter) continue;
+        CU(cudaStreamWaitEvent(c->merge, landed_ev(c, id), 0));
+        ++mops;
+        for (int32_t j : c->jobs_of_chunk[id]) {
+            const MergeJob& job = c->jobs[j];
+            if (job.adapter != c->merge_adapter) continue;
+            for (int32_t a : job.need)
+                if (!I.adapter_waited[a]) {
+                    CU(cudaStreamWaitEvent(c->merge, landed_ev(c, a), 0));
+                    I.adapter_waited[a] = 1;
+                    ++mops;
+                }
+            const int pi = prof_begin(c, K_MERGE, c->merge);
+            CU(launch_merge(job.maps, job.rows, job.cols, job.rank, job.scale, c->merge));
+            prof_end(c, pi, c->merge, 2.0 * job.rows * job.cols * job.rank,
+                     4.0 * job.rows * job.cols + 2.0 * job.rank * (job.rows + job.cols));
+            ++c->n_launches;
+            mops += 1 + prof_ops(c);
+        }
+        if (!others.empty()) {
+            CU(signal_ranks(c, c->L.f_chunk + id, others, c->merge));
+            mops += 1 + prof_ops(c);
+        }
+        if (c->last_own_chunk[ch.tensor] == id) {
+            CU(set_word(c, c->L.f_tensor + ch.tensor, c->merge));
+            I.tensor_issued[ch.tensor] = 1;
+            ++mops;
+        }
+        if (id == c->last_own_stage_chunk) {
+            CU(cudaEventRecord(c->ready_merge, c->merge));
+            ++mops;
+        }
+    }
+    CU(I.merge.add(mops));
+    return PB_OK;
 }
 
-extern "C" pb_status pb_prefill_replay(pb_ctx* c, uint32_t epoch, const int32_t* tokens, int32_t B, int32_t T) {
-    pb_status st = check_ctx(c, "pb_prefill_replay");
-    if (st) return st;
-    if (c->phase != Phase::Prefilled) return fail(PB_EPROTOCOL, "pb_prefill_replay: needs a completed cold start");
-    if (epoch <= c->epoch) return fail(PB_EINVAL, "epoch %u must exceed the previous %u", epoch, c->epoch);
-    CU(cudaStreamSynchronize(c->comp));
-    c->epoch = epoch;
-    c->n_launches = 0;
-    c->prof_n = 0;
-    CU(cudaEventRecord(c->t0, c->comp));
-    return enqueue_prefill(c, tokens, B, T, true);
+long group_merge_ops(Issuer& I, size_t gi) {
+    pb_ctx* c = I.c;
+    const CopyGroup& g = c->copies[gi];
+    long n = 0;
+    for (int32_t i = g.first; i < g.first + g.count; ++i) {
+        const int32_t id = c->plan->load[c->rank][i];
+        n += 6 + (long)c->jobs_of_chunk[id].size() * (5 + prof_ops(c));
+    }
+    return n;
 }
 
-static pb_status enqueue_prefill(pb_ctx* c, const int32_t* tokens, int32_t B, int32_t T, bool replay) {
-    pb_status st = PB_OK;
-    if (B < 1 || T < 1 || B > c->L.max_batch || T > c->L.max_seq || (int64_t)B * T > c->L.max_rows)
-        return fail(PB_EINVAL, "batch %d x seq %d exceeds the workspace (%d x %d)", B, T, c->L.max_batch, c->L.max_seq);
-    if (c->rank == 0 && !tokens) return fail(PB_EINVAL, "rank 0 needs tokens");
+pb_status issue_recv(Issuer& I, size_t ri) {
+    pb_ctx* c = I.c;
+    const int32_t id = c->plan->recv[c->rank][ri];
+    const ChunkRec& ch = c->plan->chunks[id];
+    CU(wait_word(c, c->L.f_chunk + id, c->nv));
+    CU(cudaMemcpyAsync(c->weights + ch.dev_off, c->peers[ch.loader].weights + ch.dev_off, ch.bytes,
+                       cudaMemcpyDeviceToDevice, c->nv));
+    CU(cudaEventRecord(c->gathered[id], c->nv));
+    long n = 3;
+    if (c->last_recv_chunk[ch.tensor] == id) {
+        CU(set_word(c, c->L.f_tensor + ch.tensor, c->nv));
+        I.tensor_issued[ch.tensor] = 1;
+        ++n;
+    }
+    if (id == c->last_recv_stage_chunk) {
+        CU(cudaEventRecord(c->ready_recv, c->nv));
+        ++n;
+    }
+    CU(I.nv.add(n));
+    return PB_OK;
+}
+
+void build_items(Issuer& I) {
+    pb_ctx* c = I.c;
+    const pb_plan* p = c->plan;
+    const bool opt = p->model.arch == PB_ARCH_OPT;
+    const int g = c->rank, N = c->n;
+    const auto stage = p->stages[g];
+    auto add = [&](int kind, int j, int l, std::vector<int32_t> pre) {
+        if (I.replay) pre.clear();
+        I.items.push_back(Item{kind, j, l, std::move(pre)});
+    };
+    add(I_PROLOGUE, 0, 0, {});
+    for (int j = 0; j < I.k; ++j) {
+        if (g == 0) {
+            std::vector<int32_t> pre;
+            if (j == 0) {
+                const int32_t et = p->find_tensor("embed");
+                if (c->last_own_chunk[et] >= 0) pre.push_back(et);
+                if (opt) pre.push_back(p->find_tensor("pos"));
+            }
+            add(I_EMBED, j, 0, pre);
+        } else {
+            add(I_WAITACT, j, 0, {});
+        }
+        for (int l = stage.first; l < stage.second; ++l) {
+            std::vector<int32_t> pre;
+            if (j == 0)
+                for (size_t t = 0; t < p->tensors.size(); ++t)
+                    if (p->tensors[t].layer == l) pre.push_back((int32_t)t);
+            add(I_LAYER, j, l, pre);
+        }
+        if (g < N - 1) add(I_PUSH, j, 0, {});
+    }
+    if (g == N - 1) {
+        std::vector<int32_t> pre{p->find_tensor("final_g")};
+        if (opt) pre.push_back(p->find_tensor("final_b"));
+        add(I_FINAL, 0, 0, pre);
+    }
+    if (is_head_owner(p, g)) add(I_HEAD, 0, 0, {head_tensor(p)});
+    if (g == 0) add(I_ARGMAX, 0, 0, {});
+    add(I_DONE, 0, 0, {});
+}
+
+long item_ops(Issuer& I, const Item& it) {
+    const int po = prof_ops(I.c);
+    switch (it.kind) {
+        case I_LAYER: return 16 + 8 * po;
+        case I_EMBED: return 8 + po;
+        default: return 8 + po;
+    }
+}
+
+pb_status issue_item(Issuer& I, const Item& it) {
+    pb_ctx* c = I.c;
     const pb_plan* p = c->plan;
     const auto& m = p->model;
     const bool opt = m.arch == PB_ARCH_OPT;
-    const int g = c->rank, N = c->n, d = m.d_model, hd = p->head_dim();
+    const int g = c->rank, N = c->n, d = m.d_model, hd = p->head_dim(), B = I.B, T = I.T, V = m.vocab;
     const WsLayout& L = c->L;
     cudaStream_t s = c->comp;
-    c->cur_batch = B;
-    c->cur_seq = T;
-    const int k = std::max(1, std::min(p->opts.prefill_chunks, T));
-    std::vector<int> tb(k + 1);   // token chunk boundaries, remainder to lower chunks
-    for (int j = 0, t = 0; j <= k; ++j) {
-        tb[j] = t;
-        if (j < k) t += T / k + (j < T % k ? 1 : 0);
-    }
     float* h = reinterpret_cast<float*>(c->ws + L.h);
-    if (!opt) {
-        CU(launch_rope_table(reinterpret_cast<float2*>(c->ws + L.rope), T, hd, m.rope_theta, s));
-        ++c->n_launches;
-    }
-    if (g == 0) {
-        for (int b = 0; b < B; ++b)   // token-major rows: row = t * B + b
-            for (int t = 0; t < T; ++t) c->h_tokens[t * B + b] = tokens[(size_t)b * T + t];
-        CU(cudaMemcpyAsync(c->ws + L.tokens, c->h_tokens, sizeof(int32_t) * B * T, cudaMemcpyHostToDevice, s));
-        CU(cudaMemsetAsync(c->ws + L.nan, 0, 4, s));
-    }
-    const auto stage = p->stages[g];
-    for (int j = 0; j < k; ++j) {
-        const int r0 = tb[j] * B, r1 = tb[j + 1] * B;
-        if (g == 0) {
-            if (j == 0 && !replay) {
-                // embedding rows may live on every rank (vocab slices): wait for each piece
-                const int32_t et = p->find_tensor("embed");
-                for (auto& ch : p->chunks) {
-                    if (ch.is_adapter || ch.tensor != et) continue;
-                    if (ch.loader == g) continue;
-                    CU(wait_word(c, L.f_chunk + ch.id, s));
-                }
-                if (c->last_own_chunk[et] >= 0) CU(cudaStreamWaitEvent(s, c->tensor_ready[et], 0));
-                if (opt) CU(cudaStreamWaitEvent(s, c->tensor_ready[p->find_tensor("pos")], 0));
+    __nv_bfloat16* y = reinterpret_cast<__nv_bfloat16*>(c->ws + L.y);
+    float* logits = reinterpret_cast<float*>(c->ws + L.logits);
+    const int j = it.j;
+    const int r0 = I.tb[j] * B, r1 = I.tb[j + 1] * B;
+    std::vector<int32_t> owners;
+    for (int r = 0; r < N; ++r)
+        if (is_head_owner(p, r)) owners.push_back(r);
+    switch (it.kind) {
+        case I_PROLOGUE:
+            if (!opt) {
+                CU(launch_rope_table(reinterpret_cast<float2*>(c->ws + L.rope), T, hd, m.rope_theta, s));
+                ++c->n_launches;
+            }
+            if (g == 0) {
+                CU(cudaMemcpyAsync(c->ws + L.tokens, c->h_tokens, sizeof(int32_t) * B * T, cudaMemcpyHostToDevice, s));
+                CU(cudaMemsetAsync(c->ws + L.nan, 0, 4, s));
+            }
+            break;
+        case I_EMBED: {
+            const int32_t et = p->find_tensor("embed");
+            if (j == 0 && !I.replay) {
+                // embedding rows may live on every rank (vocab slices): wait for each remote piece
+                for (auto& ch : p->chunks)
+                    if (!ch.is_adapter && ch.tensor == et && ch.loader != g) CU(wait_word(c, L.f_chunk + ch.id, s));
+                if (c->last_own_chunk[et] >= 0) CU(wait_word(c, L.f_tensor + et, s));
+                if (opt) CU(wait_word(c, L.f_tensor + p->find_tensor("pos"), s));
             }
             EmbedSrc E{};
-            const int32_t et = p->find_tensor("embed");
             if (p->opts.vocab_sliced) {
-                auto sl = std::vector<int32_t>(N + 1, 0);
+                std::vector<int32_t> sl(N + 1, 0);
                 for (auto& ch : p->chunks)
                     if (!ch.is_adapter && ch.tensor == et) sl[ch.loader + 1] = std::max(sl[ch.loader + 1], ch.r1);
                 for (int r = 0; r < N; ++r) {
@@ -829,85 +983,210 @@ static pb_status enqueue_prefill(pb_ctx* c, const int32_t* tokens, int32_t B, in
                 E.n = 1;
             }
             const int pi = prof_begin(c, K_EMBED, s);
-            CU(launch_embed(E, opt ? wt(c, -1, "pos") : nullptr, reinterpret_cast<const int32_t*>(c->ws + L.tokens), h, d,
-                            r0, r1, B, s));
+            CU(launch_embed(E, opt ? wt(c, -1, "pos") : nullptr, reinterpret_cast<const int32_t*>(c->ws + L.tokens), h,
+                            d, r0, r1, B, s));
             prof_end(c, pi, s, (opt ? 1.0 : 0.0) * (r1 - r0) * d, (r1 - r0) * d * (opt ? 8.0 : 6.0));
             ++c->n_launches;
-        } else {
+            break;
+        }
+        case I_WAITACT:
             CU(wait_word(c, L.f_act + j, s));
-        }
-        for (int l = stage.first; l < stage.second; ++l) {
-            st = run_layer(c, l, r0, r1, tb[j], tb[j + 1], B, j == 0 && !replay);
+            break;
+        case I_LAYER: {
+            pb_status st = run_layer(c, it.l, r0, r1, I.tb[j], I.tb[j + 1], B, j == 0 && !I.replay);
             if (st) return st;
+            break;
         }
-        if (g < N - 1) {
-            CU(cudaMemcpyAsync(c->peers[g + 1].ws + L.h + (size_t)r0 * d * 4, h + (size_t)r0 * d, (size_t)(r1 - r0) * d * 4,
-                               cudaMemcpyDeviceToDevice, s));
+        case I_PUSH:
+            CU(cudaMemcpyAsync(c->peers[g + 1].ws + L.h + (size_t)r0 * d * 4, h + (size_t)r0 * d,
+                               (size_t)(r1 - r0) * d * 4, cudaMemcpyDeviceToDevice, s));
             CU(signal_ranks(c, L.f_act + j, {g + 1}, s));
-        }
-    }
-    // final norm of the last position (last stage), broadcast y to the head owners
-    __nv_bfloat16* y = reinterpret_cast<__nv_bfloat16*>(c->ws + L.y);
-    std::vector<int32_t> owners;
-    for (int r = 0; r < N; ++r)
-        if (is_head_owner(p, r)) owners.push_back(r);
-    if (g == N - 1) {
-        if (!replay) {
-            CU(cudaStreamWaitEvent(s, c->tensor_ready[p->find_tensor("final_g")], 0));
-            if (opt) CU(cudaStreamWaitEvent(s, c->tensor_ready[p->find_tensor("final_b")], 0));
-        }
-        const int pi = prof_begin(c, K_NORM, s);
-        CU(launch_norm(h + (size_t)(T - 1) * B * d, d, y, d, B, d, wt(c, -1, "final_g"), opt ? wt(c, -1, "final_b") : nullptr,
-                       m.norm_eps, s));
-        prof_end(c, pi, s, 8.0 * B * d, 6.0 * B * d);
-        ++c->n_launches;
-        std::vector<int32_t> remote;
-        for (int32_t r : owners)
-            if (r != g) {
-                CU(cudaMemcpyAsync(c->peers[r].ws + L.y, y, (size_t)B * d * 2, cudaMemcpyDeviceToDevice, s));
-                remote.push_back(r);
+            break;
+        case I_FINAL: {
+            if (!I.replay) {
+                CU(wait_word(c, L.f_tensor + p->find_tensor("final_g"), s));
+                if (opt) CU(wait_word(c, L.f_tensor + p->find_tensor("final_b"), s));
             }
-        CU(signal_ranks(c, L.f_y, remote, s));
+            const int pi = prof_begin(c, K_NORM, s);
+            CU(launch_norm(h + (size_t)(T - 1) * B * d, d, y, d, B, d, wt(c, -1, "final_g"),
+                           opt ? wt(c, -1, "final_b") : nullptr, m.norm_eps, s));
+            prof_end(c, pi, s, 8.0 * B * d, 6.0 * B * d);
+            ++c->n_launches;
+            std::vector<int32_t> remote;
+            for (int32_t r : owners)
+                if (r != g) {
+                    CU(cudaMemcpyAsync(c->peers[r].ws + L.y, y, (size_t)B * d * 2, cudaMemcpyDeviceToDevice, s));
+                    remote.push_back(r);
+                }
+            CU(signal_ranks(c, L.f_y, remote, s));
+            break;
+        }
+        case I_HEAD: {
+            if (g != N - 1) CU(wait_word(c, L.f_y, s));
+            const int32_t ht = head_tensor(p);
+            if (!I.replay) CU(wait_word(c, L.f_tensor + ht, s));
+            int32_t v0, v1;
+            head_slice(p, g, &v0, &v1);
+            const __nv_bfloat16* E = reinterpret_cast<const __nv_bfloat16*>(c->weights + p->tensors[ht].dev_off);
+            const int pi = prof_begin(c, K_LOGITS, s);
+            CU(launch_logits(y, B, d, E, v0, v1, logits, V, s));
+            prof_end(c, pi, s, 2.0 * B * (v1 - v0) * d, 2.0 * (double)(v1 - v0) * d + 4.0 * B * (v1 - v0));
+            ++c->n_launches;
+            if (g != 0) {
+                CU(cudaMemcpy2DAsync(c->peers[0].ws + L.logits + (size_t)v0 * 4, (size_t)V * 4, logits + v0,
+                                     (size_t)V * 4, (size_t)(v1 - v0) * 4, B, cudaMemcpyDeviceToDevice, s));
+                CU(signal_ranks(c, L.f_logit + g, {0}, s));
+            }
+            break;
+        }
+        case I_ARGMAX: {
+            for (int32_t r : owners)
+                if (r != 0) CU(wait_word(c, L.f_logit + r, s));
+            const int pi = prof_begin(c, K_ARGMAX, s);
+            CU(launch_argmax(logits, B, V, V, reinterpret_cast<int32_t*>(c->ws + L.tok_out),
+                             reinterpret_cast<int32_t*>(c->ws + L.nan), s));
+            prof_end(c, pi, s, 0, 4.0 * B * V);
+            ++c->n_launches;
+            CU(cudaMemcpyAsync(c->h_out, c->ws + L.tok_out, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, s));
+            CU(cudaMemcpyAsync(c->h_out + B, c->ws + L.nan, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+            break;
+        }
+        case I_DONE:
+            CU(cudaEventRecord(c->done, s));
+            break;
     }
-    float* logits = reinterpret_cast<float*>(c->ws + L.logits);
-    const int V = m.vocab;
-    if (is_head_owner(p, g)) {
-        if (g != N - 1) CU(wait_word(c, L.f_y, s));
-        const int32_t ht = head_tensor(p);
-        if (!replay) CU(cudaStreamWaitEvent(s, c->tensor_ready[ht], 0));
-        int32_t v0, v1;
-        head_slice(p, g, &v0, &v1);
-        const __nv_bfloat16* E = reinterpret_cast<const __nv_bfloat16*>(c->weights + p->tensors[ht].dev_off);
-        const int pi = prof_begin(c, K_LOGITS, s);
-        CU(launch_logits(y, B, d, E, v0, v1, logits, V, s));
-        prof_end(c, pi, s, 2.0 * B * (v1 - v0) * d, 2.0 * (double)(v1 - v0) * d + 4.0 * B * (v1 - v0));
-        ++c->n_launches;
-        if (g != 0) {
-            CU(cudaMemcpy2DAsync(c->peers[0].ws + L.logits + (size_t)v0 * 4, (size_t)V * 4, logits + v0, (size_t)V * 4,
-                                 (size_t)(v1 - v0) * 4, B, cudaMemcpyDeviceToDevice, s));
-            CU(signal_ranks(c, L.f_logit + g, {0}, s));
+    return PB_OK;
+}
+
+pb_status issue_trial(pb_ctx* c, int B, int T, bool replay) {
+    const pb_plan* p = c->plan;
+    Issuer I;
+    I.c = c;
+    I.B = B;
+    I.T = T;
+    I.replay = replay;
+    I.k = std::max(1, std::min(p->opts.prefill_chunks, T));
+    I.tb.assign(I.k + 1, 0);
+    for (int j = 0, t = 0; j <= I.k; ++j) {   // prompt chunk boundaries, remainder to lower chunks
+        I.tb[j] = t;
+        if (j < I.k) t += T / I.k + (j < T % I.k ? 1 : 0);
+    }
+    I.tensor_issued.assign(p->tensors.size(), replay ? 1 : 0);
+    I.adapter_waited.assign(p->chunks.size(), 0);
+    cudaStream_t ss[4] = {c->h2d[0], c->merge, c->nv, c->comp};
+    Budget* bs[4] = {&I.h2d, &I.merge, &I.nv, &I.comp};
+    for (int i = 0; i < 4; ++i) {
+        bs[i]->s = ss[i];
+        bs[i]->pool = c->budget_events.data() + i * kEventPool;
+    }
+    build_items(I);
+    const size_t G = replay ? 0 : c->copies.size();
+    const size_t R = replay ? 0 : p->recv[c->rank].size();
+    size_t gi = 0, ri = 0, ii = 0;
+    static const bool dbg = getenv("PB_DEBUG_ISSUER") != nullptr;
+    auto last_report = std::chrono::steady_clock::now();
+    while (gi < G || ri < R || ii < I.items.size()) {
+        bool progressed = false;
+        while (gi < G && I.h2d.can(2) && I.merge.can(group_merge_ops(I, gi))) {
+            pb_status st = issue_group(I, gi++);
+            if (st) return st;
+            progressed = true;
+        }
+        const size_t target = gi >= G ? R : (gi * R) / std::max<size_t>(G, 1);
+        while (ri < target && I.nv.can(5)) {
+            pb_status st = issue_recv(I, ri++);
+            if (st) return st;
+            progressed = true;
+        }
+        while (ii < I.items.size()) {
+            const Item& it = I.items[ii];
+            bool ok = true;
+            for (int32_t t : it.prereq) ok = ok && I.tensor_issued[t];
+            if (!ok || !I.comp.can(item_ops(I, it))) break;
+            pb_status st = issue_item(I, it);
+            if (st) return st;
+            CU(I.comp.add(item_ops(I, it)));
+            ++ii;
+            progressed = true;
+        }
+        if (!progressed) {
+            std::this_thread::sleep_for(std::chrono::microseconds(20));
+            if (dbg && std::chrono::steady_clock::now() - last_report > std::chrono::seconds(2)) {
+                last_report = std::chrono::steady_clock::now();
+                const Item* it = ii < I.items.size() ? &I.items[ii] : nullptr;
+                int missing = -1;
+                if (it)
+                    for (int32_t t : it->prereq)
+                        if (!I.tensor_issued[t]) { missing = t; break; }
+                fprintf(stderr,
+                        "[pb issuer r%d] stalled: groups %zu/%zu recv %zu/%zu items %zu/%zu (kind %d j %d l %d, missing "
+                        "tensor %d) outstanding h2d %ld merge %ld nv %ld comp %ld\n",
+                        c->rank, gi, G, ri, R, ii, I.items.size(), it ? it->kind : -1, it ? it->j : -1, it ? it->l : -1,
+                        missing, I.h2d.issued - I.h2d.done, I.merge.issued - I.merge.done, I.nv.issued - I.nv.done,
+                        I.comp.issued - I.comp.done);
+            }
         }
     }
-    if (g == 0) {
-        for (int32_t r : owners)
-            if (r != 0) CU(wait_word(c, L.f_logit + r, s));
-        const int pi = prof_begin(c, K_ARGMAX, s);
-        CU(launch_argmax(logits, B, V, V, reinterpret_cast<int32_t*>(c->ws + L.tok_out),
-                         reinterpret_cast<int32_t*>(c->ws + L.nan), s));
-        prof_end(c, pi, s, 0, 4.0 * B * V);
-        ++c->n_launches;
-        CU(cudaMemcpyAsync(c->h_out, c->ws + L.tok_out, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, s));
-        CU(cudaMemcpyAsync(c->h_out + B, c->ws + L.nan, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    if (!replay) {
+        CU(cudaEventRecord(c->merge_done, c->merge));
+        CU(cudaEventRecord(c->gather_done, c->nv));
     }
-    CU(cudaEventRecord(c->done, s));
-    c->phase = Phase::Prefilled;
     return PB_OK;
+}
+
+pb_status start_issuer(pb_ctx* c, const int32_t* tokens, int32_t B, int32_t T, bool replay) {
+    if (B < 1 || T < 1 || B > c->L.max_batch || T > c->L.max_seq || (int64_t)B * T > c->L.max_rows)
+        return fail(PB_EINVAL, "batch %d x seq %d exceeds the workspace (%d x %d)", B, T, c->L.max_batch, c->L.max_seq);
+    if (c->rank == 0 && !tokens) return fail(PB_EINVAL, "rank 0 needs tokens");
+    if (c->rank == 0)
+        for (int b = 0; b < B; ++b)   // token-major rows: row = t * B + b
+            for (int t = 0; t < T; ++t) c->h_tokens[t * B + b] = tokens[(size_t)b * T + t];
+    c->cur_batch = B;
+    c->cur_seq = T;
+    join_load(c);
+    c->issue_status = PB_OK;
+    c->issue_msg[0] = '\0';
+    c->phase = Phase::Prefilled;
+    c->load_thread = std::thread([c, B, T, replay]() {
+        cudaSetDevice(c->device);
+        pb_status st = issue_trial(c, B, T, replay);
+        if (st != PB_OK) {
+            c->issue_status = st;
+            snprintf(c->issue_msg, sizeof c->issue_msg, "%s", pb_last_error());
+        }
+    });
+    return PB_OK;
+}
+
+}  // namespace
+
+extern "C" pb_status pb_prefill_enqueue(pb_ctx* c, const int32_t* tokens, int32_t B, int32_t T) {
+    pb_status st = check_ctx(c, "pb_prefill_enqueue");
+    if (st) return st;
+    if (c->phase != Phase::Gathered) return fail(PB_EPROTOCOL, "pb_prefill_enqueue: call pb_gather_layers first");
+    return start_issuer(c, tokens, B, T, false);
+}
+
+extern "C" pb_status pb_prefill_replay(pb_ctx* c, uint32_t epoch, const int32_t* tokens, int32_t B, int32_t T) {
+    pb_status st = check_ctx(c, "pb_prefill_replay");
+    if (st) return st;
+    if (c->phase != Phase::Prefilled) return fail(PB_EPROTOCOL, "pb_prefill_replay: needs a completed cold start");
+    if (epoch <= c->epoch) return fail(PB_EINVAL, "epoch %u must exceed the previous %u", epoch, c->epoch);
+    join_load(c);
+    CU(cudaStreamSynchronize(c->comp));
+    c->epoch = epoch;
+    c->n_launches = 0;
+    c->prof_n = 0;
+    CU(cudaEventRecord(c->t0, c->comp));
+    return start_issuer(c, tokens, B, T, true);
 }
 
 extern "C" pb_status pb_prefill_wait(pb_ctx* c, float* logits_out, int32_t* tokens_out) {
     pb_status st = check_ctx(c, "pb_prefill_wait");
     if (st) return st;
     if (c->phase != Phase::Prefilled) return fail(PB_EPROTOCOL, "pb_prefill_wait: nothing enqueued");
+    join_load(c);
+    if (c->issue_status != PB_OK) return fail(c->issue_status, "issuer: %s", c->issue_msg);
     CU(cudaEventSynchronize(c->done));
     CU(cudaGetLastError());
     if (c->rank == 0) {
@@ -931,6 +1210,8 @@ extern "C" pb_status pb_prefill_first_token(pb_ctx* c, const int32_t* tokens, in
 extern "C" pb_status pb_sync(pb_ctx* c) {
     pb_status st = check_ctx(c, "pb_sync");
     if (st) return st;
+    join_load(c);
+    if (c->issue_status != PB_OK) return fail(c->issue_status, "issuer: %s", c->issue_msg);
     cudaStream_t ss[] = {c->h2d[0], c->h2d[1], c->merge, c->nv, c->comp};
     for (auto s : ss) CU(cudaStreamSynchronize(s));
     CU(cudaGetLastError());

@@ -3,6 +3,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <thread>
 #include <vector>
 
 #include "kernels.hpp"
@@ -19,6 +20,7 @@ struct WsLayout {
     int32_t max_rows = 0, max_batch = 0, max_seq = 0;
     // readiness words (uint32) inside `flags`
     int32_t f_chunk = 0, f_act = 0, f_y = 0, f_logit = 0, n_words = 0;
+    int32_t f_land = 0, f_tensor = 0;   // local words: copy group landed (by first chunk id), tensor ready
 };
 WsLayout ws_layout(const pb_plan* p, int32_t batch, int32_t seq);
 
@@ -52,6 +54,7 @@ struct Peer {
 };
 
 enum class Phase { Idle, Begun, Loaded, Merged, Gathered, Prefilled };
+constexpr int kEventPool = 64;
 
 // Kernel classes timed by the optional per-launch profiler (pb_ctx_set_profiling).
 enum KClass : int { K_MERGE = 0, K_GEMM, K_ATTN, K_NORM, K_ROPE, K_EMBED, K_LOGITS, K_ARGMAX, K_SIGNAL, K_NCLASS };
@@ -81,7 +84,7 @@ struct pb_ctx {
     cudaEvent_t t0 = nullptr, merge_done = nullptr, gather_done = nullptr, done = nullptr;
     cudaEvent_t ready_merge = nullptr, ready_recv = nullptr;   // timing: last stage chunk merged / received
     int32_t last_own_stage_chunk = -1, last_recv_stage_chunk = -1;
-    std::vector<cudaEvent_t> landed, gathered, tensor_ready;
+    std::vector<cudaEvent_t> landed, gathered;
     std::vector<char> tensor_own;        // this rank loads every piece of the tensor
     std::vector<int32_t> last_own_chunk; // per base tensor: last own chunk in load order (-1 if none)
     std::vector<int32_t> last_recv_chunk;
@@ -109,6 +112,12 @@ struct pb_ctx {
     int64_t load_bytes = 0, recv_bytes = 0;
     std::vector<double> tl_landed, tl_gathered;
     bool use_wait_value = true;
+    std::thread load_thread;                 // the trial issuer (see issue_trial)
+    pb_status issue_status = PB_OK;
+    char issue_msg[512] = "";
+    int32_t merge_adapter = -1;
+    std::vector<cudaEvent_t> budget_events;
+    std::vector<cudaStream_t> owned_streams;   // created by the ctx when the caller passed NULL  // 4 streams x kEventPool progress marks
     bool profiling = false;
     std::vector<pb::ProfRec> prof;
     size_t prof_n = 0;

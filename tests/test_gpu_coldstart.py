@@ -25,6 +25,15 @@ from gpu_util import need_gpu
 pytestmark = pytest.mark.gpu
 
 _ORACLE_CACHE = {}
+_LIVE = []
+
+
+@pytest.fixture(autouse=True)
+def _free_engines():
+    yield
+    while _LIVE:
+        _LIVE.pop().close()
+    torch.cuda.synchronize()
 
 
 def oracle_logits(model, adapters, toks):
@@ -34,12 +43,15 @@ def oracle_logits(model, adapters, toks):
     return _ORACLE_CACHE[key]
 
 
-def run(model, adapters, n, toks, policy="stage", sliced=0, k=1, chunk_bytes=32 << 20, trials=1, alias=0):
+def run(model, adapters, n, toks, policy="stage", sliced=0, k=1, chunk_bytes=32 << 20, trials=1, alias=0, keep=False):
+    """keep=False closes the engines before returning (each logical rank owns 5 streams; more than
+    CUDA_DEVICE_MAX_CONNECTIONS live streams would share hardware queues)."""
     plan = Plan(model, adapters, n, policy=policy, vocab_sliced=sliced, chunk_bytes=chunk_bytes, prefill_chunks=k,
                 host_alias_layers=alias)
     base, ada = harness.build_host_images(plan)
     B, T = toks.shape
     engs = [RankEngine(plan, r, base, ada, max_batch=B, max_seq=T) for r in range(n)]
+    _LIVE.extend(engs)
     for e in engs:
         e.wire_local(engs)
     out = None
@@ -50,6 +62,9 @@ def run(model, adapters, n, toks, policy="stage", sliced=0, k=1, chunk_bytes=32 
             e.enqueue(ep, toks if e.rank == 0 else None, B, T, adapter_id=0 if adapters else -1)
         res = [e.wait(want_logits=True) for e in engs]
         out = res[0]
+    if not keep:
+        for e in engs:
+            e.close()
     return plan, engs, out, base
 
 
@@ -111,7 +126,7 @@ def test_gathered_bytes_exact():
     need_gpu()
     model, ads = TINY_OPT, (lora(8),)
     toks = synth.tokens(1, 16, model.vocab)
-    plan, engs, _, base = run(model, ads, 4, toks, policy="interleave", sliced=1, chunk_bytes=32 << 10)
+    plan, engs, _, base = run(model, ads, 4, toks, policy="interleave", sliced=1, chunk_bytes=32 << 10, keep=True)
     host = base.numpy()
     w = [e.weights_bytes() for e in engs]
     for (name, rows, cols, host_off, layer, dev_off) in plan.tensors():   # every rank: same merged model
@@ -147,7 +162,7 @@ def test_host_alias_layers():
 def test_timeline_and_protocol():
     need_gpu()
     toks = synth.tokens(1, 16, TINY_OPT.vocab)
-    plan, engs, _, _ = run(TINY_OPT, (lora(8),), 2, toks)
+    plan, engs, _, _ = run(TINY_OPT, (lora(8),), 2, toks, keep=True)
     for e in engs:
         tl = e.timeline()
         assert tl["load_bytes"] > 0 and tl["t_full_ms"] >= tl["t_ready_ms"] >= 0
@@ -178,7 +193,7 @@ def test_replay_bitwise_equals_cold_start():
     need_gpu()
     for n in (1, 2):
         toks = synth.tokens(1, 16, TINY_OPT.vocab)
-        plan, engs, (t1, l1), _ = run(TINY_OPT, (lora(8),), n, toks, policy="interleave", sliced=1, k=2)
+        plan, engs, (t1, l1), _ = run(TINY_OPT, (lora(8),), n, toks, policy="interleave", sliced=1, k=2, keep=True)
         for e in engs:
             e.replay_enqueue(2, toks if e.rank == 0 else None, 1, 16)
         res = [e.wait(want_logits=True) for e in engs]

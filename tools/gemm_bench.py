@@ -34,12 +34,13 @@ def bench(M, K, N, epi, split, reps=30):
     flops = 2 * M * (2 * N if epi == 2 else N) * K
     return us, wbytes / us / 1e3, flops / us / 1e6
 
-shapes = [("qkv", 128, 2048, 6144, 0), ("o", 128, 2048, 2048, 1), ("fc1", 128, 2048, 8192, 0), ("fc2", 128, 8192, 2048, 1),
-          ("c4_qkv_M1024", 1024, 5120, 15360, 0), ("c5_fc1_M2048", 2048, 8192, 28672, 2)]
-for name, M, K, N, epi in shapes:
-    res = []
-    for split in (0, 1, 2, 4, 8):
-        if split and split > K // 64: continue
-        us, gbs, tf = bench(M, K, N, epi, split)
-        res.append(f"S={split}: {us:7.1f}us {gbs:6.0f}GB/s {tf:6.0f}TF")
-    print(f"{name:14s} M{M} K{K} N{N}: " + " | ".join(res), flush=True)
+if __name__ == "__main__":
+  shapes = [("qkv", 128, 2048, 6144, 0), ("o", 128, 2048, 2048, 1), ("fc1", 128, 2048, 8192, 0), ("fc2", 128, 8192, 2048, 1),
+            ("c4_qkv_M1024", 1024, 5120, 15360, 0), ("c5_fc1_M2048", 2048, 8192, 28672, 2)]
+  for name, M, K, N, epi in shapes:
+      res = []
+      for split in (0, 1, 2, 4, 8):
+          if split and split > K // 64: continue
+          us, gbs, tf = bench(M, K, N, epi, split)
+          res.append(f"S={split}: {us:7.1f}us {gbs:6.0f}GB/s {tf:6.0f}TF")
+      print(f"{name:14s} M{M} K{K} N{N}: " + " | ".join(res), flush=True)
