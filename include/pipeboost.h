@@ -123,6 +123,8 @@ typedef struct {
     int64_t dev_weight_bytes;    /* per-GPU device buffer: the whole model, same offsets on every GPU */
     int64_t dev_adapter_bytes;   /* per-GPU device buffer for adapter factors (same layout as host) */
     int32_t n_tensors, n_atensors, n_chunks, n_gpus;
+    int64_t dev_adapted_bytes;   /* per-GPU device buffer for out-of-place per-adapter copies of the adapted
+                                    tensors (multi-adapter merge, pb_merge_lora(ctx, PB_MERGE_ALL)) */
 } pb_plan_sizes_t;
 PB_API pb_status pb_plan_sizes(const pb_plan* plan, pb_plan_sizes_t* out);
 
@@ -154,6 +156,7 @@ PB_API void pb_plan_free(pb_plan* plan);
 typedef struct {
     void* weights;        int64_t weights_cap;    /* device, >= dev_weight_bytes */
     void* adapters;       int64_t adapters_cap;   /* device, >= dev_adapter_bytes (may be NULL if no adapters) */
+    void* adapted;        int64_t adapted_cap;    /* device, >= dev_adapted_bytes for PB_MERGE_ALL, else may be NULL */
     void* workspace;      int64_t workspace_cap;  /* device, >= pb_plan_workspace_bytes(max_batch, max_seq) */
     int32_t max_batch, max_seq;
     /* cudaStream_t handles, five DISTINCT streams per rank; NULL = the ctx creates and owns its own
@@ -190,11 +193,14 @@ PB_API pb_status pb_trial_begin(pb_ctx* ctx, uint32_t epoch);
  * alternating the two H2D streams; a `landed` event per chunk. Async. */
 PB_API pb_status pb_load_shard(pb_ctx* ctx);
 
-/* a3 — enqueue the LoRA merge of every adapted row range this rank loaded
- * (tcgen05 kernel, in place, W <- RNE_bf16(W + s * B * A), fp32 accumulate), each
- * after its chunks land; then per-layer readiness and peer signals. Must be called
- * (even without adapters) after pb_load_shard. Async. adapter_id: which adapter to
- * merge into the base weights (the single-adapter case; -1 = none). */
+/* a3 — arm the LoRA merge of every adapted row range this rank loaded (tcgen05 kernel,
+ * W <- RNE_bf16(W + s * B * A), fp32 accumulate), each issued right after its chunks land, followed by the
+ * chunk's peer signal and readiness word. Must be called (even without adapters) after pb_load_shard.
+ * adapter_id >= 0: merge that adapter IN PLACE into the base weights (one adapter per instance);
+ * -1: no merge; PB_MERGE_ALL (-2): every adapter OUT OF PLACE into its own copy of each tensor it touches
+ * (several adapters served at once; needs bufs.adapted and the STAGE policy when n_gpus > 1),
+ * sequences then pick their adapter in pb_prefill_enqueue_ex. */
+#define PB_MERGE_ALL (-2)
 PB_API pb_status pb_merge_lora(pb_ctx* ctx, int32_t adapter_id);
 
 /* a4 — enqueue this rank's receive list: for each chunk, wait for the loader's
@@ -211,6 +217,10 @@ PB_API pb_status pb_gather_layers(pb_ctx* ctx);
  * (and on rank 0 the token D2H) is complete; pb_prefill_first_token = both.
  * Errors: PB_EINVAL (batch/seq out of range), PB_EPROTOCOL, PB_ECUDA, PB_ENUMERIC. */
 PB_API pb_status pb_prefill_enqueue(pb_ctx* ctx, const int32_t* tokens, int32_t batch, int32_t seq);
+/* Same, with the adapter of every sequence (host [batch], read on every rank; needs PB_MERGE_ALL). The batch
+ * then runs as `batch` single-sequence pipeline microbatches, each reading its adapter's merged copies. */
+PB_API pb_status pb_prefill_enqueue_ex(pb_ctx* ctx, const int32_t* tokens, const int32_t* adapter_of_seq,
+                                       int32_t batch, int32_t seq);
 PB_API pb_status pb_prefill_wait(pb_ctx* ctx, float* logits_out, int32_t* tokens_out);
 PB_API pb_status pb_prefill_first_token(pb_ctx* ctx, const int32_t* tokens, int32_t batch, int32_t seq,
                                  float* logits_out, int32_t* tokens_out);

@@ -13,6 +13,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libpipeboost.so")
 
+PB_MERGE_ALL = -2
 PB_OK, PB_EINVAL, PB_EPARTITION, PB_EPROTOCOL, PB_ECUDA, PB_ENOMEM, PB_ENUMERIC, PB_EUNSUPPORTED = \
     0, -1, -2, -3, -4, -6, -7, -8
 PB_ARCH_OPT, PB_ARCH_LLAMA = 0, 1
@@ -44,7 +45,8 @@ class pb_plan_opts(C.Structure):
 class pb_plan_sizes_t(C.Structure):
     _fields_ = [("host_base_bytes", C.c_int64), ("host_adapter_bytes", C.c_int64),
                 ("dev_weight_bytes", C.c_int64), ("dev_adapter_bytes", C.c_int64),
-                ("n_tensors", C.c_int32), ("n_atensors", C.c_int32), ("n_chunks", C.c_int32), ("n_gpus", C.c_int32)]
+                ("n_tensors", C.c_int32), ("n_atensors", C.c_int32), ("n_chunks", C.c_int32), ("n_gpus", C.c_int32),
+                ("dev_adapted_bytes", C.c_int64)]
 
 
 class pb_tensor_info(C.Structure):
@@ -60,7 +62,8 @@ class pb_atensor_info(C.Structure):
 
 class pb_rank_bufs(C.Structure):
     _fields_ = [("weights", C.c_void_p), ("weights_cap", C.c_int64), ("adapters", C.c_void_p),
-                ("adapters_cap", C.c_int64), ("workspace", C.c_void_p), ("workspace_cap", C.c_int64),
+                ("adapters_cap", C.c_int64), ("adapted", C.c_void_p), ("adapted_cap", C.c_int64),
+                ("workspace", C.c_void_p), ("workspace_cap", C.c_int64),
                 ("max_batch", C.c_int32), ("max_seq", C.c_int32), ("stream_h2d", C.c_void_p * 2),
                 ("stream_merge", C.c_void_p), ("stream_nvlink", C.c_void_p), ("stream_compute", C.c_void_p)]
 
@@ -100,6 +103,7 @@ _SIGS = {
     "pb_merge_lora": [_P, C.c_int32],
     "pb_gather_layers": [_P],
     "pb_prefill_enqueue": [_P, _P, C.c_int32, C.c_int32],
+    "pb_prefill_enqueue_ex": [_P, _P, _P, C.c_int32, C.c_int32],
     "pb_prefill_wait": [_P, _P, _P],
     "pb_prefill_replay": [_P, C.c_uint32, _P, C.c_int32, C.c_int32],
     "pb_prefill_first_token": [_P, _P, C.c_int32, C.c_int32, _P, _P],
@@ -262,6 +266,10 @@ def pb_prefill_enqueue(ctx, tokens_ptr, batch, seq):
 
 def pb_prefill_replay(ctx, epoch, tokens_ptr, batch, seq):
     check(lib().pb_prefill_replay(ctx, epoch, tokens_ptr, batch, seq))
+
+
+def pb_prefill_enqueue_ex(ctx, tokens_ptr, adapter_of_seq_ptr, batch, seq):
+    check(lib().pb_prefill_enqueue_ex(ctx, tokens_ptr, adapter_of_seq_ptr, batch, seq))
 
 
 def pb_prefill_wait(ctx, logits_ptr, tokens_ptr):

@@ -66,7 +66,9 @@ class RankEngine:
     """One rank's pb_ctx plus the device buffers and streams it borrows."""
 
     def __init__(self, plan: Plan, rank: int, host_base: torch.Tensor, host_adapters: Optional[torch.Tensor],
-                 max_batch: int = 1, max_seq: int = 128, device: Optional[torch.device] = None):
+                 max_batch: int = 1, max_seq: int = 128, device: Optional[torch.device] = None,
+                 multi_adapter: bool = False):
+        """multi_adapter=True allocates the out-of-place per-adapter copies (PB_MERGE_ALL mode)."""
         self.plan = plan
         self.rank = rank
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
@@ -77,6 +79,8 @@ class RankEngine:
         with torch.cuda.device(self.device):
             self.weights = torch.empty(s.dev_weight_bytes, dtype=torch.uint8, device=self.device)
             self.adapters = torch.empty(max(s.dev_adapter_bytes, 1), dtype=torch.uint8, device=self.device)
+            self.adapted = (torch.empty(s.dev_adapted_bytes, dtype=torch.uint8, device=self.device)
+                            if multi_adapter and s.dev_adapted_bytes else None)
             ws = plan.workspace_bytes(max_batch, max_seq)
             self.workspace = torch.empty(ws, dtype=torch.uint8, device=self.device)
             # streams: NULL -> the ctx creates five distinct non-blocking streams (torch's stream pool
@@ -86,6 +90,8 @@ class RankEngine:
         self.bufs.weights_cap = self.weights.numel()
         self.bufs.adapters = self.adapters.data_ptr() if s.dev_adapter_bytes else None
         self.bufs.adapters_cap = s.dev_adapter_bytes
+        self.bufs.adapted = self.adapted.data_ptr() if self.adapted is not None else None
+        self.bufs.adapted_cap = self.adapted.numel() if self.adapted is not None else 0
         self.bufs.workspace = self.workspace.data_ptr()
         self.bufs.workspace_cap = self.workspace.numel()
         self.bufs.max_batch = max_batch
@@ -125,8 +131,11 @@ class RankEngine:
             self.adapters.fill_(0xFF)
             torch.cuda.synchronize(self.device)
 
-    def enqueue(self, epoch: int, tokens: Optional[np.ndarray], batch: int, seq: int, adapter_id: int = 0):
-        """Enqueue a1..a5 for this rank (non-blocking). tokens [batch, seq] int32 (needed on rank 0)."""
+    def enqueue(self, epoch: int, tokens: Optional[np.ndarray], batch: int, seq: int, adapter_id: int = 0,
+                adapter_of_seq=None):
+        """Enqueue a1..a5 for this rank (non-blocking). tokens [batch, seq] int32 (needed on rank 0).
+        adapter_id: adapter merged in place, -1 none, B.PB_MERGE_ALL: all adapters out of place, with
+        adapter_of_seq[b] choosing each sequence's adapter (every rank passes the same list)."""
         self._batch = batch
         with torch.cuda.device(self.device):
             B.pb_trial_begin(self.ctx, epoch)
@@ -138,7 +147,11 @@ class RankEngine:
                 self._tok = np.ascontiguousarray(tokens, dtype=np.int32)
                 assert self._tok.shape == (batch, seq)
                 tp = self._tok.ctypes.data
-            B.pb_prefill_enqueue(self.ctx, tp, batch, seq)
+            if adapter_of_seq is None:
+                B.pb_prefill_enqueue(self.ctx, tp, batch, seq)
+            else:
+                self._aos = np.ascontiguousarray(adapter_of_seq, dtype=np.int32)
+                B.pb_prefill_enqueue_ex(self.ctx, tp, self._aos.ctypes.data, batch, seq)
 
     def wait(self, want_logits: bool = False):
         """Block until this rank's trial is done; rank 0 returns (tokens[B], logits[B, V] | None)."""

@@ -225,6 +225,20 @@ extern "C" pb_status pb_plan_create(const pb_model_desc* model, const pb_adapter
         }
     }
     p->host_adapter_bytes = round_up(aoff, kAlign);
+    // Out-of-place copies for multi-adapter serving (not part of the canonical dump).
+    {
+        const size_t NT = p->tensors.size();
+        p->adapted_off.assign(p->adapters.size() * NT, -1);
+        int64_t off = 0;
+        for (size_t a = 0; a < p->adapters.size(); ++a)
+            for (auto& mr : p->merges)
+                if (mr.adapter == (int32_t)a && p->adapted_off[a * NT + mr.base] < 0) {
+                    off = round_up(off, kAlign);
+                    p->adapted_off[a * NT + mr.base] = off;
+                    off += p->tensors[mr.base].bytes();
+                }
+        p->dev_adapted_bytes = round_up(off, kAlign);
+    }
 
     // Step 3: pieces -> chunks (global ids: base tensors in table order, then adapter factors).
     std::vector<std::vector<int32_t>> base_chunks(p->tensors.size()), ad_chunks(p->atensors.size());
@@ -403,6 +417,7 @@ extern "C" pb_status pb_plan_sizes(const pb_plan* p, pb_plan_sizes_t* out) {
     out->host_adapter_bytes = p->host_adapter_bytes;
     out->dev_weight_bytes = p->dev_weight_bytes;
     out->dev_adapter_bytes = p->host_adapter_bytes;
+    out->dev_adapted_bytes = p->dev_adapted_bytes;
     out->n_tensors = (int32_t)p->tensors.size();
     out->n_atensors = (int32_t)p->atensors.size();
     out->n_chunks = (int32_t)p->chunks.size();

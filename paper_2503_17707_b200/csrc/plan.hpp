@@ -63,6 +63,10 @@ struct pb_plan {
     std::vector<int32_t> own;
     std::vector<pb::MergeRec> merges;
     int64_t host_base_bytes = 0, host_adapter_bytes = 0, dev_weight_bytes = 0;
+    // Multi-adapter (out-of-place) merges: a full copy of every base tensor an adapter modifies, per adapter,
+    // in a separate device region. adapted_off[a * n_tensors + t] = offset, or -1 when adapter a does not touch t.
+    std::vector<int64_t> adapted_off;
+    int64_t dev_adapted_bytes = 0;
 
     // derived helpers
     int32_t head_dim() const { return model.d_model / model.n_heads; }

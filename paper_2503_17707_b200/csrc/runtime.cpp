@@ -105,7 +105,7 @@ WsLayout pb::ws_layout(const pb_plan* p, int32_t batch, int32_t seq) {
     L.max_seq = seq;
     L.f_chunk = 0;
     L.f_act = (int32_t)p->chunks.size();
-    L.f_y = L.f_act + k;
+    L.f_y = L.f_act + k * batch;   // one activation word per (microbatch, prompt chunk)
     L.f_logit = L.f_y + 1;
     L.f_land = L.f_logit + p->n_gpus;
     L.f_tensor = L.f_land + (int32_t)p->chunks.size();
@@ -145,6 +145,7 @@ static pb_status build_merge_jobs(pb_ctx* c) {
     const pb_plan* p = c->plan;
     c->jobs_of_chunk.assign(p->chunks.size(), {});
     char err[512];
+    const size_t NT = p->tensors.size();
     // adapter chunks of each atensor
     std::vector<std::vector<int32_t>> achunks(p->atensors.size());
     for (auto& ch : p->chunks)
@@ -160,22 +161,27 @@ static pb_status build_merge_jobs(pb_ctx* c) {
             if (rb <= ra) continue;
             if (rank % 8 != 0)
                 return fail(PB_EUNSUPPORTED, "merge needs rank %% 8 == 0 (TMA 16-byte row pitch), got %d", rank);
-            MergeJob j;
-            j.chunk = ch.id;
-            j.adapter = mr.adapter;
-            j.rows = rb - ra;
-            j.cols = mr.cols;
-            j.rank = rank;
-            j.scale = p->adapters[mr.adapter].alpha / (float)rank;
-            j.need = achunks[mr.a_tensor];
-            j.need.insert(j.need.end(), achunks[mr.b_tensor].begin(), achunks[mr.b_tensor].end());
-            char* W = c->weights + bt.dev_off + (int64_t)ra * bt.row_bytes();
-            const char* Bp = c->adapters + Bf.off + (int64_t)(ra - mr.row0) * Bf.row_bytes();
-            const char* Ap = c->adapters + A.off;
-            if (!make_merge_maps(&j.maps, W, bt.cols, j.rows, j.cols, Bp, Ap, rank, err, sizeof err))
-                return fail(PB_EINVAL, "merge map: %s", err);
-            c->jobs_of_chunk[ch.id].push_back((int32_t)c->jobs.size());
-            c->jobs.push_back(j);
+            for (int inplace = 1; inplace >= 0; --inplace) {
+                if (!inplace && !c->adapted) continue;
+                MergeJob j;
+                j.chunk = ch.id;
+                j.adapter = mr.adapter;
+                j.inplace = inplace != 0;
+                j.rows = rb - ra;
+                j.cols = mr.cols;
+                j.rank = rank;
+                j.scale = p->adapters[mr.adapter].alpha / (float)rank;
+                j.need = achunks[mr.a_tensor];
+                j.need.insert(j.need.end(), achunks[mr.b_tensor].begin(), achunks[mr.b_tensor].end());
+                char* tbase = inplace ? c->weights + bt.dev_off : c->adapted + p->adapted_off[mr.adapter * NT + mr.base];
+                char* W = tbase + (int64_t)ra * bt.row_bytes();
+                const char* Bp = c->adapters + Bf.off + (int64_t)(ra - mr.row0) * Bf.row_bytes();
+                const char* Ap = c->adapters + A.off;
+                if (!make_merge_maps(&j.maps, W, bt.cols, j.rows, j.cols, Bp, Ap, rank, err, sizeof err))
+                    return fail(PB_EINVAL, "merge map: %s", err);
+                c->jobs_of_chunk[ch.id].push_back((int32_t)c->jobs.size());
+                c->jobs.push_back(j);
+            }
         }
     }
     return PB_OK;
@@ -225,24 +231,28 @@ static pb_status build_prefill_maps(pb_ctx* c) {
         !make_map_bf16(&c->map_attn, c->ws + c->L.attn, R, qd, qd, 128, 64, 128, err, sizeof err) ||
         !make_map_bf16(&c->map_mlp, c->ws + c->L.mlp, R, f, f, 128, 64, 128, err, sizeof err))
         return fail(PB_EINVAL, "activation map: %s", err);
+    const bool opt = m.arch == PB_ARCH_OPT;
+    const size_t NT = p->tensors.size();
+    const int A = c->adapted ? (int)p->adapters.size() : 0;
     c->lmaps.assign(m.n_layers, LayerMaps{});
+    c->lmaps_ad.assign(A, std::vector<LayerMaps>(m.n_layers, LayerMaps{}));
     const auto st = p->stages[c->rank];
     for (int l = st.first; l < st.second; ++l) {
-        auto T = [&](const char* s) -> const TensorRec& {
-            return p->tensors[p->find_tensor("L" + std::to_string(l) + "." + s)];
-        };
-        const bool opt = m.arch == PB_ARCH_OPT;
-        const TensorRec& q = T("qkv");
-        const TensorRec& o = T("o");
-        const TensorRec& up = T(opt ? "fc1" : "gate_up");
-        const TensorRec& dn = T(opt ? "fc2" : "down");
-        LayerMaps& lm = c->lmaps[l];
-        if (!make_map_bf16(&lm.qkv, c->weights + q.dev_off, q.rows, q.cols, q.cols, 128, 64, 128, err, sizeof err) ||
-            !make_map_bf16(&lm.o, c->weights + o.dev_off, o.rows, o.cols, o.cols, 128, 64, 128, err, sizeof err) ||
-            !make_map_bf16(&lm.up, c->weights + up.dev_off, up.rows, up.cols, up.cols, opt ? 128 : 64, 64, 128, err,
-                           sizeof err) ||
-            !make_map_bf16(&lm.down, c->weights + dn.dev_off, dn.rows, dn.cols, dn.cols, 128, 64, 128, err, sizeof err))
-            return fail(PB_EINVAL, "weight map layer %d: %s", l, err);
+        auto tid = [&](const char* s) { return p->find_tensor("L" + std::to_string(l) + "." + s); };
+        const int32_t ids[4] = {tid("qkv"), tid("o"), tid(opt ? "fc1" : "gate_up"), tid(opt ? "fc2" : "down")};
+        // adapter -1: base weights; a >= 0: adapter a's out-of-place copy where it has one, else the base
+        for (int a = -1; a < A; ++a) {
+            LayerMaps& lm = a < 0 ? c->lmaps[l] : c->lmaps_ad[a][l];
+            CUtensorMap* maps[4] = {&lm.qkv, &lm.o, &lm.up, &lm.down};
+            for (int i = 0; i < 4; ++i) {
+                const TensorRec& t = p->tensors[ids[i]];
+                const int64_t off = a >= 0 ? p->adapted_off[a * NT + ids[i]] : -1;
+                const char* base = off >= 0 ? c->adapted + off : c->weights + t.dev_off;
+                const uint32_t box_rows = (i == 2 && !opt) ? 64 : 128;   // [gate; up] is read as 64 + 64 rows
+                if (!make_map_bf16(maps[i], base, t.rows, t.cols, t.cols, box_rows, 64, 128, err, sizeof err))
+                    return fail(PB_EINVAL, "weight map layer %d: %s", l, err);
+            }
+        }
     }
     return PB_OK;
 }
@@ -279,6 +289,9 @@ extern "C" pb_status pb_ctx_create(const pb_plan* plan, int32_t rank, const void
     c->weights = static_cast<char*>(bufs->weights);
     c->adapters = static_cast<char*>(bufs->adapters);
     c->ws = static_cast<char*>(bufs->workspace);
+    if (plan->adapters.size() > 0 && bufs->adapted && bufs->adapted_cap >= plan->dev_adapted_bytes &&
+        plan->dev_adapted_bytes > 0)
+        c->adapted = static_cast<char*>(bufs->adapted);
     c->bufs = *bufs;
     c->h2d[0] = (cudaStream_t)bufs->stream_h2d[0];
     c->h2d[1] = (cudaStream_t)bufs->stream_h2d[1];
@@ -591,8 +604,14 @@ extern "C" pb_status pb_merge_lora(pb_ctx* c, int32_t adapter_id) {
     pb_status st = check_ctx(c, "pb_merge_lora");
     if (st) return st;
     if (c->phase != Phase::Loaded) return fail(PB_EPROTOCOL, "pb_merge_lora: call pb_load_shard first");
-    if (adapter_id < -1 || adapter_id >= (int32_t)c->plan->adapters.size())
+    if (adapter_id < PB_MERGE_ALL || adapter_id >= (int32_t)c->plan->adapters.size())
         return fail(PB_EINVAL, "adapter_id %d out of range", adapter_id);
+    if (adapter_id == PB_MERGE_ALL) {
+        if (c->plan->adapters.empty()) return fail(PB_EINVAL, "PB_MERGE_ALL without adapters");
+        if (!c->adapted) return fail(PB_ENOMEM, "PB_MERGE_ALL needs bufs.adapted >= dev_adapted_bytes");
+        if (c->n > 1 && c->plan->opts.policy != PB_LOAD_STAGE)
+            return fail(PB_EUNSUPPORTED, "PB_MERGE_ALL with n_gpus > 1 needs the STAGE policy (stage owner = loader)");
+    }
     c->merge_adapter = adapter_id;
     c->phase = Phase::Merged;
     return PB_OK;
@@ -628,7 +647,10 @@ cudaError_t wait_tensor(pb_ctx* c, int l, const char* sfx) {
 
 // Layer l on token rows [r0, r1) (prompt positions [ta, tb)). On the first prompt chunk each step waits
 // only for the tensors it reads (layout is in compute order), so a layer starts while its tail loads.
-pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, bool first_chunk) {
+// Rows [r0, r1) are absolute workspace rows; attention / RoPE see the B-sequence block that starts at
+// row_base (token-major inside it); adapter >= 0 selects that adapter's out-of-place weight copies.
+pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, bool first_chunk, int row_base,
+                    int adapter) {
     const pb_plan* p = c->plan;
     const auto& m = p->model;
     const bool opt = m.arch == PB_ARCH_OPT;
@@ -641,7 +663,7 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, boo
     __nv_bfloat16* qkv = reinterpret_cast<__nv_bfloat16*>(c->ws + L.qkv + L.qkv_stride * li);
     __nv_bfloat16* attn = reinterpret_cast<__nv_bfloat16*>(c->ws + L.attn);
     __nv_bfloat16* mlp = reinterpret_cast<__nv_bfloat16*>(c->ws + L.mlp);
-    const LayerMaps& lm = c->lmaps[l];
+    const LayerMaps& lm = adapter >= 0 ? c->lmaps_ad[adapter][l] : c->lmaps[l];
     cudaStream_t s = c->comp;
     const int rows = r1 - r0;
     auto G = [&](int M_begin, int N, int K, int epi, const __nv_bfloat16* bias, int relu, float scale, int scale_cols,
@@ -687,13 +709,14 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, boo
     CU(gemm(c->map_x, lm.qkv, a, qdim));
     if (!opt) {
         const int pi = prof_begin(c, K_ROPE, s);
-        CU(launch_rope(qkv, qdim, r0, r1, B, H, KVH, hd, qd, reinterpret_cast<const float2*>(c->ws + L.rope), s));
+        CU(launch_rope(qkv + (size_t)row_base * qdim, qdim, r0 - row_base, r1 - row_base, B, H, KVH, hd, qd,
+                       reinterpret_cast<const float2*>(c->ws + L.rope), s));
         prof_end(c, pi, s, 6.0 * rows * (qd + kvd) / 2, 4.0 * rows * (qd + kvd));
     }
     {
         const int pi = prof_begin(c, K_ATTN, s);
-        CU(launch_attention(qkv, qdim, attn, qd, ta, tb, B, H, KVH, hd, qd, qd + kvd,
-                            opt ? 1.0f : 1.0f / sqrtf((float)hd), s));
+        CU(launch_attention(qkv + (size_t)row_base * qdim, qdim, attn + (size_t)row_base * qd, qd, ta, tb, B, H, KVH,
+                            hd, qd, qd + kvd, opt ? 1.0f : 1.0f / sqrtf((float)hd), s));
         // causal pairs: sum over queries t in [ta, tb) of (t + 1) keys
         const double pairs = (double)B * ((double)tb * (tb + 1) / 2 - (double)ta * (ta + 1) / 2);
         prof_end(c, pi, s, 4.0 * pairs * H * hd, 2.0 * rows * qd * 2 + 2.0 * B * tb * 2 * kvd);
@@ -772,7 +795,7 @@ struct Budget {
 
 enum ItemKind { I_PROLOGUE, I_EMBED, I_WAITACT, I_LAYER, I_PUSH, I_FINAL, I_HEAD, I_ARGMAX, I_DONE };
 struct Item {
-    int kind, j, l;
+    int kind, mb, j, l;
     std::vector<int32_t> prereq;   // tensors whose readiness-word writer must already be issued
 };
 
@@ -780,6 +803,8 @@ struct Issuer {
     pb_ctx* c;
     int B, T, k;
     bool replay;
+    bool mb_mode;   // PB_MERGE_ALL: every sequence is its own microbatch with its own adapter
+    int n_mb;
     std::vector<int> tb;
     std::vector<Item> items;
     std::vector<char> tensor_issued, adapter_waited;
@@ -811,9 +836,20 @@ pb_status issue_group(Issuer& I, size_t gi) {
         if (ch.is_adapter) continue;
         CU(cudaStreamWaitEvent(c->merge, landed_ev(c, id), 0));
         ++mops;
+        const bool all = c->merge_adapter == PB_MERGE_ALL;
+        if (all) {   // out of place: start every adapter's copy of this chunk from the base bytes
+            const size_t NT = p->tensors.size();
+            for (size_t a = 0; a < p->adapters.size(); ++a) {
+                const int64_t off = p->adapted_off[a * NT + ch.tensor];
+                if (off < 0) continue;
+                CU(cudaMemcpyAsync(c->adapted + off + (int64_t)ch.r0 * p->tensors[ch.tensor].row_bytes(),
+                                   c->weights + ch.dev_off, ch.bytes, cudaMemcpyDeviceToDevice, c->merge));
+                ++mops;
+            }
+        }
         for (int32_t j : c->jobs_of_chunk[id]) {
             const MergeJob& job = c->jobs[j];
-            if (job.adapter != c->merge_adapter) continue;
+            if (all ? job.inplace : (!job.inplace || job.adapter != c->merge_adapter)) continue;
             for (int32_t a : job.need)
                 if (!I.adapter_waited[a]) {
                     CU(cudaStreamWaitEvent(c->merge, landed_ev(c, a), 0));
@@ -851,7 +887,7 @@ long group_merge_ops(Issuer& I, size_t gi) {
     long n = 0;
     for (int32_t i = g.first; i < g.first + g.count; ++i) {
         const int32_t id = c->plan->load[c->rank][i];
-        n += 6 + (long)c->jobs_of_chunk[id].size() * (5 + prof_ops(c));
+        n += 6 + (long)c->plan->adapters.size() + (long)c->jobs_of_chunk[id].size() * (5 + prof_ops(c));
     }
     return n;
 }
@@ -884,40 +920,43 @@ void build_items(Issuer& I) {
     const bool opt = p->model.arch == PB_ARCH_OPT;
     const int g = c->rank, N = c->n;
     const auto stage = p->stages[g];
-    auto add = [&](int kind, int j, int l, std::vector<int32_t> pre) {
+    auto add = [&](int kind, int mb, int j, int l, std::vector<int32_t> pre) {
         if (I.replay) pre.clear();
-        I.items.push_back(Item{kind, j, l, std::move(pre)});
+        I.items.push_back(Item{kind, mb, j, l, std::move(pre)});
     };
-    add(I_PROLOGUE, 0, 0, {});
-    for (int j = 0; j < I.k; ++j) {
-        if (g == 0) {
-            std::vector<int32_t> pre;
-            if (j == 0) {
-                const int32_t et = p->find_tensor("embed");
-                if (c->last_own_chunk[et] >= 0) pre.push_back(et);
-                if (opt) pre.push_back(p->find_tensor("pos"));
+    add(I_PROLOGUE, 0, 0, 0, {});
+    for (int mb = 0; mb < I.n_mb; ++mb) {
+        for (int j = 0; j < I.k; ++j) {
+            const bool first = mb == 0 && j == 0;
+            if (g == 0) {
+                std::vector<int32_t> pre;
+                if (first) {
+                    const int32_t et = p->find_tensor("embed");
+                    if (c->last_own_chunk[et] >= 0) pre.push_back(et);
+                    if (opt) pre.push_back(p->find_tensor("pos"));
+                }
+                add(I_EMBED, mb, j, 0, pre);
+            } else {
+                add(I_WAITACT, mb, j, 0, {});
             }
-            add(I_EMBED, j, 0, pre);
-        } else {
-            add(I_WAITACT, j, 0, {});
+            for (int l = stage.first; l < stage.second; ++l) {
+                std::vector<int32_t> pre;
+                if (first)
+                    for (size_t t = 0; t < p->tensors.size(); ++t)
+                        if (p->tensors[t].layer == l) pre.push_back((int32_t)t);
+                add(I_LAYER, mb, j, l, pre);
+            }
+            if (g < N - 1) add(I_PUSH, mb, j, 0, {});
         }
-        for (int l = stage.first; l < stage.second; ++l) {
-            std::vector<int32_t> pre;
-            if (j == 0)
-                for (size_t t = 0; t < p->tensors.size(); ++t)
-                    if (p->tensors[t].layer == l) pre.push_back((int32_t)t);
-            add(I_LAYER, j, l, pre);
-        }
-        if (g < N - 1) add(I_PUSH, j, 0, {});
     }
     if (g == N - 1) {
         std::vector<int32_t> pre{p->find_tensor("final_g")};
         if (opt) pre.push_back(p->find_tensor("final_b"));
-        add(I_FINAL, 0, 0, pre);
+        add(I_FINAL, 0, 0, 0, pre);
     }
-    if (is_head_owner(p, g)) add(I_HEAD, 0, 0, {head_tensor(p)});
-    if (g == 0) add(I_ARGMAX, 0, 0, {});
-    add(I_DONE, 0, 0, {});
+    if (is_head_owner(p, g)) add(I_HEAD, 0, 0, 0, {head_tensor(p)});
+    if (g == 0) add(I_ARGMAX, 0, 0, 0, {});
+    add(I_DONE, 0, 0, 0, {});
 }
 
 long item_ops(Issuer& I, const Item& it) {
@@ -941,7 +980,12 @@ pb_status issue_item(Issuer& I, const Item& it) {
     __nv_bfloat16* y = reinterpret_cast<__nv_bfloat16*>(c->ws + L.y);
     float* logits = reinterpret_cast<float*>(c->ws + L.logits);
     const int j = it.j;
-    const int r0 = I.tb[j] * B, r1 = I.tb[j + 1] * B;
+    // microbatch mode: sequence it.mb occupies rows [mb*T, (mb+1)*T) (one sequence, Bk = 1);
+    // otherwise all B sequences share the token-major rows t*B + b.
+    const int Bk = I.mb_mode ? 1 : B;
+    const int row_base = I.mb_mode ? it.mb * T : 0;
+    const int r0 = row_base + I.tb[j] * Bk, r1 = row_base + I.tb[j + 1] * Bk;
+    const int act_word = L.f_act + it.mb * I.k + j;
     std::vector<int32_t> owners;
     for (int r = 0; r < N; ++r)
         if (is_head_owner(p, r)) owners.push_back(r);
@@ -983,33 +1027,39 @@ pb_status issue_item(Issuer& I, const Item& it) {
                 E.n = 1;
             }
             const int pi = prof_begin(c, K_EMBED, s);
-            CU(launch_embed(E, opt ? wt(c, -1, "pos") : nullptr, reinterpret_cast<const int32_t*>(c->ws + L.tokens), h,
-                            d, r0, r1, B, s));
+            CU(launch_embed(E, opt ? wt(c, -1, "pos") : nullptr,
+                            reinterpret_cast<const int32_t*>(c->ws + L.tokens) + row_base, h + (size_t)row_base * d, d,
+                            r0 - row_base, r1 - row_base, Bk, s));
             prof_end(c, pi, s, (opt ? 1.0 : 0.0) * (r1 - r0) * d, (r1 - r0) * d * (opt ? 8.0 : 6.0));
             ++c->n_launches;
             break;
         }
         case I_WAITACT:
-            CU(wait_word(c, L.f_act + j, s));
+            CU(wait_word(c, act_word, s));
             break;
         case I_LAYER: {
-            pb_status st = run_layer(c, it.l, r0, r1, I.tb[j], I.tb[j + 1], B, j == 0 && !I.replay);
+            const int adapter = I.mb_mode ? c->seq_adapter[it.mb] : -1;
+            pb_status st = run_layer(c, it.l, r0, r1, I.tb[j], I.tb[j + 1], Bk, it.mb == 0 && j == 0 && !I.replay,
+                                     row_base, adapter);
             if (st) return st;
             break;
         }
         case I_PUSH:
             CU(cudaMemcpyAsync(c->peers[g + 1].ws + L.h + (size_t)r0 * d * 4, h + (size_t)r0 * d,
                                (size_t)(r1 - r0) * d * 4, cudaMemcpyDeviceToDevice, s));
-            CU(signal_ranks(c, L.f_act + j, {g + 1}, s));
+            CU(signal_ranks(c, act_word, {g + 1}, s));
             break;
         case I_FINAL: {
             if (!I.replay) {
                 CU(wait_word(c, L.f_tensor + p->find_tensor("final_g"), s));
                 if (opt) CU(wait_word(c, L.f_tensor + p->find_tensor("final_b"), s));
             }
+            // last position of every sequence: token-major rows (T-1)*B + b, or microbatch rows b*T + T-1
+            const float* last = I.mb_mode ? h + (size_t)(T - 1) * d : h + (size_t)(T - 1) * B * d;
+            const int ldh = I.mb_mode ? T * d : d;
             const int pi = prof_begin(c, K_NORM, s);
-            CU(launch_norm(h + (size_t)(T - 1) * B * d, d, y, d, B, d, wt(c, -1, "final_g"),
-                           opt ? wt(c, -1, "final_b") : nullptr, m.norm_eps, s));
+            CU(launch_norm(last, ldh, y, d, B, d, wt(c, -1, "final_g"), opt ? wt(c, -1, "final_b") : nullptr,
+                           m.norm_eps, s));
             prof_end(c, pi, s, 8.0 * B * d, 6.0 * B * d);
             ++c->n_launches;
             std::vector<int32_t> remote;
@@ -1065,6 +1115,8 @@ pb_status issue_trial(pb_ctx* c, int B, int T, bool replay) {
     I.B = B;
     I.T = T;
     I.replay = replay;
+    I.mb_mode = c->merge_adapter == PB_MERGE_ALL;
+    I.n_mb = I.mb_mode ? B : 1;
     I.k = std::max(1, std::min(p->opts.prefill_chunks, T));
     I.tb.assign(I.k + 1, 0);
     for (int j = 0, t = 0; j <= I.k; ++j) {   // prompt chunk boundaries, remainder to lower chunks
@@ -1134,13 +1186,31 @@ pb_status issue_trial(pb_ctx* c, int B, int T, bool replay) {
     return PB_OK;
 }
 
-pb_status start_issuer(pb_ctx* c, const int32_t* tokens, int32_t B, int32_t T, bool replay) {
+pb_status start_issuer(pb_ctx* c, const int32_t* tokens, const int32_t* adapter_of_seq, int32_t B, int32_t T,
+                       bool replay) {
     if (B < 1 || T < 1 || B > c->L.max_batch || T > c->L.max_seq || (int64_t)B * T > c->L.max_rows)
         return fail(PB_EINVAL, "batch %d x seq %d exceeds the workspace (%d x %d)", B, T, c->L.max_batch, c->L.max_seq);
     if (c->rank == 0 && !tokens) return fail(PB_EINVAL, "rank 0 needs tokens");
+    const bool mb = c->merge_adapter == PB_MERGE_ALL;
+    if (!replay) {
+        c->seq_adapter.assign(B, -1);
+        if (mb) {
+            const int A = (int)c->plan->adapters.size();
+            for (int b = 0; b < B; ++b) {
+                const int a = adapter_of_seq ? adapter_of_seq[b] : b % A;
+                if (a < 0 || a >= A) return fail(PB_EINVAL, "adapter_of_seq[%d] = %d out of range", b, a);
+                c->seq_adapter[b] = a;
+            }
+        } else if (adapter_of_seq) {
+            for (int b = 0; b < B; ++b)
+                if (adapter_of_seq[b] != c->merge_adapter)
+                    return fail(PB_EINVAL, "sequence %d asks for adapter %d but the in-place merge holds %d (use "
+                                           "PB_MERGE_ALL for mixed batches)", b, adapter_of_seq[b], c->merge_adapter);
+        }
+    }
     if (c->rank == 0)
-        for (int b = 0; b < B; ++b)   // token-major rows: row = t * B + b
-            for (int t = 0; t < T; ++t) c->h_tokens[t * B + b] = tokens[(size_t)b * T + t];
+        for (int b = 0; b < B; ++b)   // token-major rows t*B + b; microbatch mode: sequence-major b*T + t
+            for (int t = 0; t < T; ++t) c->h_tokens[mb ? b * T + t : t * B + b] = tokens[(size_t)b * T + t];
     c->cur_batch = B;
     c->cur_seq = T;
     join_load(c);
@@ -1164,7 +1234,15 @@ extern "C" pb_status pb_prefill_enqueue(pb_ctx* c, const int32_t* tokens, int32_
     pb_status st = check_ctx(c, "pb_prefill_enqueue");
     if (st) return st;
     if (c->phase != Phase::Gathered) return fail(PB_EPROTOCOL, "pb_prefill_enqueue: call pb_gather_layers first");
-    return start_issuer(c, tokens, B, T, false);
+    return start_issuer(c, tokens, nullptr, B, T, false);
+}
+
+extern "C" pb_status pb_prefill_enqueue_ex(pb_ctx* c, const int32_t* tokens, const int32_t* adapter_of_seq, int32_t B,
+                                           int32_t T) {
+    pb_status st = check_ctx(c, "pb_prefill_enqueue_ex");
+    if (st) return st;
+    if (c->phase != Phase::Gathered) return fail(PB_EPROTOCOL, "pb_prefill_enqueue_ex: call pb_gather_layers first");
+    return start_issuer(c, tokens, adapter_of_seq, B, T, false);
 }
 
 extern "C" pb_status pb_prefill_replay(pb_ctx* c, uint32_t epoch, const int32_t* tokens, int32_t B, int32_t T) {
@@ -1178,7 +1256,7 @@ extern "C" pb_status pb_prefill_replay(pb_ctx* c, uint32_t epoch, const int32_t*
     c->n_launches = 0;
     c->prof_n = 0;
     CU(cudaEventRecord(c->t0, c->comp));
-    return start_issuer(c, tokens, B, T, true);
+    return start_issuer(c, tokens, nullptr, B, T, true);
 }
 
 extern "C" pb_status pb_prefill_wait(pb_ctx* c, float* logits_out, int32_t* tokens_out) {

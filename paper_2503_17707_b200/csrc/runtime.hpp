@@ -27,6 +27,7 @@ WsLayout ws_layout(const pb_plan* p, int32_t batch, int32_t seq);
 struct MergeJob {
     int32_t chunk;       // base chunk whose rows it updates
     int32_t adapter;
+    bool inplace;        // true: into the base weights; false: into adapter's out-of-place copy
     int32_t rows, cols, rank;
     float scale;
     std::vector<int32_t> need;   // adapter chunks that must have landed
@@ -99,6 +100,10 @@ struct pb_ctx {
     // prefill tensor maps
     CUtensorMap map_x, map_attn, map_mlp;
     std::vector<pb::LayerMaps> lmaps;   // indexed by layer (only this rank's stage is encoded)
+    // multi-adapter (PB_MERGE_ALL): out-of-place copies and per-adapter weight maps [adapter][layer]
+    char* adapted = nullptr;
+    std::vector<std::vector<pb::LayerMaps>> lmaps_ad;
+    std::vector<int32_t> seq_adapter;   // per sequence of the current trial (-1: base / single in-place adapter)
 
     // pinned staging
     int32_t* h_tokens = nullptr;   // [max_rows]
