@@ -76,40 +76,49 @@ def oracle_sample(w, sample_layers: int):
     ow = oracle.OracleWeights(m, ads)
     names = [n for n in ow.tensors if not n.startswith("L") or int(n[1:].split(".")[0]) in ls]
     base = {n: ow.base_bits(n) for n in names}
-    facs = [at for at in ow.atensors if at.adapter == 0 and at.layer in ls]
+    n_ad = len(ads)
+    aos = [b % n_ad for b in range(w.batch)] if n_ad > 1 else [0 if n_ad else None] * w.batch
+    used = sorted({a for a in aos if a is not None})
+    facs = [at for at in ow.atensors if at.adapter in used and at.layer in ls]
     fac_bits = {at.name: ow.adapter_bits(at) for at in facs}
     toks = synth.tokens(w.batch, w.seq, m.vocab)
     import threadpoolctl  # noqa: F401  (numpy BLAS threads = all cores by default)
-    t0 = time.perf_counter()
-    merged = dict(base)
     id2name = {t.id: n for n, t in ow.tensors.items()}
-    by_target = {}
-    for at in facs:
-        by_target.setdefault((at.layer, at.target), {})[at.factor] = at
-    for (l, tgt), f in by_target.items():
-        name = id2name[f["A"].base]
-        W = merged[name].copy()
-        r0, rows = f["A"].row0, f["B"].rows
-        W[r0:r0 + rows] = merge_bf16_bits(W[r0:r0 + rows], fac_bits[f["B"].name], fac_bits[f["A"].name], ads[0].scale)
-        merged[name] = W
+    t0 = time.perf_counter()
+    merged = {a: dict(base) for a in used} if used else {None: dict(base)}
+    for a in used:
+        by_target = {}
+        for at in facs:
+            if at.adapter == a:
+                by_target.setdefault((at.layer, at.target), {})[at.factor] = at
+        for (l, tgt), f in by_target.items():
+            name = id2name[f["A"].base]
+            W = merged[a][name].copy()
+            r0, rows = f["A"].row0, f["B"].rows
+            W[r0:r0 + rows] = merge_bf16_bits(W[r0:r0 + rows], fac_bits[f["B"].name], fac_bits[f["A"].name],
+                                              ads[a].scale)
+            merged[a][name] = W
     t_merge = time.perf_counter() - t0
     wf = {}
 
-    def Wget(n):
-        if n not in wf:
-            x = bf16_bits_to_f64(merged[n])
-            wf[n] = x.reshape(-1) if ow.tensors[n].rows == 1 else x
-        return wf[n]
+    def getter(a):
+        def Wget(n):
+            if (a, n) not in wf:
+                x = bf16_bits_to_f64(merged[a][n])
+                wf[(a, n)] = x.reshape(-1) if ow.tensors[n].rows == 1 else x
+            return wf[(a, n)]
+        return Wget
 
-    for n in merged:   # fp64 views are part of the oracle's data, not its compute
-        Wget(n)
+    for a in merged:   # fp64 views are part of the oracle's data, not its compute
+        for n in merged[a]:
+            getter(a)(n)
     t1 = time.perf_counter()
     for b in range(w.batch):
-        OF.forward_logits(m, Wget, toks[b], "bf16", layers=[])
+        OF.forward_logits(m, getter(aos[b]), toks[b], "bf16", layers=[])
     t_head = time.perf_counter() - t1
     t2 = time.perf_counter()
     for b in range(w.batch):
-        OF.forward_logits(m, Wget, toks[b], "bf16", layers=ls)
+        OF.forward_logits(m, getter(aos[b]), toks[b], "bf16", layers=ls)
     t_all = time.perf_counter() - t2
     per_layer = max(t_all - t_head, 0.0) / len(ls)
     merge_per_layer = t_merge / len(ls)
@@ -316,7 +325,7 @@ def main():
 
     w = WORKLOADS[args.workload]
     if args.policy is None:
-        args.policy = "stage" if world == 1 else "interleave"
+        args.policy = "stage" if (world == 1 or len(w.adapters) > 1) else "interleave"
     if args.vocab_sliced is None:
         args.vocab_sliced = 0 if world == 1 else 1
     if args.prefill_chunks is None:
@@ -342,8 +351,11 @@ def main():
         shm_paths = [f"{tag}_{k}" for k, _ in sizes]
         base, ada = bufs["base"], bufs["ada"]
 
+    multi = len(w.adapters) > 1   # C3: several adapters share the base, one sequence per adapter (PB_MERGE_ALL)
     eng = RankEngine(plan, rank, base, ada if plan.sizes.host_adapter_bytes else None, max_batch=w.batch,
-                     max_seq=w.seq)
+                     max_seq=w.seq, multi_adapter=multi)
+    adapter_id = B.PB_MERGE_ALL if multi else (0 if w.adapters else -1)
+    aos = [b % len(w.adapters) for b in range(w.batch)] if multi else None
     if world > 1:
         blobs = [None] * world
         dist.all_gather_object(blobs, eng.export())
@@ -367,8 +379,9 @@ def main():
         barrier()
         torch.cuda.synchronize()
         th0 = time.perf_counter()
-        res = eng.cold_start(2 * step + 1, toks if rank == 0 else None, w.batch, w.seq,
-                             adapter_id=0 if w.adapters else -1)
+        eng.enqueue(2 * step + 1, toks if rank == 0 else None, w.batch, w.seq, adapter_id=adapter_id,
+                    adapter_of_seq=aos)
+        res = eng.wait()
         th1 = time.perf_counter()
         barrier()
         torch.cuda.synchronize()

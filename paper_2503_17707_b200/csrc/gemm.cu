@@ -287,6 +287,14 @@ int gemm_split_k(int N, int K, int epi) {
     return S;
 }
 
+cudaError_t warm_gemm_kernels() {
+    cudaFuncAttributes a;
+    cudaError_t e = cudaFuncGetAttributes(&a, gemm_kernel<EPI_BF16>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, gemm_kernel<EPI_RESID>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, gemm_kernel<EPI_SILU_MUL>);
+    return e;
+}
+
 cudaError_t launch_gemm(const CUtensorMap& mapX, const CUtensorMap& mapW, const GemmArgs& a, cudaStream_t s) {
     if (a.M_end <= a.M_begin || a.N <= 0) return cudaSuccess;
     if (a.K <= 0 || a.K % 8) return cudaErrorInvalidValue;

@@ -30,11 +30,13 @@ cudaError_t launch_signal(const SignalTargets& t, uint32_t value, cudaStream_t s
 // Maps: mapW box {64 cols, 128 rows} SW128; mapB box {rk, 128} with swizzle rk*2 bytes; mapA box {64, rk} SW128,
 // rk = r rounded up to 16 / 32 / 64 (zero-filled by TMA out of bounds).
 struct MergeMaps {
-    CUtensorMap W, B, A;
+    CUtensorMap W, B, A, Wout;   // Wout: destination (== W in place; an adapter's copy out of place)
 };
 int merge_rk(int rank);  // padded K of the merge MMA (16, 32 or 64)
 bool make_merge_maps(MergeMaps* m, void* W, int64_t ldw, int rows, int cols, const void* B, const void* A, int rank,
-                     char* err, size_t errlen);
+                     char* err, size_t errlen, void* Wout = nullptr);
+// SM byte copy (16-B vectors; falls back to cudaMemcpyAsync for unaligned spans).
+cudaError_t launch_copy(void* dst, const void* src, int64_t bytes, cudaStream_t s);
 cudaError_t launch_merge(const MergeMaps& maps, int rows, int cols, int rank, float scale, cudaStream_t s);
 
 // ---------------------------------------------------------------- prefill GEMM (tcgen05)
@@ -93,5 +95,12 @@ cudaError_t launch_logits(const __nv_bfloat16* y, int B, int d, const __nv_bfloa
 // tokens[b] = argmax_v logits[b, v] (lowest index on ties); *nan_flag |= 1 if any logit is not finite.
 cudaError_t launch_argmax(const float* logits, int B, int V, int ldl, int32_t* tokens, int32_t* nan_flag,
                           cudaStream_t s);
+
+// Load every kernel of the library into the current context (CUDA lazy module loading otherwise loads a
+// function at its first launch; concurrent first launches from several issuer threads were measured to
+// deadlock). Called once per device from pb_ctx_create.
+cudaError_t warm_merge_kernels();
+cudaError_t warm_gemm_kernels();
+cudaError_t warm_simt_kernels();
 
 }  // namespace pb

@@ -14,6 +14,8 @@
 // contraction into a handful of instructions so the SMs only stream W.
 #include <cuda_bf16.h>
 
+#include <algorithm>
+
 #include "kernels.hpp"
 #include "sm100.cuh"
 
@@ -39,7 +41,8 @@ struct MergeSmem {
 template <int RK>
 __global__ void __launch_bounds__(128) merge_kernel(const __grid_constant__ CUtensorMap mapW,
                                                     const __grid_constant__ CUtensorMap mapB,
-                                                    const __grid_constant__ CUtensorMap mapA, float scale) {
+                                                    const __grid_constant__ CUtensorMap mapA,
+                                                    const __grid_constant__ CUtensorMap mapWout, float scale) {
     using S = MergeSmem<RK>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -124,8 +127,8 @@ __global__ void __launch_bounds__(128) merge_kernel(const __grid_constant__ CUte
     tc_fence_before();
     __syncthreads();
     if (tid == 0) {
-        tma_store_2d(&mapW, sW, n0, m0);
-        tma_store_2d(&mapW, sW + kWBytes / 2, n0 + 64, m0);
+        tma_store_2d(&mapWout, sW, n0, m0);                 // in place: mapWout == mapW
+        tma_store_2d(&mapWout, sW + kWBytes / 2, n0 + 64, m0);
         tma_store_commit();
         tma_store_wait_all();
     }
@@ -144,7 +147,7 @@ cudaError_t launch_rk(const MergeMaps& m, int rows, int cols, float scale, cudaS
     cudaError_t e = cudaFuncSetAttribute(merge_kernel<RK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     dim3 grid((cols + kTile - 1) / kTile, (rows + kTile - 1) / kTile);
-    merge_kernel<RK><<<grid, 128, smem, s>>>(m.W, m.B, m.A, scale);
+    merge_kernel<RK><<<grid, 128, smem, s>>>(m.W, m.B, m.A, m.Wout, scale);
     return cudaGetLastError();
 }
 
@@ -153,9 +156,10 @@ cudaError_t launch_rk(const MergeMaps& m, int rows, int cols, float scale, cudaS
 int merge_rk(int rank) { return rank <= 16 ? 16 : (rank <= 32 ? 32 : 64); }
 
 bool make_merge_maps(MergeMaps* m, void* W, int64_t ldw, int rows, int cols, const void* B, const void* A, int rank,
-                     char* err, size_t errlen) {
+                     char* err, size_t errlen, void* Wout) {
     const int rk = merge_rk(rank);
     return make_map_bf16(&m->W, W, rows, cols, ldw, 128, 64, 128, err, errlen) &&
+           make_map_bf16(&m->Wout, Wout ? Wout : W, rows, cols, ldw, 128, 64, 128, err, errlen) &&
            make_map_bf16(&m->B, B, rows, rank, rank, 128, rk, rk * 2, err, errlen) &&
            make_map_bf16(&m->A, A, rank, cols, cols, rk, 64, 128, err, errlen);
 }
@@ -167,6 +171,33 @@ cudaError_t launch_merge(const MergeMaps& m, int rows, int cols, int rank, float
         case 32: return launch_rk<32>(m, rows, cols, scale, s);
         default: return launch_rk<64>(m, rows, cols, scale, s);
     }
+}
+
+// Device-to-device byte copy on the SMs (16-byte vectors, grid-stride): used for the rows of a tensor an
+// adapter does not touch when building its out-of-place copy, so the copy engine stays free for the PCIe load.
+__global__ void __launch_bounds__(256) copy16_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
+cudaError_t launch_copy(void* dst, const void* src, int64_t bytes, cudaStream_t s) {
+    if (bytes <= 0) return cudaSuccess;
+    if ((bytes & 15) || (reinterpret_cast<uintptr_t>(dst) & 15) || (reinterpret_cast<uintptr_t>(src) & 15))
+        return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s);
+    const int64_t n = bytes / 16;
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    copy16_kernel<<<blocks, 256, 0, s>>>(static_cast<uint4*>(dst), static_cast<const uint4*>(src), n);
+    return cudaGetLastError();
+}
+
+// Force-load the module functions (CUDA lazy loading): see warm_kernels().
+cudaError_t warm_merge_kernels() {
+    cudaFuncAttributes a;
+    cudaError_t e = cudaFuncGetAttributes(&a, merge_kernel<16>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, merge_kernel<32>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, merge_kernel<64>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, copy16_kernel);
+    return e;
 }
 
 }  // namespace pb

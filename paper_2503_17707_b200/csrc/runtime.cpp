@@ -18,6 +18,8 @@
 #include <chrono>
 #include <cmath>
 #include <deque>
+#include <mutex>
+#include <set>
 #include <cstring>
 #include <cstdio>
 #include <cstdlib>
@@ -173,11 +175,13 @@ static pb_status build_merge_jobs(pb_ctx* c) {
                 j.scale = p->adapters[mr.adapter].alpha / (float)rank;
                 j.need = achunks[mr.a_tensor];
                 j.need.insert(j.need.end(), achunks[mr.b_tensor].begin(), achunks[mr.b_tensor].end());
-                char* tbase = inplace ? c->weights + bt.dev_off : c->adapted + p->adapted_off[mr.adapter * NT + mr.base];
-                char* W = tbase + (int64_t)ra * bt.row_bytes();
+                char* W = c->weights + bt.dev_off + (int64_t)ra * bt.row_bytes();
+                char* Wout = inplace ? W
+                                     : c->adapted + p->adapted_off[mr.adapter * NT + mr.base] +
+                                           (int64_t)ra * bt.row_bytes();
                 const char* Bp = c->adapters + Bf.off + (int64_t)(ra - mr.row0) * Bf.row_bytes();
                 const char* Ap = c->adapters + A.off;
-                if (!make_merge_maps(&j.maps, W, bt.cols, j.rows, j.cols, Bp, Ap, rank, err, sizeof err))
+                if (!make_merge_maps(&j.maps, W, bt.cols, j.rows, j.cols, Bp, Ap, rank, err, sizeof err, Wout))
                     return fail(PB_EINVAL, "merge map: %s", err);
                 c->jobs_of_chunk[ch.id].push_back((int32_t)c->jobs.size());
                 c->jobs.push_back(j);
@@ -280,6 +284,20 @@ extern "C" pb_status pb_ctx_create(const pb_plan* plan, int32_t rank, const void
         return fail(PB_ENOMEM, "workspace: need %lld bytes", (long long)L.total);
     char err[256];
     if (!driver_init(err, sizeof err)) return fail(PB_ECUDA, "%s", err);
+    {
+        static std::mutex warm_mu;
+        static std::set<int> warmed;
+        std::lock_guard<std::mutex> lk(warm_mu);
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (!warmed.count(dev)) {
+            cudaError_t e = warm_merge_kernels();
+            if (e == cudaSuccess) e = warm_gemm_kernels();
+            if (e == cudaSuccess) e = warm_simt_kernels();
+            if (e != cudaSuccess) return fail(PB_ECUDA, "kernel load: %s", cudaGetErrorString(e));
+            warmed.insert(dev);
+        }
+    }
 
     auto* c = new pb_ctx();
     c->plan = plan;
@@ -816,6 +834,8 @@ int prof_ops(pb_ctx* c) { return c->profiling ? 2 : 0; }
 // ---- loads and merges of one copy group
 pb_status issue_group(Issuer& I, size_t gi) {
     pb_ctx* c = I.c;
+    if (getenv("PB_DEBUG_ISSUER") && atoi(getenv("PB_DEBUG_ISSUER")) >= 2)
+        fprintf(stderr, "[pb r%d] group %zu\n", c->rank, gi);
     const pb_plan* p = c->plan;
     const CopyGroup& g = c->copies[gi];
     const auto& ld = p->load[c->rank];
@@ -837,14 +857,29 @@ pb_status issue_group(Issuer& I, size_t gi) {
         CU(cudaStreamWaitEvent(c->merge, landed_ev(c, id), 0));
         ++mops;
         const bool all = c->merge_adapter == PB_MERGE_ALL;
-        if (all) {   // out of place: start every adapter's copy of this chunk from the base bytes
+        if (all) {   // out of place: rows of the chunk no merge of adapter a writes are copied on the SMs
             const size_t NT = p->tensors.size();
+            const TensorRec& t = p->tensors[ch.tensor];
             for (size_t a = 0; a < p->adapters.size(); ++a) {
                 const int64_t off = p->adapted_off[a * NT + ch.tensor];
                 if (off < 0) continue;
-                CU(cudaMemcpyAsync(c->adapted + off + (int64_t)ch.r0 * p->tensors[ch.tensor].row_bytes(),
-                                   c->weights + ch.dev_off, ch.bytes, cudaMemcpyDeviceToDevice, c->merge));
-                ++mops;
+                std::vector<std::pair<int32_t, int32_t>> cover;
+                for (auto& mr : p->merges)
+                    if (mr.adapter == (int32_t)a && mr.base == ch.tensor) cover.push_back({mr.row0, mr.row0 + mr.rows});
+                std::sort(cover.begin(), cover.end());
+                int32_t r = ch.r0;
+                auto copy_rows = [&](int32_t r_a, int32_t r_b) -> cudaError_t {
+                    if (r_b <= r_a) return cudaSuccess;
+                    ++mops;
+                    return launch_copy(c->adapted + off + (int64_t)r_a * t.row_bytes(),
+                                       c->weights + t.dev_off + (int64_t)r_a * t.row_bytes(),
+                                       (int64_t)(r_b - r_a) * t.row_bytes(), c->merge);
+                };
+                for (auto& cv : cover) {
+                    CU(copy_rows(r, std::min(cv.first, ch.r1)));
+                    r = std::max(r, std::min(cv.second, ch.r1));
+                }
+                CU(copy_rows(r, ch.r1));
             }
         }
         for (int32_t j : c->jobs_of_chunk[id]) {
@@ -894,6 +929,8 @@ long group_merge_ops(Issuer& I, size_t gi) {
 
 pb_status issue_recv(Issuer& I, size_t ri) {
     pb_ctx* c = I.c;
+    if (getenv("PB_DEBUG_ISSUER") && atoi(getenv("PB_DEBUG_ISSUER")) >= 2)
+        fprintf(stderr, "[pb r%d] recv %zu\n", c->rank, ri);
     const int32_t id = c->plan->recv[c->rank][ri];
     const ChunkRec& ch = c->plan->chunks[id];
     CU(wait_word(c, c->L.f_chunk + id, c->nv));
@@ -968,8 +1005,14 @@ long item_ops(Issuer& I, const Item& it) {
     }
 }
 
+static bool issuer_trace() {
+    static const bool on = getenv("PB_DEBUG_ISSUER") && atoi(getenv("PB_DEBUG_ISSUER")) >= 2;
+    return on;
+}
+
 pb_status issue_item(Issuer& I, const Item& it) {
     pb_ctx* c = I.c;
+    if (issuer_trace()) fprintf(stderr, "[pb r%d] item kind=%d mb=%d j=%d l=%d\n", c->rank, it.kind, it.mb, it.j, it.l);
     const pb_plan* p = c->plan;
     const auto& m = p->model;
     const bool opt = m.arch == PB_ARCH_OPT;
@@ -1265,6 +1308,51 @@ extern "C" pb_status pb_prefill_wait(pb_ctx* c, float* logits_out, int32_t* toke
     if (c->phase != Phase::Prefilled) return fail(PB_EPROTOCOL, "pb_prefill_wait: nothing enqueued");
     join_load(c);
     if (c->issue_status != PB_OK) return fail(c->issue_status, "issuer: %s", c->issue_msg);
+    // Optional watchdog (PB_WAIT_TIMEOUT_S): poll instead of blocking; on timeout report which streams are
+    // stuck and which readiness words are still below the epoch, and return PB_ECUDA instead of hanging.
+    static const char* wt_env = getenv("PB_WAIT_TIMEOUT_S");
+    if (wt_env) {
+        const double limit = atof(wt_env);
+        const auto t_start = std::chrono::steady_clock::now();
+        for (;;) {
+            cudaError_t q = cudaEventQuery(c->done);
+            if (q == cudaSuccess) break;
+            if (q != cudaErrorNotReady) CU(q);
+            if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count() > limit) {
+                cudaStream_t ss[] = {c->h2d[0], c->merge, c->nv, c->comp};
+                const char* nm[] = {"h2d", "merge", "nvlink", "compute"};
+                char msg[1024];
+                int o = snprintf(msg, sizeof msg, "rank %d: prefill not done after %.0f s; streams:", c->rank, limit);
+                for (int i = 0; i < 4; ++i)
+                    o += snprintf(msg + o, sizeof msg - o, " %s=%s", nm[i],
+                                  cudaStreamQuery(ss[i]) == cudaSuccess ? "idle" : "busy");
+                std::vector<uint32_t> w(c->L.n_words);
+                cudaStream_t probe;
+                if (cudaStreamCreateWithFlags(&probe, cudaStreamNonBlocking) == cudaSuccess) {
+                    cudaMemcpyAsync(w.data(), c->ws + c->L.flags, 4 * w.size(), cudaMemcpyDeviceToHost, probe);
+                    cudaStreamSynchronize(probe);
+                    cudaStreamDestroy(probe);
+                    auto dump = [&](const char* name, int32_t lo, int32_t hi) {
+                        int shown = 0, low = 0;
+                        for (int32_t i = lo; i < hi; ++i)
+                            if (w[i] < c->epoch) {
+                                ++low;
+                                if (shown < 6) o += snprintf(msg + o, sizeof msg - o, "%s%d", shown++ ? "," : " ", i - lo);
+                            }
+                        o += snprintf(msg + o, sizeof msg - o, " (%s: %d below epoch)", name, low);
+                    };
+                    o += snprintf(msg + o, sizeof msg - o, "; words below epoch %u:", c->epoch);
+                    dump("chunk", c->L.f_chunk, c->L.f_act);
+                    dump("act", c->L.f_act, c->L.f_y);
+                    dump("y", c->L.f_y, c->L.f_logit);
+                    dump("logit", c->L.f_logit, c->L.f_land);
+                    dump("tensor", c->L.f_tensor, c->L.n_words);
+                }
+                return fail(PB_ECUDA, "%s", msg);
+            }
+            std::this_thread::sleep_for(std::chrono::microseconds(200));
+        }
+    }
     CU(cudaEventSynchronize(c->done));
     CU(cudaGetLastError());
     if (c->rank == 0) {

@@ -308,6 +308,19 @@ __global__ void signal_kernel(SignalTargets t, uint32_t value) {
 
 }  // namespace
 
+cudaError_t warm_simt_kernels() {
+    cudaFuncAttributes a;
+    const void* fns[] = {(const void*)norm_kernel<256, 8>, (const void*)norm_kernel<256, 40>, (const void*)embed_kernel,
+                         (const void*)rope_table_kernel, (const void*)rope_kernel, (const void*)attention_kernel<32>,
+                         (const void*)attention_kernel<64>, (const void*)attention_kernel<128>,
+                         (const void*)logits_kernel, (const void*)argmax_kernel, (const void*)signal_kernel};
+    for (const void* f : fns) {
+        cudaError_t e = cudaFuncGetAttributes(&a, f);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
 cudaError_t launch_norm(const float* h, int ldh, __nv_bfloat16* out, int ldo, int rows, int d,
                         const __nv_bfloat16* gamma, const __nv_bfloat16* beta, float eps, cudaStream_t s) {
     if (rows <= 0) return cudaSuccess;
