@@ -346,7 +346,7 @@ extern "C" pb_status pb_ctx_create(const pb_plan* plan, int32_t rank, const void
     // ~20 us while the PCIe link is saturated by the load); dependencies are device-side readiness words.
     auto mk = [&](cudaEvent_t* e) { return cudaEventCreate(e); };
     if (mk(&c->t0) || mk(&c->merge_done) || mk(&c->gather_done) || mk(&c->done) || mk(&c->ready_merge) ||
-        mk(&c->ready_recv))
+        mk(&c->ready_recv) || cudaEventCreateWithFlags(&c->tok_ev, cudaEventDisableTiming))
         return cleanup(fail(PB_ECUDA, "cudaEventCreate failed"));
     for (int32_t id : plan->load[rank])
         if (mk(&c->landed[id])) return cleanup(fail(PB_ECUDA, "cudaEventCreate failed"));
@@ -396,7 +396,7 @@ extern "C" void pb_ctx_free(pb_ctx* c) {
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     auto d = [](cudaEvent_t e) { if (e) cudaEventDestroy(e); };
-    d(c->t0); d(c->merge_done); d(c->gather_done); d(c->done); d(c->ready_merge); d(c->ready_recv);
+    d(c->t0); d(c->merge_done); d(c->gather_done); d(c->done); d(c->ready_merge); d(c->ready_recv); d(c->tok_ev);
     for (auto e : c->budget_events) d(e);
     for (auto st : c->owned_streams) cudaStreamDestroy(st);
     for (auto e : c->landed) d(e);
@@ -962,29 +962,43 @@ void build_items(Issuer& I) {
         I.items.push_back(Item{kind, mb, j, l, std::move(pre)});
     };
     add(I_PROLOGUE, 0, 0, 0, {});
-    for (int mb = 0; mb < I.n_mb; ++mb) {
-        for (int j = 0; j < I.k; ++j) {
-            const bool first = mb == 0 && j == 0;
-            if (g == 0) {
-                std::vector<int32_t> pre;
-                if (first) {
-                    const int32_t et = p->find_tensor("embed");
-                    if (c->last_own_chunk[et] >= 0) pre.push_back(et);
-                    if (opt) pre.push_back(p->find_tensor("pos"));
-                }
-                add(I_EMBED, mb, j, 0, pre);
-            } else {
-                add(I_WAITACT, mb, j, 0, {});
+    auto layer_pre = [&](int l) {
+        std::vector<int32_t> pre;
+        for (size_t t = 0; t < p->tensors.size(); ++t)
+            if (p->tensors[t].layer == l) pre.push_back((int32_t)t);
+        return pre;
+    };
+    auto head_item = [&](int mb, int j) {   // embedding (stage 0) or the previous stage's activation
+        if (g == 0) {
+            std::vector<int32_t> pre;
+            if (mb == 0 && j == 0) {
+                const int32_t et = p->find_tensor("embed");
+                if (c->last_own_chunk[et] >= 0) pre.push_back(et);
+                if (opt) pre.push_back(p->find_tensor("pos"));
             }
-            for (int l = stage.first; l < stage.second; ++l) {
-                std::vector<int32_t> pre;
-                if (first)
-                    for (size_t t = 0; t < p->tensors.size(); ++t)
-                        if (p->tensors[t].layer == l) pre.push_back((int32_t)t);
-                add(I_LAYER, mb, j, l, pre);
-            }
-            if (g < N - 1) add(I_PUSH, mb, j, 0, {});
+            add(I_EMBED, mb, j, 0, pre);
+        } else {
+            add(I_WAITACT, mb, j, 0, {});
         }
+    };
+    if (g == N - 1 && (I.n_mb > 1 || I.k > 1)) {
+        // Last stage (no downstream consumer): layer-major, so every microbatch / prompt chunk advances as each
+        // layer lands instead of all but the first waiting for the whole stage.
+        for (int l = stage.first; l < stage.second; ++l)
+            for (int mb = 0; mb < I.n_mb; ++mb)
+                for (int j = 0; j < I.k; ++j) {
+                    if (l == stage.first) head_item(mb, j);
+                    add(I_LAYER, mb, j, l, mb == 0 && j == 0 ? layer_pre(l) : std::vector<int32_t>{});
+                }
+    } else {
+        // Intermediate stage: chunk-major, so chunk 0 reaches the next stage as early as possible.
+        for (int mb = 0; mb < I.n_mb; ++mb)
+            for (int j = 0; j < I.k; ++j) {
+                head_item(mb, j);
+                for (int l = stage.first; l < stage.second; ++l)
+                    add(I_LAYER, mb, j, l, mb == 0 && j == 0 ? layer_pre(l) : std::vector<int32_t>{});
+                if (g < N - 1) add(I_PUSH, mb, j, 0, {});
+            }
     }
     if (g == N - 1) {
         std::vector<int32_t> pre{p->find_tensor("final_g")};
@@ -1039,7 +1053,12 @@ pb_status issue_item(Issuer& I, const Item& it) {
                 ++c->n_launches;
             }
             if (g == 0) {
-                CU(cudaMemcpyAsync(c->ws + L.tokens, c->h_tokens, sizeof(int32_t) * B * T, cudaMemcpyHostToDevice, s));
+                // the token upload went out on the copy lane ahead of the weights (issue_trial): an H2D copy on
+                // this stream would queue behind the whole load in the copy engine (measured: drains per stream)
+                if (I.replay)
+                    CU(cudaMemcpyAsync(c->ws + L.tokens, c->h_tokens, sizeof(int32_t) * B * T, cudaMemcpyHostToDevice, s));
+                else
+                    CU(cudaStreamWaitEvent(s, c->tok_ev, 0));
                 CU(cudaMemsetAsync(c->ws + L.nan, 0, 4, s));
             }
             break;
@@ -1175,9 +1194,15 @@ pb_status issue_trial(pb_ctx* c, int B, int T, bool replay) {
         bs[i]->pool = c->budget_events.data() + i * kEventPool;
     }
     build_items(I);
+    if (!replay && c->rank == 0) {   // prompt tokens first on the copy lane: they land in microseconds
+        CU(cudaMemcpyAsync(c->ws + c->L.tokens, c->h_tokens, sizeof(int32_t) * B * T, cudaMemcpyHostToDevice, c->h2d[0]));
+        CU(cudaEventRecord(c->tok_ev, c->h2d[0]));
+        CU(I.h2d.add(2));
+    }
     const size_t G = replay ? 0 : c->copies.size();
     const size_t R = replay ? 0 : p->recv[c->rank].size();
     size_t gi = 0, ri = 0, ii = 0;
+    bool merge_done_rec = replay, gather_done_rec = replay;
     static const bool dbg = getenv("PB_DEBUG_ISSUER") != nullptr;
     auto last_report = std::chrono::steady_clock::now();
     while (gi < G || ri < R || ii < I.items.size()) {
@@ -1187,11 +1212,19 @@ pb_status issue_trial(pb_ctx* c, int B, int T, bool replay) {
             if (st) return st;
             progressed = true;
         }
+        if (!merge_done_rec && gi == G) {   // t_full: recorded once the last merge work is on its stream
+            CU(cudaEventRecord(c->merge_done, c->merge));
+            merge_done_rec = true;
+        }
         const size_t target = gi >= G ? R : (gi * R) / std::max<size_t>(G, 1);
         while (ri < target && I.nv.can(5)) {
             pb_status st = issue_recv(I, ri++);
             if (st) return st;
             progressed = true;
+        }
+        if (!gather_done_rec && ri == R && gi == G) {
+            CU(cudaEventRecord(c->gather_done, c->nv));
+            gather_done_rec = true;
         }
         while (ii < I.items.size()) {
             const Item& it = I.items[ii];
@@ -1222,10 +1255,8 @@ pb_status issue_trial(pb_ctx* c, int B, int T, bool replay) {
             }
         }
     }
-    if (!replay) {
-        CU(cudaEventRecord(c->merge_done, c->merge));
-        CU(cudaEventRecord(c->gather_done, c->nv));
-    }
+    if (!merge_done_rec) CU(cudaEventRecord(c->merge_done, c->merge));
+    if (!gather_done_rec) CU(cudaEventRecord(c->gather_done, c->nv));
     return PB_OK;
 }
 

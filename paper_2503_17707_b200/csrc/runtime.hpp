@@ -84,6 +84,7 @@ struct pb_ctx {
     // events
     cudaEvent_t t0 = nullptr, merge_done = nullptr, gather_done = nullptr, done = nullptr;
     cudaEvent_t ready_merge = nullptr, ready_recv = nullptr;   // timing: last stage chunk merged / received
+    cudaEvent_t tok_ev = nullptr;                               // prompt tokens landed (copy lane)
     int32_t last_own_stage_chunk = -1, last_recv_stage_chunk = -1;
     std::vector<cudaEvent_t> landed, gathered;
     std::vector<char> tensor_own;        // this rank loads every piece of the tensor
