@@ -31,7 +31,7 @@ PB_API pb_status pb_op_merge(void* W, int64_t ldw, int32_t rows, int32_t cols, c
 PB_API pb_status pb_op_gemm(const void* X, int32_t x_rows, int32_t m_begin, int32_t m_end, int32_t K, const void* W,
                             int32_t n_rows, int32_t N, int32_t epi, const void* bias, int32_t relu, float scale,
                             int32_t scale_cols, void* out, int32_t ldo, void* stream);
-/* Same with an explicit cluster split-K factor (0 = the path's automatic choice, else 1..8). */
+/* Same with an explicit cluster split-K factor (0 = the path's automatic choice, else 1, 2, 4 or 8). */
 PB_API pb_status pb_op_gemm_split(const void* X, int32_t x_rows, int32_t m_begin, int32_t m_end, int32_t K,
                                   const void* W, int32_t n_rows, int32_t N, int32_t epi, const void* bias, int32_t relu,
                                   float scale, int32_t scale_cols, void* out, int32_t ldo, int32_t split_k,

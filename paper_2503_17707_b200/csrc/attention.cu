@@ -1,0 +1,302 @@
+// attention.cu — causal prefill attention on the tensor cores (tcgen05 / TMEM / TMA), head dim 64 or 128.
+//
+//   a_t = sum_{j <= t} softmax_j(q_t . k_j * score_scale) v_j        (per head; GQA: kv head = h / group)
+//   (the attention of every decoder layer in the first-token prefill; HF conventions G14)
+//
+// CTA = (128 query positions, head, sequence); 160 threads:
+//   warps 0-3 : softmax + epilogue, one query row per thread = one TMEM lane
+//   warp 4    : TMA producer and single-thread MMA issuer
+// Per 128-key tile j (keys [0, q_tile_end) only — causal):
+//   S = Q K_j^T            tcgen05.mma M128 N128, K = hd, fp32 accumulator in TMEM columns [0, 128)
+//   P = exp2(S*c - m)      softmax threads: tcgen05.ld the row, mask j > t, running max with lazy rescale
+//                          (O and l are rescaled only when the max grows by more than 2^8, FA4-style), P rounded
+//                          to bf16 into shared memory in the 128B-swizzled K-major layout the MMA reads
+//   O += P V_j             tcgen05.mma M128 N=hd, K = 128 keys, V read MN-major straight from its TMA tile,
+//                          fp32 accumulator in TMEM columns [128, 128 + hd)
+//   out = bf16(O / l)      l = sum of the bf16-rounded P actually multiplied
+// K_{j+1} streams in while softmax j runs; S_{j+1} overlaps PV_j; V is double-buffered. Q/K/V come through one
+// 3-D tensor map over the token-major qkv rows (col, sequence b, position t) whose t extent is t1, so keys
+// past the last computed position are zero-filled by TMA, never read.
+//
+// Numerics vs the oracle's storage contract: the oracle rounds the NORMALISED probabilities to
+// bf16; here the unnormalised exp2 values are rounded (the tensor-core operand) and normalisation happens
+// in fp32 at the end — a rounding-order difference bounded in tests/test_gpu_kernels.py::test_attention.
+#include <cuda_bf16.h>
+#include <math_constants.h>
+
+#include "kernels.hpp"
+#include "sm100.cuh"
+
+namespace pb {
+using namespace sm100;
+
+namespace {
+
+constexpr int QT = 128, KT = 128;
+constexpr int kAtom = 128 * 128;       // one 128-row x 64-col bf16 SW128 box = 16 KB
+constexpr float kRescale = 8.0f;       // lazy rescale threshold (log2 domain)
+
+template <int HD>
+struct AttnSmem {
+    static constexpr int kQ = HD / 64 * kAtom, kK = kQ, kV = kQ, kP = 2 * kAtom;   // V double-buffered
+    static constexpr int offQ = 0, offK = offQ + kQ, offV = offK + kK, offP = offV + 2 * kV, offBar = offP + kP;
+    static constexpr int kTotal = offBar + 128 + 1024;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_constant__ CUtensorMap map, __nv_bfloat16* __restrict__ out,
+                                                        int ldo, int t0, int t1, int group, int k_col0, int v_col0,
+                                                        float scale_log2) {
+    using SM = AttnSmem<HD>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t *sQ = smem + SM::offQ, *sK = smem + SM::offK, *sV = smem + SM::offV, *sP = smem + SM::offP;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::offBar);
+    uint64_t *q_full = bars, *k_full = bars + 1, *v_full = bars + 2 /* [2] */, *s_full = bars + 4,
+             *s_free = bars + 5, *p_full = bars + 6, *o_full = bars + 7;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int h = blockIdx.y, b = blockIdx.z, kvh = h / group;
+    const int qtile = gridDim.x - 1 - blockIdx.x;          // longest (latest) query tiles first
+    const int q0 = t0 + qtile * QT;
+    const int q_hi = min(q0 + QT, t1);
+    const int n_kv = (q_hi + KT - 1) / KT;                  // key tiles [0, n_kv)
+
+    if (tid == 0) {
+        tma_prefetch_desc(&map);
+        mbar_init(q_full, 1);
+        mbar_init(k_full, 1);
+        mbar_init(&v_full[0], 1);
+        mbar_init(&v_full[1], 1);
+        mbar_init(s_full, 1);
+        mbar_init(s_free, 4);      // one arrive per softmax warp
+        mbar_init(p_full, 4);
+        mbar_init(o_full, 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) tmem_alloc<256>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t tS = tmem, tO = tmem + 128;
+
+    if (warp == 4) {
+        if (lane == 0) {
+            constexpr int kBox = kAtom;   // bytes of one 64-col box
+            auto load_rows = [&](uint8_t* dst, uint64_t* bar, int col, int t) {
+#pragma unroll
+                for (int a = 0; a < HD / 64; ++a) tma_load_3d(dst + a * kBox, &map, bar, col + a * 64, b, t);
+            };
+            mbar_arrive_expect_tx(q_full, SM::kQ);
+            load_rows(sQ, q_full, h * HD, q0);
+            mbar_arrive_expect_tx(k_full, SM::kK);
+            load_rows(sK, k_full, k_col0 + kvh * HD, 0);
+            for (int j = 0; j < 2 && j < n_kv; ++j) {
+                mbar_arrive_expect_tx(&v_full[j], SM::kV);
+                load_rows(sV + j * SM::kV, &v_full[j], v_col0 + kvh * HD, j * KT);
+            }
+            constexpr uint32_t idS = idesc_bf16_f32(128, 128, 0, 0);
+            constexpr uint32_t idO = idesc_bf16_f32(128, HD, 0, 1);
+            mbar_wait(q_full, 0);
+            for (int j = 0; j < n_kv; ++j) {
+                const uint32_t ph = j & 1;
+                // ---- S = Q K_j^T (S columns are free once every softmax warp has read S_{j-1}); runs
+                // concurrently with PV_{j-1}
+                mbar_wait(k_full, ph);
+                if (j > 0) mbar_wait(s_free, (j - 1) & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int kk = 0; kk < HD / 16; ++kk) {
+                    const uint32_t off = (kk >> 2) * kBox + (kk & 3) * 32;
+                    umma_bf16(tS, smem_desc(smem_u32(sQ) + off, 16, 1024, kSw128),
+                              smem_desc(smem_u32(sK) + off, 16, 1024, kSw128), idS, kk > 0 ? 1u : 0u);
+                }
+                umma_commit(s_full);
+                // ---- V_{j+1} into the buffer PV_{j-1} has finished reading
+                if (j >= 1 && j + 1 < n_kv) {
+                    mbar_wait(o_full, (j - 1) & 1);
+                    const int vb = (j + 1) & 1;
+                    mbar_arrive_expect_tx(&v_full[vb], SM::kV);
+                    load_rows(sV + vb * SM::kV, &v_full[vb], v_col0 + kvh * HD, (j + 1) * KT);
+                }
+                // ---- K_{j+1} streams in while softmax j runs
+                mbar_wait(s_full, ph);
+                if (j + 1 < n_kv) {
+                    mbar_arrive_expect_tx(k_full, SM::kK);
+                    load_rows(sK, k_full, k_col0 + kvh * HD, (j + 1) * KT);
+                }
+                // ---- O += P_j V_j
+                mbar_wait(p_full, ph);
+                mbar_wait(&v_full[j & 1], (j >> 1) & 1);
+                tc_fence_after();
+                const uint32_t vbase = smem_u32(sV + (j & 1) * SM::kV);
+#pragma unroll
+                for (int kk = 0; kk < KT / 16; ++kk) {
+                    const uint64_t ad = smem_desc(smem_u32(sP) + (kk >> 2) * kBox + (kk & 3) * 32, 16, 1024, kSw128);
+                    // V tile [128 keys x hd], hd contiguous (MN-major): 64-col boxes kBox apart (LBO), 8-key groups
+                    // 1024 B apart (SBO); a K slice of 16 keys advances 2048 B.
+                    const uint64_t bd = smem_desc(vbase + kk * 2048, kBox, 1024, kSw128);
+                    umma_bf16(tO, ad, bd, idO, (j > 0 || kk > 0) ? 1u : 0u);
+                }
+                umma_commit(o_full);
+            }
+        }
+        __syncwarp();
+    } else {
+        // ---------------- softmax warps: thread = query row r
+        const int r = warp * 32 + lane;
+        const int t = q0 + r;
+        const bool row_ok = t < q_hi;
+        const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+        float m = -CUDART_INF_F, l = 0.f;
+        for (int j = 0; j < n_kv; ++j) {
+            const uint32_t ph = j & 1;
+            mbar_wait(s_full, ph);
+            tc_fence_after();
+            uint32_t sr[4][32];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tmem_ld32_async(tS + lane_off + c * 32, sr[c]);
+            tmem_wait_ld();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(s_free);
+            // scores in the log2 domain, causal mask (key > t), invalid rows fully masked
+            const int key0 = j * KT;
+            float mx = -CUDART_INF_F;
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const int key = key0 + c * 32 + i;
+                    float v = __uint_as_float(sr[c][i]) * scale_log2;
+                    v = (row_ok && key <= t) ? v : -CUDART_INF_F;
+                    sr[c][i] = __float_as_uint(v);
+                    mx = fmaxf(mx, v);
+                }
+            // lazy rescale: keep the reference max unless the row max grew by more than 2^8
+            const bool grow = mx > m + kRescale;   // false when mx == -inf
+            const float m_new = grow ? mx : m;
+            const float alpha = (grow && m != -CUDART_INF_F) ? exp2f(m - m_new) : 1.f;
+            // O (TMEM) is written by PV_{j-1}; rescaling it, and overwriting P, wait for that MMA
+            if (j > 0) {
+                mbar_wait(o_full, (j - 1) & 1);
+                tc_fence_after();
+            }
+            if (__any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll
+                for (int c = 0; c < HD / 32; ++c) {
+                    uint32_t o[32];
+                    tmem_ld32_async(tO + lane_off + c * 32, o);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+                    tmem_st32(tO + lane_off + c * 32, o);
+                }
+                tmem_wait_st();
+            }
+            l *= alpha;
+            m = m_new;
+            // P row -> bf16, 128B-swizzled K-major (16-B chunk u of row r at chunk u ^ (r & 7) of its 64-key box)
+            float rs = 0.f;
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                uint32_t w[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float s0 = __uint_as_float(sr[u >> 2][(u & 3) * 8 + 2 * e]);
+                    const float s1 = __uint_as_float(sr[u >> 2][(u & 3) * 8 + 2 * e + 1]);
+                    const float p0 = m == -CUDART_INF_F ? 0.f : exp2f(s0 - m);
+                    const float p1 = m == -CUDART_INF_F ? 0.f : exp2f(s1 - m);
+                    const __nv_bfloat162 pb = __floats2bfloat162_rn(p0, p1);
+                    const float2 pr = __bfloat1622float2(pb);
+                    rs += pr.x + pr.y;
+                    w[e] = *reinterpret_cast<const uint32_t*>(&pb);
+                }
+                uint8_t* dst = sP + (u >> 3) * kAtom + r * 128 + (((u & 7) ^ (r & 7)) << 4);
+                *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+            l += rs;
+            fence_proxy_async_smem();   // generic-proxy P writes -> visible to the tensor core
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(p_full);
+        }
+        // ---------------- epilogue: O / l -> bf16
+        mbar_wait(o_full, (n_kv - 1) & 1);
+        tc_fence_after();
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        __nv_bfloat16* o_row = out + ((size_t)t * gridDim.z + b) * ldo + h * HD;
+#pragma unroll
+        for (int c = 0; c < HD / 32; ++c) {
+            uint32_t o[32];
+            tmem_ld32_async(tO + lane_off + c * 32, o);
+            tmem_wait_ld();
+            if (row_ok) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    uint4 w;
+                    w.x = bf16x2_bits(__uint_as_float(o[8 * q + 0]) * inv, __uint_as_float(o[8 * q + 1]) * inv);
+                    w.y = bf16x2_bits(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv);
+                    w.z = bf16x2_bits(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv);
+                    w.w = bf16x2_bits(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv);
+                    *reinterpret_cast<uint4*>(o_row + c * 32 + q * 8) = w;
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        __syncwarp();
+        tc_fence_after();
+        tmem_dealloc<256>(tmem);
+    }
+}
+
+template <int HD>
+cudaError_t launch_tc(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int ldo, int t0, int t1, int B, int H,
+                      int group, int k_col0, int v_col0, float score_scale, cudaStream_t s) {
+    // 3-D view of the token-major rows: (col, sequence b, position t), t extent = t1 (keys >= t1 zero-filled).
+    const uint64_t dims[3] = {(uint64_t)ld, (uint64_t)B, (uint64_t)t1};
+    const uint64_t strides[2] = {(uint64_t)ld * 2, (uint64_t)ld * 2 * B};
+    const uint32_t box[3] = {64, 1, 128};
+    CUtensorMap map;
+    char err[256];
+    if (!make_map_bf16_3d(&map, qkv, dims, strides, box, 128, err, sizeof err)) return cudaErrorInvalidValue;
+    using SM = AttnSmem<HD>;
+    cudaError_t e = cudaFuncSetAttribute(attention_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::kTotal);
+    if (e != cudaSuccess) return e;
+    const dim3 grid((t1 - t0 + QT - 1) / QT, H, B);
+    const float scale_log2 = score_scale * 1.4426950408889634f;
+    attention_tc_kernel<HD><<<grid, 160, SM::kTotal, s>>>(map, out, ldo, t0, t1, group, k_col0, v_col0, scale_log2);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t warm_attention_kernels() {
+    cudaFuncAttributes a;
+    cudaError_t e = cudaFuncGetAttributes(&a, attention_tc_kernel<64>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, attention_tc_kernel<128>);
+    return e;
+}
+
+cudaError_t launch_attention(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int ldo, int t0, int t1, int B,
+                             int n_heads, int n_kv_heads, int hd, int k_col0, int v_col0, float score_scale,
+                             cudaStream_t s) {
+    if (t1 <= t0) return cudaSuccess;
+    const bool tma_ok = (ld % 8) == 0 && (reinterpret_cast<uintptr_t>(qkv) & 15) == 0 && (ldo % 8) == 0 &&
+                        (k_col0 % 8) == 0 && (v_col0 % 8) == 0;
+    const int group = n_heads / n_kv_heads;
+    if (tma_ok && hd == 64)
+        return launch_tc<64>(qkv, ld, out, ldo, t0, t1, B, n_heads, group, k_col0, v_col0, score_scale, s);
+    if (tma_ok && hd == 128)
+        return launch_tc<128>(qkv, ld, out, ldo, t0, t1, B, n_heads, group, k_col0, v_col0, score_scale, s);
+    return launch_attention_simt(qkv, ld, out, ldo, t0, t1, B, n_heads, n_kv_heads, hd, k_col0, v_col0, score_scale,
+                                 s);
+}
+
+}  // namespace pb

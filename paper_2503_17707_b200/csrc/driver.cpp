@@ -74,6 +74,30 @@ bool make_map_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t c
     return true;
 }
 
+bool make_map_bf16_3d(CUtensorMap* map, const void* base, const uint64_t dims[3], const uint64_t strides_bytes[2],
+                      const uint32_t box[3], int swizzle_bytes, char* err, size_t errlen) {
+    if (!driver_init(err, errlen)) return false;
+    cuuint64_t d[3] = {dims[0], dims[1], dims[2]};
+    cuuint64_t st[2] = {strides_bytes[0], strides_bytes[1]};
+    cuuint32_t bx[3] = {box[0], box[1], box[2]};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUtensorMapSwizzle sw = swizzle_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                            : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                            : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                  : CU_TENSOR_MAP_SWIZZLE_NONE;
+    CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), d, st, bx, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        const char* s = "?";
+        if (g_errstr) g_errstr(r, &s);
+        snprintf(err, errlen, "cuTensorMapEncodeTiled (3-D) failed (%d: %s) base=%p dims=%llux%llux%llu", (int)r, s,
+                 base, (unsigned long long)dims[0], (unsigned long long)dims[1], (unsigned long long)dims[2]);
+        return false;
+    }
+    return true;
+}
+
 cudaError_t stream_wait_geq(cudaStream_t s, const uint32_t* dev_addr, uint32_t value) {
     if (!g_wait32) return cudaErrorNotSupported;
     CUresult r = g_wait32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(dev_addr), value,

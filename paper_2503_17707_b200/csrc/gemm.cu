@@ -2,7 +2,10 @@
 //
 // Used for the QKV, O, FC1/FC2 (OPT) and QKV, O, gate|up, down (Llama) projections of every layer
 // (the per-layer prefill compute of P:L102-107). Both operands are K-major bf16 (activations row-major,
-// HF [out, in] weights row-major), fed by TMA with 128-byte swizzle into a 6-stage shared-memory ring.
+// HF [out, in] weights row-major), fed by TMA with 128-byte swizzle into a shared-memory ring of 6 stages
+// (3 when the grid needs two CTAs per SM). With programmatic dependent launch (GemmArgs::pdl) the producer
+// requests the first ring of WEIGHT tiles before waiting for the previous kernel (weights do not depend on
+// it), so the weight stream of one projection starts under the tail of the kernel before it.
 //
 // CTA tile 128 x 128, BK = 64; 128 threads:
 //   warp 0 / lane 0 : TMA producer   (full[s] <- expect_tx; empty[s] released by tcgen05.commit)
@@ -25,12 +28,13 @@ using namespace sm100;
 
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 64, STAGES = 6;
+constexpr int BM = 128, BN = 128, BK = 64, MAX_STAGES = 6;
 constexpr int kStageA = BM * BK * 2;  // 16 KB
 constexpr int kStageB = BN * BK * 2;  // 16 KB
-constexpr int kBarOff = STAGES * (kStageA + kStageB);
-constexpr int kSmem = kBarOff + 256 + 1024;
-static_assert(BM * BN * 4 <= kBarOff, "partial tile must fit in the stage ring");
+constexpr int kStage = kStageA + kStageB;
+constexpr int kBarBytes = 256;
+__host__ __device__ constexpr int smem_bytes(int stages) { return stages * kStage + kBarBytes + 1024; }
+static_assert(BM * BN * 4 <= 2 * kStage, "partial tile must fit in a 2-stage ring");
 
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
 
@@ -55,26 +59,32 @@ __device__ __forceinline__ float4 ld_cluster_f4(uint32_t addr) {
                  : "memory");
     return v;
 }
+// Programmatic dependent launch: let the next kernel of the stream get scheduled now; wait for the previous
+// kernel's completion (and memory) before touching anything it writes. Both are no-ops without PDL.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Partial tile: [128 rows][32 float4 chunks], chunk c of row r stored at slot c ^ (r & 31) (conflict-free
 // row-per-thread writes, and conflict-free chunk-per-thread reads).
 __device__ __forceinline__ uint32_t part_off(int row, int chunk) {
     return (uint32_t)(row * 512 + ((chunk ^ (row & 31)) << 4));
 }
 
-template <int EPI>
+// S = split-K factor = cluster size along z (compile-time so the S remote loads of the reduction are issued
+// back to back, then summed in the fixed order 0..S-1).
+template <int EPI, int S>
 __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CUtensorMap mapX,
-                                                      const __grid_constant__ CUtensorMap mapW, const GemmArgs a) {
+                                                      const __grid_constant__ CUtensorMap mapW, const GemmArgs a,
+                                                      const int stages) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sA = smem;
-    uint8_t* sB = smem + STAGES * kStageA;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kBarOff);
-    uint64_t* empty = full + STAGES;
-    uint64_t* done = empty + STAGES;
+    uint8_t* ring = smem;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * kStage);
+    uint64_t* empty = full + MAX_STAGES;
+    uint64_t* done = empty + MAX_STAGES;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int S = gridDim.z;                       // split-K factor == cluster size along z
     const int split = S > 1 ? (int)cluster_rank() : 0;
     const int m0 = a.M_begin + blockIdx.y * BM;
     // EPI_SILU_MUL: tile = 64 gate columns + the matching 64 up columns -> 64 outputs.
@@ -83,10 +93,11 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
     const int kb0 = (int)((long)nk * split / S), kb1 = (int)((long)nk * (split + 1) / S);
     const int my_k = kb1 - kb0;                    // >= 1 (host guarantees S <= nk)
 
+    pdl_launch_dependents();
     if (tid == 0) {
         tma_prefetch_desc(&mapX);
         tma_prefetch_desc(&mapW);
-        for (int s = 0; s < STAGES; ++s) {
+        for (int s = 0; s < stages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
@@ -99,28 +110,41 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
+    auto load_w = [&](int i) {
+        const int s = i % stages, kc = (kb0 + i) * BK;
+        uint8_t* sB = ring + s * kStage + kStageA;
+        if (EPI == EPI_SILU_MUL) {
+            tma_load_2d(sB, &mapW, &full[s], kc, n_out0);
+            tma_load_2d(sB + kStageB / 2, &mapW, &full[s], kc, a.up_row0 + n_out0);
+        } else {
+            tma_load_2d(sB, &mapW, &full[s], kc, n_out0);
+        }
+    };
     if (warp == 0 && lane == 0) {
-        // ---------------- TMA producer
-        for (int i = 0; i < my_k; ++i) {
-            const int s = i % STAGES, kc = (kb0 + i) * BK;
-            if (i >= STAGES) mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
-            mbar_arrive_expect_tx(&full[s], kStageA + kStageB);
-            tma_load_2d(sA + s * kStageA, &mapX, &full[s], kc, m0);
-            if (EPI == EPI_SILU_MUL) {
-                tma_load_2d(sB + s * kStageB, &mapW, &full[s], kc, n_out0);
-                tma_load_2d(sB + s * kStageB + kStageB / 2, &mapW, &full[s], kc, a.up_row0 + n_out0);
-            } else {
-                tma_load_2d(sB + s * kStageB, &mapW, &full[s], kc, n_out0);
-            }
+        // ---------------- TMA producer. The weights do not depend on the previous kernel: the first ring's
+        // worth is requested before the programmatic-dependency wait, X (the previous kernel's output) after.
+        const int pre = my_k < stages ? my_k : stages;
+        for (int i = 0; i < pre; ++i) {
+            mbar_arrive_expect_tx(&full[i], kStage);
+            load_w(i);
+        }
+        pdl_wait();
+        for (int i = 0; i < pre; ++i) tma_load_2d(ring + i * kStage, &mapX, &full[i], (kb0 + i) * BK, m0);
+        for (int i = pre; i < my_k; ++i) {
+            const int s = i % stages;
+            mbar_wait(&empty[s], ((i / stages) - 1) & 1);
+            mbar_arrive_expect_tx(&full[s], kStage);
+            tma_load_2d(ring + s * kStage, &mapX, &full[s], (kb0 + i) * BK, m0);
+            load_w(i);
         }
     } else if (warp == 1 && lane == 0) {
         // ---------------- MMA issuer
         constexpr uint32_t idesc = idesc_bf16_f32(BM, BN, 0, 0);
         for (int i = 0; i < my_k; ++i) {
-            const int s = i % STAGES;
-            mbar_wait(&full[s], (i / STAGES) & 1);
+            const int s = i % stages;
+            mbar_wait(&full[s], (i / stages) & 1);
             tc_fence_after();
-            const uint32_t a_base = smem_u32(sA + s * kStageA), b_base = smem_u32(sB + s * kStageB);
+            const uint32_t a_base = smem_u32(ring + s * kStage), b_base = a_base + kStageA;
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
                 const uint64_t ad = smem_desc(a_base + k * 32, 16, 1024, kSw128);
@@ -130,56 +154,67 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
             umma_commit(&empty[s]);
         }
         umma_commit(done);
+    } else {
+        pdl_wait();
     }
     __syncwarp();
     mbar_wait(done, 0);
     tc_fence_after();
 
     // ---------------- stage the fp32 tile (this CTA's K-partial) in shared memory; all MMAs and TMA loads
-    // have completed, so the stage ring is free.
+    // have completed, so the stage ring is free. Two batches of 64 columns (4 loads in flight, one wait).
     {
         const int row = warp * 32 + lane;
         const uint32_t t_row = tmem + ((uint32_t)(warp * 32) << 16);
-#pragma unroll 1
-        for (int cb = 0; cb < BN / 32; ++cb) {
-            float v[32];
-            tmem_ld32(t_row + cb * 32, v);
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
-                *reinterpret_cast<float4*>(smem + part_off(row, cb * 8 + q)) =
-                    make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        for (int half = 0; half < 2; ++half) {
+            uint32_t r0[32], r1[32];
+            tmem_ld32_async(t_row + half * 64, r0);
+            tmem_ld32_async(t_row + half * 64 + 32, r1);
+            tmem_wait_ld();
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                *reinterpret_cast<uint4*>(smem + part_off(row, half * 16 + q)) =
+                    make_uint4(r0[4 * q], r0[4 * q + 1], r0[4 * q + 2], r0[4 * q + 3]);
+                *reinterpret_cast<uint4*>(smem + part_off(row, half * 16 + 8 + q)) =
+                    make_uint4(r1[4 * q], r1[4 * q + 1], r1[4 * q + 2], r1[4 * q + 3]);
+            }
         }
     }
     tc_fence_before();
     if (S > 1) cluster_sync();
     else __syncthreads();
 
-    // ---------------- reduce rows [r_lo, r_hi) over the S partials (fixed order) + fused epilogue
+    // ---------------- reduce rows [r_lo, r_hi) over the S partials (fixed order 0..S-1) + fused epilogue
     const int r_lo = BM * split / S, r_hi = BM * (split + 1) / S;
     const uint32_t base = smem_u32(smem);
     const int chunks = EPI == EPI_SILU_MUL ? 16 : 32;
+    auto sum_chunk = [&](int r, int c) {
+        if constexpr (S == 1) {
+            return *reinterpret_cast<const float4*>(smem + part_off(r, c));
+        } else {
+            float4 p[S];
+#pragma unroll
+            for (int s2 = 0; s2 < S; ++s2) p[s2] = ld_cluster_f4(map_cluster(base + part_off(r, c), s2));
+            float4 acc = p[0];
+#pragma unroll
+            for (int s2 = 1; s2 < S; ++s2) {
+                acc.x += p[s2].x;
+                acc.y += p[s2].y;
+                acc.z += p[s2].z;
+                acc.w += p[s2].w;
+            }
+            return acc;
+        }
+    };
     for (int idx = tid; idx < (r_hi - r_lo) * chunks; idx += 128) {
         const int r = r_lo + idx / chunks, ch = idx % chunks;
         const int row = m0 + r;
-        auto sum_chunk = [&](int c) {
-            float4 acc = *reinterpret_cast<const float4*>(smem + part_off(r, c));
-            if (S > 1) {
-                acc = ld_cluster_f4(map_cluster(base + part_off(r, c), 0));
-                for (int s2 = 1; s2 < S; ++s2) {
-                    const float4 p = ld_cluster_f4(map_cluster(base + part_off(r, c), s2));
-                    acc.x += p.x;
-                    acc.y += p.y;
-                    acc.z += p.z;
-                    acc.w += p.w;
-                }
-            }
-            return acc;
-        };
         if (row >= a.M_end) continue;
         if (EPI == EPI_SILU_MUL) {
             const int n = n_out0 + ch * 4;
             if (n >= a.N) continue;
-            const float4 g = sum_chunk(ch), u = sum_chunk(ch + 16);
+            const float4 g = sum_chunk(r, ch), u = sum_chunk(r, ch + 16);
             const float o[4] = {silu(g.x) * u.x, silu(g.y) * u.y, silu(g.z) * u.z, silu(g.w) * u.w};
             __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(a.out) + (size_t)row * a.ldo + n;
             if (n + 4 <= a.N) {
@@ -194,7 +229,7 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
         }
         const int n = n_out0 + ch * 4;
         if (n >= a.N) continue;
-        const float4 acc = sum_chunk(ch);
+        const float4 acc = sum_chunk(r, ch);
         float v[4] = {acc.x, acc.y, acc.z, acc.w};
         const int nv = min(4, a.N - n);
         if (a.bias) {
@@ -243,62 +278,89 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
     }
 }
 
-template <int EPI>
-cudaError_t launch_epi(const CUtensorMap& mapX, const CUtensorMap& mapW, const GemmArgs& a, int S, cudaStream_t s) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    if (e != cudaSuccess) return e;
-    if (S > 1) {
-        e = cudaFuncSetAttribute(gemm_kernel<EPI>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
-    }
+template <int EPI, int S>
+cudaError_t launch_es(const CUtensorMap& mapX, const CUtensorMap& mapW, const GemmArgs& a, cudaStream_t s) {
     const int per = EPI == EPI_SILU_MUL ? BN / 2 : BN;
     const dim3 grid((a.N + per - 1) / per, (a.M_end - a.M_begin + BM - 1) / BM, S);
-    if (S == 1) {   // no cluster: plain launch (lower launch latency)
-        gemm_kernel<EPI><<<grid, 128, kSmem, s>>>(mapX, mapW, a);
-        return cudaGetLastError();
-    }
+    // Deep ring when the grid fits one CTA per SM; otherwise 3 stages (96 KB) so two CTAs share an SM.
+    const int ctas = grid.x * grid.y * grid.z;
+    const int stages = ctas <= 148 ? MAX_STAGES : 3;
+    const int smem = smem_bytes(stages);
+    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<EPI, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         smem_bytes(MAX_STAGES));
+    if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(128);
-    cfg.dynamicSmemBytes = kSmem;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 1;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = S;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (S > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = 1;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = S;
+        ++na;
+    }
+    if (a.pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, gemm_kernel<EPI>, mapX, mapW, a);
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, gemm_kernel<EPI, S>, mapX, mapW, a, stages);
+}
+
+template <int EPI>
+cudaError_t launch_epi(const CUtensorMap& mapX, const CUtensorMap& mapW, const GemmArgs& a, int S, cudaStream_t s) {
+    switch (S) {
+        case 1: return launch_es<EPI, 1>(mapX, mapW, a, s);
+        case 2: return launch_es<EPI, 2>(mapX, mapW, a, s);
+        case 4: return launch_es<EPI, 4>(mapX, mapW, a, s);
+        case 8: return launch_es<EPI, 8>(mapX, mapW, a, s);
+    }
+    return cudaErrorInvalidValue;
 }
 
 }  // namespace
 
-// Split-K factor: fill the 148 SMs with (N tiles x S) CTAs, at most 4 (measured on B200 at M = 128:
-// S = 8 loses to S = 4 on cluster scheduling + DSMEM reduction, tools/gemm_bench.py), at least eight
-// 64-wide K blocks per split. Depends on N and K only (determinism across prompt chunkings).
-int gemm_split_k(int N, int K, int epi) {
+// Split-K factor S (1, 2 or 4): the largest S <= 4 that keeps n_tiles x m_tiles x S <= 296 CTAs (two per SM
+// on 148 SMs) with at least 4 K blocks of 64 per split. It depends on (N, K, M_total) only, where M_total is
+// the row count of the WHOLE prompt batch (not of a prompt chunk), so a prompt split into chunks reduces
+// every output in the same order and gives bit-identical results. Measured on B200 at M = 128
+// (tools/gemm_bench.py, r01c): S = 4 is fastest for all four OPT-1.3B projections; clusters of 8 lose to
+// cluster scheduling (one CTA per SM needs 8 free SMs in one GPC).
+int gemm_split_k(int N, int K, int epi, int M_total) {
     const int per = epi == EPI_SILU_MUL ? BN / 2 : BN;
-    const int n_tiles = (N + per - 1) / per;
+    const long n_tiles = (N + per - 1) / per;
+    const long m_tiles = M_total > 0 ? (M_total + BM - 1) / BM : 1;
     const int nk = (K + BK - 1) / BK;
-    int S = 148 / (n_tiles > 0 ? n_tiles : 1);
-    S = S < 1 ? 1 : (S > 4 ? 4 : S);
-    while (S > 1 && nk / S < 8) --S;
+    int S = 1;
+    while (S < 4 && n_tiles * m_tiles * 2 * S <= 296 && nk / (2 * S) >= 4) S *= 2;
     return S;
 }
 
 cudaError_t warm_gemm_kernels() {
-    cudaFuncAttributes a;
-    cudaError_t e = cudaFuncGetAttributes(&a, gemm_kernel<EPI_BF16>);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, gemm_kernel<EPI_RESID>);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, gemm_kernel<EPI_SILU_MUL>);
-    return e;
+    cudaFuncAttributes at;
+    const void* fns[] = {(const void*)gemm_kernel<EPI_BF16, 1>,     (const void*)gemm_kernel<EPI_BF16, 2>,
+                         (const void*)gemm_kernel<EPI_BF16, 4>,     (const void*)gemm_kernel<EPI_BF16, 8>,
+                         (const void*)gemm_kernel<EPI_RESID, 1>,    (const void*)gemm_kernel<EPI_RESID, 2>,
+                         (const void*)gemm_kernel<EPI_RESID, 4>,    (const void*)gemm_kernel<EPI_RESID, 8>,
+                         (const void*)gemm_kernel<EPI_SILU_MUL, 1>, (const void*)gemm_kernel<EPI_SILU_MUL, 2>,
+                         (const void*)gemm_kernel<EPI_SILU_MUL, 4>, (const void*)gemm_kernel<EPI_SILU_MUL, 8>};
+    for (const void* f : fns) {
+        cudaError_t e = cudaFuncGetAttributes(&at, f);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 cudaError_t launch_gemm(const CUtensorMap& mapX, const CUtensorMap& mapW, const GemmArgs& a, cudaStream_t s) {
     if (a.M_end <= a.M_begin || a.N <= 0) return cudaSuccess;
     if (a.K <= 0 || a.K % 8) return cudaErrorInvalidValue;
-    const int S = a.split_k > 0 ? a.split_k : gemm_split_k(a.N, a.K, a.epi);
+    const int S = a.split_k > 0 ? a.split_k : gemm_split_k(a.N, a.K, a.epi, a.M_total);
     switch (a.epi) {
         case EPI_BF16: return launch_epi<EPI_BF16>(mapX, mapW, a, S, s);
         case EPI_RESID: return launch_epi<EPI_RESID>(mapX, mapW, a, S, s);

@@ -16,6 +16,10 @@ bool driver_init(char* err, size_t errlen);
 bool make_map_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld_elems,
                    uint32_t box_rows, uint32_t box_cols, int swizzle_bytes, char* err, size_t errlen);
 
+// 3-D bf16 tensor map: dims innermost first, strides (bytes) of dims 1 and 2, box innermost first.
+bool make_map_bf16_3d(CUtensorMap* map, const void* base, const uint64_t dims[3], const uint64_t strides_bytes[2],
+                      const uint32_t box[3], int swizzle_bytes, char* err, size_t errlen);
+
 // Stream memory operations / cross-rank readiness words.
 cudaError_t stream_wait_geq(cudaStream_t s, const uint32_t* dev_addr, uint32_t value);
 cudaError_t stream_write(cudaStream_t s, uint32_t* dev_addr, uint32_t value);   // after all prior stream work
@@ -57,9 +61,11 @@ struct GemmArgs {
     void* out;                  // bf16 [*, ldo] or fp32 [*, ldo]
     int ldo;
     int up_row0;                // EPI_SILU_MUL: first row of `up` in W (= N_out)
-    int split_k;                // 0 = automatic (gemm_split_k), else the cluster split-K factor (1..8)
+    int split_k;                // 0 = automatic (gemm_split_k), else the cluster split-K factor (1, 2, 4, 8)
+    int M_total;                // rows of the whole prompt batch (picks split_k; chunk-invariant), 0 = M_end-M_begin
+    int pdl;                    // 1: programmatic dependent launch after the stream's previous kernel
 };
-int gemm_split_k(int N, int K, int epi);
+int gemm_split_k(int N, int K, int epi, int M_total);
 // Maps: X box {64, 128} SW128 over [max_rows x K]; W box {64, 128} (EPI_SILU_MUL: {64, 64}) SW128 over [rows x K].
 cudaError_t launch_gemm(const CUtensorMap& mapX, const CUtensorMap& mapW, const GemmArgs& a, cudaStream_t s);
 
@@ -85,9 +91,13 @@ cudaError_t launch_rope(__nv_bfloat16* qkv, int ld, int r0, int r1, int B, int n
 
 // Causal attention for query rows [t0, t1) (token-major rows t*B+b) against keys [0, t] of the same
 // sequence; q at col h*hd, k at k_col0 + (h/group)*hd, v at v_col0 + (h/group)*hd of `qkv`.
+// hd = 64 or 128: tensor-core kernel (attention.cu); other head sizes: the SIMT kernel (simt.cu).
 cudaError_t launch_attention(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int ldo, int t0, int t1, int B,
                              int n_heads, int n_kv_heads, int hd, int k_col0, int v_col0, float score_scale,
                              cudaStream_t s);
+cudaError_t launch_attention_simt(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int ldo, int t0, int t1,
+                                  int B, int n_heads, int n_kv_heads, int hd, int k_col0, int v_col0,
+                                  float score_scale, cudaStream_t s);
 
 // logits[b, v] = sum_c y[b, c] * E[v, c] for v in [v0, v1) (fp32 out, row pitch ldl).
 cudaError_t launch_logits(const __nv_bfloat16* y, int B, int d, const __nv_bfloat16* E, int v0, int v1, float* logits,
@@ -102,5 +112,6 @@ cudaError_t launch_argmax(const float* logits, int B, int V, int ldl, int32_t* t
 cudaError_t warm_merge_kernels();
 cudaError_t warm_gemm_kernels();
 cudaError_t warm_simt_kernels();
+cudaError_t warm_attention_kernels();
 
 }  // namespace pb

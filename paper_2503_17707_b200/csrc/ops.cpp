@@ -38,7 +38,7 @@ extern "C" pb_status pb_op_gemm_split(const void* X, int32_t x_rows, int32_t m_b
                                       const void* W, int32_t n_rows, int32_t N, int32_t epi, const void* bias,
                                       int32_t relu, float scale, int32_t scale_cols, void* out, int32_t ldo,
                                       int32_t split_k, void* stream) {
-    if (split_k < 0 || split_k > 8 || (split_k > 0 && split_k > (K + 63) / 64))
+    if (split_k < 0 || split_k > 8 || (split_k & (split_k - 1)) || (split_k > 0 && split_k > (K + 63) / 64))
         return fail(PB_EINVAL, "pb_op_gemm_split: split_k %d out of range", split_k);
     if (!X || !W || !out) return fail(PB_EINVAL, "pb_op_gemm: null pointer");
     if (K % 8 || K <= 0 || epi < 0 || epi > 2 || m_begin < 0 || m_end > x_rows)
@@ -62,6 +62,7 @@ extern "C" pb_status pb_op_gemm_split(const void* X, int32_t x_rows, int32_t m_b
     a.ldo = ldo;
     a.up_row0 = N;
     a.split_k = split_k;
+    a.M_total = m_end - m_begin;
     return cuda_status(launch_gemm(mx, mw, a, (cudaStream_t)stream), "gemm");
 }
 

@@ -294,6 +294,7 @@ extern "C" pb_status pb_ctx_create(const pb_plan* plan, int32_t rank, const void
             cudaError_t e = warm_merge_kernels();
             if (e == cudaSuccess) e = warm_gemm_kernels();
             if (e == cudaSuccess) e = warm_simt_kernels();
+            if (e == cudaSuccess) e = warm_attention_kernels();
             if (e != cudaSuccess) return fail(PB_ECUDA, "kernel load: %s", cudaGetErrorString(e));
             warmed.insert(dev);
         }
@@ -699,6 +700,8 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, boo
         a.out = out;
         a.ldo = ldo;
         a.up_row0 = f;
+        a.M_total = B * c->cur_seq;   // the whole prompt batch: split-K does not change with prompt chunking
+        a.pdl = c->profiling ? 0 : 1; // per-launch timing events between kernels would cancel the overlap anyway
         return a;
     };
     // Algorithmic work of a GEMM launch: 2MNK flops; bytes = X + W + output (fp32 residual read + write).

@@ -40,6 +40,7 @@ template <int NT, int PER>
 __global__ void __launch_bounds__(NT) norm_kernel(const float* __restrict__ h, int ldh, __nv_bfloat16* __restrict__ out,
                                                   int ldo, int d, const __nv_bfloat16* __restrict__ gamma,
                                                   const __nv_bfloat16* __restrict__ beta, float eps) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // a PDL-launched GEMM may start its weight prefetch
     __shared__ float red[32];
     const float* x = h + (size_t)blockIdx.x * ldh;
     float v[PER];
@@ -116,6 +117,7 @@ __global__ void rope_table_kernel(float2* table, int T, int hd, double theta) {
 // x'_i = x_i cos - x_{i+hd/2} sin ; x'_{i+hd/2} = x_{i+hd/2} cos + x_i sin   (HF rotate_half)
 __global__ void rope_kernel(__nv_bfloat16* qkv, int ld, int r0, int B, int n_q, int n_k, int hd, int k_col0,
                             const float2* __restrict__ table) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // a PDL-launched GEMM may start its weight prefetch
     const int row = r0 + blockIdx.x;
     const int t = row / B;
     const int half = hd / 2;
@@ -139,6 +141,7 @@ __global__ void __launch_bounds__(256, 2) attention_kernel(const __nv_bfloat16* 
                                                         __nv_bfloat16* __restrict__ out, int ldo, int t0, int t1,
                                                         int B, int group, int k_col0, int v_col0,
                                                         float score_scale) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // a PDL-launched GEMM may start its weight prefetch
     constexpr int KT = 32, QT = 32, DPL = HD / 32;   // dims per lane
     extern __shared__ float attn_smem[];
     float (*sQ)[HD] = reinterpret_cast<float (*)[HD]>(attn_smem);
@@ -352,9 +355,9 @@ cudaError_t launch_rope(__nv_bfloat16* qkv, int ld, int r0, int r1, int B, int n
     return cudaGetLastError();
 }
 
-cudaError_t launch_attention(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int ldo, int t0, int t1, int B,
-                             int n_heads, int n_kv_heads, int hd, int k_col0, int v_col0, float score_scale,
-                             cudaStream_t s) {
+cudaError_t launch_attention_simt(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int ldo, int t0, int t1,
+                                  int B, int n_heads, int n_kv_heads, int hd, int k_col0, int v_col0,
+                                  float score_scale, cudaStream_t s) {
     if (t1 <= t0) return cudaSuccess;
     dim3 grid((t1 - t0 + 31) / 32, n_heads, B);
     const int group = n_heads / n_kv_heads;

@@ -141,8 +141,13 @@ def test_norm(rms, d):
 
 
 @pytest.mark.parametrize("T,Bsz,H,KVH,hd,t0,t1", [(16, 1, 4, 4, 64, 0, 16), (77, 2, 4, 2, 128, 0, 77),
-                                                  (128, 1, 2, 2, 64, 64, 128), (40, 3, 2, 1, 32, 17, 40)])
+                                                  (128, 1, 2, 2, 64, 64, 128), (40, 3, 2, 1, 32, 17, 40),
+                                                  (300, 2, 4, 2, 128, 0, 300), (520, 1, 2, 1, 64, 256, 520),
+                                                  (257, 1, 2, 2, 128, 129, 257), (384, 3, 2, 2, 64, 0, 384)])
 def test_attention(T, Bsz, H, KVH, hd, t0, t1):
+    """Tensor-core kernel for hd 64/128 (SIMT for 32) vs the oracle's exact causal attention. Bound: the final
+    bf16 rounding (1 ulp, 2 allowed) plus the bf16 rounding of the unnormalised probabilities fed to the PV
+    tensor-core product (relative 2^-9 each, so |err| <= 2^-9 * sum_j P_j |v_j|; 2^-8 allowed)."""
     need_gpu()
     rng = np.random.default_rng(T + H + hd)
     qd, kvd = H * hd, KVH * hd
@@ -159,10 +164,13 @@ def test_attention(T, Bsz, H, KVH, hd, t0, t1):
         rows = np.arange(T) * Bsz + b
         q, k, v = x[rows, :qd], x[rows, qd:qd + kvd], x[rows, qd + kvd:]
         ref = OF.causal_attention(q, k, v, H, KVH, hd, scale, lambda z: z)
+        pv_abs = OF.causal_attention(q, k, np.abs(v), H, KVH, hd, scale, lambda z: z)
         g = got[rows]
         assert np.all(g[:t0] == 0)
+        assert np.all(g[t1:] == 0)
         err = np.abs(g[t0:t1] - ref[t0:t1])
-        assert np.all(err <= 2 * bf16_ulp(ref[t0:t1]) + 1e-4), err.max()
+        bound = 2 * bf16_ulp(ref[t0:t1]) + 2.0 ** -8 * pv_abs[t0:t1] + 1e-6
+        assert np.all(err <= bound), (err - bound).max()
 
 
 def test_rope():
