@@ -15,10 +15,11 @@ from synth import host_image
 def fill_host_images(plan: Plan, base_ptr: int, ada_ptr: int | None):
     """Write the seeded model (and adapters) into host buffers laid out as `plan` says."""
     tens = plan.tensors()
-    host_image.fill_base(base_ptr, [(n, r, c, off, l) for (n, r, c, off, l, _) in tens])
+    dt = getattr(plan.model, "dtype", "bf16")
+    host_image.fill_base(base_ptr, [(n, r, c, off, l) for (n, r, c, off, l, _) in tens], dt)
     if plan.sizes.host_adapter_bytes and ada_ptr:
         items = [(n, r, c, off, a, is_b, tens[base_t][2]) for (n, r, c, off, a, is_b, base_t, _) in plan.atensors()]
-        host_image.fill_adapters(ada_ptr, items, plan.adapters)
+        host_image.fill_adapters(ada_ptr, items, plan.adapters, dt)
 
 
 def build_host_images(plan: Plan):

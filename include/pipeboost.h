@@ -25,6 +25,8 @@
  *     must not.
  *   - Data type: weights and LoRA factors are bf16 (north star; the paper never
  *     states its dtype). Residual stream and logits are fp32.
+ *     pb_model_desc.dtype = PB_DTYPE_F32 selects the fp32 debug-parity path (same
+ *     calls, same layouts with 4-byte elements).
  */
 #ifndef PIPEBOOST_H
 #define PIPEBOOST_H
@@ -55,6 +57,12 @@ typedef enum {
 
 typedef enum { PB_ARCH_OPT = 0, PB_ARCH_LLAMA = 1 } pb_arch;
 
+/* Storage type of the weights and LoRA factors (SURVEY.md §8(c) "Tolerances"):
+ *   PB_DTYPE_BF16 — the product path (tcgen05 merge / GEMM / attention), gated at 1e-2 relative;
+ *   PB_DTYPE_F32  — fp32 debug-parity path: weights, factors and every activation fp32, merge and
+ *                   projections on CUDA-core FFMA; gated at 1e-4 relative. Not timed. */
+typedef enum { PB_DTYPE_BF16 = 0, PB_DTYPE_F32 = 1 } pb_dtype;
+
 /* Decoder description (HF conventions). */
 typedef struct {
     int32_t arch;          /* pb_arch */
@@ -68,6 +76,7 @@ typedef struct {
     int32_t tied;          /* OPT: LM head tied to the token embedding */
     float norm_eps;        /* 1e-5 */
     float rope_theta;      /* 1e4 (Llama) */
+    int32_t dtype;         /* pb_dtype of weights and adapters (0 = bf16) */
 } pb_model_desc;
 
 /* LoRA targets (bit mask). OPT: Q,K,V,O,FC1,FC2. Llama: Q,K,V,O,GATE,UP,DOWN. */

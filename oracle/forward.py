@@ -15,6 +15,8 @@ Modes
            a single rounding at every storage point — norm outputs, q/k/v (after
            bias/scale/RoPE), attention probabilities P, attention output, MLP
            hidden -> bf16 (RNE); residual stream h and logits -> fp32.
+  'f32'  : the fp32 debug-parity contract (PB_DTYPE_F32 models): the same storage
+           points, every one rounded RNE to fp32.
 
 Layer-by-layer loops over heads in plain numpy; no blocking, no fusion.
 """
@@ -31,6 +33,8 @@ def _rounders(mode):
         return ident, ident
     if mode == "bf16":
         return rne_bf16, rne_f32
+    if mode == "f32":
+        return rne_f32, rne_f32
     raise ValueError(mode)
 
 

@@ -15,7 +15,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .numerics import bf16_bits_to_f64, f64_to_bf16_bits
+from .numerics import bf16_bits_to_f64, f64_to_bf16_bits, rne_f32
 
 
 def merge_f64(W: np.ndarray, B: np.ndarray, A: np.ndarray, scale: float) -> np.ndarray:
@@ -29,3 +29,12 @@ def merge_bf16_bits(W_bits: np.ndarray, B_bits: np.ndarray, A_bits: np.ndarray, 
     B = bf16_bits_to_f64(B_bits)
     A = bf16_bits_to_f64(A_bits)
     return f64_to_bf16_bits(merge_f64(W, B, A, scale))
+
+
+def merge_f32_values(W: np.ndarray, B: np.ndarray, A: np.ndarray, scale: float) -> np.ndarray:
+    """fp32 debug-parity models (SURVEY.md §8(c) "Tolerances", 1e-4 gate): RNE_f32(W + scale * B @ A),
+    W, B, A given as fp32 values. Each fp32*fp32 product is exact in fp64 (48 significant bits); the
+    r-term sum rounds in fp64 (relative error < r * 2^-53), far below the one fp32 rounding at the end.
+    Returned as a float32 array."""
+    Wd, Bd, Ad = (np.asarray(x, dtype=np.float64) for x in (W, B, A))
+    return rne_f32(merge_f64(Wd, Bd, Ad, scale)).astype(np.float32)

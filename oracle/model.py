@@ -19,7 +19,7 @@ import numpy as np
 import synth
 
 from . import plan as P
-from .merge import merge_bf16_bits
+from .merge import merge_bf16_bits, merge_f32_values
 from .numerics import bf16_bits_to_f64
 
 
@@ -33,6 +33,8 @@ class OracleWeights:
         P.build_tables(pl)
         self.tensors = {t.name: t for t in pl.tensors}
         self.atensors = pl.atensors
+        # fp32 debug-parity models store fp32 values (float32 arrays) where bf16 models store bf16 bits
+        self.dtype = getattr(model, "dtype", "bf16")
 
     def _source_name(self, name: str) -> str:
         t = self.tensors[name]
@@ -42,17 +44,17 @@ class OracleWeights:
 
     def base_bits(self, name: str) -> np.ndarray:
         t = self.tensors[name]
-        return synth.base_values(self._source_name(name), t.rows, t.cols)
+        return synth.base_values(self._source_name(name), t.rows, t.cols, self.dtype)
 
     def adapter_bits(self, at) -> np.ndarray:
         ad = self.adapters[at.adapter]
         _, _, out_f, in_f = P.target_geometry(self.model, at.target)
         return synth.adapter_values(at.adapter, at.name, at.factor, at.rows, at.cols,
-                                    in_f, ad.rank, ad.scale)
+                                    in_f, ad.rank, ad.scale, self.dtype)
 
     def merged_bits(self, name: str, adapter: int | None) -> np.ndarray:
-        """bf16 bits of the base tensor with adapter `adapter` merged into every
-        adapted row range (None: no merge)."""
+        """bf16 bits (fp32 models: float32 values) of the base tensor with adapter `adapter` merged into
+        every adapted row range (None: no merge)."""
         W = self.base_bits(name).copy()
         if adapter is None:
             return W
@@ -67,11 +69,15 @@ class OracleWeights:
             B = self.adapter_bits(f["B"])
             r0 = f["A"].row0
             rows = B.shape[0]
-            W[r0:r0 + rows] = merge_bf16_bits(W[r0:r0 + rows], B, A, ad.scale)
+            if self.dtype == "f32":
+                W[r0:r0 + rows] = merge_f32_values(W[r0:r0 + rows], B, A, ad.scale)
+            else:
+                W[r0:r0 + rows] = merge_bf16_bits(W[r0:r0 + rows], B, A, ad.scale)
         return W
 
     def get(self, name: str, adapter: int | None) -> np.ndarray:
         """fp64 values of the (merged) tensor, shaped [rows, cols] (1-row tensors flattened)."""
         t = self.tensors[name]
-        x = bf16_bits_to_f64(self.merged_bits(name, adapter))
+        raw = self.merged_bits(name, adapter)
+        x = raw.astype(np.float64) if self.dtype == "f32" else bf16_bits_to_f64(raw)
         return x.reshape(-1) if t.rows == 1 else x

@@ -30,6 +30,11 @@ from synth.configs import AdapterDesc, ModelDesc
 ALIGN = 4096
 BF16 = 2
 
+
+def elem_size(m: ModelDesc) -> int:
+    """Bytes per weight / LoRA-factor element: 2 (bf16) or 4 (fp32 debug-parity path)."""
+    return 4 if getattr(m, "dtype", "bf16") == "f32" else BF16
+
 STAGE = "stage"
 INTERLEAVE = "interleave"
 
@@ -56,10 +61,11 @@ class Tensor:
     layer: int          # -1 for non-layer tensors
     host_off: int = 0
     dev_off: int = 0
+    es: int = BF16      # element size
 
     @property
     def bytes(self) -> int:
-        return self.rows * self.cols * BF16
+        return self.rows * self.cols * self.es
 
 
 @dataclass
@@ -75,10 +81,11 @@ class ATensor:           # one LoRA factor of one adapter target
     base: int           # id of the base tensor it modifies
     row0: int           # first row of the base tensor it modifies
     off: int = 0        # host offset == device offset in the adapter region
+    es: int = BF16
 
     @property
     def bytes(self) -> int:
-        return self.rows * self.cols * BF16
+        return self.rows * self.cols * self.es
 
 
 @dataclass
@@ -215,7 +222,7 @@ def build_tables(plan: Plan) -> None:
     host = 0
     by_name = {}
     for i, (n, r, c, l) in enumerate(names):
-        t = Tensor(i, n, r, c, l)
+        t = Tensor(i, n, r, c, l, es=elem_size(m))
         dev = round_up(dev)
         t.dev_off = dev
         dev += t.bytes
@@ -241,7 +248,8 @@ def build_tables(plan: Plan) -> None:
                 base_sfx, row0, out_f, in_f = target_geometry(m, tgt)
                 base = by_name[f"L{l}.{base_sfx}"]
                 for factor, (r, c) in (("A", (ad.rank, in_f)), ("B", (out_f, ad.rank))):
-                    at = ATensor(aid, f"A{a}.L{l}.{tgt}.{factor}", r, c, l, a, tgt, factor, base.id, row0)
+                    at = ATensor(aid, f"A{a}.L{l}.{tgt}.{factor}", r, c, l, a, tgt, factor, base.id, row0,
+                                 es=elem_size(m))
                     off = round_up(off)
                     at.off = off
                     off += at.bytes
@@ -289,7 +297,7 @@ def build_chunks(plan: Plan) -> None:
     cid = 0
     per_tensor = {}
     for t in plan.tensors:
-        row_bytes = t.cols * BF16
+        row_bytes = t.cols * t.es
         rpc = rows_per_chunk(row_bytes, cb)
         lst = []
         for (p0, p1, g) in pieces(plan, t):
@@ -304,7 +312,7 @@ def build_chunks(plan: Plan) -> None:
         plan.chunks += lst
     per_atensor = {}
     for at in plan.atensors:
-        row_bytes = at.cols * BF16
+        row_bytes = at.cols * at.es
         rpc = rows_per_chunk(row_bytes, cb)
         g = layer_loader(plan, at.layer)   # part g of every adapter goes to the loader of those layers
         lst, r = [], 0
@@ -399,7 +407,8 @@ def dump(plan: Plan) -> str:
     m, o = plan.model, plan.opts
     out = ["pipeboost-plan 1",
            f"model arch={m.arch} layers={m.n_layers} d_model={m.d_model} heads={m.n_heads} "
-           f"kv_heads={m.n_kv_heads} d_ffn={m.d_ffn} vocab={m.vocab} max_pos={m.max_pos} tied={m.tied}",
+           f"kv_heads={m.n_kv_heads} d_ffn={m.d_ffn} vocab={m.vocab} max_pos={m.max_pos} tied={m.tied} "
+           f"dtype={getattr(m, 'dtype', 'bf16')}",
            f"gpus {plan.n_gpus} policy={o.policy} vocab_sliced={o.vocab_sliced} chunk_bytes={o.chunk_bytes} "
            f"prefill_chunks={o.prefill_chunks} host_alias_layers={o.host_alias_layers}"]
     for a, ad in enumerate(plan.adapters):

@@ -17,6 +17,7 @@ PB_MERGE_ALL = -2
 PB_OK, PB_EINVAL, PB_EPARTITION, PB_EPROTOCOL, PB_ECUDA, PB_ENOMEM, PB_ENUMERIC, PB_EUNSUPPORTED = \
     0, -1, -2, -3, -4, -6, -7, -8
 PB_ARCH_OPT, PB_ARCH_LLAMA = 0, 1
+PB_DTYPE_BF16, PB_DTYPE_F32 = 0, 1
 PB_LOAD_STAGE, PB_LOAD_INTERLEAVE = 0, 1
 TARGET_BITS = {"q": 1, "k": 2, "v": 4, "o": 8, "fc1": 16, "fc2": 32, "gate": 64, "up": 128, "down": 256}
 
@@ -30,7 +31,7 @@ class PBError(RuntimeError):
 class pb_model_desc(C.Structure):
     _fields_ = [("arch", C.c_int32), ("n_layers", C.c_int32), ("d_model", C.c_int32), ("n_heads", C.c_int32),
                 ("n_kv_heads", C.c_int32), ("d_ffn", C.c_int32), ("vocab", C.c_int32), ("max_pos", C.c_int32),
-                ("tied", C.c_int32), ("norm_eps", C.c_float), ("rope_theta", C.c_float)]
+                ("tied", C.c_int32), ("norm_eps", C.c_float), ("rope_theta", C.c_float), ("dtype", C.c_int32)]
 
 
 class pb_adapter_desc(C.Structure):
@@ -163,7 +164,8 @@ def check(status):
 
 def model_desc(m) -> pb_model_desc:
     return pb_model_desc(PB_ARCH_OPT if m.arch == "opt" else PB_ARCH_LLAMA, m.n_layers, m.d_model, m.n_heads,
-                         m.n_kv_heads, m.d_ffn, m.vocab, m.max_pos, m.tied, m.norm_eps, m.rope_theta)
+                         m.n_kv_heads, m.d_ffn, m.vocab, m.max_pos, m.tied, m.norm_eps, m.rope_theta,
+                         PB_DTYPE_F32 if getattr(m, "dtype", "bf16") == "f32" else PB_DTYPE_BF16)
 
 
 def adapter_desc(a) -> pb_adapter_desc:

@@ -75,7 +75,7 @@ cudaError_t launch_norm(const float* h, int ldh, __nv_bfloat16* out, int ldo, in
                         const __nv_bfloat16* beta, float eps, cudaStream_t s);
 
 struct EmbedSrc {
-    const __nv_bfloat16* base[8];  // embedding table of each owner (peer pointers allowed)
+    const void* base[8];           // embedding table of each owner (peer pointers allowed); bf16 or fp32
     int slice_begin[9];            // vocab rows [slice_begin[i], slice_begin[i+1]) live on owner i
     int n;
 };
@@ -113,5 +113,24 @@ cudaError_t warm_merge_kernels();
 cudaError_t warm_gemm_kernels();
 cudaError_t warm_simt_kernels();
 cudaError_t warm_attention_kernels();
+cudaError_t warm_f32_kernels();
+
+// ---------------------------------------------------------------- fp32 debug-parity path (f32.cu)
+// Same operations as above with fp32 weights and activations on CUDA-core FFMA (PB_DTYPE_F32; not timed).
+cudaError_t launch_merge_f32(const float* W, float* Wout, int64_t ldw, int rows, int cols, const float* B,
+                             const float* A, int rank, float scale, cudaStream_t s);
+cudaError_t launch_gemm_f32(const float* X, int ldx, int M_begin, int M_end, const float* W, int N, int K, int epi,
+                            const float* bias, int relu, float scale, int scale_cols, float* out, int ldo, int up_row0,
+                            cudaStream_t s);
+cudaError_t launch_norm_f32(const float* h, int ldh, float* out, int ldo, int rows, int d, const float* gamma,
+                            const float* beta, float eps, cudaStream_t s);
+cudaError_t launch_embed_f32(const EmbedSrc& E, const float* pos, const int32_t* tok, float* h, int d, int r0, int r1,
+                             int B, cudaStream_t s);
+cudaError_t launch_rope_f32(float* qkv, int ld, int r0, int r1, int B, int n_q, int n_k, int hd, int k_col0,
+                            const float2* table, cudaStream_t s);
+cudaError_t launch_attention_f32(const float* qkv, int ld, float* out, int ldo, int t0, int t1, int B, int n_heads,
+                                 int n_kv_heads, int hd, int k_col0, int v_col0, float score_scale, cudaStream_t s);
+cudaError_t launch_logits_f32(const float* y, int B, int d, const float* E, int v0, int v1, float* logits, int ldl,
+                              cudaStream_t s);
 
 }  // namespace pb

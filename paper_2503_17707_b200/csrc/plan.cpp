@@ -133,6 +133,7 @@ extern "C" pb_status pb_plan_create(const pb_model_desc* model, const pb_adapter
     if (m.arch == PB_ARCH_OPT && (m.n_kv_heads != m.n_heads || m.max_pos < 1))
         return pb::fail(PB_EINVAL, "OPT needs n_kv_heads == n_heads and max_pos >= 1");
     if (m.arch == PB_ARCH_LLAMA && m.tied) return pb::fail(PB_EUNSUPPORTED, "tied Llama head");
+    if (m.dtype != PB_DTYPE_BF16 && m.dtype != PB_DTYPE_F32) return pb::fail(PB_EINVAL, "dtype %d", m.dtype);
     if (n_gpus < 1 || n_gpus > kMaxGpus) return pb::fail(PB_EINVAL, "n_gpus must be in [1, 8]");
     if (n_gpus > m.n_layers) return pb::fail(PB_EPARTITION, "n_gpus %d > n_layers %d", n_gpus, m.n_layers);
     if (n_adapters < 0 || (n_adapters > 0 && !adapters)) return pb::fail(PB_EINVAL, "bad adapters");
@@ -176,7 +177,7 @@ extern "C" pb_status pb_plan_create(const pb_model_desc* model, const pb_adapter
     std::unordered_map<std::string, int32_t> idx;
     for (auto& n : names) {
         if (n.rows > INT32_MAX || n.cols > INT32_MAX) { delete p; return pb::fail(PB_EINVAL, "tensor too large"); }
-        TensorRec t{n.name, (int32_t)n.rows, (int32_t)n.cols, n.layer, 0, 0};
+        TensorRec t{n.name, (int32_t)n.rows, (int32_t)n.cols, n.layer, 0, 0, m.dtype == PB_DTYPE_F32 ? 4 : 2};
         dev = round_up(dev, kAlign);
         t.dev_off = dev;
         dev += t.bytes();
@@ -214,6 +215,7 @@ extern "C" pb_status pb_plan_create(const pb_model_desc* model, const pb_adapter
                     at.cols = f ? adapters[a].rank : (int32_t)g.in;
                     at.layer = l; at.adapter = a; at.target_bit = bit; at.is_B = f;
                     at.base = base; at.row0 = (int32_t)g.row0;
+                    at.es = m.dtype == PB_DTYPE_F32 ? 4 : 2;
                     aoff = round_up(aoff, kAlign);
                     at.off = aoff;
                     aoff += at.bytes();
@@ -350,9 +352,9 @@ static std::string dump_string(const pb_plan* p) {
     Out o;
     const pb_model_desc& m = p->model;
     o.f("pipeboost-plan 1\n");
-    o.f("model arch=%s layers=%d d_model=%d heads=%d kv_heads=%d d_ffn=%d vocab=%d max_pos=%d tied=%d\n",
+    o.f("model arch=%s layers=%d d_model=%d heads=%d kv_heads=%d d_ffn=%d vocab=%d max_pos=%d tied=%d dtype=%s\n",
         m.arch == PB_ARCH_OPT ? "opt" : "llama", m.n_layers, m.d_model, m.n_heads, m.n_kv_heads, m.d_ffn, m.vocab,
-        m.max_pos, m.tied);
+        m.max_pos, m.tied, m.dtype == PB_DTYPE_F32 ? "f32" : "bf16");
     o.f("gpus %d policy=%s vocab_sliced=%d chunk_bytes=%" PRId64 " prefill_chunks=%d host_alias_layers=%d\n", p->n_gpus,
         p->opts.policy == PB_LOAD_STAGE ? "stage" : "interleave", p->opts.vocab_sliced, p->opts.chunk_bytes,
         p->opts.prefill_chunks, p->opts.host_alias_layers);

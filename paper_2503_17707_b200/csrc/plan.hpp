@@ -15,8 +15,9 @@ struct TensorRec {
     std::string name;
     int32_t rows, cols, layer;
     int64_t host_off, dev_off;
-    int64_t bytes() const { return (int64_t)rows * cols * 2; }
-    int64_t row_bytes() const { return (int64_t)cols * 2; }
+    int32_t es = 2;   // element size: 2 (bf16) or 4 (fp32)
+    int64_t bytes() const { return (int64_t)rows * cols * es; }
+    int64_t row_bytes() const { return (int64_t)cols * es; }
 };
 
 struct ATensorRec {
@@ -27,8 +28,9 @@ struct ATensorRec {
     int32_t base;         // base tensor id
     int32_t row0;         // first base row it modifies
     int64_t off;
-    int64_t bytes() const { return (int64_t)rows * cols * 2; }
-    int64_t row_bytes() const { return (int64_t)cols * 2; }
+    int32_t es = 2;
+    int64_t bytes() const { return (int64_t)rows * cols * es; }
+    int64_t row_bytes() const { return (int64_t)cols * es; }
 };
 
 struct ChunkRec {
@@ -70,6 +72,8 @@ struct pb_plan {
 
     // derived helpers
     int32_t head_dim() const { return model.d_model / model.n_heads; }
+    bool f32() const { return model.dtype == PB_DTYPE_F32; }
+    int32_t es() const { return f32() ? 4 : 2; }
     int32_t stage_of_layer(int32_t l) const;
     int32_t find_tensor(const std::string& name) const;   // -1 if absent
 };

@@ -116,13 +116,14 @@ WsLayout pb::ws_layout(const pb_plan* p, int32_t batch, int32_t seq) {
     L.flags = o;   o = al(o + 4 * (int64_t)L.n_words);
     L.tokens = o;  o = al(o + 4 * rows);
     L.h = o;       o = al(o + 4 * rows * d);
-    L.x = o;       o = al(o + 2 * rows * d);
+    const int64_t ea = p->es();   // activation element size: bf16 (product path) or fp32 (debug-parity path)
+    L.x = o;       o = al(o + ea * rows * d);
     L.n_qkv = k > 1 ? max_stage_layers(p) : 1;
-    L.qkv_stride = al(2 * rows * qkv_dim(p));
+    L.qkv_stride = al(ea * rows * qkv_dim(p));
     L.qkv = o;     o += L.qkv_stride * L.n_qkv;
-    L.attn = o;    o = al(o + 2 * rows * qd);
-    L.mlp = o;     o = al(o + 2 * rows * f);
-    L.y = o;       o = al(o + 2 * (int64_t)batch * d);
+    L.attn = o;    o = al(o + ea * rows * qd);
+    L.mlp = o;     o = al(o + ea * rows * f);
+    L.y = o;       o = al(o + ea * (int64_t)batch * d);
     L.logits = o;  o = al(o + 4 * (int64_t)batch * m.vocab);
     L.tok_out = o; o = al(o + 4 * (int64_t)batch);
     L.nan = o;     o = al(o + 4);
@@ -161,7 +162,7 @@ static pb_status build_merge_jobs(pb_ctx* c) {
             if (ch.is_adapter || ch.tensor != mr.base || ch.loader != c->rank) continue;
             const int32_t ra = std::max(ch.r0, mr.row0), rb = std::min(ch.r1, mr.row0 + mr.rows);
             if (rb <= ra) continue;
-            if (rank % 8 != 0)
+            if (rank % 8 != 0 && !p->f32())
                 return fail(PB_EUNSUPPORTED, "merge needs rank %% 8 == 0 (TMA 16-byte row pitch), got %d", rank);
             for (int inplace = 1; inplace >= 0; --inplace) {
                 if (!inplace && !c->adapted) continue;
@@ -181,8 +182,16 @@ static pb_status build_merge_jobs(pb_ctx* c) {
                                            (int64_t)ra * bt.row_bytes();
                 const char* Bp = c->adapters + Bf.off + (int64_t)(ra - mr.row0) * Bf.row_bytes();
                 const char* Ap = c->adapters + A.off;
-                if (!make_merge_maps(&j.maps, W, bt.cols, j.rows, j.cols, Bp, Ap, rank, err, sizeof err, Wout))
+                if (p->f32()) {
+                    j.W = reinterpret_cast<const float*>(W);
+                    j.Wout = reinterpret_cast<float*>(Wout);
+                    j.Bp = reinterpret_cast<const float*>(Bp);
+                    j.Ap = reinterpret_cast<const float*>(Ap);
+                    j.ldw = bt.cols;
+                } else if (!make_merge_maps(&j.maps, W, bt.cols, j.rows, j.cols, Bp, Ap, rank, err, sizeof err,
+                                            Wout)) {
                     return fail(PB_EINVAL, "merge map: %s", err);
+                }
                 c->jobs_of_chunk[ch.id].push_back((int32_t)c->jobs.size());
                 c->jobs.push_back(j);
             }
@@ -227,6 +236,7 @@ static cudaEvent_t landed_ev(pb_ctx* c, int32_t chunk) { return c->landed[c->lan
 
 static pb_status build_prefill_maps(pb_ctx* c) {
     const pb_plan* p = c->plan;
+    if (p->f32()) return PB_OK;   // the fp32 path's SIMT kernels take plain pointers
     const auto& m = p->model;
     const int64_t d = m.d_model, qd = (int64_t)m.n_heads * p->head_dim(), f = m.d_ffn;
     const int64_t R = c->L.max_rows;
@@ -295,6 +305,7 @@ extern "C" pb_status pb_ctx_create(const pb_plan* plan, int32_t rank, const void
             if (e == cudaSuccess) e = warm_gemm_kernels();
             if (e == cudaSuccess) e = warm_simt_kernels();
             if (e == cudaSuccess) e = warm_attention_kernels();
+            if (e == cudaSuccess) e = warm_f32_kernels();
             if (e != cudaSuccess) return fail(PB_ECUDA, "kernel load: %s", cudaGetErrorString(e));
             warmed.insert(dev);
         }
@@ -664,13 +675,31 @@ cudaError_t wait_tensor(pb_ctx* c, int l, const char* sfx) {
     return wait_word(c, c->L.f_tensor + t, c->comp);
 }
 
+// fp32 debug-parity path: tensor sfx of layer l (or a non-layer tensor when l < 0); adapter >= 0 selects that
+// adapter's out-of-place copy where it has one.
+const float* wt_f32(pb_ctx* c, int l, const char* sfx, int adapter = -1) {
+    const pb_plan* p = c->plan;
+    const int32_t t = p->find_tensor(l >= 0 ? "L" + std::to_string(l) + "." + sfx : std::string(sfx));
+    if (t < 0) return nullptr;
+    if (adapter >= 0 && c->adapted) {
+        const int64_t off = p->adapted_off[(size_t)adapter * p->tensors.size() + t];
+        if (off >= 0) return reinterpret_cast<const float*>(c->adapted + off);
+    }
+    return reinterpret_cast<const float*>(c->weights + p->tensors[t].dev_off);
+}
+
+// The fp32 twin of run_layer (PB_DTYPE_F32): same steps, same waits, SIMT fp32 kernels (f32.cu).
 // Layer l on token rows [r0, r1) (prompt positions [ta, tb)). On the first prompt chunk each step waits
 // only for the tensors it reads (layout is in compute order), so a layer starts while its tail loads.
 // Rows [r0, r1) are absolute workspace rows; attention / RoPE see the B-sequence block that starts at
 // row_base (token-major inside it); adapter >= 0 selects that adapter's out-of-place weight copies.
+pb_status run_layer_f32(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, bool first_chunk, int row_base,
+                        int adapter);
+
 pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, bool first_chunk, int row_base,
                     int adapter) {
     const pb_plan* p = c->plan;
+    if (p->f32()) return run_layer_f32(c, l, r0, r1, ta, tb, B, first_chunk, row_base, adapter);
     const auto& m = p->model;
     const bool opt = m.arch == PB_ARCH_OPT;
     const int d = m.d_model, hd = p->head_dim(), H = m.n_heads, KVH = m.n_kv_heads, qd = H * hd, kvd = KVH * hd;
@@ -762,6 +791,76 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, boo
         CU(need("down"));
         a = G(r0, d, f, EPI_RESID, nullptr, 0, 1.f, 0, h, d);
         CU(gemm(c->map_mlp, lm.down, a, d));
+    }
+    c->n_launches += opt ? 7 : 8;
+    return PB_OK;
+}
+
+
+pb_status run_layer_f32(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, bool first_chunk, int row_base,
+                        int adapter) {
+    const pb_plan* p = c->plan;
+    const auto& m = p->model;
+    const bool opt = m.arch == PB_ARCH_OPT;
+    const int d = m.d_model, hd = p->head_dim(), H = m.n_heads, KVH = m.n_kv_heads, qd = H * hd, kvd = KVH * hd;
+    const int f = m.d_ffn, qdim = qkv_dim(p);
+    const WsLayout& L = c->L;
+    float* h = reinterpret_cast<float*>(c->ws + L.h);
+    float* x = reinterpret_cast<float*>(c->ws + L.x);
+    const int li = L.n_qkv > 1 ? l - p->stages[c->rank].first : 0;
+    float* qkv = reinterpret_cast<float*>(c->ws + L.qkv + L.qkv_stride * li);
+    float* attn = reinterpret_cast<float*>(c->ws + L.attn);
+    float* mlp = reinterpret_cast<float*>(c->ws + L.mlp);
+    cudaStream_t s = c->comp;
+    const int rows = r1 - r0;
+    auto W = [&](const char* sfx) { return wt_f32(c, l, sfx, adapter); };
+    auto need = [&](const char* sfx) -> cudaError_t { return first_chunk ? wait_tensor(c, l, sfx) : cudaSuccess; };
+    auto gemm = [&](const float* X, int ldx, const float* Wt, int N, int K, int epi, const float* bias, int relu,
+                    float scale, int scale_cols, float* out, int ldo, int n_w_rows) -> cudaError_t {
+        const int pi = prof_begin(c, K_GEMM, s);
+        cudaError_t e = launch_gemm_f32(X, ldx, r0, r1, Wt, N, K, epi, bias, relu, scale, scale_cols, out, ldo, f, s);
+        prof_end(c, pi, s, 2.0 * rows * n_w_rows * K, 4.0 * ((double)rows * K + (double)n_w_rows * K + 2.0 * rows * N));
+        return e;
+    };
+    auto norm = [&](const char* g_name, const char* b_name) -> cudaError_t {
+        const int pi = prof_begin(c, K_NORM, s);
+        cudaError_t e = launch_norm_f32(h + (size_t)r0 * d, d, x + (size_t)r0 * d, d, rows, d, W(g_name),
+                                        opt ? W(b_name) : nullptr, m.norm_eps, s);
+        prof_end(c, pi, s, 8.0 * rows * d, 8.0 * rows * d);
+        return e;
+    };
+    CU(need(opt ? "ln1_b" : "ln1_g"));
+    CU(norm("ln1_g", "ln1_b"));
+    CU(need(opt ? "qkv_b" : "qkv"));
+    CU(gemm(x, d, W("qkv"), qdim, d, EPI_BF16, opt ? W("qkv_b") : nullptr, 0, opt ? 1.0f / sqrtf((float)hd) : 1.0f,
+            opt ? d : 0, qkv, qdim, qdim));
+    if (!opt) {
+        const int pi = prof_begin(c, K_ROPE, s);
+        CU(launch_rope_f32(qkv + (size_t)row_base * qdim, qdim, r0 - row_base, r1 - row_base, B, H, KVH, hd, qd,
+                           reinterpret_cast<const float2*>(c->ws + L.rope), s));
+        prof_end(c, pi, s, 6.0 * rows * (qd + kvd) / 2, 8.0 * rows * (qd + kvd));
+    }
+    {
+        const int pi = prof_begin(c, K_ATTN, s);
+        CU(launch_attention_f32(qkv + (size_t)row_base * qdim, qdim, attn + (size_t)row_base * qd, qd, ta, tb, B, H,
+                                KVH, hd, qd, qd + kvd, opt ? 1.0f : 1.0f / sqrtf((float)hd), s));
+        const double pairs = (double)B * ((double)tb * (tb + 1) / 2 - (double)ta * (ta + 1) / 2);
+        prof_end(c, pi, s, 4.0 * pairs * H * hd, 4.0 * rows * qd * 2 + 4.0 * B * tb * 2 * kvd);
+    }
+    CU(need(opt ? "o_b" : "o"));
+    CU(gemm(attn, qd, W("o"), d, qd, EPI_RESID, opt ? W("o_b") : nullptr, 0, 1.f, 0, h, d, d));
+    CU(need(opt ? "ln2_b" : "ln2_g"));
+    CU(norm("ln2_g", "ln2_b"));
+    if (opt) {
+        CU(need("fc1_b"));
+        CU(gemm(x, d, W("fc1"), f, d, EPI_BF16, W("fc1_b"), 1, 1.f, 0, mlp, f, f));
+        CU(need("fc2_b"));
+        CU(gemm(mlp, f, W("fc2"), d, f, EPI_RESID, W("fc2_b"), 0, 1.f, 0, h, d, d));
+    } else {
+        CU(need("gate_up"));
+        CU(gemm(x, d, W("gate_up"), f, d, EPI_SILU_MUL, nullptr, 0, 1.f, 0, mlp, f, 2 * f));
+        CU(need("down"));
+        CU(gemm(mlp, f, W("down"), d, f, EPI_RESID, nullptr, 0, 1.f, 0, h, d, d));
     }
     c->n_launches += opt ? 7 : 8;
     return PB_OK;
@@ -895,9 +994,14 @@ pb_status issue_group(Issuer& I, size_t gi) {
                     ++mops;
                 }
             const int pi = prof_begin(c, K_MERGE, c->merge);
-            CU(launch_merge(job.maps, job.rows, job.cols, job.rank, job.scale, c->merge));
+            if (p->f32()) {
+                CU(launch_merge_f32(job.W, job.Wout, job.ldw, job.rows, job.cols, job.Bp, job.Ap, job.rank, job.scale,
+                                    c->merge));
+            } else {
+                CU(launch_merge(job.maps, job.rows, job.cols, job.rank, job.scale, c->merge));
+            }
             prof_end(c, pi, c->merge, 2.0 * job.rows * job.cols * job.rank,
-                     4.0 * job.rows * job.cols + 2.0 * job.rank * (job.rows + job.cols));
+                     p->es() * (2.0 * job.rows * job.cols + (double)job.rank * (job.rows + job.cols)));
             ++c->n_launches;
             mops += 1 + prof_ops(c);
         }
@@ -1080,7 +1184,7 @@ pb_status issue_item(Issuer& I, const Item& it) {
                 for (auto& ch : p->chunks)
                     if (!ch.is_adapter && ch.tensor == et) sl[ch.loader + 1] = std::max(sl[ch.loader + 1], ch.r1);
                 for (int r = 0; r < N; ++r) {
-                    E.base[r] = reinterpret_cast<const __nv_bfloat16*>(c->peers[r].weights + p->tensors[et].dev_off);
+                    E.base[r] = c->peers[r].weights + p->tensors[et].dev_off;
                     E.slice_begin[r] = r == 0 ? 0 : sl[r];
                 }
                 E.slice_begin[N] = INT32_MAX;
@@ -1092,9 +1196,14 @@ pb_status issue_item(Issuer& I, const Item& it) {
                 E.n = 1;
             }
             const int pi = prof_begin(c, K_EMBED, s);
-            CU(launch_embed(E, opt ? wt(c, -1, "pos") : nullptr,
-                            reinterpret_cast<const int32_t*>(c->ws + L.tokens) + row_base, h + (size_t)row_base * d, d,
-                            r0 - row_base, r1 - row_base, Bk, s));
+            if (p->f32())
+                CU(launch_embed_f32(E, opt ? wt_f32(c, -1, "pos") : nullptr,
+                                    reinterpret_cast<const int32_t*>(c->ws + L.tokens) + row_base,
+                                    h + (size_t)row_base * d, d, r0 - row_base, r1 - row_base, Bk, s));
+            else
+                CU(launch_embed(E, opt ? wt(c, -1, "pos") : nullptr,
+                                reinterpret_cast<const int32_t*>(c->ws + L.tokens) + row_base, h + (size_t)row_base * d,
+                                d, r0 - row_base, r1 - row_base, Bk, s));
             prof_end(c, pi, s, (opt ? 1.0 : 0.0) * (r1 - r0) * d, (r1 - r0) * d * (opt ? 8.0 : 6.0));
             ++c->n_launches;
             break;
@@ -1123,14 +1232,19 @@ pb_status issue_item(Issuer& I, const Item& it) {
             const float* last = I.mb_mode ? h + (size_t)(T - 1) * d : h + (size_t)(T - 1) * B * d;
             const int ldh = I.mb_mode ? T * d : d;
             const int pi = prof_begin(c, K_NORM, s);
-            CU(launch_norm(last, ldh, y, d, B, d, wt(c, -1, "final_g"), opt ? wt(c, -1, "final_b") : nullptr,
-                           m.norm_eps, s));
+            if (p->f32())
+                CU(launch_norm_f32(last, ldh, reinterpret_cast<float*>(c->ws + L.y), d, B, d, wt_f32(c, -1, "final_g"),
+                                   opt ? wt_f32(c, -1, "final_b") : nullptr, m.norm_eps, s));
+            else
+                CU(launch_norm(last, ldh, y, d, B, d, wt(c, -1, "final_g"), opt ? wt(c, -1, "final_b") : nullptr,
+                               m.norm_eps, s));
             prof_end(c, pi, s, 8.0 * B * d, 6.0 * B * d);
             ++c->n_launches;
             std::vector<int32_t> remote;
             for (int32_t r : owners)
                 if (r != g) {
-                    CU(cudaMemcpyAsync(c->peers[r].ws + L.y, y, (size_t)B * d * 2, cudaMemcpyDeviceToDevice, s));
+                    CU(cudaMemcpyAsync(c->peers[r].ws + L.y, c->ws + L.y, (size_t)B * d * p->es(),
+                                       cudaMemcpyDeviceToDevice, s));
                     remote.push_back(r);
                 }
             CU(signal_ranks(c, L.f_y, remote, s));
@@ -1144,7 +1258,11 @@ pb_status issue_item(Issuer& I, const Item& it) {
             head_slice(p, g, &v0, &v1);
             const __nv_bfloat16* E = reinterpret_cast<const __nv_bfloat16*>(c->weights + p->tensors[ht].dev_off);
             const int pi = prof_begin(c, K_LOGITS, s);
-            CU(launch_logits(y, B, d, E, v0, v1, logits, V, s));
+            if (p->f32())
+                CU(launch_logits_f32(reinterpret_cast<const float*>(c->ws + L.y), B, d,
+                                     reinterpret_cast<const float*>(E), v0, v1, logits, V, s));
+            else
+                CU(launch_logits(y, B, d, E, v0, v1, logits, V, s));
             prof_end(c, pi, s, 2.0 * B * (v1 - v0) * d, 2.0 * (double)(v1 - v0) * d + 4.0 * B * (v1 - v0));
             ++c->n_launches;
             if (g != 0) {

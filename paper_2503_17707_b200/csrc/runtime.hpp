@@ -31,7 +31,11 @@ struct MergeJob {
     int32_t rows, cols, rank;
     float scale;
     std::vector<int32_t> need;   // adapter chunks that must have landed
-    MergeMaps maps;
+    MergeMaps maps;              // bf16 path (TMA)
+    // fp32 debug-parity path: plain pointers
+    const float *W = nullptr, *Bp = nullptr, *Ap = nullptr;
+    float* Wout = nullptr;
+    int64_t ldw = 0;
 };
 
 // One cudaMemcpyAsync of the load list: a run of consecutive load-list chunks that are contiguous (up to

@@ -82,7 +82,7 @@ __global__ void embed_kernel(EmbedSrc E, const __nv_bfloat16* __restrict__ pos, 
     const int id = tok[row];
     int owner = 0;
     while (owner + 1 < E.n && id >= E.slice_begin[owner + 1]) ++owner;
-    const __nv_bfloat16* e = E.base[owner] + (size_t)id * d;
+    const __nv_bfloat16* e = static_cast<const __nv_bfloat16*>(E.base[owner]) + (size_t)id * d;
     const __nv_bfloat16* p = pos ? pos + (size_t)(t + 2) * d : nullptr;   // HF OPT position offset 2
     float* o = h + (size_t)row * d;
     for (int c = threadIdx.x * 8; c < d; c += blockDim.x * 8) {

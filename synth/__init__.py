@@ -85,6 +85,12 @@ def fill_bf16_into(ptr: int, n: int, seed: int, name: str, center: float, a: flo
     lib().pbs_fill_bf16(ctypes.c_void_p(ptr), n, start, seed, name.encode(), center, a)
 
 
+def fill_into(ptr: int, n: int, seed: int, name: str, center: float, a: float, dtype: str = "bf16"):
+    """Write n generator values at ptr as bf16 (RNE) or fp32 (the fp32 debug-parity models)."""
+    f = lib().pbs_fill_f32 if dtype == "f32" else lib().pbs_fill_bf16
+    f(ctypes.c_void_p(ptr), n, 0, seed, name.encode(), center, a)
+
+
 def values_bf16(name: str, shape, seed: int, center: float, a: float) -> np.ndarray:
     """bf16 bit patterns (uint16) of a named tensor, row-major."""
     n = int(np.prod(shape))
@@ -130,14 +136,16 @@ def kind_of(name: str) -> str:
     raise ValueError(name)
 
 
-def base_values(name: str, rows: int, cols: int) -> np.ndarray:
-    """bf16 bits of a base tensor (seed 0x5EED0001)."""
+def base_values(name: str, rows: int, cols: int, dtype: str = "bf16") -> np.ndarray:
+    """bf16 bits (uint16) — or fp32 values for dtype 'f32' — of a base tensor (seed 0x5EED0001)."""
     c, a = dist(kind_of(name))
-    return values_bf16(name, (rows, cols), SEED_WEIGHTS, c, a)
+    fn = values_f32 if dtype == "f32" else values_bf16
+    return fn(name, (rows, cols), SEED_WEIGHTS, c, a)
 
 
 def adapter_values(adapter: int, name: str, factor: str, rows: int, cols: int,
-                   fan_in: int, rank: int, scale: float) -> np.ndarray:
-    """bf16 bits of a LoRA factor (seed 0x5EED0100 + adapter)."""
+                   fan_in: int, rank: int, scale: float, dtype: str = "bf16") -> np.ndarray:
+    """bf16 bits (uint16) — or fp32 values for dtype 'f32' — of a LoRA factor (seed 0x5EED0100 + adapter)."""
     c, a = dist("lora_A" if factor == "A" else "lora_B", fan_in=fan_in, rank=rank, scale=scale)
-    return values_bf16(name, (rows, cols), SEED_ADAPTER0 + adapter, c, a)
+    fn = values_f32 if dtype == "f32" else values_bf16
+    return fn(name, (rows, cols), SEED_ADAPTER0 + adapter, c, a)

@@ -23,6 +23,7 @@ class ModelDesc:
     tied: int            # OPT: lm_head tied to embed
     norm_eps: float = 1e-5
     rope_theta: float = 1e4
+    dtype: str = "bf16"  # weights / LoRA factors: 'bf16' (the product path) or 'f32' (fp32 debug-parity gate)
 
     @property
     def head_dim(self) -> int:
@@ -56,6 +57,8 @@ LLAMA_ALL = ("q", "k", "v", "o", "gate", "up", "down")
 
 TINY_OPT = ModelDesc("opt", 4, 256, 4, 4, 1024, 1024, 128, 1)
 TINY_LLAMA = ModelDesc("llama", 4, 256, 4, 2, 688, 1000, 0, 0)      # GQA tiny shape (HF cross-check)
+TINY_OPT_F32 = ModelDesc("opt", 4, 256, 4, 4, 1024, 1024, 128, 1, dtype="f32")
+TINY_LLAMA_F32 = ModelDesc("llama", 4, 256, 4, 2, 688, 1000, 0, 0, dtype="f32")
 OPT_1_3B = ModelDesc("opt", 24, 2048, 32, 32, 8192, 50272, 2048, 1)
 LLAMA2_7B = ModelDesc("llama", 32, 4096, 32, 32, 11008, 32000, 0, 0)
 OPT_13B = ModelDesc("opt", 40, 5120, 40, 40, 20480, 50272, 2048, 1)
@@ -69,6 +72,8 @@ def lora(rank: int, targets=("q", "v")) -> AdapterDesc:
 
 WORKLOADS = {
     "C1": Workload("C1", TINY_OPT, (lora(8),), 1, 16, (2,), "tiny OPT, 2 shards"),
+    # fp32 debug-parity run of C1 (SURVEY.md §8(c) "Tolerances": the 1e-4 gate; not timed)
+    "C1f32": Workload("C1f32", TINY_OPT_F32, (lora(8),), 1, 16, (2,), "tiny OPT fp32, 2 shards"),
     "C2": Workload("C2", OPT_1_3B, (lora(16),), 1, 128, (1, 2, 4, 8), "OPT-1.3B + r16 q,v"),
     "C3": Workload("C3", LLAMA2_7B, tuple(lora(16) for _ in range(4)), 4, 512, (8,), "Llama-2-7B + 4 adapters"),
     "C4": Workload("C4", OPT_13B, (lora(64, OPT_ALL),), 1, 1024, (2, 4, 8), "OPT-13B + r64 all"),

@@ -15,7 +15,7 @@ import synth
 from oracle import OracleWeights, first_token_logits
 from oracle import forward as OF
 from oracle import plan as P
-from synth.configs import TINY_LLAMA, TINY_OPT, lora
+from synth.configs import TINY_LLAMA, TINY_LLAMA_F32, TINY_OPT, TINY_OPT_F32, lora
 
 
 def hf_state_dict(m, W):
@@ -103,6 +103,29 @@ def test_oracle_matches_hf_transformers_fp64(model):
     rel = np.abs(ours - ref).max() / np.abs(ref).max()
     assert rel < 1e-6, rel          # HF upcasts softmax to fp32: ~3e-8 observed
     assert OF.first_token(ours) == int(np.argmax(ref))
+
+
+@pytest.mark.parametrize("model", [TINY_OPT_F32, TINY_LLAMA_F32], ids=["opt", "llama"])
+def test_f32_oracle_matches_hf_transformers(model):
+    """fp32 debug-parity models (the 1e-4 gate): the oracle's 'exact' mode on the fp32 weights equals HF in
+    float64, and its 'f32' storage mode equals HF run natively in float32 (a third-party fp32 forward) to
+    well inside 1e-4."""
+    ads = (lora(8),)
+    ow = OracleWeights(model, ads)
+    W = lambda n: ow.get(n, 0)
+    toks = synth.tokens(1, 16, model.vocab)[0]
+    exact = OF.forward_logits(model, W, toks, "exact")
+    f32 = OF.forward_logits(model, W, toks, "f32")
+    hf = hf_model(model).double().eval()
+    hf.load_state_dict(hf_state_dict(model, W), strict=False)
+    x = torch.from_numpy(toks.astype(np.int64))[None]
+    with torch.no_grad():
+        ref64 = hf(x).logits[0, -1].numpy()
+        ref32 = hf.float()(x).logits[0, -1].double().numpy()
+    assert np.abs(exact - ref64).max() / np.abs(ref64).max() < 1e-6
+    rel = np.abs(f32 - ref32).max() / np.abs(ref32).max()
+    assert rel < 2e-5, rel
+    assert 0 < np.abs(f32 - exact).max() / np.abs(exact).max() < 1e-5
 
 
 def test_merge_moves_logits():

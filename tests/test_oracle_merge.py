@@ -118,3 +118,63 @@ def test_transpose_identity():
     B = rand_bf16(rng, (9, 3), 0.5)
     A = rand_bf16(rng, (3, 11), 0.5)
     assert np.array_equal(merge_bf16_bits(W, B, A, 2.0).T, merge_bf16_bits(W.T.copy(), A.T.copy(), B.T.copy(), 2.0))
+
+
+# ---------------------------------------------------------------------------------------------------
+# fp32 debug-parity models (SURVEY.md §8(c) "Tolerances", 1e-4 gate): W' = RNE_f32(W + s B A)
+# ---------------------------------------------------------------------------------------------------
+
+def frac_round_sig(q: Fraction, bits: int) -> Fraction:
+    """Round a rational to `bits` significant bits, ties to even (no exponent limits: normal range only)."""
+    if q == 0:
+        return Fraction(0)
+    sign = -1 if q < 0 else 1
+    a = abs(q)
+    e = 0
+    while a >= 2:
+        a /= 2
+        e += 1
+    while a < 1:
+        a *= 2
+        e -= 1
+    scaled = a * (2 ** (bits - 1))
+    n = scaled.numerator // scaled.denominator
+    rem = scaled - n
+    if rem > Fraction(1, 2) or (rem == Fraction(1, 2) and n % 2 == 1):
+        n += 1
+    return sign * Fraction(n, 2 ** (bits - 1)) * (Fraction(2) ** e)
+
+
+@pytest.mark.parametrize("shape", [(3, 1, 5), (4, 2, 3), (5, 8, 7), (2, 16, 3)])
+def test_merge_f32_correctly_rounded_bruteforce(shape):
+    """Exact rationals + hand-written round-half-even to 24 significant bits: the fp32 oracle merge is the
+    correctly rounded value (its fp64 accumulation cannot move a result across an fp32 rounding boundary
+    at these sizes unless the exact value sits within 2^-50 of a tie, which these random draws do not)."""
+    from oracle.merge import merge_f32_values
+    o, r, i = shape
+    rng = np.random.default_rng(100 + sum(shape))
+    W = rng.uniform(-0.05, 0.05, (o, i)).astype(np.float32)
+    B = rng.uniform(-0.5, 0.5, (o, r)).astype(np.float32)
+    A = rng.uniform(-0.5, 0.5, (r, i)).astype(np.float32)
+    s = 2.0
+    got = merge_f32_values(W, B, A, s)
+    assert got.dtype == np.float32
+    for a in range(o):
+        for b in range(i):
+            exact = Fraction(float(W[a, b])) + Fraction(s) * sum(
+                Fraction(float(B[a, k])) * Fraction(float(A[k, b])) for k in range(r))
+            assert Fraction(float(got[a, b])) == frac_round_sig(exact, 24), (a, b)
+
+
+def test_merge_f32_identity_and_one_hot():
+    from oracle.merge import merge_f32_values
+    rng = np.random.default_rng(7)
+    W = rng.uniform(-0.05, 0.05, (6, 9)).astype(np.float32)
+    B = rng.uniform(-0.5, 0.5, (6, 4)).astype(np.float32)
+    assert np.array_equal(merge_f32_values(W, np.zeros_like(B), rng.uniform(-1, 1, (4, 9)).astype(np.float32), 2.0), W)
+    A = np.zeros((4, 9), dtype=np.float32)
+    A[2, 5] = 1.0                                             # one-hot A: delta = s * B[:, 2] e_5^T
+    got = merge_f32_values(W, B, A, 2.0)
+    want = W.copy()
+    want[:, 5] = (W[:, 5].astype(np.float64) + 2.0 * B[:, 2].astype(np.float64)).astype(np.float32)
+    assert np.array_equal(got, want)

@@ -26,11 +26,15 @@ def o_dump(model, adapters, n, policy, sliced, cb, k=1, alias=0):
     return OP.dump(OP.make_plan(model, adapters, n, OP.PlanOpts(policy, sliced, cb, k, alias)))
 
 
-def test_dump_c1_matches():
-    w = WORKLOADS["C1"]
-    a = c_dump(w.model, w.adapters, 2, "stage", 0, 32 << 20)
-    b = o_dump(w.model, w.adapters, 2, "stage", 0, 32 << 20)
-    assert a == b
+@pytest.mark.parametrize("tag", ["C1", "C1f32"])
+def test_dump_c1_matches(tag):
+    w = WORKLOADS[tag]
+    for n, policy, sliced, cb in [(2, "stage", 0, 32 << 20), (2, "interleave", 1, 4 << 10), (4, "stage", 1, 64 << 10)]:
+        a = c_dump(w.model, w.adapters, n, policy, sliced, cb)
+        b = o_dump(w.model, w.adapters, n, policy, sliced, cb)
+        assert a == b, (tag, n, policy)
+    if tag == "C1f32":   # 4-byte elements: twice the bytes of the bf16 plan, same tensor table
+        assert "dtype=f32" in a
 
 
 @pytest.mark.parametrize("tag", ["C2", "C3", "C4", "C5a", "C5b"])
@@ -52,7 +56,8 @@ def test_dump_random_sweep():
         hd = rng.choice([8, 16, 32])
         kvh = H if arch == "opt" else rng.choice([h for h in (1, 2, 4) if H % h == 0])
         m = ModelDesc(arch, L, H * hd, H, kvh, rng.choice([16, 48, 96]), rng.randint(8, 300),
-                      rng.randint(1, 40) if arch == "opt" else 0, rng.choice([0, 1]) if arch == "opt" else 0)
+                      rng.randint(1, 40) if arch == "opt" else 0, rng.choice([0, 1]) if arch == "opt" else 0,
+                      dtype=rng.choice(["bf16", "bf16", "f32"]))
         tg = ("q", "k", "v", "o", "fc1", "fc2") if arch == "opt" else ("q", "k", "v", "o", "gate", "up", "down")
         ads = tuple(AdapterDesc(rng.choice([1, 3, 8, 16, 64]), rng.choice([1.0, 2.5, 16.0]),
                                 tuple(t for t in tg if rng.random() < 0.5) or ("q",))
