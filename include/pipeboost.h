@@ -158,6 +158,27 @@ PB_API pb_status pb_plan_atensor(const pb_plan* plan, int32_t i, pb_atensor_info
 
 PB_API void pb_plan_free(pb_plan* plan);
 
+/* f1 — recovery for model loading (§4.4.2 "Recovery for model loading").
+ * After GPUs crash during the cold start, build the plan that finishes it on the survivors without moving
+ * any byte a survivor already holds:
+ *   alive    host [plan n_gpus]: 1 = the GPU survived, 0 = crashed;
+ *   resident host [plan n_gpus x n_chunks] bytes: 1 = that chunk is resident on that GPU (landed, and merged
+ *            when its tensor is adapted); rows of crashed GPUs are ignored.
+ * The new plan has m = (number of survivors) ranks. Its stages are m contiguous balanced blocks of layers
+ * ("Load Balance", "Layer Contiguity") assigned to survivors so that the bytes each already
+ * holds in its block are maximal (first maximum over all m! assignments in lexicographic order, so a tie
+ * keeps the lower GPU id on the lower block); new rank r runs block r (pb_plan_gpu_of_rank maps it back to
+ * the original GPU). Same tensor table, chunk table and offsets as `plan`; embedding / head whole
+ * (vocab_sliced = 0). Every chunk no survivor holds is loaded once, by the rank whose block needs it; the
+ * receive lists bring each rank its block's missing chunks first, then the rest of the model in rotation
+ * order — e.g. GPUs 1, 2 of 4 crash: GPU 0 keeps "0, 1, 2, 3", GPU 3 becomes "2, 3, 0, 1".
+ * pb_ctx_create on the new plan treats held chunks as already resident (marks them ready at trial start).
+ * Errors: PB_EINVAL (null / no survivor), PB_EPARTITION (more survivors than layers),
+ * PB_EUNSUPPORTED (re-planning a re-plan). *out receives a plan to release with pb_plan_free. */
+PB_API pb_status pb_plan_replan(const pb_plan* plan, const int32_t* alive, const uint8_t* resident, pb_plan** out);
+/* Original GPU index of rank `rank` of a re-plan (identity for a plan from pb_plan_create). */
+PB_API pb_status pb_plan_gpu_of_rank(const pb_plan* plan, int32_t rank, int32_t* gpu);
+
 /* ------------------------------------------------------------------------ */
 /* Per-rank context                                                           */
 /* ------------------------------------------------------------------------ */

@@ -22,8 +22,9 @@ Plain Python lists and ints; no numpy, no cleverness.
 """
 from __future__ import annotations
 
-from dataclasses import dataclass, field
-from typing import List, Tuple
+import itertools
+from dataclasses import dataclass, field, replace
+from typing import List, Optional, Sequence, Tuple
 
 from synth.configs import AdapterDesc, ModelDesc
 
@@ -117,6 +118,10 @@ class Plan:
     host_base_bytes: int = 0
     host_adapter_bytes: int = 0
     dev_weight_bytes: int = 0
+    # f1 re-plans only (replan below): original GPU id of each new rank, and the chunks each new rank
+    # already holds (never re-transferred)
+    survivors: Optional[List[int]] = None
+    resident: Optional[List[List[int]]] = None
 
 
 def round_up(x: int, a: int = ALIGN) -> int:
@@ -400,6 +405,164 @@ def make_plan(model: ModelDesc, adapters, n_gpus: int, opts: PlanOpts = PlanOpts
 
 
 # ---------------------------------------------------------------------------
+# f1 — recovery for model loading (§4.4.2)
+# ---------------------------------------------------------------------------
+
+def replan(plan: Plan, alive: Sequence[int], resident: Sequence[Sequence[int]]) -> Plan:
+    """Re-plan the cold start over the GPUs that survived a crash during loading.
+
+    alive[g] (0/1) for every GPU of `plan`; resident[g] = ids of the chunks GPU g already holds (landed,
+    and merged where adapted). The paper's two principles and its worked example
+    (GPUs 1 and 2 of 4 crash, GPU 0 keeps "0, 1, 2, 3", GPU 3 becomes "2, 3, 0, 1"):
+
+    R1 survivors = alive GPUs in id order; m = their count (0 -> error; m > L -> PartitionError).
+    R2 blocks    = partition(L, m): contiguous (Layer Contiguity), balanced (Load Balance).
+    R3 blocks -> survivors: the assignment that maximises the bytes of each block's layer chunks its
+       survivor already holds, over all m! assignments in lexicographic order (first maximum wins, so on a
+       tie a lower GPU id keeps a lower block). New rank r = the survivor running block r
+       (pipeline order = block order).
+    R4 source of every chunk: the lowest new rank already holding it; else (missing everywhere) the rank
+       whose block contains its layer; embed/pos -> rank 0, final norm / LM head -> rank m-1 (whole,
+       vocab_sliced = 0). LoRA factor parts a rank's merges need and it does not hold are re-read from host
+       by that rank (reading: a few KB per layer; the paper does not discuss adapters under recovery).
+    R5 load list of rank r = chunks it sources and does not hold, canonical order (layer by layer, a
+       layer's adapter parts first as in build_chunks) — its block's missing layers.
+    R6 receive list of rank r = the base chunks its stage needs that it neither holds nor loads, in
+       canonical order, then every other base chunk it lacks in rotation order of sources (r+i) mod m —
+       "its block's missing segments first, then all remaining segments of the model".
+    Already-held chunks are never loaded or received again.
+    """
+    N = plan.n_gpus
+    if len(alive) != N or len(resident) != N:
+        raise ValueError("alive / resident need one entry per GPU")
+    surv = [g for g in range(N) if alive[g]]
+    m = len(surv)
+    if m == 0:
+        raise ValueError("no surviving GPU")
+    L = plan.model.n_layers
+    blocks = partition(L, m)                                       # R2 (raises PartitionError)
+    held = {g: set(resident[g]) for g in surv}
+    tens, chunks = plan.tensors, plan.chunks
+
+    def layer_of(c: Chunk) -> int:
+        return tens[c.tensor].layer if c.kind == "base" else plan.atensors[c.tensor].layer
+
+    def overlap(g: int, blk) -> int:
+        a, b = blk
+        return sum(c.bytes for c in chunks if c.kind == "base" and a <= layer_of(c) < b and c.id in held[g])
+
+    best, best_perm = -1, None                                     # R3
+    for perm in itertools.permutations(range(m)):
+        tot = sum(overlap(surv[i], blocks[perm[i]]) for i in range(m))
+        if tot > best:
+            best, best_perm = tot, perm
+    gpu_of_rank = [0] * m
+    for i in range(m):
+        gpu_of_rank[best_perm[i]] = surv[i]
+    rank_held = [held[gpu_of_rank[r]] for r in range(m)]
+
+    def block_rank(layer: int) -> int:
+        for r, (a, b) in enumerate(blocks):
+            if a <= layer < b:
+                return r
+        raise AssertionError(layer)
+
+    def home_rank(c: Chunk) -> int:                                # rank that needs / would load chunk c
+        l = layer_of(c)
+        if l >= 0:
+            return block_rank(l)
+        return 0 if tens[c.tensor].name in ("embed", "pos") else m - 1
+
+    new = Plan(plan.model, plan.adapters, m, replace(plan.opts, vocab_sliced=0))
+    new.stages = blocks
+    new.tensors, new.atensors = tens, plan.atensors
+    new.host_base_bytes, new.host_adapter_bytes = plan.host_base_bytes, plan.host_adapter_bytes
+    new.dev_weight_bytes = plan.dev_weight_bytes
+    new.survivors = gpu_of_rank
+    # R4: sources of base chunks
+    src = {}
+    for c in chunks:
+        if c.kind == "base":
+            holders = [r for r in range(m) if c.id in rank_held[r]]
+            src[c.id] = min(holders) if holders else home_rank(c)
+    # LoRA factor parts a rank needs for the merges of the base chunks it loads, and does not hold
+    need_ad = [set() for _ in range(m)]
+    for c in chunks:
+        if c.kind == "base" and c.id not in rank_held[src[c.id]]:
+            r = src[c.id]
+            for at in plan.atensors:
+                if at.base == c.tensor:
+                    for ac in chunks:
+                        if ac.kind == "adapter" and ac.tensor == at.id and ac.id not in rank_held[r]:
+                            need_ad[r].add(ac.id)
+    for c in chunks:
+        if c.kind == "adapter":
+            loaders = [r for r in range(m) if c.id in need_ad[r]]
+            holders = [r for r in range(m) if c.id in rank_held[r]]
+            src[c.id] = loaders[0] if loaders else (min(holders) if holders else home_rank(c))
+    new.chunks = [replace(c, loader=src[c.id]) for c in chunks]
+    # R5: load lists in the canonical order of build_chunks (per layer: adapter parts, then base tensors)
+    order = []
+    ad_by_layer = {}
+    for at in plan.atensors:
+        ad_by_layer.setdefault(at.layer, []).append(at.id)
+    base_by_tensor = {}
+    ad_chunks = {}
+    for c in chunks:
+        (base_by_tensor if c.kind == "base" else ad_chunks).setdefault(c.tensor, []).append(c.id)
+    i = 0
+    while i < len(tens):
+        t = tens[i]
+        if t.layer < 0:
+            order += base_by_tensor[t.id]
+            i += 1
+            continue
+        l = t.layer
+        for aid in ad_by_layer.get(l, []):
+            order += ad_chunks[aid]
+        while i < len(tens) and tens[i].layer == l:
+            order += base_by_tensor[tens[i].id]
+            i += 1
+    new.load = [[] for _ in range(m)]
+    for cid in order:
+        c = chunks[cid]
+        if c.kind == "base":
+            r = src[cid]
+            if cid not in rank_held[r]:
+                new.load[r].append(cid)
+        else:
+            for r in range(m):
+                if cid in need_ad[r]:
+                    new.load[r].append(cid)
+    # R6: receive lists
+    have = [set(rank_held[r]) | set(new.load[r]) for r in range(m)]
+    new.recv = []
+    for r in range(m):
+        a, b = blocks[r]
+        lst, seen = [], set()
+        for cid in order:
+            c = chunks[cid]
+            if c.kind != "base" or cid in have[r]:
+                continue
+            l = tens[c.tensor].layer
+            if (a <= l < b) or (l < 0 and home_rank(c) == r):
+                lst.append(cid)
+                seen.add(cid)
+        for k in range(1, m):
+            p = (r + k) % m
+            for cid in order:
+                c = chunks[cid]
+                if c.kind == "base" and src[cid] == p and cid not in have[r] and cid not in seen:
+                    lst.append(cid)
+                    seen.add(cid)
+        new.recv.append(lst)
+    new.resident = [sorted(rank_held[r]) for r in range(m)]
+    A = len(plan.adapters)
+    new.own = [(r % A) if A else -1 for r in range(m)]
+    return new
+
+
+# ---------------------------------------------------------------------------
 # Canonical text dump (compared byte for byte with pb_plan_dump)
 # ---------------------------------------------------------------------------
 
@@ -430,6 +593,9 @@ def dump(plan: Plan) -> str:
         out.append(f"recv {g}:" + "".join(f" {x}" for x in plan.recv[g]))
     for g in range(plan.n_gpus):
         out.append(f"own {g} adapter={plan.own[g]}")
+    if plan.survivors is not None:
+        for g in range(plan.n_gpus):
+            out.append(f"replan rank {g} gpu={plan.survivors[g]} resident:" + "".join(f" {x}" for x in plan.resident[g]))
     out.append(f"sizes host_base={plan.host_base_bytes} host_adapter={plan.host_adapter_bytes} "
                f"dev_weights={plan.dev_weight_bytes} dev_adapters={plan.host_adapter_bytes}")
     out.append("end")

@@ -95,6 +95,8 @@ _SIGS = {
     "pb_plan_tensor": [_P, C.c_int32, C.POINTER(pb_tensor_info)],
     "pb_plan_atensor": [_P, C.c_int32, C.POINTER(pb_atensor_info)],
     "pb_plan_free": [_P],
+    "pb_plan_replan": [_P, _P, _P, C.POINTER(_P)],
+    "pb_plan_gpu_of_rank": [_P, C.c_int32, C.POINTER(C.c_int32)],
     "pb_ctx_create": [_P, C.c_int32, _P, _P, C.POINTER(pb_rank_bufs), C.POINTER(_P)],
     "pb_ctx_export": [_P, _P, C.c_size_t, C.POINTER(C.c_size_t)],
     "pb_ctx_import_peer": [_P, C.c_int32, _P, C.c_size_t],
@@ -222,6 +224,22 @@ def pb_plan_atensor(plan, i) -> pb_atensor_info:
 
 def pb_plan_free(plan):
     lib().pb_plan_free(plan)
+
+
+def pb_plan_replan(plan, alive, resident):
+    """alive: sequence of 0/1 per GPU; resident: uint8 array [n_gpus, n_chunks] (1 = held)."""
+    import numpy as np
+    a = (C.c_int32 * len(alive))(*[int(x) for x in alive])
+    r = np.ascontiguousarray(resident, dtype=np.uint8)
+    out = _P()
+    check(lib().pb_plan_replan(plan, a, r.ctypes.data, C.byref(out)))
+    return out
+
+
+def pb_plan_gpu_of_rank(plan, rank) -> int:
+    v = C.c_int32(0)
+    check(lib().pb_plan_gpu_of_rank(plan, rank, C.byref(v)))
+    return v.value
 
 
 def pb_ctx_create(plan, rank, host_base_ptr, host_adapters_ptr, bufs: pb_rank_bufs):

@@ -325,6 +325,172 @@ extern "C" pb_status pb_plan_create(const pb_model_desc* model, const pb_adapter
     PB_TRY_END
 }
 
+// ------------------------------------------------------------------------------------------------
+// f1 — recovery for model loading (§4.4.2). Steps R1-R6 as in oracle/plan.py
+// replan(): survivors, balanced contiguous blocks, overlap-maximising block assignment (lexicographic
+// first maximum over all m! assignments), sources, load lists (missing chunks only), receive lists.
+// ------------------------------------------------------------------------------------------------
+extern "C" pb_status pb_plan_replan(const pb_plan* plan, const int32_t* alive, const uint8_t* resident,
+                                    pb_plan** out) {
+    PB_TRY_BEGIN
+    using namespace pb;
+    if (!plan || !alive || !resident || !out) return pb::fail(PB_EINVAL, "pb_plan_replan: null argument");
+    *out = nullptr;
+    if (!plan->survivors.empty()) return pb::fail(PB_EUNSUPPORTED, "pb_plan_replan: re-planning a re-plan");
+    const int32_t N = plan->n_gpus, L = plan->model.n_layers;
+    const int32_t NC = (int32_t)plan->chunks.size();
+    std::vector<int32_t> surv;
+    for (int32_t g = 0; g < N; ++g)
+        if (alive[g]) surv.push_back(g);
+    const int32_t m = (int32_t)surv.size();
+    if (m == 0) return pb::fail(PB_EINVAL, "pb_plan_replan: no surviving GPU");
+    if (m > L) return pb::fail(PB_EPARTITION, "%d survivors > %d layers", m, L);
+    const auto blocks = balanced(L, m);                                                // R2
+    auto layer_of = [&](const ChunkRec& c) {
+        return c.is_adapter ? plan->atensors[c.tensor].layer : plan->tensors[c.tensor].layer;
+    };
+    // R3: overlap[i][b] = bytes of block b's layer chunks survivor i holds
+    std::vector<std::vector<int64_t>> ov(m, std::vector<int64_t>(m, 0));
+    for (int32_t i = 0; i < m; ++i)
+        for (const ChunkRec& c : plan->chunks) {
+            if (c.is_adapter || !resident[(size_t)surv[i] * NC + c.id]) continue;
+            const int32_t l = layer_of(c);
+            if (l < 0) continue;
+            for (int32_t b = 0; b < m; ++b)
+                if (l >= blocks[b].first && l < blocks[b].second) ov[i][b] += c.bytes;
+        }
+    std::vector<int32_t> perm(m), best_perm;
+    for (int32_t i = 0; i < m; ++i) perm[i] = i;
+    int64_t best = -1;
+    do {
+        int64_t tot = 0;
+        for (int32_t i = 0; i < m; ++i) tot += ov[i][perm[i]];
+        if (tot > best) {
+            best = tot;
+            best_perm = perm;
+        }
+    } while (std::next_permutation(perm.begin(), perm.end()));
+    std::vector<int32_t> gpu_of_rank(m);
+    for (int32_t i = 0; i < m; ++i) gpu_of_rank[best_perm[i]] = surv[i];
+    auto held = [&](int32_t r, int32_t c) { return resident[(size_t)gpu_of_rank[r] * NC + c] != 0; };
+    auto block_rank = [&](int32_t l) {
+        for (int32_t r = 0; r < m; ++r)
+            if (l >= blocks[r].first && l < blocks[r].second) return r;
+        return -1;
+    };
+    auto home_rank = [&](const ChunkRec& c) {
+        const int32_t l = layer_of(c);
+        if (l >= 0) return block_rank(l);
+        const std::string& nm = plan->tensors[c.tensor].name;
+        return (nm == "embed" || nm == "pos") ? 0 : m - 1;
+    };
+
+    auto* p = new pb_plan(*plan);
+    p->n_gpus = m;
+    p->opts.vocab_sliced = 0;
+    p->stages = blocks;
+    p->survivors = gpu_of_rank;
+    p->resident.assign(m, std::vector<char>(NC, 0));
+    for (int32_t r = 0; r < m; ++r)
+        for (int32_t c = 0; c < NC; ++c) p->resident[r][c] = held(r, c) ? 1 : 0;
+    // R4: sources
+    std::vector<int32_t> src(NC, -1);
+    for (const ChunkRec& c : plan->chunks) {
+        if (c.is_adapter) continue;
+        for (int32_t r = 0; r < m && src[c.id] < 0; ++r)
+            if (held(r, c.id)) src[c.id] = r;
+        if (src[c.id] < 0) src[c.id] = home_rank(c);
+    }
+    std::vector<std::vector<char>> need_ad(m, std::vector<char>(NC, 0));
+    for (const ChunkRec& c : plan->chunks) {
+        if (c.is_adapter || held(src[c.id], c.id)) continue;
+        const int32_t r = src[c.id];
+        for (size_t ai = 0; ai < plan->atensors.size(); ++ai) {
+            if (plan->atensors[ai].base != c.tensor) continue;
+            for (const ChunkRec& ac : plan->chunks)
+                if (ac.is_adapter && ac.tensor == (int32_t)ai && !held(r, ac.id)) need_ad[r][ac.id] = 1;
+        }
+    }
+    for (const ChunkRec& c : plan->chunks) {
+        if (!c.is_adapter) continue;
+        int32_t s = -1;
+        for (int32_t r = 0; r < m && s < 0; ++r)
+            if (need_ad[r][c.id]) s = r;
+        for (int32_t r = 0; r < m && s < 0; ++r)
+            if (held(r, c.id)) s = r;
+        src[c.id] = s >= 0 ? s : home_rank(c);
+    }
+    for (ChunkRec& c : p->chunks) c.loader = src[c.id];
+    // canonical order (pb_plan_create's load order): per layer, adapter parts then base tensors
+    std::vector<std::vector<int32_t>> base_chunks(p->tensors.size()), ad_chunks(p->atensors.size());
+    for (const ChunkRec& c : p->chunks) (c.is_adapter ? ad_chunks : base_chunks)[c.tensor].push_back(c.id);
+    std::vector<std::vector<int32_t>> ad_of_layer(L);
+    for (size_t ai = 0; ai < p->atensors.size(); ++ai) ad_of_layer[p->atensors[ai].layer].push_back((int32_t)ai);
+    std::vector<int32_t> order;
+    for (size_t ti = 0; ti < p->tensors.size();) {
+        const int32_t l = p->tensors[ti].layer;
+        if (l < 0) {
+            order.insert(order.end(), base_chunks[ti].begin(), base_chunks[ti].end());
+            ++ti;
+            continue;
+        }
+        for (int32_t ai : ad_of_layer[l]) order.insert(order.end(), ad_chunks[ai].begin(), ad_chunks[ai].end());
+        for (; ti < p->tensors.size() && p->tensors[ti].layer == l; ++ti)
+            order.insert(order.end(), base_chunks[ti].begin(), base_chunks[ti].end());
+    }
+    // R5: load lists
+    p->load.assign(m, {});
+    for (int32_t cid : order) {
+        const ChunkRec& c = p->chunks[cid];
+        if (!c.is_adapter) {
+            if (!held(src[cid], cid)) p->load[src[cid]].push_back(cid);
+        } else {
+            for (int32_t r = 0; r < m; ++r)
+                if (need_ad[r][cid]) p->load[r].push_back(cid);
+        }
+    }
+    // R6: receive lists
+    p->recv.assign(m, {});
+    for (int32_t r = 0; r < m; ++r) {
+        std::vector<char> have(NC, 0), seen(NC, 0);
+        for (int32_t c = 0; c < NC; ++c) have[c] = held(r, c);
+        for (int32_t c : p->load[r]) have[c] = 1;
+        auto& rv = p->recv[r];
+        for (int32_t cid : order) {
+            const ChunkRec& c = p->chunks[cid];
+            if (c.is_adapter || have[cid]) continue;
+            const int32_t l = p->tensors[c.tensor].layer;
+            if ((l >= blocks[r].first && l < blocks[r].second) || (l < 0 && home_rank(c) == r)) {
+                rv.push_back(cid);
+                seen[cid] = 1;
+            }
+        }
+        for (int32_t k = 1; k < m; ++k) {
+            const int32_t q = (r + k) % m;
+            for (int32_t cid : order) {
+                const ChunkRec& c = p->chunks[cid];
+                if (!c.is_adapter && src[cid] == q && !have[cid] && !seen[cid]) {
+                    rv.push_back(cid);
+                    seen[cid] = 1;
+                }
+            }
+        }
+    }
+    const int32_t A = (int32_t)p->adapters.size();
+    p->own.clear();
+    for (int32_t r = 0; r < m; ++r) p->own.push_back(A ? r % A : -1);
+    *out = p;
+    return PB_OK;
+    PB_TRY_END
+}
+
+extern "C" pb_status pb_plan_gpu_of_rank(const pb_plan* p, int32_t rank, int32_t* gpu) {
+    if (!p || !gpu) return pb::fail(PB_EINVAL, "pb_plan_gpu_of_rank: null argument");
+    if (rank < 0 || rank >= p->n_gpus) return pb::fail(PB_EINVAL, "rank %d out of range", rank);
+    *gpu = p->survivors.empty() ? rank : p->survivors[rank];
+    return PB_OK;
+}
+
 namespace {
 struct Out {
     std::string s;
@@ -392,6 +558,13 @@ static std::string dump_string(const pb_plan* p) {
         o.f("\n");
     }
     for (int g = 0; g < p->n_gpus; ++g) o.f("own %d adapter=%d\n", g, p->own[g]);
+    if (!p->survivors.empty())
+        for (int g = 0; g < p->n_gpus; ++g) {
+            o.f("replan rank %d gpu=%d resident:", g, p->survivors[g]);
+            for (size_t c = 0; c < p->chunks.size(); ++c)
+                if (p->resident[g][c]) o.f(" %zu", c);
+            o.f("\n");
+        }
     o.f("sizes host_base=%" PRId64 " host_adapter=%" PRId64 " dev_weights=%" PRId64 " dev_adapters=%" PRId64 "\n",
         p->host_base_bytes, p->host_adapter_bytes, p->dev_weight_bytes, p->host_adapter_bytes);
     o.f("end\n");

@@ -69,6 +69,13 @@ struct pb_plan {
     // in a separate device region. adapted_off[a * n_tensors + t] = offset, or -1 when adapter a does not touch t.
     std::vector<int64_t> adapted_off;
     int64_t dev_adapted_bytes = 0;
+    // f1 re-plans (pb_plan_replan): original GPU of every new rank, and per rank the chunks it already holds
+    // (never loaded or received again). Empty for a plan made by pb_plan_create.
+    std::vector<int32_t> survivors;
+    std::vector<std::vector<char>> resident;   // [rank][chunk]
+    bool is_resident(int32_t rank, int32_t chunk) const {
+        return !resident.empty() && resident[rank][chunk];
+    }
 
     // derived helpers
     int32_t head_dim() const { return model.d_model / model.n_heads; }
