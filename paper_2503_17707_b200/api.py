@@ -35,6 +35,43 @@ class Plan:
     def dump(self) -> str:
         return B.pb_plan_dump(self.handle)
 
+    def replan(self, alive, resident) -> "Plan":
+        """f1 (P:L349-365): the plan that finishes the cold start on the GPUs still alive. alive[g] 0/1 per GPU;
+        resident: uint8 [n_gpus, n_chunks], 1 = GPU g already holds that chunk (never moved again).
+        Rank r of the new plan runs on original GPU gpu_of_rank(r)."""
+        new = Plan.__new__(Plan)
+        new.model, new.adapters = self.model, self.adapters
+        new.opts = self.opts
+        new.handle = B.pb_plan_replan(self.handle, alive, resident)
+        new.sizes = B.pb_plan_sizes(new.handle)
+        new.n_gpus = new.sizes.n_gpus
+        return new
+
+    def gpu_of_rank(self, rank: int) -> int:
+        return B.pb_plan_gpu_of_rank(self.handle, rank)
+
+    def chunks(self):
+        """(id, is_adapter, tensor, r0, r1, dev_off, bytes, loader) of every chunk, parsed from the canonical dump."""
+        out = []
+        for ln in self.dump().splitlines():
+            if ln.startswith("chunk "):
+                f = ln.split()
+                kv = dict(x.split("=", 1) for x in f[3:])
+                r0, r1 = kv["rows"][1:-1].split(",")
+                out.append((int(f[1]), f[2] == "adapter", int(kv["tensor"]), int(r0), int(r1), int(kv["dev_off"]),
+                            int(kv["bytes"]), int(kv["loader"])))
+        return out
+
+    def lists(self):
+        """Per-rank load and receive lists (chunk ids), parsed from the canonical dump."""
+        load, recv = {}, {}
+        for ln in self.dump().splitlines():
+            if ln.startswith("load ") or ln.startswith("recv "):
+                head, _, rest = ln.partition(":")
+                kind, g = head.split()
+                (load if kind == "load" else recv)[int(g)] = [int(x) for x in rest.split()]
+        return [load[g] for g in range(self.sizes.n_gpus)], [recv[g] for g in range(self.sizes.n_gpus)]
+
     def tensors(self):
         out = []
         for i in range(self.sizes.n_tensors):
@@ -67,8 +104,10 @@ class RankEngine:
 
     def __init__(self, plan: Plan, rank: int, host_base: torch.Tensor, host_adapters: Optional[torch.Tensor],
                  max_batch: int = 1, max_seq: int = 128, device: Optional[torch.device] = None,
-                 multi_adapter: bool = False):
-        """multi_adapter=True allocates the out-of-place per-adapter copies (PB_MERGE_ALL mode)."""
+                 multi_adapter: bool = False, reuse: Optional["RankEngine"] = None):
+        """multi_adapter=True allocates the out-of-place per-adapter copies (PB_MERGE_ALL mode).
+        reuse: a (closed or live) engine of the same GPU whose weight / adapter buffers hold what a re-plan
+        (Plan.replan) marks as resident — the recovery trial continues in them instead of fresh buffers."""
         self.plan = plan
         self.rank = rank
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
@@ -77,10 +116,13 @@ class RankEngine:
         self.host_adapters = host_adapters
         s = plan.sizes
         with torch.cuda.device(self.device):
-            self.weights = torch.empty(s.dev_weight_bytes, dtype=torch.uint8, device=self.device)
-            self.adapters = torch.empty(max(s.dev_adapter_bytes, 1), dtype=torch.uint8, device=self.device)
-            self.adapted = (torch.empty(s.dev_adapted_bytes, dtype=torch.uint8, device=self.device)
-                            if multi_adapter and s.dev_adapted_bytes else None)
+            if reuse is not None:
+                self.weights, self.adapters, self.adapted = reuse.weights, reuse.adapters, reuse.adapted
+            else:
+                self.weights = torch.empty(s.dev_weight_bytes, dtype=torch.uint8, device=self.device)
+                self.adapters = torch.empty(max(s.dev_adapter_bytes, 1), dtype=torch.uint8, device=self.device)
+                self.adapted = (torch.empty(s.dev_adapted_bytes, dtype=torch.uint8, device=self.device)
+                                if multi_adapter and s.dev_adapted_bytes else None)
             ws = plan.workspace_bytes(max_batch, max_seq)
             self.workspace = torch.empty(ws, dtype=torch.uint8, device=self.device)
             # streams: NULL -> the ctx creates five distinct non-blocking streams (torch's stream pool

@@ -28,6 +28,8 @@ struct SignalTargets {
     int n;
 };
 cudaError_t launch_signal(const SignalTargets& t, uint32_t value, cudaStream_t s);
+// base[idx[i]] = value (release, system scope) for i < n; idx is a device array.
+cudaError_t launch_set_words(uint32_t* base, const int32_t* idx, int n, uint32_t value, cudaStream_t s);
 
 // ---------------------------------------------------------------- a3: LoRA merge (tcgen05)
 // W[rows x cols] (row pitch ldw) <- RNE_bf16(W + scale * B[rows x r] * A[r x cols]), fp32 accumulate in TMEM.

@@ -111,7 +111,8 @@ WsLayout pb::ws_layout(const pb_plan* p, int32_t batch, int32_t seq) {
     L.f_logit = L.f_y + 1;
     L.f_land = L.f_logit + p->n_gpus;
     L.f_tensor = L.f_land + (int32_t)p->chunks.size();
-    L.n_words = L.f_tensor + (int32_t)p->tensors.size();
+    L.f_tensor_recv = L.f_tensor + (int32_t)p->tensors.size();
+    L.n_words = L.f_tensor_recv + (int32_t)p->tensors.size();
     int64_t o = 0;
     L.flags = o;   o = al(o + 4 * (int64_t)L.n_words);
     L.tokens = o;  o = al(o + 4 * rows);
@@ -128,6 +129,7 @@ WsLayout pb::ws_layout(const pb_plan* p, int32_t batch, int32_t seq) {
     L.tok_out = o; o = al(o + 4 * (int64_t)batch);
     L.nan = o;     o = al(o + 4);
     L.rope = o;    o = al(o + (m.arch == PB_ARCH_LLAMA ? 8 * (int64_t)seq * (hd / 2) : 0));
+    L.held = o;    o = al(o + (p->survivors.empty() ? 0 : 4 * (int64_t)p->chunks.size()));   // re-plan signal list
     L.total = al(o, 4096);
     return L;
 }
@@ -159,7 +161,7 @@ static pb_status build_merge_jobs(pb_ctx* c) {
         const auto& Bf = p->atensors[mr.b_tensor];
         const int rank = p->adapters[mr.adapter].rank;
         for (auto& ch : p->chunks) {
-            if (ch.is_adapter || ch.tensor != mr.base || ch.loader != c->rank) continue;
+            if (ch.is_adapter || ch.tensor != mr.base || ch.loader != c->rank || p->is_resident(c->rank, ch.id)) continue;
             const int32_t ra = std::max(ch.r0, mr.row0), rb = std::min(ch.r1, mr.row0 + mr.rows);
             if (rb <= ra) continue;
             if (rank % 8 != 0 && !p->f32())
@@ -386,6 +388,15 @@ extern "C" pb_status pb_ctx_create(const pb_plan* plan, int32_t rank, const void
             if (in_stage(id)) c->last_recv_stage_chunk = id;
     }
 
+    if (!plan->survivors.empty()) {   // re-plan: chunks this rank holds that other ranks will copy from it
+        std::vector<int32_t> held;
+        for (const ChunkRec& ch : plan->chunks)
+            if (!ch.is_adapter && ch.loader == rank && plan->is_resident(rank, ch.id)) held.push_back(ch.id);
+        c->n_held_src = (int32_t)held.size();
+        if (!held.empty() &&
+            cudaMemcpy(c->ws + L.held, held.data(), 4 * held.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+            return cleanup(fail(PB_ECUDA, "held-chunk list upload failed"));
+    }
     build_copy_groups(c);
     pb_status st = build_merge_jobs(c);
     if (st != PB_OK) return cleanup(st);
@@ -617,6 +628,11 @@ extern "C" pb_status pb_trial_begin(pb_ctx* c, uint32_t epoch) {
     CU(cudaEventRecord(c->t0, c->h2d[0]));
     cudaStream_t others[] = {c->h2d[1], c->merge, c->nv, c->comp};
     for (auto s : others) CU(cudaStreamWaitEvent(s, c->t0, 0));
+    // re-plan resume: chunks this rank already holds are ready for the peers that receive them from it
+    for (int r = 0; r < c->n && c->n_held_src > 0; ++r)
+        if (r != c->rank)
+            CU(launch_set_words(flag_ptr(c->peers[r].ws, c->L, c->L.f_chunk),
+                                reinterpret_cast<const int32_t*>(c->ws + c->L.held), c->n_held_src, epoch, c->merge));
     c->phase = Phase::Begun;
     return PB_OK;
 }
@@ -638,6 +654,7 @@ extern "C" pb_status pb_merge_lora(pb_ctx* c, int32_t adapter_id) {
         return fail(PB_EINVAL, "adapter_id %d out of range", adapter_id);
     if (adapter_id == PB_MERGE_ALL) {
         if (c->plan->adapters.empty()) return fail(PB_EINVAL, "PB_MERGE_ALL without adapters");
+        if (!c->plan->survivors.empty()) return fail(PB_EUNSUPPORTED, "PB_MERGE_ALL on a re-plan");
         if (!c->adapted) return fail(PB_ENOMEM, "PB_MERGE_ALL needs bufs.adapted >= dev_adapted_bytes");
         if (c->n > 1 && c->plan->opts.policy != PB_LOAD_STAGE)
             return fail(PB_EUNSUPPORTED, "PB_MERGE_ALL with n_gpus > 1 needs the STAGE policy (stage owner = loader)");
@@ -669,10 +686,20 @@ const __nv_bfloat16* wt(pb_ctx* c, int l, const char* sfx) {
 }
 
 
+// Tensor t is complete in this rank's HBM: its own-loaded part merged (f_tensor) and its received part copied
+// (f_tensor_recv); chunks a re-plan marks as already held need no wait.
+cudaError_t wait_tensor_ready(pb_ctx* c, int32_t t, cudaStream_t s) {
+    if (c->last_own_chunk[t] >= 0) {
+        cudaError_t e = wait_word(c, c->L.f_tensor + t, s);
+        if (e != cudaSuccess) return e;
+    }
+    if (c->last_recv_chunk[t] >= 0) return wait_word(c, c->L.f_tensor_recv + t, s);
+    return cudaSuccess;
+}
+
 cudaError_t wait_tensor(pb_ctx* c, int l, const char* sfx) {
     const pb_plan* p = c->plan;
-    const int32_t t = p->find_tensor("L" + std::to_string(l) + "." + sfx);
-    return wait_word(c, c->L.f_tensor + t, c->comp);
+    return wait_tensor_ready(c, p->find_tensor("L" + std::to_string(l) + "." + sfx), c->comp);
 }
 
 // fp32 debug-parity path: tensor sfx of layer l (or a non-layer tensor when l < 0); adapter >= 0 selects that
@@ -927,7 +954,8 @@ struct Issuer {
     int n_mb;
     std::vector<int> tb;
     std::vector<Item> items;
-    std::vector<char> tensor_issued, adapter_waited;
+    // the own / received part of a tensor has its readiness write issued (prerequisites of compute items)
+    std::vector<char> own_issued, recv_issued, adapter_waited;
     Budget h2d, merge, nv, comp;
 };
 
@@ -1011,7 +1039,7 @@ pb_status issue_group(Issuer& I, size_t gi) {
         }
         if (c->last_own_chunk[ch.tensor] == id) {
             CU(set_word(c, c->L.f_tensor + ch.tensor, c->merge));
-            I.tensor_issued[ch.tensor] = 1;
+            I.own_issued[ch.tensor] = 1;
             ++mops;
         }
         if (id == c->last_own_stage_chunk) {
@@ -1021,6 +1049,17 @@ pb_status issue_group(Issuer& I, size_t gi) {
     }
     CU(I.merge.add(mops));
     return PB_OK;
+}
+
+// A compute item's prerequisite t >= 0: every part of tensor t this rank does not already hold (own loads and
+// received chunks) has its readiness write issued; -(t+1): only the own-loaded part (vocab slices).
+bool prereq_issued(const Issuer& I, int32_t t) {
+    const pb_ctx* c = I.c;
+    if (t < 0) {
+        t = -t - 1;
+        return I.own_issued[t] || c->last_own_chunk[t] < 0;
+    }
+    return (I.own_issued[t] || c->last_own_chunk[t] < 0) && (I.recv_issued[t] || c->last_recv_chunk[t] < 0);
 }
 
 long group_merge_ops(Issuer& I, size_t gi) {
@@ -1046,8 +1085,8 @@ pb_status issue_recv(Issuer& I, size_t ri) {
     CU(cudaEventRecord(c->gathered[id], c->nv));
     long n = 3;
     if (c->last_recv_chunk[ch.tensor] == id) {
-        CU(set_word(c, c->L.f_tensor + ch.tensor, c->nv));
-        I.tensor_issued[ch.tensor] = 1;
+        CU(set_word(c, c->L.f_tensor_recv + ch.tensor, c->nv));
+        I.recv_issued[ch.tensor] = 1;
         ++n;
     }
     if (id == c->last_recv_stage_chunk) {
@@ -1080,7 +1119,11 @@ void build_items(Issuer& I) {
             std::vector<int32_t> pre;
             if (mb == 0 && j == 0) {
                 const int32_t et = p->find_tensor("embed");
-                if (c->last_own_chunk[et] >= 0) pre.push_back(et);
+                if (p->opts.vocab_sliced) {
+                    if (c->last_own_chunk[et] >= 0) pre.push_back(-et - 1);   // own slice only
+                } else {
+                    pre.push_back(et);
+                }
                 if (opt) pre.push_back(p->find_tensor("pos"));
             }
             add(I_EMBED, mb, j, 0, pre);
@@ -1112,7 +1155,7 @@ void build_items(Issuer& I) {
         if (opt) pre.push_back(p->find_tensor("final_b"));
         add(I_FINAL, 0, 0, 0, pre);
     }
-    if (is_head_owner(p, g)) add(I_HEAD, 0, 0, 0, {head_tensor(p)});
+    if (is_head_owner(p, g)) add(I_HEAD, 0, 0, 0, {p->opts.vocab_sliced ? -head_tensor(p) - 1 : head_tensor(p)});
     if (g == 0) add(I_ARGMAX, 0, 0, 0, {});
     add(I_DONE, 0, 0, 0, {});
 }
@@ -1172,11 +1215,15 @@ pb_status issue_item(Issuer& I, const Item& it) {
         case I_EMBED: {
             const int32_t et = p->find_tensor("embed");
             if (j == 0 && !I.replay) {
-                // embedding rows may live on every rank (vocab slices): wait for each remote piece
-                for (auto& ch : p->chunks)
-                    if (!ch.is_adapter && ch.tensor == et && ch.loader != g) CU(wait_word(c, L.f_chunk + ch.id, s));
-                if (c->last_own_chunk[et] >= 0) CU(wait_word(c, L.f_tensor + et, s));
-                if (opt) CU(wait_word(c, L.f_tensor + p->find_tensor("pos"), s));
+                if (p->opts.vocab_sliced) {
+                    // embedding rows live on every rank (vocab slices): wait for each remote piece at its owner
+                    for (auto& ch : p->chunks)
+                        if (!ch.is_adapter && ch.tensor == et && ch.loader != g) CU(wait_word(c, L.f_chunk + ch.id, s));
+                    if (c->last_own_chunk[et] >= 0) CU(wait_word(c, L.f_tensor + et, s));
+                } else {
+                    CU(wait_tensor_ready(c, et, s));
+                }
+                if (opt) CU(wait_tensor_ready(c, p->find_tensor("pos"), s));
             }
             EmbedSrc E{};
             if (p->opts.vocab_sliced) {
@@ -1225,8 +1272,8 @@ pb_status issue_item(Issuer& I, const Item& it) {
             break;
         case I_FINAL: {
             if (!I.replay) {
-                CU(wait_word(c, L.f_tensor + p->find_tensor("final_g"), s));
-                if (opt) CU(wait_word(c, L.f_tensor + p->find_tensor("final_b"), s));
+                CU(wait_tensor_ready(c, p->find_tensor("final_g"), s));
+                if (opt) CU(wait_tensor_ready(c, p->find_tensor("final_b"), s));
             }
             // last position of every sequence: token-major rows (T-1)*B + b, or microbatch rows b*T + T-1
             const float* last = I.mb_mode ? h + (size_t)(T - 1) * d : h + (size_t)(T - 1) * B * d;
@@ -1253,7 +1300,10 @@ pb_status issue_item(Issuer& I, const Item& it) {
         case I_HEAD: {
             if (g != N - 1) CU(wait_word(c, L.f_y, s));
             const int32_t ht = head_tensor(p);
-            if (!I.replay) CU(wait_word(c, L.f_tensor + ht, s));
+            if (!I.replay) {   // vocab slices: this rank's own rows; whole head: every part of it
+                if (p->opts.vocab_sliced) CU(wait_word(c, L.f_tensor + ht, s));
+                else CU(wait_tensor_ready(c, ht, s));
+            }
             int32_t v0, v1;
             head_slice(p, g, &v0, &v1);
             const __nv_bfloat16* E = reinterpret_cast<const __nv_bfloat16*>(c->weights + p->tensors[ht].dev_off);
@@ -1306,7 +1356,8 @@ pb_status issue_trial(pb_ctx* c, int B, int T, bool replay) {
         I.tb[j] = t;
         if (j < I.k) t += T / I.k + (j < T % I.k ? 1 : 0);
     }
-    I.tensor_issued.assign(p->tensors.size(), replay ? 1 : 0);
+    I.own_issued.assign(p->tensors.size(), replay ? 1 : 0);
+    I.recv_issued.assign(p->tensors.size(), replay ? 1 : 0);
     I.adapter_waited.assign(p->chunks.size(), 0);
     cudaStream_t ss[4] = {c->h2d[0], c->merge, c->nv, c->comp};
     Budget* bs[4] = {&I.h2d, &I.merge, &I.nv, &I.comp};
@@ -1350,7 +1401,7 @@ pb_status issue_trial(pb_ctx* c, int B, int T, bool replay) {
         while (ii < I.items.size()) {
             const Item& it = I.items[ii];
             bool ok = true;
-            for (int32_t t : it.prereq) ok = ok && I.tensor_issued[t];
+            for (int32_t t : it.prereq) ok = ok && prereq_issued(I, t);
             if (!ok || !I.comp.can(item_ops(I, it))) break;
             pb_status st = issue_item(I, it);
             if (st) return st;
@@ -1366,7 +1417,7 @@ pb_status issue_trial(pb_ctx* c, int B, int T, bool replay) {
                 int missing = -1;
                 if (it)
                     for (int32_t t : it->prereq)
-                        if (!I.tensor_issued[t]) { missing = t; break; }
+                        if (!prereq_issued(I, t)) { missing = t; break; }
                 fprintf(stderr,
                         "[pb issuer r%d] stalled: groups %zu/%zu recv %zu/%zu items %zu/%zu (kind %d j %d l %d, missing "
                         "tensor %d) outstanding h2d %ld merge %ld nv %ld comp %ld\n",

@@ -15,12 +15,13 @@ namespace pb {
 // peer can address it: flags | tokens | h | x | qkv[n_qkv] | attn | mlp | y | logits | tok_out | nan | rope.
 struct WsLayout {
     int64_t flags = 0, tokens = 0, h = 0, x = 0, qkv = 0, qkv_stride = 0, attn = 0, mlp = 0, y = 0, logits = 0,
-            tok_out = 0, nan = 0, rope = 0, total = 0;
+            tok_out = 0, nan = 0, rope = 0, held = 0, total = 0;
     int32_t n_qkv = 1;
     int32_t max_rows = 0, max_batch = 0, max_seq = 0;
     // readiness words (uint32) inside `flags`
     int32_t f_chunk = 0, f_act = 0, f_y = 0, f_logit = 0, n_words = 0;
     int32_t f_land = 0, f_tensor = 0;   // local words: copy group landed (by first chunk id), tensor ready
+    int32_t f_tensor_recv = 0;          // local words: the received part of a tensor is in place
 };
 WsLayout ws_layout(const pb_plan* p, int32_t batch, int32_t seq);
 
@@ -94,6 +95,7 @@ struct pb_ctx {
     std::vector<char> tensor_own;        // this rank loads every piece of the tensor
     std::vector<int32_t> last_own_chunk; // per base tensor: last own chunk in load order (-1 if none)
     std::vector<int32_t> last_recv_chunk;
+    int32_t n_held_src = 0;              // re-plan: chunks this rank holds and other ranks receive from it
 
     std::vector<pb::CopyGroup> copies;
     std::vector<int32_t> landed_alias;   // chunk -> first chunk of its copy group (owner of the landed event)

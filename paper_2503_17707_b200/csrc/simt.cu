@@ -309,14 +309,31 @@ __global__ void signal_kernel(SignalTargets t, uint32_t value) {
     }
 }
 
+// Re-plan resume: publish `value` into words base[idx[i]] (a peer's chunk readiness words for the chunks this
+// rank already holds), one thread per word.
+__global__ void set_words_kernel(uint32_t* base, const int32_t* __restrict__ idx, int n, uint32_t value) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        __threadfence_system();
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(base + idx[i]), "r"(value) : "memory");
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_set_words(uint32_t* base, const int32_t* idx, int n, uint32_t value, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    set_words_kernel<<<(n + 255) / 256, 256, 0, s>>>(base, idx, n, value);
+    return cudaGetLastError();
+}
 
 cudaError_t warm_simt_kernels() {
     cudaFuncAttributes a;
     const void* fns[] = {(const void*)norm_kernel<256, 8>, (const void*)norm_kernel<256, 40>, (const void*)embed_kernel,
                          (const void*)rope_table_kernel, (const void*)rope_kernel, (const void*)attention_kernel<32>,
                          (const void*)attention_kernel<64>, (const void*)attention_kernel<128>,
-                         (const void*)logits_kernel, (const void*)argmax_kernel, (const void*)signal_kernel};
+                         (const void*)logits_kernel, (const void*)argmax_kernel, (const void*)signal_kernel,
+                         (const void*)set_words_kernel};
     for (const void* f : fns) {
         cudaError_t e = cudaFuncGetAttributes(&a, f);
         if (e != cudaSuccess) return e;
