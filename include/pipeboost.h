@@ -134,6 +134,8 @@ typedef struct {
     int32_t n_tensors, n_atensors, n_chunks, n_gpus;
     int64_t dev_adapted_bytes;   /* per-GPU device buffer for out-of-place per-adapter copies of the adapted
                                     tensors (multi-adapter merge, pb_merge_lora(ctx, PB_MERGE_ALL)) */
+    int64_t dev_backup_bytes;    /* per-GPU device buffer for the pristine base of every adapted tensor
+                                    (saved by the cold-start merges; needed by pb_switch_adapter) */
 } pb_plan_sizes_t;
 PB_API pb_status pb_plan_sizes(const pb_plan* plan, pb_plan_sizes_t* out);
 
@@ -195,6 +197,7 @@ typedef struct {
     void* stream_merge;   /* cudaStream_t: merge kernels + per-layer readiness */
     void* stream_nvlink;  /* cudaStream_t: peer (NVLink) receive copies */
     void* stream_compute; /* cudaStream_t: prefill kernels */
+    void* backup;         int64_t backup_cap;     /* device, >= dev_backup_bytes to enable pb_switch_adapter, else NULL */
 } pb_rank_bufs;
 
 /* Create rank `rank`'s context on the current CUDA device. host_base / host_adapters
@@ -254,6 +257,36 @@ PB_API pb_status pb_prefill_enqueue_ex(pb_ctx* ctx, const int32_t* tokens, const
 PB_API pb_status pb_prefill_wait(pb_ctx* ctx, float* logits_out, int32_t* tokens_out);
 PB_API pb_status pb_prefill_first_token(pb_ctx* ctx, const int32_t* tokens, int32_t batch, int32_t seq,
                                  float* logits_out, int32_t* tokens_out);
+
+/* f2 — epoch-based adapter switching (§4.3.2). Replace the adapter merged
+ * into this rank's STAGE layers by `adapter_id` (or by none: -1): every adapted tensor of the stage is restored
+ * from its pristine base copy (bufs.backup, saved by the cold start's merges) and the new adapter is merged
+ * from it — W = RNE_bf16(W_base + s B A), so any sequence of switches gives exactly the weights a cold start
+ * with that adapter gives (no drift). LoRA factors the rank did not load are fetched from the host image.
+ * Enqueued on the compute stream behind every prefill already enqueued on this rank: a stage switches only
+ * after finishing the batches handed to it, so along the pipeline the stages switch one after another
+ * ("Each GPU switches adapters only after completing the batch received from the preceding GPU").
+ * Requires a completed cold start with an in-place adapter (pb_merge_lora(ctx, a >= 0) or -1) and
+ * bufs.backup. Serve the next batch with pb_prefill_replay. Async; errors: PB_EINVAL, PB_EPROTOCOL,
+ * PB_ENOMEM (no backup buffer), PB_EUNSUPPORTED (PB_MERGE_ALL mode: every adapter is already merged). */
+PB_API pb_status pb_switch_adapter(pb_ctx* ctx, int32_t adapter_id);
+
+/* f2 scheduling (SPEC lora-scheduler S:L340-405): which adapter's batch runs next. Host only.
+ * One FIFO queue per adapter plus the base-model queue (adapter -1). While an epoch of epoch_ms lasts,
+ * batches come from the active adapter ("prioritizes the scheduling of batches corresponding to the currently
+ * activated adapter"); when it has expired, the next non-empty queue in round-robin order (ids ascending,
+ * base first) takes over ("At regular intervals, PipeBoost switches adapters"), except that a queue left
+ * waiting over more than starvation_epochs expirations goes first; an empty active queue hands over at once.
+ * pb_epoch_next returns the batch (up to max_batch request ids, FIFO, written to ids[]) and switch_needed = 1
+ * when the stages must pb_switch_adapter first; *adapter = -2 and *n = 0 when every queue is empty.
+ * Errors: PB_EINVAL (null, bad config, unknown adapter). Not thread-safe per scheduler. */
+typedef struct pb_epoch pb_epoch;
+PB_API pb_status pb_epoch_create(int32_t n_adapters, double epoch_ms, int32_t starvation_epochs, pb_epoch** out);
+PB_API pb_status pb_epoch_set_active(pb_epoch* sched, int32_t adapter, double now_ms);  /* what the stages hold */
+PB_API pb_status pb_epoch_enqueue(pb_epoch* sched, int32_t adapter, int64_t request_id);
+PB_API pb_status pb_epoch_next(pb_epoch* sched, double now_ms, int32_t max_batch, int32_t* adapter,
+                               int32_t* switch_needed, int64_t* ids, int32_t* n);
+PB_API void pb_epoch_free(pb_epoch* sched);
 
 /* Warm re-run of the last trial's prefill on the now-resident merged weights (no load / merge / gather,
  * no readiness waits on weights): the single-GPU-resident regime after T_full. Used by bench.py

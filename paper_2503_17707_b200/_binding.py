@@ -47,7 +47,7 @@ class pb_plan_sizes_t(C.Structure):
     _fields_ = [("host_base_bytes", C.c_int64), ("host_adapter_bytes", C.c_int64),
                 ("dev_weight_bytes", C.c_int64), ("dev_adapter_bytes", C.c_int64),
                 ("n_tensors", C.c_int32), ("n_atensors", C.c_int32), ("n_chunks", C.c_int32), ("n_gpus", C.c_int32),
-                ("dev_adapted_bytes", C.c_int64)]
+                ("dev_adapted_bytes", C.c_int64), ("dev_backup_bytes", C.c_int64)]
 
 
 class pb_tensor_info(C.Structure):
@@ -66,7 +66,8 @@ class pb_rank_bufs(C.Structure):
                 ("adapters_cap", C.c_int64), ("adapted", C.c_void_p), ("adapted_cap", C.c_int64),
                 ("workspace", C.c_void_p), ("workspace_cap", C.c_int64),
                 ("max_batch", C.c_int32), ("max_seq", C.c_int32), ("stream_h2d", C.c_void_p * 2),
-                ("stream_merge", C.c_void_p), ("stream_nvlink", C.c_void_p), ("stream_compute", C.c_void_p)]
+                ("stream_merge", C.c_void_p), ("stream_nvlink", C.c_void_p), ("stream_compute", C.c_void_p),
+                ("backup", C.c_void_p), ("backup_cap", C.c_int64)]
 
 
 class pb_timeline_t(C.Structure):
@@ -109,6 +110,13 @@ _SIGS = {
     "pb_prefill_enqueue_ex": [_P, _P, _P, C.c_int32, C.c_int32],
     "pb_prefill_wait": [_P, _P, _P],
     "pb_prefill_replay": [_P, C.c_uint32, _P, C.c_int32, C.c_int32],
+    "pb_switch_adapter": [_P, C.c_int32],
+    "pb_epoch_create": [C.c_int32, C.c_double, C.c_int32, C.POINTER(_P)],
+    "pb_epoch_set_active": [_P, C.c_int32, C.c_double],
+    "pb_epoch_enqueue": [_P, C.c_int32, C.c_int64],
+    "pb_epoch_next": [_P, C.c_double, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32), _P,
+                      C.POINTER(C.c_int32)],
+    "pb_epoch_free": [_P],
     "pb_prefill_first_token": [_P, _P, C.c_int32, C.c_int32, _P, _P],
     "pb_sync": [_P],
     "pb_timeline": [_P, C.POINTER(pb_timeline_t)],
@@ -132,7 +140,7 @@ _SIGS = {
     "pb_op_argmax": [_P, C.c_int32, C.c_int32, C.c_int32, _P, _P, _P],
     "pb_op_embed": [_P, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P],
 }
-_VOID = {"pb_plan_free", "pb_ctx_free"}
+_VOID = {"pb_plan_free", "pb_ctx_free", "pb_epoch_free"}
 
 _lib = None
 
@@ -286,6 +294,41 @@ def pb_prefill_enqueue(ctx, tokens_ptr, batch, seq):
 
 def pb_prefill_replay(ctx, epoch, tokens_ptr, batch, seq):
     check(lib().pb_prefill_replay(ctx, epoch, tokens_ptr, batch, seq))
+
+
+class EpochScheduler:
+    """pb_epoch_*: f2 epoch-based adapter scheduling (host side)."""
+
+    def __init__(self, n_adapters, epoch_ms, starvation_epochs=3):
+        self.h = _P()
+        check(lib().pb_epoch_create(n_adapters, epoch_ms, starvation_epochs, C.byref(self.h)))
+
+    def set_active(self, adapter, now_ms=0.0):
+        check(lib().pb_epoch_set_active(self.h, adapter, now_ms))
+
+    def enqueue(self, adapter, request_id):
+        check(lib().pb_epoch_enqueue(self.h, adapter, request_id))
+
+    def next_batch(self, now_ms, max_batch):
+        import numpy as np
+        a, sw, n = C.c_int32(0), C.c_int32(0), C.c_int32(0)
+        ids = np.zeros(max_batch, dtype=np.int64)
+        check(lib().pb_epoch_next(self.h, now_ms, max_batch, C.byref(a), C.byref(sw), ids.ctypes.data, C.byref(n)))
+        if a.value == -2:
+            return None, False, []
+        return a.value, bool(sw.value), [int(x) for x in ids[:n.value]]
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().pb_epoch_free(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+def pb_switch_adapter(ctx, adapter_id):
+    check(lib().pb_switch_adapter(ctx, adapter_id))
 
 
 def pb_prefill_enqueue_ex(ctx, tokens_ptr, adapter_of_seq_ptr, batch, seq):

@@ -104,10 +104,11 @@ class RankEngine:
 
     def __init__(self, plan: Plan, rank: int, host_base: torch.Tensor, host_adapters: Optional[torch.Tensor],
                  max_batch: int = 1, max_seq: int = 128, device: Optional[torch.device] = None,
-                 multi_adapter: bool = False, reuse: Optional["RankEngine"] = None):
+                 multi_adapter: bool = False, reuse: Optional["RankEngine"] = None, switchable: bool = False):
         """multi_adapter=True allocates the out-of-place per-adapter copies (PB_MERGE_ALL mode).
         reuse: a (closed or live) engine of the same GPU whose weight / adapter buffers hold what a re-plan
-        (Plan.replan) marks as resident — the recovery trial continues in them instead of fresh buffers."""
+        (Plan.replan) marks as resident — the recovery trial continues in them instead of fresh buffers.
+        switchable=True allocates the pristine-base buffer that pb_switch_adapter (f2) re-merges from."""
         self.plan = plan
         self.rank = rank
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
@@ -123,6 +124,8 @@ class RankEngine:
                 self.adapters = torch.empty(max(s.dev_adapter_bytes, 1), dtype=torch.uint8, device=self.device)
                 self.adapted = (torch.empty(s.dev_adapted_bytes, dtype=torch.uint8, device=self.device)
                                 if multi_adapter and s.dev_adapted_bytes else None)
+            self.backup = (torch.empty(s.dev_backup_bytes, dtype=torch.uint8, device=self.device)
+                           if switchable and s.dev_backup_bytes else None)
             ws = plan.workspace_bytes(max_batch, max_seq)
             self.workspace = torch.empty(ws, dtype=torch.uint8, device=self.device)
             # streams: NULL -> the ctx creates five distinct non-blocking streams (torch's stream pool
@@ -143,6 +146,8 @@ class RankEngine:
         self.bufs.stream_merge = None
         self.bufs.stream_nvlink = None
         self.bufs.stream_compute = None
+        self.bufs.backup = self.backup.data_ptr() if self.backup is not None else None
+        self.bufs.backup_cap = self.backup.numel() if self.backup is not None else 0
         ha = host_adapters.data_ptr() if (host_adapters is not None and s.host_adapter_bytes) else None
         with torch.cuda.device(self.device):
             self.ctx = B.pb_ctx_create(plan.handle, rank, host_base.data_ptr(), ha, self.bufs)
@@ -218,6 +223,12 @@ class RankEngine:
             batch, seq = np.asarray(tokens).shape
         self.enqueue(epoch, tokens, batch, seq, adapter_id)
         return self.wait(want_logits)
+
+    def switch_adapter(self, adapter_id: int):
+        """f2: re-merge this rank's stage with `adapter_id` (-1: base model) behind the prefills
+        already enqueued; serve the next batch with replay_enqueue."""
+        with torch.cuda.device(self.device):
+            B.pb_switch_adapter(self.ctx, adapter_id)
 
     def replay_enqueue(self, epoch: int, tokens: Optional[np.ndarray], batch: int, seq: int):
         """Warm prefill re-run on the resident weights (pb_prefill_replay); complete with wait()."""

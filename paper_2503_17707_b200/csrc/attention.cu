@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
              *s_free = bars + 5, *p_full = bars + 6, *o_full = bars + 7;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
 
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    pdl_launch_dependents();
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int h = blockIdx.y, b = blockIdx.z, kvh = h / group;
     const int qtile = gridDim.x - 1 - blockIdx.x;          // longest (latest) query tiles first
@@ -82,6 +82,7 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     const uint32_t tS = tmem, tO = tmem + 128;
+    pdl_wait();   // q/k/v are the previous kernel's output
 
     if (warp == 4) {
         if (lane == 0) {
@@ -258,7 +259,7 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
 
 template <int HD>
 cudaError_t launch_tc(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int ldo, int t0, int t1, int B, int H,
-                      int group, int k_col0, int v_col0, float score_scale, cudaStream_t s) {
+                      int group, int k_col0, int v_col0, float score_scale, cudaStream_t s, bool pdl) {
     // 3-D view of the token-major rows: (col, sequence b, position t), t extent = t1 (keys >= t1 zero-filled).
     const uint64_t dims[3] = {(uint64_t)ld, (uint64_t)B, (uint64_t)t1};
     const uint64_t strides[2] = {(uint64_t)ld * 2, (uint64_t)ld * 2 * B};
@@ -267,12 +268,12 @@ cudaError_t launch_tc(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int 
     char err[256];
     if (!make_map_bf16_3d(&map, qkv, dims, strides, box, 128, err, sizeof err)) return cudaErrorInvalidValue;
     using SM = AttnSmem<HD>;
-    cudaError_t e = cudaFuncSetAttribute(attention_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::kTotal);
+    cudaError_t e = smem_attr_once<attention_tc_kernel<HD>>(SM::kTotal);
     if (e != cudaSuccess) return e;
     const dim3 grid((t1 - t0 + QT - 1) / QT, H, B);
     const float scale_log2 = score_scale * 1.4426950408889634f;
-    attention_tc_kernel<HD><<<grid, 160, SM::kTotal, s>>>(map, out, ldo, t0, t1, group, k_col0, v_col0, scale_log2);
-    return cudaGetLastError();
+    return launch_pdl(attention_tc_kernel<HD>, grid, 160, SM::kTotal, s, pdl, map, out, ldo, t0, t1, group, k_col0,
+                      v_col0, scale_log2);
 }
 
 }  // namespace
@@ -286,15 +287,15 @@ cudaError_t warm_attention_kernels() {
 
 cudaError_t launch_attention(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int ldo, int t0, int t1, int B,
                              int n_heads, int n_kv_heads, int hd, int k_col0, int v_col0, float score_scale,
-                             cudaStream_t s) {
+                             cudaStream_t s, bool pdl) {
     if (t1 <= t0) return cudaSuccess;
     const bool tma_ok = (ld % 8) == 0 && (reinterpret_cast<uintptr_t>(qkv) & 15) == 0 && (ldo % 8) == 0 &&
                         (k_col0 % 8) == 0 && (v_col0 % 8) == 0;
     const int group = n_heads / n_kv_heads;
     if (tma_ok && hd == 64)
-        return launch_tc<64>(qkv, ld, out, ldo, t0, t1, B, n_heads, group, k_col0, v_col0, score_scale, s);
+        return launch_tc<64>(qkv, ld, out, ldo, t0, t1, B, n_heads, group, k_col0, v_col0, score_scale, s, pdl);
     if (tma_ok && hd == 128)
-        return launch_tc<128>(qkv, ld, out, ldo, t0, t1, B, n_heads, group, k_col0, v_col0, score_scale, s);
+        return launch_tc<128>(qkv, ld, out, ldo, t0, t1, B, n_heads, group, k_col0, v_col0, score_scale, s, pdl);
     return launch_attention_simt(qkv, ld, out, ldo, t0, t1, B, n_heads, n_kv_heads, hd, k_col0, v_col0, score_scale,
                                  s);
 }

@@ -59,10 +59,6 @@ __device__ __forceinline__ float4 ld_cluster_f4(uint32_t addr) {
                  : "memory");
     return v;
 }
-// Programmatic dependent launch: let the next kernel of the stream get scheduled now; wait for the previous
-// kernel's completion (and memory) before touching anything it writes. Both are no-ops without PDL.
-__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // Partial tile: [128 rows][32 float4 chunks], chunk c of row r stored at slot c ^ (r & 31) (conflict-free
 // row-per-thread writes, and conflict-free chunk-per-thread reads).
@@ -286,8 +282,7 @@ cudaError_t launch_es(const CUtensorMap& mapX, const CUtensorMap& mapW, const Ge
     const int ctas = grid.x * grid.y * grid.z;
     const int stages = ctas <= 148 ? MAX_STAGES : 3;
     const int smem = smem_bytes(stages);
-    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<EPI, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         smem_bytes(MAX_STAGES));
+    cudaError_t e = smem_attr_once<gemm_kernel<EPI, S>>(smem_bytes(MAX_STAGES));
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;

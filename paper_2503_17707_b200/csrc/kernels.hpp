@@ -4,9 +4,43 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
 
 namespace pb {
+
+// Launch with an optional programmatic-dependent-launch edge to the previous kernel of the stream (the kernel
+// must call pdl_wait() before reading anything that kernel wrote).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
+                              Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): the call costs microseconds of host
+// time and the prefill issues thousands of launches, which would leave the GPU waiting on the issuer.
+template <auto Fn>
+inline cudaError_t smem_attr_once(int bytes) {
+    static std::atomic<unsigned long long> done{0};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    e = cudaFuncSetAttribute(Fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_release);
+    return e;
+}
 
 // ---------------------------------------------------------------- tensor maps (TMA)
 // Resolved once from the driver (cudaGetDriverEntryPoint), no libcuda link dependency.
@@ -74,7 +108,7 @@ cudaError_t launch_gemm(const CUtensorMap& mapX, const CUtensorMap& mapW, const 
 // ---------------------------------------------------------------- SIMT kernels
 // Row norm over d of fp32 rows -> bf16: LayerNorm (beta != null) or RMSNorm (beta == null).
 cudaError_t launch_norm(const float* h, int ldh, __nv_bfloat16* out, int ldo, int rows, int d, const __nv_bfloat16* gamma,
-                        const __nv_bfloat16* beta, float eps, cudaStream_t s);
+                        const __nv_bfloat16* beta, float eps, cudaStream_t s, bool pdl = false);
 
 struct EmbedSrc {
     const void* base[8];           // embedding table of each owner (peer pointers allowed); bf16 or fp32
@@ -83,30 +117,30 @@ struct EmbedSrc {
 };
 // h[row, :] = E[tok[row]] (+ P[pos(row) + 2]) as fp32, rows [r0, r1), row = t * B + b.
 cudaError_t launch_embed(const EmbedSrc& E, const __nv_bfloat16* pos, const int32_t* tok, float* h, int d, int r0,
-                         int r1, int B, cudaStream_t s);
+                         int r1, int B, cudaStream_t s, bool pdl = false);
 
 // RoPE cos/sin table [T x hd/2] (float2), angles t * theta^(-2i/hd) computed in fp64.
 cudaError_t launch_rope_table(float2* table, int T, int hd, double theta, cudaStream_t s);
 // In-place rotate_half RoPE on q (n_q heads at col 0) and k (n_k heads at col q_cols) of rows [r0, r1).
 cudaError_t launch_rope(__nv_bfloat16* qkv, int ld, int r0, int r1, int B, int n_q, int n_k, int hd, int k_col0,
-                        const float2* table, cudaStream_t s);
+                        const float2* table, cudaStream_t s, bool pdl = false);
 
 // Causal attention for query rows [t0, t1) (token-major rows t*B+b) against keys [0, t] of the same
 // sequence; q at col h*hd, k at k_col0 + (h/group)*hd, v at v_col0 + (h/group)*hd of `qkv`.
 // hd = 64 or 128: tensor-core kernel (attention.cu); other head sizes: the SIMT kernel (simt.cu).
 cudaError_t launch_attention(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int ldo, int t0, int t1, int B,
                              int n_heads, int n_kv_heads, int hd, int k_col0, int v_col0, float score_scale,
-                             cudaStream_t s);
+                             cudaStream_t s, bool pdl = false);
 cudaError_t launch_attention_simt(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int ldo, int t0, int t1,
                                   int B, int n_heads, int n_kv_heads, int hd, int k_col0, int v_col0,
                                   float score_scale, cudaStream_t s);
 
 // logits[b, v] = sum_c y[b, c] * E[v, c] for v in [v0, v1) (fp32 out, row pitch ldl).
 cudaError_t launch_logits(const __nv_bfloat16* y, int B, int d, const __nv_bfloat16* E, int v0, int v1, float* logits,
-                          int ldl, cudaStream_t s);
+                          int ldl, cudaStream_t s, bool pdl = false);
 // tokens[b] = argmax_v logits[b, v] (lowest index on ties); *nan_flag |= 1 if any logit is not finite.
 cudaError_t launch_argmax(const float* logits, int B, int V, int ldl, int32_t* tokens, int32_t* nan_flag,
-                          cudaStream_t s);
+                          cudaStream_t s, bool pdl = false);
 
 // Load every kernel of the library into the current context (CUDA lazy module loading otherwise loads a
 // function at its first launch; concurrent first launches from several issuer threads were measured to

@@ -109,9 +109,8 @@ int32_t pb_plan::stage_of_layer(int32_t l) const {
 }
 
 int32_t pb_plan::find_tensor(const std::string& name) const {
-    for (size_t i = 0; i < tensors.size(); ++i)
-        if (tensors[i].name == name) return (int32_t)i;
-    return -1;
+    auto it = name_index.find(name);
+    return it == name_index.end() ? -1 : it->second;
 }
 
 static int32_t layer_loader(const pb_plan* p, int32_t l) {
@@ -190,6 +189,7 @@ extern "C" pb_status pb_plan_create(const pb_model_desc* model, const pb_adapter
             host += t.bytes();
         }
         idx[t.name] = (int32_t)p->tensors.size();
+        p->name_index[t.name] = (int32_t)p->tensors.size();
         p->tensors.push_back(t);
     }
     p->dev_weight_bytes = round_up(dev, kAlign);
@@ -240,6 +240,17 @@ extern "C" pb_status pb_plan_create(const pb_model_desc* model, const pb_adapter
                     off += p->tensors[mr.base].bytes();
                 }
         p->dev_adapted_bytes = round_up(off, kAlign);
+        // f2: pristine copy of every tensor some adapter modifies (one region, union over adapters), saved by
+        // the cold-start merges so an adapter switch re-merges from the base (no bf16 drift across switches).
+        p->backup_off.assign(NT, -1);
+        off = 0;
+        for (auto& mr : p->merges)
+            if (p->backup_off[mr.base] < 0) {
+                off = round_up(off, kAlign);
+                p->backup_off[mr.base] = off;
+                off += p->tensors[mr.base].bytes();
+            }
+        p->dev_backup_bytes = round_up(off, kAlign);
     }
 
     // Step 3: pieces -> chunks (global ids: base tensors in table order, then adapter factors).
@@ -593,6 +604,7 @@ extern "C" pb_status pb_plan_sizes(const pb_plan* p, pb_plan_sizes_t* out) {
     out->dev_weight_bytes = p->dev_weight_bytes;
     out->dev_adapter_bytes = p->host_adapter_bytes;
     out->dev_adapted_bytes = p->dev_adapted_bytes;
+    out->dev_backup_bytes = p->dev_backup_bytes;
     out->n_tensors = (int32_t)p->tensors.size();
     out->n_atensors = (int32_t)p->atensors.size();
     out->n_chunks = (int32_t)p->chunks.size();

@@ -2,6 +2,7 @@
 #pragma once
 #include <cstdint>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/pipeboost.h"
@@ -69,6 +70,9 @@ struct pb_plan {
     // in a separate device region. adapted_off[a * n_tensors + t] = offset, or -1 when adapter a does not touch t.
     std::vector<int64_t> adapted_off;
     int64_t dev_adapted_bytes = 0;
+    // f2 adapter switching: backup_off[t] = offset of tensor t's pristine copy (-1: no adapter touches t)
+    std::vector<int64_t> backup_off;
+    int64_t dev_backup_bytes = 0;
     // f1 re-plans (pb_plan_replan): original GPU of every new rank, and per rank the chunks it already holds
     // (never loaded or received again). Empty for a plan made by pb_plan_create.
     std::vector<int32_t> survivors;
@@ -82,5 +86,6 @@ struct pb_plan {
     bool f32() const { return model.dtype == PB_DTYPE_F32; }
     int32_t es() const { return f32() ? 4 : 2; }
     int32_t stage_of_layer(int32_t l) const;
-    int32_t find_tensor(const std::string& name) const;   // -1 if absent
+    int32_t find_tensor(const std::string& name) const;   // -1 if absent (O(1): the prefill looks tensors up per layer)
+    std::unordered_map<std::string, int32_t> name_index;
 };

@@ -324,6 +324,10 @@ extern "C" pb_status pb_ctx_create(const pb_plan* plan, int32_t rank, const void
     if (plan->adapters.size() > 0 && bufs->adapted && bufs->adapted_cap >= plan->dev_adapted_bytes &&
         plan->dev_adapted_bytes > 0)
         c->adapted = static_cast<char*>(bufs->adapted);
+    if (plan->dev_backup_bytes > 0 && bufs->backup && bufs->backup_cap >= plan->dev_backup_bytes)
+        c->backup = static_cast<char*>(bufs->backup);
+    c->in_load.assign(plan->chunks.size(), 0);
+    for (int32_t id : plan->load[rank]) c->in_load[id] = 1;
     c->bufs = *bufs;
     c->h2d[0] = (cudaStream_t)bufs->stream_h2d[0];
     c->h2d[1] = (cudaStream_t)bufs->stream_h2d[1];
@@ -425,6 +429,7 @@ extern "C" void pb_ctx_free(pb_ctx* c) {
     for (auto e : c->landed) d(e);
     for (auto e : c->gathered) d(e);
     for (auto& r : c->prof) { d(r.a); d(r.b); }
+    for (auto& g : c->replay_graphs) cudaGraphExecDestroy(g.exec);
     for (auto& p : c->peers)
         for (void* b : p.ipc_bases) cudaIpcCloseMemHandle(b);
     if (c->h_tokens) cudaFreeHost(c->h_tokens);
@@ -523,6 +528,12 @@ static uint32_t* flag_ptr(char* ws, const WsLayout& L, int32_t word) {
     return reinterpret_cast<uint32_t*>(ws + L.flags) + word;
 }
 
+// Record an event observed outside the work (timeline, profiling): while the replay is being captured into a
+// CUDA graph it must become an event-record node (cudaEventRecordExternal), not a capture-internal dependency.
+static cudaError_t record_ev(pb_ctx* c, cudaEvent_t e, cudaStream_t s) {
+    return c->capturing ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal) : cudaEventRecord(e, s);
+}
+
 static int prof_begin(pb_ctx* c, int cls, cudaStream_t s) {
     if (!c->profiling) return -1;
     if (c->prof_n == c->prof.size()) {
@@ -533,7 +544,7 @@ static int prof_begin(pb_ctx* c, int cls, cudaStream_t s) {
     ProfRec& r = c->prof[c->prof_n];
     r.cls = cls;
     r.flops = r.bytes = 0;
-    if (cudaEventRecord(r.a, s) != cudaSuccess) return -1;
+    if (record_ev(c, r.a, s) != cudaSuccess) return -1;
     return (int)c->prof_n++;
 }
 
@@ -542,7 +553,7 @@ static void prof_end(pb_ctx* c, int i, cudaStream_t s, double flops, double byte
     ProfRec& r = c->prof[i];
     r.flops = flops;
     r.bytes = bytes;
-    cudaEventRecord(r.b, s);
+    record_ev(c, r.b, s);
 }
 
 // Publish readiness word `word` (= epoch) on the given ranks.
@@ -772,7 +783,7 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, boo
     auto norm = [&](const char* g_name, const char* b_name) -> cudaError_t {
         const int pi = prof_begin(c, K_NORM, s);
         cudaError_t e = launch_norm(h + (size_t)r0 * d, d, x + (size_t)r0 * d, d, rows, d, wt(c, l, g_name),
-                                    opt ? wt(c, l, b_name) : nullptr, m.norm_eps, s);
+                                    opt ? wt(c, l, b_name) : nullptr, m.norm_eps, s, !c->profiling);
         prof_end(c, pi, s, 8.0 * rows * d, 6.0 * rows * d);
         return e;
     };
@@ -787,13 +798,13 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, boo
     if (!opt) {
         const int pi = prof_begin(c, K_ROPE, s);
         CU(launch_rope(qkv + (size_t)row_base * qdim, qdim, r0 - row_base, r1 - row_base, B, H, KVH, hd, qd,
-                       reinterpret_cast<const float2*>(c->ws + L.rope), s));
+                       reinterpret_cast<const float2*>(c->ws + L.rope), s, !c->profiling));
         prof_end(c, pi, s, 6.0 * rows * (qd + kvd) / 2, 4.0 * rows * (qd + kvd));
     }
     {
         const int pi = prof_begin(c, K_ATTN, s);
         CU(launch_attention(qkv + (size_t)row_base * qdim, qdim, attn + (size_t)row_base * qd, qd, ta, tb, B, H, KVH,
-                            hd, qd, qd + kvd, opt ? 1.0f : 1.0f / sqrtf((float)hd), s));
+                            hd, qd, qd + kvd, opt ? 1.0f : 1.0f / sqrtf((float)hd), s, !c->profiling));
         // causal pairs: sum over queries t in [ta, tb) of (t + 1) keys
         const double pairs = (double)B * ((double)tb * (tb + 1) / 2 - (double)ta * (ta + 1) / 2);
         prof_end(c, pi, s, 4.0 * pairs * H * hd, 2.0 * rows * qd * 2 + 2.0 * B * tb * 2 * kvd);
@@ -908,6 +919,7 @@ namespace {
 
 struct Budget {
     static constexpr int kMarkEvery = 16, kCap = 384;
+    bool capture = false;          // stream capture: nothing executes, no queue to bound, no events to poll
     cudaStream_t s = nullptr;
     cudaEvent_t* pool = nullptr;   // kPool events, reused cyclically (at most kCap/kMarkEvery+1 in flight)
     size_t next = 0;
@@ -928,12 +940,13 @@ struct Budget {
     // True when n more ops fit. A request larger than the cap is admitted once the stream is empty; the
     // ops issued since the last mark get a mark of their own so that "empty" becomes observable.
     bool can(long n) {
-        if (issued - done + n <= kCap) return true;
+        if (capture || issued - done + n <= kCap) return true;
         if (since > 0 && mark() != cudaSuccess) return false;
         poll();
         return issued - done + n <= kCap || issued == done;
     }
     cudaError_t add(long n) {
+        if (capture) return cudaSuccess;
         issued += n;
         since += n;
         return since >= kMarkEvery ? mark() : cudaSuccess;
@@ -987,6 +1000,12 @@ pb_status issue_group(Issuer& I, size_t gi) {
         CU(cudaStreamWaitEvent(c->merge, landed_ev(c, id), 0));
         ++mops;
         const bool all = c->merge_adapter == PB_MERGE_ALL;
+        if (c->backup && !all && p->backup_off[ch.tensor] >= 0) {   // f2: keep the pristine base of the chunk
+            CU(launch_copy(c->backup + p->backup_off[ch.tensor] + (int64_t)ch.r0 * p->tensors[ch.tensor].row_bytes(),
+                           c->weights + ch.dev_off, ch.bytes, c->merge));
+            ++c->n_launches;
+            ++mops;
+        }
         if (all) {   // out of place: rows of the chunk no merge of adapter a writes are copied on the SMs
             const size_t NT = p->tensors.size();
             const TensorRec& t = p->tensors[ch.tensor];
@@ -1068,7 +1087,7 @@ long group_merge_ops(Issuer& I, size_t gi) {
     long n = 0;
     for (int32_t i = g.first; i < g.first + g.count; ++i) {
         const int32_t id = c->plan->load[c->rank][i];
-        n += 6 + (long)c->plan->adapters.size() + (long)c->jobs_of_chunk[id].size() * (5 + prof_ops(c));
+        n += 7 + (long)c->plan->adapters.size() + (long)c->jobs_of_chunk[id].size() * (5 + prof_ops(c));
     }
     return n;
 }
@@ -1250,7 +1269,7 @@ pb_status issue_item(Issuer& I, const Item& it) {
             else
                 CU(launch_embed(E, opt ? wt(c, -1, "pos") : nullptr,
                                 reinterpret_cast<const int32_t*>(c->ws + L.tokens) + row_base, h + (size_t)row_base * d,
-                                d, r0 - row_base, r1 - row_base, Bk, s));
+                                d, r0 - row_base, r1 - row_base, Bk, s, !c->profiling));
             prof_end(c, pi, s, (opt ? 1.0 : 0.0) * (r1 - r0) * d, (r1 - r0) * d * (opt ? 8.0 : 6.0));
             ++c->n_launches;
             break;
@@ -1284,7 +1303,7 @@ pb_status issue_item(Issuer& I, const Item& it) {
                                    opt ? wt_f32(c, -1, "final_b") : nullptr, m.norm_eps, s));
             else
                 CU(launch_norm(last, ldh, y, d, B, d, wt(c, -1, "final_g"), opt ? wt(c, -1, "final_b") : nullptr,
-                               m.norm_eps, s));
+                               m.norm_eps, s, !c->profiling));
             prof_end(c, pi, s, 8.0 * B * d, 6.0 * B * d);
             ++c->n_launches;
             std::vector<int32_t> remote;
@@ -1312,7 +1331,7 @@ pb_status issue_item(Issuer& I, const Item& it) {
                 CU(launch_logits_f32(reinterpret_cast<const float*>(c->ws + L.y), B, d,
                                      reinterpret_cast<const float*>(E), v0, v1, logits, V, s));
             else
-                CU(launch_logits(y, B, d, E, v0, v1, logits, V, s));
+                CU(launch_logits(y, B, d, E, v0, v1, logits, V, s, !c->profiling));
             prof_end(c, pi, s, 2.0 * B * (v1 - v0) * d, 2.0 * (double)(v1 - v0) * d + 4.0 * B * (v1 - v0));
             ++c->n_launches;
             if (g != 0) {
@@ -1327,7 +1346,7 @@ pb_status issue_item(Issuer& I, const Item& it) {
                 if (r != 0) CU(wait_word(c, L.f_logit + r, s));
             const int pi = prof_begin(c, K_ARGMAX, s);
             CU(launch_argmax(logits, B, V, V, reinterpret_cast<int32_t*>(c->ws + L.tok_out),
-                             reinterpret_cast<int32_t*>(c->ws + L.nan), s));
+                             reinterpret_cast<int32_t*>(c->ws + L.nan), s, !c->profiling));
             prof_end(c, pi, s, 0, 4.0 * B * V);
             ++c->n_launches;
             CU(cudaMemcpyAsync(c->h_out, c->ws + L.tok_out, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, s));
@@ -1335,7 +1354,7 @@ pb_status issue_item(Issuer& I, const Item& it) {
             break;
         }
         case I_DONE:
-            CU(cudaEventRecord(c->done, s));
+            CU(record_ev(c, c->done, s));
             break;
     }
     return PB_OK;
@@ -1364,6 +1383,7 @@ pb_status issue_trial(pb_ctx* c, int B, int T, bool replay) {
     for (int i = 0; i < 4; ++i) {
         bs[i]->s = ss[i];
         bs[i]->pool = c->budget_events.data() + i * kEventPool;
+        bs[i]->capture = c->capturing;
     }
     build_items(I);
     if (!replay && c->rank == 0) {   // prompt tokens first on the copy lane: they land in microseconds
@@ -1501,8 +1521,118 @@ extern "C" pb_status pb_prefill_replay(pb_ctx* c, uint32_t epoch, const int32_t*
     c->epoch = epoch;
     c->n_launches = 0;
     c->prof_n = 0;
+    if (c->n == 1 && c->merge_adapter != PB_MERGE_ALL) {
+        // Single rank: the replay has no cross-rank waits, so it is captured once as a CUDA graph and relaunched
+        // (the token upload / result download are graph nodes on the pinned staging buffers).
+        if (B < 1 || T < 1 || B > c->L.max_batch || T > c->L.max_seq || (int64_t)B * T > c->L.max_rows)
+            return fail(PB_EINVAL, "batch %d x seq %d exceeds the workspace", B, T);
+        if (!tokens) return fail(PB_EINVAL, "rank 0 needs tokens");
+        for (int b = 0; b < B; ++b)
+            for (int t = 0; t < T; ++t) c->h_tokens[t * B + b] = tokens[(size_t)b * T + t];
+        c->cur_batch = B;
+        c->cur_seq = T;
+        const int pi = c->profiling ? 1 : 0;
+        pb_ctx::ReplayGraph* rg = nullptr;
+        for (auto& g : c->replay_graphs)
+            if (g.B == B && g.T == T && g.profiled == pi) rg = &g;
+        if (!rg) {
+            CU(cudaStreamBeginCapture(c->comp, cudaStreamCaptureModeThreadLocal));
+            c->capturing = true;
+            pb_status ist = issue_trial(c, B, T, true);
+            c->capturing = false;
+            cudaGraph_t g = nullptr;
+            cudaError_t ce = cudaStreamEndCapture(c->comp, &g);
+            if (ist != PB_OK) {
+                if (g) cudaGraphDestroy(g);
+                return ist;
+            }
+            CU(ce);
+            cudaGraphExec_t ge = nullptr;
+            cudaError_t ie = cudaGraphInstantiate(&ge, g, 0);
+            cudaGraphDestroy(g);
+            CU(ie);
+            c->replay_graphs.push_back({B, T, pi, ge, c->n_launches, c->prof_n,
+                                        std::vector<ProfRec>(c->prof.begin(), c->prof.begin() + c->prof_n)});
+            rg = &c->replay_graphs.back();
+        }
+        c->n_launches = rg->launches;
+        c->prof_n = rg->prof_n;
+        for (size_t i = 0; i < rg->prof_n; ++i) c->prof[i] = rg->prof[i];
+        c->issue_status = PB_OK;
+        c->phase = Phase::Prefilled;
+        CU(cudaEventRecord(c->t0, c->comp));
+        CU(cudaGraphLaunch(rg->exec, c->comp));
+        return PB_OK;
+    }
     CU(cudaEventRecord(c->t0, c->comp));
     return start_issuer(c, tokens, nullptr, B, T, true);
+}
+
+// ------------------------------------------------------------------------------------------------
+// f2 — epoch-based adapter switching
+// ------------------------------------------------------------------------------------------------
+extern "C" pb_status pb_switch_adapter(pb_ctx* c, int32_t adapter_id) {
+    pb_status st = check_ctx(c, "pb_switch_adapter");
+    if (st) return st;
+    const pb_plan* p = c->plan;
+    if (c->phase != Phase::Prefilled) return fail(PB_EPROTOCOL, "pb_switch_adapter: needs a completed cold start");
+    if (c->merge_adapter == PB_MERGE_ALL)
+        return fail(PB_EUNSUPPORTED, "pb_switch_adapter: PB_MERGE_ALL already holds every adapter (per-sequence)");
+    if (adapter_id < -1 || adapter_id >= (int32_t)p->adapters.size())
+        return fail(PB_EINVAL, "adapter_id %d out of range", adapter_id);
+    if (!c->backup) return fail(PB_ENOMEM, "pb_switch_adapter needs bufs.backup >= dev_backup_bytes");
+    if (!p->survivors.empty()) return fail(PB_EUNSUPPORTED, "pb_switch_adapter on a re-plan");
+    join_load(c);   // the trial issuer has issued everything: the switch queues behind it on the compute stream
+    if (c->issue_status != PB_OK) return fail(c->issue_status, "%s", c->issue_msg);
+    cudaStream_t s = c->comp;
+    const auto stage = p->stages[c->rank];
+    const char* hb = static_cast<const char*>(c->host_base);
+    const char* ha = static_cast<const char*>(c->host_adapters);
+    auto in_stage = [&](int32_t t) { return p->tensors[t].layer >= stage.first && p->tensors[t].layer < stage.second; };
+    // 1. restore the pristine base of every adapted tensor of the stage: from the copy saved by this rank's
+    //    cold-start merge where it loaded the chunk, else from the host image
+    for (const ChunkRec& ch : p->chunks) {
+        if (ch.is_adapter || !in_stage(ch.tensor) || p->backup_off[ch.tensor] < 0) continue;
+        if (c->in_load[ch.id]) {
+            CU(launch_copy(c->weights + ch.dev_off,
+                           c->backup + p->backup_off[ch.tensor] + (int64_t)ch.r0 * p->tensors[ch.tensor].row_bytes(),
+                           ch.bytes, s));
+            ++c->n_launches;
+        } else {
+            CU(cudaMemcpyAsync(c->weights + ch.dev_off, hb + ch.host_off, ch.bytes, cudaMemcpyHostToDevice, s));
+        }
+    }
+    // 2. merge the new adapter in place (factors this rank did not load come from the host image)
+    if (adapter_id >= 0) {
+        for (const ChunkRec& ch : p->chunks)
+            if (ch.is_adapter && p->atensors[ch.tensor].adapter == adapter_id && in_stage(p->atensors[ch.tensor].base) &&
+                !c->in_load[ch.id])
+                CU(cudaMemcpyAsync(c->adapters + ch.dev_off, ha + ch.host_off, ch.bytes, cudaMemcpyHostToDevice, s));
+        char err[512];
+        for (const MergeRec& mr : p->merges) {
+            if (mr.adapter != adapter_id || !in_stage(mr.base)) continue;
+            const TensorRec& bt = p->tensors[mr.base];
+            const ATensorRec& A = p->atensors[mr.a_tensor];
+            const ATensorRec& Bf = p->atensors[mr.b_tensor];
+            const int rank = p->adapters[adapter_id].rank;
+            const float scale = p->adapters[adapter_id].alpha / (float)rank;
+            char* W = c->weights + bt.dev_off + (int64_t)mr.row0 * bt.row_bytes();
+            if (p->f32()) {
+                CU(launch_merge_f32(reinterpret_cast<const float*>(W), reinterpret_cast<float*>(W), bt.cols, mr.rows,
+                                    mr.cols, reinterpret_cast<const float*>(c->adapters + Bf.off),
+                                    reinterpret_cast<const float*>(c->adapters + A.off), rank, scale, s));
+            } else {
+                MergeMaps maps;
+                if (!make_merge_maps(&maps, W, bt.cols, mr.rows, mr.cols, c->adapters + Bf.off, c->adapters + A.off,
+                                     rank, err, sizeof err))
+                    return fail(PB_EINVAL, "merge map: %s", err);
+                CU(launch_merge(maps, mr.rows, mr.cols, rank, scale, s));
+            }
+            ++c->n_launches;
+        }
+    }
+    c->merge_adapter = adapter_id;
+    return PB_OK;
 }
 
 extern "C" pb_status pb_prefill_wait(pb_ctx* c, float* logits_out, int32_t* tokens_out) {

@@ -109,6 +109,8 @@ struct pb_ctx {
     std::vector<pb::LayerMaps> lmaps;   // indexed by layer (only this rank's stage is encoded)
     // multi-adapter (PB_MERGE_ALL): out-of-place copies and per-adapter weight maps [adapter][layer]
     char* adapted = nullptr;
+    char* backup = nullptr;              // f2: pristine copies of adapted tensors (bufs.backup), or null
+    std::vector<char> in_load;           // chunk is in this rank's load list (its pristine bytes were saved here)
     std::vector<std::vector<pb::LayerMaps>> lmaps_ad;
     std::vector<int32_t> seq_adapter;   // per sequence of the current trial (-1: base / single in-place adapter)
 
@@ -131,6 +133,17 @@ struct pb_ctx {
     std::vector<cudaEvent_t> budget_events;
     std::vector<cudaStream_t> owned_streams;   // created by the ctx when the caller passed NULL  // 4 streams x kEventPool progress marks
     bool profiling = false;
+    // Warm replay as a CUDA graph (single-rank contexts): captured once per (batch, seq, profiling) and
+    // relaunched, so the prefill's ~200 launches cost one host call instead of ~4 us of issue time each.
+    bool capturing = false;
+    struct ReplayGraph {
+        int32_t B, T, profiled;
+        cudaGraphExec_t exec;
+        int32_t launches;
+        size_t prof_n;
+        std::vector<pb::ProfRec> prof;   // class / algorithmic work of each timed launch (events shared)
+    };
+    std::vector<ReplayGraph> replay_graphs;
     std::vector<pb::ProfRec> prof;
     size_t prof_n = 0;
 };

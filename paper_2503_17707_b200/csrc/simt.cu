@@ -7,8 +7,10 @@
 #include <math_constants.h>
 
 #include "kernels.hpp"
+#include "sm100.cuh"
 
 namespace pb {
+using namespace sm100;
 
 namespace {
 
@@ -40,7 +42,8 @@ template <int NT, int PER>
 __global__ void __launch_bounds__(NT) norm_kernel(const float* __restrict__ h, int ldh, __nv_bfloat16* __restrict__ out,
                                                   int ldo, int d, const __nv_bfloat16* __restrict__ gamma,
                                                   const __nv_bfloat16* __restrict__ beta, float eps) {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // a PDL-launched GEMM may start its weight prefetch
+    pdl_launch_dependents();   // a PDL-launched GEMM may start its weight prefetch
+    pdl_wait();                // PDL-launched: the previous kernel's output is visible from here on
     __shared__ float red[32];
     const float* x = h + (size_t)blockIdx.x * ldh;
     float v[PER];
@@ -77,6 +80,8 @@ __global__ void __launch_bounds__(NT) norm_kernel(const float* __restrict__ h, i
 // ------------------------------------------------------------------ embedding (+ OPT learned positions)
 __global__ void embed_kernel(EmbedSrc E, const __nv_bfloat16* __restrict__ pos, const int32_t* __restrict__ tok,
                              float* __restrict__ h, int d, int r0, int B) {
+    pdl_launch_dependents();
+    pdl_wait();
     const int row = r0 + blockIdx.x;
     const int t = row / B;
     const int id = tok[row];
@@ -117,7 +122,8 @@ __global__ void rope_table_kernel(float2* table, int T, int hd, double theta) {
 // x'_i = x_i cos - x_{i+hd/2} sin ; x'_{i+hd/2} = x_{i+hd/2} cos + x_i sin   (HF rotate_half)
 __global__ void rope_kernel(__nv_bfloat16* qkv, int ld, int r0, int B, int n_q, int n_k, int hd, int k_col0,
                             const float2* __restrict__ table) {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // a PDL-launched GEMM may start its weight prefetch
+    pdl_launch_dependents();   // a PDL-launched GEMM may start its weight prefetch
+    pdl_wait();                // PDL-launched: the previous kernel's output is visible from here on
     const int row = r0 + blockIdx.x;
     const int t = row / B;
     const int half = hd / 2;
@@ -141,7 +147,8 @@ __global__ void __launch_bounds__(256, 2) attention_kernel(const __nv_bfloat16* 
                                                         __nv_bfloat16* __restrict__ out, int ldo, int t0, int t1,
                                                         int B, int group, int k_col0, int v_col0,
                                                         float score_scale) {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // a PDL-launched GEMM may start its weight prefetch
+    pdl_launch_dependents();   // a PDL-launched GEMM may start its weight prefetch
+    pdl_wait();                // PDL-launched: the previous kernel's output is visible from here on
     constexpr int KT = 32, QT = 32, DPL = HD / 32;   // dims per lane
     extern __shared__ float attn_smem[];
     float (*sQ)[HD] = reinterpret_cast<float (*)[HD]>(attn_smem);
@@ -238,6 +245,8 @@ __global__ void __launch_bounds__(256, 2) attention_kernel(const __nv_bfloat16* 
 __global__ void __launch_bounds__(256) logits_kernel(const __nv_bfloat16* __restrict__ y, int B, int d,
                                                      const __nv_bfloat16* __restrict__ E, int v0, int v1,
                                                      float* __restrict__ logits, int ldl) {
+    pdl_launch_dependents();
+    pdl_wait();
     extern __shared__ float sy[];
     for (int i = threadIdx.x; i < B * d; i += blockDim.x) sy[i] = __bfloat162float(y[i]);
     __syncthreads();
@@ -267,6 +276,8 @@ __global__ void __launch_bounds__(256) logits_kernel(const __nv_bfloat16* __rest
 // ------------------------------------------------------------------ argmax (lowest index wins ties)
 __global__ void __launch_bounds__(1024) argmax_kernel(const float* __restrict__ logits, int V, int ldl,
                                                       int32_t* tokens, int32_t* nan_flag) {
+    pdl_launch_dependents();
+    pdl_wait();
     __shared__ float sv[32];
     __shared__ int si[32];
     const float* x = logits + (size_t)blockIdx.x * ldl;
@@ -342,20 +353,18 @@ cudaError_t warm_simt_kernels() {
 }
 
 cudaError_t launch_norm(const float* h, int ldh, __nv_bfloat16* out, int ldo, int rows, int d,
-                        const __nv_bfloat16* gamma, const __nv_bfloat16* beta, float eps, cudaStream_t s) {
+                        const __nv_bfloat16* gamma, const __nv_bfloat16* beta, float eps, cudaStream_t s, bool pdl) {
     if (rows <= 0) return cudaSuccess;
-    if (d <= 256 * 8) norm_kernel<256, 8><<<rows, 256, 0, s>>>(h, ldh, out, ldo, d, gamma, beta, eps);
-    else if (d <= 256 * 40) norm_kernel<256, 40><<<rows, 256, 0, s>>>(h, ldh, out, ldo, d, gamma, beta, eps);
-    else return cudaErrorInvalidValue;
-    return cudaGetLastError();
+    if (d <= 256 * 8) return launch_pdl(norm_kernel<256, 8>, rows, 256, 0, s, pdl, h, ldh, out, ldo, d, gamma, beta, eps);
+    if (d <= 256 * 40) return launch_pdl(norm_kernel<256, 40>, rows, 256, 0, s, pdl, h, ldh, out, ldo, d, gamma, beta, eps);
+    return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_embed(const EmbedSrc& E, const __nv_bfloat16* pos, const int32_t* tok, float* h, int d, int r0,
-                         int r1, int B, cudaStream_t s) {
+                         int r1, int B, cudaStream_t s, bool pdl) {
     if (r1 <= r0) return cudaSuccess;
     if (d % 8) return cudaErrorInvalidValue;
-    embed_kernel<<<r1 - r0, 128, 0, s>>>(E, pos, tok, h, d, r0, B);
-    return cudaGetLastError();
+    return launch_pdl(embed_kernel, r1 - r0, 128, 0, s, pdl, E, pos, tok, h, d, r0, B);
 }
 
 cudaError_t launch_rope_table(float2* table, int T, int hd, double theta, cudaStream_t s) {
@@ -366,10 +375,9 @@ cudaError_t launch_rope_table(float2* table, int T, int hd, double theta, cudaSt
 }
 
 cudaError_t launch_rope(__nv_bfloat16* qkv, int ld, int r0, int r1, int B, int n_q, int n_k, int hd, int k_col0,
-                        const float2* table, cudaStream_t s) {
+                        const float2* table, cudaStream_t s, bool pdl) {
     if (r1 <= r0) return cudaSuccess;
-    rope_kernel<<<r1 - r0, 256, 0, s>>>(qkv, ld, r0, B, n_q, n_k, hd, k_col0, table);
-    return cudaGetLastError();
+    return launch_pdl(rope_kernel, r1 - r0, 256, 0, s, pdl, qkv, ld, r0, B, n_q, n_k, hd, k_col0, table);
 }
 
 cudaError_t launch_attention_simt(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int ldo, int t0, int t1,
@@ -381,7 +389,7 @@ cudaError_t launch_attention_simt(const __nv_bfloat16* qkv, int ld, __nv_bfloat1
     const int sm = (32 * hd + hd * 33 + 32 * hd) * (int)sizeof(float);
 #define PB_ATTN(HD)                                                                                        \
     case HD: {                                                                                             \
-        cudaError_t e = cudaFuncSetAttribute(attention_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm); \
+        cudaError_t e = smem_attr_once<attention_kernel<HD>>(sm);                                            \
         if (e != cudaSuccess) return e;                                                                    \
         attention_kernel<HD><<<grid, 256, sm, s>>>(qkv, ld, out, ldo, t0, t1, B, group, k_col0, v_col0, score_scale); \
         break;                                                                                             \
@@ -397,22 +405,20 @@ cudaError_t launch_attention_simt(const __nv_bfloat16* qkv, int ld, __nv_bfloat1
 }
 
 cudaError_t launch_logits(const __nv_bfloat16* y, int B, int d, const __nv_bfloat16* E, int v0, int v1, float* logits,
-                          int ldl, cudaStream_t s) {
+                          int ldl, cudaStream_t s, bool pdl) {
     if (v1 <= v0) return cudaSuccess;
     if (B > 8 || d % 8) return cudaErrorInvalidValue;
     const size_t sm = (size_t)B * d * sizeof(float);
-    if (sm > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(logits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (sm > 48 * 1024) {   // B <= 8 rows of d <= 10240 fp32: at most 320 KB is refused by the launch itself
+        cudaError_t e = smem_attr_once<logits_kernel>(227 * 1024);
         if (e != cudaSuccess) return e;
     }
-    logits_kernel<<<(v1 - v0 + 7) / 8, 256, sm, s>>>(y, B, d, E, v0, v1, logits, ldl);
-    return cudaGetLastError();
+    return launch_pdl(logits_kernel, (v1 - v0 + 7) / 8, 256, sm, s, pdl, y, B, d, E, v0, v1, logits, ldl);
 }
 
 cudaError_t launch_argmax(const float* logits, int B, int V, int ldl, int32_t* tokens, int32_t* nan_flag,
-                          cudaStream_t s) {
-    argmax_kernel<<<B, 1024, 0, s>>>(logits, V, ldl, tokens, nan_flag);
-    return cudaGetLastError();
+                          cudaStream_t s, bool pdl) {
+    return launch_pdl(argmax_kernel, B, 1024, 0, s, pdl, logits, V, ldl, tokens, nan_flag);
 }
 
 cudaError_t launch_signal(const SignalTargets& t, uint32_t value, cudaStream_t s) {

@@ -18,9 +18,23 @@ using namespace pb::sm100;
 
 constexpr int BM = 128, BN = 128, BK = 64;
 
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ unsigned long long g_stamps[1024][5];   // per CTA: start, first stage landed, mainloop done, end, smid
+
 template <int STAGES, bool LOADX, bool MMA, bool MCAST>
 __global__ void __launch_bounds__(128, 1) probe(const __grid_constant__ CUtensorMap mapX,
                                                 const __grid_constant__ CUtensorMap mapW, int K, float* out) {
+    const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    if (threadIdx.x == 0 && cta < 1024) {
+        g_stamps[cta][0] = gtimer();
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_stamps[cta][4] = smid;
+    }
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     constexpr int SA = BM * BK * 2, SB = BN * BK * 2;
@@ -66,6 +80,7 @@ __global__ void __launch_bounds__(128, 1) probe(const __grid_constant__ CUtensor
         for (int i = 0; i < my; ++i) {
             const int s = i % STAGES;
             mbar_wait(&full[s], (i / STAGES) & 1);
+            if (i == 0 && cta < 1024) g_stamps[cta][1] = gtimer();
             tc_fence_after();
             if (MMA) {
                 const uint32_t a = smem_u32(sA + (LOADX ? s : 0) * SA), b = smem_u32(sB + s * SB);
@@ -83,6 +98,7 @@ __global__ void __launch_bounds__(128, 1) probe(const __grid_constant__ CUtensor
     }
     __syncwarp();
     mbar_wait(done, 0);
+    if (threadIdx.x == 0 && cta < 1024) g_stamps[cta][2] = gtimer();
     tc_fence_after();
     float v[32];
     tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16), v);
@@ -97,6 +113,7 @@ __global__ void __launch_bounds__(128, 1) probe(const __grid_constant__ CUtensor
         tc_fence_after();
         tmem_dealloc<BN>(tmem);
     }
+    if (threadIdx.x == 0 && cta < 1024) g_stamps[cta][3] = gtimer();
 }
 
 // Pure streaming reference: every CTA reads its contiguous byte range with ld.global.v4 (no TMA, no smem).
@@ -150,6 +167,28 @@ static void run(const char* tag, int N, int K, int S, const std::vector<void*>& 
         cudaEventElapsedTime(&ms, a, b);
         tot += ms;
     }
+    {   // CTA timeline of one more launch: start spread, first-data latency, streaming time, epilogue, SM load
+        kern<<<grid, 128, smem>>>(mx, mw[0], K, out);
+        cudaDeviceSynchronize();
+        static unsigned long long st[1024][5];
+        cudaMemcpyFromSymbol(st, g_stamps, sizeof st);
+        const int n = grid.x * grid.y * grid.z;
+        unsigned long long t0 = ~0ull, tmax = 0;
+        double s_first = 0, s_main = 0, s_epi = 0, start_max = 0;
+        int per_sm[256] = {0}, sm_max = 0;
+        for (int i = 0; i < n && i < 1024; ++i) t0 = st[i][0] < t0 ? st[i][0] : t0;
+        for (int i = 0; i < n && i < 1024; ++i) {
+            start_max = fmax(start_max, (double)(st[i][0] - t0));
+            s_first += st[i][1] - st[i][0];
+            s_main += st[i][2] - st[i][1];
+            s_epi += st[i][3] - st[i][2];
+            tmax = st[i][3] > tmax ? st[i][3] : tmax;
+            if (++per_sm[st[i][4] & 255] > sm_max) sm_max = per_sm[st[i][4] & 255];
+        }
+        printf("    timeline: span %.2f us, CTA starts spread %.2f us, mean first-data %.2f us, mean stream %.2f us, "
+               "mean epilogue %.2f us, max CTAs/SM %d\n", (tmax - t0) / 1e3, start_max / 1e3, s_first / n / 1e3,
+               s_main / n / 1e3, s_epi / n / 1e3, sm_max);
+    }
     const double us = tot * 1e3 / reps, wb = (double)N * K * 2;
     printf("%-10s N%5d K%5d S%2d stages%d loadX%d mma%d: %7.2f us  W %6.0f GB/s  CTAs %d\n", tag, N, K, S, STAGES,
            (int)LOADX, (int)MMA, us, wb / us / 1e3, grid.x * grid.z);
@@ -196,11 +235,9 @@ int main() {
             }
         }
         const int nt = sh.N / BN, nk = sh.K / BK;
-        for (int S : {1, 2, 4, 8, 16}) {
+        for (int S : {1, 2, 3, 4, 6, 8}) {
             if (S > nk || nt * S > 600) continue;
             run<6, true, true>(sh.tag, sh.N, sh.K, S, Ws, X, out);
-            run<6, false, true>(sh.tag, sh.N, sh.K, S, Ws, X, out);
-            run<6, true, false>(sh.tag, sh.N, sh.K, S, Ws, X, out);
             run<6, false, false>(sh.tag, sh.N, sh.K, S, Ws, X, out);
             run<3, true, true>(sh.tag, sh.N, sh.K, S, Ws, X, out);
         }
