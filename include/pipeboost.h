@@ -258,6 +258,26 @@ PB_API pb_status pb_prefill_wait(pb_ctx* ctx, float* logits_out, int32_t* tokens
 PB_API pb_status pb_prefill_first_token(pb_ctx* ctx, const int32_t* tokens, int32_t batch, int32_t seq,
                                  float* logits_out, int32_t* tokens_out);
 
+/* f3 — pipelined decode. Compute the next token of every sequence
+ * of the batch this context last prefilled (pb_prefill_enqueue / pb_prefill_replay): the position after the
+ * prompt and the tokens decoded so far, fed with the previous step's argmax (already on the device, no host
+ * round trip), attending over the KV cache the prefill and earlier steps left in the workspace (one q|k|v
+ * slot per layer). Pipelined like the prefill: stage g runs its layers on the new position and hands the
+ * activation to stage g+1; every rank calls it (SPMD) with the same new epoch. Complete with pb_prefill_wait
+ * (tokens_out = the new tokens, on rank 0 or on a replica). Needs max_seq > prompt + decoded steps.
+ * Errors: PB_EPROTOCOL (nothing prefilled, or prefilled in the other mode), PB_EINVAL (epoch, max_seq),
+ * PB_EUNSUPPORTED (PB_MERGE_ALL microbatches). */
+PB_API pb_status pb_decode_step(pb_ctx* ctx, uint32_t epoch);
+
+/* f3 — seamless strategy switch: "Once all GPUs ... have fully loaded the complete model, PipeBoost
+ * can seamlessly switch to ... single-GPU independent inference ... batches of requests submitted after the
+ * switching point are executed using the new inference parallelism strategy." on = 1: this GPU serves its own
+ * batches with the WHOLE model it holds after T_full (every layer, local head, no cross-rank traffic):
+ * pb_prefill_replay (tokens on every replica) and pb_decode_step then run independently per rank. Requires a
+ * completed cold start whose merges and receive copies have finished (pb_sync). on = 0: back to the pipeline.
+ * Errors: PB_EPROTOCOL (no cold start / T_full not reached), PB_EUNSUPPORTED (PB_MERGE_ALL). */
+PB_API pb_status pb_ctx_set_replica(pb_ctx* ctx, int32_t on);
+
 /* f2 — epoch-based adapter switching (§4.3.2). Replace the adapter merged
  * into this rank's STAGE layers by `adapter_id` (or by none: -1): every adapted tensor of the stage is restored
  * from its pristine base copy (bufs.backup, saved by the cold start's merges) and the new adapter is merged

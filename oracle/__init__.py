@@ -45,3 +45,18 @@ def first_token_logits(model, adapters, tokens_bt, adapter_of_seq=None, mode="bf
         out.append(forward.forward_logits(model, W, np.asarray(tokens_bt[b]), mode))
     logits = np.stack(out)
     return logits, np.array([forward.first_token(x) for x in logits], dtype=np.int32)
+
+
+def teacher_forced_logits(model, adapters, prompt_bt, generated_bt, mode="bf16", adapter=0):
+    """f3 pins ("the first token is generated and returned ... to GPU 0"): decode step
+    i of sequence b must produce exactly the logits of the plain forward over prompt[b] + generated[b, :i] — the
+    definition a KV cache only accelerates. Returns [n + 1, B, V]: entry i uses the first i generated tokens
+    (entry 0 = the prompt alone, i.e. the first-token prefill)."""
+    B, n = generated_bt.shape
+    out = []
+    for i in range(n + 1):
+        seqs = np.concatenate([prompt_bt, generated_bt[:, :i]], axis=1) if i else prompt_bt
+        aos = [adapter if adapters else None] * B
+        lg, _ = first_token_logits(model, adapters, seqs, adapter_of_seq=aos, mode=mode)
+        out.append(lg)
+    return np.stack(out)

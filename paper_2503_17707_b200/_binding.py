@@ -111,6 +111,8 @@ _SIGS = {
     "pb_prefill_wait": [_P, _P, _P],
     "pb_prefill_replay": [_P, C.c_uint32, _P, C.c_int32, C.c_int32],
     "pb_switch_adapter": [_P, C.c_int32],
+    "pb_decode_step": [_P, C.c_uint32],
+    "pb_ctx_set_replica": [_P, C.c_int32],
     "pb_epoch_create": [C.c_int32, C.c_double, C.c_int32, C.POINTER(_P)],
     "pb_epoch_set_active": [_P, C.c_int32, C.c_double],
     "pb_epoch_enqueue": [_P, C.c_int32, C.c_int64],
@@ -325,6 +327,14 @@ class EpochScheduler:
                 self.h = None
         except Exception:
             pass
+
+
+def pb_decode_step(ctx, epoch):
+    check(lib().pb_decode_step(ctx, epoch))
+
+
+def pb_ctx_set_replica(ctx, on):
+    check(lib().pb_ctx_set_replica(ctx, int(on)))
 
 
 def pb_switch_adapter(ctx, adapter_id):

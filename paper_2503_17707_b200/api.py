@@ -204,14 +204,14 @@ class RankEngine:
         """Block until this rank's trial is done; rank 0 returns (tokens[B], logits[B, V] | None)."""
         with torch.cuda.device(self.device):
             logits, lp, tp = None, None, None
-            if self.rank == 0:
+            if self.rank == 0 or getattr(self, "replica", False):
                 tp = self._out_tokens.ctypes.data
                 if want_logits:
                     logits = np.empty((self._batch, self.plan.model.vocab), dtype=np.float32)
                     lp = logits.ctypes.data
             B.pb_prefill_wait(self.ctx, lp, tp)
             B.pb_sync(self.ctx)
-            if self.rank == 0:
+            if self.rank == 0 or getattr(self, "replica", False):
                 return self._out_tokens[:self._batch].copy(), logits
             return None, None
 
@@ -223,6 +223,18 @@ class RankEngine:
             batch, seq = np.asarray(tokens).shape
         self.enqueue(epoch, tokens, batch, seq, adapter_id)
         return self.wait(want_logits)
+
+    def decode_enqueue(self, epoch: int):
+        """f3: one decode step of the last prefilled batch (every rank, same epoch); complete with wait()."""
+        with torch.cuda.device(self.device):
+            B.pb_decode_step(self.ctx, epoch)
+
+    def set_replica(self, on: bool = True):
+        """f3: serve later batches with the whole model on this GPU (after T_full)."""
+        with torch.cuda.device(self.device):
+            B.pb_sync(self.ctx)
+            B.pb_ctx_set_replica(self.ctx, 1 if on else 0)
+        self.replica = on
 
     def switch_adapter(self, adapter_id: int):
         """f2: re-merge this rank's stage with `adapter_id` (-1: base model) behind the prefills

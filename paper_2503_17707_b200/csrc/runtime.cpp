@@ -119,7 +119,10 @@ WsLayout pb::ws_layout(const pb_plan* p, int32_t batch, int32_t seq) {
     L.h = o;       o = al(o + 4 * rows * d);
     const int64_t ea = p->es();   // activation element size: bf16 (product path) or fp32 (debug-parity path)
     L.x = o;       o = al(o + ea * rows * d);
-    L.n_qkv = k > 1 ? max_stage_layers(p) : 1;
+    // one q|k|v slot per layer: prompt chunks and decode steps read the K/V of earlier positions (the KV cache),
+    // and a replica (f3) runs every layer
+    L.n_qkv = m.n_layers;
+    (void)k;
     L.qkv_stride = al(ea * rows * qkv_dim(p));
     L.qkv = o;     o += L.qkv_stride * L.n_qkv;
     L.attn = o;    o = al(o + ea * rows * qd);
@@ -252,8 +255,8 @@ static pb_status build_prefill_maps(pb_ctx* c) {
     const int A = c->adapted ? (int)p->adapters.size() : 0;
     c->lmaps.assign(m.n_layers, LayerMaps{});
     c->lmaps_ad.assign(A, std::vector<LayerMaps>(m.n_layers, LayerMaps{}));
-    const auto st = p->stages[c->rank];
-    for (int l = st.first; l < st.second; ++l) {
+    // every layer, not only this rank's stage: a replica (f3, after T_full) runs the whole model
+    for (int l = 0; l < m.n_layers; ++l) {
         auto tid = [&](const char* s) { return p->find_tensor("L" + std::to_string(l) + "." + s); };
         const int32_t ids[4] = {tid("qkv"), tid("o"), tid(opt ? "fc1" : "gate_up"), tid(opt ? "fc2" : "down")};
         // adapter -1: base weights; a >= 0: adapter a's out-of-place copy where it has one, else the base
@@ -745,7 +748,7 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, boo
     const WsLayout& L = c->L;
     float* h = reinterpret_cast<float*>(c->ws + L.h);
     __nv_bfloat16* x = reinterpret_cast<__nv_bfloat16*>(c->ws + L.x);
-    const int li = L.n_qkv > 1 ? l - p->stages[c->rank].first : 0;
+    const int li = l;
     __nv_bfloat16* qkv = reinterpret_cast<__nv_bfloat16*>(c->ws + L.qkv + L.qkv_stride * li);
     __nv_bfloat16* attn = reinterpret_cast<__nv_bfloat16*>(c->ws + L.attn);
     __nv_bfloat16* mlp = reinterpret_cast<__nv_bfloat16*>(c->ws + L.mlp);
@@ -767,7 +770,7 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, boo
         a.out = out;
         a.ldo = ldo;
         a.up_row0 = f;
-        a.M_total = B * c->cur_seq;   // the whole prompt batch: split-K does not change with prompt chunking
+        a.M_total = c->gemm_m_total;  // whole prompt batch (or one decode step): chunking never changes split-K
         a.pdl = c->profiling ? 0 : 1; // per-launch timing events between kernels would cancel the overlap anyway
         return a;
     };
@@ -845,7 +848,7 @@ pb_status run_layer_f32(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B,
     const WsLayout& L = c->L;
     float* h = reinterpret_cast<float*>(c->ws + L.h);
     float* x = reinterpret_cast<float*>(c->ws + L.x);
-    const int li = L.n_qkv > 1 ? l - p->stages[c->rank].first : 0;
+    const int li = l;
     float* qkv = reinterpret_cast<float*>(c->ws + L.qkv + L.qkv_stride * li);
     float* attn = reinterpret_cast<float*>(c->ws + L.attn);
     float* mlp = reinterpret_cast<float*>(c->ws + L.mlp);
@@ -964,6 +967,8 @@ struct Issuer {
     int B, T, k;
     bool replay;
     bool mb_mode;   // PB_MERGE_ALL: every sequence is its own microbatch with its own adapter
+    bool replica = false;   // f3: this GPU runs the whole model alone (after T_full)
+    int dec_t = -1;         // f3: decode step producing the token after position dec_t - 1 (prompt: -1)
     int n_mb;
     std::vector<int> tb;
     std::vector<Item> items;
@@ -1121,7 +1126,9 @@ void build_items(Issuer& I) {
     const pb_plan* p = c->plan;
     const bool opt = p->model.arch == PB_ARCH_OPT;
     const int g = c->rank, N = c->n;
-    const auto stage = p->stages[g];
+    const bool rep = I.replica;
+    const auto stage = rep ? std::make_pair(0, p->model.n_layers) : p->stages[g];
+    const bool first = g == 0 || rep, last = g == N - 1 || rep;
     auto add = [&](int kind, int mb, int j, int l, std::vector<int32_t> pre) {
         if (I.replay) pre.clear();
         I.items.push_back(Item{kind, mb, j, l, std::move(pre)});
@@ -1134,7 +1141,7 @@ void build_items(Issuer& I) {
         return pre;
     };
     auto head_item = [&](int mb, int j) {   // embedding (stage 0) or the previous stage's activation
-        if (g == 0) {
+        if (first) {
             std::vector<int32_t> pre;
             if (mb == 0 && j == 0) {
                 const int32_t et = p->find_tensor("embed");
@@ -1150,7 +1157,7 @@ void build_items(Issuer& I) {
             add(I_WAITACT, mb, j, 0, {});
         }
     };
-    if (g == N - 1 && (I.n_mb > 1 || I.k > 1)) {
+    if (last && (I.n_mb > 1 || I.k > 1)) {
         // Last stage (no downstream consumer): layer-major, so every microbatch / prompt chunk advances as each
         // layer lands instead of all but the first waiting for the whole stage.
         for (int l = stage.first; l < stage.second; ++l)
@@ -1166,16 +1173,17 @@ void build_items(Issuer& I) {
                 head_item(mb, j);
                 for (int l = stage.first; l < stage.second; ++l)
                     add(I_LAYER, mb, j, l, mb == 0 && j == 0 ? layer_pre(l) : std::vector<int32_t>{});
-                if (g < N - 1) add(I_PUSH, mb, j, 0, {});
+                if (!last) add(I_PUSH, mb, j, 0, {});
             }
     }
-    if (g == N - 1) {
+    if (last) {
         std::vector<int32_t> pre{p->find_tensor("final_g")};
         if (opt) pre.push_back(p->find_tensor("final_b"));
         add(I_FINAL, 0, 0, 0, pre);
     }
-    if (is_head_owner(p, g)) add(I_HEAD, 0, 0, 0, {p->opts.vocab_sliced ? -head_tensor(p) - 1 : head_tensor(p)});
-    if (g == 0) add(I_ARGMAX, 0, 0, 0, {});
+    if (rep || is_head_owner(p, g))
+        add(I_HEAD, 0, 0, 0, {p->opts.vocab_sliced ? -head_tensor(p) - 1 : head_tensor(p)});
+    if (first) add(I_ARGMAX, 0, 0, 0, {});
     add(I_DONE, 0, 0, 0, {});
 }
 
@@ -1200,6 +1208,7 @@ pb_status issue_item(Issuer& I, const Item& it) {
     const auto& m = p->model;
     const bool opt = m.arch == PB_ARCH_OPT;
     const int g = c->rank, N = c->n, d = m.d_model, hd = p->head_dim(), B = I.B, T = I.T, V = m.vocab;
+    const bool rep = I.replica;
     const WsLayout& L = c->L;
     cudaStream_t s = c->comp;
     float* h = reinterpret_cast<float*>(c->ws + L.h);
@@ -1212,19 +1221,24 @@ pb_status issue_item(Issuer& I, const Item& it) {
     const int row_base = I.mb_mode ? it.mb * T : 0;
     const int r0 = row_base + I.tb[j] * Bk, r1 = row_base + I.tb[j + 1] * Bk;
     const int act_word = L.f_act + it.mb * I.k + j;
-    std::vector<int32_t> owners;
-    for (int r = 0; r < N; ++r)
-        if (is_head_owner(p, r)) owners.push_back(r);
+    std::vector<int32_t> owners;   // ranks computing a slice of the logits (a replica: itself, the whole vocabulary)
+    if (rep) owners.push_back(g);
+    else
+        for (int r = 0; r < N; ++r)
+            if (is_head_owner(p, r)) owners.push_back(r);
     switch (it.kind) {
         case I_PROLOGUE:
-            if (!opt) {
-                CU(launch_rope_table(reinterpret_cast<float2*>(c->ws + L.rope), T, hd, m.rope_theta, s));
+            if (!opt) {   // positions up to the workspace's max_seq: decode steps reuse the table
+                CU(launch_rope_table(reinterpret_cast<float2*>(c->ws + L.rope), L.max_seq, hd, m.rope_theta, s));
                 ++c->n_launches;
             }
-            if (g == 0) {
+            if (g == 0 || rep) {
                 // the token upload went out on the copy lane ahead of the weights (issue_trial): an H2D copy on
                 // this stream would queue behind the whole load in the copy engine (measured: drains per stream)
-                if (I.replay)
+                if (I.dec_t >= 0)   // decode: the previous step's tokens become position dec_t's inputs
+                    CU(cudaMemcpyAsync(c->ws + L.tokens + sizeof(int32_t) * (size_t)I.dec_t * B, c->ws + L.tok_out,
+                                       sizeof(int32_t) * B, cudaMemcpyDeviceToDevice, s));
+                else if (I.replay)
                     CU(cudaMemcpyAsync(c->ws + L.tokens, c->h_tokens, sizeof(int32_t) * B * T, cudaMemcpyHostToDevice, s));
                 else
                     CU(cudaStreamWaitEvent(s, c->tok_ev, 0));
@@ -1245,7 +1259,7 @@ pb_status issue_item(Issuer& I, const Item& it) {
                 if (opt) CU(wait_tensor_ready(c, p->find_tensor("pos"), s));
             }
             EmbedSrc E{};
-            if (p->opts.vocab_sliced) {
+            if (p->opts.vocab_sliced && !rep) {
                 std::vector<int32_t> sl(N + 1, 0);
                 for (auto& ch : p->chunks)
                     if (!ch.is_adapter && ch.tensor == et) sl[ch.loader + 1] = std::max(sl[ch.loader + 1], ch.r1);
@@ -1317,14 +1331,14 @@ pb_status issue_item(Issuer& I, const Item& it) {
             break;
         }
         case I_HEAD: {
-            if (g != N - 1) CU(wait_word(c, L.f_y, s));
+            if (!rep && g != N - 1) CU(wait_word(c, L.f_y, s));
             const int32_t ht = head_tensor(p);
             if (!I.replay) {   // vocab slices: this rank's own rows; whole head: every part of it
                 if (p->opts.vocab_sliced) CU(wait_word(c, L.f_tensor + ht, s));
                 else CU(wait_tensor_ready(c, ht, s));
             }
-            int32_t v0, v1;
-            head_slice(p, g, &v0, &v1);
+            int32_t v0 = 0, v1 = V;
+            if (!rep) head_slice(p, g, &v0, &v1);
             const __nv_bfloat16* E = reinterpret_cast<const __nv_bfloat16*>(c->weights + p->tensors[ht].dev_off);
             const int pi = prof_begin(c, K_LOGITS, s);
             if (p->f32())
@@ -1334,7 +1348,7 @@ pb_status issue_item(Issuer& I, const Item& it) {
                 CU(launch_logits(y, B, d, E, v0, v1, logits, V, s, !c->profiling));
             prof_end(c, pi, s, 2.0 * B * (v1 - v0) * d, 2.0 * (double)(v1 - v0) * d + 4.0 * B * (v1 - v0));
             ++c->n_launches;
-            if (g != 0) {
+            if (g != 0 && !rep) {
                 CU(cudaMemcpy2DAsync(c->peers[0].ws + L.logits + (size_t)v0 * 4, (size_t)V * 4, logits + v0,
                                      (size_t)V * 4, (size_t)(v1 - v0) * 4, B, cudaMemcpyDeviceToDevice, s));
                 CU(signal_ranks(c, L.f_logit + g, {0}, s));
@@ -1343,7 +1357,7 @@ pb_status issue_item(Issuer& I, const Item& it) {
         }
         case I_ARGMAX: {
             for (int32_t r : owners)
-                if (r != 0) CU(wait_word(c, L.f_logit + r, s));
+                if (r != g) CU(wait_word(c, L.f_logit + r, s));
             const int pi = prof_begin(c, K_ARGMAX, s);
             CU(launch_argmax(logits, B, V, V, reinterpret_cast<int32_t*>(c->ws + L.tok_out),
                              reinterpret_cast<int32_t*>(c->ws + L.nan), s, !c->profiling));
@@ -1369,11 +1383,20 @@ pb_status issue_trial(pb_ctx* c, int B, int T, bool replay) {
     I.replay = replay;
     I.mb_mode = c->merge_adapter == PB_MERGE_ALL;
     I.n_mb = I.mb_mode ? B : 1;
-    I.k = std::max(1, std::min(p->opts.prefill_chunks, T));
-    I.tb.assign(I.k + 1, 0);
-    for (int j = 0, t = 0; j <= I.k; ++j) {   // prompt chunk boundaries, remainder to lower chunks
-        I.tb[j] = t;
-        if (j < I.k) t += T / I.k + (j < T % I.k ? 1 : 0);
+    I.replica = c->replica;
+    I.dec_t = c->decode_t;
+    if (I.dec_t >= 0) {   // f3 decode step: one "prompt chunk" holding position dec_t of every sequence
+        I.k = 1;
+        I.tb = {I.dec_t, I.dec_t + 1};
+        c->gemm_m_total = B;
+    } else {
+        I.k = std::max(1, std::min(p->opts.prefill_chunks, T));
+        I.tb.assign(I.k + 1, 0);
+        for (int j = 0, t = 0; j <= I.k; ++j) {   // prompt chunk boundaries, remainder to lower chunks
+            I.tb[j] = t;
+            if (j < I.k) t += T / I.k + (j < T % I.k ? 1 : 0);
+        }
+        c->gemm_m_total = B * T;
     }
     I.own_issued.assign(p->tensors.size(), replay ? 1 : 0);
     I.recv_issued.assign(p->tensors.size(), replay ? 1 : 0);
@@ -1456,7 +1479,7 @@ pb_status start_issuer(pb_ctx* c, const int32_t* tokens, const int32_t* adapter_
                        bool replay) {
     if (B < 1 || T < 1 || B > c->L.max_batch || T > c->L.max_seq || (int64_t)B * T > c->L.max_rows)
         return fail(PB_EINVAL, "batch %d x seq %d exceeds the workspace (%d x %d)", B, T, c->L.max_batch, c->L.max_seq);
-    if (c->rank == 0 && !tokens) return fail(PB_EINVAL, "rank 0 needs tokens");
+    if ((c->rank == 0 || c->replica) && !tokens) return fail(PB_EINVAL, "rank 0 (every rank of a replica) needs tokens");
     const bool mb = c->merge_adapter == PB_MERGE_ALL;
     if (!replay) {
         c->seq_adapter.assign(B, -1);
@@ -1474,11 +1497,13 @@ pb_status start_issuer(pb_ctx* c, const int32_t* tokens, const int32_t* adapter_
                                            "PB_MERGE_ALL for mixed batches)", b, adapter_of_seq[b], c->merge_adapter);
         }
     }
-    if (c->rank == 0)
+    if (c->rank == 0 || c->replica)
         for (int b = 0; b < B; ++b)   // token-major rows t*B + b; microbatch mode: sequence-major b*T + t
             for (int t = 0; t < T; ++t) c->h_tokens[mb ? b * T + t : t * B + b] = tokens[(size_t)b * T + t];
     c->cur_batch = B;
     c->cur_seq = T;
+    c->n_decoded = 0;
+    c->prompt_replica = c->replica;
     join_load(c);
     c->issue_status = PB_OK;
     c->issue_msg[0] = '\0';
@@ -1521,20 +1546,22 @@ extern "C" pb_status pb_prefill_replay(pb_ctx* c, uint32_t epoch, const int32_t*
     c->epoch = epoch;
     c->n_launches = 0;
     c->prof_n = 0;
-    if (c->n == 1 && c->merge_adapter != PB_MERGE_ALL) {
+    if ((c->n == 1 || c->replica) && c->merge_adapter != PB_MERGE_ALL) {
         // Single rank: the replay has no cross-rank waits, so it is captured once as a CUDA graph and relaunched
         // (the token upload / result download are graph nodes on the pinned staging buffers).
         if (B < 1 || T < 1 || B > c->L.max_batch || T > c->L.max_seq || (int64_t)B * T > c->L.max_rows)
             return fail(PB_EINVAL, "batch %d x seq %d exceeds the workspace", B, T);
-        if (!tokens) return fail(PB_EINVAL, "rank 0 needs tokens");
+        if (!tokens) return fail(PB_EINVAL, "rank 0 (every rank of a replica) needs tokens");
         for (int b = 0; b < B; ++b)
             for (int t = 0; t < T; ++t) c->h_tokens[t * B + b] = tokens[(size_t)b * T + t];
         c->cur_batch = B;
         c->cur_seq = T;
-        const int pi = c->profiling ? 1 : 0;
+        c->n_decoded = 0;
+        c->prompt_replica = c->replica;
+        const int pi = c->profiling ? 1 : 0, rp = c->replica ? 1 : 0;
         pb_ctx::ReplayGraph* rg = nullptr;
         for (auto& g : c->replay_graphs)
-            if (g.B == B && g.T == T && g.profiled == pi) rg = &g;
+            if (g.B == B && g.T == T && g.profiled == pi && g.replica == rp) rg = &g;
         if (!rg) {
             CU(cudaStreamBeginCapture(c->comp, cudaStreamCaptureModeThreadLocal));
             c->capturing = true;
@@ -1551,7 +1578,7 @@ extern "C" pb_status pb_prefill_replay(pb_ctx* c, uint32_t epoch, const int32_t*
             cudaError_t ie = cudaGraphInstantiate(&ge, g, 0);
             cudaGraphDestroy(g);
             CU(ie);
-            c->replay_graphs.push_back({B, T, pi, ge, c->n_launches, c->prof_n,
+            c->replay_graphs.push_back({B, T, pi, rp, ge, c->n_launches, c->prof_n,
                                         std::vector<ProfRec>(c->prof.begin(), c->prof.begin() + c->prof_n)});
             rg = &c->replay_graphs.back();
         }
@@ -1566,6 +1593,61 @@ extern "C" pb_status pb_prefill_replay(pb_ctx* c, uint32_t epoch, const int32_t*
     }
     CU(cudaEventRecord(c->t0, c->comp));
     return start_issuer(c, tokens, nullptr, B, T, true);
+}
+
+// ------------------------------------------------------------------------------------------------
+// f3 — pipelined decode and the switch to single-GPU replicas
+// ------------------------------------------------------------------------------------------------
+extern "C" pb_status pb_decode_step(pb_ctx* c, uint32_t epoch) {
+    pb_status st = check_ctx(c, "pb_decode_step");
+    if (st) return st;
+    if (c->phase != Phase::Prefilled) return fail(PB_EPROTOCOL, "pb_decode_step: needs a prefilled batch");
+    if (c->merge_adapter == PB_MERGE_ALL)
+        return fail(PB_EUNSUPPORTED, "pb_decode_step: PB_MERGE_ALL microbatches (decode one adapter per batch)");
+    if (epoch <= c->epoch) return fail(PB_EINVAL, "epoch %u must exceed the previous %u", epoch, c->epoch);
+    if (c->prompt_replica != c->replica)
+        return fail(PB_EPROTOCOL, "pb_decode_step: the batch was prefilled in the other mode (pipeline / replica); "
+                                  "prefill it again in this mode first (P:L295: batches after the switch)");
+    const int32_t t = c->cur_seq + c->n_decoded;
+    if (t >= c->L.max_seq) return fail(PB_EINVAL, "decode position %d reaches the workspace's max_seq %d", t, c->L.max_seq);
+    join_load(c);
+    if (c->issue_status != PB_OK) return fail(c->issue_status, "%s", c->issue_msg);
+    CU(cudaStreamSynchronize(c->comp));
+    c->epoch = epoch;
+    c->n_launches = 0;
+    c->prof_n = 0;
+    c->n_decoded++;
+    CU(cudaEventRecord(c->t0, c->comp));
+    const int B = c->cur_batch;
+    c->issue_status = PB_OK;
+    c->issue_msg[0] = '\0';
+    c->load_thread = std::thread([c, B, t]() {
+        cudaSetDevice(c->device);
+        c->decode_t = t;
+        pb_status ist = issue_trial(c, B, t + 1, true);
+        c->decode_t = -1;
+        if (ist != PB_OK) {
+            c->issue_status = ist;
+            snprintf(c->issue_msg, sizeof c->issue_msg, "%s", pb_last_error());
+        }
+    });
+    return PB_OK;
+}
+
+extern "C" pb_status pb_ctx_set_replica(pb_ctx* c, int32_t on) {
+    pb_status st = check_ctx(c, "pb_ctx_set_replica");
+    if (st) return st;
+    if (on) {
+        if (c->phase != Phase::Prefilled) return fail(PB_EPROTOCOL, "pb_ctx_set_replica: needs a completed cold start");
+        join_load(c);
+        // T_full: every merge and every receive copy of the cold start has completed on this GPU
+        if (cudaStreamQuery(c->merge) != cudaSuccess || cudaStreamQuery(c->nv) != cudaSuccess ||
+            cudaEventQuery(c->gather_done) != cudaSuccess || cudaEventQuery(c->merge_done) != cudaSuccess)
+            return fail(PB_EPROTOCOL, "pb_ctx_set_replica: T_full not reached (pb_sync first)");
+        if (c->merge_adapter == PB_MERGE_ALL) return fail(PB_EUNSUPPORTED, "replica of a PB_MERGE_ALL context");
+    }
+    c->replica = on != 0;
+    return PB_OK;
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -1688,7 +1770,7 @@ extern "C" pb_status pb_prefill_wait(pb_ctx* c, float* logits_out, int32_t* toke
     }
     CU(cudaEventSynchronize(c->done));
     CU(cudaGetLastError());
-    if (c->rank == 0) {
+    if (c->rank == 0 || c->replica) {
         const int B = c->cur_batch;
         if (tokens_out) memcpy(tokens_out, c->h_out, sizeof(int32_t) * B);
         if (logits_out)

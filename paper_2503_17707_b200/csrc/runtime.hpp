@@ -136,8 +136,14 @@ struct pb_ctx {
     // Warm replay as a CUDA graph (single-rank contexts): captured once per (batch, seq, profiling) and
     // relaunched, so the prefill's ~200 launches cost one host call instead of ~4 us of issue time each.
     bool capturing = false;
+    // f3: replica mode (the whole model on this GPU, after T_full) and decode-step state
+    bool replica = false;
+    int32_t decode_t = -1;       // position of the token the current decode trial computes (-1: a prompt trial)
+    int32_t n_decoded = 0;       // decode steps since the last prompt trial
+    bool prompt_replica = false; // the last prompt trial ran in replica mode (its KV cache covers every layer)
+    int32_t gemm_m_total = 0;    // rows that pick the GEMM split-K (whole prompt batch, or one decode step)
     struct ReplayGraph {
-        int32_t B, T, profiled;
+        int32_t B, T, profiled, replica;
         cudaGraphExec_t exec;
         int32_t launches;
         size_t prof_n;

@@ -71,8 +71,8 @@ def main():
         toks = prompts[batch_ids]
         eng.replay_enqueue(epoch[0], toks, len(batch_ids), T)
         epoch[0] += 1
-        tok, _ = eng.wait()
-        return tok
+        tok, logits = eng.wait(want_logits=True)
+        return tok, logits
 
     def run(schedule):
         active = [adapters[0]]
@@ -88,10 +88,10 @@ def main():
                     j += 1
                 ids = list(range(i, j))
                 switches += int(adapters[i] != active[0])
-                out = serve(ids, adapters[i], active)
+                out, lg = serve(ids, adapters[i], active)
                 t = now_ms()
                 for k, r in enumerate(ids):
-                    done[r], toks_out[r] = t, int(out[k])
+                    done[r], toks_out[r] = t, (int(out[k]), lg[k].copy())
                 i = j
         else:
             s = B.EpochScheduler(2, a.epoch_ms)
@@ -103,23 +103,34 @@ def main():
                 if ad is None:
                     break
                 switches += int(sw)
-                out = serve(ids, ad, active)
+                out, lg = serve(ids, ad, active)
                 t = now_ms()
                 for k, r in enumerate(ids):
-                    done[r], toks_out[r] = t, int(out[k])
+                    done[r], toks_out[r] = t, (int(out[k]), lg[k].copy())
         return switches, max(done.values()), statistics.mean(done.values()), toks_out
 
     run("eager")   # warm-up (graph capture per batch size)
     run("epoch")
     se, me, ce, te = run("eager")
     sp, mp, cp, tp = run("epoch")
-    assert te == tp, "first tokens differ between schedules"
+    # Same request, same adapter: the logits differ only by the GEMM's split-K summation order, which depends on
+    # the batch size a schedule happened to give the request; tokens must agree unless the top-2 margin is
+    # within that difference.
+    worst, same = 0.0, 0
+    for r in range(a.requests):
+        (ta, la), (tb, lb) = te[r], tp[r]
+        err = float(np.abs(la - lb).max())
+        worst = max(worst, err / float(np.abs(la).max()))
+        srt = np.sort(la)
+        assert ta == tb or srt[-1] - srt[-2] <= 2 * err, r
+        same += ta == tb
+    assert worst <= 1e-2, worst
     line = {"metric": "f2 epoch-based adapter switching vs eager (burst)", "workload": a.workload,
             "requests": a.requests, "max_batch": a.max_batch, "p_switch": a.p_switch, "epoch_ms": a.epoch_ms,
             "eager": {"switches": se, "makespan_ms": me, "mean_completion_ms": ce},
             "epoch": {"switches": sp, "makespan_ms": mp, "mean_completion_ms": cp},
             "mean_completion_reduction": 1 - cp / ce,
-            "first_tokens": "identical under both schedules",
+            "first_tokens_identical": f"{same}/{a.requests}", "logits_max_rel_diff": worst,
             "paper": "P:L561-565, Fig. 9: 63.1% lower latency at 25 RPS (their hardware, their trace)"}
     print(json.dumps(line), flush=True)
     eng.close()
