@@ -319,7 +319,227 @@ cudaError_t launch_epi(const CUtensorMap& mapX, const CUtensorMap& mapW, const G
     return cudaErrorInvalidValue;
 }
 
+// ------------------------------------------------------------------------------------------------------------
+// Large-M path (the prompt batch spans several 128-row tiles; S = 1): persistent, warp-specialised, 128 x 256
+// tiles (one tcgen05.mma M128 N256 K16 per 16-wide K step), a 4-stage TMA ring of 48 KB stages, and two
+// 256-column TMEM accumulators so the epilogue of tile i overlaps the mainloop of tile i+1.
+//   warp 0 lane 0 : TMA producer (X box 128 x 64; W as two 128-row boxes, SiLU: four 64-row boxes)
+//   warp 1 lane 0 : MMA issuer
+//   warps 2-5     : epilogue, one output row per thread (TMEM lane quadrant = warp % 4)
+// Tiles are visited n-major (all M tiles of one N tile back to back) so each weight tile is read from HBM once
+// and re-read from L2 by the other M tiles while the activations (M x K) stay L2-resident.
+// ------------------------------------------------------------------------------------------------------------
+constexpr int BIG_BN = 256, BIG_STAGES = 4;
+constexpr int kBigA = BM * BK * 2, kBigB = BIG_BN * BK * 2, kBigStage = kBigA + kBigB;   // 16 + 32 KB
+constexpr int kBigSmem = BIG_STAGES * kBigStage + 256 + 1024;
+
+template <int EPI>
+__global__ void __launch_bounds__(192, 1) gemm_big_kernel(const __grid_constant__ CUtensorMap mapX,
+                                                          const __grid_constant__ CUtensorMap mapW, const GemmArgs a) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + BIG_STAGES * kBigStage);
+    uint64_t* empty = full + BIG_STAGES;
+    uint64_t* acc_full = empty + BIG_STAGES;    // [2] MMA -> epilogue
+    uint64_t* acc_empty = acc_full + 2;         // [2] epilogue -> MMA (128 arrivals)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr int per = EPI == EPI_SILU_MUL ? BIG_BN / 2 : BIG_BN;   // outputs per tile along N
+    const int n_tiles = (a.N + per - 1) / per;
+    const int m_tiles = (a.M_end - a.M_begin + BM - 1) / BM;
+    const int tiles = n_tiles * m_tiles;
+    const int nk = (a.K + BK - 1) / BK;
+
+    pdl_launch_dependents();
+    if (tid == 0) {
+        tma_prefetch_desc(&mapX);
+        tma_prefetch_desc(&mapW);
+        for (int s = 0; s < BIG_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], 128);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 0) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    pdl_wait();
+
+    if (warp == 0) {
+        if (lane == 0) {   // ---------------- TMA producer
+            int it = 0;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+                const int m0 = a.M_begin + (t % m_tiles) * BM, n0 = (t / m_tiles) * per;
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int s = it % BIG_STAGES, kc = kb * BK;
+                    if (it >= BIG_STAGES) mbar_wait(&empty[s], ((it / BIG_STAGES) - 1) & 1);
+                    uint8_t* sA = smem + s * kBigStage;
+                    uint8_t* sB = sA + kBigA;
+                    mbar_arrive_expect_tx(&full[s], kBigStage);
+                    tma_load_2d(sA, &mapX, &full[s], kc, m0);
+                    if (EPI == EPI_SILU_MUL) {   // [gate 128 | up 128] rows as four 64-row boxes
+                        tma_load_2d(sB, &mapW, &full[s], kc, n0);
+                        tma_load_2d(sB + kBigB / 4, &mapW, &full[s], kc, n0 + 64);
+                        tma_load_2d(sB + kBigB / 2, &mapW, &full[s], kc, a.up_row0 + n0);
+                        tma_load_2d(sB + 3 * kBigB / 4, &mapW, &full[s], kc, a.up_row0 + n0 + 64);
+                    } else {
+                        tma_load_2d(sB, &mapW, &full[s], kc, n0);
+                        tma_load_2d(sB + kBigB / 2, &mapW, &full[s], kc, n0 + 128);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {   // ---------------- MMA issuer
+            constexpr uint32_t idesc = idesc_bf16_f32(BM, BIG_BN, 0, 0);
+            int it = 0, local = 0;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+                const int b = local & 1;
+                const uint32_t acc = tmem + b * BIG_BN;
+                if (local >= 2) mbar_wait(&acc_empty[b], ((local >> 1) - 1) & 1);
+                tc_fence_after();
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int s = it % BIG_STAGES;
+                    mbar_wait(&full[s], (it / BIG_STAGES) & 1);
+                    tc_fence_after();
+                    const uint32_t a_base = smem_u32(smem + s * kBigStage), b_base = a_base + kBigA;
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k)
+                        umma_bf16(acc, smem_desc(a_base + k * 32, 16, 1024, kSw128),
+                                  smem_desc(b_base + k * 32, 16, 1024, kSw128), idesc, (kb | k) != 0 ? 1u : 0u);
+                    umma_commit(&empty[s]);
+                }
+                umma_commit(&acc_full[b]);
+            }
+        }
+    } else {   // ---------------- epilogue warps 2..5: row = TMEM lane
+        const int quad = warp & 3, row_in_tile = quad * 32 + lane;
+        const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+        int local = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+            const int b = local & 1;
+            const int m0 = a.M_begin + (t % m_tiles) * BM, n0 = (t / m_tiles) * per;
+            mbar_wait(&acc_full[b], (local >> 1) & 1);
+            tc_fence_after();
+            const int row = m0 + row_in_tile;
+            const bool row_ok = row < a.M_end;
+            const uint32_t acc = tmem + b * BIG_BN + lane_off;
+            if (EPI == EPI_SILU_MUL) {
+#pragma unroll 1
+                for (int cb = 0; cb < 4; ++cb) {   // 32 gate columns + the matching 32 up columns
+                    uint32_t g[32], u[32];
+                    tmem_ld32_async(acc + cb * 32, g);
+                    tmem_ld32_async(acc + 128 + cb * 32, u);
+                    tmem_wait_ld();
+                    const int n = n0 + cb * 32;
+                    if (!row_ok || n >= a.N) continue;
+                    __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(a.out) + (size_t)row * a.ldo + n;
+                    if (n + 32 <= a.N) {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            float o[8];
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) {
+                                const float gv = __uint_as_float(g[8 * q + e]);
+                                o[e] = silu(gv) * __uint_as_float(u[8 * q + e]);
+                            }
+                            *reinterpret_cast<uint4*>(out + 8 * q) =
+                                make_uint4(bf16x2_bits(o[0], o[1]), bf16x2_bits(o[2], o[3]), bf16x2_bits(o[4], o[5]),
+                                           bf16x2_bits(o[6], o[7]));
+                        }
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 32; ++e)
+                            if (n + e < a.N)
+                                out[e] = __float2bfloat16_rn(silu(__uint_as_float(g[e])) * __uint_as_float(u[e]));
+                    }
+                }
+            } else {
+#pragma unroll 1
+                for (int cb = 0; cb < BIG_BN / 32; ++cb) {
+                    uint32_t r[32];
+                    tmem_ld32_async(acc + cb * 32, r);
+                    tmem_wait_ld();
+                    const int n = n0 + cb * 32;
+                    if (!row_ok || n >= a.N) continue;
+                    float v[32];
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        v[e] = __uint_as_float(r[e]);
+                        if (a.bias && n + e < a.N) v[e] += __bfloat162float(a.bias[n + e]);
+                    }
+                    const int nv = min(32, a.N - n);
+                    if (EPI == EPI_BF16) {
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) {
+                            if (n + e < a.scale_cols) v[e] *= a.scale;
+                            if (a.relu) v[e] = fmaxf(v[e], 0.f);
+                        }
+                        __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(a.out) + (size_t)row * a.ldo + n;
+                        if (nv == 32) {
+#pragma unroll
+                            for (int q = 0; q < 4; ++q)
+                                *reinterpret_cast<uint4*>(out + 8 * q) =
+                                    make_uint4(bf16x2_bits(v[8 * q], v[8 * q + 1]), bf16x2_bits(v[8 * q + 2], v[8 * q + 3]),
+                                               bf16x2_bits(v[8 * q + 4], v[8 * q + 5]),
+                                               bf16x2_bits(v[8 * q + 6], v[8 * q + 7]));
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < 32; ++e)
+                                if (e < nv) out[e] = __float2bfloat16_rn(v[e]);
+                        }
+                    } else {   // EPI_RESID: h += acc + bias
+                        float* h = reinterpret_cast<float*>(a.out) + (size_t)row * a.ldo + n;
+                        if (nv == 32) {
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                float4 x = *reinterpret_cast<float4*>(h + 4 * q);
+                                x.x += v[4 * q];
+                                x.y += v[4 * q + 1];
+                                x.z += v[4 * q + 2];
+                                x.w += v[4 * q + 3];
+                                *reinterpret_cast<float4*>(h + 4 * q) = x;
+                            }
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < 32; ++e)
+                                if (e < nv) h[e] += v[e];
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&acc_empty[b]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        __syncwarp();
+        tc_fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+}
+
+template <int EPI>
+cudaError_t launch_big(const CUtensorMap& mapX, const CUtensorMap& mapW, const GemmArgs& a, cudaStream_t s) {
+    cudaError_t e = smem_attr_once<gemm_big_kernel<EPI>>(kBigSmem);
+    if (e != cudaSuccess) return e;
+    const int per = EPI == EPI_SILU_MUL ? BIG_BN / 2 : BIG_BN;
+    const int tiles = ((a.N + per - 1) / per) * ((a.M_end - a.M_begin + BM - 1) / BM);
+    const int grid = tiles < 148 ? tiles : 148;
+    return launch_pdl(gemm_big_kernel<EPI>, dim3(grid), dim3(192), kBigSmem, s, a.pdl != 0, mapX, mapW, a);
+}
+
 }  // namespace
+
 
 // Split-K factor S (1, 2 or 4): the largest S <= 4 that keeps n_tiles x m_tiles x S <= 296 CTAs (two per SM
 // on 148 SMs) with at least 4 K blocks of 64 per split. It depends on (N, K, M_total) only, where M_total is
@@ -344,7 +564,9 @@ cudaError_t warm_gemm_kernels() {
                          (const void*)gemm_kernel<EPI_RESID, 1>,    (const void*)gemm_kernel<EPI_RESID, 2>,
                          (const void*)gemm_kernel<EPI_RESID, 4>,    (const void*)gemm_kernel<EPI_RESID, 8>,
                          (const void*)gemm_kernel<EPI_SILU_MUL, 1>, (const void*)gemm_kernel<EPI_SILU_MUL, 2>,
-                         (const void*)gemm_kernel<EPI_SILU_MUL, 4>, (const void*)gemm_kernel<EPI_SILU_MUL, 8>};
+                         (const void*)gemm_kernel<EPI_SILU_MUL, 4>, (const void*)gemm_kernel<EPI_SILU_MUL, 8>,
+                         (const void*)gemm_big_kernel<EPI_BF16>,     (const void*)gemm_big_kernel<EPI_RESID>,
+                         (const void*)gemm_big_kernel<EPI_SILU_MUL>};
     for (const void* f : fns) {
         cudaError_t e = cudaFuncGetAttributes(&at, f);
         if (e != cudaSuccess) return e;
@@ -356,6 +578,15 @@ cudaError_t launch_gemm(const CUtensorMap& mapX, const CUtensorMap& mapW, const 
     if (a.M_end <= a.M_begin || a.N <= 0) return cudaSuccess;
     if (a.K <= 0 || a.K % 8) return cudaErrorInvalidValue;
     const int S = a.split_k > 0 ? a.split_k : gemm_split_k(a.N, a.K, a.epi, a.M_total);
+    // The kernel is chosen from the WHOLE prompt (M_total), never from the rows of this launch, so a prompt split
+    // into chunks runs every output through the same kernel and the same summation order.
+    if (S == 1 && a.split_k <= 0 && a.M_total > BM) {
+        switch (a.epi) {
+            case EPI_BF16: return launch_big<EPI_BF16>(mapX, mapW, a, s);
+            case EPI_RESID: return launch_big<EPI_RESID>(mapX, mapW, a, s);
+            case EPI_SILU_MUL: return launch_big<EPI_SILU_MUL>(mapX, mapW, a, s);
+        }
+    }
     switch (a.epi) {
         case EPI_BF16: return launch_epi<EPI_BF16>(mapX, mapW, a, S, s);
         case EPI_RESID: return launch_epi<EPI_RESID>(mapX, mapW, a, S, s);

@@ -120,6 +120,21 @@ def test_pipelined_equals_sequential_bitwise(model):
         assert np.array_equal(tn, t1)
 
 
+def test_long_prompt_chunking_bitwise():
+    """A prompt batch spanning several 128-row tiles (M_total = 300: the persistent 128x256 GEMM) gives
+    bit-identical logits whether it runs in one chunk or three, on one or two stages."""
+    need_gpu()
+    from synth.configs import ModelDesc
+    model = ModelDesc("opt", 4, 256, 4, 4, 1024, 1024, 256, 1)
+    ads = (lora(8),)
+    toks = synth.tokens(2, 150, model.vocab)
+    _, _, (t1, ref), _ = run(model, ads, 1, toks)
+    check_against_oracle(model, ads, toks, ref, t1)
+    for n, k in ((1, 3), (2, 2)):
+        _, _, (tn, ln), _ = run(model, ads, n, toks, policy="interleave", k=k, chunk_bytes=64 << 10)
+        assert np.array_equal(ln.view(np.uint32), ref.view(np.uint32)), (n, k)
+
+
 def test_gathered_bytes_exact():
     """After the trial every rank's weights equal the loader's bytes; unadapted = host image,
     adapted ranges = oracle merge within the merge bound."""

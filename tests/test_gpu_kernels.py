@@ -68,7 +68,9 @@ def _gemm_case(rng, M, K, N):
 
 
 @pytest.mark.parametrize("M,K,N,m0,m1", [(128, 256, 768, 0, 128), (16, 256, 1024, 0, 16), (300, 512, 384, 0, 300),
-                                         (256, 2048, 640, 128, 256), (200, 192, 136, 40, 170), (130, 688, 256, 0, 130)])
+                                         (256, 2048, 640, 128, 256), (200, 192, 136, 40, 170), (130, 688, 256, 0, 130),
+                                         (1024, 1024, 3072, 0, 1024), (2048, 512, 8192, 0, 2000),
+                                         (700, 1536, 1000, 100, 700)])
 def test_gemm_bf16_epilogue(M, K, N, m0, m1):
     need_gpu()
     rng = np.random.default_rng(M + K + N)
@@ -87,10 +89,12 @@ def test_gemm_bf16_epilogue(M, K, N, m0, m1):
     assert np.all(err <= bf16_ulp(r) + 1e-6 * np.abs(r).max()), err.max()
 
 
-def test_gemm_relu_and_resid_and_silu():
+@pytest.mark.parametrize("M,K,N,f", [(192, 320, 256, 136), (1536, 1024, 2560, 2752)])
+def test_gemm_relu_and_resid_and_silu(M, K, N, f):
+    """Small shapes take the split-K kernel or the persistent 128x256 kernel at S = 1; the second case runs the
+    persistent kernel over more tiles than SMs (both TMEM accumulators cycle)."""
     need_gpu()
-    rng = np.random.default_rng(11)
-    M, K, N = 192, 320, 256
+    rng = np.random.default_rng(11 + M)
     X, W, bias = _gemm_case(rng, M, K, N)
     Xd, Wd, bd = dev_bf16(X), dev_bf16(W), dev_bf16(bias)
     ref = bf16_bits_to_f64(X) @ bf16_bits_to_f64(W).T + bf16_bits_to_f64(bias)
@@ -107,7 +111,6 @@ def test_gemm_relu_and_resid_and_silu():
     torch.cuda.synchronize()
     assert np.allclose(h.cpu().numpy(), h0 + ref, rtol=1e-5, atol=1e-5)
     # SiLU(gate) * up with W = [gate; up]
-    f = 136
     Wgu = rbits(rng, (2 * f, K), 0.05)
     out2 = torch.zeros((M, f), dtype=torch.bfloat16, device="cuda")
     Wgud = dev_bf16(Wgu)
