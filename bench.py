@@ -429,7 +429,8 @@ def main():
                 continue
             t = a["total_ms"] * 1e-3
             # binding resource = the larger of (flops / tensor peak) and (bytes / HBM peak)
-            tensor_bound = k in ("gemm",) and a["flops"] / (bf16_sus * 1e12) > a["bytes"] / (hbm * 1e9)
+            # GEMMs and attention are tensor-core contractions; the rest are memory / latency-bound row kernels
+            tensor_bound = k in ("gemm", "attention") and a["flops"] / (bf16_sus * 1e12) > a["bytes"] / (hbm * 1e9)
             if tensor_bound:
                 ach, peak, unit = a["flops"] / t / 1e12, bf16_sus, "TFLOP/s"
             else:

@@ -46,7 +46,7 @@ struct AttnSmem {
 template <int HD>
 __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_constant__ CUtensorMap map, __nv_bfloat16* __restrict__ out,
                                                         int ldo, int t0, int t1, int group, int k_col0, int v_col0,
-                                                        float scale_log2) {
+                                                        float scale_log2, const int* dyn) {
     using SM = AttnSmem<HD>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -59,6 +59,10 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
     pdl_launch_dependents();
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int h = blockIdx.y, b = blockIdx.z, kvh = h / group;
+    if (dyn) {   // f3 decode graph: the position is read on the device
+        t0 += *dyn;
+        t1 += *dyn;
+    }
     const int qtile = gridDim.x - 1 - blockIdx.x;          // longest (latest) query tiles first
     const int q0 = t0 + qtile * QT;
     const int q_hi = min(q0 + QT, t1);
@@ -259,9 +263,12 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
 
 template <int HD>
 cudaError_t launch_tc(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int ldo, int t0, int t1, int B, int H,
-                      int group, int k_col0, int v_col0, float score_scale, cudaStream_t s, bool pdl) {
-    // 3-D view of the token-major rows: (col, sequence b, position t), t extent = t1 (keys >= t1 zero-filled).
-    const uint64_t dims[3] = {(uint64_t)ld, (uint64_t)B, (uint64_t)t1};
+                      int group, int k_col0, int v_col0, float score_scale, cudaStream_t s, bool pdl,
+                      const int* dyn, int t_extent) {
+    // 3-D view of the token-major rows: (col, sequence b, position t), t extent = t1 (keys >= t1 zero-filled);
+    // a decode graph's positions are only known on the device: the view then spans t_extent positions and the
+    // causal mask (key <= query) keeps later rows out.
+    const uint64_t dims[3] = {(uint64_t)ld, (uint64_t)B, (uint64_t)(dyn ? t_extent : t1)};
     const uint64_t strides[2] = {(uint64_t)ld * 2, (uint64_t)ld * 2 * B};
     const uint32_t box[3] = {64, 1, 128};
     CUtensorMap map;
@@ -273,7 +280,7 @@ cudaError_t launch_tc(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int 
     const dim3 grid((t1 - t0 + QT - 1) / QT, H, B);
     const float scale_log2 = score_scale * 1.4426950408889634f;
     return launch_pdl(attention_tc_kernel<HD>, grid, 160, SM::kTotal, s, pdl, map, out, ldo, t0, t1, group, k_col0,
-                      v_col0, scale_log2);
+                      v_col0, scale_log2, dyn);
 }
 
 }  // namespace
@@ -287,15 +294,18 @@ cudaError_t warm_attention_kernels() {
 
 cudaError_t launch_attention(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int ldo, int t0, int t1, int B,
                              int n_heads, int n_kv_heads, int hd, int k_col0, int v_col0, float score_scale,
-                             cudaStream_t s, bool pdl) {
+                             cudaStream_t s, bool pdl, const int* dyn, int t_extent) {
     if (t1 <= t0) return cudaSuccess;
     const bool tma_ok = (ld % 8) == 0 && (reinterpret_cast<uintptr_t>(qkv) & 15) == 0 && (ldo % 8) == 0 &&
                         (k_col0 % 8) == 0 && (v_col0 % 8) == 0;
     const int group = n_heads / n_kv_heads;
     if (tma_ok && hd == 64)
-        return launch_tc<64>(qkv, ld, out, ldo, t0, t1, B, n_heads, group, k_col0, v_col0, score_scale, s, pdl);
+        return launch_tc<64>(qkv, ld, out, ldo, t0, t1, B, n_heads, group, k_col0, v_col0, score_scale, s, pdl, dyn,
+                             t_extent);
     if (tma_ok && hd == 128)
-        return launch_tc<128>(qkv, ld, out, ldo, t0, t1, B, n_heads, group, k_col0, v_col0, score_scale, s, pdl);
+        return launch_tc<128>(qkv, ld, out, ldo, t0, t1, B, n_heads, group, k_col0, v_col0, score_scale, s, pdl, dyn,
+                              t_extent);
+    if (dyn) return cudaErrorNotSupported;   // decode graphs run on the tensor-core kernel only (hd 64 / 128)
     return launch_attention_simt(qkv, ld, out, ldo, t0, t1, B, n_heads, n_kv_heads, hd, k_col0, v_col0, score_scale,
                                  s);
 }

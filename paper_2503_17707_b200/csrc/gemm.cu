@@ -82,7 +82,9 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int split = S > 1 ? (int)cluster_rank() : 0;
-    const int m0 = a.M_begin + blockIdx.y * BM;
+    const int m_shift = a.m_dyn ? *a.m_dyn * a.m_dyn_mul : 0;   // f3 decode graphs: rows known on the device
+    const int m0 = a.M_begin + m_shift + blockIdx.y * BM;
+    const int m_end = a.M_end + m_shift;
     // EPI_SILU_MUL: tile = 64 gate columns + the matching 64 up columns -> 64 outputs.
     const int n_out0 = blockIdx.x * (EPI == EPI_SILU_MUL ? BN / 2 : BN);
     const int nk = (a.K + BK - 1) / BK;            // K tail: TMA zero-fills out-of-bounds columns
@@ -206,7 +208,7 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
     for (int idx = tid; idx < (r_hi - r_lo) * chunks; idx += 128) {
         const int r = r_lo + idx / chunks, ch = idx % chunks;
         const int row = m0 + r;
-        if (row >= a.M_end) continue;
+        if (row >= m_end) continue;
         if (EPI == EPI_SILU_MUL) {
             const int n = n_out0 + ch * 4;
             if (n >= a.N) continue;
@@ -580,7 +582,7 @@ cudaError_t launch_gemm(const CUtensorMap& mapX, const CUtensorMap& mapW, const 
     const int S = a.split_k > 0 ? a.split_k : gemm_split_k(a.N, a.K, a.epi, a.M_total);
     // The kernel is chosen from the WHOLE prompt (M_total), never from the rows of this launch, so a prompt split
     // into chunks runs every output through the same kernel and the same summation order.
-    if (S == 1 && a.split_k <= 0 && a.M_total > BM) {
+    if (S == 1 && a.split_k <= 0 && a.M_total > BM && !a.m_dyn) {
         switch (a.epi) {
             case EPI_BF16: return launch_big<EPI_BF16>(mapX, mapW, a, s);
             case EPI_RESID: return launch_big<EPI_RESID>(mapX, mapW, a, s);

@@ -62,6 +62,8 @@ struct SignalTargets {
     int n;
 };
 cudaError_t launch_signal(const SignalTargets& t, uint32_t value, cudaStream_t s);
+// f3 decode: tokens[(*dyn) * B + b] = tok_out[b] (the previous step's argmax becomes this step's input).
+cudaError_t launch_feed_tokens(int32_t* tokens, const int32_t* tok_out, const int* dyn, int B, cudaStream_t s);
 // base[idx[i]] = value (release, system scope) for i < n; idx is a device array.
 cudaError_t launch_set_words(uint32_t* base, const int32_t* idx, int n, uint32_t value, cudaStream_t s);
 
@@ -98,6 +100,8 @@ struct GemmArgs {
     int ldo;
     int up_row0;                // EPI_SILU_MUL: first row of `up` in W (= N_out)
     int split_k;                // 0 = automatic (gemm_split_k), else the cluster split-K factor (1, 2, 4, 8)
+    const int* m_dyn;           // f3 decode graphs: rows shift by (*m_dyn) * m_dyn_mul (device), or null
+    int m_dyn_mul;
     int M_total;                // rows of the whole prompt batch (picks split_k; chunk-invariant), 0 = M_end-M_begin
     int pdl;                    // 1: programmatic dependent launch after the stream's previous kernel
 };
@@ -107,8 +111,10 @@ cudaError_t launch_gemm(const CUtensorMap& mapX, const CUtensorMap& mapW, const 
 
 // ---------------------------------------------------------------- SIMT kernels
 // Row norm over d of fp32 rows -> bf16: LayerNorm (beta != null) or RMSNorm (beta == null).
+// dyn (f3 decode graphs): input rows shift by (*dyn) * dyn_in and output rows by (*dyn) * dyn_out (device).
 cudaError_t launch_norm(const float* h, int ldh, __nv_bfloat16* out, int ldo, int rows, int d, const __nv_bfloat16* gamma,
-                        const __nv_bfloat16* beta, float eps, cudaStream_t s, bool pdl = false);
+                        const __nv_bfloat16* beta, float eps, cudaStream_t s, bool pdl = false,
+                        const int* dyn = nullptr, int dyn_in = 0, int dyn_out = 0);
 
 struct EmbedSrc {
     const void* base[8];           // embedding table of each owner (peer pointers allowed); bf16 or fp32
@@ -117,20 +123,21 @@ struct EmbedSrc {
 };
 // h[row, :] = E[tok[row]] (+ P[pos(row) + 2]) as fp32, rows [r0, r1), row = t * B + b.
 cudaError_t launch_embed(const EmbedSrc& E, const __nv_bfloat16* pos, const int32_t* tok, float* h, int d, int r0,
-                         int r1, int B, cudaStream_t s, bool pdl = false);
+                         int r1, int B, cudaStream_t s, bool pdl = false, const int* dyn = nullptr);
 
 // RoPE cos/sin table [T x hd/2] (float2), angles t * theta^(-2i/hd) computed in fp64.
 cudaError_t launch_rope_table(float2* table, int T, int hd, double theta, cudaStream_t s);
 // In-place rotate_half RoPE on q (n_q heads at col 0) and k (n_k heads at col q_cols) of rows [r0, r1).
 cudaError_t launch_rope(__nv_bfloat16* qkv, int ld, int r0, int r1, int B, int n_q, int n_k, int hd, int k_col0,
-                        const float2* table, cudaStream_t s, bool pdl = false);
+                        const float2* table, cudaStream_t s, bool pdl = false, const int* dyn = nullptr);
 
 // Causal attention for query rows [t0, t1) (token-major rows t*B+b) against keys [0, t] of the same
 // sequence; q at col h*hd, k at k_col0 + (h/group)*hd, v at v_col0 + (h/group)*hd of `qkv`.
 // hd = 64 or 128: tensor-core kernel (attention.cu); other head sizes: the SIMT kernel (simt.cu).
+// dyn (f3 decode graphs): positions shift by *dyn; t_extent then bounds the keys' TMA view (>= every t1 + *dyn).
 cudaError_t launch_attention(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int ldo, int t0, int t1, int B,
                              int n_heads, int n_kv_heads, int hd, int k_col0, int v_col0, float score_scale,
-                             cudaStream_t s, bool pdl = false);
+                             cudaStream_t s, bool pdl = false, const int* dyn = nullptr, int t_extent = 0);
 cudaError_t launch_attention_simt(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int ldo, int t0, int t1,
                                   int B, int n_heads, int n_kv_heads, int hd, int k_col0, int v_col0,
                                   float score_scale, cudaStream_t s);

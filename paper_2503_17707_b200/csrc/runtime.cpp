@@ -133,6 +133,7 @@ WsLayout pb::ws_layout(const pb_plan* p, int32_t batch, int32_t seq) {
     L.nan = o;     o = al(o + 4);
     L.rope = o;    o = al(o + (m.arch == PB_ARCH_LLAMA ? 8 * (int64_t)seq * (hd / 2) : 0));
     L.held = o;    o = al(o + (p->survivors.empty() ? 0 : 4 * (int64_t)p->chunks.size()));   // re-plan signal list
+    L.dpos = o;    o = al(o + 4);   // f3 decode graphs: the step's position
     L.total = al(o, 4096);
     return L;
 }
@@ -409,11 +410,15 @@ extern "C" pb_status pb_ctx_create(const pb_plan* plan, int32_t rank, const void
     if (st != PB_OK) return cleanup(st);
     st = build_prefill_maps(c);
     if (st != PB_OK) return cleanup(st);
-    if (cudaHostAlloc((void**)&c->h_tokens, sizeof(int32_t) * L.max_rows, cudaHostAllocPortable) != cudaSuccess ||
+    if (cudaHostAlloc((void**)&c->h_pos, sizeof(int32_t), cudaHostAllocPortable) != cudaSuccess ||
+        cudaHostAlloc((void**)&c->h_tokens, sizeof(int32_t) * L.max_rows, cudaHostAllocPortable) != cudaSuccess ||
         cudaHostAlloc((void**)&c->h_out, sizeof(int32_t) * (L.max_batch + 1), cudaHostAllocPortable) != cudaSuccess)
         return cleanup(fail(PB_ECUDA, "cudaHostAlloc failed"));
-    // readiness words start at 0 (epochs are >= 1)
-    if (cudaMemset(c->ws + L.flags, 0, 4 * (size_t)L.n_words) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
+    // readiness words start at 0 (epochs are >= 1); the q|k|v slots start at 0 so a key row no step has written
+    // yet is finite (decode graphs view keys up to max_seq and mask the later ones)
+    if (cudaMemset(c->ws + L.flags, 0, 4 * (size_t)L.n_words) != cudaSuccess ||
+        cudaMemset(c->ws + L.qkv, 0, (size_t)L.qkv_stride * L.n_qkv) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess)
         return cleanup(fail(PB_ECUDA, "flag init failed"));
     *out = c;
     return PB_OK;
@@ -433,6 +438,8 @@ extern "C" void pb_ctx_free(pb_ctx* c) {
     for (auto e : c->gathered) d(e);
     for (auto& r : c->prof) { d(r.a); d(r.b); }
     for (auto& g : c->replay_graphs) cudaGraphExecDestroy(g.exec);
+    for (auto& g : c->decode_graphs) cudaGraphExecDestroy(g.exec);
+    if (c->h_pos) cudaFreeHost(c->h_pos);
     for (auto& p : c->peers)
         for (void* b : p.ipc_bases) cudaIpcCloseMemHandle(b);
     if (c->h_tokens) cudaFreeHost(c->h_tokens);
@@ -772,6 +779,8 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, boo
         a.up_row0 = f;
         a.M_total = c->gemm_m_total;  // whole prompt batch (or one decode step): chunking never changes split-K
         a.pdl = c->profiling ? 0 : 1; // per-launch timing events between kernels would cancel the overlap anyway
+        a.m_dyn = c->dyn_pos;         // decode graph: rows r0.. are relative to position * B
+        a.m_dyn_mul = B;
         return a;
     };
     // Algorithmic work of a GEMM launch: 2MNK flops; bytes = X + W + output (fp32 residual read + write).
@@ -786,7 +795,7 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, boo
     auto norm = [&](const char* g_name, const char* b_name) -> cudaError_t {
         const int pi = prof_begin(c, K_NORM, s);
         cudaError_t e = launch_norm(h + (size_t)r0 * d, d, x + (size_t)r0 * d, d, rows, d, wt(c, l, g_name),
-                                    opt ? wt(c, l, b_name) : nullptr, m.norm_eps, s, !c->profiling);
+                                    opt ? wt(c, l, b_name) : nullptr, m.norm_eps, s, !c->profiling, c->dyn_pos, B, B);
         prof_end(c, pi, s, 8.0 * rows * d, 6.0 * rows * d);
         return e;
     };
@@ -801,13 +810,14 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, boo
     if (!opt) {
         const int pi = prof_begin(c, K_ROPE, s);
         CU(launch_rope(qkv + (size_t)row_base * qdim, qdim, r0 - row_base, r1 - row_base, B, H, KVH, hd, qd,
-                       reinterpret_cast<const float2*>(c->ws + L.rope), s, !c->profiling));
+                       reinterpret_cast<const float2*>(c->ws + L.rope), s, !c->profiling, c->dyn_pos));
         prof_end(c, pi, s, 6.0 * rows * (qd + kvd) / 2, 4.0 * rows * (qd + kvd));
     }
     {
         const int pi = prof_begin(c, K_ATTN, s);
         CU(launch_attention(qkv + (size_t)row_base * qdim, qdim, attn + (size_t)row_base * qd, qd, ta, tb, B, H, KVH,
-                            hd, qd, qd + kvd, opt ? 1.0f : 1.0f / sqrtf((float)hd), s, !c->profiling));
+                            hd, qd, qd + kvd, opt ? 1.0f : 1.0f / sqrtf((float)hd), s, !c->profiling, c->dyn_pos,
+                            L.max_seq));
         // causal pairs: sum over queries t in [ta, tb) of (t + 1) keys
         const double pairs = (double)B * ((double)tb * (tb + 1) / 2 - (double)ta * (ta + 1) / 2);
         prof_end(c, pi, s, 4.0 * pairs * H * hd, 2.0 * rows * qd * 2 + 2.0 * B * tb * 2 * kvd);
@@ -1228,14 +1238,19 @@ pb_status issue_item(Issuer& I, const Item& it) {
             if (is_head_owner(p, r)) owners.push_back(r);
     switch (it.kind) {
         case I_PROLOGUE:
-            if (!opt) {   // positions up to the workspace's max_seq: decode steps reuse the table
+            if (!opt && I.dec_t < 0) {   // positions up to the workspace's max_seq: decode steps reuse the table
                 CU(launch_rope_table(reinterpret_cast<float2*>(c->ws + L.rope), L.max_seq, hd, m.rope_theta, s));
                 ++c->n_launches;
             }
             if (g == 0 || rep) {
                 // the token upload went out on the copy lane ahead of the weights (issue_trial): an H2D copy on
                 // this stream would queue behind the whole load in the copy engine (measured: drains per stream)
-                if (I.dec_t >= 0)   // decode: the previous step's tokens become position dec_t's inputs
+                if (c->dyn_pos) {   // decode graph: position from the host's pinned word, then feed the tokens
+                    CU(cudaMemcpyAsync(c->ws + L.dpos, c->h_pos, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+                    CU(launch_feed_tokens(reinterpret_cast<int32_t*>(c->ws + L.tokens),
+                                          reinterpret_cast<const int32_t*>(c->ws + L.tok_out), c->dyn_pos, B, s));
+                    ++c->n_launches;
+                } else if (I.dec_t >= 0)   // decode: the previous step's tokens become position dec_t's inputs
                     CU(cudaMemcpyAsync(c->ws + L.tokens + sizeof(int32_t) * (size_t)I.dec_t * B, c->ws + L.tok_out,
                                        sizeof(int32_t) * B, cudaMemcpyDeviceToDevice, s));
                 else if (I.replay)
@@ -1283,7 +1298,7 @@ pb_status issue_item(Issuer& I, const Item& it) {
             else
                 CU(launch_embed(E, opt ? wt(c, -1, "pos") : nullptr,
                                 reinterpret_cast<const int32_t*>(c->ws + L.tokens) + row_base, h + (size_t)row_base * d,
-                                d, r0 - row_base, r1 - row_base, Bk, s, !c->profiling));
+                                d, r0 - row_base, r1 - row_base, Bk, s, !c->profiling, c->dyn_pos));
             prof_end(c, pi, s, (opt ? 1.0 : 0.0) * (r1 - r0) * d, (r1 - r0) * d * (opt ? 8.0 : 6.0));
             ++c->n_launches;
             break;
@@ -1317,7 +1332,7 @@ pb_status issue_item(Issuer& I, const Item& it) {
                                    opt ? wt_f32(c, -1, "final_b") : nullptr, m.norm_eps, s));
             else
                 CU(launch_norm(last, ldh, y, d, B, d, wt(c, -1, "final_g"), opt ? wt(c, -1, "final_b") : nullptr,
-                               m.norm_eps, s, !c->profiling));
+                               m.norm_eps, s, !c->profiling, c->dyn_pos, B, 0));
             prof_end(c, pi, s, 8.0 * B * d, 6.0 * B * d);
             ++c->n_launches;
             std::vector<int32_t> remote;
@@ -1617,8 +1632,46 @@ extern "C" pb_status pb_decode_step(pb_ctx* c, uint32_t epoch) {
     c->n_launches = 0;
     c->prof_n = 0;
     c->n_decoded++;
-    CU(cudaEventRecord(c->t0, c->comp));
     const int B = c->cur_batch;
+    const int hd = c->plan->head_dim();
+    if ((c->n == 1 || c->replica) && !c->plan->f32() && (hd == 64 || hd == 128)) {
+        // Single GPU (or a replica): the step is a CUDA graph captured once per batch size; the position is a
+        // device word filled from a pinned host word by the graph's first node, so every step relaunches it.
+        pb_ctx::DecodeGraph* dg = nullptr;
+        for (auto& g : c->decode_graphs)
+            if (g.B == B) dg = &g;
+        if (!dg) {
+            const int saved = c->n_launches;
+            CU(cudaStreamBeginCapture(c->comp, cudaStreamCaptureModeThreadLocal));
+            c->capturing = true;
+            c->decode_t = 0;
+            c->dyn_pos = reinterpret_cast<const int*>(c->ws + c->L.dpos);
+            pb_status ist = issue_trial(c, B, 1, true);
+            c->capturing = false;
+            c->decode_t = -1;
+            c->dyn_pos = nullptr;
+            cudaGraph_t g = nullptr;
+            cudaError_t ce = cudaStreamEndCapture(c->comp, &g);
+            if (ist != PB_OK) {
+                if (g) cudaGraphDestroy(g);
+                return ist;
+            }
+            CU(ce);
+            cudaGraphExec_t ge = nullptr;
+            cudaError_t ie = cudaGraphInstantiate(&ge, g, 0);
+            cudaGraphDestroy(g);
+            CU(ie);
+            c->decode_graphs.push_back({B, ge, c->n_launches - saved});
+            dg = &c->decode_graphs.back();
+        }
+        c->n_launches = dg->launches;
+        *c->h_pos = t;
+        c->issue_status = PB_OK;
+        CU(cudaEventRecord(c->t0, c->comp));
+        CU(cudaGraphLaunch(dg->exec, c->comp));
+        return PB_OK;
+    }
+    CU(cudaEventRecord(c->t0, c->comp));
     c->issue_status = PB_OK;
     c->issue_msg[0] = '\0';
     c->load_thread = std::thread([c, B, t]() {

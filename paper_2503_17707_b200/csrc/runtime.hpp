@@ -15,7 +15,7 @@ namespace pb {
 // peer can address it: flags | tokens | h | x | qkv[n_qkv] | attn | mlp | y | logits | tok_out | nan | rope.
 struct WsLayout {
     int64_t flags = 0, tokens = 0, h = 0, x = 0, qkv = 0, qkv_stride = 0, attn = 0, mlp = 0, y = 0, logits = 0,
-            tok_out = 0, nan = 0, rope = 0, held = 0, total = 0;
+            tok_out = 0, nan = 0, rope = 0, held = 0, dpos = 0, total = 0;
     int32_t n_qkv = 1;
     int32_t max_rows = 0, max_batch = 0, max_seq = 0;
     // readiness words (uint32) inside `flags`
@@ -142,6 +142,15 @@ struct pb_ctx {
     int32_t n_decoded = 0;       // decode steps since the last prompt trial
     bool prompt_replica = false; // the last prompt trial ran in replica mode (its KV cache covers every layer)
     int32_t gemm_m_total = 0;    // rows that pick the GEMM split-K (whole prompt batch, or one decode step)
+    // decode graphs (single rank / replica): captured once per batch size with every position read on the device
+    const int* dyn_pos = nullptr;  // set while capturing a decode graph: device int holding the step's position
+    int32_t* h_pos = nullptr;      // pinned: the host writes the position here before each graph launch
+    struct DecodeGraph {
+        int32_t B;
+        cudaGraphExec_t exec;
+        int32_t launches;
+    };
+    std::vector<DecodeGraph> decode_graphs;
     struct ReplayGraph {
         int32_t B, T, profiled, replica;
         cudaGraphExec_t exec;

@@ -41,11 +41,18 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 template <int NT, int PER>
 __global__ void __launch_bounds__(NT) norm_kernel(const float* __restrict__ h, int ldh, __nv_bfloat16* __restrict__ out,
                                                   int ldo, int d, const __nv_bfloat16* __restrict__ gamma,
-                                                  const __nv_bfloat16* __restrict__ beta, float eps) {
+                                                  const __nv_bfloat16* __restrict__ beta, float eps, const int* dyn,
+                                                  int dyn_in, int dyn_out) {
     pdl_launch_dependents();   // a PDL-launched GEMM may start its weight prefetch
     pdl_wait();                // PDL-launched: the previous kernel's output is visible from here on
     __shared__ float red[32];
-    const float* x = h + (size_t)blockIdx.x * ldh;
+    long long row = blockIdx.x, orow = blockIdx.x;
+    if (dyn != nullptr) {
+        const long long t = *dyn;
+        row += t * dyn_in;
+        orow += t * dyn_out;
+    }
+    const float* x = h + row * (long long)ldh;
     float v[PER];
     float s = 0.f;
 #pragma unroll
@@ -65,7 +72,7 @@ __global__ void __launch_bounds__(NT) norm_kernel(const float* __restrict__ h, i
     }
     const float var = block_sum<NT>(q, red) / d;
     const float rstd = rsqrtf(var + eps);
-    __nv_bfloat16* o = out + (size_t)blockIdx.x * ldo;
+    __nv_bfloat16* o = out + orow * (long long)ldo;
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
         const int c = threadIdx.x + i * NT;
@@ -79,10 +86,10 @@ __global__ void __launch_bounds__(NT) norm_kernel(const float* __restrict__ h, i
 
 // ------------------------------------------------------------------ embedding (+ OPT learned positions)
 __global__ void embed_kernel(EmbedSrc E, const __nv_bfloat16* __restrict__ pos, const int32_t* __restrict__ tok,
-                             float* __restrict__ h, int d, int r0, int B) {
+                             float* __restrict__ h, int d, int r0, int B, const int* dyn) {
     pdl_launch_dependents();
     pdl_wait();
-    const int row = r0 + blockIdx.x;
+    const int row = r0 + blockIdx.x + (dyn ? *dyn * B : 0);
     const int t = row / B;
     const int id = tok[row];
     int owner = 0;
@@ -121,10 +128,10 @@ __global__ void rope_table_kernel(float2* table, int T, int hd, double theta) {
 
 // x'_i = x_i cos - x_{i+hd/2} sin ; x'_{i+hd/2} = x_{i+hd/2} cos + x_i sin   (HF rotate_half)
 __global__ void rope_kernel(__nv_bfloat16* qkv, int ld, int r0, int B, int n_q, int n_k, int hd, int k_col0,
-                            const float2* __restrict__ table) {
+                            const float2* __restrict__ table, const int* dyn) {
     pdl_launch_dependents();   // a PDL-launched GEMM may start its weight prefetch
     pdl_wait();                // PDL-launched: the previous kernel's output is visible from here on
-    const int row = r0 + blockIdx.x;
+    const int row = r0 + blockIdx.x + (dyn ? *dyn * B : 0);
     const int t = row / B;
     const int half = hd / 2;
     const int total = (n_q + n_k) * half;
@@ -330,7 +337,17 @@ __global__ void set_words_kernel(uint32_t* base, const int32_t* __restrict__ idx
     }
 }
 
+__global__ void feed_tokens_kernel(int32_t* tokens, const int32_t* __restrict__ tok_out, const int* dyn, int B) {
+    const int b = threadIdx.x;
+    if (b < B) tokens[*dyn * B + b] = tok_out[b];
+}
+
 }  // namespace
+
+cudaError_t launch_feed_tokens(int32_t* tokens, const int32_t* tok_out, const int* dyn, int B, cudaStream_t s) {
+    feed_tokens_kernel<<<1, 32, 0, s>>>(tokens, tok_out, dyn, B);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_set_words(uint32_t* base, const int32_t* idx, int n, uint32_t value, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
@@ -344,7 +361,7 @@ cudaError_t warm_simt_kernels() {
                          (const void*)rope_table_kernel, (const void*)rope_kernel, (const void*)attention_kernel<32>,
                          (const void*)attention_kernel<64>, (const void*)attention_kernel<128>,
                          (const void*)logits_kernel, (const void*)argmax_kernel, (const void*)signal_kernel,
-                         (const void*)set_words_kernel};
+                         (const void*)set_words_kernel, (const void*)feed_tokens_kernel};
     for (const void* f : fns) {
         cudaError_t e = cudaFuncGetAttributes(&a, f);
         if (e != cudaSuccess) return e;
@@ -353,18 +370,23 @@ cudaError_t warm_simt_kernels() {
 }
 
 cudaError_t launch_norm(const float* h, int ldh, __nv_bfloat16* out, int ldo, int rows, int d,
-                        const __nv_bfloat16* gamma, const __nv_bfloat16* beta, float eps, cudaStream_t s, bool pdl) {
+                        const __nv_bfloat16* gamma, const __nv_bfloat16* beta, float eps, cudaStream_t s, bool pdl,
+                        const int* dyn, int dyn_in, int dyn_out) {
     if (rows <= 0) return cudaSuccess;
-    if (d <= 256 * 8) return launch_pdl(norm_kernel<256, 8>, rows, 256, 0, s, pdl, h, ldh, out, ldo, d, gamma, beta, eps);
-    if (d <= 256 * 40) return launch_pdl(norm_kernel<256, 40>, rows, 256, 0, s, pdl, h, ldh, out, ldo, d, gamma, beta, eps);
+    if (d <= 256 * 8)
+        return launch_pdl(norm_kernel<256, 8>, rows, 256, 0, s, pdl, h, ldh, out, ldo, d, gamma, beta, eps, dyn, dyn_in,
+                          dyn_out);
+    if (d <= 256 * 40)
+        return launch_pdl(norm_kernel<256, 40>, rows, 256, 0, s, pdl, h, ldh, out, ldo, d, gamma, beta, eps, dyn, dyn_in,
+                          dyn_out);
     return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_embed(const EmbedSrc& E, const __nv_bfloat16* pos, const int32_t* tok, float* h, int d, int r0,
-                         int r1, int B, cudaStream_t s, bool pdl) {
+                         int r1, int B, cudaStream_t s, bool pdl, const int* dyn) {
     if (r1 <= r0) return cudaSuccess;
     if (d % 8) return cudaErrorInvalidValue;
-    return launch_pdl(embed_kernel, r1 - r0, 128, 0, s, pdl, E, pos, tok, h, d, r0, B);
+    return launch_pdl(embed_kernel, r1 - r0, 128, 0, s, pdl, E, pos, tok, h, d, r0, B, dyn);
 }
 
 cudaError_t launch_rope_table(float2* table, int T, int hd, double theta, cudaStream_t s) {
@@ -375,9 +397,9 @@ cudaError_t launch_rope_table(float2* table, int T, int hd, double theta, cudaSt
 }
 
 cudaError_t launch_rope(__nv_bfloat16* qkv, int ld, int r0, int r1, int B, int n_q, int n_k, int hd, int k_col0,
-                        const float2* table, cudaStream_t s, bool pdl) {
+                        const float2* table, cudaStream_t s, bool pdl, const int* dyn) {
     if (r1 <= r0) return cudaSuccess;
-    return launch_pdl(rope_kernel, r1 - r0, 256, 0, s, pdl, qkv, ld, r0, B, n_q, n_k, hd, k_col0, table);
+    return launch_pdl(rope_kernel, r1 - r0, 256, 0, s, pdl, qkv, ld, r0, B, n_q, n_k, hd, k_col0, table, dyn);
 }
 
 cudaError_t launch_attention_simt(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int ldo, int t0, int t1,

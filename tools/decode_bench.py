@@ -61,7 +61,8 @@ def main():
             "prompt": w.seq, "steps": a.steps, "ttft_ms": ttft, "decode_ms_median": med,
             "decode_ms_min": min(step_ms), "replica_decode_ms_median": statistics.median(rep_ms[2:]),
             "hbm_bound_ms": bound_ms, "frac_of_hbm_bound": bound_ms / med, "tokens": out[:8],
-            "note": "eager launches (~4 us host time each, ~190 per step): host-bound; see DESIGN.md §5"}
+            "note": "single GPU: each step is one CUDA graph (position read on the device); ~8 kernels per layer, "
+                    "fixed per-kernel cost dominates at M = batch rows (DESIGN.md §5)"}
     print(json.dumps(line), flush=True)
     eng.close()
 
