@@ -14,7 +14,7 @@
 //   O += P V_j             tcgen05.mma M128 N=hd, K = 128 keys, V read MN-major straight from its TMA tile,
 //                          fp32 accumulator in TMEM columns [128, 128 + hd)
 //   out = bf16(O / l)      l = sum of the bf16-rounded P actually multiplied
-// K_{j+1} streams in while softmax j runs; S_{j+1} overlaps PV_j; V is double-buffered. Q/K/V come through one
+// K and V are double-buffered (K_{j+2} streams in while softmax j runs); S_{j+1} overlaps softmax j and PV_j. Q/K/V come through one
 // 3-D tensor map over the token-major qkv rows (col, sequence b, position t) whose t extent is t1, so keys
 // past the last computed position are zero-filled by TMA, never read.
 //
@@ -38,8 +38,8 @@ constexpr float kRescale = 8.0f;       // lazy rescale threshold (log2 domain)
 
 template <int HD>
 struct AttnSmem {
-    static constexpr int kQ = HD / 64 * kAtom, kK = kQ, kV = kQ, kP = 2 * kAtom;   // V double-buffered
-    static constexpr int offQ = 0, offK = offQ + kQ, offV = offK + kK, offP = offV + 2 * kV, offBar = offP + kP;
+    static constexpr int kQ = HD / 64 * kAtom, kK = kQ, kV = kQ, kP = 2 * kAtom;   // K and V double-buffered
+    static constexpr int offQ = 0, offK = offQ + kQ, offV = offK + 2 * kK, offP = offV + 2 * kV, offBar = offP + kP;
     static constexpr int kTotal = offBar + 128 + 1024;
 };
 
@@ -52,9 +52,9 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *sQ = smem + SM::offQ, *sK = smem + SM::offK, *sV = smem + SM::offV, *sP = smem + SM::offP;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::offBar);
-    uint64_t *q_full = bars, *k_full = bars + 1, *v_full = bars + 2 /* [2] */, *s_full = bars + 4,
-             *s_free = bars + 5, *p_full = bars + 6, *o_full = bars + 7;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+    uint64_t *q_full = bars, *k_full = bars + 1 /* [2] */, *v_full = bars + 3 /* [2] */, *s_full = bars + 5,
+             *s_free = bars + 6, *p_full = bars + 7, *o_full = bars + 8;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
 
     pdl_launch_dependents();
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -71,7 +71,8 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
     if (tid == 0) {
         tma_prefetch_desc(&map);
         mbar_init(q_full, 1);
-        mbar_init(k_full, 1);
+        mbar_init(&k_full[0], 1);
+        mbar_init(&k_full[1], 1);
         mbar_init(&v_full[0], 1);
         mbar_init(&v_full[1], 1);
         mbar_init(s_full, 1);
@@ -97,41 +98,47 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
             };
             mbar_arrive_expect_tx(q_full, SM::kQ);
             load_rows(sQ, q_full, h * HD, q0);
-            mbar_arrive_expect_tx(k_full, SM::kK);
-            load_rows(sK, k_full, k_col0 + kvh * HD, 0);
-            for (int j = 0; j < 2 && j < n_kv; ++j) {
+            for (int j = 0; j < 2 && j < n_kv; ++j) {   // K_0, K_1, V_0, V_1 up front
+                mbar_arrive_expect_tx(&k_full[j], SM::kK);
+                load_rows(sK + j * SM::kK, &k_full[j], k_col0 + kvh * HD, j * KT);
                 mbar_arrive_expect_tx(&v_full[j], SM::kV);
                 load_rows(sV + j * SM::kV, &v_full[j], v_col0 + kvh * HD, j * KT);
             }
             constexpr uint32_t idS = idesc_bf16_f32(128, 128, 0, 0);
             constexpr uint32_t idO = idesc_bf16_f32(128, HD, 0, 1);
             mbar_wait(q_full, 0);
-            for (int j = 0; j < n_kv; ++j) {
-                const uint32_t ph = j & 1;
-                // ---- S = Q K_j^T (S columns are free once every softmax warp has read S_{j-1}); runs
-                // concurrently with PV_{j-1}
-                mbar_wait(k_full, ph);
-                if (j > 0) mbar_wait(s_free, (j - 1) & 1);
+            auto issue_S = [&](int j) {   // S = Q K_j^T into the (single) S columns
+                mbar_wait(&k_full[j & 1], (j >> 1) & 1);
                 tc_fence_after();
+                const uint32_t kbase = smem_u32(sK + (j & 1) * SM::kK);
 #pragma unroll
                 for (int kk = 0; kk < HD / 16; ++kk) {
                     const uint32_t off = (kk >> 2) * kBox + (kk & 3) * 32;
                     umma_bf16(tS, smem_desc(smem_u32(sQ) + off, 16, 1024, kSw128),
-                              smem_desc(smem_u32(sK) + off, 16, 1024, kSw128), idS, kk > 0 ? 1u : 0u);
+                              smem_desc(kbase + off, 16, 1024, kSw128), idS, kk > 0 ? 1u : 0u);
                 }
                 umma_commit(s_full);
+            };
+            issue_S(0);
+            for (int j = 0; j < n_kv; ++j) {
+                const uint32_t ph = j & 1;
+                // ---- S_j done: its K buffer takes K_{j+2}
+                mbar_wait(s_full, ph);
+                if (j + 2 < n_kv) {
+                    mbar_arrive_expect_tx(&k_full[j & 1], SM::kK);
+                    load_rows(sK + (j & 1) * SM::kK, &k_full[j & 1], k_col0 + kvh * HD, (j + 2) * KT);
+                }
+                // ---- S_{j+1} as soon as softmax j has read S_j out of TMEM: it runs during softmax j
+                if (j + 1 < n_kv) {
+                    mbar_wait(s_free, ph);
+                    issue_S(j + 1);
+                }
                 // ---- V_{j+1} into the buffer PV_{j-1} has finished reading
                 if (j >= 1 && j + 1 < n_kv) {
                     mbar_wait(o_full, (j - 1) & 1);
                     const int vb = (j + 1) & 1;
                     mbar_arrive_expect_tx(&v_full[vb], SM::kV);
                     load_rows(sV + vb * SM::kV, &v_full[vb], v_col0 + kvh * HD, (j + 1) * KT);
-                }
-                // ---- K_{j+1} streams in while softmax j runs
-                mbar_wait(s_full, ph);
-                if (j + 1 < n_kv) {
-                    mbar_arrive_expect_tx(k_full, SM::kK);
-                    load_rows(sK, k_full, k_col0 + kvh * HD, (j + 1) * KT);
                 }
                 // ---- O += P_j V_j
                 mbar_wait(p_full, ph);
