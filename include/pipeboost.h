@@ -222,6 +222,18 @@ PB_API pb_status pb_ctx_link_local(pb_ctx* ctx, int32_t peer, pb_ctx* peer_ctx);
  * epoch, so device flags never need resetting. */
 PB_API pb_status pb_trial_begin(pb_ctx* ctx, uint32_t epoch);
 
+/* f4 — storage tier ("a model checkpoint already residing in DRAM" is the
+ * paper's starting point; its Table 1, charges 20.9-30.8% of TTFT to reading the checkpoint). With a
+ * file source, the base weights of the cold start come from `path` — the checkpoint in the canonical host
+ * layout (byte host_off of the plan at file offset host_off) — instead of the pinned host image: a reader
+ * thread pread()s this rank's own copy groups, in load order, into the caller's PINNED, 4 KiB-aligned
+ * staging buffer (>= 2 slots of the largest group; O_DIRECT when the file system allows), and each slot is
+ * DMA'd as soon as it is full and refilled once its copy has landed — file reads, PCIe and merges overlap
+ * chunk by chunk, every rank reading only its disjoint slice. LoRA factors still come from host_adapters.
+ * path = NULL returns to the pinned image. Call between trials. Errors: PB_EINVAL (open / staging),
+ * PB_ENOMEM (staging too small), PB_EPROTOCOL (a trial is being armed); read errors surface from the trial. */
+PB_API pb_status pb_ctx_set_file_source(pb_ctx* ctx, const char* path, void* staging, int64_t staging_bytes);
+
 /* a2 — enqueue this rank's load list: chunked cudaMemcpyAsync pinned host -> HBM,
  * alternating the two H2D streams; a `landed` event per chunk. Async. */
 PB_API pb_status pb_load_shard(pb_ctx* ctx);

@@ -112,6 +112,7 @@ _SIGS = {
     "pb_prefill_replay": [_P, C.c_uint32, _P, C.c_int32, C.c_int32],
     "pb_switch_adapter": [_P, C.c_int32],
     "pb_decode_step": [_P, C.c_uint32],
+    "pb_ctx_set_file_source": [_P, C.c_char_p, _P, C.c_int64],
     "pb_ctx_set_replica": [_P, C.c_int32],
     "pb_epoch_create": [C.c_int32, C.c_double, C.c_int32, C.POINTER(_P)],
     "pb_epoch_set_active": [_P, C.c_int32, C.c_double],
@@ -327,6 +328,10 @@ class EpochScheduler:
                 self.h = None
         except Exception:
             pass
+
+
+def pb_ctx_set_file_source(ctx, path, staging_ptr, staging_bytes):
+    check(lib().pb_ctx_set_file_source(ctx, path.encode() if path else None, staging_ptr, staging_bytes))
 
 
 def pb_decode_step(ctx, epoch):

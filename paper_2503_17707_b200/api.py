@@ -224,6 +224,18 @@ class RankEngine:
         self.enqueue(epoch, tokens, batch, seq, adapter_id)
         return self.wait(want_logits)
 
+    def set_file_source(self, path: Optional[str], staging_bytes: int = 256 << 20):
+        """f4: read the base weights of later cold starts from the checkpoint file `path` (canonical host layout)
+        through a pinned staging ring of `staging_bytes`; None returns to the pinned host image."""
+        if path is None:
+            B.pb_ctx_set_file_source(self.ctx, None, None, 0)
+            self._staging = None
+            return
+        self._staging = torch.empty(staging_bytes + 4096, dtype=torch.uint8, pin_memory=True)
+        base = (self._staging.data_ptr() + 4095) // 4096 * 4096
+        with torch.cuda.device(self.device):
+            B.pb_ctx_set_file_source(self.ctx, path, base, staging_bytes)
+
     def decode_enqueue(self, epoch: int):
         """f3: one decode step of the last prefilled batch (every rank, same epoch); complete with wait()."""
         with torch.cuda.device(self.device):

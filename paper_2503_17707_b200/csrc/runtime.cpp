@@ -231,7 +231,7 @@ static void build_copy_groups(pb_ctx* c) {
                 continue;
             }
         }
-        c->copies.push_back(CopyGroup{src, dst, ch.bytes, i, 1});
+        c->copies.push_back(CopyGroup{src, dst, ch.bytes, i, 1, false});
     }
     c->landed_alias.assign(p->chunks.size(), -1);
     for (const CopyGroup& g : c->copies)
@@ -1000,8 +1000,14 @@ pb_status issue_group(Issuer& I, size_t gi) {
     // The landed event doubles as the merge stream's dependency: the issuer issues every copy before the
     // waits on it, so a plain event works and the copy lane carries no memop (a stream write after each
     // copy stalls the copy engine between groups, measured ~10 us per group on B200).
-    CU(cudaMemcpyAsync(g.dst, g.src, g.bytes, cudaMemcpyHostToDevice, c->h2d[0]));
+    const char* src = g.src;
+    if (g.from_file) {   // f4: the reader has staged this group (checked by the issuer loop)
+        if (c->file->read_error.load()) return fail(PB_ECUDA, "checkpoint read failed: %s", strerror(c->file->read_error.load()));
+        src = c->file->ready((int64_t)gi);
+    }
+    CU(cudaMemcpyAsync(g.dst, src, g.bytes, cudaMemcpyHostToDevice, c->h2d[0]));
     CU(cudaEventRecord(c->landed[ld[g.first]], c->h2d[0]));
+    if (g.from_file) c->file->issued((int64_t)gi, c->landed[ld[g.first]]);
     CU(I.h2d.add(2));
     static thread_local std::vector<int32_t> others;
     others.clear();
@@ -1424,6 +1430,7 @@ pb_status issue_trial(pb_ctx* c, int B, int T, bool replay) {
         bs[i]->capture = c->capturing;
     }
     build_items(I);
+    if (!replay && c->file) c->file->start(c->copies, static_cast<const char*>(c->host_base));
     if (!replay && c->rank == 0) {   // prompt tokens first on the copy lane: they land in microseconds
         CU(cudaMemcpyAsync(c->ws + c->L.tokens, c->h_tokens, sizeof(int32_t) * B * T, cudaMemcpyHostToDevice, c->h2d[0]));
         CU(cudaEventRecord(c->tok_ev, c->h2d[0]));
@@ -1437,7 +1444,11 @@ pb_status issue_trial(pb_ctx* c, int B, int T, bool replay) {
     auto last_report = std::chrono::steady_clock::now();
     while (gi < G || ri < R || ii < I.items.size()) {
         bool progressed = false;
-        while (gi < G && I.h2d.can(2) && I.merge.can(group_merge_ops(I, gi))) {
+        if (c->file && !replay) c->file->reclaim();
+        auto staged = [&](size_t k) {   // f4: a file-backed group can go once the reader has filled its slot
+            return !c->copies[k].from_file || c->file->ready((int64_t)k) || c->file->read_error.load();
+        };
+        while (gi < G && staged(gi) && I.h2d.can(2) && I.merge.can(group_merge_ops(I, gi))) {
             pb_status st = issue_group(I, gi++);
             if (st) return st;
             progressed = true;

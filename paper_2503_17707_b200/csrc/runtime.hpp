@@ -8,6 +8,9 @@
 
 #include "kernels.hpp"
 #include "plan.hpp"
+#include "storage.hpp"
+
+#include <memory>
 
 namespace pb {
 
@@ -46,6 +49,7 @@ struct CopyGroup {
     char* dst;
     int64_t bytes;
     int32_t first, count;   // range in the rank's load list
+    bool from_file = false; // f4: staged from the checkpoint file (pb_ctx_set_file_source)
 };
 
 struct LayerMaps {
@@ -98,6 +102,7 @@ struct pb_ctx {
     int32_t n_held_src = 0;              // re-plan: chunks this rank holds and other ranks receive from it
 
     std::vector<pb::CopyGroup> copies;
+    std::unique_ptr<pb::FileSource> file;   // f4: checkpoint file reader (null: pinned host image)
     std::vector<int32_t> landed_alias;   // chunk -> first chunk of its copy group (owner of the landed event)
 
     // merges: per chunk, indices into jobs
