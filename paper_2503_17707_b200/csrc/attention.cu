@@ -10,9 +10,9 @@
 //   S = Q K_j^T            tcgen05.mma M128 N128, K = hd, fp32 accumulator in TMEM columns [0, 128)
 //   P = exp2(S*c - m)      softmax threads: tcgen05.ld the row, mask j > t, running max with lazy rescale
 //                          (O and l are rescaled only when the max grows by more than 2^8, FA4-style), P rounded
-//                          to bf16 into shared memory in the 128B-swizzled K-major layout the MMA reads
-//   O += P V_j             tcgen05.mma M128 N=hd, K = 128 keys, V read MN-major straight from its TMA tile,
-//                          fp32 accumulator in TMEM columns [128, 128 + hd)
+//                          to bf16 pairs and stored back into TMEM (tcgen05.st) — no shared-memory round trip
+//   O += P V_j             tcgen05.mma M128 N=hd, K = 128 keys, A = P read from TMEM, V read MN-major straight
+//                          from its TMA tile, fp32 accumulator in TMEM columns [128, 128 + hd)
 //   out = bf16(O / l)      l = sum of the bf16-rounded P actually multiplied
 // K and V are double-buffered (K_{j+2} streams in while softmax j runs); S_{j+1} overlaps softmax j and PV_j. Q/K/V come through one
 // 3-D tensor map over the token-major qkv rows (col, sequence b, position t) whose t extent is t1, so keys
@@ -36,10 +36,18 @@ constexpr int QT = 128, KT = 128;
 constexpr int kAtom = 128 * 128;       // one 128-row x 64-col bf16 SW128 box = 16 KB
 constexpr float kRescale = 8.0f;       // lazy rescale threshold (log2 domain)
 
+__device__ __forceinline__ float fast_exp2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 template <int HD>
 struct AttnSmem {
-    static constexpr int kQ = HD / 64 * kAtom, kK = kQ, kV = kQ, kP = 2 * kAtom;   // K and V double-buffered
-    static constexpr int offQ = 0, offK = offQ + kQ, offV = offK + 2 * kK, offP = offV + 2 * kV, offBar = offP + kP;
+    static constexpr int kQ = HD / 64 * kAtom, kK = kQ, kV = kQ;   // K and V double-buffered; P lives in TMEM
+    static constexpr int offQ = 0, offK = offQ + kQ, offV = offK + 2 * kK, offBar = offV + 2 * kV;
+    // TMEM: S [0, 128) fp32, O [128, 128 + HD) fp32, P [128 + HD, 192 + HD) bf16 pairs (A operand of PV)
+    static constexpr uint32_t kTmemCols = HD == 64 ? 256 : 512;
     static constexpr int kTotal = offBar + 128 + 1024;
 };
 
@@ -50,7 +58,7 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
     using SM = AttnSmem<HD>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t *sQ = smem + SM::offQ, *sK = smem + SM::offK, *sV = smem + SM::offV, *sP = smem + SM::offP;
+    uint8_t *sQ = smem + SM::offQ, *sK = smem + SM::offK, *sV = smem + SM::offV;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::offBar);
     uint64_t *q_full = bars, *k_full = bars + 1 /* [2] */, *v_full = bars + 3 /* [2] */, *s_full = bars + 5,
              *s_free = bars + 6, *p_full = bars + 7, *o_full = bars + 8;
@@ -81,12 +89,12 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
         mbar_init(o_full, 1);
         fence_mbar_init();
     }
-    if (warp == 0) tmem_alloc<256>(tmem_slot);
+    if (warp == 0) tmem_alloc<SM::kTmemCols>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t tS = tmem, tO = tmem + 128;
+    const uint32_t tS = tmem, tO = tmem + 128, tP = tmem + 128 + HD;
     pdl_wait();   // q/k/v are the previous kernel's output
 
     if (warp == 4) {
@@ -147,11 +155,10 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
                 const uint32_t vbase = smem_u32(sV + (j & 1) * SM::kV);
 #pragma unroll
                 for (int kk = 0; kk < KT / 16; ++kk) {
-                    const uint64_t ad = smem_desc(smem_u32(sP) + (kk >> 2) * kBox + (kk & 3) * 32, 16, 1024, kSw128);
-                    // V tile [128 keys x hd], hd contiguous (MN-major): 64-col boxes kBox apart (LBO), 8-key groups
-                    // 1024 B apart (SBO); a K slice of 16 keys advances 2048 B.
+                    // A = P from TMEM: 16 keys = 8 packed columns. B = V tile [128 keys x hd], hd contiguous
+                    // (MN-major): 64-col boxes kBox apart (LBO), 8-key groups 1024 B apart (SBO); 16 keys = 2048 B.
                     const uint64_t bd = smem_desc(vbase + kk * 2048, kBox, 1024, kSw128);
-                    umma_bf16(tO, ad, bd, idO, (j > 0 || kk > 0) ? 1u : 0u);
+                    umma_bf16_ts(tO, tP + kk * 8, bd, idO, (j > 0 || kk > 0) ? 1u : 0u);
                 }
                 umma_commit(o_full);
             }
@@ -161,7 +168,7 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
         // ---------------- softmax warps: thread = query row r
         const int r = warp * 32 + lane;
         const int t = q0 + r;
-        const bool row_ok = t < q_hi;
+        const bool row_ok = t < q_hi;   // rows past t1 are computed (never masked, always finite) but not stored
         const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
         float m = -CUDART_INF_F, l = 0.f;
         for (int j = 0; j < n_kv; ++j) {
@@ -175,19 +182,29 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(s_free);
-            // scores in the log2 domain, causal mask (key > t), invalid rows fully masked
+            // causal mask (key > t) only on the tiles that reach past the first query of this query tile; the
+            // max is taken on raw scores and scaled once (scale > 0). Rows past t1 are computed but never stored.
             const int key0 = j * KT;
             float mx = -CUDART_INF_F;
+            if (key0 + KT - 1 > q0) {
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
+                for (int c = 0; c < 4; ++c)
 #pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    const int key = key0 + c * 32 + i;
-                    float v = __uint_as_float(sr[c][i]) * scale_log2;
-                    v = (row_ok && key <= t) ? v : -CUDART_INF_F;
-                    sr[c][i] = __float_as_uint(v);
-                    mx = fmaxf(mx, v);
-                }
+                    for (int i = 0; i < 32; ++i) {
+                        float v = __uint_as_float(sr[c][i]);
+                        if (key0 + c * 32 + i > t) {
+                            v = -CUDART_INF_F;
+                            sr[c][i] = __float_as_uint(v);
+                        }
+                        mx = fmaxf(mx, v);
+                    }
+            } else {
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(sr[c][i]));
+            }
+            mx *= scale_log2;
             // lazy rescale: keep the reference max unless the row max grew by more than 2^8
             const bool grow = mx > m + kRescale;   // false when mx == -inf
             const float m_new = grow ? mx : m;
@@ -211,27 +228,26 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
             }
             l *= alpha;
             m = m_new;
-            // P row -> bf16, 128B-swizzled K-major (16-B chunk u of row r at chunk u ^ (r & 7) of its 64-key box)
+            // P row -> bf16 pairs straight into TMEM (the A operand of the PV MMA): 32 keys -> 16 columns
             float rs = 0.f;
 #pragma unroll
-            for (int u = 0; u < 16; ++u) {
-                uint32_t w[4];
+            for (int cb = 0; cb < 4; ++cb) {
+                uint32_t w[16];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const float s0 = __uint_as_float(sr[u >> 2][(u & 3) * 8 + 2 * e]);
-                    const float s1 = __uint_as_float(sr[u >> 2][(u & 3) * 8 + 2 * e + 1]);
-                    const float p0 = m == -CUDART_INF_F ? 0.f : exp2f(s0 - m);
-                    const float p1 = m == -CUDART_INF_F ? 0.f : exp2f(s1 - m);
+                for (int e = 0; e < 16; ++e) {
+                    const float s0 = __uint_as_float(sr[cb][2 * e]);
+                    const float s1 = __uint_as_float(sr[cb][2 * e + 1]);
+                    const float p0 = fast_exp2(fmaf(s0, scale_log2, -m));   // masked: ex2(-inf) = 0
+                    const float p1 = fast_exp2(fmaf(s1, scale_log2, -m));
                     const __nv_bfloat162 pb = __floats2bfloat162_rn(p0, p1);
                     const float2 pr = __bfloat1622float2(pb);
                     rs += pr.x + pr.y;
                     w[e] = *reinterpret_cast<const uint32_t*>(&pb);
                 }
-                uint8_t* dst = sP + (u >> 3) * kAtom + r * 128 + (((u & 7) ^ (r & 7)) << 4);
-                *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+                tmem_st16(tP + lane_off + cb * 16, w);
             }
+            tmem_wait_st();
             l += rs;
-            fence_proxy_async_smem();   // generic-proxy P writes -> visible to the tensor core
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(p_full);
@@ -264,7 +280,7 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
     if (warp == 0) {
         __syncwarp();
         tc_fence_after();
-        tmem_dealloc<256>(tmem);
+        tmem_dealloc<SM::kTmemCols>(tmem);
     }
 }
 

@@ -18,7 +18,9 @@ def rbits(rng, shape, a):
 
 
 @pytest.mark.parametrize("rows,cols,rank", [(256, 256, 8), (384, 640, 16), (200, 328, 16), (512, 512, 64),
-                                            (128, 1024, 32), (1000, 136, 16), (2048, 2048, 16)])
+                                            (128, 1024, 32), (1000, 136, 16), (2048, 2048, 16),
+                                            # full-size targets: OPT-13B q|k|v|o (C4, r=64), Llama-2-70B q (C5a)
+                                            (5120, 5120, 64), (8192, 8192, 16)])
 def test_merge_within_one_ulp_of_correct_rounding(rows, cols, rank):
     need_gpu()
     rng = np.random.default_rng(rows * 7 + cols + rank)
