@@ -46,10 +46,15 @@ def bench(M, K, N, epi, split, reps=30):
 
 if __name__ == "__main__":
   shapes = [("qkv", 128, 2048, 6144, 0), ("o", 128, 2048, 2048, 1), ("fc1", 128, 2048, 8192, 0), ("fc2", 128, 8192, 2048, 1),
-            ("c4_qkv_M1024", 1024, 5120, 15360, 0), ("c5_fc1_M2048", 2048, 8192, 28672, 2)]
+            ("c4_qkv_M1024", 1024, 5120, 15360, 0), ("c4_o_M1024", 1024, 5120, 5120, 1),
+            ("c4_fc1_M1024", 1024, 5120, 20480, 0), ("c4_fc2_M1024", 1024, 20480, 5120, 1),
+            ("c5_fc1_M2048", 2048, 8192, 28672, 2), ("c3_qkv_M512", 512, 4096, 12288, 0)]
+  import os
+  only_big = os.environ.get("GEMM_BENCH_BIG")
   for name, M, K, N, epi in shapes:
+      if only_big and M <= 128: continue
       res = []
-      for split in ((0, 1, 2, 4, 8) if M <= 256 else (0, 1, 2)):
+      for split in ((0, 1, 2, 4, 8) if M <= 256 else ((0,) if only_big else (0, 1, 2))):
           if split and split > K // 64: continue
           us, gbs, tf = bench(M, K, N, epi, split)
           res.append(f"S={split}: graph {us:6.1f}us {gbs:5.0f}GB/s {tf:5.0f}TF ev {LAST_EV_US:6.1f}us")
