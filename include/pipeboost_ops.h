@@ -64,6 +64,14 @@ PB_API pb_status pb_op_argmax(const float* logits, int32_t B, int32_t V, int32_t
 PB_API pb_status pb_op_embed(const void* E, const void* pos, const int32_t* tok, float* h, int32_t d, int32_t r0,
                              int32_t r1, int32_t B, void* stream);
 
+/* Debug: copy the layer-chain item trace (recorded when PB_CHAIN_TRACE=1 at context creation time) of launch
+ * slots [0, n_slots) to HOST memory `out` (n_slots * 1024 items * 8 uint64: claim, dependency met, accumulator
+ * ready, published (bit 63 = this split finished the tile), arrival counted, smid << 48 | job << 40 | item-in-job,
+ * first staged partial landed, reduction done; globaltimer ns), followed by the same shape of per-chunk stamps of
+ * finishing epilogues (chunk k: [2k] partials staged, [2k+1] chunk done). `out` holds 2 * n_slots * 1024 * 8.
+ * n_slots <= 64. */
+PB_API pb_status pb_op_chain_trace(uint64_t* out, int32_t n_slots);
+
 #ifdef __cplusplus
 }
 #endif

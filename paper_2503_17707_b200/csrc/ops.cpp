@@ -122,3 +122,8 @@ extern "C" pb_status pb_op_embed(const void* E, const void* pos, const int32_t* 
                                     (cudaStream_t)stream),
                        "embed");
 }
+
+extern "C" pb_status pb_op_chain_trace(uint64_t* out, int32_t n_slots) {
+    if (!out || n_slots < 1 || n_slots > 64) return fail(PB_EINVAL, "pb_op_chain_trace: bad arguments");
+    return cuda_status(chain_trace_copy(reinterpret_cast<unsigned long long*>(out), n_slots), "chain trace");
+}

@@ -7,6 +7,7 @@
 #include <math_constants.h>
 
 #include "kernels.hpp"
+#include "rownorm.cuh"
 #include "sm100.cuh"
 
 namespace pb {
@@ -43,6 +44,7 @@ __global__ void __launch_bounds__(NT) norm_kernel(const float* __restrict__ h, i
                                                   int ldo, int d, const __nv_bfloat16* __restrict__ gamma,
                                                   const __nv_bfloat16* __restrict__ beta, float eps, const int* dyn,
                                                   int dyn_in, int dyn_out) {
+    static_assert(NT == rownorm::kVT, "one thread per rownorm virtual thread");
     pdl_launch_dependents();   // a PDL-launched GEMM may start its weight prefetch
     pdl_wait();                // PDL-launched: the previous kernel's output is visible from here on
     __shared__ float red[32];
@@ -53,34 +55,39 @@ __global__ void __launch_bounds__(NT) norm_kernel(const float* __restrict__ h, i
         orow += t * dyn_out;
     }
     const float* x = h + row * (long long)ldh;
+    // rownorm.cuh arithmetic (bit-identical to the layer chain's norm items): thread t = virtual thread t
     float v[PER];
     float s = 0.f;
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
         const int c = threadIdx.x + i * NT;
         v[i] = c < d ? x[c] : 0.f;
-        s += v[i];
+        if (c < d) s = rownorm::acc_sum(s, v[i]);
     }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     float mean = 0.f;
-    if (beta) mean = block_sum<NT>(s, red) / d;
+    if (beta) {
+        s = rownorm::warp_sum(s);
+        if (l == 0) red[w] = s;
+        __syncthreads();
+        mean = rownorm::mean_of(rownorm::combine8(red, l), d);
+        __syncthreads();
+    }
     float q = 0.f;
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
         const int c = threadIdx.x + i * NT;
-        const float t = c < d ? v[i] - mean : 0.f;
-        q += t * t;
+        if (c < d) q = rownorm::acc_sq(q, v[i], mean);
     }
-    const float var = block_sum<NT>(q, red) / d;
-    const float rstd = rsqrtf(var + eps);
+    q = rownorm::warp_sum(q);
+    if (l == 0) red[w] = q;
+    __syncthreads();
+    const float rstd = rownorm::rstd_of(rownorm::combine8(red, l), d, eps);
     __nv_bfloat16* o = out + orow * (long long)ldo;
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
         const int c = threadIdx.x + i * NT;
-        if (c < d) {
-            float y = (v[i] - mean) * rstd * __bfloat162float(gamma[c]);
-            if (beta) y += __bfloat162float(beta[c]);
-            o[c] = __float2bfloat16_rn(y);
-        }
+        if (c < d) o[c] = rownorm::out(v[i], mean, rstd, gamma, beta, c);
     }
 }
 

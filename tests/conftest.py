@@ -13,3 +13,6 @@ def pytest_configure(config):
 # Several logical ranks share one GPU in the multi-rank tests; every rank has 5 streams and some of
 # them block on device-side readiness waits, so give each stream its own hardware queue.
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+# A cross-rank wait that never resolves fails the test with the runtime's report (which streams are busy, which
+# readiness words are below the epoch) instead of hanging the suite.
+os.environ.setdefault("PB_WAIT_TIMEOUT_S", "120")
