@@ -96,6 +96,35 @@ constexpr uint32_t kMagic = 0x50424950;  // "PBIP"
 
 }  // namespace
 
+// Process-wide pool of idle ctx-owned streams per device. CUDA maps streams onto CUDA_DEVICE_MAX_CONNECTIONS
+// hardware queues round-robin in creation order, so a process that keeps creating contexts (tests, several
+// logical ranks on one GPU) eventually puts two ranks' streams on one queue, where a device-side readiness wait
+// can block the very work that satisfies it. Reusing handles keeps the set of queues fixed.
+namespace {
+std::mutex g_stream_mu;
+std::vector<std::pair<int, cudaStream_t>> g_stream_pool;
+cudaError_t stream_take(int dev, cudaStream_t* s) {
+    {
+        std::lock_guard<std::mutex> lk(g_stream_mu);
+        for (size_t i = 0; i < g_stream_pool.size(); ++i)
+            if (g_stream_pool[i].first == dev) {
+                *s = g_stream_pool[i].second;
+                g_stream_pool.erase(g_stream_pool.begin() + (long)i);
+                return cudaSuccess;
+            }
+    }
+    return cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
+}
+void stream_give(int dev, cudaStream_t s) {
+    if (cudaStreamQuery(s) != cudaSuccess) {   // still busy (a failed trial): never hand it to another ctx
+        cudaStreamDestroy(s);
+        return;
+    }
+    std::lock_guard<std::mutex> lk(g_stream_mu);
+    g_stream_pool.emplace_back(dev, s);
+}
+}  // namespace
+
 WsLayout pb::ws_layout(const pb_plan* p, int32_t batch, int32_t seq) {
     WsLayout L;
     const auto& m = p->model;
@@ -354,7 +383,7 @@ extern "C" pb_status pb_ctx_create(const pb_plan* plan, int32_t rank, const void
     cudaStream_t* mine[5] = {&c->h2d[0], &c->h2d[1], &c->merge, &c->nv, &c->comp};
     for (auto* sp : mine)
         if (!*sp) {
-            if (cudaStreamCreateWithFlags(sp, cudaStreamNonBlocking) != cudaSuccess) {
+            if (stream_take(c->device, sp) != cudaSuccess) {
                 for (auto* q : mine)
                     if (*q && q != sp) { /* owned ones are released by pb_ctx_free below */ }
                 return fail(PB_ECUDA, "cudaStreamCreateWithFlags failed");
@@ -446,7 +475,7 @@ extern "C" void pb_ctx_free(pb_ctx* c) {
     auto d = [](cudaEvent_t e) { if (e) cudaEventDestroy(e); };
     d(c->t0); d(c->merge_done); d(c->gather_done); d(c->done); d(c->ready_merge); d(c->ready_recv); d(c->tok_ev);
     for (auto e : c->budget_events) d(e);
-    for (auto st : c->owned_streams) cudaStreamDestroy(st);
+    for (auto st : c->owned_streams) stream_give(c->device, st);
     for (auto e : c->landed) d(e);
     for (auto e : c->gathered) d(e);
     for (auto& r : c->prof) { d(r.a); d(r.b); }
