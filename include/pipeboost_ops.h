@@ -27,7 +27,8 @@ PB_API pb_status pb_op_merge(void* W, int64_t ldw, int32_t rows, int32_t cols, c
  * epi 0: out bf16 [*, ldo] = (X W^T + bias) * (col < scale_cols ? scale : 1), ReLU if relu;
  * epi 1: out fp32 [*, ldo] += X W^T + bias;
  * epi 2: W = [gate; up] with N = d_ffn outputs: out bf16 = silu(X gate^T) * (X up^T).
- * K % 64 == 0. bias may be NULL. */
+ * K % 64 == 0. bias may be NULL. m_end - m_begin <= 2 (f3 decode sizes): the weight-streaming GEMV (CUDA cores,
+ * fixed-order fp32 sums); otherwise the tcgen05 kernels. */
 PB_API pb_status pb_op_gemm(const void* X, int32_t x_rows, int32_t m_begin, int32_t m_end, int32_t K, const void* W,
                             int32_t n_rows, int32_t N, int32_t epi, const void* bias, int32_t relu, float scale,
                             int32_t scale_cols, void* out, int32_t ldo, void* stream);

@@ -20,6 +20,7 @@
 // S is chosen from (N, K) only — never from M — so a prompt split into chunks gives bit-identical results.
 #include <cuda_bf16.h>
 
+
 #include "kernels.hpp"
 #include "sm100.cuh"
 
@@ -540,6 +541,160 @@ cudaError_t launch_big(const CUtensorMap& mapX, const CUtensorMap& mapW, const G
     return launch_pdl(gemm_big_kernel<EPI>, dim3(grid), dim3(192), kBigSmem, s, a.pdl != 0, mapX, mapW, a);
 }
 
+// ------------------------------------------------------------------------------------------------------------
+// Weight-streaming GEMV for M <= 2 rows (f3 decode steps; tiny prompts). At M = 1 or 2 a projection is a pure
+// weight stream (intensity <= 2 flop/B), the tensor core's 128-row tile would be >= 98 % padding, and the split-K
+// cluster kernel's fixed latency (TMEM, cluster barriers, DSMEM reduction) dominates. Here a CTA of 8 warps owns
+// 4 weight rows (EPI_SILU_MUL: 2 gate + the 2 matching up rows -> 2 outputs) and splits K across its warps;
+// every lane streams 16-B weight vectors with no L1 allocation (ld.global.nc.L1::no_allocate), the M activation
+// rows come through L1, fp32 FMAs in a fixed order, a butterfly per warp and the 8 warp sums added in order 0..7
+// — deterministic, independent of which rows a launch covers. The first weight vectors are loaded before the
+// programmatic-dependency wait (weights never depend on the previous kernel).
+constexpr int GV_ROWS = 4, GV_WARPS = 8, GV_UNROLL = 2;
+
+__device__ __forceinline__ uint4 ld_stream16(const void* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void bf16x8_to_f32(const uint4& v, float (&f)[8]) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        f[2 * i] = __uint_as_float(w[i] << 16);
+        f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    }
+}
+
+template <int EPI, int MR>
+__global__ void __launch_bounds__(GV_WARPS * 32) gemv_kernel(const GemmArgs a) {
+    __shared__ float red[GV_WARPS][GV_ROWS][MR];
+    pdl_launch_dependents();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int M = a.M_end - a.M_begin;
+    // weight rows of this CTA; out-of-range rows read row 0 and are never stored
+    int wrow[GV_ROWS];
+    bool wok[GV_ROWS];
+#pragma unroll
+    for (int r = 0; r < GV_ROWS; ++r) {
+        int n;
+        if (EPI == EPI_SILU_MUL) {
+            const int o = blockIdx.x * 2 + (r & 1);
+            wok[r] = o < a.N;
+            n = r < 2 ? o : a.up_row0 + o;
+        } else {
+            n = blockIdx.x * GV_ROWS + r;
+            wok[r] = n < a.N;
+        }
+        wrow[r] = wok[r] ? n : 0;
+    }
+    // K range of this warp, in 8-element vectors: vectors [v0, v1) of every row
+    const int nvec = a.K / 8;
+    const int per_w = (nvec + GV_WARPS - 1) / GV_WARPS;
+    const int v0 = warp * per_w, v1 = min(nvec, v0 + per_w);
+    float acc[GV_ROWS][MR];
+#pragma unroll
+    for (int r = 0; r < GV_ROWS; ++r)
+#pragma unroll
+        for (int m = 0; m < MR; ++m) acc[r][m] = 0.f;
+    const int step = 32 * GV_UNROLL;
+    int vb = v0;
+    // first batch of weight vectors before the dependency wait
+    uint4 wv[GV_UNROLL][GV_ROWS];
+    auto load_w = [&](int base) {
+#pragma unroll
+        for (int u = 0; u < GV_UNROLL; ++u) {
+            const int v = base + u * 32 + lane;
+#pragma unroll
+            for (int r = 0; r < GV_ROWS; ++r)
+                wv[u][r] = v < v1 ? ld_stream16(a.W + (size_t)wrow[r] * a.K + (size_t)v * 8) : make_uint4(0, 0, 0, 0);
+        }
+    };
+    if (vb < v1) load_w(vb);
+    pdl_wait();
+    const int m_shift = a.m_dyn ? *a.m_dyn * a.m_dyn_mul : 0;
+    const int m0 = a.M_begin + m_shift;
+    for (; vb < v1; vb += step) {
+        if (vb != v0) load_w(vb);   // the first batch was requested before the dependency wait
+#pragma unroll
+        for (int u = 0; u < GV_UNROLL; ++u) {
+            const int v = vb + u * 32 + lane;
+            if (v >= v1) break;
+            float wf[GV_ROWS][8];
+#pragma unroll
+            for (int r = 0; r < GV_ROWS; ++r) bf16x8_to_f32(wv[u][r], wf[r]);
+            uint4 xv[MR];
+#pragma unroll
+            for (int m = 0; m < MR; ++m)
+                if (m < M) xv[m] = __ldg(reinterpret_cast<const uint4*>(a.X + (size_t)(m0 + m) * a.ldx) + v);
+#pragma unroll
+            for (int m = 0; m < MR; ++m) {
+                if (m >= M) break;
+                float xf[8];
+                bf16x8_to_f32(xv[m], xf);
+#pragma unroll
+                for (int r = 0; r < GV_ROWS; ++r)
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) acc[r][m] = __fmaf_rn(wf[r][e], xf[e], acc[r][m]);
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < GV_ROWS; ++r)
+#pragma unroll
+        for (int m = 0; m < MR; ++m) {
+            float v = acc[r][m];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) red[warp][r][m] = v;
+        }
+    __syncthreads();
+    // epilogue: one thread per (output, row)
+    const int outs = EPI == EPI_SILU_MUL ? 2 : GV_ROWS;
+    const int t = threadIdx.x;
+    if (t >= outs * M) return;
+    const int r = t % outs, m = t / outs;
+    auto total = [&](int rr) {
+        float v = red[0][rr][m];
+#pragma unroll
+        for (int w = 1; w < GV_WARPS; ++w) v += red[w][rr][m];
+        return v;
+    };
+    const int row = m0 + m;
+    if (EPI == EPI_SILU_MUL) {
+        if (!wok[r]) return;
+        const int n = blockIdx.x * 2 + r;
+        reinterpret_cast<__nv_bfloat16*>(a.out)[(size_t)row * a.ldo + n] =
+            __float2bfloat16_rn(silu(total(r)) * total(r + 2));
+        return;
+    }
+    if (!wok[r]) return;
+    const int n = wrow[r];
+    float v = total(r);
+    if (a.bias) v += __bfloat162float(a.bias[n]);
+    if (EPI == EPI_BF16) {
+        if (n < a.scale_cols) v *= a.scale;
+        if (a.relu) v = fmaxf(v, 0.0f);
+        reinterpret_cast<__nv_bfloat16*>(a.out)[(size_t)row * a.ldo + n] = __float2bfloat16_rn(v);
+    } else {
+        float* h = reinterpret_cast<float*>(a.out) + (size_t)row * a.ldo + n;
+        *h += v;
+    }
+}
+
+template <int EPI>
+cudaError_t launch_gemv_epi(const GemmArgs& a, cudaStream_t s) {
+    const int M = a.M_end - a.M_begin;
+    const int per = EPI == EPI_SILU_MUL ? 2 : GV_ROWS;
+    const dim3 grid((a.N + per - 1) / per);
+    const bool pdl = a.pdl != 0;
+    static_assert(kGemvAutoRows <= 2, "instantiate gemv_kernel for more rows");
+    if (M <= 1) return launch_pdl(gemv_kernel<EPI, 1>, grid, dim3(GV_WARPS * 32), 0, s, pdl, a);
+    return launch_pdl(gemv_kernel<EPI, 2>, grid, dim3(GV_WARPS * 32), 0, s, pdl, a);
+}
+
 }  // namespace
 
 
@@ -568,7 +723,10 @@ cudaError_t warm_gemm_kernels() {
                          (const void*)gemm_kernel<EPI_SILU_MUL, 1>, (const void*)gemm_kernel<EPI_SILU_MUL, 2>,
                          (const void*)gemm_kernel<EPI_SILU_MUL, 4>, (const void*)gemm_kernel<EPI_SILU_MUL, 8>,
                          (const void*)gemm_big_kernel<EPI_BF16>,     (const void*)gemm_big_kernel<EPI_RESID>,
-                         (const void*)gemm_big_kernel<EPI_SILU_MUL>};
+                         (const void*)gemm_big_kernel<EPI_SILU_MUL>,
+                         (const void*)gemv_kernel<EPI_BF16, 1>,  (const void*)gemv_kernel<EPI_BF16, 2>,
+                         (const void*)gemv_kernel<EPI_RESID, 1>, (const void*)gemv_kernel<EPI_RESID, 2>,
+                         (const void*)gemv_kernel<EPI_SILU_MUL, 1>, (const void*)gemv_kernel<EPI_SILU_MUL, 2>};
     for (const void* f : fns) {
         cudaError_t e = cudaFuncGetAttributes(&at, f);
         if (e != cudaSuccess) return e;
@@ -579,6 +737,17 @@ cudaError_t warm_gemm_kernels() {
 cudaError_t launch_gemm(const CUtensorMap& mapX, const CUtensorMap& mapW, const GemmArgs& a, cudaStream_t s) {
     if (a.M_end <= a.M_begin || a.N <= 0) return cudaSuccess;
     if (a.K <= 0 || a.K % 8) return cudaErrorInvalidValue;
+    // M_total <= 8 (a decode step or a tiny prompt; chosen from the whole batch, so chunks agree): weight-streaming GEMV
+    // Measured on B200, C2 decode ms/step GEMV vs tensor-core path: B=1 1.07 vs 1.46, B=2 1.56 vs 1.56, B=4 1.95 vs
+    // 1.73 (the GEMV's fp32 FMA work grows with M and its registers with it), hence M_total <= kGemvAutoRows.
+    if (a.X && a.W && a.split_k <= 0 && a.M_total >= 1 && a.M_total <= kGemvAutoRows &&
+        a.M_end - a.M_begin <= kGemvAutoRows) {
+        switch (a.epi) {
+            case EPI_BF16: return launch_gemv_epi<EPI_BF16>(a, s);
+            case EPI_RESID: return launch_gemv_epi<EPI_RESID>(a, s);
+            case EPI_SILU_MUL: return launch_gemv_epi<EPI_SILU_MUL>(a, s);
+        }
+    }
     const int S = a.split_k > 0 ? a.split_k : gemm_split_k(a.N, a.K, a.epi, a.M_total);
     // The kernel is chosen from the WHOLE prompt (M_total), never from the rows of this launch, so a prompt split
     // into chunks runs every output through the same kernel and the same summation order.

@@ -104,7 +104,13 @@ struct GemmArgs {
     int m_dyn_mul;
     int M_total;                // rows of the whole prompt batch (picks split_k; chunk-invariant), 0 = M_end-M_begin
     int pdl;                    // 1: programmatic dependent launch after the stream's previous kernel
+    // plain pointers for the weight-streaming GEMV (M_total <= kGemvAutoRows: decode steps, tiny prompts);
+    // null = tensor-core kernels only
+    const __nv_bfloat16* X;     // [*, ldx] (rows as for mapX)
+    int ldx;
+    const __nv_bfloat16* W;     // [rows x K] row-major (rows as for mapW)
 };
+constexpr int kGemvAutoRows = 2;   // rows up to which launch_gemm picks the GEMV
 int gemm_split_k(int N, int K, int epi, int M_total);
 // Maps: X box {64, 128} SW128 over [max_rows x K]; W box {64, 128} (EPI_SILU_MUL: {64, 64}) SW128 over [rows x K].
 cudaError_t launch_gemm(const CUtensorMap& mapX, const CUtensorMap& mapW, const GemmArgs& a, cudaStream_t s);

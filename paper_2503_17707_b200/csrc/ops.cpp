@@ -63,6 +63,9 @@ extern "C" pb_status pb_op_gemm_split(const void* X, int32_t x_rows, int32_t m_b
     a.up_row0 = N;
     a.split_k = split_k;
     a.M_total = m_end - m_begin;
+    a.X = static_cast<const __nv_bfloat16*>(X);   // M <= 8 with split_k == 0: the weight-streaming GEMV
+    a.ldx = K;
+    a.W = static_cast<const __nv_bfloat16*>(W);
     return cuda_status(launch_gemm(mx, mw, a, (cudaStream_t)stream), "gemm");
 }
 

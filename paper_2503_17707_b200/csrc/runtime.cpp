@@ -310,6 +310,7 @@ static pb_status build_prefill_maps(pb_ctx* c) {
                 const uint32_t box_rows = (i == 2 && !opt) ? 64 : 128;   // [gate; up] is read as 64 + 64 rows
                 if (!make_map_bf16(maps[i], base, t.rows, t.cols, t.cols, box_rows, 64, 128, err, sizeof err))
                     return fail(PB_EINVAL, "weight map layer %d: %s", l, err);
+                lm.w[i] = reinterpret_cast<const __nv_bfloat16*>(base);
             }
         }
     }
@@ -827,7 +828,11 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, boo
         return a;
     };
     // Algorithmic work of a GEMM launch: 2MNK flops; bytes = X + W + output (fp32 residual read + write).
-    auto gemm = [&](const CUtensorMap& mx, const CUtensorMap& mw, const GemmArgs& a, int n_w_rows) -> cudaError_t {
+    auto gemm = [&](const CUtensorMap& mx, const CUtensorMap& mw, GemmArgs a, int n_w_rows, const __nv_bfloat16* X,
+                    int ldx, const __nv_bfloat16* W) -> cudaError_t {
+        a.X = X;
+        a.ldx = ldx;
+        a.W = W;
         const int pi = prof_begin(c, K_GEMM, s);
         cudaError_t e = launch_gemm(mx, mw, a, s);
         const double M = rows, N = a.N, K = a.K;
@@ -849,7 +854,7 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, boo
     CU(need(opt ? "qkv_b" : "qkv"));
     GemmArgs a = G(r0, qdim, d, EPI_BF16, opt ? wt(c, l, "qkv_b") : nullptr, 0, opt ? 1.0f / sqrtf((float)hd) : 1.0f,
                    opt ? d : 0, qkv, qdim);
-    CU(gemm(c->map_x, lm.qkv, a, qdim));
+    CU(gemm(c->map_x, lm.qkv, a, qdim, x, d, lm.w[0]));
     if (!opt) {
         const int pi = prof_begin(c, K_ROPE, s);
         CU(launch_rope(qkv + (size_t)row_base * qdim, qdim, r0 - row_base, r1 - row_base, B, H, KVH, hd, qd,
@@ -931,24 +936,24 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, boo
     }
     CU(need(opt ? "o_b" : "o"));
     a = G(r0, d, qd, EPI_RESID, opt ? wt(c, l, "o_b") : nullptr, 0, 1.f, 0, h, d);
-    CU(gemm(c->map_attn, lm.o, a, d));
+    CU(gemm(c->map_attn, lm.o, a, d, attn, qd, lm.w[1]));
     // --- MLP block
     CU(need(opt ? "ln2_b" : "ln2_g"));
     CU(norm("ln2_g", "ln2_b"));
     if (opt) {
         CU(need("fc1_b"));
         a = G(r0, f, d, EPI_BF16, wt(c, l, "fc1_b"), 1, 1.f, 0, mlp, f);
-        CU(gemm(c->map_x, lm.up, a, f));
+        CU(gemm(c->map_x, lm.up, a, f, x, d, lm.w[2]));
         CU(need("fc2_b"));
         a = G(r0, d, f, EPI_RESID, wt(c, l, "fc2_b"), 0, 1.f, 0, h, d);
-        CU(gemm(c->map_mlp, lm.down, a, d));
+        CU(gemm(c->map_mlp, lm.down, a, d, mlp, f, lm.w[3]));
     } else {
         CU(need("gate_up"));
         a = G(r0, f, d, EPI_SILU_MUL, nullptr, 0, 1.f, 0, mlp, f);
-        CU(gemm(c->map_x, lm.up, a, 2 * f));
+        CU(gemm(c->map_x, lm.up, a, 2 * f, x, d, lm.w[2]));
         CU(need("down"));
         a = G(r0, d, f, EPI_RESID, nullptr, 0, 1.f, 0, h, d);
-        CU(gemm(c->map_mlp, lm.down, a, d));
+        CU(gemm(c->map_mlp, lm.down, a, d, mlp, f, lm.w[3]));
     }
     c->n_launches += opt ? 7 : 8;
     return PB_OK;

@@ -72,7 +72,9 @@ def _gemm_case(rng, M, K, N):
 @pytest.mark.parametrize("M,K,N,m0,m1", [(128, 256, 768, 0, 128), (16, 256, 1024, 0, 16), (300, 512, 384, 0, 300),
                                          (256, 2048, 640, 128, 256), (200, 192, 136, 40, 170), (130, 688, 256, 0, 130),
                                          (1024, 1024, 3072, 0, 1024), (2048, 512, 8192, 0, 2000),
-                                         (700, 1536, 1000, 100, 700)])
+                                         (700, 1536, 1000, 100, 700),
+                                         # M <= 2: the weight-streaming GEMV (decode sizes), ragged N and K
+                                         (1, 2048, 640, 0, 1), (2, 512, 136, 0, 2), (3, 688, 258, 1, 3)])
 def test_gemm_bf16_epilogue(M, K, N, m0, m1):
     need_gpu()
     rng = np.random.default_rng(M + K + N)
@@ -91,10 +93,11 @@ def test_gemm_bf16_epilogue(M, K, N, m0, m1):
     assert np.all(err <= bf16_ulp(r) + 1e-6 * np.abs(r).max()), err.max()
 
 
-@pytest.mark.parametrize("M,K,N,f", [(192, 320, 256, 136), (1536, 1024, 2560, 2752)])
+@pytest.mark.parametrize("M,K,N,f", [(192, 320, 256, 136), (1536, 1024, 2560, 2752), (2, 320, 256, 136),
+                                     (1, 2048, 512, 330)])
 def test_gemm_relu_and_resid_and_silu(M, K, N, f):
     """Small shapes take the split-K kernel or the persistent 128x256 kernel at S = 1; the second case runs the
-    persistent kernel over more tiles than SMs (both TMEM accumulators cycle)."""
+    persistent kernel over more tiles than SMs (both TMEM accumulators cycle); M <= 2 takes the GEMV."""
     need_gpu()
     rng = np.random.default_rng(11 + M)
     X, W, bias = _gemm_case(rng, M, K, N)
