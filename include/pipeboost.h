@@ -260,7 +260,7 @@ PB_API pb_status pb_gather_layers(pb_ctx* ctx);
  * and optionally the fp32 logits (host [batch][vocab] or NULL).
  * pb_prefill_enqueue only enqueues; pb_prefill_wait blocks until this rank's work
  * (and on rank 0 the token D2H) is complete; pb_prefill_first_token = both.
- * Errors: PB_EINVAL (batch/seq out of range), PB_EPROTOCOL, PB_ECUDA, PB_ENUMERIC. */
+ * Errors: PB_EINVAL (batch/seq out of range, a token outside [0, vocab)), PB_EPROTOCOL, PB_ECUDA, PB_ENUMERIC. */
 PB_API pb_status pb_prefill_enqueue(pb_ctx* ctx, const int32_t* tokens, int32_t batch, int32_t seq);
 /* Same, with the adapter of every sequence (host [batch], read on every rank; needs PB_MERGE_ALL). The batch
  * then runs as `batch` single-sequence pipeline microbatches, each reading its adapter's merged copies. */

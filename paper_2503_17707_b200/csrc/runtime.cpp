@@ -1619,6 +1619,12 @@ pb_status start_issuer(pb_ctx* c, const int32_t* tokens, const int32_t* adapter_
     if (B < 1 || T < 1 || B > c->L.max_batch || T > c->L.max_seq || (int64_t)B * T > c->L.max_rows)
         return fail(PB_EINVAL, "batch %d x seq %d exceeds the workspace (%d x %d)", B, T, c->L.max_batch, c->L.max_seq);
     if ((c->rank == 0 || c->replica) && !tokens) return fail(PB_EINVAL, "rank 0 (every rank of a replica) needs tokens");
+    if (tokens) {
+        const int32_t V = c->plan->model.vocab;
+        for (int64_t i = 0; i < (int64_t)B * T; ++i)
+            if (tokens[i] < 0 || tokens[i] >= V)
+                return fail(PB_EINVAL, "token %d at [%lld] outside the vocabulary [0, %d)", tokens[i], (long long)i, V);
+    }
     const bool mb = c->merge_adapter == PB_MERGE_ALL;
     if (!replay) {
         c->seq_adapter.assign(B, -1);
@@ -1691,6 +1697,10 @@ extern "C" pb_status pb_prefill_replay(pb_ctx* c, uint32_t epoch, const int32_t*
         if (B < 1 || T < 1 || B > c->L.max_batch || T > c->L.max_seq || (int64_t)B * T > c->L.max_rows)
             return fail(PB_EINVAL, "batch %d x seq %d exceeds the workspace", B, T);
         if (!tokens) return fail(PB_EINVAL, "rank 0 (every rank of a replica) needs tokens");
+        for (int64_t i = 0; i < (int64_t)B * T; ++i)
+            if (tokens[i] < 0 || tokens[i] >= c->plan->model.vocab)
+                return fail(PB_EINVAL, "token %d at [%lld] outside the vocabulary [0, %d)", tokens[i], (long long)i,
+                            c->plan->model.vocab);
         for (int b = 0; b < B; ++b)
             for (int t = 0; t < T; ++t) c->h_tokens[t * B + b] = tokens[(size_t)b * T + t];
         c->cur_batch = B;

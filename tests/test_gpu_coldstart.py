@@ -321,3 +321,48 @@ def test_f32_path_within_1e4(model):
         for e in engs:
             e.close()
         _LIVE.clear()
+
+
+@pytest.mark.parametrize("model", [TINY_OPT, TINY_LLAMA], ids=["opt", "llama"])
+def test_degenerate_prompts(model):
+    """One-token prompts (M = B rows: the GEMV at B <= 2, the tensor cores above) against the oracle and bit-identical
+    across pipeline depth; the largest batch the workspace takes (8) with the longest prompt it was sized for."""
+    need_gpu()
+    ads = (lora(8),)
+    for B in (1, 2, 8):
+        toks = synth.tokens(B, 1, model.vocab)
+        _, _, (t1, ref), _ = run(model, ads, 1, toks)
+        check_against_oracle(model, ads, toks, ref, t1)
+        _, _, (t2, l2), _ = run(model, ads, 2, toks, policy="interleave", sliced=1, chunk_bytes=64 << 10)
+        assert np.array_equal(l2.view(np.uint32), ref.view(np.uint32)) and np.array_equal(t2, t1), B
+    toks = synth.tokens(8, 24, model.vocab)
+    _, _, (t8, l8), _ = run(model, ads, 1, toks)
+    check_against_oracle(model, ads, toks, l8, t8)
+
+
+def test_invalid_prompts_fail_loudly_and_leave_the_context_usable():
+    """Empty or oversized batches, and token ids outside the vocabulary, are refused with PB_EINVAL before any
+    device work; the next trial on the same context still runs and matches the oracle."""
+    need_gpu()
+    from paper_2503_17707_b200 import _binding as B
+    toks = synth.tokens(1, 16, TINY_OPT.vocab)
+    plan = Plan(TINY_OPT, (lora(8),), 1, chunk_bytes=32 << 20)
+    base, ada = harness.build_host_images(plan)
+    eng = RankEngine(plan, 0, base, ada, max_batch=2, max_seq=16)
+    _LIVE.append(eng)
+    eng.wire_local([eng])
+    bad = [(np.zeros((0, 16), np.int32), 0, 16), (np.zeros((1, 0), np.int32), 1, 0),
+           (np.zeros((3, 16), np.int32), 3, 16), (np.zeros((1, 17), np.int32), 1, 17)]
+    over = toks.copy()
+    over[0, 5] = TINY_OPT.vocab
+    neg = toks.copy()
+    neg[0, 0] = -1
+    bad += [(over, 1, 16), (neg, 1, 16)]
+    for ep, (tk, b, t) in enumerate(bad, start=1):
+        eng.invalidate()
+        with pytest.raises(B.PBError) as ei:
+            eng.enqueue(ep, tk, b, t, adapter_id=0)
+        assert ei.value.status == B.PB_EINVAL, (b, t)
+    eng.invalidate()
+    tokens, logits = eng.cold_start(len(bad) + 1, toks, want_logits=True)
+    check_against_oracle(TINY_OPT, (lora(8),), toks, logits, tokens)
