@@ -36,6 +36,15 @@ constexpr int kStage = kStageA + kStageB;
 constexpr int kBarBytes = 256;
 __host__ __device__ constexpr int smem_bytes(int stages) { return stages * kStage + kBarBytes + 1024; }
 static_assert(BM * BN * 4 <= 2 * kStage, "partial tile must fit in a 2-stage ring");
+// The split-K kernel also runs with 64-column tiles (TBN = 64; bias / residual epilogues) when a projection has so
+// few 128-column tiles that fewer than half the SMs would stream its weights (gemm_tile_n).
+constexpr int kMaxStagesAny = 8;
+template <int TBN> __host__ __device__ constexpr int stage_bytes() { return kStageA + TBN * BK * 2; }
+template <int TBN> __host__ __device__ constexpr int max_stages() { return TBN == 128 ? MAX_STAGES : 8; }
+template <int TBN> __host__ __device__ constexpr int smem_bytes_t(int stages) {
+    return stages * stage_bytes<TBN>() + kBarBytes + 1024;
+}
+static_assert(BM * 64 * 4 <= 2 * (kStageA + 64 * BK * 2), "64-column partial tile must fit in a 2-stage ring");
 
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
 
@@ -61,24 +70,27 @@ __device__ __forceinline__ float4 ld_cluster_f4(uint32_t addr) {
     return v;
 }
 
-// Partial tile: [128 rows][32 float4 chunks], chunk c of row r stored at slot c ^ (r & 31) (conflict-free
-// row-per-thread writes, and conflict-free chunk-per-thread reads).
+// Partial tile: [128 rows][TBN/4 float4 chunks], chunk c of row r stored at slot c ^ (r % (TBN/4)) (row-per-thread
+// writes and chunk-per-thread reads spread over the banks).
+template <int TBN>
 __device__ __forceinline__ uint32_t part_off(int row, int chunk) {
-    return (uint32_t)(row * 512 + ((chunk ^ (row & 31)) << 4));
+    return (uint32_t)(row * (TBN * 4) + ((chunk ^ (row & (TBN / 4 - 1))) << 4));
 }
 
 // S = split-K factor = cluster size along z (compile-time so the S remote loads of the reduction are issued
 // back to back, then summed in the fixed order 0..S-1).
-template <int EPI, int S>
+template <int EPI, int S, int TBN = BN>
 __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CUtensorMap mapX,
                                                       const __grid_constant__ CUtensorMap mapW, const GemmArgs a,
                                                       const int stages) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* ring = smem;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * kStage);
-    uint64_t* empty = full + MAX_STAGES;
-    uint64_t* done = empty + MAX_STAGES;
+    static_assert(TBN == BN || (TBN == 64 && EPI != EPI_SILU_MUL), "64-column tiles: bias / residual epilogues");
+    constexpr int kStageT = stage_bytes<TBN>();
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * kStageT);
+    uint64_t* empty = full + kMaxStagesAny;
+    uint64_t* done = empty + kMaxStagesAny;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -87,7 +99,7 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
     const int m0 = a.M_begin + m_shift + blockIdx.y * BM;
     const int m_end = a.M_end + m_shift;
     // EPI_SILU_MUL: tile = 64 gate columns + the matching 64 up columns -> 64 outputs.
-    const int n_out0 = blockIdx.x * (EPI == EPI_SILU_MUL ? BN / 2 : BN);
+    const int n_out0 = blockIdx.x * (EPI == EPI_SILU_MUL ? BN / 2 : TBN);
     const int nk = (a.K + BK - 1) / BK;            // K tail: TMA zero-fills out-of-bounds columns
     const int kb0 = (int)((long)nk * split / S), kb1 = (int)((long)nk * (split + 1) / S);
     const int my_k = kb1 - kb0;                    // >= 1 (host guarantees S <= nk)
@@ -103,7 +115,7 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
         mbar_init(done, 1);
         fence_mbar_init();
     }
-    if (warp == 0) tmem_alloc<BN>(tmem_slot);
+    if (warp == 0) tmem_alloc<TBN>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -111,7 +123,7 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
 
     auto load_w = [&](int i) {
         const int s = i % stages, kc = (kb0 + i) * BK;
-        uint8_t* sB = ring + s * kStage + kStageA;
+        uint8_t* sB = ring + s * kStageT + kStageA;
         if (EPI == EPI_SILU_MUL) {
             tma_load_2d(sB, &mapW, &full[s], kc, n_out0);
             tma_load_2d(sB + kStageB / 2, &mapW, &full[s], kc, a.up_row0 + n_out0);
@@ -124,26 +136,26 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
         // worth is requested before the programmatic-dependency wait, X (the previous kernel's output) after.
         const int pre = my_k < stages ? my_k : stages;
         for (int i = 0; i < pre; ++i) {
-            mbar_arrive_expect_tx(&full[i], kStage);
+            mbar_arrive_expect_tx(&full[i], kStageT);
             load_w(i);
         }
         pdl_wait();
-        for (int i = 0; i < pre; ++i) tma_load_2d(ring + i * kStage, &mapX, &full[i], (kb0 + i) * BK, m0);
+        for (int i = 0; i < pre; ++i) tma_load_2d(ring + i * kStageT, &mapX, &full[i], (kb0 + i) * BK, m0);
         for (int i = pre; i < my_k; ++i) {
             const int s = i % stages;
             mbar_wait(&empty[s], ((i / stages) - 1) & 1);
-            mbar_arrive_expect_tx(&full[s], kStage);
-            tma_load_2d(ring + s * kStage, &mapX, &full[s], (kb0 + i) * BK, m0);
+            mbar_arrive_expect_tx(&full[s], kStageT);
+            tma_load_2d(ring + s * kStageT, &mapX, &full[s], (kb0 + i) * BK, m0);
             load_w(i);
         }
     } else if (warp == 1 && lane == 0) {
         // ---------------- MMA issuer
-        constexpr uint32_t idesc = idesc_bf16_f32(BM, BN, 0, 0);
+        constexpr uint32_t idesc = idesc_bf16_f32(BM, TBN, 0, 0);
         for (int i = 0; i < my_k; ++i) {
             const int s = i % stages;
             mbar_wait(&full[s], (i / stages) & 1);
             tc_fence_after();
-            const uint32_t a_base = smem_u32(ring + s * kStage), b_base = a_base + kStageA;
+            const uint32_t a_base = smem_u32(ring + s * kStageT), b_base = a_base + kStageA;
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
                 const uint64_t ad = smem_desc(a_base + k * 32, 16, 1024, kSw128);
@@ -166,16 +178,16 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
         const int row = warp * 32 + lane;
         const uint32_t t_row = tmem + ((uint32_t)(warp * 32) << 16);
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
+        for (int half = 0; half < TBN / 64; ++half) {
             uint32_t r0[32], r1[32];
             tmem_ld32_async(t_row + half * 64, r0);
             tmem_ld32_async(t_row + half * 64 + 32, r1);
             tmem_wait_ld();
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-                *reinterpret_cast<uint4*>(smem + part_off(row, half * 16 + q)) =
+                *reinterpret_cast<uint4*>(smem + part_off<TBN>(row, half * 16 + q)) =
                     make_uint4(r0[4 * q], r0[4 * q + 1], r0[4 * q + 2], r0[4 * q + 3]);
-                *reinterpret_cast<uint4*>(smem + part_off(row, half * 16 + 8 + q)) =
+                *reinterpret_cast<uint4*>(smem + part_off<TBN>(row, half * 16 + 8 + q)) =
                     make_uint4(r1[4 * q], r1[4 * q + 1], r1[4 * q + 2], r1[4 * q + 3]);
             }
         }
@@ -187,14 +199,14 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
     // ---------------- reduce rows [r_lo, r_hi) over the S partials (fixed order 0..S-1) + fused epilogue
     const int r_lo = BM * split / S, r_hi = BM * (split + 1) / S;
     const uint32_t base = smem_u32(smem);
-    const int chunks = EPI == EPI_SILU_MUL ? 16 : 32;
+    const int chunks = EPI == EPI_SILU_MUL ? 16 : TBN / 4;
     auto sum_chunk = [&](int r, int c) {
         if constexpr (S == 1) {
-            return *reinterpret_cast<const float4*>(smem + part_off(r, c));
+            return *reinterpret_cast<const float4*>(smem + part_off<TBN>(r, c));
         } else {
             float4 p[S];
 #pragma unroll
-            for (int s2 = 0; s2 < S; ++s2) p[s2] = ld_cluster_f4(map_cluster(base + part_off(r, c), s2));
+            for (int s2 = 0; s2 < S; ++s2) p[s2] = ld_cluster_f4(map_cluster(base + part_off<TBN>(r, c), s2));
             float4 acc = p[0];
 #pragma unroll
             for (int s2 = 1; s2 < S; ++s2) {
@@ -273,19 +285,19 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
     if (warp == 0) {
         __syncwarp();
         tc_fence_after();
-        tmem_dealloc<BN>(tmem);
+        tmem_dealloc<TBN>(tmem);
     }
 }
 
-template <int EPI, int S>
+template <int EPI, int S, int TBN = BN>
 cudaError_t launch_es(const CUtensorMap& mapX, const CUtensorMap& mapW, const GemmArgs& a, cudaStream_t s) {
-    const int per = EPI == EPI_SILU_MUL ? BN / 2 : BN;
+    const int per = EPI == EPI_SILU_MUL ? BN / 2 : TBN;
     const dim3 grid((a.N + per - 1) / per, (a.M_end - a.M_begin + BM - 1) / BM, S);
     // Deep ring when the grid fits one CTA per SM; otherwise 3 stages (96 KB) so two CTAs share an SM.
     const int ctas = grid.x * grid.y * grid.z;
-    const int stages = ctas <= 148 ? MAX_STAGES : 3;
-    const int smem = smem_bytes(stages);
-    cudaError_t e = smem_attr_once<gemm_kernel<EPI, S>>(smem_bytes(MAX_STAGES));
+    const int stages = ctas <= 148 ? max_stages<TBN>() : 3;
+    const int smem = smem_bytes_t<TBN>(stages);
+    cudaError_t e = smem_attr_once<gemm_kernel<EPI, S, TBN>>(smem_bytes_t<TBN>(max_stages<TBN>()));
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
@@ -308,11 +320,22 @@ cudaError_t launch_es(const CUtensorMap& mapX, const CUtensorMap& mapW, const Ge
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    return cudaLaunchKernelEx(&cfg, gemm_kernel<EPI, S>, mapX, mapW, a, stages);
+    return cudaLaunchKernelEx(&cfg, gemm_kernel<EPI, S, TBN>, mapX, mapW, a, stages);
 }
 
 template <int EPI>
-cudaError_t launch_epi(const CUtensorMap& mapX, const CUtensorMap& mapW, const GemmArgs& a, int S, cudaStream_t s) {
+cudaError_t launch_epi(const CUtensorMap& mapX, const CUtensorMap& mapW, const GemmArgs& a, int S, int tbn,
+                       cudaStream_t s) {
+    if constexpr (EPI != EPI_SILU_MUL) {
+        if (tbn == 64) {
+            switch (S) {
+                case 1: return launch_es<EPI, 1, 64>(mapX, *a.mapW64, a, s);
+                case 2: return launch_es<EPI, 2, 64>(mapX, *a.mapW64, a, s);
+                case 4: return launch_es<EPI, 4, 64>(mapX, *a.mapW64, a, s);
+            }
+            return cudaErrorInvalidValue;
+        }
+    }
     switch (S) {
         case 1: return launch_es<EPI, 1>(mapX, mapW, a, s);
         case 2: return launch_es<EPI, 2>(mapX, mapW, a, s);
@@ -704,6 +727,15 @@ cudaError_t launch_gemv_epi(const GemmArgs& a, cudaStream_t s) {
 // every output in the same order and gives bit-identical results. Measured on B200 at M = 128
 // (tools/gemm_bench.py, r01c): S = 4 is fastest for all four OPT-1.3B projections; clusters of 8 lose to
 // cluster scheduling (one CTA per SM needs 8 free SMs in one GPC).
+// Tile width of the split-K kernel: 64 columns when the projection has a single row tile and its 128-column tiles x
+// S would keep fewer than half of the 148 SMs streaming weights (C2: O and FC2, N = 2048 -> 16 x 4 = 64 CTAs), so
+// twice as many SMs share the weight stream. Depends on (N, K, epi, M_total) only, like S.
+int gemm_tile_n(int N, int K, int epi, int M_total) {
+    if (epi == EPI_SILU_MUL || M_total > BM) return BN;
+    const long n_tiles = (N + BN - 1) / BN;
+    return n_tiles * gemm_split_k(N, K, epi, M_total) <= 74 ? 64 : BN;
+}
+
 int gemm_split_k(int N, int K, int epi, int M_total) {
     const int per = epi == EPI_SILU_MUL ? BN / 2 : BN;
     const long n_tiles = (N + per - 1) / per;
@@ -722,6 +754,9 @@ cudaError_t warm_gemm_kernels() {
                          (const void*)gemm_kernel<EPI_RESID, 4>,    (const void*)gemm_kernel<EPI_RESID, 8>,
                          (const void*)gemm_kernel<EPI_SILU_MUL, 1>, (const void*)gemm_kernel<EPI_SILU_MUL, 2>,
                          (const void*)gemm_kernel<EPI_SILU_MUL, 4>, (const void*)gemm_kernel<EPI_SILU_MUL, 8>,
+                         (const void*)gemm_kernel<EPI_BF16, 1, 64>, (const void*)gemm_kernel<EPI_BF16, 2, 64>,
+                         (const void*)gemm_kernel<EPI_BF16, 4, 64>, (const void*)gemm_kernel<EPI_RESID, 1, 64>,
+                         (const void*)gemm_kernel<EPI_RESID, 2, 64>, (const void*)gemm_kernel<EPI_RESID, 4, 64>,
                          (const void*)gemm_big_kernel<EPI_BF16>,     (const void*)gemm_big_kernel<EPI_RESID>,
                          (const void*)gemm_big_kernel<EPI_SILU_MUL>,
                          (const void*)gemv_kernel<EPI_BF16, 1>,  (const void*)gemv_kernel<EPI_BF16, 2>,
@@ -758,10 +793,11 @@ cudaError_t launch_gemm(const CUtensorMap& mapX, const CUtensorMap& mapW, const 
             case EPI_SILU_MUL: return launch_big<EPI_SILU_MUL>(mapX, mapW, a, s);
         }
     }
+    const int tbn = a.split_k <= 0 && a.mapW64 ? gemm_tile_n(a.N, a.K, a.epi, a.M_total) : BN;
     switch (a.epi) {
-        case EPI_BF16: return launch_epi<EPI_BF16>(mapX, mapW, a, S, s);
-        case EPI_RESID: return launch_epi<EPI_RESID>(mapX, mapW, a, S, s);
-        case EPI_SILU_MUL: return launch_epi<EPI_SILU_MUL>(mapX, mapW, a, S, s);
+        case EPI_BF16: return launch_epi<EPI_BF16>(mapX, mapW, a, S, tbn, s);
+        case EPI_RESID: return launch_epi<EPI_RESID>(mapX, mapW, a, S, tbn, s);
+        case EPI_SILU_MUL: return launch_epi<EPI_SILU_MUL>(mapX, mapW, a, S, tbn, s);
     }
     return cudaErrorInvalidValue;
 }

@@ -109,7 +109,10 @@ struct GemmArgs {
     const __nv_bfloat16* X;     // [*, ldx] (rows as for mapX)
     int ldx;
     const __nv_bfloat16* W;     // [rows x K] row-major (rows as for mapW)
+    // the same weights with 64-row boxes (64-column tiles, gemm_tile_n); null = 128-column tiles only (host pointer)
+    const CUtensorMap* mapW64;
 };
+int gemm_tile_n(int N, int K, int epi, int M_total);
 constexpr int kGemvAutoRows = 2;   // rows up to which launch_gemm picks the GEMV
 int gemm_split_k(int N, int K, int epi, int M_total);
 // Maps: X box {64, 128} SW128 over [max_rows x K]; W box {64, 128} (EPI_SILU_MUL: {64, 64}) SW128 over [rows x K].

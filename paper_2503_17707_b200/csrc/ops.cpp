@@ -63,7 +63,12 @@ extern "C" pb_status pb_op_gemm_split(const void* X, int32_t x_rows, int32_t m_b
     a.up_row0 = N;
     a.split_k = split_k;
     a.M_total = m_end - m_begin;
-    a.X = static_cast<const __nv_bfloat16*>(X);   // M <= 8 with split_k == 0: the weight-streaming GEMV
+    CUtensorMap mw64;
+    if (epi != EPI_SILU_MUL) {
+        if (!make_map_bf16(&mw64, W, n_rows, K, K, 64, 64, 128, err, sizeof err)) return fail(PB_EINVAL, "%s", err);
+        a.mapW64 = &mw64;   // 64-column tiles where gemm_tile_n picks them
+    }
+    a.X = static_cast<const __nv_bfloat16*>(X);   // M <= 2 with split_k == 0: the weight-streaming GEMV
     a.ldx = K;
     a.W = static_cast<const __nv_bfloat16*>(W);
     return cuda_status(launch_gemm(mx, mw, a, (cudaStream_t)stream), "gemm");

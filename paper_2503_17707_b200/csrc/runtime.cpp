@@ -311,6 +311,9 @@ static pb_status build_prefill_maps(pb_ctx* c) {
                 if (!make_map_bf16(maps[i], base, t.rows, t.cols, t.cols, box_rows, 64, 128, err, sizeof err))
                     return fail(PB_EINVAL, "weight map layer %d: %s", l, err);
                 lm.w[i] = reinterpret_cast<const __nv_bfloat16*>(base);
+                if (!(i == 2 && !opt) &&
+                    !make_map_bf16(&lm.w64[i], base, t.rows, t.cols, t.cols, 64, 64, 128, err, sizeof err))
+                    return fail(PB_EINVAL, "weight map layer %d: %s", l, err);
             }
         }
     }
@@ -828,11 +831,13 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, boo
         return a;
     };
     // Algorithmic work of a GEMM launch: 2MNK flops; bytes = X + W + output (fp32 residual read + write).
+    // weight wi of the layer (0 qkv, 1 o, 2 fc1 | gate_up, 3 fc2 | down): its tensor maps and plain pointer
     auto gemm = [&](const CUtensorMap& mx, const CUtensorMap& mw, GemmArgs a, int n_w_rows, const __nv_bfloat16* X,
-                    int ldx, const __nv_bfloat16* W) -> cudaError_t {
+                    int ldx, int wi) -> cudaError_t {
         a.X = X;
         a.ldx = ldx;
-        a.W = W;
+        a.W = lm.w[wi];
+        a.mapW64 = (wi == 2 && !opt) ? nullptr : &lm.w64[wi];
         const int pi = prof_begin(c, K_GEMM, s);
         cudaError_t e = launch_gemm(mx, mw, a, s);
         const double M = rows, N = a.N, K = a.K;
@@ -854,7 +859,7 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, boo
     CU(need(opt ? "qkv_b" : "qkv"));
     GemmArgs a = G(r0, qdim, d, EPI_BF16, opt ? wt(c, l, "qkv_b") : nullptr, 0, opt ? 1.0f / sqrtf((float)hd) : 1.0f,
                    opt ? d : 0, qkv, qdim);
-    CU(gemm(c->map_x, lm.qkv, a, qdim, x, d, lm.w[0]));
+    CU(gemm(c->map_x, lm.qkv, a, qdim, x, d, 0));
     if (!opt) {
         const int pi = prof_begin(c, K_ROPE, s);
         CU(launch_rope(qkv + (size_t)row_base * qdim, qdim, r0 - row_base, r1 - row_base, B, H, KVH, hd, qd,
@@ -936,24 +941,24 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, boo
     }
     CU(need(opt ? "o_b" : "o"));
     a = G(r0, d, qd, EPI_RESID, opt ? wt(c, l, "o_b") : nullptr, 0, 1.f, 0, h, d);
-    CU(gemm(c->map_attn, lm.o, a, d, attn, qd, lm.w[1]));
+    CU(gemm(c->map_attn, lm.o, a, d, attn, qd, 1));
     // --- MLP block
     CU(need(opt ? "ln2_b" : "ln2_g"));
     CU(norm("ln2_g", "ln2_b"));
     if (opt) {
         CU(need("fc1_b"));
         a = G(r0, f, d, EPI_BF16, wt(c, l, "fc1_b"), 1, 1.f, 0, mlp, f);
-        CU(gemm(c->map_x, lm.up, a, f, x, d, lm.w[2]));
+        CU(gemm(c->map_x, lm.up, a, f, x, d, 2));
         CU(need("fc2_b"));
         a = G(r0, d, f, EPI_RESID, wt(c, l, "fc2_b"), 0, 1.f, 0, h, d);
-        CU(gemm(c->map_mlp, lm.down, a, d, mlp, f, lm.w[3]));
+        CU(gemm(c->map_mlp, lm.down, a, d, mlp, f, 3));
     } else {
         CU(need("gate_up"));
         a = G(r0, f, d, EPI_SILU_MUL, nullptr, 0, 1.f, 0, mlp, f);
-        CU(gemm(c->map_x, lm.up, a, 2 * f, x, d, lm.w[2]));
+        CU(gemm(c->map_x, lm.up, a, 2 * f, x, d, 2));
         CU(need("down"));
         a = G(r0, d, f, EPI_RESID, nullptr, 0, 1.f, 0, h, d);
-        CU(gemm(c->map_mlp, lm.down, a, d, mlp, f, lm.w[3]));
+        CU(gemm(c->map_mlp, lm.down, a, d, mlp, f, 3));
     }
     c->n_launches += opt ? 7 : 8;
     return PB_OK;

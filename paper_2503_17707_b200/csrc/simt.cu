@@ -46,6 +46,15 @@ __global__ void __launch_bounds__(NT) norm_kernel(const float* __restrict__ h, i
                                                   int dyn_in, int dyn_out) {
     static_assert(NT == rownorm::kVT, "one thread per rownorm virtual thread");
     pdl_launch_dependents();   // a PDL-launched GEMM may start its weight prefetch
+    // gamma / beta are weights (resident before this kernel is enqueued): fetched under the previous kernel's tail
+    // (raw bf16 in registers: converting here would stall on the loads before the activation loads are issued)
+    __nv_bfloat16 gm[PER], bt[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int c = threadIdx.x + i * NT;
+        gm[i] = c < d ? gamma[c] : __float2bfloat16_rn(0.f);
+        bt[i] = c < d && beta ? beta[c] : __float2bfloat16_rn(0.f);
+    }
     pdl_wait();                // PDL-launched: the previous kernel's output is visible from here on
     __shared__ float red[32];
     long long row = blockIdx.x, orow = blockIdx.x;
@@ -87,7 +96,7 @@ __global__ void __launch_bounds__(NT) norm_kernel(const float* __restrict__ h, i
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
         const int c = threadIdx.x + i * NT;
-        if (c < d) o[c] = rownorm::out(v[i], mean, rstd, gamma, beta, c);
+        if (c < d) o[c] = rownorm::out_f(v[i], mean, rstd, __bfloat162float(gm[i]), __bfloat162float(bt[i]), beta != nullptr);
     }
 }
 
