@@ -268,35 +268,55 @@ __global__ void __launch_bounds__(256, 2) attention_kernel(const __nv_bfloat16* 
 __global__ void __launch_bounds__(256) logits_kernel(const __nv_bfloat16* __restrict__ y, int B, int d,
                                                      const __nv_bfloat16* __restrict__ E, int v0, int v1,
                                                      float* __restrict__ logits, int ldl) {
+    // One warp per vocabulary row. Lane l accumulates columns l*8 + 256 k in ascending order; the row's 16-B
+    // vectors are requested in groups of 8 before any is used, the first group before the programmatic-dependency
+    // wait (the head weights are resident; y is the previous kernel's output). y (B x d bf16, a few KB) is read
+    // through L1.
     pdl_launch_dependents();
-    pdl_wait();
-    extern __shared__ float sy[];
-    for (int i = threadIdx.x; i < B * d; i += blockDim.x) sy[i] = __bfloat162float(y[i]);
-    __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int v = v0 + blockIdx.x * 8 + warp;
+    constexpr int G = 8;
+    const int nvec = d / 8;   // 16-B vectors per row
+    const __nv_bfloat16* e = E + (size_t)(v < v1 ? v : v0) * d;
+    uint4 ev[G];
+    auto load_group = [&](int k0) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const int vec = (k0 + g) * 32 + lane;
+            ev[g] = vec < nvec ? __ldg(reinterpret_cast<const uint4*>(e) + vec) : make_uint4(0, 0, 0, 0);
+        }
+    };
+    load_group(0);
+    pdl_wait();
     if (v >= v1) return;
-    const __nv_bfloat16* e = E + (size_t)v * d;
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int c = lane * 8; c < d; c += 256) {
-        uint4 ev = __ldg(reinterpret_cast<const uint4*>(e + c));
-        const __nv_bfloat16* eb = reinterpret_cast<const __nv_bfloat16*>(&ev);
-        float f[8];
+    for (int k0 = 0; k0 * 32 < nvec; k0 += G) {
+        if (k0 > 0) load_group(k0);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) f[i] = __bfloat162float(eb[i]);
-        for (int b = 0; b < B; ++b) {
-            const float* yb = sy + b * d + c;
+        for (int g = 0; g < G; ++g) {
+            const int vec = (k0 + g) * 32 + lane;
+            if (vec >= nvec) break;
+            const __nv_bfloat16* eb = reinterpret_cast<const __nv_bfloat16*>(&ev[g]);
+            float f[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) acc[b] = fmaf(f[i], yb[i], acc[b]);
+            for (int i = 0; i < 8; ++i) f[i] = __bfloat162float(eb[i]);
+            for (int b = 0; b < B; ++b) {
+                const uint4 yv = __ldg(reinterpret_cast<const uint4*>(y + (size_t)b * d) + vec);
+                const __nv_bfloat16* yb = reinterpret_cast<const __nv_bfloat16*>(&yv);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) acc[b] = fmaf(f[i], __bfloat162float(yb[i]), acc[b]);
+            }
         }
     }
     for (int b = 0; b < B; ++b) {
-        const float s = warp_sum(acc[b]);
-        if (lane == 0) logits[(size_t)b * ldl + v] = s;
+        const float s2 = warp_sum(acc[b]);
+        if (lane == 0) logits[(size_t)b * ldl + v] = s2;
     }
 }
 
 // ------------------------------------------------------------------ argmax (lowest index wins ties)
+// One CTA per sequence; every thread keeps 8 loads in flight (strided, coalesced), then a butterfly per warp and
+// one over the warps. The (value, lowest index) maximum does not depend on the visiting order.
 __global__ void __launch_bounds__(1024) argmax_kernel(const float* __restrict__ logits, int V, int ldl,
                                                       int32_t* tokens, int32_t* nan_flag) {
     pdl_launch_dependents();
@@ -307,10 +327,21 @@ __global__ void __launch_bounds__(1024) argmax_kernel(const float* __restrict__ 
     float best = -CUDART_INF_F;
     int bi = 0x7fffffff;
     bool bad = false;
-    for (int v = threadIdx.x; v < V; v += blockDim.x) {
-        const float f = x[v];
-        if (!isfinite(f)) bad = true;
-        if (f > best || (f == best && v < bi)) { best = f; bi = v; }
+    constexpr int U = 8;
+    for (int v = threadIdx.x; v < V; v += U * blockDim.x) {
+        float f[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int vv = v + u * blockDim.x;
+            f[u] = vv < V ? x[vv] : -CUDART_INF_F;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int vv = v + u * blockDim.x;
+            if (vv >= V) break;
+            if (!isfinite(f[u])) bad = true;
+            if (f[u] > best || (f[u] == best && vv < bi)) { best = f[u]; bi = vv; }
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -446,12 +477,7 @@ cudaError_t launch_logits(const __nv_bfloat16* y, int B, int d, const __nv_bfloa
                           int ldl, cudaStream_t s, bool pdl) {
     if (v1 <= v0) return cudaSuccess;
     if (B > 8 || d % 8) return cudaErrorInvalidValue;
-    const size_t sm = (size_t)B * d * sizeof(float);
-    if (sm > 48 * 1024) {   // B <= 8 rows of d <= 10240 fp32: at most 320 KB is refused by the launch itself
-        cudaError_t e = smem_attr_once<logits_kernel>(227 * 1024);
-        if (e != cudaSuccess) return e;
-    }
-    return launch_pdl(logits_kernel, (v1 - v0 + 7) / 8, 256, sm, s, pdl, y, B, d, E, v0, v1, logits, ldl);
+    return launch_pdl(logits_kernel, (v1 - v0 + 7) / 8, 256, 0, s, pdl, y, B, d, E, v0, v1, logits, ldl);
 }
 
 cudaError_t launch_argmax(const float* logits, int B, int V, int ldl, int32_t* tokens, int32_t* nan_flag,
