@@ -44,7 +44,10 @@ def parse():
     ap.add_argument("--workload", default="C2")
     ap.add_argument("--policy", default=None, choices=[None, "stage", "interleave"])
     ap.add_argument("--vocab-sliced", type=int, default=None)
-    ap.add_argument("--chunk-mb", type=int, default=64)
+    ap.add_argument("--chunk-mb", type=int, default=None,
+                    help="DMA group / merge granularity; default 128 on one GPU (measured on B200, C2: 16/32/64/128/256 MB"
+                         " -> 0.965/0.971/0.981/0.988/0.988 of the PCIe bound: every group boundary costs a landed-event"
+                         " record on the saturated link), 64 with several GPUs (finer stage / gather interleave)")
     ap.add_argument("--prefill-chunks", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
@@ -53,7 +56,20 @@ def parse():
                     help="host_alias_layers K: layer l is DMA'd from the host image of layer l mod K (DRAM-limited boxes)")
     ap.add_argument("--dist-backend", default="nccl", help="torch.distributed backend for barriers/handle exchange")
     ap.add_argument("--same-gpu", action="store_true", help="all ranks on cuda:0 (testing the N>1 path on one GPU)")
-    return ap.parse_args()
+    args = ap.parse_args()
+    # the same defaults on both arms (the reference arm reports this configuration too)
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    from synth.configs import WORKLOADS
+    w = WORKLOADS[args.workload]
+    if args.policy is None:
+        args.policy = "stage" if (world == 1 or len(w.adapters) > 1) else "interleave"
+    if args.vocab_sliced is None:
+        args.vocab_sliced = 0 if world == 1 else 1
+    if args.prefill_chunks is None:
+        args.prefill_chunks = 1 if world == 1 else 2
+    if args.chunk_mb is None:
+        args.chunk_mb = 128 if world == 1 else 64
+    return args
 
 
 # ----------------------------------------------------------------------------------------------------
@@ -324,12 +340,6 @@ def main():
         return t.item()
 
     w = WORKLOADS[args.workload]
-    if args.policy is None:
-        args.policy = "stage" if (world == 1 or len(w.adapters) > 1) else "interleave"
-    if args.vocab_sliced is None:
-        args.vocab_sliced = 0 if world == 1 else 1
-    if args.prefill_chunks is None:
-        args.prefill_chunks = 1 if world == 1 else 2
     plan = Plan(w.model, w.adapters, world, policy=args.policy, vocab_sliced=args.vocab_sliced,
                 chunk_bytes=args.chunk_mb << 20, prefill_chunks=args.prefill_chunks, host_alias_layers=args.host_alias)
     S = plan.sizes.dev_weight_bytes + plan.sizes.dev_adapter_bytes   # bytes DMA'd per cold start (all ranks)
