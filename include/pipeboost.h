@@ -339,7 +339,9 @@ typedef struct {
     int64_t load_bytes;      /* bytes this rank moved over PCIe in the trial */
     int64_t recv_bytes;      /* bytes this rank received over NVLink */
     int32_t n_chunks;
-    const double* chunk_landed_ms;   /* [n_chunks], -1 where not loaded by this rank */
+    const double* chunk_landed_ms;   /* [n_chunks], -1 where not loaded by this rank; per-chunk times only when the
+                                      * context was created with PB_LANDED_TIMING=1 (timing events on the saturated
+                                      * copy lane cost ~20 us each), else -1 (load_done_ms is always set) */
     const double* chunk_gathered_ms; /* [n_chunks], -1 where not received by this rank */
     int32_t n_launches;      /* kernels this rank launched in the trial */
 } pb_timeline_t;

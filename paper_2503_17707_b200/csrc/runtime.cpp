@@ -414,8 +414,11 @@ extern "C" pb_status pb_ctx_create(const pb_plan* plan, int32_t rank, const void
     if (mk(&c->t0) || mk(&c->merge_done) || mk(&c->gather_done) || mk(&c->done) || mk(&c->ready_merge) ||
         mk(&c->ready_recv) || cudaEventCreateWithFlags(&c->tok_ev, cudaEventDisableTiming))
         return cleanup(fail(PB_ECUDA, "cudaEventCreate failed"));
+    if (const char* lt = getenv("PB_LANDED_TIMING")) c->landed_timing = atoi(lt) != 0;
+    if (mk(&c->load_end)) return cleanup(fail(PB_ECUDA, "cudaEventCreate failed"));
     for (int32_t id : plan->load[rank])
-        if (mk(&c->landed[id])) return cleanup(fail(PB_ECUDA, "cudaEventCreate failed"));
+        if (c->landed_timing ? mk(&c->landed[id]) : cudaEventCreateWithFlags(&c->landed[id], cudaEventDisableTiming))
+            return cleanup(fail(PB_ECUDA, "cudaEventCreate failed"));
     c->budget_events.assign(4 * kEventPool, nullptr);
     for (auto& e : c->budget_events)
         if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming)) return cleanup(fail(PB_ECUDA, "cudaEventCreate failed"));
@@ -478,6 +481,7 @@ extern "C" void pb_ctx_free(pb_ctx* c) {
     cudaDeviceSynchronize();
     auto d = [](cudaEvent_t e) { if (e) cudaEventDestroy(e); };
     d(c->t0); d(c->merge_done); d(c->gather_done); d(c->done); d(c->ready_merge); d(c->ready_recv); d(c->tok_ev);
+    d(c->load_end);
     for (auto e : c->budget_events) d(e);
     for (auto st : c->owned_streams) stream_give(c->device, st);
     for (auto e : c->landed) d(e);
@@ -1124,6 +1128,7 @@ pb_status issue_group(Issuer& I, size_t gi) {
     }
     CU(cudaMemcpyAsync(g.dst, src, g.bytes, cudaMemcpyHostToDevice, c->h2d[0]));
     CU(cudaEventRecord(c->landed[ld[g.first]], c->h2d[0]));
+    if (gi + 1 == c->copies.size()) CU(cudaEventRecord(c->load_end, c->h2d[0]));
     if (g.from_file) c->file->issued((int64_t)gi, c->landed[ld[g.first]]);
     CU(I.h2d.add(2));
     static thread_local std::vector<int32_t> others;
@@ -2002,9 +2007,9 @@ extern "C" pb_status pb_timeline(pb_ctx* c, pb_timeline_t* out) {
         if (!e || cudaEventElapsedTime(&v, c->t0, e) != cudaSuccess) { cudaGetLastError(); return -1; }
         return v;
     };
-    double load_done = 0;
+    double load_done = c->copies.empty() ? 0 : ms(c->load_end);
     for (int32_t id : p->load[c->rank]) {
-        c->tl_landed[id] = ms(landed_ev(c, id));
+        c->tl_landed[id] = c->landed_timing ? ms(landed_ev(c, id)) : -1;
         load_done = std::max(load_done, c->tl_landed[id]);
     }
     for (int32_t id : p->recv[c->rank]) c->tl_gathered[id] = ms(c->gathered[id]);

@@ -94,6 +94,11 @@ struct pb_ctx {
 
     // events
     cudaEvent_t t0 = nullptr, merge_done = nullptr, gather_done = nullptr, done = nullptr;
+    cudaEvent_t load_end = nullptr;   // timing event after the last copy group (load_done)
+    // per-group landed events carry timestamps (chunk_landed_ms) only with PB_LANDED_TIMING=1: measured on B200,
+    // a timing-event record on the saturated copy lane costs ~20 us (C2 at 128 MB groups: 0.9895 -> 0.9934 of the
+    // PCIe bound without them)
+    bool landed_timing = false;
     cudaEvent_t ready_merge = nullptr, ready_recv = nullptr;   // timing: last stage chunk merged / received
     cudaEvent_t tok_ev = nullptr;                               // prompt tokens landed (copy lane)
     int32_t last_own_stage_chunk = -1, last_recv_stage_chunk = -1;

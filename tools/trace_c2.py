@@ -2,6 +2,7 @@
 chunks land vs when its kernels run."""
 import os, sys, json
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+os.environ.setdefault("PB_LANDED_TIMING", "1")   # per-chunk landed timestamps
 sys.path.insert(0, ".")
 import numpy as np, torch
 import harness, synth

@@ -1,6 +1,7 @@
 """C3 timeline: per layer, when its chunks land, when its merges run, when its compute runs."""
 import os, sys
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+os.environ.setdefault("PB_LANDED_TIMING", "1")   # per-chunk landed timestamps
 sys.path.insert(0, ".")
 import numpy as np, torch, harness, synth
 from paper_2503_17707_b200 import _binding as B
