@@ -248,13 +248,21 @@ static pb_status build_merge_jobs(pb_ctx* c) {
 // Coalesce the load list into DMA groups: a chunk joins the current group when it continues it in both
 // address spaces with the same (< 4 KiB alignment) gap, and either the group stays within chunk_bytes or
 // the chunk is small (biases / norms). Fewer, larger copies keep the copy engine at link speed.
+// Within the last 2 x chunk_bytes of the load the groups are capped at 32 MB: what lands last is all that is
+// left to compute after the link goes idle, so the final layers start as their own tensors arrive (measured
+// per-group cost without timing events ~5 us).
 static void build_copy_groups(pb_ctx* c) {
     const pb_plan* p = c->plan;
     const auto& ld = p->load[c->rank];
-    const int64_t cap = p->opts.chunk_bytes, small = 256 << 10;
+    const int64_t cap_main = p->opts.chunk_bytes, small = 256 << 10;
+    const int64_t cap_tail = std::min<int64_t>(cap_main, 32 << 20);
+    int64_t total = 0, before = 0;
+    for (int32_t id : ld) total += p->chunks[id].bytes;
     c->copies.clear();
     for (int32_t i = 0; i < (int32_t)ld.size(); ++i) {
         const ChunkRec& ch = p->chunks[ld[i]];
+        const int64_t cap = total - before <= 2 * cap_main ? cap_tail : cap_main;
+        before += ch.bytes;
         const char* hbase = static_cast<const char*>(ch.is_adapter ? c->host_adapters : c->host_base);
         char* dbase = ch.is_adapter ? c->adapters : c->weights;
         const char* src = hbase + ch.host_off;
