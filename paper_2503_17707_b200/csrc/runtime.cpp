@@ -40,12 +40,6 @@ namespace {
 
 int64_t al(int64_t x, int64_t a = 256) { return (x + a - 1) / a * a; }
 
-int max_stage_layers(const pb_plan* p) {
-    int m = 0;
-    for (auto& s : p->stages) m = std::max(m, s.second - s.first);
-    return m;
-}
-
 int32_t qkv_dim(const pb_plan* p) { return (p->model.n_heads + 2 * p->model.n_kv_heads) * p->head_dim(); }
 
 // Head tensor: tied OPT -> embed, otherwise lm_head.
