@@ -51,6 +51,13 @@ if __name__ == "__main__":
             ("c5_fc1_M2048", 2048, 8192, 28672, 2), ("c3_qkv_M512", 512, 4096, 12288, 0)]
   import os
   only_big = os.environ.get("GEMM_BENCH_BIG")
+  if os.environ.get("GEMM_BENCH_GEMV"):   # M = 1 (decode): the weight-streaming GEMV, split 0 only
+      for name, M, K, N, epi in [("qkv", 1, 2048, 6144, 0), ("o", 1, 2048, 2048, 1), ("fc1", 1, 2048, 8192, 0),
+                                 ("fc2", 1, 8192, 2048, 1), ("c4_fc1", 1, 5120, 20480, 0), ("c4_fc2", 1, 20480, 5120, 1),
+                                 ("l70_gate_up", 1, 8192, 28672, 2)]:
+          us, gbs, tf = bench(M, K, N, epi, 0)
+          print(f"{name:14s} M{M} K{K} N{N}: graph {us:6.1f}us {gbs:5.0f}GB/s ev {LAST_EV_US:6.1f}us", flush=True)
+      sys.exit(0)
   for name, M, K, N, epi in shapes:
       if only_big and M <= 128: continue
       res = []
