@@ -358,20 +358,30 @@ cudaError_t launch_epi(const CUtensorMap& mapX, const CUtensorMap& mapW, const G
 constexpr int BIG_BN = 256, BIG_STAGES = 4;
 constexpr int kBigA = BM * BK * 2, kBigB = BIG_BN * BK * 2, kBigStage = kBigA + kBigB;   // 16 + 32 KB
 constexpr int kBigSmem = BIG_STAGES * kBigStage + 256 + 1024;
+// The same kernel with TBN = 192-column tiles (bias / residual epilogues) where 256-column tiles fill the last wave
+// badly (gemm_big_tile_n): W arrives as a 128-row box + a 64-row box (mapW64), 5 stages of 40 KB.
+template <int TBN> __host__ __device__ constexpr int big_stages() { return TBN == 256 ? BIG_STAGES : 5; }
+template <int TBN> __host__ __device__ constexpr int big_stage_bytes() { return kBigA + TBN * BK * 2; }
+template <int TBN> __host__ __device__ constexpr int big_smem() {
+    return big_stages<TBN>() * big_stage_bytes<TBN>() + 256 + 1024;
+}
 
-template <int EPI>
+template <int EPI, int TBN = BIG_BN>
 __global__ void __launch_bounds__(192, 1) gemm_big_kernel(const __grid_constant__ CUtensorMap mapX,
-                                                          const __grid_constant__ CUtensorMap mapW, const GemmArgs a) {
+                                                          const __grid_constant__ CUtensorMap mapW,
+                                                          const __grid_constant__ CUtensorMap mapW64, const GemmArgs a) {
+    static_assert(TBN == BIG_BN || (TBN == 192 && EPI != EPI_SILU_MUL), "192-column tiles: bias / residual epilogues");
+    constexpr int NST = big_stages<TBN>(), kStg = big_stage_bytes<TBN>();
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + BIG_STAGES * kBigStage);
-    uint64_t* empty = full + BIG_STAGES;
-    uint64_t* acc_full = empty + BIG_STAGES;    // [2] MMA -> epilogue
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + NST * kStg);
+    uint64_t* empty = full + NST;
+    uint64_t* acc_full = empty + NST;           // [2] MMA -> epilogue
     uint64_t* acc_empty = acc_full + 2;         // [2] epilogue -> MMA (128 arrivals)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    constexpr int per = EPI == EPI_SILU_MUL ? BIG_BN / 2 : BIG_BN;   // outputs per tile along N
+    constexpr int per = EPI == EPI_SILU_MUL ? BIG_BN / 2 : TBN;   // outputs per tile along N
     const int n_tiles = (a.N + per - 1) / per;
     const int m_tiles = (a.M_end - a.M_begin + BM - 1) / BM;
     const int tiles = n_tiles * m_tiles;
@@ -381,7 +391,8 @@ __global__ void __launch_bounds__(192, 1) gemm_big_kernel(const __grid_constant_
     if (tid == 0) {
         tma_prefetch_desc(&mapX);
         tma_prefetch_desc(&mapW);
-        for (int s = 0; s < BIG_STAGES; ++s) {
+        if (TBN == 192) tma_prefetch_desc(&mapW64);
+        for (int s = 0; s < NST; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
@@ -404,11 +415,11 @@ __global__ void __launch_bounds__(192, 1) gemm_big_kernel(const __grid_constant_
             for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
                 const int m0 = a.M_begin + (t % m_tiles) * BM, n0 = (t / m_tiles) * per;
                 for (int kb = 0; kb < nk; ++kb, ++it) {
-                    const int s = it % BIG_STAGES, kc = kb * BK;
-                    if (it >= BIG_STAGES) mbar_wait(&empty[s], ((it / BIG_STAGES) - 1) & 1);
-                    uint8_t* sA = smem + s * kBigStage;
+                    const int s = it % NST, kc = kb * BK;
+                    if (it >= NST) mbar_wait(&empty[s], ((it / NST) - 1) & 1);
+                    uint8_t* sA = smem + s * kStg;
                     uint8_t* sB = sA + kBigA;
-                    mbar_arrive_expect_tx(&full[s], kBigStage);
+                    mbar_arrive_expect_tx(&full[s], kStg);
                     tma_load_2d(sA, &mapX, &full[s], kc, m0);
                     if (EPI == EPI_SILU_MUL) {   // [gate 128 | up 128] rows as four 64-row boxes
                         tma_load_2d(sB, &mapW, &full[s], kc, n0);
@@ -417,25 +428,26 @@ __global__ void __launch_bounds__(192, 1) gemm_big_kernel(const __grid_constant_
                         tma_load_2d(sB + 3 * kBigB / 4, &mapW, &full[s], kc, a.up_row0 + n0 + 64);
                     } else {
                         tma_load_2d(sB, &mapW, &full[s], kc, n0);
-                        tma_load_2d(sB + kBigB / 2, &mapW, &full[s], kc, n0 + 128);
+                        if (TBN == 192) tma_load_2d(sB + kBigB / 2, &mapW64, &full[s], kc, n0 + 128);
+                        else tma_load_2d(sB + kBigB / 2, &mapW, &full[s], kc, n0 + 128);
                     }
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {   // ---------------- MMA issuer
-            constexpr uint32_t idesc = idesc_bf16_f32(BM, BIG_BN, 0, 0);
+            constexpr uint32_t idesc = idesc_bf16_f32(BM, TBN, 0, 0);
             int it = 0, local = 0;
             for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
                 const int b = local & 1;
-                const uint32_t acc = tmem + b * BIG_BN;
+                const uint32_t acc = tmem + b * TBN;
                 if (local >= 2) mbar_wait(&acc_empty[b], ((local >> 1) - 1) & 1);
                 tc_fence_after();
                 for (int kb = 0; kb < nk; ++kb, ++it) {
-                    const int s = it % BIG_STAGES;
-                    mbar_wait(&full[s], (it / BIG_STAGES) & 1);
+                    const int s = it % NST;
+                    mbar_wait(&full[s], (it / NST) & 1);
                     tc_fence_after();
-                    const uint32_t a_base = smem_u32(smem + s * kBigStage), b_base = a_base + kBigA;
+                    const uint32_t a_base = smem_u32(smem + s * kStg), b_base = a_base + kBigA;
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k)
                         umma_bf16(acc, smem_desc(a_base + k * 32, 16, 1024, kSw128),
@@ -456,7 +468,7 @@ __global__ void __launch_bounds__(192, 1) gemm_big_kernel(const __grid_constant_
             tc_fence_after();
             const int row = m0 + row_in_tile;
             const bool row_ok = row < a.M_end;
-            const uint32_t acc = tmem + b * BIG_BN + lane_off;
+            const uint32_t acc = tmem + b * TBN + lane_off;
             if (EPI == EPI_SILU_MUL) {
 #pragma unroll 1
                 for (int cb = 0; cb < 4; ++cb) {   // 32 gate columns + the matching 32 up columns
@@ -489,7 +501,7 @@ __global__ void __launch_bounds__(192, 1) gemm_big_kernel(const __grid_constant_
                 }
             } else {
 #pragma unroll 1
-                for (int cb = 0; cb < BIG_BN / 32; ++cb) {
+                for (int cb = 0; cb < TBN / 32; ++cb) {
                     uint32_t r[32];
                     tmem_ld32_async(acc + cb * 32, r);
                     tmem_wait_ld();
@@ -554,14 +566,28 @@ __global__ void __launch_bounds__(192, 1) gemm_big_kernel(const __grid_constant_
     }
 }
 
-template <int EPI>
-cudaError_t launch_big(const CUtensorMap& mapX, const CUtensorMap& mapW, const GemmArgs& a, cudaStream_t s) {
-    cudaError_t e = smem_attr_once<gemm_big_kernel<EPI>>(kBigSmem);
+template <int EPI, int TBN = BIG_BN>
+cudaError_t launch_big(const CUtensorMap& mapX, const CUtensorMap& mapW, const CUtensorMap& mapW64, const GemmArgs& a,
+                       cudaStream_t s) {
+    cudaError_t e = smem_attr_once<gemm_big_kernel<EPI, TBN>>(big_smem<TBN>());
     if (e != cudaSuccess) return e;
-    const int per = EPI == EPI_SILU_MUL ? BIG_BN / 2 : BIG_BN;
+    const int per = EPI == EPI_SILU_MUL ? BIG_BN / 2 : TBN;
     const int tiles = ((a.N + per - 1) / per) * ((a.M_end - a.M_begin + BM - 1) / BM);
     const int grid = tiles < 148 ? tiles : 148;
-    return launch_pdl(gemm_big_kernel<EPI>, dim3(grid), dim3(192), kBigSmem, s, a.pdl != 0, mapX, mapW, a);
+    return launch_pdl(gemm_big_kernel<EPI, TBN>, dim3(grid), dim3(192), big_smem<TBN>(), s, a.pdl != 0, mapX, mapW,
+                      mapW64, a);
+}
+
+// Tile width of the persistent kernel: 192 columns when 256-column tiles leave the last wave less than 3/4 full on
+// average and 192 fills it better (C3 QKV: 192 -> 256 tiles; C4 O / FC2: 160 -> 216), else 256. Depends on
+// (N, epi, rows of the whole prompt) only.
+int gemm_big_tile_n(int N, int epi, int M_total) {
+    if (epi == EPI_SILU_MUL) return BIG_BN;
+    const long m_tiles = (M_total + BM - 1) / BM;
+    const long t256 = (N + 255) / 256 * m_tiles, t192 = (N + 191) / 192 * m_tiles;
+    const double f256 = (double)t256 / (148.0 * ((t256 + 147) / 148)), f192 = (double)t192 / (148.0 * ((t192 + 147) / 148));
+    const double time256 = 256.0 * ((t256 + 147) / 148), time192 = 192.0 * ((t192 + 147) / 148);
+    return f256 < 0.75 && f192 > f256 && time192 < time256 ? 192 : BIG_BN;
 }
 
 // ------------------------------------------------------------------------------------------------------------
@@ -759,6 +785,7 @@ cudaError_t warm_gemm_kernels() {
                          (const void*)gemm_kernel<EPI_RESID, 2, 64>, (const void*)gemm_kernel<EPI_RESID, 4, 64>,
                          (const void*)gemm_big_kernel<EPI_BF16>,     (const void*)gemm_big_kernel<EPI_RESID>,
                          (const void*)gemm_big_kernel<EPI_SILU_MUL>,
+                         (const void*)gemm_big_kernel<EPI_BF16, 192>, (const void*)gemm_big_kernel<EPI_RESID, 192>,
                          (const void*)gemv_kernel<EPI_BF16, 1>,  (const void*)gemv_kernel<EPI_BF16, 2>,
                          (const void*)gemv_kernel<EPI_RESID, 1>, (const void*)gemv_kernel<EPI_RESID, 2>,
                          (const void*)gemv_kernel<EPI_SILU_MUL, 1>, (const void*)gemv_kernel<EPI_SILU_MUL, 2>};
@@ -787,10 +814,15 @@ cudaError_t launch_gemm(const CUtensorMap& mapX, const CUtensorMap& mapW, const 
     // The kernel is chosen from the WHOLE prompt (M_total), never from the rows of this launch, so a prompt split
     // into chunks runs every output through the same kernel and the same summation order.
     if (S == 1 && a.split_k <= 0 && a.M_total > BM && !a.m_dyn) {
+        const bool t192 = a.mapW64 && gemm_big_tile_n(a.N, a.epi, a.M_total) == 192;
         switch (a.epi) {
-            case EPI_BF16: return launch_big<EPI_BF16>(mapX, mapW, a, s);
-            case EPI_RESID: return launch_big<EPI_RESID>(mapX, mapW, a, s);
-            case EPI_SILU_MUL: return launch_big<EPI_SILU_MUL>(mapX, mapW, a, s);
+            case EPI_BF16:
+                return t192 ? launch_big<EPI_BF16, 192>(mapX, mapW, *a.mapW64, a, s)
+                            : launch_big<EPI_BF16>(mapX, mapW, mapW, a, s);
+            case EPI_RESID:
+                return t192 ? launch_big<EPI_RESID, 192>(mapX, mapW, *a.mapW64, a, s)
+                            : launch_big<EPI_RESID>(mapX, mapW, mapW, a, s);
+            case EPI_SILU_MUL: return launch_big<EPI_SILU_MUL>(mapX, mapW, mapW, a, s);
         }
     }
     const int tbn = a.split_k <= 0 && a.mapW64 ? gemm_tile_n(a.N, a.K, a.epi, a.M_total) : BN;

@@ -1542,7 +1542,8 @@ pb_status issue_trial(pb_ctx* c, int B, int T, bool replay) {
             I.tb[j] = t;
             if (j < I.k) t += T / I.k + (j < T % I.k ? 1 : 0);
         }
-        c->gemm_m_total = B * T;
+        // rows one GEMM launch covers at most: the whole batch, or one sequence in microbatch mode (PB_MERGE_ALL)
+        c->gemm_m_total = I.mb_mode ? T : B * T;
     }
     I.own_issued.assign(p->tensors.size(), replay ? 1 : 0);
     I.recv_issued.assign(p->tensors.size(), replay ? 1 : 0);
