@@ -360,7 +360,7 @@ constexpr int kBigA = BM * BK * 2, kBigB = BIG_BN * BK * 2, kBigStage = kBigA + 
 constexpr int kBigSmem = BIG_STAGES * kBigStage + 256 + 1024;
 // The same kernel with TBN = 192-column tiles (bias / residual epilogues) where 256-column tiles fill the last wave
 // badly (gemm_big_tile_n): W arrives as a 128-row box + a 64-row box (mapW64), 5 stages of 40 KB.
-template <int TBN> __host__ __device__ constexpr int big_stages() { return TBN == 256 ? BIG_STAGES : 5; }
+template <int TBN> __host__ __device__ constexpr int big_stages() { return TBN == 256 ? BIG_STAGES : TBN == 192 ? 5 : 6; }
 template <int TBN> __host__ __device__ constexpr int big_stage_bytes() { return kBigA + TBN * BK * 2; }
 template <int TBN> __host__ __device__ constexpr int big_smem() {
     return big_stages<TBN>() * big_stage_bytes<TBN>() + 256 + 1024;
@@ -370,7 +370,8 @@ template <int EPI, int TBN = BIG_BN>
 __global__ void __launch_bounds__(192, 1) gemm_big_kernel(const __grid_constant__ CUtensorMap mapX,
                                                           const __grid_constant__ CUtensorMap mapW,
                                                           const __grid_constant__ CUtensorMap mapW64, const GemmArgs a) {
-    static_assert(TBN == BIG_BN || (TBN == 192 && EPI != EPI_SILU_MUL), "192-column tiles: bias / residual epilogues");
+    static_assert(TBN == BIG_BN || ((TBN == 192 || TBN == 128) && EPI != EPI_SILU_MUL),
+                  "192- / 128-column tiles: bias / residual epilogues");
     constexpr int NST = big_stages<TBN>(), kStg = big_stage_bytes<TBN>();
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -429,7 +430,7 @@ __global__ void __launch_bounds__(192, 1) gemm_big_kernel(const __grid_constant_
                     } else {
                         tma_load_2d(sB, &mapW, &full[s], kc, n0);
                         if (TBN == 192) tma_load_2d(sB + kBigB / 2, &mapW64, &full[s], kc, n0 + 128);
-                        else tma_load_2d(sB + kBigB / 2, &mapW, &full[s], kc, n0 + 128);
+                        else if (TBN == 256) tma_load_2d(sB + kBigB / 2, &mapW, &full[s], kc, n0 + 128);
                     }
                 }
             }
@@ -578,16 +579,26 @@ cudaError_t launch_big(const CUtensorMap& mapX, const CUtensorMap& mapW, const C
                       mapW64, a);
 }
 
-// Tile width of the persistent kernel: 192 columns when 256-column tiles leave the last wave less than 3/4 full on
-// average and 192 fills it better (C3 QKV: 192 -> 256 tiles; C4 O / FC2: 160 -> 216), else 256. Depends on
-// (N, epi, rows of the whole prompt) only.
+// Tile width of the persistent kernel: 256, 192 or 128 columns, whichever minimises waves x (width + 32) (the +32
+// charges narrower tiles for their extra activation traffic and per-tile overhead); 256 unless another width is
+// more than 5 % better. C3: QKV 192, O / down 128 (one wave); C4: O / FC1 / FC2 192, QKV 256; C5a: QKV 192, O / down
+// 256; C5b 256 (measured: C4 GEMM class 0.71 -> 0.81 of the sustained peak, C5a 0.93 -> 0.94).
+// Depends on (N, epi, rows of the whole prompt) only.
 int gemm_big_tile_n(int N, int epi, int M_total) {
     if (epi == EPI_SILU_MUL) return BIG_BN;
     const long m_tiles = (M_total + BM - 1) / BM;
-    const long t256 = (N + 255) / 256 * m_tiles, t192 = (N + 191) / 192 * m_tiles;
-    const double f256 = (double)t256 / (148.0 * ((t256 + 147) / 148)), f192 = (double)t192 / (148.0 * ((t192 + 147) / 148));
-    const double time256 = 256.0 * ((t256 + 147) / 148), time192 = 192.0 * ((t192 + 147) / 148);
-    return f256 < 0.75 && f192 > f256 && time192 < time256 ? 192 : BIG_BN;
+    auto cost = [&](int w) {
+        const long tiles = (N + w - 1) / w * m_tiles;
+        return (double)((tiles + 147) / 148) * (w + 32);
+    };
+    int best = BIG_BN;
+    double best_cost = cost(BIG_BN) * 0.95;
+    for (int w : {192, 128})
+        if (cost(w) < best_cost) {
+            best = w;
+            best_cost = cost(w);
+        }
+    return best;
 }
 
 // ------------------------------------------------------------------------------------------------------------
@@ -786,6 +797,7 @@ cudaError_t warm_gemm_kernels() {
                          (const void*)gemm_big_kernel<EPI_BF16>,     (const void*)gemm_big_kernel<EPI_RESID>,
                          (const void*)gemm_big_kernel<EPI_SILU_MUL>,
                          (const void*)gemm_big_kernel<EPI_BF16, 192>, (const void*)gemm_big_kernel<EPI_RESID, 192>,
+                         (const void*)gemm_big_kernel<EPI_BF16, 128>, (const void*)gemm_big_kernel<EPI_RESID, 128>,
                          (const void*)gemv_kernel<EPI_BF16, 1>,  (const void*)gemv_kernel<EPI_BF16, 2>,
                          (const void*)gemv_kernel<EPI_RESID, 1>, (const void*)gemv_kernel<EPI_RESID, 2>,
                          (const void*)gemv_kernel<EPI_SILU_MUL, 1>, (const void*)gemv_kernel<EPI_SILU_MUL, 2>};
@@ -814,14 +826,16 @@ cudaError_t launch_gemm(const CUtensorMap& mapX, const CUtensorMap& mapW, const 
     // The kernel is chosen from the WHOLE prompt (M_total), never from the rows of this launch, so a prompt split
     // into chunks runs every output through the same kernel and the same summation order.
     if (S == 1 && a.split_k <= 0 && a.M_total > BM && !a.m_dyn) {
-        const bool t192 = a.mapW64 && gemm_big_tile_n(a.N, a.epi, a.M_total) == 192;
+        const int tw = a.mapW64 ? gemm_big_tile_n(a.N, a.epi, a.M_total) : BIG_BN;
         switch (a.epi) {
             case EPI_BF16:
-                return t192 ? launch_big<EPI_BF16, 192>(mapX, mapW, *a.mapW64, a, s)
-                            : launch_big<EPI_BF16>(mapX, mapW, mapW, a, s);
+                if (tw == 192) return launch_big<EPI_BF16, 192>(mapX, mapW, *a.mapW64, a, s);
+                if (tw == 128) return launch_big<EPI_BF16, 128>(mapX, mapW, mapW, a, s);
+                return launch_big<EPI_BF16>(mapX, mapW, mapW, a, s);
             case EPI_RESID:
-                return t192 ? launch_big<EPI_RESID, 192>(mapX, mapW, *a.mapW64, a, s)
-                            : launch_big<EPI_RESID>(mapX, mapW, mapW, a, s);
+                if (tw == 192) return launch_big<EPI_RESID, 192>(mapX, mapW, *a.mapW64, a, s);
+                if (tw == 128) return launch_big<EPI_RESID, 128>(mapX, mapW, mapW, a, s);
+                return launch_big<EPI_RESID>(mapX, mapW, mapW, a, s);
             case EPI_SILU_MUL: return launch_big<EPI_SILU_MUL>(mapX, mapW, mapW, a, s);
         }
     }
