@@ -73,6 +73,8 @@ def _gemm_case(rng, M, K, N):
                                          (256, 2048, 640, 128, 256), (200, 192, 136, 40, 170), (130, 688, 256, 0, 130),
                                          (1024, 1024, 3072, 0, 1024), (2048, 512, 8192, 0, 2000),
                                          (700, 1536, 1000, 100, 700),
+                                         # persistent kernel with 192-column tiles and a ragged last tile
+                                         (1024, 512, 3000, 0, 1024),
                                          # M <= 2: the weight-streaming GEMV (decode sizes), ragged N and K
                                          (1, 2048, 640, 0, 1), (2, 512, 136, 0, 2), (3, 688, 258, 1, 3)])
 def test_gemm_bf16_epilogue(M, K, N, m0, m1):
@@ -94,10 +96,11 @@ def test_gemm_bf16_epilogue(M, K, N, m0, m1):
 
 
 @pytest.mark.parametrize("M,K,N,f", [(192, 320, 256, 136), (1536, 1024, 2560, 2752), (2, 320, 256, 136),
-                                     (1, 2048, 512, 330)])
+                                     (1, 2048, 512, 330), (1024, 512, 3000, 136), (600, 256, 1000, 136)])
 def test_gemm_relu_and_resid_and_silu(M, K, N, f):
     """Small shapes take the split-K kernel or the persistent 128x256 kernel at S = 1; the second case runs the
-    persistent kernel over more tiles than SMs (both TMEM accumulators cycle); M <= 2 takes the GEMV."""
+    persistent kernel over more tiles than SMs (both TMEM accumulators cycle); M <= 2 takes the GEMV; the last two
+    take the persistent kernel's 192- and 128-column tiles (ragged N)."""
     need_gpu()
     rng = np.random.default_rng(11 + M)
     X, W, bias = _gemm_case(rng, M, K, N)
