@@ -36,6 +36,8 @@
 // version would need the cluster/DSMEM reduction inside the persistent loop.
 #include <cuda_bf16.h>
 
+#include <cstring>
+
 #include "kernels.hpp"
 #include "rownorm.cuh"
 #include "sm100.cuh"
@@ -58,8 +60,8 @@ __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x));
 // Debug trace (PB_CHAIN_TRACE=1; tools/chain_trace.py): per launch slot and item, globaltimer stamps of
 // claim, activation dependency satisfied, accumulator ready, output published, plus smid / job / item.
 constexpr int kTraceSlots = 64, kTraceItems = 1024;
-__device__ unsigned long long g_trace[kTraceSlots][kTraceItems][8];
-__device__ unsigned long long g_trace2[kTraceSlots][kTraceItems][8];   // finishing epilogue, per chunk
+constexpr size_t kTraceWords = (size_t)kTraceSlots * kTraceItems * 8;   // per table; two tables (items, chunks)
+unsigned long long* g_trace_buf = nullptr;   // device buffer, allocated on the first traced launch
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -72,7 +74,8 @@ __device__ __forceinline__ unsigned smid() {
 }
 #define TRACE(item, k, v)                                                                               \
     do {                                                                                                \
-        if (a.trace_slot >= 0 && (item) < kTraceItems) g_trace[a.trace_slot % kTraceSlots][item][k] = (v); \
+        if (a.trace_slot >= 0 && (item) < kTraceItems)                                                  \
+            a.trace[((size_t)(a.trace_slot % kTraceSlots) * kTraceItems + (item)) * 8 + (k)] = (v);       \
     } while (0)
 
 __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
@@ -466,7 +469,8 @@ __global__ void __launch_bounds__(192, 1) chain_kernel(const __grid_constant__ C
                     mbar_wait(&rbar[k & 1], (uint32_t)((red_uses * 2 + (k >> 1)) & 1));
                     if (k == 0 && et == 0) TRACE(item, 6, gtime());
                     if (et == 0 && a.trace_slot >= 0 && item < kTraceItems)
-                        g_trace2[a.trace_slot % kTraceSlots][item][2 * k] = gtime();
+                        a.trace[kTraceWords + ((size_t)(a.trace_slot % kTraceSlots) * kTraceItems + item) * 8 + 2 * k] =
+                            gtime();
                     const float4* buf = reinterpret_cast<const float4*>(sbuf + (k & 1) * kStageBufBytes);
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
@@ -536,7 +540,8 @@ __global__ void __launch_bounds__(192, 1) chain_kernel(const __grid_constant__ C
                         reduce32(cb, v);
                         refill(cb, cb);
                         if (et == 0 && a.trace_slot >= 0 && item < kTraceItems)
-                            g_trace2[a.trace_slot % kTraceSlots][item][2 * cb + 1] = gtime();
+                            a.trace[kTraceWords + ((size_t)(a.trace_slot % kTraceSlots) * kTraceItems + item) * 8 +
+                                    2 * cb + 1] = gtime();
                         if (!row_ok || n >= J.N) continue;
 #pragma unroll
                         for (int e = 0; e < 32; ++e)
@@ -621,9 +626,14 @@ size_t chain_part_bytes(int N, int K, int epi) {
 // Copy the trace of launch slots [0, n) to host memory (n * kTraceItems * 8 words), then the per-chunk trace.
 cudaError_t chain_trace_copy(unsigned long long* host, int n) {
     if (n > kTraceSlots) n = kTraceSlots;
-    cudaError_t e = cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * n * kTraceItems * 8);
+    const size_t words = (size_t)n * kTraceItems * 8;
+    if (!g_trace_buf) {   // nothing traced yet
+        memset(host, 0, 2 * words * sizeof(unsigned long long));
+        return cudaSuccess;
+    }
+    cudaError_t e = cudaMemcpy(host, g_trace_buf, words * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return e;
-    return cudaMemcpyFromSymbol(host + (size_t)n * kTraceItems * 8, g_trace2, sizeof(unsigned long long) * n * kTraceItems * 8);
+    return cudaMemcpy(host + words, g_trace_buf + kTraceWords, words * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
 }
 
 cudaError_t warm_chain_kernel() {
@@ -646,13 +656,21 @@ cudaError_t launch_chain(const ChainArgs& a, cudaStream_t s) {
     }
     cudaError_t e = smem_attr_once<chain_kernel>(kSmem);
     if (e != cudaSuccess) return e;
+    ChainArgs args = a;
+    if (args.trace_slot >= 0) {
+        if (!g_trace_buf) {
+            if ((e = cudaMalloc(&g_trace_buf, 2 * kTraceWords * sizeof(unsigned long long))) != cudaSuccess) return e;
+            if ((e = cudaMemset(g_trace_buf, 0, 2 * kTraceWords * sizeof(unsigned long long))) != cudaSuccess) return e;
+        }
+        args.trace = g_trace_buf;
+    }
     static int sms = 0;
     if (!sms) {
         int dev = 0;
         if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
         if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
     }
-    return launch_pdl(chain_kernel, dim3(sms), dim3(192), kSmem, s, a.pdl != 0, a);
+    return launch_pdl(chain_kernel, dim3(sms), dim3(192), kSmem, s, a.pdl != 0, args);
 }
 
 }  // namespace pb

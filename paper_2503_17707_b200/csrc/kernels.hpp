@@ -150,6 +150,7 @@ struct alignas(64) ChainArgs {
     float* part;               // split-K partial tiles: max over jobs of S * tiles * 128 * 128 fp32
     int pdl;
     int trace_slot;            // >= 0: record per-item timestamps in launch slot trace_slot (debug)
+    unsigned long long* trace; // set by launch_chain when tracing
 };
 cudaError_t chain_trace_copy(unsigned long long* host, int n_slots);
 int chain_norm_ok(int d);                          // d within the norm item's register budget
