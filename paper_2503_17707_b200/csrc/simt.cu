@@ -315,40 +315,52 @@ __global__ void __launch_bounds__(256) logits_kernel(const __nv_bfloat16* __rest
 }
 
 // ------------------------------------------------------------------ argmax (lowest index wins ties)
-// One CTA per sequence; every thread keeps 8 loads in flight (strided, coalesced), then a butterfly per warp and
-// one over the warps. The (value, lowest index) maximum does not depend on the visiting order.
+// A cluster of AM_CTAS CTAs per sequence: CTA c scans the c-th slice of the row with 8 loads in flight per thread,
+// reduces it (butterfly per warp, then over the warps), and CTA 0 combines the slices' (value, index) pairs through
+// distributed shared memory. The (value, lowest index) maximum does not depend on the visiting order.
+constexpr int AM_CTAS = 8;
+
+__device__ __forceinline__ void am_better(float& best, int& bi, float ov, int oi) {
+    if (ov > best || (ov == best && oi < bi)) {
+        best = ov;
+        bi = oi;
+    }
+}
+
 __global__ void __launch_bounds__(1024) argmax_kernel(const float* __restrict__ logits, int V, int ldl,
                                                       int32_t* tokens, int32_t* nan_flag) {
     pdl_launch_dependents();
     pdl_wait();
     __shared__ float sv[32];
     __shared__ int si[32];
-    const float* x = logits + (size_t)blockIdx.x * ldl;
+    __shared__ float cv;   // this CTA's slice result, read by CTA 0 of the cluster
+    __shared__ int ci;
+    uint32_t crank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+    const float* x = logits + (size_t)blockIdx.y * ldl;
+    const int per = (V + AM_CTAS - 1) / AM_CTAS, lo = (int)crank * per, hi = min(V, lo + per);
     float best = -CUDART_INF_F;
     int bi = 0x7fffffff;
     bool bad = false;
     constexpr int U = 8;
-    for (int v = threadIdx.x; v < V; v += U * blockDim.x) {
+    for (int v = lo + threadIdx.x; v < hi; v += U * blockDim.x) {
         float f[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int vv = v + u * blockDim.x;
-            f[u] = vv < V ? x[vv] : -CUDART_INF_F;
+            f[u] = vv < hi ? x[vv] : -CUDART_INF_F;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int vv = v + u * blockDim.x;
-            if (vv >= V) break;
+            if (vv >= hi) break;
             if (!isfinite(f[u])) bad = true;
-            if (f[u] > best || (f[u] == best && vv < bi)) { best = f[u]; bi = vv; }
+            am_better(best, bi, f[u], vv);
         }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const float ov = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
-    }
+    for (int o = 16; o > 0; o >>= 1)
+        am_better(best, bi, __shfl_xor_sync(0xffffffffu, best, o), __shfl_xor_sync(0xffffffffu, bi, o));
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     if (l == 0) { sv[w] = best; si[w] = bi; }
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nan_flag, 1);
@@ -356,13 +368,28 @@ __global__ void __launch_bounds__(1024) argmax_kernel(const float* __restrict__ 
         best = l < (blockDim.x >> 5) ? sv[l] : -CUDART_INF_F;
         bi = l < (blockDim.x >> 5) ? si[l] : 0x7fffffff;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const float ov = __shfl_xor_sync(0xffffffffu, best, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-            if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
-        }
-        if (l == 0) tokens[blockIdx.x] = bi == 0x7fffffff ? 0 : bi;
+        for (int o = 16; o > 0; o >>= 1)
+            am_better(best, bi, __shfl_xor_sync(0xffffffffu, best, o), __shfl_xor_sync(0xffffffffu, bi, o));
+        if (l == 0) { cv = best; ci = bi; }
     }
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (crank == 0 && w == 0) {
+        float ov = -CUDART_INF_F;
+        int oi = 0x7fffffff;
+        if (l < AM_CTAS) {
+            uint32_t av, ai;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(av) : "r"((uint32_t)__cvta_generic_to_shared(&cv)), "r"(l));
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ai) : "r"((uint32_t)__cvta_generic_to_shared(&ci)), "r"(l));
+            asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(ov) : "r"(av) : "memory");
+            asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(oi) : "r"(ai) : "memory");
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+            am_better(ov, oi, __shfl_xor_sync(0xffffffffu, ov, o), __shfl_xor_sync(0xffffffffu, oi, o));
+        if (l == 0) tokens[blockIdx.y] = oi == 0x7fffffff ? 0 : oi;
+    }
+    // keep every CTA's shared slice result alive until CTA 0 has read it
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 // ------------------------------------------------------------------ cross-rank readiness words
@@ -482,7 +509,21 @@ cudaError_t launch_logits(const __nv_bfloat16* y, int B, int d, const __nv_bfloa
 
 cudaError_t launch_argmax(const float* logits, int B, int V, int ldl, int32_t* tokens, int32_t* nan_flag,
                           cudaStream_t s, bool pdl) {
-    return launch_pdl(argmax_kernel, B, 1024, 0, s, pdl, logits, V, ldl, tokens, nan_flag);
+    if (B <= 0) return cudaSuccess;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(AM_CTAS, B);
+    cfg.blockDim = dim3(1024);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = AM_CTAS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 2 : 1;
+    return cudaLaunchKernelEx(&cfg, argmax_kernel, logits, V, ldl, tokens, nan_flag);
 }
 
 cudaError_t launch_signal(const SignalTargets& t, uint32_t value, cudaStream_t s) {

@@ -206,6 +206,29 @@ def test_rope():
         assert np.array_equal(got[rows, qd + kvd:], xf[rows, qd + kvd:])
 
 
+def test_argmax_large_vocab_ties_across_slices():
+    """The argmax kernel splits a row over a cluster of CTAs: an exact tie between two slices resolves to the lowest
+    index, the maximum in the last (ragged) slice is found, and a NaN anywhere raises the flag."""
+    need_gpu()
+    rng = np.random.default_rng(4)
+    V = 50272
+    lg = rng.standard_normal((3, V)).astype(np.float32)
+    lg[0, 40000] = lg[0, 7] = 50.0          # tie across slices
+    lg[1, V - 1] = 60.0                     # last element of the ragged last slice
+    lg[2, 25000] = 70.0
+    toks = torch.zeros(3, dtype=torch.int32, device="cuda")
+    nan = torch.zeros(1, dtype=torch.int32, device="cuda")
+    lgd = dev_f32(lg)
+    B.pb_op_argmax(ptr(lgd), 3, V, V, ptr(toks), ptr(nan), stream())
+    torch.cuda.synchronize()
+    assert toks.cpu().tolist() == [7, V - 1, 25000] and nan.item() == 0
+    lg[1, 33333] = np.nan
+    lgd = dev_f32(lg)
+    B.pb_op_argmax(ptr(lgd), 3, V, V, ptr(toks), ptr(nan), stream())
+    torch.cuda.synchronize()
+    assert nan.item() == 1
+
+
 def test_logits_argmax_embed():
     need_gpu()
     rng = np.random.default_rng(9)
