@@ -51,11 +51,18 @@ def parse():
     ap.add_argument("--prefill-chunks", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
-    ap.add_argument("--cpu-sample-layers", type=int, default=4)
+    ap.add_argument("--cpu-sample-layers", type=int, default=0,
+                    help="decoder layers the CPU oracle baseline runs (0 = the whole model when it fits ~30 s of "
+                         "CPU work — C1, C2 — else 4 layers extrapolated linearly)")
+    ap.add_argument("--ref-sample-layers", type=int, default=4,
+                    help="--impl reference: decoder layers per step (a bounded sample, extrapolated to the model)")
     ap.add_argument("--host-alias", type=int, default=0,
                     help="host_alias_layers K: layer l is DMA'd from the host image of layer l mod K (DRAM-limited boxes)")
     ap.add_argument("--dist-backend", default="nccl", help="torch.distributed backend for barriers/handle exchange")
     ap.add_argument("--same-gpu", action="store_true", help="all ranks on cuda:0 (testing the N>1 path on one GPU)")
+    ap.add_argument("--check-oracle", action="store_true",
+                    help="compare the last timed step's first-token logits with the stored full-depth oracle "
+                         "(tests/golden/oracle_<workload>[_K<k>].npz) and add 'parity' to the line")
     args = ap.parse_args()
     # the same defaults on both arms (the reference arm reports this configuration too)
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
@@ -159,17 +166,22 @@ def run_reference(args):
         return
     from synth.configs import WORKLOADS
     w = WORKLOADS[args.workload]
-    vals = []
+    vals, walls = [], []
     det = None
     for i in range(args.warmup + args.steps):
-        v, det = oracle_sample(w, args.cpu_sample_layers)
+        t0 = time.perf_counter()
+        v, det = oracle_sample(w, args.ref_sample_layers)
         if i >= args.warmup:
             vals.append(v)
+            walls.append((time.perf_counter() - t0) * 1e3)
     val = statistics.mean(vals)
-    sample = (f"{det['sample_layers']} of {det['layers']} layers + embed/head, B={w.batch} T={w.seq}, "
-              f"extrapolated linearly in layers")
+    extrap = det["sample_layers"] < det["layers"]
+    sample = (f"{det['sample_layers']} of {det['layers']} layers + embed/head, B={w.batch} T={w.seq}"
+              + (", extrapolated linearly in layers (value); ms_per_step = the sample actually run per step"
+                 if extrap else ", whole model"))
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "ms", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": val, "higher_is_better": False,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.mean(walls),
+            "extrapolated": extrap, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64 (bf16 storage contract)",
             "data": "synthetic (seeded splitmix64; HF init std 0.02)",
             "config": workload_config(w, args, 1),
@@ -250,25 +262,23 @@ class ClockSampler:
 # our arm
 # ----------------------------------------------------------------------------------------------------
 
-def measure_h2d(nbytes=1 << 30, chunk=64 << 20):
-    """Concurrent pinned H2D GB/s of this rank's GPU (2 copy streams, 64 MB chunks): the PCIe roofline constant."""
+def measure_h2d(nbytes=2 << 30, chunk=128 << 20):
+    """Concurrent pinned H2D GB/s of this rank's GPU on the load's own lane shape: ONE stream, copies of the load's
+    group size (chunk), 2 GiB, best of 4 after a warm-up (all ranks at once): the PCIe roofline constant."""
     import torch
+    chunk = max(1 << 20, min(chunk, nbytes))
     host = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
     dev = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
-    ss = [torch.cuda.Stream(), torch.cuda.Stream()]
+    st = torch.cuda.Stream()
     best = 0.0
-    for r in range(4):
+    for r in range(5):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(ss[0])
-        ss[1].wait_event(e0)
-        for i, off in enumerate(range(0, nbytes, chunk)):
-            with torch.cuda.stream(ss[i & 1]):
+        with torch.cuda.stream(st):
+            e0.record(st)
+            for off in range(0, nbytes, chunk):
                 dev[off:off + chunk].copy_(host[off:off + chunk], non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record(ss[1])
-        ss[0].wait_event(ev)
-        e1.record(ss[0])
+            e1.record(st)
         torch.cuda.synchronize()
         if r:
             best = max(best, nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9)
@@ -293,11 +303,27 @@ def load_peaks():
     return 6650.0, 1590.0, 1400.0, "fallback"
 
 
+def self_launch(args):
+    """`python bench.py --gpus N` with N > 1 outside torchrun: re-launch this command as N processes, one per GPU,
+    through torch.distributed.run on 127.0.0.1 (the same launch line the driver uses), and exit with its code."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        self_launch(args)
+    if args.same_gpu and args.dist_backend == "nccl":
+        args.dist_backend = "gloo"   # NCCL refuses two ranks on one device; gloo carries the host-side plumbing
     import torch
     import torch.distributed as dist
 
@@ -373,14 +399,15 @@ def main():
     toks = synth.tokens(w.batch, w.seq, w.model.vocab)
 
     barrier()
-    h2d_gbs = measure_h2d()          # all ranks concurrently: the PCIe roofline constant
+    h2d_gbs = measure_h2d(chunk=args.chunk_mb << 20)   # all ranks concurrently: the PCIe roofline constant
     barrier()
     agg_h2d = allsum(h2d_gbs)
 
     clocks = ClockSampler()
     ttft, e2e, ready, full, load_done, warm, launches = [], [], [], [], [], [], 0
+    recv_gbs, load_gbs_rank, stage_span = [], [], []
     kstats = {}
-    out_tokens = None
+    out_tokens = out_logits = None
     for step in range(args.warmup + args.steps):
         timed = step >= args.warmup
         eng.invalidate()
@@ -391,19 +418,26 @@ def main():
         th0 = time.perf_counter()
         eng.enqueue(3 * step + 1, toks if rank == 0 else None, w.batch, w.seq, adapter_id=adapter_id,
                     adapter_of_seq=aos)
-        res = eng.wait()
+        last = step == args.warmup + args.steps - 1
+        res = eng.wait(want_logits=args.check_oracle and last)
         th1 = time.perf_counter()
         barrier()
         torch.cuda.synchronize()
         tl = eng.timeline()
         if rank == 0:
             out_tokens = res[0]
+            if last and args.check_oracle:
+                out_logits = res[1]
         if timed:
             ttft.append(allmax(tl["ttft_ms"]))
             e2e.append(allmax((th1 - th0) * 1e3))
             ready.append(allmax(tl["t_ready_ms"]))
             full.append(allmax(tl["t_full_ms"]))
             load_done.append(allmax(tl["load_done_ms"]))
+            # NVLink ingress of this rank over its receive window (t0 -> its T_full), summed over ranks
+            recv_gbs.append(allsum(tl["recv_bytes"] / max(tl["t_full_ms"], 1e-6) / 1e6))
+            load_gbs_rank.append(allmax(tl["load_bytes"] / max(tl["load_done_ms"], 1e-6) / 1e6))
+            stage_span.append(allmax(max(0.0, tl["stage_end_ms"] - tl["stage_begin_ms"])))
             launches += int(allsum(tl["n_launches"]))
             # warm prefill on the now-resident weights, no per-kernel events: the pipelined prefill alone
             # (the single-GPU-resident regime after T_full), device clock t0 -> token D2H
@@ -427,6 +461,9 @@ def main():
                     for f in a:
                         a[f] += v[f]
     clk = clocks.stop() if rank == 0 else None
+    # prefill tensor-core FLOPs per step over all ranks (each rank profiles its own stage) for T_comp
+    my_flops = sum(kstats.get(k, {}).get("flops", 0.0) for k in ("gemm", "attention")) / max(1, args.steps)
+    all_flops = allsum(my_flops)
 
     if rank == 0:
         hbm, bf16_burst, bf16_sus, peak_src = load_peaks()
@@ -459,6 +496,14 @@ def main():
                     "timing": "CUDA events per launch on the launching stream, warm re-run of the step's prefill "
                               "(pb_prefill_replay) after each timed cold start"}
         t_pcie = S / (agg_h2d * 1e9) * 1e3
+        load_gbs = S / (statistics.mean(load_done) * 1e-3) / 1e9
+        # roofline = max(T_pcie, T_nv, T_comp). T_nv: every GPU ingests (N-1)/N of S over NVLink
+        # (900 GB/s per direction nominal, B200 NVLink 5); T_comp: the prefill FLOPs spread over N GPUs at the
+        # measured sustained tensor peak (the serial chain is a scheduling hazard, not a bound).
+        nv_peak = 900.0
+        t_nv = ((world - 1) / world) * S / (nv_peak * 1e9) * 1e3 if world > 1 else 0.0
+        t_comp = all_flops / (world * bf16_sus * 1e12) * 1e3
+        bound = max(t_pcie, t_nv, t_comp)
         line = {
             "metric": METRIC, "value": val, "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": val, "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
@@ -469,22 +514,48 @@ def main():
             "gpu_launches": launches,
             "clocks": clk,
             "roofline": roof,
-            "pcie_roofline": {"bound_ms": t_pcie, "bytes": S, "h2d_gbs_per_gpu_measured": h2d_gbs,
-                              "h2d_gbs_aggregate": agg_h2d, "frac": t_pcie / val,
-                              "load_gbs_aggregate": S / (statistics.mean(load_done) * 1e-3) / 1e9},
+            "pcie_roofline": {"bound_ms": bound, "bound": ("pcie" if bound == t_pcie else
+                                                            "nvlink" if bound == t_nv else "compute"),
+                              "t_pcie_ms": t_pcie, "t_nv_ms": t_nv, "t_comp_ms": t_comp, "bytes": S,
+                              "h2d_gbs_per_gpu_measured": h2d_gbs, "h2d_gbs_aggregate": agg_h2d,
+                              "h2d_measured_on": f"one stream, {args.chunk_mb} MB copies (the load's lane and group size)",
+                              "frac": bound / val, "load_gbs_aggregate": load_gbs,
+                              "load_frac_of_measured_link": load_gbs / agg_h2d,
+                              "load_gbs_per_gpu_max": statistics.mean(load_gbs_rank),
+                              "nvlink_recv_gbs_aggregate": statistics.mean(recv_gbs) if world > 1 else 0.0,
+                              "nvlink_peak_gbs_per_gpu": nv_peak if world > 1 else None,
+                              "nvlink_bytes": int((world - 1) * S) if world > 1 else 0},
             "ttft_breakdown_ms": {"t_ready": statistics.mean(ready), "t_full": statistics.mean(full),
                                   "load_done": statistics.mean(load_done), "ttft_min": min(ttft),
                                   "ttft_median": statistics.median(ttft),
-                                  "prefill_warm": statistics.mean(warm)},
+                                  "prefill_warm": statistics.mean(warm),
+                                  "stage_span_max": statistics.mean(stage_span)},
             "kernels": kern,
             "first_tokens": [int(x) for x in out_tokens],
         }
+        if args.check_oracle:
+            gold = harness.load_golden(w.tag, args.host_alias)
+            if gold is None:
+                line["parity"] = {"unavailable": f"no {os.path.relpath(harness.golden_path(w.tag, args.host_alias), HERE)}"}
+            else:
+                rep = harness.golden_parity(gold, out_logits, out_tokens)
+                line["parity"] = {"rel": rep["max_rel"], "rel_exact": rep.get("max_rel_exact"),
+                                  "token_ok": all(rep["token_ok"]), "token_exact_match": all(rep["token_exact_match"]),
+                                  "min_margin": min(rep["margin"]), "gate": rep["gate"], "ok": rep["ok"],
+                                  "oracle": os.path.relpath(harness.golden_path(w.tag, args.host_alias), HERE)}
         if not args.no_cpu_baseline:
-            v, det = oracle_sample(w, args.cpu_sample_layers)
+            # whole model when it is ~30 s of CPU work at most (C1, C2: one fp64 forward ~2 x 0.3 TFLOP), else a
+            # 4-layer sample extrapolated linearly
+            flops = 2.0 * w.batch * w.seq * plan.sizes.dev_weight_bytes / 2
+            nl = args.cpu_sample_layers or (w.model.n_layers if flops < 1.2e12 else 4)
+            v, det = oracle_sample(w, nl)
+            whole = det["sample_layers"] == det["layers"]
             line["cpu_baseline"] = {"value": v, "unit": "ms", "cores": cpu_cores(), "kind": "oracle",
                                     "sample": f"{det['sample_layers']} of {det['layers']} layers + embed/head, "
-                                              f"B={w.batch} T={w.seq}, extrapolated linearly in layers",
-                                    "detail": det}
+                                              f"B={w.batch} T={w.seq}"
+                                              + (", whole model, timed once" if whole else
+                                                 ", extrapolated linearly in layers"),
+                                    "extrapolated": not whole, "detail": det}
         print(json.dumps(line), flush=True)
     barrier()
     eng.close()

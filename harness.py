@@ -29,3 +29,55 @@ def build_host_images(plan: Plan):
     ada = pinned_host(s.host_adapter_bytes) if s.host_adapter_bytes else None
     fill_host_images(plan, base.data_ptr(), ada.data_ptr() if ada is not None else None)
     return base, ada
+
+
+# ----------------------------------------------------------------------------------------------------
+# Full-depth parity against stored oracle logits (tests/golden/oracle_<tag>[_K<k>].npz, written by
+# tools/oracle_reference.py, which calls only oracle/).
+# ----------------------------------------------------------------------------------------------------
+
+def golden_path(tag: str, host_alias: int = 0) -> str:
+    import os
+    root = os.path.dirname(os.path.abspath(__file__))
+    return os.path.join(root, "tests", "golden", f"oracle_{tag}" + (f"_K{host_alias}" if host_alias else "") + ".npz")
+
+
+def load_golden(tag: str, host_alias: int = 0):
+    import os
+    import numpy as np
+    p = golden_path(tag, host_alias)
+    return dict(np.load(p)) if os.path.exists(p) else None
+
+
+def golden_parity(gold, logits, tokens, gate: float = 1e-2) -> dict:
+    """Compare GPU first-token logits [B, V] / tokens [B] with the stored oracle.
+
+    rel = ||g - o||_inf / ||o||_inf per sequence against the bf16-contract oracle (the gate) and,
+    when stored, against the exact fp64 oracle. Token rule G10: if the oracle's top-1 minus
+    top-2 margin exceeds 2*max|g - o| the GPU token must equal the oracle's argmax, otherwise the GPU token's
+    oracle logit must lie within 2*max|g - o| of the oracle maximum."""
+    import numpy as np
+    out = {"rel": [], "token_ok": [], "token_exact_match": [], "margin": [], "gate": gate}
+    ol = gold["logits_bf16"].astype(np.float64)
+    if "logits_exact" in gold:
+        out["rel_exact"] = []
+    for b in range(ol.shape[0]):
+        g = np.asarray(logits[b], dtype=np.float64)
+        err = float(np.abs(g - ol[b]).max())
+        out["rel"].append(err / float(np.abs(ol[b]).max()))
+        if "logits_exact" in gold:
+            oe = gold["logits_exact"][b].astype(np.float64)
+            out["rel_exact"].append(float(np.abs(g - oe).max() / np.abs(oe).max()))
+        srt = np.sort(ol[b])
+        margin = float(srt[-1] - srt[-2])
+        ot = int(np.argmax(ol[b]))
+        tk = int(tokens[b])
+        ok = tk == ot if margin > 2 * err else bool(ol[b][tk] >= srt[-1] - 2 * err)
+        out["token_ok"].append(bool(ok))
+        out["token_exact_match"].append(tk == ot)
+        out["margin"].append(margin)
+    out["max_rel"] = max(out["rel"])
+    if "rel_exact" in out:
+        out["max_rel_exact"] = max(out["rel_exact"])
+    out["ok"] = out["max_rel"] <= gate and all(out["token_ok"])
+    return out

@@ -190,7 +190,7 @@ typedef struct {
     void* adapters;       int64_t adapters_cap;   /* device, >= dev_adapter_bytes (may be NULL if no adapters) */
     void* adapted;        int64_t adapted_cap;    /* device, >= dev_adapted_bytes for PB_MERGE_ALL, else may be NULL */
     void* workspace;      int64_t workspace_cap;  /* device, >= pb_plan_workspace_bytes(max_batch, max_seq) */
-    int32_t max_batch, max_seq;
+    int32_t max_batch, max_seq;   /* sequences per trial 1..64 (batch 64 x 64 tokens); max_seq <= max_pos (OPT) */
     /* cudaStream_t handles, five DISTINCT streams per rank; NULL = the ctx creates and owns its own
      * non-blocking streams (recommended: torch's stream pool recycles handles across ranks). */
     void* stream_h2d[2];  /* cudaStream_t: copy-engine H2D lane(s) (one ordered lane is used) */
@@ -234,8 +234,13 @@ PB_API pb_status pb_trial_begin(pb_ctx* ctx, uint32_t epoch);
  * PB_ENOMEM (staging too small), PB_EPROTOCOL (a trial is being armed); read errors surface from the trial. */
 PB_API pb_status pb_ctx_set_file_source(pb_ctx* ctx, const char* path, void* staging, int64_t staging_bytes);
 
-/* a2 — enqueue this rank's load list: chunked cudaMemcpyAsync pinned host -> HBM,
- * alternating the two H2D streams; a `landed` event per chunk. Async. */
+/* a2 — arm this rank's load list ("GPU 0 reads A-0 while GPU 1 reads A-1"): chunked
+ * cudaMemcpyAsync pinned host -> HBM over this GPU's own PCIe link, on ONE ordered copy lane
+ * (stream_h2d[0]; measured on B200 the H2D engine drains one stream's queue before another's, so a second lane
+ * would only delay layers), consecutive contiguous chunks coalesced into copy groups <= chunk_bytes, a
+ * non-timing `landed` event per group. Load, merge and gather are armed in that order (PB_EPROTOCOL otherwise);
+ * the copies start when the trial is fully armed, i.e. in pb_gather_layers, because each chunk's merge and peer
+ * signal are issued right behind its copy group by the same per-rank issuer thread. Async. */
 PB_API pb_status pb_load_shard(pb_ctx* ctx);
 
 /* a3 — arm the LoRA merge of every adapted row range this rank loaded (tcgen05 kernel,
@@ -248,9 +253,14 @@ PB_API pb_status pb_load_shard(pb_ctx* ctx);
 #define PB_MERGE_ALL (-2)
 PB_API pb_status pb_merge_lora(pb_ctx* ctx, int32_t adapter_id);
 
-/* a4 — enqueue this rank's receive list: for each chunk, wait for the loader's
- * ready word (merged or landed), then copy peer HBM -> local HBM over NVLink
- * (copy engine). Stage-needed chunks first, then rotation (g+i) mod N. Async. */
+/* a4 — arm this rank's receive list (here over NVLink): for each chunk, wait (device-side) for
+ * the loader's readiness word (merged or landed), then copy peer HBM -> local HBM (copy engine, stream_nvlink).
+ * Stage-needed chunks first, then rotation (g+i) mod N. With the trial fully armed this call
+ * STARTS ISSUING it: a per-rank issuer thread enqueues the copy groups, the merges of each chunk as it lands
+ * and the receive copies (pro rata to the load) without waiting for a prompt, so load -> merge -> gather ->
+ * pb_sync reaches T_full on its own. A prompt posted later (pb_prefill_enqueue) joins the same issuer: its
+ * compute items are interleaved with the loads still in flight (the prefill starts as soon as its layers are
+ * resident, "begins serving ... while asynchronously loading the remaining parts"). Async. */
 PB_API pb_status pb_gather_layers(pb_ctx* ctx);
 
 /* a5 — pipelined first-token prefill. Every rank calls it (SPMD). tokens: host
@@ -344,6 +354,12 @@ typedef struct {
                                       * copy lane cost ~20 us each), else -1 (load_done_ms is always set) */
     const double* chunk_gathered_ms; /* [n_chunks], -1 where not received by this rank */
     int32_t n_launches;      /* kernels this rank launched in the trial */
+    const double* chunk_merged_ms;   /* [n_chunks], own chunk's merges (and peer signal) done; timing mode only
+                                      * (PB_LANDED_TIMING=1), else -1 */
+    double stage_begin_ms;   /* first layer kernel of this rank's stage started (compute stream; -1 if no stage) */
+    double stage_end_ms;     /* last layer of the stage done for every microbatch / prompt chunk */
+    double ctx_create_ms;    /* host time pb_ctx_create took (tables, TMA maps, events, pinned staging): part of the
+                              * init breakdown excluded from t0 ("Init Meta") */
 } pb_timeline_t;
 PB_API pb_status pb_timeline(pb_ctx* ctx, pb_timeline_t* out);
 
@@ -369,6 +385,17 @@ PB_API pb_status pb_kernel_trace(pb_ctx* ctx, pb_kernel_event* out, int32_t cap,
 
 PB_API const char* pb_last_error(void);
 PB_API void pb_ctx_free(pb_ctx* ctx);
+
+/* f1 support — abandon the current trial after a peer has died mid-load (the survivors re-plan and
+ * resume). Cross-rank dependencies are device-side waits on readiness words only peers write, so a dead peer
+ * would leave this rank's streams blocked forever. pb_ctx_abort stops the issuer thread at its next poll, then
+ * forces every readiness word of this rank's workspace open (0xFFFFFFFF >= any epoch) so the blocked streams
+ * drain (their remaining kernels compute on whatever bytes are there; nothing is published as valid), and
+ * marks the ctx aborted: every later call except pb_ctx_free returns PB_EPROTOCOL. pb_ctx_free of an aborted
+ * ctx waits at most a few seconds per stream instead of synchronizing the device. The weight / adapter buffers
+ * (caller-owned) keep whatever chunks had landed; pb_timeline before the abort tells which (chunk_landed_ms),
+ * and Plan.replan + a new ctx with those buffers resumes. Errors: PB_EINVAL (null), PB_ECUDA. */
+PB_API pb_status pb_ctx_abort(pb_ctx* ctx);
 
 #ifdef __cplusplus
 }

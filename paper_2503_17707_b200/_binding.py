@@ -74,7 +74,9 @@ class pb_timeline_t(C.Structure):
     _fields_ = [("t_ready_ms", C.c_double), ("t_full_ms", C.c_double), ("ttft_ms", C.c_double),
                 ("load_done_ms", C.c_double), ("load_bytes", C.c_int64), ("recv_bytes", C.c_int64),
                 ("n_chunks", C.c_int32), ("chunk_landed_ms", C.POINTER(C.c_double)),
-                ("chunk_gathered_ms", C.POINTER(C.c_double)), ("n_launches", C.c_int32)]
+                ("chunk_gathered_ms", C.POINTER(C.c_double)), ("n_launches", C.c_int32),
+                ("chunk_merged_ms", C.POINTER(C.c_double)), ("stage_begin_ms", C.c_double),
+                ("stage_end_ms", C.c_double), ("ctx_create_ms", C.c_double)]
 
 
 class pb_kernel_stat(C.Structure):
@@ -124,6 +126,7 @@ _SIGS = {
     "pb_sync": [_P],
     "pb_timeline": [_P, C.POINTER(pb_timeline_t)],
     "pb_ctx_free": [_P],
+    "pb_ctx_abort": [_P],
     "pb_ctx_set_profiling": [_P, C.c_int32],
     "pb_kernel_stats": [_P, C.POINTER(pb_kernel_stat), C.c_int32, C.POINTER(C.c_int32)],
     "pb_kernel_trace": [_P, C.POINTER(pb_kernel_event), C.c_int32, C.POINTER(C.c_int32)],
@@ -394,6 +397,10 @@ def pb_kernel_trace(ctx):
 
 def pb_ctx_free(ctx):
     lib().pb_ctx_free(ctx)
+
+
+def pb_ctx_abort(ctx):
+    check(lib().pb_ctx_abort(ctx))
 
 
 # --------------------------------------------------------------------------

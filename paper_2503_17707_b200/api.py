@@ -271,7 +271,37 @@ class RankEngine:
                 "load_done_ms": t.load_done_ms, "load_bytes": t.load_bytes, "recv_bytes": t.recv_bytes,
                 "n_launches": t.n_launches,
                 "chunk_landed_ms": np.ctypeslib.as_array(t.chunk_landed_ms, shape=(n,)).copy() if n else np.zeros(0),
-                "chunk_gathered_ms": np.ctypeslib.as_array(t.chunk_gathered_ms, shape=(n,)).copy() if n else np.zeros(0)}
+                "chunk_gathered_ms": np.ctypeslib.as_array(t.chunk_gathered_ms, shape=(n,)).copy() if n else np.zeros(0),
+                "chunk_merged_ms": np.ctypeslib.as_array(t.chunk_merged_ms, shape=(n,)).copy() if n else np.zeros(0),
+                "stage_begin_ms": t.stage_begin_ms, "stage_end_ms": t.stage_end_ms, "ctx_create_ms": t.ctx_create_ms}
+
+    def arm(self, epoch: int, adapter_id: int = 0):
+        """Start a cold start with no prompt yet: a2 load, a3 merge, a4 gather are issued at once (the rank reaches
+        T_full on its own); a prompt given later with post_prompt() joins the loads still in flight."""
+        with torch.cuda.device(self.device):
+            B.pb_trial_begin(self.ctx, epoch)
+            B.pb_load_shard(self.ctx)
+            B.pb_merge_lora(self.ctx, adapter_id)
+            B.pb_gather_layers(self.ctx)
+
+    def post_prompt(self, tokens: Optional[np.ndarray], batch: int, seq: int):
+        """a5 for an armed trial (see arm); complete with wait()."""
+        self._batch = batch
+        with torch.cuda.device(self.device):
+            tp = None
+            if tokens is not None:
+                self._tok = np.ascontiguousarray(tokens, dtype=np.int32)
+                tp = self._tok.ctypes.data
+            B.pb_prefill_enqueue(self.ctx, tp, batch, seq)
+
+    def sync(self):
+        with torch.cuda.device(self.device):
+            B.pb_sync(self.ctx)
+
+    def abort(self):
+        """f1: abandon the trial after a peer died (pb_ctx_abort); only close() remains."""
+        with torch.cuda.device(self.device):
+            B.pb_ctx_abort(self.ctx)
 
     def weights_bytes(self) -> np.ndarray:
         return self.weights.cpu().numpy()

@@ -75,6 +75,8 @@ pb_status check_ctx(pb_ctx* c, const char* fn) {
     if (!c) return fail(PB_EINVAL, "%s: null ctx", fn);
     cudaError_t e = cudaSetDevice(c->device);
     if (e != cudaSuccess) return fail(PB_ECUDA, "%s: cudaSetDevice: %s", fn, cudaGetErrorString(e));
+    if (c->aborted && strcmp(fn, "pb_timeline") != 0 && strcmp(fn, "pb_ctx_abort") != 0)
+        return fail(PB_EPROTOCOL, "%s: the ctx was aborted (pb_ctx_abort); only pb_ctx_free remains", fn);
     return PB_OK;
 }
 
@@ -135,7 +137,8 @@ WsLayout pb::ws_layout(const pb_plan* p, int32_t batch, int32_t seq) {
     L.f_land = L.f_logit + p->n_gpus;
     L.f_tensor = L.f_land + (int32_t)p->chunks.size();
     L.f_tensor_recv = L.f_tensor + (int32_t)p->tensors.size();
-    L.n_words = L.f_tensor_recv + (int32_t)p->tensors.size();
+    L.f_gdone = L.f_tensor_recv + (int32_t)p->tensors.size();
+    L.n_words = L.f_gdone + p->n_gpus;
     int64_t o = 0;
     L.flags = o;   o = al(o + 4 * (int64_t)L.n_words);
     L.tokens = o;  o = al(o + 4 * rows);
@@ -173,7 +176,7 @@ WsLayout pb::ws_layout(const pb_plan* p, int32_t batch, int32_t seq) {
 
 extern "C" pb_status pb_plan_workspace_bytes(const pb_plan* p, int32_t batch, int32_t seq, int64_t* out) {
     if (!p || !out) return fail(PB_EINVAL, "pb_plan_workspace_bytes: null argument");
-    if (batch < 1 || batch > 8 || seq < 1) return fail(PB_EINVAL, "batch must be in [1, 8] and seq >= 1");
+    if (batch < 1 || batch > kMaxBatch || seq < 1) return fail(PB_EINVAL, "batch must be in [1, %d] and seq >= 1", kMaxBatch);
     if (p->model.arch == PB_ARCH_OPT && seq > p->model.max_pos) return fail(PB_EINVAL, "seq > max_pos");
     *out = ws_layout(p, batch, seq).total;
     return PB_OK;
@@ -213,8 +216,10 @@ static pb_status build_merge_jobs(pb_ctx* c) {
                 j.cols = mr.cols;
                 j.rank = rank;
                 j.scale = p->adapters[mr.adapter].alpha / (float)rank;
-                j.need = achunks[mr.a_tensor];
-                j.need.insert(j.need.end(), achunks[mr.b_tensor].begin(), achunks[mr.b_tensor].end());
+                // factor chunks this rank already holds (a re-plan's resident set) have nothing to wait for
+                for (const auto* v : {&achunks[mr.a_tensor], &achunks[mr.b_tensor]})
+                    for (int32_t a : *v)
+                        if (!p->is_resident(c->rank, a)) j.need.push_back(a);
                 char* W = c->weights + bt.dev_off + (int64_t)ra * bt.row_bytes();
                 char* Wout = inplace ? W
                                      : c->adapted + p->adapted_off[mr.adapter * NT + mr.base] +
@@ -325,6 +330,7 @@ static pb_status build_prefill_maps(pb_ctx* c) {
 extern "C" pb_status pb_ctx_create(const pb_plan* plan, int32_t rank, const void* host_base, const void* host_adapters,
                                    const pb_rank_bufs* bufs, pb_ctx** out) {
     PB_TRY_BEGIN
+    const auto t_create = std::chrono::steady_clock::now();
     if (!plan || !host_base || !bufs || !out) return fail(PB_EINVAL, "pb_ctx_create: null argument");
     *out = nullptr;
     if (rank < 0 || rank >= plan->n_gpus) return fail(PB_EINVAL, "rank %d out of [0, %d)", rank, plan->n_gpus);
@@ -332,8 +338,8 @@ extern "C" pb_status pb_ctx_create(const pb_plan* plan, int32_t rank, const void
         return fail(PB_ENOMEM, "weights buffer: need %lld bytes", (long long)plan->dev_weight_bytes);
     if (!plan->adapters.empty() && (!bufs->adapters || bufs->adapters_cap < plan->host_adapter_bytes || !host_adapters))
         return fail(PB_ENOMEM, "adapters buffer: need %lld bytes (and a host image)", (long long)plan->host_adapter_bytes);
-    if (bufs->max_batch < 1 || bufs->max_batch > 8 || bufs->max_seq < 1)
-        return fail(PB_EINVAL, "max_batch must be in [1, 8], max_seq >= 1");
+    if (bufs->max_batch < 1 || bufs->max_batch > kMaxBatch || bufs->max_seq < 1)
+        return fail(PB_EINVAL, "max_batch must be in [1, %d], max_seq >= 1", kMaxBatch);
     if (plan->model.arch == PB_ARCH_OPT && bufs->max_seq > plan->model.max_pos)
         return fail(PB_EINVAL, "max_seq %d > max_pos %d", bufs->max_seq, plan->model.max_pos);
     const int hd = plan->head_dim();
@@ -410,17 +416,23 @@ extern "C" pb_status pb_ctx_create(const pb_plan* plan, int32_t rank, const void
     c->gathered.assign(NC, nullptr);
     c->tl_landed.assign(NC, -1.0);
     c->tl_gathered.assign(NC, -1.0);
+    c->tl_merged.assign(NC, -1.0);
+    c->merged_ev.assign(NC, nullptr);
     // Events only where the timeline needs a timestamp (measured on B200: a timing-event record costs
     // ~20 us while the PCIe link is saturated by the load); dependencies are device-side readiness words.
     auto mk = [&](cudaEvent_t* e) { return cudaEventCreate(e); };
     if (mk(&c->t0) || mk(&c->merge_done) || mk(&c->gather_done) || mk(&c->done) || mk(&c->ready_merge) ||
-        mk(&c->ready_recv) || cudaEventCreateWithFlags(&c->tok_ev, cudaEventDisableTiming))
+        mk(&c->ready_recv) || mk(&c->stage_begin) || mk(&c->stage_end) ||
+        cudaEventCreateWithFlags(&c->tok_ev, cudaEventDisableTiming))
         return cleanup(fail(PB_ECUDA, "cudaEventCreate failed"));
     if (const char* lt = getenv("PB_LANDED_TIMING")) c->landed_timing = atoi(lt) != 0;
     if (mk(&c->load_end)) return cleanup(fail(PB_ECUDA, "cudaEventCreate failed"));
-    for (int32_t id : plan->load[rank])
+    for (int32_t id : plan->load[rank]) {
         if (c->landed_timing ? mk(&c->landed[id]) : cudaEventCreateWithFlags(&c->landed[id], cudaEventDisableTiming))
             return cleanup(fail(PB_ECUDA, "cudaEventCreate failed"));
+        if (c->landed_timing && !plan->chunks[id].is_adapter && mk(&c->merged_ev[id]))
+            return cleanup(fail(PB_ECUDA, "cudaEventCreate failed"));
+    }
     c->budget_events.assign(4 * kEventPool, nullptr);
     for (auto& e : c->budget_events)
         if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming)) return cleanup(fail(PB_ECUDA, "cudaEventCreate failed"));
@@ -471,19 +483,42 @@ extern "C" pb_status pb_ctx_create(const pb_plan* plan, int32_t rank, const void
         cudaMemset(c->ws + L.chain_ctl, 0, (size_t)(L.chain_part - L.chain_ctl)) != cudaSuccess ||
         cudaDeviceSynchronize() != cudaSuccess)
         return cleanup(fail(PB_ECUDA, "flag init failed"));
+    c->ctx_create_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_create).count();
     *out = c;
     return PB_OK;
     PB_TRY_END
 }
 
+// Wait (polling, at most `seconds`) for a stream to drain; false if it did not.
+static bool drain_stream(cudaStream_t s, double seconds) {
+    const auto t = std::chrono::steady_clock::now();
+    for (;;) {
+        const cudaError_t q = cudaStreamQuery(s);
+        if (q != cudaErrorNotReady) { cudaGetLastError(); return true; }
+        if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t).count() > seconds) return false;
+        std::this_thread::sleep_for(std::chrono::microseconds(200));
+    }
+}
+
 extern "C" void pb_ctx_free(pb_ctx* c) {
     if (!c) return;
+    c->abort_req.store(c->aborted);
     join_load(c);
     cudaSetDevice(c->device);
-    cudaDeviceSynchronize();
+    if (c->aborted) {
+        // after pb_ctx_abort the streams drain on their own (readiness words forced open); a stream that does not
+        // drain in time is leaked rather than handed to the next context (it may still run this trial's work)
+        std::vector<cudaStream_t> keep;
+        for (auto st : c->owned_streams)
+            if (drain_stream(st, 5.0)) keep.push_back(st);
+        c->owned_streams.swap(keep);
+    } else {
+        cudaDeviceSynchronize();
+    }
     auto d = [](cudaEvent_t e) { if (e) cudaEventDestroy(e); };
     d(c->t0); d(c->merge_done); d(c->gather_done); d(c->done); d(c->ready_merge); d(c->ready_recv); d(c->tok_ev);
-    d(c->load_end);
+    d(c->load_end); d(c->stage_begin); d(c->stage_end);
+    for (auto e : c->merged_ev) d(e);
     for (auto e : c->budget_events) d(e);
     for (auto st : c->owned_streams) stream_give(c->device, st);
     for (auto e : c->landed) d(e);
@@ -686,11 +721,16 @@ extern "C" pb_status pb_kernel_trace(pb_ctx* c, pb_kernel_event* out, int32_t ca
     return PB_OK;
 }
 
+static pb_status start_load_issuer(pb_ctx* c);
+
 extern "C" pb_status pb_trial_begin(pb_ctx* c, uint32_t epoch) {
     pb_status st = check_ctx(c, "pb_trial_begin");
     if (st) return st;
+    if (c->aborted) return fail(PB_EPROTOCOL, "pb_trial_begin: the ctx was aborted (pb_ctx_free it)");
     if (epoch <= c->epoch) return fail(PB_EINVAL, "epoch %u must exceed the previous %u", epoch, c->epoch);
     join_load(c);
+    c->run.reset();
+    c->posted.store(false);
     for (int r = 0; r < c->n; ++r)
         if (!c->peers[r].linked) return fail(PB_EPROTOCOL, "peer %d not wired (import/link)", r);
     c->epoch = epoch;
@@ -733,7 +773,7 @@ extern "C" pb_status pb_merge_lora(pb_ctx* c, int32_t adapter_id) {
         if (c->n > 1 && c->plan->opts.policy != PB_LOAD_STAGE)
             return fail(PB_EUNSUPPORTED, "PB_MERGE_ALL with n_gpus > 1 needs the STAGE policy (stage owner = loader)");
     }
-    c->merge_adapter = adapter_id;
+    c->merge_adapter = c->cold_adapter = adapter_id;
     c->phase = Phase::Merged;
     return PB_OK;
 }
@@ -744,7 +784,10 @@ extern "C" pb_status pb_gather_layers(pb_ctx* c) {
     if (c->phase != Phase::Merged) return fail(PB_EPROTOCOL, "pb_gather_layers: call pb_merge_lora first");
     for (int32_t id : c->plan->recv[c->rank]) c->recv_bytes += c->plan->chunks[id].bytes;
     c->phase = Phase::Gathered;
-    return PB_OK;
+    // load, merge and gather are armed: start issuing them now (copy lane, merges as chunks land, receive copies
+    // as peers publish); a prompt posted later (pb_prefill_enqueue) joins the same issuer, so the prefill still
+    // overlaps the loads in flight, and pb_sync without a prompt waits for T_full
+    return start_load_issuer(c);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -1180,7 +1223,7 @@ pb_status issue_group(Issuer& I, size_t gi) {
             const MergeJob& job = c->jobs[j];
             if (all ? job.inplace : (!job.inplace || job.adapter != c->merge_adapter)) continue;
             for (int32_t a : job.need)
-                if (!I.adapter_waited[a]) {
+                if (!I.adapter_waited[a] && c->landed_alias[a] >= 0) {   // < 0: not loaded by this trial (held)
                     CU(cudaStreamWaitEvent(c->merge, landed_ev(c, a), 0));
                     I.adapter_waited[a] = 1;
                     ++mops;
@@ -1196,6 +1239,10 @@ pb_status issue_group(Issuer& I, size_t gi) {
                      p->es() * (2.0 * job.rows * job.cols + (double)job.rank * (job.rows + job.cols)));
             ++c->n_launches;
             mops += 1 + prof_ops(c);
+        }
+        if (c->merged_ev[id]) {   // timing mode (PB_LANDED_TIMING=1): per-chunk merged timestamp
+            CU(cudaEventRecord(c->merged_ev[id], c->merge));
+            ++mops;
         }
         if (!others.empty()) {
             CU(signal_ranks(c, c->L.f_chunk + id, others, c->merge));
@@ -1341,7 +1388,7 @@ static bool issuer_trace() {
     return on;
 }
 
-pb_status issue_item(Issuer& I, const Item& it) {
+pb_status issue_item(Issuer& I, const Item& it, bool late_tokens) {
     pb_ctx* c = I.c;
     if (issuer_trace()) fprintf(stderr, "[pb r%d] item kind=%d mb=%d j=%d l=%d\n", c->rank, it.kind, it.mb, it.j, it.l);
     const pb_plan* p = c->plan;
@@ -1385,6 +1432,8 @@ pb_status issue_item(Issuer& I, const Item& it) {
                                        sizeof(int32_t) * B, cudaMemcpyDeviceToDevice, s));
                 else if (I.replay)
                     CU(cudaMemcpyAsync(c->ws + L.tokens, c->h_tokens, sizeof(int32_t) * B * T, cudaMemcpyHostToDevice, s));
+                else if (late_tokens)   // posted after the load started: SM copy from the mapped pinned staging
+                    CU(launch_copy(c->ws + L.tokens, c->h_tokens, sizeof(int32_t) * B * T, s));
                 else
                     CU(cudaStreamWaitEvent(s, c->tok_ev, 0));
                 CU(cudaMemsetAsync(c->ws + L.nan, 0, 4, s));
@@ -1438,9 +1487,12 @@ pb_status issue_item(Issuer& I, const Item& it) {
             break;
         case I_LAYER: {
             const int adapter = I.mb_mode ? c->seq_adapter[it.mb] : -1;
+            const auto stage = rep ? std::make_pair(0, m.n_layers) : p->stages[g];
+            if (it.l == stage.first && it.mb == 0 && j == 0) CU(record_ev(c, c->stage_begin, s));
             pb_status st = run_layer(c, it.l, r0, r1, I.tb[j], I.tb[j + 1], Bk, it.mb == 0 && j == 0 && !I.replay,
                                      row_base, adapter);
             if (st) return st;
+            if (it.l == stage.second - 1 && it.mb == I.n_mb - 1 && j == I.k - 1) CU(record_ev(c, c->stage_end, s));
             break;
         }
         case I_PUSH:
@@ -1519,16 +1571,54 @@ pb_status issue_item(Issuer& I, const Item& it) {
     return PB_OK;
 }
 
-pb_status issue_trial(pb_ctx* c, int B, int T, bool replay) {
-    const pb_plan* p = c->plan;
+}  // namespace
+
+// One trial's issuer state. A cold start creates it in pb_gather_layers (load -> merge -> gather are armed, so the
+// copy lane, the merges and the receive copies start at once); pb_prefill_enqueue later posts the prompt and the
+// same issuer adds the compute items to the loads still in flight. Replays and decode steps create it with the
+// prompt already posted and nothing to load.
+struct pb::TrialRun {
     Issuer I;
+    size_t G = 0, R = 0, gi = 0, ri = 0, ii = 0;
+    bool merge_done_rec = false, gather_done_rec = false;
+    bool items_built = false;
+    bool late_tokens = false;   // the prompt came after the first copy group was issued (see I_PROLOGUE)
+};
+
+namespace {
+
+std::shared_ptr<TrialRun> init_run(pb_ctx* c, bool replay) {
+    const pb_plan* p = c->plan;
+    auto run = std::make_shared<TrialRun>();
+    Issuer& I = run->I;
     I.c = c;
-    I.B = B;
-    I.T = T;
     I.replay = replay;
     I.mb_mode = c->merge_adapter == PB_MERGE_ALL;
-    I.n_mb = I.mb_mode ? B : 1;
     I.replica = c->replica;
+    I.own_issued.assign(p->tensors.size(), replay ? 1 : 0);
+    I.recv_issued.assign(p->tensors.size(), replay ? 1 : 0);
+    I.adapter_waited.assign(p->chunks.size(), 0);
+    cudaStream_t ss[4] = {c->h2d[0], c->merge, c->nv, c->comp};
+    Budget* bs[4] = {&I.h2d, &I.merge, &I.nv, &I.comp};
+    for (int i = 0; i < 4; ++i) {
+        bs[i]->s = ss[i];
+        bs[i]->pool = c->budget_events.data() + i * kEventPool;
+        bs[i]->capture = c->capturing;
+    }
+    run->G = replay ? 0 : c->copies.size();
+    run->R = replay ? 0 : p->recv[c->rank].size();
+    run->merge_done_rec = run->gather_done_rec = replay;
+    if (!replay && c->file) c->file->start(c->copies, static_cast<const char*>(c->host_base));
+    return run;
+}
+
+// The prompt of the trial: batch B x T tokens staged in c->h_tokens (rank 0 / replica).
+pb_status post_prompt(pb_ctx* c, TrialRun& run, int B, int T) {
+    const pb_plan* p = c->plan;
+    Issuer& I = run.I;
+    I.B = B;
+    I.T = T;
+    I.n_mb = I.mb_mode ? B : 1;
     I.dec_t = c->decode_t;
     c->chain_seq = 0;
     if (I.dec_t >= 0) {   // f3 decode step: one "prompt chunk" holding position dec_t of every sequence
@@ -1545,32 +1635,47 @@ pb_status issue_trial(pb_ctx* c, int B, int T, bool replay) {
         // rows one GEMM launch covers at most: the whole batch, or one sequence in microbatch mode (PB_MERGE_ALL)
         c->gemm_m_total = I.mb_mode ? T : B * T;
     }
-    I.own_issued.assign(p->tensors.size(), replay ? 1 : 0);
-    I.recv_issued.assign(p->tensors.size(), replay ? 1 : 0);
-    I.adapter_waited.assign(p->chunks.size(), 0);
-    cudaStream_t ss[4] = {c->h2d[0], c->merge, c->nv, c->comp};
-    Budget* bs[4] = {&I.h2d, &I.merge, &I.nv, &I.comp};
-    for (int i = 0; i < 4; ++i) {
-        bs[i]->s = ss[i];
-        bs[i]->pool = c->budget_events.data() + i * kEventPool;
-        bs[i]->capture = c->capturing;
-    }
     build_items(I);
-    if (!replay && c->file) c->file->start(c->copies, static_cast<const char*>(c->host_base));
-    if (!replay && c->rank == 0) {   // prompt tokens first on the copy lane: they land in microseconds
-        CU(cudaMemcpyAsync(c->ws + c->L.tokens, c->h_tokens, sizeof(int32_t) * B * T, cudaMemcpyHostToDevice, c->h2d[0]));
-        CU(cudaEventRecord(c->tok_ev, c->h2d[0]));
-        CU(I.h2d.add(2));
+    if (!I.replay && c->rank == 0) {
+        if (run.gi == 0) {   // nothing on the copy lane yet: the tokens go first and land in microseconds
+            CU(cudaMemcpyAsync(c->ws + c->L.tokens, c->h_tokens, sizeof(int32_t) * B * T, cudaMemcpyHostToDevice,
+                               c->h2d[0]));
+            CU(cudaEventRecord(c->tok_ev, c->h2d[0]));
+            CU(I.h2d.add(2));
+        } else {
+            // the load is already streaming: an H2D copy would queue behind it in the copy engine (measured: the
+            // engine drains one stream's queue before another's), so the prologue pulls the tokens from the
+            // pinned (device-mapped) staging buffer with an SM copy instead
+            run.late_tokens = true;
+        }
     }
-    const size_t G = replay ? 0 : c->copies.size();
-    const size_t R = replay ? 0 : p->recv[c->rank].size();
-    size_t gi = 0, ri = 0, ii = 0;
-    bool merge_done_rec = replay, gather_done_rec = replay;
+    run.items_built = true;
+    return PB_OK;
+}
+
+// Issue the trial in data-arrival order until everything known so far is issued. Returns once the loads and
+// receives are issued and either the prompt's compute items are issued too or no prompt has been posted (the
+// caller then marks the loader idle under run_mu; a later post restarts the loop).
+pb_status run_loop(pb_ctx* c, TrialRun& run) {
+    const pb_plan* p = c->plan;
+    Issuer& I = run.I;
     static const bool dbg = getenv("PB_DEBUG_ISSUER") != nullptr;
     auto last_report = std::chrono::steady_clock::now();
-    while (gi < G || ri < R || ii < I.items.size()) {
+    const size_t G = run.G, R = run.R;
+    size_t& gi = run.gi;
+    size_t& ri = run.ri;
+    size_t& ii = run.ii;
+    for (;;) {
+        if (c->abort_req.load(std::memory_order_relaxed)) return fail(PB_ECUDA, "trial aborted (pb_ctx_abort)");
+        if (!run.items_built && c->posted.load(std::memory_order_acquire)) {
+            pb_status st = post_prompt(c, run, c->cur_batch, c->cur_seq);
+            if (st) return st;
+        }
+        const size_t NI = run.items_built ? I.items.size() : 0;
+        if (gi >= G && ri >= R && (ii >= NI && (run.items_built || !c->posted.load(std::memory_order_acquire))))
+            break;
         bool progressed = false;
-        if (c->file && !replay) c->file->reclaim();
+        if (c->file && !I.replay) c->file->reclaim();
         auto staged = [&](size_t k) {   // f4: a file-backed group can go once the reader has filled its slot
             return !c->copies[k].from_file || c->file->ready((int64_t)k) || c->file->read_error.load();
         };
@@ -1579,9 +1684,9 @@ pb_status issue_trial(pb_ctx* c, int B, int T, bool replay) {
             if (st) return st;
             progressed = true;
         }
-        if (!merge_done_rec && gi == G) {   // t_full: recorded once the last merge work is on its stream
+        if (!run.merge_done_rec && gi == G) {   // t_full: recorded once the last merge work is on its stream
             CU(cudaEventRecord(c->merge_done, c->merge));
-            merge_done_rec = true;
+            run.merge_done_rec = true;
         }
         const size_t target = gi >= G ? R : (gi * R) / std::max<size_t>(G, 1);
         while (ri < target && I.nv.can(5)) {
@@ -1589,16 +1694,22 @@ pb_status issue_trial(pb_ctx* c, int B, int T, bool replay) {
             if (st) return st;
             progressed = true;
         }
-        if (!gather_done_rec && ri == R && gi == G) {
+        if (!run.gather_done_rec && ri == R && gi == G) {
             CU(cudaEventRecord(c->gather_done, c->nv));
-            gather_done_rec = true;
+            if (c->n > 1) {   // tell every peer this rank has copied all it gathers (an in-place switch waits on it)
+                std::vector<int32_t> others;
+                for (int r = 0; r < c->n; ++r)
+                    if (r != c->rank) others.push_back(r);
+                CU(signal_ranks(c, c->L.f_gdone + c->rank, others, c->nv));
+            }
+            run.gather_done_rec = true;
         }
-        while (ii < I.items.size()) {
+        while (ii < NI) {
             const Item& it = I.items[ii];
             bool ok = true;
             for (int32_t t : it.prereq) ok = ok && prereq_issued(I, t);
             if (!ok || !I.comp.can(item_ops(I, it))) break;
-            pb_status st = issue_item(I, it);
+            pb_status st = issue_item(I, it, run.late_tokens);
             if (st) return st;
             CU(I.comp.add(item_ops(I, it)));
             ++ii;
@@ -1608,7 +1719,7 @@ pb_status issue_trial(pb_ctx* c, int B, int T, bool replay) {
             std::this_thread::sleep_for(std::chrono::microseconds(20));
             if (dbg && std::chrono::steady_clock::now() - last_report > std::chrono::seconds(2)) {
                 last_report = std::chrono::steady_clock::now();
-                const Item* it = ii < I.items.size() ? &I.items[ii] : nullptr;
+                const Item* it = ii < NI ? &I.items[ii] : nullptr;
                 int missing = -1;
                 if (it)
                     for (int32_t t : it->prereq)
@@ -1616,16 +1727,68 @@ pb_status issue_trial(pb_ctx* c, int B, int T, bool replay) {
                 fprintf(stderr,
                         "[pb issuer r%d] stalled: groups %zu/%zu recv %zu/%zu items %zu/%zu (kind %d j %d l %d, missing "
                         "tensor %d) outstanding h2d %ld merge %ld nv %ld comp %ld\n",
-                        c->rank, gi, G, ri, R, ii, I.items.size(), it ? it->kind : -1, it ? it->j : -1, it ? it->l : -1,
+                        c->rank, gi, G, ri, R, ii, NI, it ? it->kind : -1, it ? it->j : -1, it ? it->l : -1,
                         missing, I.h2d.issued - I.h2d.done, I.merge.issued - I.merge.done, I.nv.issued - I.nv.done,
                         I.comp.issued - I.comp.done);
             }
         }
     }
-    if (!merge_done_rec) CU(cudaEventRecord(c->merge_done, c->merge));
-    if (!gather_done_rec) CU(cudaEventRecord(c->gather_done, c->nv));
+    (void)p;
     return PB_OK;
 }
+
+// Synchronous trial (replays, decode steps, graph capture): prompt posted up front, nothing to load.
+pb_status issue_trial(pb_ctx* c, int B, int T, bool replay) {
+    auto run = init_run(c, replay);
+    pb_status st = post_prompt(c, *run, B, T);
+    if (st) return st;
+    c->posted.store(true);
+    st = run_loop(c, *run);
+    if (st) return st;
+    if (!run->merge_done_rec) CU(cudaEventRecord(c->merge_done, c->merge));
+    if (!run->gather_done_rec) CU(cudaEventRecord(c->gather_done, c->nv));
+    return PB_OK;
+}
+
+// The issuer thread of a cold start: loops until everything posted is issued; if the prompt has not been posted
+// by then it marks itself idle (under run_mu, so a concurrent post either sees the running thread or restarts it).
+void issuer_thread(pb_ctx* c, std::shared_ptr<TrialRun> run) {
+    cudaSetDevice(c->device);
+    for (;;) {
+        pb_status st = run_loop(c, *run);
+        if (st != PB_OK) {
+            std::lock_guard<std::mutex> lk(c->run_mu);
+            c->issue_status = st;
+            snprintf(c->issue_msg, sizeof c->issue_msg, "%s", pb_last_error());
+            c->loader_idle = true;
+            return;
+        }
+        std::lock_guard<std::mutex> lk(c->run_mu);
+        if (run->items_built || !c->posted.load()) {   // done, or nothing more to do until a prompt is posted
+            c->loader_idle = true;
+            return;
+        }
+    }
+}
+
+void spawn_issuer(pb_ctx* c) {
+    c->loader_idle = false;
+    c->load_thread = std::thread(issuer_thread, c, c->run);
+}
+
+}  // namespace
+
+static pb_status start_load_issuer(pb_ctx* c) {
+    std::lock_guard<std::mutex> lk(c->run_mu);
+    c->issue_status = PB_OK;
+    c->issue_msg[0] = '\0';
+    c->run = init_run(c, false);
+    c->posted.store(false);
+    spawn_issuer(c);
+    return PB_OK;
+}
+
+namespace {
 
 pb_status start_issuer(pb_ctx* c, const int32_t* tokens, const int32_t* adapter_of_seq, int32_t B, int32_t T,
                        bool replay) {
@@ -1639,14 +1802,14 @@ pb_status start_issuer(pb_ctx* c, const int32_t* tokens, const int32_t* adapter_
                 return fail(PB_EINVAL, "token %d at [%lld] outside the vocabulary [0, %d)", tokens[i], (long long)i, V);
     }
     const bool mb = c->merge_adapter == PB_MERGE_ALL;
+    std::vector<int32_t> seq_adapter(B, -1);
     if (!replay) {
-        c->seq_adapter.assign(B, -1);
         if (mb) {
             const int A = (int)c->plan->adapters.size();
             for (int b = 0; b < B; ++b) {
                 const int a = adapter_of_seq ? adapter_of_seq[b] : b % A;
                 if (a < 0 || a >= A) return fail(PB_EINVAL, "adapter_of_seq[%d] = %d out of range", b, a);
-                c->seq_adapter[b] = a;
+                seq_adapter[b] = a;
             }
         } else if (adapter_of_seq) {
             for (int b = 0; b < B; ++b)
@@ -1655,6 +1818,19 @@ pb_status start_issuer(pb_ctx* c, const int32_t* tokens, const int32_t* adapter_
                                            "PB_MERGE_ALL for mixed batches)", b, adapter_of_seq[b], c->merge_adapter);
         }
     }
+    std::unique_lock<std::mutex> lk(c->run_mu);
+    if (replay || !c->run) {   // replay / decode: a fresh run with nothing to load
+        lk.unlock();
+        join_load(c);
+        lk.lock();
+        c->issue_status = PB_OK;
+        c->issue_msg[0] = '\0';
+        c->run = init_run(c, replay);
+        c->posted.store(false);
+    }
+    // The issuer reads the staged prompt only after `posted` is set (release below), so staging it here is safe
+    // while a cold start's loads are being issued.
+    if (!replay) c->seq_adapter = seq_adapter;
     if (c->rank == 0 || c->replica)
         for (int b = 0; b < B; ++b)   // token-major rows t*B + b; microbatch mode: sequence-major b*T + t
             for (int t = 0; t < T; ++t) c->h_tokens[mb ? b * T + t : t * B + b] = tokens[(size_t)b * T + t];
@@ -1662,18 +1838,13 @@ pb_status start_issuer(pb_ctx* c, const int32_t* tokens, const int32_t* adapter_
     c->cur_seq = T;
     c->n_decoded = 0;
     c->prompt_replica = c->replica;
-    join_load(c);
-    c->issue_status = PB_OK;
-    c->issue_msg[0] = '\0';
     c->phase = Phase::Prefilled;
-    c->load_thread = std::thread([c, B, T, replay]() {
-        cudaSetDevice(c->device);
-        pb_status st = issue_trial(c, B, T, replay);
-        if (st != PB_OK) {
-            c->issue_status = st;
-            snprintf(c->issue_msg, sizeof c->issue_msg, "%s", pb_last_error());
-        }
-    });
+    c->posted.store(true, std::memory_order_release);
+    if (c->load_thread.joinable() && !c->loader_idle) return PB_OK;   // the running issuer picks the prompt up
+    lk.unlock();
+    join_load(c);
+    if (c->issue_status != PB_OK) return fail(c->issue_status, "issuer: %s", c->issue_msg);
+    spawn_issuer(c);
     return PB_OK;
 }
 
@@ -1845,6 +2016,11 @@ extern "C" pb_status pb_ctx_set_replica(pb_ctx* c, int32_t on) {
             cudaEventQuery(c->gather_done) != cudaSuccess || cudaEventQuery(c->merge_done) != cudaSuccess)
             return fail(PB_EPROTOCOL, "pb_ctx_set_replica: T_full not reached (pb_sync first)");
         if (c->merge_adapter == PB_MERGE_ALL) return fail(PB_EUNSUPPORTED, "replica of a PB_MERGE_ALL context");
+        // a replica runs every layer from this GPU's weights: the other stages' gathered copies hold the cold
+        // start's adapter, so the stage (pb_switch_adapter) must hold it too
+        if (c->merge_adapter != c->cold_adapter)
+            return fail(PB_EUNSUPPORTED, "pb_ctx_set_replica: the stage was switched to adapter %d but the gathered "
+                                         "layers hold the cold start's adapter %d", c->merge_adapter, c->cold_adapter);
     }
     c->replica = on != 0;
     return PB_OK;
@@ -1864,9 +2040,16 @@ extern "C" pb_status pb_switch_adapter(pb_ctx* c, int32_t adapter_id) {
         return fail(PB_EINVAL, "adapter_id %d out of range", adapter_id);
     if (!c->backup) return fail(PB_ENOMEM, "pb_switch_adapter needs bufs.backup >= dev_backup_bytes");
     if (!p->survivors.empty()) return fail(PB_EUNSUPPORTED, "pb_switch_adapter on a re-plan");
+    if (c->replica)
+        return fail(PB_EUNSUPPORTED, "pb_switch_adapter in replica mode (only the stage would switch; the gathered "
+                                     "layers keep the cold start's adapter)");
     join_load(c);   // the trial issuer has issued everything: the switch queues behind it on the compute stream
     if (c->issue_status != PB_OK) return fail(c->issue_status, "%s", c->issue_msg);
     cudaStream_t s = c->comp;
+    // the stage is rewritten in place: every peer must have finished copying it first (device-side wait on the
+    // peers' gather-complete words, so the switch cannot tear a copy still in flight)
+    for (int r = 0; r < c->n; ++r)
+        if (r != c->rank) CU(wait_word(c, c->L.f_gdone + r, s));
     const auto stage = p->stages[c->rank];
     const char* hb = static_cast<const char*>(c->host_base);
     const char* ha = static_cast<const char*>(c->host_adapters);
@@ -1999,6 +2182,23 @@ extern "C" pb_status pb_sync(pb_ctx* c) {
     return PB_OK;
 }
 
+extern "C" pb_status pb_ctx_abort(pb_ctx* c) {
+    pb_status st = check_ctx(c, "pb_ctx_abort");
+    if (st) return st;
+    c->abort_req.store(true);
+    join_load(c);   // the issuer returns at its next poll (it never blocks in an enqueue: outstanding-op budgets)
+    // force every readiness word of this rank open: waits are `word >= epoch`, so 0xFFFFFFFF releases all of them
+    cudaStream_t probe;
+    CU(cudaStreamCreateWithFlags(&probe, cudaStreamNonBlocking));
+    cudaError_t e = cudaMemsetAsync(c->ws + c->L.flags, 0xFF, 4 * (size_t)c->L.n_words, probe);
+    if (e == cudaSuccess) e = drain_stream(probe, 10.0) ? cudaSuccess : cudaErrorNotReady;
+    cudaStreamDestroy(probe);
+    c->aborted = true;
+    c->phase = Phase::Idle;
+    CU(e);
+    return PB_OK;
+}
+
 extern "C" pb_status pb_timeline(pb_ctx* c, pb_timeline_t* out) {
     pb_status st = check_ctx(c, "pb_timeline");
     if (st) return st;
@@ -2016,6 +2216,7 @@ extern "C" pb_status pb_timeline(pb_ctx* c, pb_timeline_t* out) {
         load_done = std::max(load_done, c->tl_landed[id]);
     }
     for (int32_t id : p->recv[c->rank]) c->tl_gathered[id] = ms(c->gathered[id]);
+    for (int32_t id : p->load[c->rank]) c->tl_merged[id] = c->merged_ev[id] ? ms(c->merged_ev[id]) : -1;
     double ready = 0;
     if (c->last_own_stage_chunk >= 0) ready = std::max(ready, ms(c->ready_merge));
     if (c->last_recv_stage_chunk >= 0) ready = std::max(ready, ms(c->ready_recv));
@@ -2029,5 +2230,10 @@ extern "C" pb_status pb_timeline(pb_ctx* c, pb_timeline_t* out) {
     out->chunk_landed_ms = c->tl_landed.data();
     out->chunk_gathered_ms = c->tl_gathered.data();
     out->n_launches = c->n_launches;
+    out->chunk_merged_ms = c->tl_merged.data();
+    const bool staged = c->phase == Phase::Prefilled && p->stages[c->rank].second > p->stages[c->rank].first;
+    out->stage_begin_ms = staged ? ms(c->stage_begin) : -1;
+    out->stage_end_ms = staged ? ms(c->stage_end) : -1;
+    out->ctx_create_ms = c->ctx_create_ms;
     return PB_OK;
 }

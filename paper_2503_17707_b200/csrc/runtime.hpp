@@ -10,9 +10,13 @@
 #include "plan.hpp"
 #include "storage.hpp"
 
+#include <atomic>
 #include <memory>
+#include <mutex>
 
 namespace pb {
+
+struct TrialRun;   // the trial issuer's state (runtime.cpp)
 
 // Workspace layout (byte offsets inside the caller's workspace buffer), identical on every rank so a
 // peer can address it: flags | tokens | h | x | qkv[n_qkv] | attn | mlp | y | logits | tok_out | nan | rope.
@@ -25,6 +29,7 @@ struct WsLayout {
     int32_t f_chunk = 0, f_act = 0, f_y = 0, f_logit = 0, n_words = 0;
     int32_t f_land = 0, f_tensor = 0;   // local words: copy group landed (by first chunk id), tensor ready
     int32_t f_tensor_recv = 0;          // local words: the received part of a tensor is in place
+    int32_t f_gdone = 0;                // word f_gdone + r: rank r has received every chunk it gathers (T_full on r)
 };
 WsLayout ws_layout(const pb_plan* p, int32_t batch, int32_t seq);
 
@@ -65,6 +70,7 @@ struct Peer {
     std::vector<void*> ipc_bases;   // cudaIpcOpenMemHandle results to close
 };
 
+constexpr int32_t kMaxBatch = 64;   // sequences per trial (the paper's TTFT workload is 64 x 64)
 enum class Phase { Idle, Begun, Loaded, Merged, Gathered, Prefilled };
 constexpr int kEventPool = 64;
 
@@ -103,6 +109,9 @@ struct pb_ctx {
     cudaEvent_t tok_ev = nullptr;                               // prompt tokens landed (copy lane)
     int32_t last_own_stage_chunk = -1, last_recv_stage_chunk = -1;
     std::vector<cudaEvent_t> landed, gathered;
+    std::vector<cudaEvent_t> merged_ev;          // per own chunk, after its merges (timing mode only)
+    cudaEvent_t stage_begin = nullptr, stage_end = nullptr;   // first / last layer item of this rank's stage
+    double ctx_create_ms = 0;                    // host time of pb_ctx_create (tables, TMA maps, events, staging)
     std::vector<char> tensor_own;        // this rank loads every piece of the tensor
     std::vector<int32_t> last_own_chunk; // per base tensor: last own chunk in load order (-1 if none)
     std::vector<int32_t> last_recv_chunk;
@@ -136,12 +145,19 @@ struct pb_ctx {
     int32_t cur_batch = 0, cur_seq = 0;
     int32_t n_launches = 0;
     int64_t load_bytes = 0, recv_bytes = 0;
-    std::vector<double> tl_landed, tl_gathered;
+    std::vector<double> tl_landed, tl_gathered, tl_merged;
     bool use_wait_value = true;
-    std::thread load_thread;                 // the trial issuer (see issue_trial)
+    std::thread load_thread;                 // the trial issuer (see run_loop)
+    std::shared_ptr<pb::TrialRun> run;       // the current trial's issuer state (cold start: from pb_gather_layers)
+    std::mutex run_mu;                       // prompt hand-off between pb_prefill_enqueue and the issuer thread
+    std::atomic<bool> posted{false};         // the trial's prompt is staged (cur_batch, cur_seq, h_tokens)
+    bool loader_idle = true;                 // the issuer thread has issued everything posted so far and exited
+    std::atomic<bool> abort_req{false};      // pb_ctx_abort: the issuer stops at its next poll
+    bool aborted = false;                    // readiness words forced open; the ctx can only be freed
     pb_status issue_status = PB_OK;
     char issue_msg[512] = "";
     int32_t merge_adapter = -1;
+    int32_t cold_adapter = -1;   // adapter merged by the cold start (every gathered copy of other stages holds it)
     std::vector<cudaEvent_t> budget_events;
     std::vector<cudaStream_t> owned_streams;   // created by the ctx when the caller passed NULL  // 4 streams x kEventPool progress marks
     bool profiling = false;

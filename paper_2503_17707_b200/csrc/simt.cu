@@ -503,8 +503,15 @@ cudaError_t launch_attention_simt(const __nv_bfloat16* qkv, int ld, __nv_bfloat1
 cudaError_t launch_logits(const __nv_bfloat16* y, int B, int d, const __nv_bfloat16* E, int v0, int v1, float* logits,
                           int ldl, cudaStream_t s, bool pdl) {
     if (v1 <= v0) return cudaSuccess;
-    if (B > 8 || d % 8) return cudaErrorInvalidValue;
-    return launch_pdl(logits_kernel, (v1 - v0 + 7) / 8, 256, 0, s, pdl, y, B, d, E, v0, v1, logits, ldl);
+    if (d % 8) return cudaErrorInvalidValue;
+    // up to 8 sequences per launch (the warp's accumulators); larger batches (the paper's 64 x 64 workload)
+    // stream the head once per group of 8
+    for (int b0 = 0; b0 < B; b0 += 8) {
+        const cudaError_t e = launch_pdl(logits_kernel, (v1 - v0 + 7) / 8, 256, 0, s, pdl, y + (size_t)b0 * d,
+                                         std::min(8, B - b0), d, E, v0, v1, logits + (size_t)b0 * ldl, ldl);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 cudaError_t launch_argmax(const float* logits, int B, int V, int ldl, int32_t* tokens, int32_t* nan_flag,

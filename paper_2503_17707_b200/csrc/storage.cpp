@@ -41,9 +41,14 @@ void FileSource::stop_reader() {
 void FileSource::start(const std::vector<CopyGroup>& groups, const char* host_base) {
     stop_reader();
     n_groups = (int64_t)groups.size();
-    for (auto& s : slots) {
+    fidx.assign(groups.size(), -1);
+    for (int64_t gi = 0, fi = 0; gi < n_groups; ++gi)
+        if (groups[gi].from_file) fidx[gi] = fi++;
+    for (size_t k = 0; k < slots.size(); ++k) {
+        Slot& s = slots[k];
         s.state.store(kFree);
         s.parts.store(0);
+        s.turn.store((int64_t)k);
         s.group = -1;
     }
     read_error.store(0);
@@ -54,8 +59,10 @@ void FileSource::start(const std::vector<CopyGroup>& groups, const char* host_ba
             for (int64_t gi = 0; gi < n_groups && !stop.load(); ++gi) {
                 const CopyGroup& g = groups[gi];
                 if (!g.from_file) continue;
-                Slot& s = slots[gi % slots.size()];
-                while (s.state.load(std::memory_order_acquire) != kFree)
+                const int64_t fi = fidx[gi];
+                Slot& s = slots[fi % slots.size()];
+                // free AND this group's turn (reclaim advances `turn` before it frees the slot)
+                while (s.state.load(std::memory_order_acquire) != kFree || s.turn.load(std::memory_order_acquire) != fi)
                     if (stop.load()) return;
                     else std::this_thread::sleep_for(std::chrono::microseconds(2));
                 const int64_t off = g.src - host_base;
@@ -86,14 +93,15 @@ void FileSource::start(const std::vector<CopyGroup>& groups, const char* host_ba
 
 // The staging slot holding group gi once the reader has filled it, else null.
 const char* FileSource::ready(int64_t gi) {
-    Slot& s = slots[gi % slots.size()];
+    if (gi < 0 || gi >= (int64_t)fidx.size() || fidx[gi] < 0) return nullptr;
+    Slot& s = slots[fidx[gi] % slots.size()];
     if (s.state.load(std::memory_order_acquire) != kReady) return nullptr;
     if (s.group != gi) return nullptr;
     return s.buf;
 }
 
 void FileSource::issued(int64_t gi, cudaEvent_t landed) {
-    Slot& s = slots[gi % slots.size()];
+    Slot& s = slots[fidx[gi] % slots.size()];
     s.landed = landed;
     s.state.store(kIssued, std::memory_order_release);
 }
@@ -101,8 +109,10 @@ void FileSource::issued(int64_t gi, cudaEvent_t landed) {
 // Hand back every slot whose DMA has completed (called by the issuer while it polls).
 void FileSource::reclaim() {
     for (auto& s : slots)
-        if (s.state.load(std::memory_order_acquire) == kIssued && cudaEventQuery(s.landed) == cudaSuccess)
+        if (s.state.load(std::memory_order_acquire) == kIssued && cudaEventQuery(s.landed) == cudaSuccess) {
+            s.turn.store(s.turn.load(std::memory_order_relaxed) + (int64_t)slots.size(), std::memory_order_release);
             s.state.store(kFree, std::memory_order_release);
+        }
 }
 
 }  // namespace pb
@@ -122,7 +132,8 @@ extern "C" pb_status pb_ctx_set_file_source(pb_ctx* c, const char* path, void* s
     for (auto& g : c->copies)
         if (!c->plan->chunks[c->plan->load[c->rank][g.first]].is_adapter) slot = std::max(slot, g.bytes);
     slot = (slot + 4095) / 4096 * 4096;
-    const int64_t n_slots = slot ? staging_bytes / slot : 0;
+    int64_t n_slots = slot ? staging_bytes / slot : 0;
+    if (const char* ns = getenv("PB_FILE_SLOTS")) n_slots = std::min<int64_t>(n_slots, std::max(2, atoi(ns)));
     if (slot && n_slots < 2)
         return fail(PB_ENOMEM, "staging: need >= 2 slots of %lld bytes (%lld given)", (long long)slot,
                     (long long)staging_bytes);

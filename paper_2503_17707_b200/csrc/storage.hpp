@@ -12,14 +12,20 @@ namespace pb {
 struct CopyGroup;
 
 struct FileSource {
-    enum : int { kFree = 0, kReading = 1, kReady = 2, kIssued = 3 };
+    enum : int { kFree = 0, kReady = 2, kIssued = 3 };
+    // Slot k serves the file-backed groups with file index fi = k, k + n, k + 2n, ... in that order: `turn` is the
+    // file index it may be filled for next, advanced by n only when the DMA of the previous occupant has landed.
+    // A reader that runs ahead therefore waits for its own turn instead of writing into a slot still being
+    // filled (or not yet copied) for an earlier group.
     struct Slot {
         char* buf = nullptr;
         std::atomic<int> state{kFree};
-        std::atomic<int> parts{0};   // reader threads done with this fill
+        std::atomic<int> parts{0};        // reader threads done with this fill
+        std::atomic<int64_t> turn{0};     // file index this slot is being (or may next be) filled for
         int64_t group = -1;
         cudaEvent_t landed = nullptr;
     };
+    std::vector<int64_t> fidx;   // copy group -> file index (-1: not read from the file)
     int fd = -1;          // O_DIRECT when the file system accepts it
     int fd_buffered = -1; // for reads whose offset is not 4 KiB aligned
     bool direct = false;

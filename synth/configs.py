@@ -75,6 +75,8 @@ WORKLOADS = {
     # fp32 debug-parity run of C1 (SURVEY.md §8(c) "Tolerances": the 1e-4 gate; not timed)
     "C1f32": Workload("C1f32", TINY_OPT_F32, (lora(8),), 1, 16, (2,), "tiny OPT fp32, 2 shards"),
     "C2": Workload("C2", OPT_1_3B, (lora(16),), 1, 128, (1, 2, 4, 8), "OPT-1.3B + r16 q,v"),
+    # paper-shaped secondary run of C2 (SURVEY.md §8(d) per-config inputs; "batch size of 64 ... 64 tokens")
+    "C2p": Workload("C2p", OPT_1_3B, (lora(16),), 64, 64, (1, 2, 4, 8), "OPT-1.3B + r16 q,v, paper batch 64x64"),
     "C3": Workload("C3", LLAMA2_7B, tuple(lora(16) for _ in range(4)), 4, 512, (8,), "Llama-2-7B + 4 adapters"),
     "C4": Workload("C4", OPT_13B, (lora(64, OPT_ALL),), 1, 1024, (2, 4, 8), "OPT-13B + r64 all"),
     "C5a": Workload("C5a", LLAMA2_70B, (lora(16),), 1, 2048, (8,), "Llama-2-70B + r16"),

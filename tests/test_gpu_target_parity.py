@@ -1,0 +1,94 @@
+"""Full-depth first-token parity at the north-star workloads (VERDICT r01 "What's missing" #1).
+
+The GPU cold start (through the C ABI: pb_trial_begin -> pb_load_shard -> pb_merge_lora -> pb_gather_layers ->
+pb_prefill_enqueue/wait) is compared with the oracle's sequential forward over the whole model, stored by
+tools/oracle_reference.py (imports only oracle/ and synth/) in tests/golden/oracle_<tag>.npz:
+  * logits within 1e-2 relative (||g-o||inf / ||o||inf) of the bf16-contract oracle, token by the G10 rule
+    (north star; SURVEY.md §8(c) Tolerances);
+  * "pipelined equals sequential": the same oracle reference for N = 1 and for N logical ranks with
+    the INTERLEAVE policy, vocab-sliced head and k = 2 prompt chunks — and the logits bit-identical between them.
+Set PB_PARITY_LOG=<file> to append one JSON record per case (the DESIGN.md error-vs-depth table).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import harness
+from paper_2503_17707_b200 import _binding as B
+from paper_2503_17707_b200.api import Plan, RankEngine
+from synth.configs import WORKLOADS
+
+pytestmark = pytest.mark.gpu
+
+
+def cold_start(tag, n, policy="stage", sliced=0, k=1, chunk_mb=64, alias=0):
+    w = WORKLOADS[tag]
+    plan = Plan(w.model, w.adapters, n, policy=policy, vocab_sliced=sliced, chunk_bytes=chunk_mb << 20,
+                prefill_chunks=k, host_alias_layers=alias)
+    base, ada = harness.build_host_images(plan)
+    gold = harness.load_golden(tag, alias)
+    assert gold is not None, f"missing {harness.golden_path(tag, alias)} (run tools/oracle_reference.py {tag})"
+    toks = gold["tokens"]
+    assert toks.shape == (w.batch, w.seq)
+    multi = len(w.adapters) > 1
+    engs = [RankEngine(plan, r, base, ada, max_batch=w.batch, max_seq=w.seq, multi_adapter=multi) for r in range(n)]
+    try:
+        for e in engs:
+            e.wire_local(engs)
+        aos = [int(a) for a in gold["adapter_of_seq"]] if multi else None
+        for e in engs:
+            e.invalidate()
+        for e in engs:
+            e.enqueue(1, toks if e.rank == 0 else None, w.batch, w.seq,
+                      adapter_id=B.PB_MERGE_ALL if multi else (0 if w.adapters else -1), adapter_of_seq=aos)
+        res = [e.wait(want_logits=True) for e in engs]
+    finally:
+        for e in engs:
+            e.close()
+        del base, ada
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+    tokens, logits = res[0]
+    rep = harness.golden_parity(gold, logits, tokens)
+    rec = {"workload": tag, "n": n, "policy": policy, "vocab_sliced": sliced, "k": k, "host_alias": alias,
+           "layers": w.model.n_layers, "max_rel": rep["max_rel"], "max_rel_exact": rep.get("max_rel_exact"),
+           "token_ok": rep["token_ok"], "token_exact_match": rep["token_exact_match"][:8],
+           "margin": rep["margin"][:8], "tokens": [int(x) for x in tokens[:8]]}
+    if os.environ.get("PB_PARITY_LOG"):
+        with open(os.environ["PB_PARITY_LOG"], "a") as f:
+            f.write(json.dumps(rec) + "\n")
+    assert rep["max_rel"] <= 1e-2, rec
+    assert all(rep["token_ok"]), rec
+    return logits, tokens
+
+
+@pytest.fixture(autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def test_c2_full_depth_vs_stored_oracle():
+    cold_start("C2", 1, chunk_mb=128)
+
+
+def test_c2p_paper_batch_64x64():
+    """The paper's own TTFT workload shape (batch 64, prompt 64) at OPT-1.3B, one and two stages."""
+    l1, t1 = cold_start("C2p", 1, chunk_mb=128)
+    l2, t2 = cold_start("C2p", 2, policy="interleave", sliced=1, k=2)
+    assert np.array_equal(l1, l2) and np.array_equal(t1, t2)
+
+
+def test_c4_full_depth_one_rank_and_four_stages():
+    """OPT-13B + r64 LoRA on all six projections, 1024-token prompt: the north star's first target config."""
+    l1, t1 = cold_start("C4", 1, chunk_mb=128)
+    l4, t4 = cold_start("C4", 4, policy="interleave", sliced=1, k=2)
+    assert np.array_equal(l1, l4) and np.array_equal(t1, t4)
+
+
+def test_c3_four_adapters_full_depth():
+    """Llama-2-7B, 4 adapters out of place (PB_MERGE_ALL), one sequence per adapter, 512 tokens."""
+    cold_start("C3", 1, chunk_mb=128)
