@@ -389,7 +389,7 @@ PB_API void pb_ctx_free(pb_ctx* ctx);
 /* f1 support — abandon the current trial after a peer has died mid-load (the survivors re-plan and
  * resume). Cross-rank dependencies are device-side waits on readiness words only peers write, so a dead peer
  * would leave this rank's streams blocked forever. pb_ctx_abort stops the issuer thread at its next poll, then
- * forces every readiness word of this rank's workspace open (0xFFFFFFFF >= any epoch) so the blocked streams
+ * forces every readiness word of this rank's workspace open (epoch + 2^30: the waits compare cyclically) so the blocked streams
  * drain (their remaining kernels compute on whatever bytes are there; nothing is published as valid), and
  * marks the ctx aborted: every later call except pb_ctx_free returns PB_EPROTOCOL. pb_ctx_free of an aborted
  * ctx waits at most a few seconds per stream instead of synchronizing the device. The weight / adapter buffers

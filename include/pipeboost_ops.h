@@ -38,6 +38,16 @@ PB_API pb_status pb_op_gemm_split(const void* X, int32_t x_rows, int32_t m_begin
                                   float scale, int32_t scale_cols, void* out, int32_t ldo, int32_t split_k,
                                   void* stream);
 
+/* Llama QKV projection with the rotary embedding fused into the epilogue (DESIGN.md §3 storage contract:
+ * q/k = RNE_bf16(rope(X Wqkv^T)), one rounding): epi 0 without bias / scale, then columns [0, rope_cols) (q and k
+ * heads of hd = 64 or 128, head-aligned) rotated HF rotate_half style at position (row - row0) / B with
+ * theta^(-2i/hd) angles; columns >= rope_cols (v) plain. table: device scratch of T*hd/2*8 bytes (filled here,
+ * positions < T). split_k as in pb_op_gemm_split; M <= 2 rows take the GEMV. */
+PB_API pb_status pb_op_gemm_rope(const void* X, int32_t x_rows, int32_t m_begin, int32_t m_end, int32_t K,
+                                 const void* W, int32_t N, void* out, int32_t ldo, int32_t rope_cols, int32_t hd,
+                                 int32_t row0, int32_t B, int32_t T, float theta, void* table, int32_t split_k,
+                                 void* stream);
+
 /* LayerNorm (beta != NULL) or RMSNorm (beta == NULL): fp32 h [rows x d] -> bf16 out [rows x d]. */
 PB_API pb_status pb_op_norm(const float* h, int32_t rows, int32_t d, const void* gamma, const void* beta, float eps,
                             void* out, void* stream);
@@ -53,7 +63,7 @@ PB_API pb_status pb_op_attention(const void* qkv, int32_t ld, void* out, int32_t
 PB_API pb_status pb_op_rope(void* qkv, int32_t ld, int32_t r0, int32_t r1, int32_t B, int32_t T, int32_t n_q,
                             int32_t n_k, int32_t hd, int32_t k_col0, float theta, void* table, void* stream);
 
-/* logits[b, v] (fp32, pitch ldl) = y[b] . E[v] for v in [v0, v1); y bf16 [B x d], B <= 8. */
+/* logits[b, v] (fp32, pitch ldl) = y[b] . E[v] for v in [v0, v1); y bf16 [B x d] (8 sequences per launch). */
 PB_API pb_status pb_op_logits(const void* y, int32_t B, int32_t d, const void* E, int32_t v0, int32_t v1,
                               float* logits, int32_t ldl, void* stream);
 
@@ -65,13 +75,6 @@ PB_API pb_status pb_op_argmax(const float* logits, int32_t B, int32_t V, int32_t
 PB_API pb_status pb_op_embed(const void* E, const void* pos, const int32_t* tok, float* h, int32_t d, int32_t r0,
                              int32_t r1, int32_t B, void* stream);
 
-/* Debug: copy the layer-chain item trace (recorded when PB_CHAIN_TRACE=1 at context creation time) of launch
- * slots [0, n_slots) to HOST memory `out` (n_slots * 1024 items * 8 uint64: claim, dependency met, accumulator
- * ready, published (bit 63 = this split finished the tile), arrival counted, smid << 48 | job << 40 | item-in-job,
- * first staged partial landed, reduction done; globaltimer ns), followed by the same shape of per-chunk stamps of
- * finishing epilogues (chunk k: [2k] partials staged, [2k+1] chunk done). `out` holds 2 * n_slots * 1024 * 8.
- * n_slots <= 64. */
-PB_API pb_status pb_op_chain_trace(uint64_t* out, int32_t n_slots);
 
 #ifdef __cplusplus
 }

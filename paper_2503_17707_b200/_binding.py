@@ -137,8 +137,9 @@ _SIGS = {
                    C.c_int32, C.c_float, C.c_int32, _P, C.c_int32, _P],
     "pb_op_gemm_split": [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int32, C.c_int32, C.c_int32, _P,
                          C.c_int32, C.c_float, C.c_int32, _P, C.c_int32, C.c_int32, _P],
+    "pb_op_gemm_rope": [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int32, _P, C.c_int32, C.c_int32,
+                        C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_float, _P, C.c_int32, _P],
     "pb_op_norm": [_P, C.c_int32, C.c_int32, _P, _P, C.c_float, _P, _P],
-    "pb_op_chain_trace": [_P, C.c_int32],
     "pb_op_attention": [_P, C.c_int32, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                         C.c_int32, C.c_int32, C.c_int32, C.c_float, _P],
     "pb_op_rope": [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
@@ -422,16 +423,14 @@ def pb_op_gemm_split(X, x_rows, m_begin, m_end, K, W, n_rows, N, epi, bias, relu
                                  ldo, split_k, stream))
 
 
+def pb_op_gemm_rope(X, x_rows, m_begin, m_end, K, W, N, out, ldo, rope_cols, hd, row0, B, T, theta, table, split_k,
+                    stream):
+    check(lib().pb_op_gemm_rope(X, x_rows, m_begin, m_end, K, W, N, out, ldo, rope_cols, hd, row0, B, T, theta, table,
+                                split_k, stream))
+
+
 def pb_op_norm(h, rows, d, gamma, beta, eps, out, stream=0):
     check(lib().pb_op_norm(h, rows, d, gamma, beta, eps, out, stream))
-
-
-def pb_op_chain_trace(n_slots):
-    """Debug: the layer-chain item trace (PB_CHAIN_TRACE=1) as a uint64 array [n_slots, 1024, 8]."""
-    import numpy as np
-    out = np.zeros((2, n_slots, 1024, 8), dtype=np.uint64)
-    check(lib().pb_op_chain_trace(out.ctypes.data, n_slots))
-    return out[0], out[1]
 
 
 def pb_op_attention(qkv, ld, out, ldo, t0, t1, B, n_heads, n_kv_heads, hd, k_col0, v_col0, score_scale, stream=0):

@@ -6,21 +6,19 @@
 // CTA = (128 query positions, head, sequence); 160 threads:
 //   warps 0-3 : softmax + epilogue, one query row per thread = one TMEM lane
 //   warp 4    : TMA producer and single-thread MMA issuer
-// Per 128-key tile j (keys [0, q_tile_end) only — causal):
-//   S = Q K_j^T            tcgen05.mma M128 N128, K = hd, fp32 accumulator in TMEM columns [0, 128)
-//   P = exp2(S*c - m)      softmax threads: tcgen05.ld the row, mask j > t, running max with lazy rescale
-//                          (O and l are rescaled only when the max grows by more than 2^8, FA4-style), P rounded
-//                          to bf16 pairs and stored back into TMEM (tcgen05.st) — no shared-memory round trip
-//   O += P V_j             tcgen05.mma M128 N=hd, K = 128 keys, A = P read from TMEM, V read MN-major straight
+// Two passes over the 128-key tiles j (keys [0, q_tile_end) only — causal), so that the probabilities are rounded
+// to bf16 after normalisation, at exactly the storage contract's rounding point:
+//   pass A:  S = Q K_j^T   tcgen05.mma M128 N128, K = hd, fp32 accumulator in TMEM columns [0, 128);
+//            softmax threads: tcgen05.ld the row, mask j > t, running max m (exact) and l = sum exp2(s*c - m)
+//   pass B:  S = Q K_j^T again; P = RNE_bf16(exp2(s*c - m) / l) stored as bf16 pairs into TMEM (tcgen05.st);
+//            O += P V_j    tcgen05.mma M128 N=hd, K = 128 keys, A = P read from TMEM, V read MN-major straight
 //                          from its TMA tile, fp32 accumulator in TMEM columns [128, 128 + hd)
-//   out = bf16(O / l)      l = sum of the bf16-rounded P actually multiplied
-// K and V are double-buffered (K_{j+2} streams in while softmax j runs); S_{j+1} overlaps softmax j and PV_j. Q/K/V come through one
+//   out = RNE_bf16(O)
+// K streams through a 2-buffer ring over the 2 x n_kv iterations (K of iteration i+2 loads while softmax i runs),
+// V is double-buffered in pass B; S_{i+1} is issued as soon as softmax i has read S_i. Q/K/V come through one
 // 3-D tensor map over the token-major qkv rows (col, sequence b, position t) whose t extent is t1, so keys
 // past the last computed position are zero-filled by TMA, never read.
-//
-// Numerics vs the oracle's storage contract: the oracle rounds the NORMALISED probabilities to
-// bf16; here the unnormalised exp2 values are rounded (the tensor-core operand) and normalisation happens
-// in fp32 at the end — a rounding-order difference bounded in tests/test_gpu_kernels.py::test_attention.
+// Cost of contract-exact rounding: the QK^T MMAs and the exponentials run twice (pass A has no PV).
 #include <cuda_bf16.h>
 #include <math_constants.h>
 
@@ -34,7 +32,6 @@ namespace {
 
 constexpr int QT = 128, KT = 128;
 constexpr int kAtom = 128 * 128;       // one 128-row x 64-col bf16 SW128 box = 16 KB
-constexpr float kRescale = 8.0f;       // lazy rescale threshold (log2 domain)
 
 __device__ __forceinline__ float fast_exp2(float x) {
     float y;
@@ -97,6 +94,12 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
     const uint32_t tS = tmem, tO = tmem + 128, tP = tmem + 128 + HD;
     pdl_wait();   // q/k/v are the previous kernel's output
 
+    // Two passes over the key tiles, so the probabilities are rounded to bf16 AFTER normalisation, exactly where the
+    // storage contract rounds them (P = RNE_bf16(softmax(S))):
+    //   pass A (iterations i < n_kv):  S_j -> row max m and row sum l = sum exp2(s*c - m) (exact rescale per tile)
+    //   pass B (iterations i >= n_kv): S_j again -> P = RNE_bf16(exp2(s*c - m) / l) -> O += P V_j
+    // The output is then RNE_bf16(O) with no final division.
+    const int NI = 2 * n_kv;
     if (warp == 4) {
         if (lane == 0) {
             constexpr int kBox = kAtom;   // bytes of one 64-col box
@@ -104,21 +107,24 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
 #pragma unroll
                 for (int a = 0; a < HD / 64; ++a) tma_load_3d(dst + a * kBox, &map, bar, col + a * 64, b, t);
             };
+            auto kv_of = [&](int i) { return i < n_kv ? i : i - n_kv; };
             mbar_arrive_expect_tx(q_full, SM::kQ);
             load_rows(sQ, q_full, h * HD, q0);
-            for (int j = 0; j < 2 && j < n_kv; ++j) {   // K_0, K_1, V_0, V_1 up front
-                mbar_arrive_expect_tx(&k_full[j], SM::kK);
-                load_rows(sK + j * SM::kK, &k_full[j], k_col0 + kvh * HD, j * KT);
+            for (int i = 0; i < 2 && i < NI; ++i) {   // K of iterations 0 and 1
+                mbar_arrive_expect_tx(&k_full[i], SM::kK);
+                load_rows(sK + i * SM::kK, &k_full[i], k_col0 + kvh * HD, kv_of(i) * KT);
+            }
+            for (int j = 0; j < 2 && j < n_kv; ++j) {   // V_0, V_1 (read in pass B)
                 mbar_arrive_expect_tx(&v_full[j], SM::kV);
                 load_rows(sV + j * SM::kV, &v_full[j], v_col0 + kvh * HD, j * KT);
             }
             constexpr uint32_t idS = idesc_bf16_f32(128, 128, 0, 0);
             constexpr uint32_t idO = idesc_bf16_f32(128, HD, 0, 1);
             mbar_wait(q_full, 0);
-            auto issue_S = [&](int j) {   // S = Q K_j^T into the (single) S columns
-                mbar_wait(&k_full[j & 1], (j >> 1) & 1);
+            auto issue_S = [&](int i) {   // S = Q K^T into the (single) S columns
+                mbar_wait(&k_full[i & 1], (i >> 1) & 1);
                 tc_fence_after();
-                const uint32_t kbase = smem_u32(sK + (j & 1) * SM::kK);
+                const uint32_t kbase = smem_u32(sK + (i & 1) * SM::kK);
 #pragma unroll
                 for (int kk = 0; kk < HD / 16; ++kk) {
                     const uint32_t off = (kk >> 2) * kBox + (kk & 3) * 32;
@@ -128,19 +134,21 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
                 umma_commit(s_full);
             };
             issue_S(0);
-            for (int j = 0; j < n_kv; ++j) {
-                const uint32_t ph = j & 1;
-                // ---- S_j done: its K buffer takes K_{j+2}
+            for (int i = 0; i < NI; ++i) {
+                const uint32_t ph = i & 1;
+                // ---- S_i done: its K buffer takes the K of iteration i + 2
                 mbar_wait(s_full, ph);
-                if (j + 2 < n_kv) {
-                    mbar_arrive_expect_tx(&k_full[j & 1], SM::kK);
-                    load_rows(sK + (j & 1) * SM::kK, &k_full[j & 1], k_col0 + kvh * HD, (j + 2) * KT);
+                if (i + 2 < NI) {
+                    mbar_arrive_expect_tx(&k_full[i & 1], SM::kK);
+                    load_rows(sK + (i & 1) * SM::kK, &k_full[i & 1], k_col0 + kvh * HD, kv_of(i + 2) * KT);
                 }
-                // ---- S_{j+1} as soon as softmax j has read S_j out of TMEM: it runs during softmax j
-                if (j + 1 < n_kv) {
+                // ---- S_{i+1} as soon as the softmax has read S_i out of TMEM
+                if (i + 1 < NI) {
                     mbar_wait(s_free, ph);
-                    issue_S(j + 1);
+                    issue_S(i + 1);
                 }
+                if (i < n_kv) continue;
+                const int j = i - n_kv;
                 // ---- V_{j+1} into the buffer PV_{j-1} has finished reading
                 if (j >= 1 && j + 1 < n_kv) {
                     mbar_wait(o_full, (j - 1) & 1);
@@ -149,7 +157,7 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
                     load_rows(sV + vb * SM::kV, &v_full[vb], v_col0 + kvh * HD, (j + 1) * KT);
                 }
                 // ---- O += P_j V_j
-                mbar_wait(p_full, ph);
+                mbar_wait(p_full, j & 1);
                 mbar_wait(&v_full[j & 1], (j >> 1) & 1);
                 tc_fence_after();
                 const uint32_t vbase = smem_u32(sV + (j & 1) * SM::kV);
@@ -170,9 +178,11 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
         const int t = q0 + r;
         const bool row_ok = t < q_hi;   // rows past t1 are computed (never masked, always finite) but not stored
         const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-        float m = -CUDART_INF_F, l = 0.f;
-        for (int j = 0; j < n_kv; ++j) {
-            const uint32_t ph = j & 1;
+        float m = -CUDART_INF_F, l = 0.f, inv_l = 0.f;
+        for (int i = 0; i < NI; ++i) {
+            const uint32_t ph = i & 1;
+            const bool pass_b = i >= n_kv;
+            const int j = pass_b ? i - n_kv : i;
             mbar_wait(s_full, ph);
             tc_fence_after();
             uint32_t sr[4][32];
@@ -182,80 +192,57 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(s_free);
-            // causal mask (key > t) only on the tiles that reach past the first query of this query tile; the
-            // max is taken on raw scores and scaled once (scale > 0). Rows past t1 are computed but never stored.
+            // causal mask (key > t) only on the tiles that reach past the first query of this query tile
             const int key0 = j * KT;
-            float mx = -CUDART_INF_F;
             if (key0 + KT - 1 > q0) {
 #pragma unroll
                 for (int c = 0; c < 4; ++c)
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        float v = __uint_as_float(sr[c][i]);
-                        if (key0 + c * 32 + i > t) {
-                            v = -CUDART_INF_F;
-                            sr[c][i] = __float_as_uint(v);
-                        }
-                        mx = fmaxf(mx, v);
-                    }
-            } else {
+                    for (int e = 0; e < 32; ++e)
+                        if (key0 + c * 32 + e > t) sr[c][e] = __float_as_uint(-CUDART_INF_F);
+            }
+            if (!pass_b) {
+                // ---- pass A: exact running max (scale > 0: max of raw scores, scaled once) and rescaled sum
+                float mx = -CUDART_INF_F;
 #pragma unroll
                 for (int c = 0; c < 4; ++c)
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(sr[c][i]));
+                    for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(sr[c][e]));
+                const float m_new = fmaxf(m, mx * scale_log2);
+                float rs = 0.f;
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) rs += fast_exp2(fmaf(__uint_as_float(sr[c][e]), scale_log2, -m_new));
+                l = (m == -CUDART_INF_F ? 0.f : l * fast_exp2(m - m_new)) + rs;
+                m = m_new;
+                continue;
             }
-            mx *= scale_log2;
-            // lazy rescale: keep the reference max unless the row max grew by more than 2^8
-            const bool grow = mx > m + kRescale;   // false when mx == -inf
-            const float m_new = grow ? mx : m;
-            const float alpha = (grow && m != -CUDART_INF_F) ? exp2f(m - m_new) : 1.f;
-            // O (TMEM) is written by PV_{j-1}; rescaling it, and overwriting P, wait for that MMA
-            if (j > 0) {
+            // ---- pass B: P = RNE_bf16(exp2(s*c - m) / l) straight into TMEM (the A operand of the PV MMA)
+            if (j == 0) inv_l = 1.f / l;   // l >= 1: the row maximum contributes exp2(0)
+            if (j > 0) {   // P (TMEM) is read by PV_{j-1}
                 mbar_wait(o_full, (j - 1) & 1);
                 tc_fence_after();
             }
-            if (__any_sync(0xffffffffu, alpha != 1.f)) {
-#pragma unroll
-                for (int c = 0; c < HD / 32; ++c) {
-                    uint32_t o[32];
-                    tmem_ld32_async(tO + lane_off + c * 32, o);
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-                    tmem_st32(tO + lane_off + c * 32, o);
-                }
-                tmem_wait_st();
-            }
-            l *= alpha;
-            m = m_new;
-            // P row -> bf16 pairs straight into TMEM (the A operand of the PV MMA): 32 keys -> 16 columns
-            float rs = 0.f;
 #pragma unroll
             for (int cb = 0; cb < 4; ++cb) {
                 uint32_t w[16];
 #pragma unroll
                 for (int e = 0; e < 16; ++e) {
-                    const float s0 = __uint_as_float(sr[cb][2 * e]);
-                    const float s1 = __uint_as_float(sr[cb][2 * e + 1]);
-                    const float p0 = fast_exp2(fmaf(s0, scale_log2, -m));   // masked: ex2(-inf) = 0
-                    const float p1 = fast_exp2(fmaf(s1, scale_log2, -m));
-                    const __nv_bfloat162 pb = __floats2bfloat162_rn(p0, p1);
-                    const float2 pr = __bfloat1622float2(pb);
-                    rs += pr.x + pr.y;
-                    w[e] = *reinterpret_cast<const uint32_t*>(&pb);
+                    const float p0 = fast_exp2(fmaf(__uint_as_float(sr[cb][2 * e]), scale_log2, -m)) * inv_l;
+                    const float p1 = fast_exp2(fmaf(__uint_as_float(sr[cb][2 * e + 1]), scale_log2, -m)) * inv_l;
+                    w[e] = bf16x2_bits(p0, p1);
                 }
                 tmem_st16(tP + lane_off + cb * 16, w);
             }
             tmem_wait_st();
-            l += rs;
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(p_full);
         }
-        // ---------------- epilogue: O / l -> bf16
+        // ---------------- epilogue: out = RNE_bf16(O)
         mbar_wait(o_full, (n_kv - 1) & 1);
         tc_fence_after();
-        const float inv = l > 0.f ? 1.f / l : 0.f;
         __nv_bfloat16* o_row = out + ((size_t)t * gridDim.z + b) * ldo + h * HD;
 #pragma unroll
         for (int c = 0; c < HD / 32; ++c) {
@@ -266,10 +253,10 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     uint4 w;
-                    w.x = bf16x2_bits(__uint_as_float(o[8 * q + 0]) * inv, __uint_as_float(o[8 * q + 1]) * inv);
-                    w.y = bf16x2_bits(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv);
-                    w.z = bf16x2_bits(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv);
-                    w.w = bf16x2_bits(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv);
+                    w.x = bf16x2_bits(__uint_as_float(o[8 * q + 0]), __uint_as_float(o[8 * q + 1]));
+                    w.y = bf16x2_bits(__uint_as_float(o[8 * q + 2]), __uint_as_float(o[8 * q + 3]));
+                    w.z = bf16x2_bits(__uint_as_float(o[8 * q + 4]), __uint_as_float(o[8 * q + 5]));
+                    w.w = bf16x2_bits(__uint_as_float(o[8 * q + 6]), __uint_as_float(o[8 * q + 7]));
                     *reinterpret_cast<uint4*>(o_row + c * 32 + q * 8) = w;
                 }
             }

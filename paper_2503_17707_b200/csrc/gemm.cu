@@ -48,6 +48,25 @@ static_assert(BM * 64 * 4 <= 2 * (kStageA + 64 * BK * 2), "64-column partial til
 
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
 
+// HF rotate_half RoPE on fp32 values (x1 = columns ci.., x2 = columns ci + hd/2.. of one head, both already summed):
+// x1' = x1 cos - x2 sin, x2' = x2 cos + x1 sin, angle = position * theta^(-2i/hd) from the fp64-built table.
+template <int NV>
+__device__ __forceinline__ void rope_rotate(const GemmArgs& a, int row, int ci, float (&x1)[NV], float (&x2)[NV]) {
+    const int half = a.rope_hd >> 1;
+    const int pos = (row - a.rope_row0) / a.rope_B;
+    const float2* tb = a.rope + (size_t)pos * half + ci;
+#pragma unroll
+    for (int e = 0; e < NV; ++e) {
+        const float2 cs = tb[e];
+        const float u = x1[e], w = x2[e];
+        x1[e] = fmaf(u, cs.x, -w * cs.y);
+        x2[e] = fmaf(w, cs.x, u * cs.y);
+    }
+}
+__device__ __forceinline__ void rope_rotate4(const GemmArgs& a, int row, int ci, float (&x1)[4], float (&x2)[4]) {
+    rope_rotate<4>(a, row, ci, x1, x2);
+}
+
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -240,6 +259,24 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
         }
         const int n = n_out0 + ch * 4;
         if (n >= a.N) continue;
+        if (EPI == EPI_BF16 && a.rope && n < a.rope_cols) {
+            // rotary pair (i, i + hd/2) of one head, both halves in this tile (128-column tiles, head-aligned): the
+            // thread owning the first half rotates and writes both, from the fp32 sums
+            const int half = a.rope_hd >> 1, ci = n % a.rope_hd;
+            if (ci >= half) continue;
+            const float4 p1 = sum_chunk(r, ch), p2 = sum_chunk(r, ch + (half >> 2));
+            float x1[4] = {p1.x, p1.y, p1.z, p1.w}, x2[4] = {p2.x, p2.y, p2.z, p2.w};
+            rope_rotate4(a, row, ci, x1, x2);
+            __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(a.out) + (size_t)row * a.ldo + n;
+            uint2 w1, w2;
+            w1.x = bf16x2_bits(x1[0], x1[1]);
+            w1.y = bf16x2_bits(x1[2], x1[3]);
+            w2.x = bf16x2_bits(x2[0], x2[1]);
+            w2.y = bf16x2_bits(x2[2], x2[3]);
+            *reinterpret_cast<uint2*>(out) = w1;
+            *reinterpret_cast<uint2*>(out + half) = w2;
+            continue;
+        }
         const float4 acc = sum_chunk(r, ch);
         float v[4] = {acc.x, acc.y, acc.z, acc.w};
         const int nv = min(4, a.N - n);
@@ -503,10 +540,41 @@ __global__ void __launch_bounds__(192, 1) gemm_big_kernel(const __grid_constant_
             } else {
 #pragma unroll 1
                 for (int cb = 0; cb < TBN / 32; ++cb) {
+                    const int n = n0 + cb * 32;
+                    if (EPI == EPI_BF16 && a.rope && n < a.rope_cols) {
+                        // rotary pair blocks (cb, cb + hd/64) of one head (256- / 128-column tiles are head-aligned):
+                        // rotate the fp32 accumulators, round once, write both halves
+                        const int half = a.rope_hd >> 1, ci = n % a.rope_hd;
+                        if (ci >= half) continue;
+                        uint32_t r1[32], r2[32];
+                        tmem_ld32_async(acc + cb * 32, r1);
+                        tmem_ld32_async(acc + cb * 32 + half, r2);
+                        tmem_wait_ld();
+                        if (!row_ok) continue;
+                        float x1[32], x2[32];
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) {
+                            x1[e] = __uint_as_float(r1[e]);
+                            x2[e] = __uint_as_float(r2[e]);
+                        }
+                        rope_rotate<32>(a, row, ci, x1, x2);
+                        __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(a.out) + (size_t)row * a.ldo + n;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            *reinterpret_cast<uint4*>(out + 8 * q) =
+                                make_uint4(bf16x2_bits(x1[8 * q], x1[8 * q + 1]), bf16x2_bits(x1[8 * q + 2], x1[8 * q + 3]),
+                                           bf16x2_bits(x1[8 * q + 4], x1[8 * q + 5]),
+                                           bf16x2_bits(x1[8 * q + 6], x1[8 * q + 7]));
+                            *reinterpret_cast<uint4*>(out + half + 8 * q) =
+                                make_uint4(bf16x2_bits(x2[8 * q], x2[8 * q + 1]), bf16x2_bits(x2[8 * q + 2], x2[8 * q + 3]),
+                                           bf16x2_bits(x2[8 * q + 4], x2[8 * q + 5]),
+                                           bf16x2_bits(x2[8 * q + 6], x2[8 * q + 7]));
+                        }
+                        continue;
+                    }
                     uint32_t r[32];
                     tmem_ld32_async(acc + cb * 32, r);
                     tmem_wait_ld();
-                    const int n = n0 + cb * 32;
                     if (!row_ok || n >= a.N) continue;
                     float v[32];
 #pragma unroll
@@ -644,6 +712,12 @@ __global__ void __launch_bounds__(GV_WARPS * 32) gemv_kernel(const GemmArgs a) {
             const int o = blockIdx.x * 2 + (r & 1);
             wok[r] = o < a.N;
             n = r < 2 ? o : a.up_row0 + o;
+        } else if (EPI == EPI_BF16 && a.rope && (int)blockIdx.x * GV_ROWS < a.rope_cols) {
+            // rotary CTA: rows {i, i+1} of a head's first half and their partners {i + hd/2, i + hd/2 + 1}
+            const int half = a.rope_hd >> 1, per_head = half / 2;
+            const int head = blockIdx.x / per_head, i0 = (blockIdx.x % per_head) * 2;
+            n = head * a.rope_hd + (r >= 2 ? half : 0) + i0 + (r & 1);
+            wok[r] = true;
         } else {
             n = blockIdx.x * GV_ROWS + r;
             wok[r] = n < a.N;
@@ -734,6 +808,15 @@ __global__ void __launch_bounds__(GV_WARPS * 32) gemv_kernel(const GemmArgs a) {
     const int n = wrow[r];
     float v = total(r);
     if (a.bias) v += __bfloat162float(a.bias[n]);
+    if (EPI == EPI_BF16 && a.rope && n < a.rope_cols) {   // rotary CTA: the partner row is r ^ 2
+        float w = total(r ^ 2);
+        if (a.bias) w += __bfloat162float(a.bias[wrow[r ^ 2]]);
+        const int half = a.rope_hd >> 1, ci = n % a.rope_hd;
+        float x1[1] = {r < 2 ? v : w}, x2[1] = {r < 2 ? w : v};
+        rope_rotate<1>(a, row, ci % half, x1, x2);
+        reinterpret_cast<__nv_bfloat16*>(a.out)[(size_t)row * a.ldo + n] = __float2bfloat16_rn(r < 2 ? x1[0] : x2[0]);
+        return;
+    }
     if (EPI == EPI_BF16) {
         if (n < a.scale_cols) v *= a.scale;
         if (a.relu) v = fmaxf(v, 0.0f);
@@ -811,6 +894,9 @@ cudaError_t warm_gemm_kernels() {
 cudaError_t launch_gemm(const CUtensorMap& mapX, const CUtensorMap& mapW, const GemmArgs& a, cudaStream_t s) {
     if (a.M_end <= a.M_begin || a.N <= 0) return cudaSuccess;
     if (a.K <= 0 || a.K % 8) return cudaErrorInvalidValue;
+    if (a.rope && (a.epi != EPI_BF16 || (a.rope_hd != 64 && a.rope_hd != 128) || a.rope_cols % a.rope_hd ||
+                   a.rope_B < 1 || a.bias || a.scale_cols > 0 || a.relu))
+        return cudaErrorInvalidValue;
     // M_total <= 8 (a decode step or a tiny prompt; chosen from the whole batch, so chunks agree): weight-streaming GEMV
     // Measured on B200, C2 decode ms/step GEMV vs tensor-core path: B=1 1.07 vs 1.46, B=2 1.56 vs 1.56, B=4 1.95 vs
     // 1.73 (the GEMV's fp32 FMA work grows with M and its registers with it), hence M_total <= kGemvAutoRows.
@@ -826,7 +912,8 @@ cudaError_t launch_gemm(const CUtensorMap& mapX, const CUtensorMap& mapW, const 
     // The kernel is chosen from the WHOLE prompt (M_total), never from the rows of this launch, so a prompt split
     // into chunks runs every output through the same kernel and the same summation order.
     if (S == 1 && a.split_k <= 0 && a.M_total > BM && !a.m_dyn) {
-        const int tw = a.mapW64 ? gemm_big_tile_n(a.N, a.epi, a.M_total) : BIG_BN;
+        int tw = a.mapW64 ? gemm_big_tile_n(a.N, a.epi, a.M_total) : BIG_BN;
+        if (a.rope && tw == 192) tw = BIG_BN;   // rotary pairs need head-aligned tiles
         switch (a.epi) {
             case EPI_BF16:
                 if (tw == 192) return launch_big<EPI_BF16, 192>(mapX, mapW, *a.mapW64, a, s);
@@ -839,7 +926,7 @@ cudaError_t launch_gemm(const CUtensorMap& mapX, const CUtensorMap& mapW, const 
             case EPI_SILU_MUL: return launch_big<EPI_SILU_MUL>(mapX, mapW, mapW, a, s);
         }
     }
-    const int tbn = a.split_k <= 0 && a.mapW64 ? gemm_tile_n(a.N, a.K, a.epi, a.M_total) : BN;
+    const int tbn = a.split_k <= 0 && a.mapW64 && !a.rope ? gemm_tile_n(a.N, a.K, a.epi, a.M_total) : BN;
     switch (a.epi) {
         case EPI_BF16: return launch_epi<EPI_BF16>(mapX, mapW, a, S, tbn, s);
         case EPI_RESID: return launch_epi<EPI_RESID>(mapX, mapW, a, S, tbn, s);

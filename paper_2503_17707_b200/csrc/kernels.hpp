@@ -111,6 +111,12 @@ struct GemmArgs {
     const __nv_bfloat16* W;     // [rows x K] row-major (rows as for mapW)
     // the same weights with 64-row boxes (64-column tiles, gemm_tile_n); null = 128-column tiles only (host pointer)
     const CUtensorMap* mapW64;
+    // Llama QKV (EPI_BF16): rotary embedding applied to the fp32 accumulator BEFORE the one bf16 rounding, so
+    // q/k = RNE_bf16(rope(x Wqk^T)) exactly as the storage contract says. Columns [0, rope_cols)
+    // are q and k heads of rope_hd columns each (head-aligned); output row r is at position
+    // (r - rope_row0) / rope_B; rope = [positions][rope_hd / 2] (cos, sin) table. null = no rotation.
+    const float2* rope;
+    int rope_cols, rope_hd, rope_row0, rope_B;
 };
 int gemm_tile_n(int N, int K, int epi, int M_total);
 constexpr int kGemvAutoRows = 2;   // rows up to which launch_gemm picks the GEMV
@@ -118,44 +124,6 @@ int gemm_split_k(int N, int K, int epi, int M_total);
 // Maps: X box {64, 128} SW128 over [max_rows x K]; W box {64, 128} (EPI_SILU_MUL: {64, 64}) SW128 over [rows x K].
 cudaError_t launch_gemm(const CUtensorMap& mapX, const CUtensorMap& mapW, const GemmArgs& a, cudaStream_t s);
 
-// ---------------------------------------------------------------- layer chain (chain.cu)
-// One persistent launch for a dependent sequence of prefill steps at prompt sizes of one 128-row tile: the
-// post-attention half of a layer, O (+ residual) -> norm 2 -> FC1 | gate·up -> FC2 | down (+ residual).
-// Every job's arithmetic is bit-identical to the per-op kernels (gemm_kernel<EPI, S> with the same split-K S,
-// norm_kernel), so results do not depend on which path ran.
-enum ChainJobType : int { CHAIN_GEMM = 0, CHAIN_NORM = 1 };
-constexpr int kChainMaxJobs = 4;
-constexpr int kChainMaxTiles = 1024;                                  // output tiles per GEMM job
-constexpr int kChainCtlWords = 8 + kChainMaxJobs * kChainMaxTiles;   // next, exited, done[jobs], tile arrivals
-constexpr int kChainCtlSets = 4;                                       // rotated over consecutive launches
-struct alignas(64) ChainJob {
-    CUtensorMap mx, mw;        // GEMM: the maps launch_gemm takes
-    int type;
-    int epi, S, N, K, relu, scale_cols, ldo, up_row0;   // GEMM (S = gemm_split_k of the same shape)
-    float scale;
-    const __nv_bfloat16* bias;
-    void* out;
-    const float* h;            // NORM: fp32 rows [*, ldh] -> bf16 nout [*, ldno]
-    __nv_bfloat16* nout;
-    const __nv_bfloat16* gamma;
-    const __nv_bfloat16* beta; // null: RMSNorm
-    int ldh, ldno, d;
-    float eps;
-};
-struct alignas(64) ChainArgs {
-    ChainJob job[kChainMaxJobs];
-    int n_jobs;
-    int M_begin, M_end;        // rows computed (M_end - M_begin <= 128)
-    uint32_t* ctl;             // kChainCtlWords zeroed words (the kernel leaves them zeroed)
-    float* part;               // split-K partial tiles: max over jobs of S * tiles * 128 * 128 fp32
-    int pdl;
-    int trace_slot;            // >= 0: record per-item timestamps in launch slot trace_slot (debug)
-    unsigned long long* trace; // set by launch_chain when tracing
-};
-cudaError_t chain_trace_copy(unsigned long long* host, int n_slots);
-int chain_norm_ok(int d);                          // d within the norm item's register budget
-size_t chain_part_bytes(int N, int K, int epi);    // partial bytes a GEMM job of this shape needs
-cudaError_t launch_chain(const ChainArgs& a, cudaStream_t s);
 
 // ---------------------------------------------------------------- SIMT kernels
 // Row norm over d of fp32 rows -> bf16: LayerNorm (beta != null) or RMSNorm (beta == null).
@@ -202,7 +170,6 @@ cudaError_t launch_argmax(const float* logits, int B, int V, int ldl, int32_t* t
 // deadlock). Called once per device from pb_ctx_create.
 cudaError_t warm_merge_kernels();
 cudaError_t warm_gemm_kernels();
-cudaError_t warm_chain_kernel();
 cudaError_t warm_simt_kernels();
 cudaError_t warm_attention_kernels();
 cudaError_t warm_f32_kernels();

@@ -74,6 +74,47 @@ extern "C" pb_status pb_op_gemm_split(const void* X, int32_t x_rows, int32_t m_b
     return cuda_status(launch_gemm(mx, mw, a, (cudaStream_t)stream), "gemm");
 }
 
+extern "C" pb_status pb_op_gemm_rope(const void* X, int32_t x_rows, int32_t m_begin, int32_t m_end, int32_t K,
+                                     const void* W, int32_t N, void* out, int32_t ldo, int32_t rope_cols, int32_t hd,
+                                     int32_t row0, int32_t B, int32_t T, float theta, void* table, int32_t split_k,
+                                     void* stream) {
+    if (!X || !W || !out || !table) return fail(PB_EINVAL, "pb_op_gemm_rope: null pointer");
+    if (K % 8 || K <= 0 || m_begin < 0 || m_end > x_rows || B < 1 || T < 1 || (hd != 64 && hd != 128) ||
+        rope_cols % hd || rope_cols > N || row0 > m_begin || (m_end - 1 - row0) / B >= T)
+        return fail(PB_EINVAL, "pb_op_gemm_rope: bad shape");
+    if (split_k < 0 || split_k > 8 || (split_k & (split_k - 1)))
+        return fail(PB_EINVAL, "pb_op_gemm_rope: split_k %d out of range", split_k);
+    cudaStream_t s = (cudaStream_t)stream;
+    pb_status st = cuda_status(launch_rope_table(static_cast<float2*>(table), T, hd, theta, s), "rope table");
+    if (st) return st;
+    CUtensorMap mx, mw;
+    char err[512];
+    if (!make_map_bf16(&mx, X, x_rows, K, K, 128, 64, 128, err, sizeof err) ||
+        !make_map_bf16(&mw, W, N, K, K, 128, 64, 128, err, sizeof err))
+        return fail(PB_EINVAL, "%s", err);
+    GemmArgs a{};
+    a.M_begin = m_begin;
+    a.M_end = m_end;
+    a.N = N;
+    a.K = K;
+    a.epi = EPI_BF16;
+    a.scale = 1.0f;
+    a.out = out;
+    a.ldo = ldo;
+    a.up_row0 = N;
+    a.split_k = split_k;
+    a.M_total = m_end - m_begin;
+    a.X = static_cast<const __nv_bfloat16*>(X);
+    a.ldx = K;
+    a.W = static_cast<const __nv_bfloat16*>(W);
+    a.rope = static_cast<const float2*>(table);
+    a.rope_cols = rope_cols;
+    a.rope_hd = hd;
+    a.rope_row0 = row0;
+    a.rope_B = B;
+    return cuda_status(launch_gemm(mx, mw, a, s), "gemm rope");
+}
+
 extern "C" pb_status pb_op_norm(const float* h, int32_t rows, int32_t d, const void* gamma, const void* beta, float eps,
                                 void* out, void* stream) {
     if (!h || !gamma || !out) return fail(PB_EINVAL, "pb_op_norm: null pointer");
@@ -131,7 +172,3 @@ extern "C" pb_status pb_op_embed(const void* E, const void* pos, const int32_t* 
                        "embed");
 }
 
-extern "C" pb_status pb_op_chain_trace(uint64_t* out, int32_t n_slots) {
-    if (!out || n_slots < 1 || n_slots > 64) return fail(PB_EINVAL, "pb_op_chain_trace: bad arguments");
-    return cuda_status(chain_trace_copy(reinterpret_cast<unsigned long long*>(out), n_slots), "chain trace");
-}

@@ -160,16 +160,6 @@ WsLayout pb::ws_layout(const pb_plan* p, int32_t batch, int32_t seq) {
     L.rope = o;    o = al(o + (m.arch == PB_ARCH_LLAMA ? 8 * (int64_t)seq * (hd / 2) : 0));
     L.held = o;    o = al(o + (p->survivors.empty() ? 0 : 4 * (int64_t)p->chunks.size()));   // re-plan signal list
     L.dpos = o;    o = al(o + 4);   // f3 decode graphs: the step's position
-    // layer chain: control words (rotated sets) and the split-K partial tiles of its GEMM jobs (bf16 path)
-    L.chain_ctl = o; o = al(o + (ea == 2 ? 4 * (int64_t)kChainCtlWords * kChainCtlSets : 0));
-    int64_t part = 0;
-    if (ea == 2) {
-        const int up_epi = m.arch == PB_ARCH_OPT ? EPI_BF16 : EPI_SILU_MUL;
-        part = std::max<int64_t>({(int64_t)chain_part_bytes((int)d, (int)qd, EPI_RESID),
-                                  (int64_t)chain_part_bytes((int)f, (int)d, up_epi),
-                                  (int64_t)chain_part_bytes((int)d, (int)f, EPI_RESID)});
-    }
-    L.chain_part = o; o = al(o + part);
     L.total = al(o, 4096);
     return L;
 }
@@ -360,7 +350,6 @@ extern "C" pb_status pb_ctx_create(const pb_plan* plan, int32_t rank, const void
         if (!warmed.count(dev)) {
             cudaError_t e = warm_merge_kernels();
             if (e == cudaSuccess) e = warm_gemm_kernels();
-            if (e == cudaSuccess) e = warm_chain_kernel();
             if (e == cudaSuccess) e = warm_simt_kernels();
             if (e == cudaSuccess) e = warm_attention_kernels();
             if (e == cudaSuccess) e = warm_f32_kernels();
@@ -475,12 +464,10 @@ extern "C" pb_status pb_ctx_create(const pb_plan* plan, int32_t rank, const void
         cudaHostAlloc((void**)&c->h_tokens, sizeof(int32_t) * L.max_rows, cudaHostAllocPortable) != cudaSuccess ||
         cudaHostAlloc((void**)&c->h_out, sizeof(int32_t) * (L.max_batch + 1), cudaHostAllocPortable) != cudaSuccess)
         return cleanup(fail(PB_ECUDA, "cudaHostAlloc failed"));
-    if (const char* ch = getenv("PB_CHAIN")) c->use_chain = atoi(ch) != 0;
     // readiness words start at 0 (epochs are >= 1); the q|k|v slots start at 0 so a key row no step has written
     // yet is finite (decode graphs view keys up to max_seq and mask the later ones)
     if (cudaMemset(c->ws + L.flags, 0, 4 * (size_t)L.n_words) != cudaSuccess ||
         cudaMemset(c->ws + L.qkv, 0, (size_t)L.qkv_stride * L.n_qkv) != cudaSuccess ||
-        cudaMemset(c->ws + L.chain_ctl, 0, (size_t)(L.chain_part - L.chain_ctl)) != cudaSuccess ||
         cudaDeviceSynchronize() != cudaSuccess)
         return cleanup(fail(PB_ECUDA, "flag init failed"));
     c->ctx_create_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_create).count();
@@ -687,8 +674,7 @@ extern "C" pb_status pb_kernel_stats(pb_ctx* c, pb_kernel_stat* out, int32_t cap
     pb_status st = check_ctx(c, "pb_kernel_stats");
     if (st) return st;
     if (!n) return fail(PB_EINVAL, "pb_kernel_stats: null n");
-    static const char* names[K_NCLASS] = {"merge", "gemm", "attention", "norm", "rope", "embed", "logits", "argmax", "signal",
-                                          "layer_chain"};
+    static const char* names[K_NCLASS] = {"merge", "gemm", "attention", "norm", "rope", "embed", "logits", "argmax", "signal"};
     pb_kernel_stat agg[K_NCLASS];
     for (int k = 0; k < K_NCLASS; ++k) agg[k] = {names[k], 0, 0.0, 0.0, 0.0};
     for (size_t i = 0; i < c->prof_n; ++i) {
@@ -908,13 +894,14 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, boo
     CU(need(opt ? "qkv_b" : "qkv"));
     GemmArgs a = G(r0, qdim, d, EPI_BF16, opt ? wt(c, l, "qkv_b") : nullptr, 0, opt ? 1.0f / sqrtf((float)hd) : 1.0f,
                    opt ? d : 0, qkv, qdim);
-    CU(gemm(c->map_x, lm.qkv, a, qdim, x, d, 0));
-    if (!opt) {
-        const int pi = prof_begin(c, K_ROPE, s);
-        CU(launch_rope(qkv + (size_t)row_base * qdim, qdim, r0 - row_base, r1 - row_base, B, H, KVH, hd, qd,
-                       reinterpret_cast<const float2*>(c->ws + L.rope), s, !c->profiling, c->dyn_pos));
-        prof_end(c, pi, s, 6.0 * rows * (qd + kvd) / 2, 4.0 * rows * (qd + kvd));
+    if (!opt) {   // Llama: RoPE on the fp32 accumulator inside the QKV epilogue, one rounding (storage contract)
+        a.rope = reinterpret_cast<const float2*>(c->ws + L.rope);
+        a.rope_cols = qd + kvd;
+        a.rope_hd = hd;
+        a.rope_row0 = row_base;
+        a.rope_B = B;
     }
+    CU(gemm(c->map_x, lm.qkv, a, qdim, x, d, 0));
     {
         const int pi = prof_begin(c, K_ATTN, s);
         CU(launch_attention(qkv + (size_t)row_base * qdim, qdim, attn + (size_t)row_base * qd, qd, ta, tb, B, H, KVH,
@@ -923,70 +910,6 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, boo
         // causal pairs: sum over queries t in [ta, tb) of (t + 1) keys
         const double pairs = (double)B * ((double)tb * (tb + 1) / 2 - (double)ta * (ta + 1) / 2);
         prof_end(c, pi, s, 4.0 * pairs * H * hd, 2.0 * rows * qd * 2 + 2.0 * B * tb * 2 * kvd);
-    }
-    if (c->use_chain && c->gemm_m_total <= 128 && !c->dyn_pos && chain_norm_ok(d)) {
-        // O -> norm 2 -> FC1 | gate·up -> FC2 | down as one persistent launch (chain.cu; bit-identical to the
-        // per-op kernels below)
-        CU(need(opt ? "o_b" : "o"));
-        CU(need(opt ? "ln2_b" : "ln2_g"));
-        CU(need(opt ? "fc1_b" : "gate_up"));
-        CU(need(opt ? "fc2_b" : "down"));
-        ChainArgs ca{};
-        auto gj = [&](ChainJob& J, const CUtensorMap& mx, const CUtensorMap& mw, const GemmArgs& g) {
-            J.mx = mx;
-            J.mw = mw;
-            J.type = CHAIN_GEMM;
-            J.epi = g.epi;
-            J.S = gemm_split_k(g.N, g.K, g.epi, g.M_total);
-            J.N = g.N;
-            J.K = g.K;
-            J.relu = g.relu;
-            J.scale_cols = g.scale_cols;
-            J.ldo = g.ldo;
-            J.up_row0 = g.up_row0;
-            J.scale = g.scale;
-            J.bias = g.bias;
-            J.out = g.out;
-        };
-        gj(ca.job[0], c->map_attn, lm.o, G(r0, d, qd, EPI_RESID, opt ? wt(c, l, "o_b") : nullptr, 0, 1.f, 0, h, d));
-        ChainJob& nj = ca.job[1];
-        nj.type = CHAIN_NORM;
-        nj.h = h;
-        nj.ldh = d;
-        nj.nout = x;
-        nj.ldno = d;
-        nj.d = d;
-        nj.gamma = wt(c, l, "ln2_g");
-        nj.beta = opt ? wt(c, l, "ln2_b") : nullptr;
-        nj.eps = m.norm_eps;
-        if (opt) {
-            gj(ca.job[2], c->map_x, lm.up, G(r0, f, d, EPI_BF16, wt(c, l, "fc1_b"), 1, 1.f, 0, mlp, f));
-            gj(ca.job[3], c->map_mlp, lm.down, G(r0, d, f, EPI_RESID, wt(c, l, "fc2_b"), 0, 1.f, 0, h, d));
-        } else {
-            gj(ca.job[2], c->map_x, lm.up, G(r0, f, d, EPI_SILU_MUL, nullptr, 0, 1.f, 0, mlp, f));
-            gj(ca.job[3], c->map_mlp, lm.down, G(r0, d, f, EPI_RESID, nullptr, 0, 1.f, 0, h, d));
-        }
-        ca.n_jobs = 4;
-        ca.M_begin = r0;
-        ca.M_end = r1;
-        ca.ctl = reinterpret_cast<uint32_t*>(c->ws + L.chain_ctl) +
-                 (size_t)(c->chain_seq++ % kChainCtlSets) * kChainCtlWords;
-        ca.part = reinterpret_cast<float*>(c->ws + L.chain_part);
-        ca.pdl = c->profiling ? 0 : 1;
-        static const bool trace = getenv("PB_CHAIN_TRACE") && atoi(getenv("PB_CHAIN_TRACE")) != 0;
-        static std::atomic<int> trace_next{0};
-        ca.trace_slot = trace ? trace_next++ : -1;
-        const double M = rows;
-        const int wup = opt ? f : 2 * f;
-        const double flops = 2.0 * M * ((double)d * qd + (double)wup * d + (double)d * f) + 8.0 * M * d;
-        const double bytes = (2.0 * M * qd + 2.0 * d * qd + 8.0 * M * d) + 6.0 * M * d +
-                             (2.0 * M * d + 2.0 * wup * d + 2.0 * M * f) + (2.0 * M * f + 2.0 * d * f + 8.0 * M * d);
-        const int pi = prof_begin(c, K_CHAIN, s);
-        CU(launch_chain(ca, s));
-        prof_end(c, pi, s, flops, bytes);
-        c->n_launches += 4;   // ln1, qkv (+ rope), attention, chain
-        if (!opt) c->n_launches += 1;
-        return PB_OK;
     }
     CU(need(opt ? "o_b" : "o"));
     a = G(r0, d, qd, EPI_RESID, opt ? wt(c, l, "o_b") : nullptr, 0, 1.f, 0, h, d);
@@ -1009,7 +932,7 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, boo
         a = G(r0, d, f, EPI_RESID, nullptr, 0, 1.f, 0, h, d);
         CU(gemm(c->map_mlp, lm.down, a, d, mlp, f, 3));
     }
-    c->n_launches += opt ? 7 : 8;
+    c->n_launches += 7;   // norm, qkv (+ RoPE for Llama), attention, o, norm, fc1|gate_up, fc2|down
     return PB_OK;
 }
 
@@ -1620,7 +1543,6 @@ pb_status post_prompt(pb_ctx* c, TrialRun& run, int B, int T) {
     I.T = T;
     I.n_mb = I.mb_mode ? B : 1;
     I.dec_t = c->decode_t;
-    c->chain_seq = 0;
     if (I.dec_t >= 0) {   // f3 decode step: one "prompt chunk" holding position dec_t of every sequence
         I.k = 1;
         I.tb = {I.dec_t, I.dec_t + 1};
@@ -1868,9 +1790,17 @@ extern "C" pb_status pb_prefill_enqueue_ex(pb_ctx* c, const int32_t* tokens, con
 extern "C" pb_status pb_prefill_replay(pb_ctx* c, uint32_t epoch, const int32_t* tokens, int32_t B, int32_t T) {
     pb_status st = check_ctx(c, "pb_prefill_replay");
     if (st) return st;
-    if (c->phase != Phase::Prefilled) return fail(PB_EPROTOCOL, "pb_prefill_replay: needs a completed cold start");
+    if (c->phase != Phase::Prefilled && c->phase != Phase::Gathered)
+        return fail(PB_EPROTOCOL, "pb_prefill_replay: needs a completed cold start");
     if (epoch <= c->epoch) return fail(PB_EINVAL, "epoch %u must exceed the previous %u", epoch, c->epoch);
     join_load(c);
+    if (c->phase == Phase::Gathered) {   // a cold start without a prompt: serve once it has reached T_full
+        if (c->issue_status != PB_OK) return fail(c->issue_status, "issuer: %s", c->issue_msg);
+        if (cudaEventQuery(c->gather_done) != cudaSuccess || cudaEventQuery(c->merge_done) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(PB_EPROTOCOL, "pb_prefill_replay: the armed cold start has not reached T_full (pb_sync first)");
+        }
+    }
     CU(cudaStreamSynchronize(c->comp));
     c->epoch = epoch;
     c->n_launches = 0;
@@ -2187,12 +2117,14 @@ extern "C" pb_status pb_ctx_abort(pb_ctx* c) {
     if (st) return st;
     c->abort_req.store(true);
     join_load(c);   // the issuer returns at its next poll (it never blocks in an enqueue: outstanding-op budgets)
-    // force every readiness word of this rank open: waits are `word >= epoch`, so 0xFFFFFFFF releases all of them
-    cudaStream_t probe;
-    CU(cudaStreamCreateWithFlags(&probe, cudaStreamNonBlocking));
-    cudaError_t e = cudaMemsetAsync(c->ws + c->L.flags, 0xFF, 4 * (size_t)c->L.n_words, probe);
-    if (e == cudaSuccess) e = drain_stream(probe, 10.0) ? cudaSuccess : cudaErrorNotReady;
-    cudaStreamDestroy(probe);
+    // force every readiness word of this rank open. CU_STREAM_WAIT_VALUE_GEQ compares cyclically,
+    // (int32_t)(word - epoch) >= 0, so the words get epoch + 2^30 (0xFFFFFFFF would read as "before" the epoch)
+    // on the ctx's spare lane (stream_h2d[1]): it never waits on a readiness word and owns its hardware queue (a
+    // freshly created stream could share a queue with a blocked one and sit behind the very wait it must release)
+    const std::vector<uint32_t> open_words((size_t)c->L.n_words, c->epoch + 0x40000000u);
+    cudaError_t e = cudaMemcpyAsync(c->ws + c->L.flags, open_words.data(), 4 * open_words.size(),
+                                    cudaMemcpyHostToDevice, c->h2d[1]);
+    if (e == cudaSuccess) e = drain_stream(c->h2d[1], 10.0) ? cudaSuccess : cudaErrorNotReady;
     c->aborted = true;
     c->phase = Phase::Idle;
     CU(e);

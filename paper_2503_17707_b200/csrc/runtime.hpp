@@ -22,7 +22,7 @@ struct TrialRun;   // the trial issuer's state (runtime.cpp)
 // peer can address it: flags | tokens | h | x | qkv[n_qkv] | attn | mlp | y | logits | tok_out | nan | rope.
 struct WsLayout {
     int64_t flags = 0, tokens = 0, h = 0, x = 0, qkv = 0, qkv_stride = 0, attn = 0, mlp = 0, y = 0, logits = 0,
-            tok_out = 0, nan = 0, rope = 0, held = 0, dpos = 0, chain_ctl = 0, chain_part = 0, total = 0;
+            tok_out = 0, nan = 0, rope = 0, held = 0, dpos = 0, total = 0;
     int32_t n_qkv = 1;
     int32_t max_rows = 0, max_batch = 0, max_seq = 0;
     // readiness words (uint32) inside `flags`
@@ -75,7 +75,7 @@ enum class Phase { Idle, Begun, Loaded, Merged, Gathered, Prefilled };
 constexpr int kEventPool = 64;
 
 // Kernel classes timed by the optional per-launch profiler (pb_ctx_set_profiling).
-enum KClass : int { K_MERGE = 0, K_GEMM, K_ATTN, K_NORM, K_ROPE, K_EMBED, K_LOGITS, K_ARGMAX, K_SIGNAL, K_CHAIN, K_NCLASS };
+enum KClass : int { K_MERGE = 0, K_GEMM, K_ATTN, K_NORM, K_ROPE, K_EMBED, K_LOGITS, K_ARGMAX, K_SIGNAL, K_NCLASS };
 struct ProfRec {
     int cls;
     cudaEvent_t a, b;
@@ -170,11 +170,6 @@ struct pb_ctx {
     int32_t n_decoded = 0;       // decode steps since the last prompt trial
     bool prompt_replica = false; // the last prompt trial ran in replica mode (its KV cache covers every layer)
     int32_t gemm_m_total = 0;    // rows that pick the GEMM split-K (whole prompt batch, or one decode step)
-    // layer chain (chain.cu): the post-attention half of a layer as one persistent launch when the whole prompt
-    // is one 128-row tile. Opt-in (PB_CHAIN=1): measured slower than the per-op kernels on B200;
-    // bit-identical results either way
-    bool use_chain = false;
-    uint32_t chain_seq = 0;      // launches so far in this trial: picks the control-word set (rotated)
     // decode graphs (single rank / replica): captured once per batch size with every position read on the device
     const int* dyn_pos = nullptr;  // set while capturing a decode graph: device int holding the step's position
     int32_t* h_pos = nullptr;      // pinned: the host writes the position here before each graph launch

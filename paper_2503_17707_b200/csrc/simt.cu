@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(NT) norm_kernel(const float* __restrict__ h, i
         orow += t * dyn_out;
     }
     const float* x = h + row * (long long)ldh;
-    // rownorm.cuh arithmetic (bit-identical to the layer chain's norm items): thread t = virtual thread t
+    // rownorm.cuh arithmetic: thread t = virtual thread t
     float v[PER];
     float s = 0.f;
 #pragma unroll

@@ -202,35 +202,6 @@ def test_c2_full_size_single_gpu():
     print("C2 rel err", rel)
 
 
-def _with_chain(fn):
-    """Run fn with the layer chain enabled (PB_CHAIN is read when a context is created)."""
-    import os
-    os.environ["PB_CHAIN"] = "1"
-    try:
-        return fn()
-    finally:
-        del os.environ["PB_CHAIN"]
-
-
-@pytest.mark.parametrize("case", ["opt", "llama", "opt_chunked_2rank", "c2"])
-def test_layer_chain_bitwise_equals_per_op(case):
-    """The persistent layer chain (O -> norm 2 -> FC1 -> FC2 as one launch, chain.cu) gives logits bit-identical
-    to the per-op kernels: same split-K ranges and summation order, same epilogues, same norm arithmetic
-    (rownorm.cuh). c2: the full OPT-1.3B bench workload (split-K S = 4 on every projection)."""
-    need_gpu()
-    if case == "c2":
-        w = WORKLOADS["C2"]
-        model, ads, toks, kw = w.model, w.adapters, synth.tokens(1, w.seq, w.model.vocab), {}
-    else:
-        model = TINY_LLAMA if case == "llama" else TINY_OPT
-        ads, toks = (lora(8),), synth.tokens(3, 37, model.vocab)
-        kw = dict(policy="interleave", k=2, chunk_bytes=64 << 10) if "chunked" in case else {}
-    n = 2 if "2rank" in case else 1
-    _, _, (t_chain, l_chain), _ = _with_chain(lambda: run(model, ads, n, toks, **kw))
-    _, _, (t_op, l_op), _ = run(model, ads, n, toks, **kw)
-    assert np.array_equal(l_chain.view(np.uint32), l_op.view(np.uint32)), case
-    assert np.array_equal(t_chain, t_op)
-    check_against_oracle(model, ads, toks, l_chain, t_chain)
 
 
 def test_replay_bitwise_equals_cold_start():

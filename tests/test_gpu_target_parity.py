@@ -55,8 +55,12 @@ def cold_start(tag, n, policy="stage", sliced=0, k=1, chunk_mb=64, alias=0):
     rep = harness.golden_parity(gold, logits, tokens)
     rec = {"workload": tag, "n": n, "policy": policy, "vocab_sliced": sliced, "k": k, "host_alias": alias,
            "layers": w.model.n_layers, "max_rel": rep["max_rel"], "max_rel_exact": rep.get("max_rel_exact"),
+           "rel": rep["rel"][:8], "rel_exact": rep.get("rel_exact", [])[:8],
            "token_ok": rep["token_ok"], "token_exact_match": rep["token_exact_match"][:8],
            "margin": rep["margin"][:8], "tokens": [int(x) for x in tokens[:8]]}
+    if os.environ.get("PB_PARITY_DUMP"):   # GPU logits for offline analysis (never an oracle input)
+        os.makedirs(os.environ["PB_PARITY_DUMP"], exist_ok=True)
+        np.save(os.path.join(os.environ["PB_PARITY_DUMP"], f"gpu_{tag}_n{n}_{policy}_k{k}.npy"), logits)
     if os.environ.get("PB_PARITY_LOG"):
         with open(os.environ["PB_PARITY_LOG"], "a") as f:
             f.write(json.dumps(rec) + "\n")
