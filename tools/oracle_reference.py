@@ -49,6 +49,8 @@ def main():
     ap.add_argument("--host-alias", type=int, default=0)
     ap.add_argument("--modes", default="bf16,exact")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--append", action="store_true",
+                    help="keep the modes already stored in the output file (e.g. run bf16 and exact as separate jobs)")
     args = ap.parse_args()
     w = WORKLOADS[args.workload]
     m = w.model
@@ -60,6 +62,13 @@ def main():
             "seq": w.seq, "modes": [], "seconds": {}, "cores": os.cpu_count(),
             "source": "tools/oracle_reference.py (oracle.first_token_logits; imports oracle/ and synth/ only)"}
     path = args.out or golden_path(w.tag, args.host_alias)
+    if args.append and os.path.exists(path):
+        old = dict(np.load(path))
+        assert np.array_equal(old["tokens"], toks), "stored prompt differs"
+        prev = json.loads(str(old.pop("meta")))
+        out.update({k: v for k, v in old.items() if k not in out})
+        meta["modes"] = list(prev.get("modes", []))
+        meta["seconds"] = dict(prev.get("seconds", {}))
     for mode in args.modes.split(","):
         t0 = time.time()
         lg, tk = oracle.first_token_logits(m, w.adapters, toks, adapter_of_seq=aos, mode=mode,
