@@ -3,15 +3,19 @@
 //   W'[i, j] = RNE_bf16( W[i, j] + s * sum_k B[i, k] * A[k, j] ),  s = alpha / r
 //   (P:L111-114 LoRA definition; "parameters of the LoRA adapter are merged back into the base model")
 //
-// One CTA owns a 128 x 128 tile of W. The elected thread issues three TMA loads on two mbarriers:
-// the tiny operands (B tile [128 x rk], A tile [rk x 128]) and the 32 KB W tile. As soon as the operands
-// land it issues rk/16 tcgen05.mma (M=128, N=128, K=16) into a 128-column TMEM accumulator; the W tile
-// keeps streaming meanwhile. The epilogue (4 warps, one W row per thread = one TMEM lane) reads 32
-// accumulator columns at a time with tcgen05.ld, adds s*acc to W in fp32, rounds to bf16 in place in
-// shared memory (128B-swizzled, conflict-free) and one thread TMA-stores the tile back.
-//
-// HBM-bound: 4 bytes/element (read + write W) against r/2 flop/byte; the tensor core turns the K=r
-// contraction into a handful of instructions so the SMs only stream W.
+// HBM-bound: 4 bytes/element (read + write W) against r/2 flop/byte, so the kernel is built to keep W streaming:
+// a PERSISTENT grid (one CTA per SM, at most one per 128 x 128 tile) walks the W tiles t = blockIdx.x,
+// blockIdx.x + gridDim.x, ... through a ring of shared-memory stages, three warp roles overlapping:
+//   warp 0 lane 0  TMA producer: per tile one stage = W tile (32 KB, two SW128 boxes of 64 columns) + the LoRA
+//                  B tile [128 x rk] (K-major) + A tile [rk x 128] (MN-major); the W load of tile i+stages-1 is in
+//                  flight while tile i is merged.
+//   warp 1 lane 0  MMA issuer: rk/16 tcgen05.mma M128 N128 K16 per tile into one of TWO 128-column TMEM
+//                  accumulators (tile i+1's product is formed while tile i's epilogue drains the other).
+//   warps 2-5      epilogue, one W row per thread (TMEM lane quadrant = warp % 4): tcgen05.ld 32 columns at a time,
+//                  W + s*acc in fp32 rounded to bf16 in place in the stage (swizzle-aware, conflict-free), then one
+//                  thread TMA-stores the tile; a stage is handed back to the producer only once the store has
+//                  finished READING it (cp.async.bulk.wait_group.read), so stores drain under the next tiles.
+// The arithmetic per element is one fp32 FMA of the fp32 TMEM sum and one RNE rounding (DESIGN.md §3 G2).
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -26,6 +30,9 @@ namespace {
 
 constexpr int kTile = 128;
 constexpr int kWBytes = kTile * kTile * 2;  // 32 KB, two 64-column SW128 boxes
+constexpr int kMergeThreads = 192;
+constexpr int kMergeSmemBudget = 200 * 1024;
+constexpr int kNumSms = 148;   // B200 (sm_100a): one persistent CTA per SM
 
 template <int RK>
 struct MergeSmem {
@@ -34,120 +41,161 @@ struct MergeSmem {
     static constexpr int offW = 0;
     static constexpr int offB = kWBytes;
     static constexpr int offA = offB + ((kB + 1023) / 1024) * 1024;
-    static constexpr int offBar = offA + kA;
-    static constexpr int kTotal = offBar + 64;
+    static constexpr int kStage = ((offA + kA + 1023) / 1024) * 1024;
+    static constexpr int kStages = std::min(6, (kMergeSmemBudget - 1024) / kStage);
+    static constexpr int offBar = kStages * kStage;
+    static constexpr int kTotal = offBar + 256;
 };
 
 template <int RK>
-__global__ void __launch_bounds__(128) merge_kernel(const __grid_constant__ CUtensorMap mapW,
-                                                    const __grid_constant__ CUtensorMap mapB,
-                                                    const __grid_constant__ CUtensorMap mapA,
-                                                    const __grid_constant__ CUtensorMap mapWout, float scale) {
+__global__ void __launch_bounds__(kMergeThreads, 1) merge_kernel(const __grid_constant__ CUtensorMap mapW,
+                                                                 const __grid_constant__ CUtensorMap mapB,
+                                                                 const __grid_constant__ CUtensorMap mapA,
+                                                                 const __grid_constant__ CUtensorMap mapWout,
+                                                                 int tiles_n, int n_tiles, float scale) {
     using S = MergeSmem<RK>;
+    constexpr int NS = S::kStages;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sW = smem + S::offW;
-    uint8_t* sB = smem + S::offB;
-    uint8_t* sA = smem + S::offA;
-    uint64_t* bar_ops = reinterpret_cast<uint64_t*>(smem + S::offBar);
-    uint64_t* bar_w = bar_ops + 1;
-    uint64_t* bar_mma = bar_ops + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_ops + 3);
+    uint64_t* full_ops = reinterpret_cast<uint64_t*>(smem + S::offBar);   // [NS] B + A landed
+    uint64_t* full_w = full_ops + NS;                                     // [NS] W landed
+    uint64_t* empty = full_w + NS;                                        // [NS] stage free (store read it)
+    uint64_t* acc_full = empty + NS;                                      // [2] product in TMEM
+    uint64_t* acc_empty = acc_full + 2;                                   // [2] epilogue drained TMEM
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int n0 = blockIdx.x * kTile, m0 = blockIdx.y * kTile;
-
     if (tid == 0) {
         tma_prefetch_desc(&mapW);
         tma_prefetch_desc(&mapB);
         tma_prefetch_desc(&mapA);
-        mbar_init(bar_ops, 1);
-        mbar_init(bar_w, 1);
-        mbar_init(bar_mma, 1);
+        tma_prefetch_desc(&mapWout);
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&full_ops[s], 1);
+            mbar_init(&full_w[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], 4);
+        }
         fence_mbar_init();
     }
-    if (warp == 0) tmem_alloc<128>(tmem_slot);
+    if (warp == 0) tmem_alloc<256>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    const int my_tiles = n_tiles > (int)blockIdx.x ? (n_tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 
-    if (tid == 0) {
-        mbar_arrive_expect_tx(bar_ops, S::kB + S::kA);
-        tma_load_2d(sB, &mapB, bar_ops, 0, m0);
-        tma_load_2d(sA, &mapA, bar_ops, n0, 0);
-        tma_load_2d(sA + RK * 128, &mapA, bar_ops, n0 + 64, 0);
-        mbar_arrive_expect_tx(bar_w, kWBytes);
-        tma_load_2d(sW, &mapW, bar_w, n0, m0);
-        tma_load_2d(sW + kWBytes / 2, &mapW, bar_w, n0 + 64, m0);
-
-        mbar_wait(bar_ops, 0);
-        tc_fence_after();
-        constexpr uint64_t kBSw = RK == 16 ? kSw32 : (RK == 32 ? kSw64 : kSw128);
-        constexpr uint32_t idesc = idesc_bf16_f32(128, 128, /*a_mn=*/0, /*b_mn=*/1);
-#pragma unroll
-        for (int kk = 0; kk < RK / 16; ++kk) {
-            // A operand = LoRA B tile, K-major: 8-row core groups RK*2*8 bytes apart; K slice advances 32 B.
-            const uint64_t a_desc = smem_desc(smem_u32(sB) + kk * 32, 16, RK * 2 * 8, kBSw);
-            // B operand = LoRA A tile, MN-major SW128: 64-column boxes RK*128 B apart (LBO),
-            // 8-row K groups 1024 B apart (SBO); K slice of 16 rows advances 2048 B.
-            const uint64_t b_desc = smem_desc(smem_u32(sA) + kk * 2048, RK * 128, 1024, kSw128);
-            umma_bf16(tmem, a_desc, b_desc, idesc, kk > 0 ? 1u : 0u);
-        }
-        umma_commit(bar_mma);
-    }
-    __syncwarp();
-    mbar_wait(bar_mma, 0);
-    mbar_wait(bar_w, 0);
-    tc_fence_after();
-
-    // Epilogue: thread = W row (TMEM lane). Row r of a 64-col SW128 box: 16-B chunk j lives at chunk j ^ (r & 7).
-    const int row = warp * 32 + lane;
-#pragma unroll 1
-    for (int cb = 0; cb < 4; ++cb) {
-        float acc[32];
-        tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + cb * 32, acc);
-        uint8_t* box = sW + (cb >> 1) * (kWBytes / 2) + row * 128;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int j = (cb & 1) * 4 + q;
-            uint4* p = reinterpret_cast<uint4*>(box + ((j ^ (row & 7)) << 4));
-            uint4 w = *p;
-            uint32_t* wv = reinterpret_cast<uint32_t*>(&w);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                __nv_bfloat162 pair = *reinterpret_cast<__nv_bfloat162*>(&wv[e]);
-                float2 f = __bfloat1622float2(pair);
-                wv[e] = bf16x2_bits(fmaf(scale, acc[q * 8 + 2 * e], f.x), fmaf(scale, acc[q * 8 + 2 * e + 1], f.y));
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- TMA producer
+            for (int i = 0; i < my_tiles; ++i) {
+                const int t = blockIdx.x + i * gridDim.x, m0 = (t / tiles_n) * kTile, n0 = (t % tiles_n) * kTile;
+                const int s = i % NS;
+                if (i >= NS) mbar_wait(&empty[s], ((i / NS) - 1) & 1);
+                uint8_t* st = smem + s * S::kStage;
+                mbar_arrive_expect_tx(&full_ops[s], S::kB + S::kA);
+                tma_load_2d(st + S::offB, &mapB, &full_ops[s], 0, m0);
+                tma_load_2d(st + S::offA, &mapA, &full_ops[s], n0, 0);
+                tma_load_2d(st + S::offA + RK * 128, &mapA, &full_ops[s], n0 + 64, 0);
+                mbar_arrive_expect_tx(&full_w[s], kWBytes);
+                tma_load_2d(st + S::offW, &mapW, &full_w[s], n0, m0);
+                tma_load_2d(st + S::offW + kWBytes / 2, &mapW, &full_w[s], n0 + 64, m0);
             }
-            *p = w;
         }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ---------------- MMA issuer
+            constexpr uint64_t kBSw = RK == 16 ? kSw32 : (RK == 32 ? kSw64 : kSw128);
+            constexpr uint32_t idesc = idesc_bf16_f32(128, 128, /*a_mn=*/0, /*b_mn=*/1);
+            for (int i = 0; i < my_tiles; ++i) {
+                const int s = i % NS, b = i & 1;
+                if (i >= 2) mbar_wait(&acc_empty[b], ((i >> 1) - 1) & 1);
+                mbar_wait(&full_ops[s], (i / NS) & 1);
+                tc_fence_after();
+                const uint32_t sB = smem_u32(smem + s * S::kStage + S::offB);
+                const uint32_t sA = smem_u32(smem + s * S::kStage + S::offA);
+#pragma unroll
+                for (int kk = 0; kk < RK / 16; ++kk) {
+                    // A operand = LoRA B tile, K-major: 8-row core groups RK*2*8 bytes apart; K slice advances 32 B.
+                    const uint64_t a_desc = smem_desc(sB + kk * 32, 16, RK * 2 * 8, kBSw);
+                    // B operand = LoRA A tile, MN-major SW128: 64-column boxes RK*128 B apart (LBO),
+                    // 8-row K groups 1024 B apart (SBO); K slice of 16 rows advances 2048 B.
+                    const uint64_t b_desc = smem_desc(sA + kk * 2048, RK * 128, 1024, kSw128);
+                    umma_bf16(tmem + b * 128, a_desc, b_desc, idesc, kk > 0 ? 1u : 0u);
+                }
+                umma_commit(&acc_full[b]);
+            }
+        }
+    } else {
+        // ---------------- epilogue (warps 2-5). Row r of a 64-col SW128 box: 16-B chunk j lives at chunk j ^ (r & 7).
+        const int quad = warp & 3, row = quad * 32 + lane;
+        const bool leader = warp == 2 && lane == 0;
+        for (int i = 0; i < my_tiles; ++i) {
+            const int t = blockIdx.x + i * gridDim.x, m0 = (t / tiles_n) * kTile, n0 = (t % tiles_n) * kTile;
+            const int s = i % NS, b = i & 1;
+            uint8_t* sW = smem + s * S::kStage + S::offW;
+            mbar_wait(&acc_full[b], (i >> 1) & 1);
+            mbar_wait(&full_w[s], (i / NS) & 1);
+            tc_fence_after();
+            const uint32_t t_row = tmem + b * 128 + ((uint32_t)(quad * 32) << 16);
+#pragma unroll 1
+            for (int cb = 0; cb < 4; ++cb) {
+                float acc[32];
+                tmem_ld32(t_row + cb * 32, acc);
+                uint8_t* box = sW + (cb >> 1) * (kWBytes / 2) + row * 128;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int j = (cb & 1) * 4 + q;
+                    uint4* p = reinterpret_cast<uint4*>(box + ((j ^ (row & 7)) << 4));
+                    uint4 w = *p;
+                    uint32_t* wv = reinterpret_cast<uint32_t*>(&w);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        __nv_bfloat162 pair = *reinterpret_cast<__nv_bfloat162*>(&wv[e]);
+                        float2 f = __bfloat1622float2(pair);
+                        wv[e] = bf16x2_bits(fmaf(scale, acc[q * 8 + 2 * e], f.x),
+                                            fmaf(scale, acc[q * 8 + 2 * e + 1], f.y));
+                    }
+                    *p = w;
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[b]);     // TMEM buffer b may take tile i+2's product
+            fence_proxy_async_smem();                       // generic smem writes -> visible to the TMA store
+            named_bar_sync(1, 128);
+            if (leader) {
+                tma_store_2d(&mapWout, sW, n0, m0);         // in place: mapWout == mapW
+                tma_store_2d(&mapWout, sW + kWBytes / 2, n0 + 64, m0);
+                tma_store_commit();
+                if (i >= 1) {
+                    tma_store_wait_read_n<1>();              // tile i-1's store has read its stage
+                    mbar_arrive(&empty[(i - 1) % NS]);
+                }
+            }
+        }
+        if (leader) tma_store_wait_all();
     }
-    fence_proxy_async_smem();
     tc_fence_before();
     __syncthreads();
-    if (tid == 0) {
-        tma_store_2d(&mapWout, sW, n0, m0);                 // in place: mapWout == mapW
-        tma_store_2d(&mapWout, sW + kWBytes / 2, n0 + 64, m0);
-        tma_store_commit();
-        tma_store_wait_all();
-    }
     if (warp == 0) {
         __syncwarp();
         tc_fence_after();
-        tmem_dealloc<128>(tmem);
+        tmem_dealloc<256>(tmem);
     }
 }
 
 template <int RK>
 cudaError_t launch_rk(const MergeMaps& m, int rows, int cols, float scale, cudaStream_t s) {
-    // >= 57 KB of shared memory keeps at most 4 CTAs per SM, so 4 x 128 TMEM columns never over-subscribe.
-    int smem = MergeSmem<RK>::kTotal + 1024;
-    if (smem < 57 * 1024) smem = 57 * 1024;
-    cudaError_t e = cudaFuncSetAttribute(merge_kernel<RK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    constexpr int smem = MergeSmem<RK>::kTotal + 1024;
+    cudaError_t e = smem_attr_once<merge_kernel<RK>>(smem);
     if (e != cudaSuccess) return e;
-    dim3 grid((cols + kTile - 1) / kTile, (rows + kTile - 1) / kTile);
-    merge_kernel<RK><<<grid, 128, smem, s>>>(m.W, m.B, m.A, m.Wout, scale);
+    const int tiles_n = (cols + kTile - 1) / kTile, tiles = tiles_n * ((rows + kTile - 1) / kTile);
+    const int grid = std::min(tiles, kNumSms);
+    merge_kernel<RK><<<grid, kMergeThreads, smem, s>>>(m.W, m.B, m.A, m.Wout, tiles_n, tiles, scale);
     return cudaGetLastError();
 }
 

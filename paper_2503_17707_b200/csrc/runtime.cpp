@@ -25,8 +25,23 @@
 #include <cstdlib>
 #include <unistd.h>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX ranges (visible to Nsight Systems when one is attached)
+
 #include "errors.hpp"
 #include "runtime.hpp"
+
+namespace {
+// NVTX range for the calling host thread (the issuer's trial, a copy group, a layer's launches, a blocking wait).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    NvtxRange(const char* fmt, int a, int b) {
+        char buf[96];
+        snprintf(buf, sizeof buf, fmt, a, b);
+        nvtxRangePushA(buf);
+    }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 using namespace pb;
 
@@ -1081,6 +1096,7 @@ int prof_ops(pb_ctx* c) { return c->profiling ? 2 : 0; }
 // ---- loads and merges of one copy group
 pb_status issue_group(Issuer& I, size_t gi) {
     pb_ctx* c = I.c;
+    NvtxRange nv("pb.load+merge group %d (rank %d)", (int)gi, c->rank);
     if (getenv("PB_DEBUG_ISSUER") && atoi(getenv("PB_DEBUG_ISSUER")) >= 2)
         fprintf(stderr, "[pb r%d] group %zu\n", c->rank, gi);
     const pb_plan* p = c->plan;
@@ -1209,6 +1225,7 @@ long group_merge_ops(Issuer& I, size_t gi) {
 
 pb_status issue_recv(Issuer& I, size_t ri) {
     pb_ctx* c = I.c;
+    NvtxRange nv("pb.gather recv %d (rank %d)", (int)ri, c->rank);
     if (getenv("PB_DEBUG_ISSUER") && atoi(getenv("PB_DEBUG_ISSUER")) >= 2)
         fprintf(stderr, "[pb r%d] recv %zu\n", c->rank, ri);
     const int32_t id = c->plan->recv[c->rank][ri];
@@ -1313,6 +1330,7 @@ static bool issuer_trace() {
 
 pb_status issue_item(Issuer& I, const Item& it, bool late_tokens) {
     pb_ctx* c = I.c;
+    NvtxRange nv("pb.prefill item kind %d layer %d", it.kind, it.l);
     if (issuer_trace()) fprintf(stderr, "[pb r%d] item kind=%d mb=%d j=%d l=%d\n", c->rank, it.kind, it.mb, it.j, it.l);
     const pb_plan* p = c->plan;
     const auto& m = p->model;
@@ -1676,6 +1694,7 @@ pb_status issue_trial(pb_ctx* c, int B, int T, bool replay) {
 // by then it marks itself idle (under run_mu, so a concurrent post either sees the running thread or restarts it).
 void issuer_thread(pb_ctx* c, std::shared_ptr<TrialRun> run) {
     cudaSetDevice(c->device);
+    NvtxRange nv("pb.issuer trial (rank %d, epoch %d)", c->rank, (int)c->epoch);
     for (;;) {
         pb_status st = run_loop(c, *run);
         if (st != PB_OK) {
@@ -2031,6 +2050,7 @@ extern "C" pb_status pb_switch_adapter(pb_ctx* c, int32_t adapter_id) {
 }
 
 extern "C" pb_status pb_prefill_wait(pb_ctx* c, float* logits_out, int32_t* tokens_out) {
+    NvtxRange nv("pb_prefill_wait");
     pb_status st = check_ctx(c, "pb_prefill_wait");
     if (st) return st;
     if (c->phase != Phase::Prefilled) return fail(PB_EPROTOCOL, "pb_prefill_wait: nothing enqueued");

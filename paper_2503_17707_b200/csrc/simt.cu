@@ -38,22 +38,26 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 }
 
 // ------------------------------------------------------------------ LayerNorm / RMSNorm
-// One CTA per row; the row is held in registers (d <= 256 * 40). Two-pass fp32 statistics.
-template <int NT, int PER>
-__global__ void __launch_bounds__(NT) norm_kernel(const float* __restrict__ h, int ldh, __nv_bfloat16* __restrict__ out,
-                                                  int ldo, int d, const __nv_bfloat16* __restrict__ gamma,
-                                                  const __nv_bfloat16* __restrict__ beta, float eps, const int* dyn,
-                                                  int dyn_in, int dyn_out) {
-    static_assert(NT == rownorm::kVT, "one thread per rownorm virtual thread");
+// One CTA of 256 threads per row, the row held in registers: thread t owns the 8-element groups t, t + 256, ...
+// (G groups, d <= 256 * 8 * G), read as two 16-byte fp32 vectors and written as one 16-byte bf16 vector; gamma /
+// beta arrive as 16-byte bf16 vectors requested before the programmatic-dependency wait (they are weights,
+// resident before the kernel is enqueued). Two-pass fp32 statistics (rownorm.cuh): mean, then the mean of squared
+// deviations, each summed per thread in element order, then by a warp butterfly and over the 8 warps.
+template <int G>
+__global__ void __launch_bounds__(256) norm_kernel(const float* __restrict__ h, int ldh, __nv_bfloat16* __restrict__ out,
+                                                   int ldo, int d, const __nv_bfloat16* __restrict__ gamma,
+                                                   const __nv_bfloat16* __restrict__ beta, float eps, const int* dyn,
+                                                   int dyn_in, int dyn_out) {
+    constexpr int NT = 256;
+    static_assert(NT == rownorm::kVT, "8 warps per row (rownorm::combine8)");
     pdl_launch_dependents();   // a PDL-launched GEMM may start its weight prefetch
-    // gamma / beta are weights (resident before this kernel is enqueued): fetched under the previous kernel's tail
-    // (raw bf16 in registers: converting here would stall on the loads before the activation loads are issued)
-    __nv_bfloat16 gm[PER], bt[PER];
+    const int ng = d >> 3;     // 8-element groups in the row
+    uint4 gm[G], bt[G];
 #pragma unroll
-    for (int i = 0; i < PER; ++i) {
-        const int c = threadIdx.x + i * NT;
-        gm[i] = c < d ? gamma[c] : __float2bfloat16_rn(0.f);
-        bt[i] = c < d && beta ? beta[c] : __float2bfloat16_rn(0.f);
+    for (int i = 0; i < G; ++i) {
+        const int g = threadIdx.x + i * NT;
+        gm[i] = g < ng ? __ldg(reinterpret_cast<const uint4*>(gamma) + g) : make_uint4(0, 0, 0, 0);
+        bt[i] = g < ng && beta ? __ldg(reinterpret_cast<const uint4*>(beta) + g) : make_uint4(0, 0, 0, 0);
     }
     pdl_wait();                // PDL-launched: the previous kernel's output is visible from here on
     __shared__ float red[32];
@@ -63,19 +67,29 @@ __global__ void __launch_bounds__(NT) norm_kernel(const float* __restrict__ h, i
         row += t * dyn_in;
         orow += t * dyn_out;
     }
-    const float* x = h + row * (long long)ldh;
-    // rownorm.cuh arithmetic: thread t = virtual thread t
-    float v[PER];
-    float s = 0.f;
+    const float4* x = reinterpret_cast<const float4*>(h + row * (long long)ldh);
+    float v[G][8];
 #pragma unroll
-    for (int i = 0; i < PER; ++i) {
-        const int c = threadIdx.x + i * NT;
-        v[i] = c < d ? x[c] : 0.f;
-        if (c < d) s = rownorm::acc_sum(s, v[i]);
+    for (int i = 0; i < G; ++i) {
+        const int g = threadIdx.x + i * NT;
+        float4 lo = make_float4(0.f, 0.f, 0.f, 0.f), hi = lo;
+        if (g < ng) {
+            lo = x[2 * g];
+            hi = x[2 * g + 1];
+        }
+        v[i][0] = lo.x; v[i][1] = lo.y; v[i][2] = lo.z; v[i][3] = lo.w;
+        v[i][4] = hi.x; v[i][5] = hi.y; v[i][6] = hi.z; v[i][7] = hi.w;
     }
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     float mean = 0.f;
     if (beta) {
+        float s = 0.f;
+#pragma unroll
+        for (int i = 0; i < G; ++i)
+            if (threadIdx.x + i * NT < ng) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) s = rownorm::acc_sum(s, v[i][e]);
+            }
         s = rownorm::warp_sum(s);
         if (l == 0) red[w] = s;
         __syncthreads();
@@ -84,19 +98,31 @@ __global__ void __launch_bounds__(NT) norm_kernel(const float* __restrict__ h, i
     }
     float q = 0.f;
 #pragma unroll
-    for (int i = 0; i < PER; ++i) {
-        const int c = threadIdx.x + i * NT;
-        if (c < d) q = rownorm::acc_sq(q, v[i], mean);
-    }
+    for (int i = 0; i < G; ++i)
+        if (threadIdx.x + i * NT < ng) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) q = rownorm::acc_sq(q, v[i][e], mean);
+        }
     q = rownorm::warp_sum(q);
     if (l == 0) red[w] = q;
     __syncthreads();
     const float rstd = rownorm::rstd_of(rownorm::combine8(red, l), d, eps);
-    __nv_bfloat16* o = out + orow * (long long)ldo;
+    uint4* o = reinterpret_cast<uint4*>(out + orow * (long long)ldo);
 #pragma unroll
-    for (int i = 0; i < PER; ++i) {
-        const int c = threadIdx.x + i * NT;
-        if (c < d) o[c] = rownorm::out_f(v[i], mean, rstd, __bfloat162float(gm[i]), __bfloat162float(bt[i]), beta != nullptr);
+    for (int i = 0; i < G; ++i) {
+        const int g = threadIdx.x + i * NT;
+        if (g >= ng) continue;
+        const __nv_bfloat16* gp = reinterpret_cast<const __nv_bfloat16*>(&gm[i]);
+        const __nv_bfloat16* bp = reinterpret_cast<const __nv_bfloat16*>(&bt[i]);
+        uint4 r;
+        uint16_t* rp = reinterpret_cast<uint16_t*>(&r);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const __nv_bfloat16 y = rownorm::out_f(v[i][e], mean, rstd, __bfloat162float(gp[e]),
+                                                   __bfloat162float(bp[e]), beta != nullptr);
+            rp[e] = *reinterpret_cast<const uint16_t*>(&y);
+        }
+        o[g] = r;
     }
 }
 
@@ -431,7 +457,8 @@ cudaError_t launch_set_words(uint32_t* base, const int32_t* idx, int n, uint32_t
 
 cudaError_t warm_simt_kernels() {
     cudaFuncAttributes a;
-    const void* fns[] = {(const void*)norm_kernel<256, 8>, (const void*)norm_kernel<256, 40>, (const void*)embed_kernel,
+    const void* fns[] = {(const void*)norm_kernel<1>, (const void*)norm_kernel<2>, (const void*)norm_kernel<3>,
+                         (const void*)norm_kernel<4>, (const void*)norm_kernel<5>, (const void*)embed_kernel,
                          (const void*)rope_table_kernel, (const void*)rope_kernel, (const void*)attention_kernel<32>,
                          (const void*)attention_kernel<64>, (const void*)attention_kernel<128>,
                          (const void*)logits_kernel, (const void*)argmax_kernel, (const void*)signal_kernel,
@@ -447,12 +474,23 @@ cudaError_t launch_norm(const float* h, int ldh, __nv_bfloat16* out, int ldo, in
                         const __nv_bfloat16* gamma, const __nv_bfloat16* beta, float eps, cudaStream_t s, bool pdl,
                         const int* dyn, int dyn_in, int dyn_out) {
     if (rows <= 0) return cudaSuccess;
-    if (d <= 256 * 8)
-        return launch_pdl(norm_kernel<256, 8>, rows, 256, 0, s, pdl, h, ldh, out, ldo, d, gamma, beta, eps, dyn, dyn_in,
+    // 16-byte vectors: d % 8 == 0 and 16-byte aligned rows / gamma / beta (every path buffer is)
+    if (d % 8 || ldh % 4 || ldo % 8 || (reinterpret_cast<uintptr_t>(h) & 15) || (reinterpret_cast<uintptr_t>(out) & 15) ||
+        (reinterpret_cast<uintptr_t>(gamma) & 15) || (reinterpret_cast<uintptr_t>(beta) & 15))
+        return cudaErrorInvalidValue;
+    const int groups = (d / 8 + 255) / 256;
+#define PB_NORM_CASE(G)                                                                                                \
+    case G:                                                                                                            \
+        return launch_pdl(norm_kernel<G>, rows, 256, 0, s, pdl, h, ldh, out, ldo, d, gamma, beta, eps, dyn, dyn_in,   \
                           dyn_out);
-    if (d <= 256 * 40)
-        return launch_pdl(norm_kernel<256, 40>, rows, 256, 0, s, pdl, h, ldh, out, ldo, d, gamma, beta, eps, dyn, dyn_in,
-                          dyn_out);
+    switch (groups) {
+        PB_NORM_CASE(1)
+        PB_NORM_CASE(2)
+        PB_NORM_CASE(3)
+        PB_NORM_CASE(4)
+        PB_NORM_CASE(5)
+    }
+#undef PB_NORM_CASE
     return cudaErrorInvalidValue;
 }
 

@@ -58,6 +58,14 @@ if __name__ == "__main__":
           us, gbs, tf = bench(M, K, N, epi, 0)
           print(f"{name:14s} M{M} K{K} N{N}: graph {us:6.1f}us {gbs:5.0f}GB/s ev {LAST_EV_US:6.1f}us", flush=True)
       sys.exit(0)
+  if os.environ.get("GEMM_BENCH_SMALLM"):   # is the activation (X) operand's L2 traffic what limits M = 128?
+      for name, M0, K, N, epi in shapes[:4]:
+          res = []
+          for M in (16, 32, 64, 128):
+              us, gbs, tf = bench(M, K, N, epi, 0)
+              res.append(f"M{M}: {us:6.1f}us {gbs:5.0f}GB/s")
+          print(f"{name:6s} K{K} N{N} auto split: " + " | ".join(res), flush=True)
+      sys.exit(0)
   for name, M, K, N, epi in shapes:
       if only_big and M <= 128: continue
       res = []
