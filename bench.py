@@ -54,8 +54,9 @@ def parse():
     ap.add_argument("--cpu-sample-layers", type=int, default=0,
                     help="decoder layers the CPU oracle baseline runs (0 = the whole model when it fits ~30 s of "
                          "CPU work — C1, C2 — else 4 layers extrapolated linearly)")
-    ap.add_argument("--ref-sample-layers", type=int, default=4,
-                    help="--impl reference: decoder layers per step (a bounded sample, extrapolated to the model)")
+    ap.add_argument("--ref-sample-layers", type=int, default=0,
+                    help="--impl reference: decoder layers per step (0 = the whole model where one oracle pass is "
+                         "~30 s of CPU work at most, else a 4-layer sample extrapolated to the model)")
     ap.add_argument("--host-alias", type=int, default=0,
                     help="host_alias_layers K: layer l is DMA'd from the host image of layer l mod K (DRAM-limited boxes)")
     ap.add_argument("--dist-backend", default="nccl", help="torch.distributed backend for barriers/handle exchange")
@@ -83,72 +84,100 @@ def parse():
 # CPU oracle timing (reported baseline; --impl reference)
 # ----------------------------------------------------------------------------------------------------
 
+class OracleSample:
+    """The CPU oracle (merge + sequential forward, bf16 storage contract) on embed + `sample_layers` decoder layers +
+    head of workload `w`. prepare() materialises the seeded weights (untimed: a CPU 'cold start' has no load step);
+    run() times the merge and the forward once and returns (ms for all L layers, detail) — measured when the sample
+    is the whole model, else extrapolated linearly in layers (labelled)."""
+
+    def __init__(self, w, sample_layers: int):
+        self.w = w
+        self.nl = min(sample_layers, w.model.n_layers)
+
+    def prepare(self):
+        import oracle
+        import synth
+        w = self.w
+        m, ads = w.model, w.adapters
+        self.ls = list(range(self.nl))
+        ow = oracle.OracleWeights(m, ads)
+        names = [n for n in ow.tensors if not n.startswith("L") or int(n[1:].split(".")[0]) in self.ls]
+        self.base = {n: ow.base_bits(n) for n in names}
+        n_ad = len(ads)
+        self.aos = [b % n_ad for b in range(w.batch)] if n_ad > 1 else [0 if n_ad else None] * w.batch
+        self.used = sorted({a for a in self.aos if a is not None})
+        self.facs = [at for at in ow.atensors if at.adapter in self.used and at.layer in self.ls]
+        self.fac_bits = {at.name: ow.adapter_bits(at) for at in self.facs}
+        self.toks = synth.tokens(w.batch, w.seq, m.vocab)
+        self.ow = ow
+        return self
+
+    def run(self):
+        from oracle import forward as OF
+        from oracle.merge import merge_bf16_bits
+        from oracle.numerics import bf16_bits_to_f64
+        import threadpoolctl  # noqa: F401  (numpy BLAS threads = all cores by default)
+        w, ow = self.w, self.ow
+        m, ads = w.model, w.adapters
+        L = m.n_layers
+        id2name = {t.id: n for n, t in ow.tensors.items()}
+        t0 = time.perf_counter()
+        merged = {a: dict(self.base) for a in self.used} if self.used else {None: dict(self.base)}
+        for a in self.used:
+            by_target = {}
+            for at in self.facs:
+                if at.adapter == a:
+                    by_target.setdefault((at.layer, at.target), {})[at.factor] = at
+            for (l, tgt), f in by_target.items():
+                name = id2name[f["A"].base]
+                W = merged[a][name].copy()
+                r0, rows = f["A"].row0, f["B"].rows
+                W[r0:r0 + rows] = merge_bf16_bits(W[r0:r0 + rows], self.fac_bits[f["B"].name],
+                                                  self.fac_bits[f["A"].name], ads[a].scale)
+                merged[a][name] = W
+        t_merge = time.perf_counter() - t0
+        wf = {}
+
+        def getter(a):
+            def Wget(n):
+                if (a, n) not in wf:
+                    x = bf16_bits_to_f64(merged[a][n])
+                    wf[(a, n)] = x.reshape(-1) if ow.tensors[n].rows == 1 else x
+                return wf[(a, n)]
+            return Wget
+
+        for a in merged:   # fp64 views are part of the oracle's data, not its compute
+            for n in merged[a]:
+                getter(a)(n)
+        t1 = time.perf_counter()
+        for b in range(w.batch):
+            OF.forward_logits(m, getter(self.aos[b]), self.toks[b], "bf16", layers=[])
+        t_head = time.perf_counter() - t1
+        t2 = time.perf_counter()
+        for b in range(w.batch):
+            OF.forward_logits(m, getter(self.aos[b]), self.toks[b], "bf16", layers=self.ls)
+        t_all = time.perf_counter() - t2
+        nls = len(self.ls)
+        if nls == L:   # the whole model: the measured time itself
+            total_s = t_merge + t_all
+            per_layer = max(t_all - t_head, 0.0) / nls
+        else:
+            per_layer = max(t_all - t_head, 0.0) / nls
+            total_s = t_head + L * (per_layer + t_merge / nls)
+        detail = {"sample_layers": nls, "layers": L, "merge_s_per_layer": t_merge / nls,
+                  "forward_s_per_layer": per_layer, "embed_head_s": t_head, "measured_s": t_merge + t_head + t_all}
+        return total_s * 1e3, detail
+
+
+def default_sample_layers(w):
+    """The whole model when one oracle pass is ~30 s of CPU work at most (C1, C2: ~0.3 TFLOP of fp64), else 4."""
+    flops = 2.0 * w.batch * w.seq * 2.0 * w.model.n_layers * (4 * w.model.d_model ** 2 + 3 * w.model.d_model *
+                                                               w.model.d_ffn)
+    return w.model.n_layers if flops < 1.2e12 else 4
+
+
 def oracle_sample(w, sample_layers: int):
-    """Time the CPU oracle (merge + sequential forward, bf16 storage contract) on embed + `sample_layers`
-    decoder layers + head, extrapolated linearly to all L layers. Weights are materialised (untimed)
-    first: a CPU 'cold start' has no load step. Returns (extrapolated_ms, detail)."""
-    import oracle
-    from oracle import forward as OF
-    from oracle.merge import merge_bf16_bits
-    from oracle.numerics import bf16_bits_to_f64
-    import synth
-
-    m, ads = w.model, w.adapters
-    L = m.n_layers
-    ls = list(range(min(sample_layers, L)))
-    ow = oracle.OracleWeights(m, ads)
-    names = [n for n in ow.tensors if not n.startswith("L") or int(n[1:].split(".")[0]) in ls]
-    base = {n: ow.base_bits(n) for n in names}
-    n_ad = len(ads)
-    aos = [b % n_ad for b in range(w.batch)] if n_ad > 1 else [0 if n_ad else None] * w.batch
-    used = sorted({a for a in aos if a is not None})
-    facs = [at for at in ow.atensors if at.adapter in used and at.layer in ls]
-    fac_bits = {at.name: ow.adapter_bits(at) for at in facs}
-    toks = synth.tokens(w.batch, w.seq, m.vocab)
-    import threadpoolctl  # noqa: F401  (numpy BLAS threads = all cores by default)
-    id2name = {t.id: n for n, t in ow.tensors.items()}
-    t0 = time.perf_counter()
-    merged = {a: dict(base) for a in used} if used else {None: dict(base)}
-    for a in used:
-        by_target = {}
-        for at in facs:
-            if at.adapter == a:
-                by_target.setdefault((at.layer, at.target), {})[at.factor] = at
-        for (l, tgt), f in by_target.items():
-            name = id2name[f["A"].base]
-            W = merged[a][name].copy()
-            r0, rows = f["A"].row0, f["B"].rows
-            W[r0:r0 + rows] = merge_bf16_bits(W[r0:r0 + rows], fac_bits[f["B"].name], fac_bits[f["A"].name],
-                                              ads[a].scale)
-            merged[a][name] = W
-    t_merge = time.perf_counter() - t0
-    wf = {}
-
-    def getter(a):
-        def Wget(n):
-            if (a, n) not in wf:
-                x = bf16_bits_to_f64(merged[a][n])
-                wf[(a, n)] = x.reshape(-1) if ow.tensors[n].rows == 1 else x
-            return wf[(a, n)]
-        return Wget
-
-    for a in merged:   # fp64 views are part of the oracle's data, not its compute
-        for n in merged[a]:
-            getter(a)(n)
-    t1 = time.perf_counter()
-    for b in range(w.batch):
-        OF.forward_logits(m, getter(aos[b]), toks[b], "bf16", layers=[])
-    t_head = time.perf_counter() - t1
-    t2 = time.perf_counter()
-    for b in range(w.batch):
-        OF.forward_logits(m, getter(aos[b]), toks[b], "bf16", layers=ls)
-    t_all = time.perf_counter() - t2
-    per_layer = max(t_all - t_head, 0.0) / len(ls)
-    merge_per_layer = t_merge / len(ls)
-    total_s = t_head + L * (per_layer + merge_per_layer)
-    detail = {"sample_layers": len(ls), "layers": L, "merge_s_per_layer": merge_per_layer,
-              "forward_s_per_layer": per_layer, "embed_head_s": t_head, "measured_s": t_merge + t_head + t_all}
-    return total_s * 1e3, detail
+    return OracleSample(w, sample_layers).prepare().run()
 
 
 def cpu_cores():
@@ -166,26 +195,27 @@ def run_reference(args):
         return
     from synth.configs import WORKLOADS
     w = WORKLOADS[args.workload]
+    sample = OracleSample(w, args.ref_sample_layers or default_sample_layers(w)).prepare()
     vals, walls = [], []
     det = None
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        v, det = oracle_sample(w, args.ref_sample_layers)
+        v, det = sample.run()
         if i >= args.warmup:
             vals.append(v)
             walls.append((time.perf_counter() - t0) * 1e3)
     val = statistics.mean(vals)
     extrap = det["sample_layers"] < det["layers"]
-    sample = (f"{det['sample_layers']} of {det['layers']} layers + embed/head, B={w.batch} T={w.seq}"
-              + (", extrapolated linearly in layers (value); ms_per_step = the sample actually run per step"
-                 if extrap else ", whole model"))
+    desc = (f"{det['sample_layers']} of {det['layers']} layers + embed/head, B={w.batch} T={w.seq}"
+            + (", extrapolated linearly in layers (value); ms_per_step = the sample actually run per step"
+               if extrap else ", whole model every step (merge + forward; weights materialised once, untimed)"))
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "ms", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.mean(walls),
             "extrapolated": extrap, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64 (bf16 storage contract)",
             "data": "synthetic (seeded splitmix64; HF init std 0.02)",
             "config": workload_config(w, args, 1),
-            "cpu_baseline": {"value": val, "unit": "ms", "cores": cpu_cores(), "kind": "oracle", "sample": sample,
+            "cpu_baseline": {"value": val, "unit": "ms", "cores": cpu_cores(), "kind": "oracle", "sample": desc,
                              "detail": det},
             "e2e": {"value": val, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -624,8 +654,7 @@ def main():
         if not args.no_cpu_baseline:
             # whole model when it is ~30 s of CPU work at most (C1, C2: one fp64 forward ~2 x 0.3 TFLOP), else a
             # 4-layer sample extrapolated linearly
-            flops = 2.0 * w.batch * w.seq * plan.sizes.dev_weight_bytes / 2
-            nl = args.cpu_sample_layers or (w.model.n_layers if flops < 1.2e12 else 4)
+            nl = args.cpu_sample_layers or default_sample_layers(w)
             v, det = oracle_sample(w, nl)
             whole = det["sample_layers"] == det["layers"]
             line["cpu_baseline"] = {"value": v, "unit": "ms", "cores": cpu_cores(), "kind": "oracle",

@@ -88,10 +88,20 @@ def golden_parity(gold, logits, tokens, gate: float = 1e-2) -> dict:
         margin = float(srt[-1] - srt[-2])
         ot = int(np.argmax(ol[b]))
         tk = int(tokens[b])
-        ok = tk == ot if margin > 2 * err else bool(ol[b][tk] >= srt[-1] - 2 * err)
-        out["token_ok"].append(bool(ok))
+        tok_ok = tk == ot if margin > 2 * err else bool(ol[b][tk] >= srt[-1] - 2 * err)
+        out["token_ok"].append(bool(tok_ok))
         out["token_exact_match"].append(tk == ot)
         out["margin"].append(margin)
+    # sequences whose full logit rows are not stored (C2p keeps 16 of 64): the G10 token rule with the largest
+    # absolute error seen on the stored rows, against the stored oracle argmax / margin
+    if "argmax_bf16" in gold and gold["argmax_bf16"].shape[0] > ol.shape[0]:
+        err_all = max(float(np.abs(np.asarray(logits[b], dtype=np.float64) - ol[b]).max()) for b in range(ol.shape[0]))
+        for b in range(ol.shape[0], gold["argmax_bf16"].shape[0]):
+            ot, margin, tk = int(gold["argmax_bf16"][b]), float(gold["margin_bf16"][b]), int(tokens[b])
+            tok_ok = tk == ot if margin > 2 * err_all else True   # near tie: any token within the bound is accepted
+            out["token_ok"].append(bool(tok_ok))
+            out["token_exact_match"].append(tk == ot)
+            out["margin"].append(margin)
     out["max_rel"] = max(out["rel"])
     if "rel_exact" in out:
         out["max_rel_exact"] = max(out["rel_exact"])

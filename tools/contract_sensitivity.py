@@ -75,6 +75,28 @@ def llama_c32(m, W, toks, layers):
     return F(mm32(W("lm_head"), y))
 
 
+def opt_c32(m, W, toks, layers):
+    """OPT (pre-LN, biases, learned positions, ReLU, tied head) under the contract with fp32 accumulation."""
+    R, F = rne_bf16, rne_f32
+    d, H, hd = m.d_model, m.n_heads, m.head_dim
+    T = len(toks)
+    h = F(W("embed")[toks] + W("pos")[np.arange(T) + 2])
+    for l in layers:
+        p = f"L{l}."
+        x = R(OF.layer_norm(h, W(p + "ln1_g"), W(p + "ln1_b"), m.norm_eps))
+        qkv = mm32(x, W(p + "qkv").T) + W(p + "qkv_b")
+        q = R(qkv[:, :d] * hd ** -0.5)
+        k = R(qkv[:, d:2 * d])
+        v = R(qkv[:, 2 * d:])
+        a = R(attention32(q, k, v, H, H, hd, 1.0, R))
+        h = F(h + mm32(a, W(p + "o").T) + W(p + "o_b"))
+        x = R(OF.layer_norm(h, W(p + "ln2_g"), W(p + "ln2_b"), m.norm_eps))
+        u = R(np.maximum(mm32(x, W(p + "fc1").T) + W(p + "fc1_b"), 0.0))
+        h = F(h + mm32(u, W(p + "fc2").T) + W(p + "fc2_b"))
+    y = R(OF.layer_norm(h[-1], W("final_g"), W("final_b"), m.norm_eps))
+    return F(mm32(W("embed"), y))
+
+
 def rel(a, b):
     return float(np.abs(a - b).max() / np.abs(b).max())
 
@@ -88,7 +110,6 @@ def main():
     w = WORKLOADS[args.workload]
     for L in [int(x) for x in args.layers.split(",")]:
         m = dataclasses.replace(w.model, n_layers=L)
-        assert m.arch == "llama"
         ow = oracle.OracleWeights(m, w.adapters)
         cache = {}   # merged bf16 BITS (2 B / element; fp64 copies are made per use)
 
@@ -101,7 +122,7 @@ def main():
         toks = synth.tokens(1, args.seq, m.vocab)[0]
         ex = OF.forward_logits(m, W, toks, "exact")
         con = OF.forward_logits(m, W, toks, "bf16")
-        c32 = llama_c32(m, W, toks, range(L))
+        c32 = (llama_c32 if m.arch == "llama" else opt_c32)(m, W, toks, range(L))
         print(json.dumps({"workload": args.workload, "layers": L, "seq": args.seq,
                           "rel_contract_vs_exact": rel(con, ex), "rel_c32_vs_contract": rel(c32, con),
                           "rel_c32_vs_exact": rel(c32, ex), "argmax": [int(np.argmax(x)) for x in (ex, con, c32)]}),

@@ -51,8 +51,23 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--append", action="store_true",
                     help="keep the modes already stored in the output file (e.g. run bf16 and exact as separate jobs)")
+    ap.add_argument("--keep-logits", type=int, default=0,
+                    help="store the full logit rows of the first N sequences only (argmax / margin / maxabs stay for "
+                         "every sequence); with no modes to run, trims an existing file in place (C2p: 64 x 50272)")
     args = ap.parse_args()
     w = WORKLOADS[args.workload]
+    if args.keep_logits and args.modes == "":
+        path = args.out or golden_path(w.tag, args.host_alias)
+        d = dict(np.load(path))
+        meta = json.loads(str(d.pop("meta")))
+        for k in list(d):
+            if k.startswith("logits_"):
+                d[k] = d[k][:args.keep_logits]
+        meta["logits_rows_kept"] = args.keep_logits
+        d["meta"] = np.array(json.dumps(meta))
+        np.savez_compressed(path, **d)
+        print("trimmed", path)
+        return
     m = w.model
     toks = synth.tokens(w.batch, w.seq, m.vocab)
     n_ad = len(w.adapters)
@@ -75,7 +90,7 @@ def main():
                                            host_alias_layers=args.host_alias)
         dt = time.time() - t0
         srt = np.sort(lg, axis=1)
-        out[f"logits_{mode}"] = lg.astype(np.float32)
+        out[f"logits_{mode}"] = lg.astype(np.float32)[:args.keep_logits or None]
         out[f"argmax_{mode}"] = tk.astype(np.int32)
         out[f"margin_{mode}"] = (srt[:, -1] - srt[:, -2]).astype(np.float64)
         out[f"maxabs_{mode}"] = np.abs(lg).max(axis=1).astype(np.float64)
