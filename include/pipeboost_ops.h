@@ -38,15 +38,6 @@ PB_API pb_status pb_op_gemm_split(const void* X, int32_t x_rows, int32_t m_begin
                                   float scale, int32_t scale_cols, void* out, int32_t ldo, int32_t split_k,
                                   void* stream);
 
-/* The skinny-M split-K kernel with an explicit shape (tests and sweeps; the path picks it by itself when the whole
- * prompt batch is one 128-row tile): split_k in {1, 2, 4, 8, 16} CTAs of a cluster each reduce 1/split_k of K, and
- * each CTA computes tiles_per_cta in {1, 2, 4} consecutive 128-column tiles (SiLU*up: 64 outputs per tile) from
- * one load of every activation box. m_end - m_begin <= 128 rows per 128-row tile of the grid. */
-PB_API pb_status pb_op_gemm_skinny(const void* X, int32_t x_rows, int32_t m_begin, int32_t m_end, int32_t K,
-                                   const void* W, int32_t n_rows, int32_t N, int32_t epi, const void* bias, int32_t relu,
-                                   float scale, int32_t scale_cols, void* out, int32_t ldo, int32_t split_k,
-                                   int32_t tiles_per_cta, void* stream);
-
 /* Llama QKV projection with the rotary embedding fused into the epilogue (DESIGN.md §3 storage contract:
  * q/k = RNE_bf16(rope(X Wqkv^T)), one rounding): epi 0 without bias / scale, then columns [0, rope_cols) (q and k
  * heads of hd = 64 or 128, head-aligned) rotated HF rotate_half style at position (row - row0) / B with

@@ -137,8 +137,6 @@ _SIGS = {
                    C.c_int32, C.c_float, C.c_int32, _P, C.c_int32, _P],
     "pb_op_gemm_split": [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int32, C.c_int32, C.c_int32, _P,
                          C.c_int32, C.c_float, C.c_int32, _P, C.c_int32, C.c_int32, _P],
-    "pb_op_gemm_skinny": [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int32, C.c_int32, C.c_int32, _P,
-                          C.c_int32, C.c_float, C.c_int32, _P, C.c_int32, C.c_int32, C.c_int32, _P],
     "pb_op_gemm_rope": [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int32, _P, C.c_int32, C.c_int32,
                         C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_float, _P, C.c_int32, _P],
     "pb_op_norm": [_P, C.c_int32, C.c_int32, _P, _P, C.c_float, _P, _P],
@@ -423,12 +421,6 @@ def pb_op_gemm_split(X, x_rows, m_begin, m_end, K, W, n_rows, N, epi, bias, relu
                      split_k, stream=0):
     check(lib().pb_op_gemm_split(X, x_rows, m_begin, m_end, K, W, n_rows, N, epi, bias, relu, scale, scale_cols, out,
                                  ldo, split_k, stream))
-
-
-def pb_op_gemm_skinny(X, x_rows, m_begin, m_end, K, W, n_rows, N, epi, bias, relu, scale, scale_cols, out, ldo,
-                      split_k, tiles_per_cta, stream=0):
-    check(lib().pb_op_gemm_skinny(X, x_rows, m_begin, m_end, K, W, n_rows, N, epi, bias, relu, scale, scale_cols, out,
-                                  ldo, split_k, tiles_per_cta, stream))
 
 
 def pb_op_gemm_rope(X, x_rows, m_begin, m_end, K, W, N, out, ldo, rope_cols, hd, row0, B, T, theta, table, split_k,

@@ -328,339 +328,14 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
     }
 }
 
-// ------------------------------------------------------------------------------------------------------------
-// Skinny-M split-K kernel (the whole prompt batch is one 128-row tile: C2's M = 128). At this M every projection
-// is a weight stream (M flop/byte), and what the SMs ingest besides the weights is the activation tile X (L2) and
-// the split-K partials (DSMEM): per weight byte 128/(NT*128) bytes of X and 2*S*M/K bytes of fp32 partials. The
-// plain kernel above (one 128- or 64-column tile per CTA) ingests 1-2 bytes of X per weight byte, and on B200 the
-// L2 -> SM fabric (~6.3 KB/clk chip-wide) then caps the weight stream well below HBM bandwidth. Here a CTA owns
-// NT consecutive 128-column tiles (NT accumulators, NT*128 TMEM columns) and one 1/S slice of K, loops k-outer /
-// tile-inner, so each X box (16 KB) is loaded ONCE and feeds NT weight tiles:
-//   warp 0 lane 0 : TMA producer — X boxes through a 3-deep ring, W tiles through a 9-deep ring (the first W
-//                   tiles requested before the programmatic-dependency wait: weights never depend on the previous
-//                   kernel)
-//   warp 1 lane 0 : MMA issuer   — 4 x tcgen05.mma M128 N128 K16 per (k block, tile) into accumulator j
-//   warps 0-3     : epilogue per tile j: TMEM -> fp32 partial in shared memory (two buffers, alternating), one
-//                   cluster barrier, rows [s*128/S, (s+1)*128/S) reduced over the S partials through DSMEM in the
-//                   FIXED order 0..S-1, fused epilogue (bias / q-scale / ReLU / SiLU*up / RoPE / fp32 residual).
-// (S, NT) depend on (N, K, epi, M_total) only (gemm_skinny_shape), so prompt chunks give bit-identical results.
-constexpr int SK_XS = 3, SK_WS = 9;                       // X ring, W ring depth (16 KB each)
-constexpr int SK_RING = (SK_XS + SK_WS) * kStageA;        // 192 KB; also holds the two 64 KB partial buffers
-constexpr int SK_SMEM = SK_RING + 256 + 1024;
-static_assert(2 * BM * BN * 4 <= SK_RING, "two fp32 partial tiles must fit in the ring");
-
-template <int NT> __host__ __device__ constexpr uint32_t sk_tmem_cols() { return NT == 1 ? 128 : NT == 2 ? 256 : 512; }
-
-template <int EPI, int S, int NT>
-__global__ void __launch_bounds__(128, 1) gemm_skinny_kernel(const __grid_constant__ CUtensorMap mapX,
-                                                             const __grid_constant__ CUtensorMap mapW, const GemmArgs a) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* xring = smem;
-    uint8_t* wring = smem + SK_XS * kStageA;
-    uint64_t* xfull = reinterpret_cast<uint64_t*>(smem + SK_RING);
-    uint64_t* xempty = xfull + SK_XS;
-    uint64_t* wfull = xempty + SK_XS;
-    uint64_t* wempty = wfull + SK_WS;
-    uint64_t* done = wempty + SK_WS;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
-    constexpr uint32_t kCols = sk_tmem_cols<NT>();
-    constexpr int per = EPI == EPI_SILU_MUL ? BN / 2 : BN;   // output columns per tile
-
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int split = S > 1 ? (int)cluster_rank() : 0;
-    const int m_shift = a.m_dyn ? *a.m_dyn * a.m_dyn_mul : 0;
-    const int m0 = a.M_begin + m_shift + blockIdx.y * BM;
-    const int m_end = a.M_end + m_shift;
-    const int n_base = blockIdx.x * NT * per;
-    const int nk = (a.K + BK - 1) / BK;
-    const int kb0 = (int)((long)nk * split / S), kb1 = (int)((long)nk * (split + 1) / S);
-    const int my_k = kb1 - kb0;
-    const int nw = my_k * NT;                                 // W tiles this CTA streams
-
-    pdl_launch_dependents();
-    if (tid == 0) {
-        tma_prefetch_desc(&mapX);
-        tma_prefetch_desc(&mapW);
-        for (int i = 0; i < SK_XS; ++i) {
-            mbar_init(&xfull[i], 1);
-            mbar_init(&xempty[i], 1);
-        }
-        for (int i = 0; i < SK_WS; ++i) {
-            mbar_init(&wfull[i], 1);
-            mbar_init(&wempty[i], 1);
-        }
-        mbar_init(done, 1);
-        fence_mbar_init();
-    }
-    if (warp == 0) tmem_alloc<kCols>(tmem_slot);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-
-    auto load_w = [&](int w) {   // W tile w = (k block w / NT, tile w % NT) into ring slot w % SK_WS
-        const int i = w / NT, j = w % NT, s = w % SK_WS, kc = (kb0 + i) * BK;
-        const int n0 = n_base + j * per;
-        uint8_t* dst = wring + s * kStageA;
-        mbar_arrive_expect_tx(&wfull[s], kStageB);
-        if (EPI == EPI_SILU_MUL) {
-            tma_load_2d(dst, &mapW, &wfull[s], kc, n0);
-            tma_load_2d(dst + kStageB / 2, &mapW, &wfull[s], kc, a.up_row0 + n0);
-        } else {
-            tma_load_2d(dst, &mapW, &wfull[s], kc, n0);
-        }
-    };
-    if (warp == 0 && lane == 0) {
-        // ---------------- TMA producer
-        const int pre = nw < SK_WS ? nw : SK_WS;
-        for (int w = 0; w < pre; ++w) load_w(w);
-        pdl_wait();
-        for (int i = 0; i < my_k; ++i) {
-            const int xs = i % SK_XS;
-            if (i >= SK_XS) mbar_wait(&xempty[xs], ((i / SK_XS) - 1) & 1);
-            mbar_arrive_expect_tx(&xfull[xs], kStageA);
-            tma_load_2d(xring + xs * kStageA, &mapX, &xfull[xs], (kb0 + i) * BK, m0);
-            for (int j = 0; j < NT; ++j) {
-                const int w = i * NT + j;
-                if (w < pre) continue;
-                mbar_wait(&wempty[w % SK_WS], ((w / SK_WS) - 1) & 1);
-                load_w(w);
-            }
-        }
-    } else if (warp == 1 && lane == 0) {
-        // ---------------- MMA issuer
-        constexpr uint32_t idesc = idesc_bf16_f32(BM, BN, 0, 0);
-        for (int i = 0; i < my_k; ++i) {
-            const int xs = i % SK_XS;
-            mbar_wait(&xfull[xs], (i / SK_XS) & 1);
-            const uint32_t a_base = smem_u32(xring + xs * kStageA);
-            for (int j = 0; j < NT; ++j) {
-                const int w = i * NT + j, ws = w % SK_WS;
-                mbar_wait(&wfull[ws], (w / SK_WS) & 1);
-                tc_fence_after();
-                const uint32_t b_base = smem_u32(wring + ws * kStageA);
-#pragma unroll
-                for (int k = 0; k < BK / 16; ++k) {
-                    const uint64_t ad = smem_desc(a_base + k * 32, 16, 1024, kSw128);
-                    const uint64_t bd = smem_desc(b_base + k * 32, 16, 1024, kSw128);
-                    umma_bf16(tmem + j * BN, ad, bd, idesc, (i | k) != 0 ? 1u : 0u);
-                }
-                umma_commit(&wempty[ws]);
-            }
-            umma_commit(&xempty[xs]);
-        }
-        umma_commit(done);
-    } else {
-        pdl_wait();
-    }
-    __syncwarp();
-    mbar_wait(done, 0);
-    tc_fence_after();
-
-    const int r_lo = BM * split / S, r_hi = BM * (split + 1) / S;
-    for (int j = 0; j < NT; ++j) {
-        const int n_out0 = n_base + j * per;
-        uint8_t* part = smem + (j & 1) * (BM * BN * 4);
-        // ---- this CTA's K-partial of tile j -> shared memory (every MMA and TMA load has completed)
-        {
-            const int row = warp * 32 + lane;
-            const uint32_t t_row = tmem + j * BN + ((uint32_t)(warp * 32) << 16);
-#pragma unroll
-            for (int half = 0; half < 2; ++half) {
-                uint32_t r0[32], r1[32];
-                tmem_ld32_async(t_row + half * 64, r0);
-                tmem_ld32_async(t_row + half * 64 + 32, r1);
-                tmem_wait_ld();
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    *reinterpret_cast<uint4*>(part + part_off<BN>(row, half * 16 + q)) =
-                        make_uint4(r0[4 * q], r0[4 * q + 1], r0[4 * q + 2], r0[4 * q + 3]);
-                    *reinterpret_cast<uint4*>(part + part_off<BN>(row, half * 16 + 8 + q)) =
-                        make_uint4(r1[4 * q], r1[4 * q + 1], r1[4 * q + 2], r1[4 * q + 3]);
-                }
-            }
-        }
-        // every CTA of the cluster has staged tile j (and finished reducing tile j-1, so the other buffer is free)
-        if (S > 1) cluster_sync();
-        else __syncthreads();
-        if (n_out0 >= a.N) continue;
-        const uint32_t base = smem_u32(part);
-        constexpr int chunks = EPI == EPI_SILU_MUL ? 16 : BN / 4;
-        auto sum_chunk = [&](int r, int c) {
-            if constexpr (S == 1) {
-                return *reinterpret_cast<const float4*>(part + part_off<BN>(r, c));
-            } else {
-                float4 p[S];
-#pragma unroll
-                for (int s2 = 0; s2 < S; ++s2) p[s2] = ld_cluster_f4(map_cluster(base + part_off<BN>(r, c), s2));
-                float4 acc = p[0];
-#pragma unroll
-                for (int s2 = 1; s2 < S; ++s2) {
-                    acc.x += p[s2].x;
-                    acc.y += p[s2].y;
-                    acc.z += p[s2].z;
-                    acc.w += p[s2].w;
-                }
-                return acc;
-            }
-        };
-        for (int idx = tid; idx < (r_hi - r_lo) * chunks; idx += 128) {
-            const int r = r_lo + idx / chunks, ch = idx % chunks;
-            const int row = m0 + r;
-            if (row >= m_end) continue;
-            const int n = n_out0 + ch * 4;
-            if (n >= a.N) continue;
-            if (EPI == EPI_SILU_MUL) {
-                const float4 g = sum_chunk(r, ch), u = sum_chunk(r, ch + 16);
-                const float o[4] = {silu(g.x) * u.x, silu(g.y) * u.y, silu(g.z) * u.z, silu(g.w) * u.w};
-                __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(a.out) + (size_t)row * a.ldo + n;
-                if (n + 4 <= a.N) {
-                    uint2 w;
-                    w.x = bf16x2_bits(o[0], o[1]);
-                    w.y = bf16x2_bits(o[2], o[3]);
-                    *reinterpret_cast<uint2*>(out) = w;
-                } else {
-                    for (int c = 0; c < 4 && n + c < a.N; ++c) out[c] = __float2bfloat16_rn(o[c]);
-                }
-                continue;
-            }
-            if (EPI == EPI_BF16 && a.rope && n < a.rope_cols) {
-                const int half = a.rope_hd >> 1, ci = n % a.rope_hd;
-                if (ci >= half) continue;
-                const float4 p1 = sum_chunk(r, ch), p2 = sum_chunk(r, ch + (half >> 2));
-                float x1[4] = {p1.x, p1.y, p1.z, p1.w}, x2[4] = {p2.x, p2.y, p2.z, p2.w};
-                rope_rotate4(a, row, ci, x1, x2);
-                __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(a.out) + (size_t)row * a.ldo + n;
-                uint2 w1, w2;
-                w1.x = bf16x2_bits(x1[0], x1[1]);
-                w1.y = bf16x2_bits(x1[2], x1[3]);
-                w2.x = bf16x2_bits(x2[0], x2[1]);
-                w2.y = bf16x2_bits(x2[2], x2[3]);
-                *reinterpret_cast<uint2*>(out) = w1;
-                *reinterpret_cast<uint2*>(out + half) = w2;
-                continue;
-            }
-            const float4 acc = sum_chunk(r, ch);
-            float v[4] = {acc.x, acc.y, acc.z, acc.w};
-            const int nv = min(4, a.N - n);
-            if (a.bias) {
-#pragma unroll
-                for (int c = 0; c < 4; ++c) v[c] += c < nv ? __bfloat162float(a.bias[n + c]) : 0.f;
-            }
-            if (EPI == EPI_BF16) {
-                if (n < a.scale_cols) {
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) v[c] *= (n + c < a.scale_cols) ? a.scale : 1.0f;
-                }
-                if (a.relu) {
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) v[c] = fmaxf(v[c], 0.0f);
-                }
-                __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(a.out) + (size_t)row * a.ldo + n;
-                if (nv == 4) {
-                    uint2 w;
-                    w.x = bf16x2_bits(v[0], v[1]);
-                    w.y = bf16x2_bits(v[2], v[3]);
-                    *reinterpret_cast<uint2*>(out) = w;
-                } else {
-                    for (int c = 0; c < nv; ++c) out[c] = __float2bfloat16_rn(v[c]);
-                }
-            } else {  // EPI_RESID: h += acc + bias (fp32)
-                float* h = reinterpret_cast<float*>(a.out) + (size_t)row * a.ldo + n;
-                if (nv == 4) {
-                    float4 x = *reinterpret_cast<float4*>(h);
-                    x.x += v[0];
-                    x.y += v[1];
-                    x.z += v[2];
-                    x.w += v[3];
-                    *reinterpret_cast<float4*>(h) = x;
-                } else {
-                    for (int c = 0; c < nv; ++c) h[c] += v[c];
-                }
-            }
-        }
-    }
-    if (S > 1) cluster_sync();   // keep the partials alive until every peer has read them
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 0) {
-        __syncwarp();
-        tc_fence_after();
-        tmem_dealloc<kCols>(tmem);
-    }
-}
-
-template <int EPI, int S, int NT>
-cudaError_t launch_skinny_t(const CUtensorMap& mapX, const CUtensorMap& mapW, const GemmArgs& a, cudaStream_t s) {
-    constexpr int per = EPI == EPI_SILU_MUL ? BN / 2 : BN;
-    const dim3 grid((a.N + NT * per - 1) / (NT * per), (a.M_end - a.M_begin + BM - 1) / BM, S);
-    static std::atomic<unsigned long long> done{0};
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
-    const unsigned long long bit = 1ull << (dev & 63);
-    if (!(done.load(std::memory_order_acquire) & bit)) {
-        e = cudaFuncSetAttribute(gemm_skinny_kernel<EPI, S, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, SK_SMEM);
-        if (e == cudaSuccess && S > 8)
-            e = cudaFuncSetAttribute(gemm_skinny_kernel<EPI, S, NT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
-        done.fetch_or(bit, std::memory_order_release);
-    }
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = grid;
-    cfg.blockDim = dim3(128);
-    cfg.dynamicSmemBytes = SK_SMEM;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[2];
-    int na = 0;
-    if (S > 1) {
-        attr[na].id = cudaLaunchAttributeClusterDimension;
-        attr[na].val.clusterDim.x = 1;
-        attr[na].val.clusterDim.y = 1;
-        attr[na].val.clusterDim.z = S;
-        ++na;
-    }
-    if (a.pdl) {
-        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[na].val.programmaticStreamSerializationAllowed = 1;
-        ++na;
-    }
-    cfg.attrs = attr;
-    cfg.numAttrs = na;
-    return cudaLaunchKernelEx(&cfg, gemm_skinny_kernel<EPI, S, NT>, mapX, mapW, a);
-}
-
-template <int EPI, int NT>
-cudaError_t launch_skinny_nt(const CUtensorMap& mapX, const CUtensorMap& mapW, const GemmArgs& a, int S, cudaStream_t s) {
-    switch (S) {
-        case 1: return launch_skinny_t<EPI, 1, NT>(mapX, mapW, a, s);
-        case 2: return launch_skinny_t<EPI, 2, NT>(mapX, mapW, a, s);
-        case 4: return launch_skinny_t<EPI, 4, NT>(mapX, mapW, a, s);
-        case 8: return launch_skinny_t<EPI, 8, NT>(mapX, mapW, a, s);
-        case 16: return launch_skinny_t<EPI, 16, NT>(mapX, mapW, a, s);
-    }
-    return cudaErrorInvalidValue;
-}
-
-template <int EPI>
-cudaError_t launch_skinny(const CUtensorMap& mapX, const CUtensorMap& mapW, const GemmArgs& a, int S, int NT,
-                          cudaStream_t s) {
-    switch (NT) {
-        case 1: return launch_skinny_nt<EPI, 1>(mapX, mapW, a, S, s);
-        case 2: return launch_skinny_nt<EPI, 2>(mapX, mapW, a, S, s);
-        case 4: return launch_skinny_nt<EPI, 4>(mapX, mapW, a, S, s);
-    }
-    return cudaErrorInvalidValue;
-}
-
 template <int EPI, int S, int TBN = BN>
 cudaError_t launch_es(const CUtensorMap& mapX, const CUtensorMap& mapW, const GemmArgs& a, cudaStream_t s) {
     const int per = EPI == EPI_SILU_MUL ? BN / 2 : TBN;
     const dim3 grid((a.N + per - 1) / per, (a.M_end - a.M_begin + BM - 1) / BM, S);
     // Deep ring when the grid fits one CTA per SM; otherwise 3 stages (96 KB) so two CTAs share an SM.
     const int ctas = grid.x * grid.y * grid.z;
-    const int stages = ctas <= 148 ? max_stages<TBN>() : 3;
+    static const int forced = getenv("PB_GEMM_STAGES") ? atoi(getenv("PB_GEMM_STAGES")) : 0;   // experiments
+    const int stages = forced >= 2 && forced <= max_stages<TBN>() ? forced : ctas <= 148 ? max_stages<TBN>() : 3;
     const int smem = smem_bytes_t<TBN>(stages);
     cudaError_t e = smem_attr_once<gemm_kernel<EPI, S, TBN>>(smem_bytes_t<TBN>(max_stages<TBN>()));
     if (e != cudaSuccess) return e;
@@ -721,7 +396,7 @@ cudaError_t launch_epi(const CUtensorMap& mapX, const CUtensorMap& mapW, const G
 // and re-read from L2 by the other M tiles while the activations (M x K) stay L2-resident.
 // ------------------------------------------------------------------------------------------------------------
 constexpr int BIG_BN = 256, BIG_STAGES = 4;
-constexpr int kBigA = BM * BK * 2, kBigB = BIG_BN * BK * 2, kBigStage = kBigA + kBigB;   // 16 + 32 KB
+constexpr int kBigA = BM * BK * 2, kBigB = BIG_BN * BK * 2;   // 16 KB activation box, 32 KB weight boxes per stage
 // The same kernel with TBN = 192-column tiles (bias / residual epilogues) where 256-column tiles fill the last wave
 // badly (gemm_big_tile_n): W arrives as a 128-row box + a 64-row box (mapW64), 5 stages of 40 KB.
 template <int TBN> __host__ __device__ constexpr int big_stages() { return TBN == 256 ? BIG_STAGES : TBN == 192 ? 5 : 6; }
@@ -1183,50 +858,6 @@ int gemm_tile_n(int N, int K, int epi, int M_total) {
     return n_tiles * gemm_split_k(N, K, epi, M_total) <= 74 ? 64 : BN;
 }
 
-// (S, NT) of the skinny kernel: minimise max(weight bytes / (CTAs x 45 GB/s per streaming SM), on-chip bytes /
-// 11 TB/s) where on-chip bytes = weights x (1 + X bytes per weight byte (1/NT) + partial bytes per weight byte
-// (2 S M / K)), with at least 2 K blocks per split and at most one CTA per SM; ties go to the smaller sum of the two
-// terms. PB_SKINNY="S,NT" overrides (measurement sweeps), PB_SKINNY=0 disables the skinny kernel. Depends on
-// (N, K, epi, M_total) only.
-bool gemm_skinny_shape(int N, int K, int epi, int M_total, int* S_out, int* NT_out) {
-    static const char* env = getenv("PB_SKINNY");
-    if (env && env[0] == '0' && env[1] == 0) return false;
-    if (M_total <= kGemvAutoRows || M_total > BM) return false;
-    if (env && env[0]) {
-        int s = 0, nt = 0;
-        if (sscanf(env, "%d,%d", &s, &nt) == 2 && s >= 1 && nt >= 1) {
-            *S_out = s;
-            *NT_out = nt;
-            return true;
-        }
-    }
-    const int per = epi == EPI_SILU_MUL ? BN / 2 : BN;
-    const long n_tiles = (N + per - 1) / per;
-    const int nk = (K + BK - 1) / BK;
-    const double wbytes = (epi == EPI_SILU_MUL ? 2.0 : 1.0) * N * K * 2.0;
-    double best = 1e30, best2 = 1e30;
-    int bs = 0, bn = 0;
-    for (int nt : {1, 2, 4})
-        for (int sp : {1, 2, 4, 8, 16}) {
-            if (nk / sp < 2) continue;
-            const long ctas = (n_tiles + nt - 1) / nt * sp;
-            if (ctas > 148) continue;
-            const double t1 = wbytes / (ctas * 45e9);
-            const double t2 = wbytes * (1.0 + (double)M_total / (nt * BM) + 2.0 * sp * M_total / K) / 11e12;
-            const double t = t1 > t2 ? t1 : t2;
-            if (t < best * 0.98 || (t < best * 1.02 && t1 + t2 < best2)) {
-                best = t;
-                best2 = t1 + t2;
-                bs = sp;
-                bn = nt;
-            }
-        }
-    if (!bs) return false;
-    *S_out = bs;
-    *NT_out = bn;
-    return true;
-}
-
 int gemm_split_k(int N, int K, int epi, int M_total) {
     const int per = epi == EPI_SILU_MUL ? BN / 2 : BN;
     const long n_tiles = (N + per - 1) / per;
@@ -1277,20 +908,6 @@ cudaError_t launch_gemm(const CUtensorMap& mapX, const CUtensorMap& mapW, const 
             case EPI_BF16: return launch_gemv_epi<EPI_BF16>(a, s);
             case EPI_RESID: return launch_gemv_epi<EPI_RESID>(a, s);
             case EPI_SILU_MUL: return launch_gemv_epi<EPI_SILU_MUL>(a, s);
-        }
-    }
-    {
-        int sS = 0, sNT = 0;
-        if (a.skinny_nt > 0) {
-            sS = a.split_k > 0 ? a.split_k : 1;
-            sNT = a.skinny_nt;
-        }
-        if (a.skinny_nt > 0 || (a.split_k <= 0 && gemm_skinny_shape(a.N, a.K, a.epi, a.M_total, &sS, &sNT))) {
-            switch (a.epi) {
-                case EPI_BF16: return launch_skinny<EPI_BF16>(mapX, mapW, a, sS, sNT, s);
-                case EPI_RESID: return launch_skinny<EPI_RESID>(mapX, mapW, a, sS, sNT, s);
-                case EPI_SILU_MUL: return launch_skinny<EPI_SILU_MUL>(mapX, mapW, a, sS, sNT, s);
-            }
         }
     }
     const int S = a.split_k > 0 ? a.split_k : gemm_split_k(a.N, a.K, a.epi, a.M_total);

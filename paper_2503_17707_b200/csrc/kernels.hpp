@@ -100,7 +100,6 @@ struct GemmArgs {
     int ldo;
     int up_row0;                // EPI_SILU_MUL: first row of `up` in W (= N_out)
     int split_k;                // 0 = automatic (gemm_split_k), else the cluster split-K factor (1, 2, 4, 8)
-    int skinny_nt;              // > 0: force the skinny kernel with NT tiles per CTA and S = split_k (tests, sweeps)
     const int* m_dyn;           // f3 decode graphs: rows shift by (*m_dyn) * m_dyn_mul (device), or null
     int m_dyn_mul;
     int M_total;                // rows of the whole prompt batch (picks split_k; chunk-invariant), 0 = M_end-M_begin
@@ -122,9 +121,7 @@ struct GemmArgs {
 int gemm_tile_n(int N, int K, int epi, int M_total);
 constexpr int kGemvAutoRows = 2;   // rows up to which launch_gemm picks the GEMV
 int gemm_split_k(int N, int K, int epi, int M_total);
-// Skinny kernel shape (single 128-row tile, 2 < M_total <= 128): split-K factor S and tiles per CTA NT; false = use
-// the plain split-K kernel.
-bool gemm_skinny_shape(int N, int K, int epi, int M_total, int* S, int* NT);
+
 // Maps: X box {64, 128} SW128 over [max_rows x K]; W box {64, 128} (EPI_SILU_MUL: {64, 64}) SW128 over [rows x K].
 cudaError_t launch_gemm(const CUtensorMap& mapX, const CUtensorMap& mapW, const GemmArgs& a, cudaStream_t s);
 

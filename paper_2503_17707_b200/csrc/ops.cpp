@@ -36,7 +36,7 @@ extern "C" pb_status pb_op_gemm(const void* X, int32_t x_rows, int32_t m_begin, 
 
 static pb_status gemm_op(const void* X, int32_t x_rows, int32_t m_begin, int32_t m_end, int32_t K, const void* W,
                          int32_t n_rows, int32_t N, int32_t epi, const void* bias, int32_t relu, float scale,
-                         int32_t scale_cols, void* out, int32_t ldo, int32_t split_k, int32_t skinny_nt, void* stream);
+                         int32_t scale_cols, void* out, int32_t ldo, int32_t split_k, void* stream);
 
 extern "C" pb_status pb_op_gemm_split(const void* X, int32_t x_rows, int32_t m_begin, int32_t m_end, int32_t K,
                                       const void* W, int32_t n_rows, int32_t N, int32_t epi, const void* bias,
@@ -44,25 +44,13 @@ extern "C" pb_status pb_op_gemm_split(const void* X, int32_t x_rows, int32_t m_b
                                       int32_t split_k, void* stream) {
     if (split_k < 0 || split_k > 8 || (split_k & (split_k - 1)) || (split_k > 0 && split_k > (K + 63) / 64))
         return fail(PB_EINVAL, "pb_op_gemm_split: split_k %d out of range", split_k);
-    return gemm_op(X, x_rows, m_begin, m_end, K, W, n_rows, N, epi, bias, relu, scale, scale_cols, out, ldo, split_k, 0,
-                   stream);
-}
-
-extern "C" pb_status pb_op_gemm_skinny(const void* X, int32_t x_rows, int32_t m_begin, int32_t m_end, int32_t K,
-                                       const void* W, int32_t n_rows, int32_t N, int32_t epi, const void* bias,
-                                       int32_t relu, float scale, int32_t scale_cols, void* out, int32_t ldo,
-                                       int32_t split_k, int32_t tiles_per_cta, void* stream) {
-    if (split_k < 1 || split_k > 16 || (split_k & (split_k - 1)) || split_k > (K + 63) / 64)
-        return fail(PB_EINVAL, "pb_op_gemm_skinny: split_k %d out of range", split_k);
-    if (tiles_per_cta != 1 && tiles_per_cta != 2 && tiles_per_cta != 4)
-        return fail(PB_EINVAL, "pb_op_gemm_skinny: tiles_per_cta %d not 1, 2 or 4", tiles_per_cta);
     return gemm_op(X, x_rows, m_begin, m_end, K, W, n_rows, N, epi, bias, relu, scale, scale_cols, out, ldo, split_k,
-                   tiles_per_cta, stream);
+                   stream);
 }
 
 static pb_status gemm_op(const void* X, int32_t x_rows, int32_t m_begin, int32_t m_end, int32_t K, const void* W,
                          int32_t n_rows, int32_t N, int32_t epi, const void* bias, int32_t relu, float scale,
-                         int32_t scale_cols, void* out, int32_t ldo, int32_t split_k, int32_t skinny_nt, void* stream) {
+                         int32_t scale_cols, void* out, int32_t ldo, int32_t split_k, void* stream) {
     if (!X || !W || !out) return fail(PB_EINVAL, "pb_op_gemm: null pointer");
     if (K % 8 || K <= 0 || epi < 0 || epi > 2 || m_begin < 0 || m_end > x_rows)
         return fail(PB_EINVAL, "pb_op_gemm: bad shape (K=%d epi=%d)", K, epi);
@@ -85,7 +73,6 @@ static pb_status gemm_op(const void* X, int32_t x_rows, int32_t m_begin, int32_t
     a.ldo = ldo;
     a.up_row0 = N;
     a.split_k = split_k;
-    a.skinny_nt = skinny_nt;
     a.M_total = m_end - m_begin;
     CUtensorMap mw64;
     if (epi != EPI_SILU_MUL) {

@@ -133,68 +133,6 @@ def test_gemm_relu_and_resid_and_silu(M, K, N, f):
     assert np.all(err <= 2 * bf16_ulp(r2) + 1e-5), err.max()
 
 
-@pytest.mark.parametrize("S,NT", [(1, 1), (2, 2), (4, 1), (4, 4), (8, 2), (16, 1), (16, 4)])
-@pytest.mark.parametrize("M,K,N,m0,m1,f", [(128, 2048, 1000, 0, 128, 520), (77, 1024, 640, 5, 77, 200),
-                                           (128, 8192, 384, 0, 128, 136)])
-def test_gemm_skinny_all_shapes(S, NT, M, K, N, m0, m1, f):
-    """Skinny split-K kernel (one 128-row tile, NT tiles per CTA from one load of each activation box, S-way
-    cluster split-K reduced in a fixed order) for every (S, NT) the path may pick, all three epilogues, ragged N
-    (a CTA's last tiles partly or wholly past N) and a row window."""
-    need_gpu()
-    if K // 64 < S:
-        pytest.skip("fewer K blocks than splits")
-    rng = np.random.default_rng(S * 100 + NT + M + N)
-    X, W, bias = _gemm_case(rng, M, K, N)
-    Xd, Wd, bd = dev_bf16(X), dev_bf16(W), dev_bf16(bias)
-    ref = bf16_bits_to_f64(X) @ bf16_bits_to_f64(W).T + bf16_bits_to_f64(bias)
-    sc_cols = N // 3
-    out = torch.zeros((M, N), dtype=torch.bfloat16, device="cuda")
-    B.pb_op_gemm_skinny(ptr(Xd), M, m0, m1, K, ptr(Wd), N, N, 0, ptr(bd), 1, 0.125, sc_cols, ptr(out), N, S, NT,
-                        stream())
-    torch.cuda.synchronize()
-    r = ref.copy()
-    r[:, :sc_cols] *= 0.125
-    r = np.maximum(r, 0)[m0:m1]
-    got = bf16_bits_to_f64(host_bits(out))
-    assert np.all(got[:m0] == 0) and np.all(got[m1:] == 0)
-    assert np.all(np.abs(got[m0:m1] - r) <= bf16_ulp(r) + 1e-6 * np.abs(r).max())
-    h0 = rng.standard_normal((M, N)).astype(np.float32)
-    h = dev_f32(h0)
-    B.pb_op_gemm_skinny(ptr(Xd), M, m0, m1, K, ptr(Wd), N, N, 1, ptr(bd), 0, 1.0, 0, ptr(h), N, S, NT, stream())
-    torch.cuda.synchronize()
-    want = h0.astype(np.float64)
-    want[m0:m1] += ref[m0:m1]
-    assert np.allclose(h.cpu().numpy(), want, rtol=1e-5, atol=1e-5)
-    Wgu = rbits(rng, (2 * f, K), 0.05)
-    out2 = torch.zeros((M, f), dtype=torch.bfloat16, device="cuda")
-    Wgud = dev_bf16(Wgu)
-    B.pb_op_gemm_skinny(ptr(Xd), M, m0, m1, K, ptr(Wgud), 2 * f, f, 2, 0, 0, 1.0, 0, ptr(out2), f, S, NT, stream())
-    torch.cuda.synchronize()
-    gu = bf16_bits_to_f64(X) @ bf16_bits_to_f64(Wgu).T
-    g, u = gu[m0:m1, :f], gu[m0:m1, f:]
-    r2 = g / (1 + np.exp(-g)) * u
-    err = np.abs(bf16_bits_to_f64(host_bits(out2))[m0:m1] - r2)
-    assert np.all(err <= 2 * bf16_ulp(r2) + 1e-5), err.max()
-
-
-def test_gemm_skinny_equals_across_row_windows():
-    """Prompt chunks: the same output rows computed as one launch or as two row windows are bit-identical (the
-    shape depends on M_total only; here both calls force the same S, NT)."""
-    need_gpu()
-    rng = np.random.default_rng(3)
-    X, W, bias = _gemm_case(rng, 128, 2048, 2048)
-    Xd, Wd, bd = dev_bf16(X), dev_bf16(W), dev_bf16(bias)
-    a = torch.zeros((128, 2048), dtype=torch.bfloat16, device="cuda")
-    b = torch.zeros((128, 2048), dtype=torch.bfloat16, device="cuda")
-    B.pb_op_gemm_skinny(ptr(Xd), 128, 0, 128, 2048, ptr(Wd), 2048, 2048, 0, ptr(bd), 0, 1.0, 0, ptr(a), 2048, 8, 2,
-                        stream())
-    for lo, hi in ((0, 64), (64, 128)):
-        B.pb_op_gemm_skinny(ptr(Xd), 128, lo, hi, 2048, ptr(Wd), 2048, 2048, 0, ptr(bd), 0, 1.0, 0, ptr(b), 2048, 8, 2,
-                            stream())
-    torch.cuda.synchronize()
-    assert np.array_equal(host_bits(a), host_bits(b))
-
-
 @pytest.mark.parametrize("rms", [False, True])
 @pytest.mark.parametrize("d", [256, 2048, 4096, 5120, 8192, 9216])
 def test_norm(rms, d):
