@@ -23,6 +23,13 @@ extern "C" {
 PB_API pb_status pb_op_merge(void* W, int64_t ldw, int32_t rows, int32_t cols, const void* B, const void* A,
                              int32_t rank, float scale, void* stream);
 
+/* n <= 8 merges of the same rank in ONE persistent launch (their 128x128 tiles walked as one list): job i is
+ * W[i] [rows[i] x cols[i]] (pitch ldw[i]) <- RNE_bf16(W[i] + scale[i] * B[i] * A[i]) with the layouts of pb_op_merge.
+ * The path merges the adapted chunks of one DMA group this way. */
+PB_API pb_status pb_op_merge_batch(int32_t n, void* const* W, const int64_t* ldw, const int32_t* rows,
+                                   const int32_t* cols, const void* const* B, const void* const* A, int32_t rank,
+                                   const float* scale, void* stream);
+
 /* Prefill GEMM: X [*, K] bf16 (rows [m_begin, m_end) used; the map spans x_rows rows), W [n_rows x K] bf16.
  * epi 0: out bf16 [*, ldo] = (X W^T + bias) * (col < scale_cols ? scale : 1), ReLU if relu;
  * epi 1: out fp32 [*, ldo] += X W^T + bias;
@@ -37,6 +44,12 @@ PB_API pb_status pb_op_gemm_split(const void* X, int32_t x_rows, int32_t m_begin
                                   const void* W, int32_t n_rows, int32_t N, int32_t epi, const void* bias, int32_t relu,
                                   float scale, int32_t scale_cols, void* out, int32_t ldo, int32_t split_k,
                                   void* stream);
+
+/* Debug / measurement only: every following pb_op_gemm* launch of the split-K kernel writes 8 %globaltimer stamps
+ * per CTA to trace (device, uint64 [grid CTAs][8]: entry, prologue done, activation wait passed, last load issued,
+ * first stage landed, last MMA done, partial staged + cluster barrier, epilogue done), or none (trace = NULL); pdl != 0
+ * launches them with programmatic dependent launch, as the prefill path does. Process-wide; not thread-safe. */
+PB_API pb_status pb_op_debug_gemm(void* trace, int32_t pdl);
 
 /* Llama QKV projection with the rotary embedding fused into the epilogue (DESIGN.md §3 storage contract:
  * q/k = RNE_bf16(rope(X Wqkv^T)), one rounding): epi 0 without bias / scale, then columns [0, rope_cols) (q and k

@@ -137,6 +137,8 @@ _SIGS = {
                    C.c_int32, C.c_float, C.c_int32, _P, C.c_int32, _P],
     "pb_op_gemm_split": [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int32, C.c_int32, C.c_int32, _P,
                          C.c_int32, C.c_float, C.c_int32, _P, C.c_int32, C.c_int32, _P],
+    "pb_op_debug_gemm": [_P, C.c_int32],
+    "pb_op_merge_batch": [C.c_int32, _P, _P, _P, _P, _P, _P, C.c_int32, _P, _P],
     "pb_op_gemm_rope": [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int32, _P, C.c_int32, C.c_int32,
                         C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_float, _P, C.c_int32, _P],
     "pb_op_norm": [_P, C.c_int32, C.c_int32, _P, _P, C.c_float, _P, _P],
@@ -421,6 +423,19 @@ def pb_op_gemm_split(X, x_rows, m_begin, m_end, K, W, n_rows, N, epi, bias, relu
                      split_k, stream=0):
     check(lib().pb_op_gemm_split(X, x_rows, m_begin, m_end, K, W, n_rows, N, epi, bias, relu, scale, scale_cols, out,
                                  ldo, split_k, stream))
+
+
+def pb_op_merge_batch(W, ldw, rows, cols, Bs, As, rank, scales, stream=0):
+    """Lists of device pointers / ints / floats, one entry per job (<= 8)."""
+    n = len(W)
+    arr = lambda t, v: (t * n)(*v)  # noqa: E731
+    check(lib().pb_op_merge_batch(n, arr(C.c_void_p, W), arr(C.c_int64, ldw), arr(C.c_int32, rows),
+                                  arr(C.c_int32, cols), arr(C.c_void_p, Bs), arr(C.c_void_p, As), rank,
+                                  arr(C.c_float, scales), stream))
+
+
+def pb_op_debug_gemm(trace, pdl):
+    check(lib().pb_op_debug_gemm(trace, pdl))
 
 
 def pb_op_gemm_rope(X, x_rows, m_begin, m_end, K, W, N, out, ldo, rope_cols, hd, row0, B, T, theta, table, split_k,

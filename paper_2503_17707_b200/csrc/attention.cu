@@ -99,7 +99,11 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
     //   pass A (iterations i < n_kv):  S_j -> row max m and row sum l = sum exp2(s*c - m) (exact rescale per tile)
     //   pass B (iterations i >= n_kv): S_j again -> P = RNE_bf16(exp2(s*c - m) / l) -> O += P V_j
     // The output is then RNE_bf16(O) with no final division.
-    const int NI = 2 * n_kv;
+    // One key tile (T <= 128: C2's prompt, short decode contexts): the row max and sum come from the same S the
+    // probabilities use, so a single pass computes E = exp2(s*c - m) once, l = sum E, P = RNE_bf16(E / l) — the same
+    // values, in the same order, as the two passes would (no second QK^T, no second exponential).
+    const bool single = n_kv == 1;
+    const int NI = single ? 1 : 2 * n_kv;
     if (warp == 4) {
         if (lane == 0) {
             constexpr int kBox = kAtom;   // bytes of one 64-col box
@@ -107,7 +111,7 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
 #pragma unroll
                 for (int a = 0; a < HD / 64; ++a) tma_load_3d(dst + a * kBox, &map, bar, col + a * 64, b, t);
             };
-            auto kv_of = [&](int i) { return i < n_kv ? i : i - n_kv; };
+            auto kv_of = [&](int i) { return single ? 0 : (i < n_kv ? i : i - n_kv); };
             mbar_arrive_expect_tx(q_full, SM::kQ);
             load_rows(sQ, q_full, h * HD, q0);
             for (int i = 0; i < 2 && i < NI; ++i) {   // K of iterations 0 and 1
@@ -147,8 +151,8 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
                     mbar_wait(s_free, ph);
                     issue_S(i + 1);
                 }
-                if (i < n_kv) continue;
-                const int j = i - n_kv;
+                if (i < n_kv && !single) continue;
+                const int j = single ? 0 : i - n_kv;
                 // ---- V_{j+1} into the buffer PV_{j-1} has finished reading
                 if (j >= 1 && j + 1 < n_kv) {
                     mbar_wait(o_full, (j - 1) & 1);
@@ -181,8 +185,8 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
         float m = -CUDART_INF_F, l = 0.f, inv_l = 0.f;
         for (int i = 0; i < NI; ++i) {
             const uint32_t ph = i & 1;
-            const bool pass_b = i >= n_kv;
-            const int j = pass_b ? i - n_kv : i;
+            const bool pass_b = single || i >= n_kv;
+            const int j = single ? 0 : (pass_b ? i - n_kv : i);
             mbar_wait(s_full, ph);
             tc_fence_after();
             uint32_t sr[4][32];
@@ -216,6 +220,39 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
                     for (int e = 0; e < 32; ++e) rs += fast_exp2(fmaf(__uint_as_float(sr[c][e]), scale_log2, -m_new));
                 l = (m == -CUDART_INF_F ? 0.f : l * fast_exp2(m - m_new)) + rs;
                 m = m_new;
+                continue;
+            }
+            if (single) {   // ---- one key tile: max, then E = exp2(s*c - m) kept in sr, l = sum E (pass A's order)
+                float mx = -CUDART_INF_F;
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(sr[c][e]));
+                m = mx * scale_log2;
+                float rs = 0.f;
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        const float ev = fast_exp2(fmaf(__uint_as_float(sr[c][e]), scale_log2, -m));
+                        sr[c][e] = __float_as_uint(ev);
+                        rs += ev;
+                    }
+                l = rs;
+                inv_l = 1.f / l;
+#pragma unroll
+                for (int cb = 0; cb < 4; ++cb) {
+                    uint32_t w[16];
+#pragma unroll
+                    for (int e = 0; e < 16; ++e)
+                        w[e] = bf16x2_bits(__uint_as_float(sr[cb][2 * e]) * inv_l,
+                                           __uint_as_float(sr[cb][2 * e + 1]) * inv_l);
+                    tmem_st16(tP + lane_off + cb * 16, w);
+                }
+                tmem_wait_st();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(p_full);
                 continue;
             }
             // ---- pass B: P = RNE_bf16(exp2(s*c - m) / l) straight into TMEM (the A operand of the PV MMA)

@@ -98,6 +98,18 @@ __device__ __forceinline__ uint32_t part_off(int row, int chunk) {
     return (uint32_t)(row * (TBN * 4) + ((chunk ^ (row & (TBN / 4 - 1))) << 4));
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// Phase stamps of the debug trace (pb_op_debug_gemm): slot k of CTA (x, y, z) in a.trace[cta * 8 + k].
+#define PB_GEMM_STAMP(k)                                                                                              \
+    do {                                                                                                              \
+        if (a.trace)                                                                                                  \
+            a.trace[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 8 + (k)] = gtimer();          \
+    } while (0)
+
 // S = split-K factor = cluster size along z (compile-time so the S remote loads of the reduction are issued
 // back to back, then summed in the fixed order 0..S-1).
 template <int EPI, int S, int TBN = BN>
@@ -125,6 +137,7 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
     const int kb0 = (int)((long)nk * split / S), kb1 = (int)((long)nk * (split + 1) / S);
     const int my_k = kb1 - kb0;                    // >= 1 (host guarantees S <= nk)
 
+    if (tid == 0) PB_GEMM_STAMP(0);
     pdl_launch_dependents();
     if (tid == 0) {
         tma_prefetch_desc(&mapX);
@@ -141,6 +154,7 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    if (tid == 0) PB_GEMM_STAMP(1);
 
     auto load_w = [&](int i) {
         const int s = i % stages, kc = (kb0 + i) * BK;
@@ -161,6 +175,7 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
             load_w(i);
         }
         pdl_wait();
+        PB_GEMM_STAMP(2);
         for (int i = 0; i < pre; ++i) tma_load_2d(ring + i * kStageT, &mapX, &full[i], (kb0 + i) * BK, m0);
         for (int i = pre; i < my_k; ++i) {
             const int s = i % stages;
@@ -169,12 +184,14 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
             tma_load_2d(ring + s * kStageT, &mapX, &full[s], (kb0 + i) * BK, m0);
             load_w(i);
         }
+        PB_GEMM_STAMP(3);
     } else if (warp == 1 && lane == 0) {
         // ---------------- MMA issuer
         constexpr uint32_t idesc = idesc_bf16_f32(BM, TBN, 0, 0);
         for (int i = 0; i < my_k; ++i) {
             const int s = i % stages;
             mbar_wait(&full[s], (i / stages) & 1);
+            if (i == 0) PB_GEMM_STAMP(4);
             tc_fence_after();
             const uint32_t a_base = smem_u32(ring + s * kStageT), b_base = a_base + kStageA;
 #pragma unroll
@@ -192,6 +209,7 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
     __syncwarp();
     mbar_wait(done, 0);
     tc_fence_after();
+    if (tid == 0) PB_GEMM_STAMP(5);
 
     // ---------------- stage the fp32 tile (this CTA's K-partial) in shared memory; all MMAs and TMA loads
     // have completed, so the stage ring is free. Two batches of 64 columns (4 loads in flight, one wait).
@@ -216,6 +234,7 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
     tc_fence_before();
     if (S > 1) cluster_sync();
     else __syncthreads();
+    if (tid == 0) PB_GEMM_STAMP(6);
 
     // ---------------- reduce rows [r_lo, r_hi) over the S partials (fixed order 0..S-1) + fused epilogue
     const int r_lo = BM * split / S, r_hi = BM * (split + 1) / S;
@@ -319,6 +338,7 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
         }
     }
     if (S > 1) cluster_sync();   // keep this CTA's partial alive until every peer has read it
+    if (tid == 0) PB_GEMM_STAMP(7);
     tc_fence_before();
     __syncthreads();
     if (warp == 0) {
@@ -863,8 +883,9 @@ int gemm_split_k(int N, int K, int epi, int M_total) {
     const long n_tiles = (N + per - 1) / per;
     const long m_tiles = M_total > 0 ? (M_total + BM - 1) / BM : 1;
     const int nk = (K + BK - 1) / BK;
+    static const long max_ctas = getenv("PB_GEMM_CTAS") ? atol(getenv("PB_GEMM_CTAS")) : 296;   // experiments
     int S = 1;
-    while (S < 4 && n_tiles * m_tiles * 2 * S <= 296 && nk / (2 * S) >= 4) S *= 2;
+    while (S < 4 && n_tiles * m_tiles * 2 * S <= max_ctas && nk / (2 * S) >= 4) S *= 2;
     return S;
 }
 

@@ -80,6 +80,15 @@ bool make_merge_maps(MergeMaps* m, void* W, int64_t ldw, int rows, int cols, con
 // SM byte copy (16-B vectors; falls back to cudaMemcpyAsync for unaligned spans).
 cudaError_t launch_copy(void* dst, const void* src, int64_t bytes, cudaStream_t s);
 cudaError_t launch_merge(const MergeMaps& maps, int rows, int cols, int rank, float scale, cudaStream_t s);
+// Up to kMaxMergeJobs merges of the same padded rank in ONE persistent launch (the tiles of all jobs are walked as
+// one list): the adapted tensors of a DMA group merge in one kernel instead of one launch each.
+constexpr int kMaxMergeJobs = 8;
+struct MergeJobDesc {
+    const MergeMaps* maps;
+    int rows, cols, rank;
+    float scale;
+};
+cudaError_t launch_merge_batch(const MergeJobDesc* jobs, int n, cudaStream_t s);
 
 // ---------------------------------------------------------------- prefill GEMM (tcgen05)
 // out = X[M x K] * W[N x K]^T with a fused epilogue. X rows [m_begin, m_end) are computed.
@@ -100,6 +109,7 @@ struct GemmArgs {
     int ldo;
     int up_row0;                // EPI_SILU_MUL: first row of `up` in W (= N_out)
     int split_k;                // 0 = automatic (gemm_split_k), else the cluster split-K factor (1, 2, 4, 8)
+    unsigned long long* trace;  // debug (pb_op_debug_gemm): 8 %globaltimer stamps per CTA of the split-K kernel, or null
     const int* m_dyn;           // f3 decode graphs: rows shift by (*m_dyn) * m_dyn_mul (device), or null
     int m_dyn_mul;
     int M_total;                // rows of the whole prompt batch (picks split_k; chunk-invariant), 0 = M_end-M_begin

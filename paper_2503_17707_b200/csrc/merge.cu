@@ -47,12 +47,28 @@ struct MergeSmem {
     static constexpr int kTotal = offBar + 256;
 };
 
+// The jobs of one launch: tensor maps (kernel parameters, as TMA requires) and each job's tile range.
+struct MergeBatch {
+    CUtensorMap W[kMaxMergeJobs], B[kMaxMergeJobs], A[kMaxMergeJobs], Wout[kMaxMergeJobs];
+    int tiles_n[kMaxMergeJobs];    // 128-column tiles per row of tiles
+    int tile_end[kMaxMergeJobs];   // exclusive end of the job's tiles in the launch's tile list
+    float scale[kMaxMergeJobs];
+    int n_jobs;
+};
+
+struct TileRef {
+    int job, m0, n0;
+};
+__device__ __forceinline__ TileRef tile_ref(const MergeBatch& P, int t) {
+    int j = 0;
+    while (j + 1 < P.n_jobs && t >= P.tile_end[j]) ++j;
+    const int lt = t - (j ? P.tile_end[j - 1] : 0);
+    return {j, (lt / P.tiles_n[j]) * kTile, (lt % P.tiles_n[j]) * kTile};
+}
+
 template <int RK>
-__global__ void __launch_bounds__(kMergeThreads, 1) merge_kernel(const __grid_constant__ CUtensorMap mapW,
-                                                                 const __grid_constant__ CUtensorMap mapB,
-                                                                 const __grid_constant__ CUtensorMap mapA,
-                                                                 const __grid_constant__ CUtensorMap mapWout,
-                                                                 int tiles_n, int n_tiles, float scale) {
+__global__ void __launch_bounds__(kMergeThreads, 1) merge_kernel(const __grid_constant__ MergeBatch P) {
+    const int n_tiles = P.tile_end[P.n_jobs - 1];
     using S = MergeSmem<RK>;
     constexpr int NS = S::kStages;
     extern __shared__ uint8_t smem_raw[];
@@ -66,10 +82,12 @@ __global__ void __launch_bounds__(kMergeThreads, 1) merge_kernel(const __grid_co
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
-        tma_prefetch_desc(&mapW);
-        tma_prefetch_desc(&mapB);
-        tma_prefetch_desc(&mapA);
-        tma_prefetch_desc(&mapWout);
+        for (int j = 0; j < P.n_jobs; ++j) {
+            tma_prefetch_desc(&P.W[j]);
+            tma_prefetch_desc(&P.B[j]);
+            tma_prefetch_desc(&P.A[j]);
+            tma_prefetch_desc(&P.Wout[j]);
+        }
         for (int s = 0; s < NS; ++s) {
             mbar_init(&full_ops[s], 1);
             mbar_init(&full_w[s], 1);
@@ -92,17 +110,18 @@ __global__ void __launch_bounds__(kMergeThreads, 1) merge_kernel(const __grid_co
         if (lane == 0) {
             // ---------------- TMA producer
             for (int i = 0; i < my_tiles; ++i) {
-                const int t = blockIdx.x + i * gridDim.x, m0 = (t / tiles_n) * kTile, n0 = (t % tiles_n) * kTile;
+                const TileRef tr = tile_ref(P, blockIdx.x + i * gridDim.x);
+                const int m0 = tr.m0, n0 = tr.n0, j = tr.job;
                 const int s = i % NS;
                 if (i >= NS) mbar_wait(&empty[s], ((i / NS) - 1) & 1);
                 uint8_t* st = smem + s * S::kStage;
                 mbar_arrive_expect_tx(&full_ops[s], S::kB + S::kA);
-                tma_load_2d(st + S::offB, &mapB, &full_ops[s], 0, m0);
-                tma_load_2d(st + S::offA, &mapA, &full_ops[s], n0, 0);
-                tma_load_2d(st + S::offA + RK * 128, &mapA, &full_ops[s], n0 + 64, 0);
+                tma_load_2d(st + S::offB, &P.B[j], &full_ops[s], 0, m0);
+                tma_load_2d(st + S::offA, &P.A[j], &full_ops[s], n0, 0);
+                tma_load_2d(st + S::offA + RK * 128, &P.A[j], &full_ops[s], n0 + 64, 0);
                 mbar_arrive_expect_tx(&full_w[s], kWBytes);
-                tma_load_2d(st + S::offW, &mapW, &full_w[s], n0, m0);
-                tma_load_2d(st + S::offW + kWBytes / 2, &mapW, &full_w[s], n0 + 64, m0);
+                tma_load_2d(st + S::offW, &P.W[j], &full_w[s], n0, m0);
+                tma_load_2d(st + S::offW + kWBytes / 2, &P.W[j], &full_w[s], n0 + 64, m0);
             }
         }
     } else if (warp == 1) {
@@ -134,7 +153,9 @@ __global__ void __launch_bounds__(kMergeThreads, 1) merge_kernel(const __grid_co
         const int quad = warp & 3, row = quad * 32 + lane;
         const bool leader = warp == 2 && lane == 0;
         for (int i = 0; i < my_tiles; ++i) {
-            const int t = blockIdx.x + i * gridDim.x, m0 = (t / tiles_n) * kTile, n0 = (t % tiles_n) * kTile;
+            const TileRef tr = tile_ref(P, blockIdx.x + i * gridDim.x);
+            const int m0 = tr.m0, n0 = tr.n0, j = tr.job;
+            const float scale = P.scale[j];
             const int s = i % NS, b = i & 1;
             uint8_t* sW = smem + s * S::kStage + S::offW;
             mbar_wait(&acc_full[b], (i >> 1) & 1);
@@ -168,8 +189,8 @@ __global__ void __launch_bounds__(kMergeThreads, 1) merge_kernel(const __grid_co
             fence_proxy_async_smem();                       // generic smem writes -> visible to the TMA store
             named_bar_sync(1, 128);
             if (leader) {
-                tma_store_2d(&mapWout, sW, n0, m0);         // in place: mapWout == mapW
-                tma_store_2d(&mapWout, sW + kWBytes / 2, n0 + 64, m0);
+                tma_store_2d(&P.Wout[j], sW, n0, m0);       // in place: Wout == W
+                tma_store_2d(&P.Wout[j], sW + kWBytes / 2, n0 + 64, m0);
                 tma_store_commit();
                 if (i >= 1) {
                     tma_store_wait_read_n<1>();              // tile i-1's store has read its stage
@@ -189,13 +210,27 @@ __global__ void __launch_bounds__(kMergeThreads, 1) merge_kernel(const __grid_co
 }
 
 template <int RK>
-cudaError_t launch_rk(const MergeMaps& m, int rows, int cols, float scale, cudaStream_t s) {
+cudaError_t launch_rk(const MergeJobDesc* jobs, int n, cudaStream_t s) {
     constexpr int smem = MergeSmem<RK>::kTotal + 1024;
     cudaError_t e = smem_attr_once<merge_kernel<RK>>(smem);
     if (e != cudaSuccess) return e;
-    const int tiles_n = (cols + kTile - 1) / kTile, tiles = tiles_n * ((rows + kTile - 1) / kTile);
-    const int grid = std::min(tiles, kNumSms);
-    merge_kernel<RK><<<grid, kMergeThreads, smem, s>>>(m.W, m.B, m.A, m.Wout, tiles_n, tiles, scale);
+    MergeBatch P;
+    int tiles = 0, nj = 0;
+    for (int i = 0; i < n; ++i) {
+        if (jobs[i].rows <= 0 || jobs[i].cols <= 0) continue;
+        P.W[nj] = jobs[i].maps->W;
+        P.B[nj] = jobs[i].maps->B;
+        P.A[nj] = jobs[i].maps->A;
+        P.Wout[nj] = jobs[i].maps->Wout;
+        P.tiles_n[nj] = (jobs[i].cols + kTile - 1) / kTile;
+        tiles += P.tiles_n[nj] * ((jobs[i].rows + kTile - 1) / kTile);
+        P.tile_end[nj] = tiles;
+        P.scale[nj] = jobs[i].scale;
+        ++nj;
+    }
+    if (nj == 0) return cudaSuccess;
+    P.n_jobs = nj;
+    merge_kernel<RK><<<std::min(tiles, kNumSms), kMergeThreads, smem, s>>>(P);
     return cudaGetLastError();
 }
 
@@ -212,13 +247,22 @@ bool make_merge_maps(MergeMaps* m, void* W, int64_t ldw, int rows, int cols, con
            make_map_bf16(&m->A, A, rank, cols, cols, rk, 64, 128, err, errlen);
 }
 
-cudaError_t launch_merge(const MergeMaps& m, int rows, int cols, int rank, float scale, cudaStream_t s) {
-    if (rows <= 0 || cols <= 0) return cudaSuccess;
-    switch (merge_rk(rank)) {
-        case 16: return launch_rk<16>(m, rows, cols, scale, s);
-        case 32: return launch_rk<32>(m, rows, cols, scale, s);
-        default: return launch_rk<64>(m, rows, cols, scale, s);
+cudaError_t launch_merge_batch(const MergeJobDesc* jobs, int n, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    if (n > kMaxMergeJobs) return cudaErrorInvalidValue;
+    const int rk = merge_rk(jobs[0].rank);
+    for (int i = 1; i < n; ++i)
+        if (merge_rk(jobs[i].rank) != rk) return cudaErrorInvalidValue;   // one padded rank per launch
+    switch (rk) {
+        case 16: return launch_rk<16>(jobs, n, s);
+        case 32: return launch_rk<32>(jobs, n, s);
+        default: return launch_rk<64>(jobs, n, s);
     }
+}
+
+cudaError_t launch_merge(const MergeMaps& m, int rows, int cols, int rank, float scale, cudaStream_t s) {
+    const MergeJobDesc j{&m, rows, cols, rank, scale};
+    return launch_merge_batch(&j, 1, s);
 }
 
 // Device-to-device byte copy on the SMs (16-byte vectors, grid-stride): used for the rows of a tensor an

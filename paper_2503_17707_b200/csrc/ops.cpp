@@ -27,11 +27,45 @@ extern "C" pb_status pb_op_merge(void* W, int64_t ldw, int32_t rows, int32_t col
     return cuda_status(launch_merge(m, rows, cols, rank, scale, (cudaStream_t)stream), "merge");
 }
 
+extern "C" pb_status pb_op_merge_batch(int32_t n, void* const* W, const int64_t* ldw, const int32_t* rows,
+                                       const int32_t* cols, const void* const* B, const void* const* A, int32_t rank,
+                                       const float* scale, void* stream) {
+    if (n < 0 || n > kMaxMergeJobs) return fail(PB_EINVAL, "pb_op_merge_batch: n = %d (1..%d)", n, kMaxMergeJobs);
+    if (n == 0) return PB_OK;
+    if (!W || !ldw || !rows || !cols || !B || !A || !scale) return fail(PB_EINVAL, "pb_op_merge_batch: null array");
+    if (rank < 8 || rank > 64 || rank % 8) return fail(PB_EINVAL, "pb_op_merge_batch: rank %d", rank);
+    MergeMaps maps[kMaxMergeJobs];
+    MergeJobDesc jobs[kMaxMergeJobs];
+    char err[512];
+    for (int i = 0; i < n; ++i) {
+        if (!W[i] || !B[i] || !A[i]) return fail(PB_EINVAL, "pb_op_merge_batch: null pointer in job %d", i);
+        if (cols[i] % 8 || ldw[i] % 8 || rows[i] < 0 || cols[i] < 0)
+            return fail(PB_EINVAL, "pb_op_merge_batch: job %d needs cols %% 8 == 0", i);
+        if (!aligned16(W[i]) || !aligned16(B[i]) || !aligned16(A[i]))
+            return fail(PB_EINVAL, "pb_op_merge_batch: job %d bases must be 16-B aligned", i);
+        if (rows[i] && cols[i] && !make_merge_maps(&maps[i], W[i], ldw[i], rows[i], cols[i], B[i], A[i], rank, err,
+                                                   sizeof err))
+            return fail(PB_EINVAL, "%s", err);
+        jobs[i] = MergeJobDesc{&maps[i], rows[i], cols[i], rank, scale[i]};
+    }
+    return cuda_status(launch_merge_batch(jobs, n, (cudaStream_t)stream), "merge batch");
+}
+
 extern "C" pb_status pb_op_gemm(const void* X, int32_t x_rows, int32_t m_begin, int32_t m_end, int32_t K,
                                 const void* W, int32_t n_rows, int32_t N, int32_t epi, const void* bias, int32_t relu,
                                 float scale, int32_t scale_cols, void* out, int32_t ldo, void* stream) {
     return pb_op_gemm_split(X, x_rows, m_begin, m_end, K, W, n_rows, N, epi, bias, relu, scale, scale_cols, out, ldo, 0,
                             stream);
+}
+
+// debug state of pb_op_debug_gemm (process-wide; the op tests and tools/gemm_phases.py set it)
+static unsigned long long* g_gemm_trace = nullptr;
+static int g_gemm_pdl = 0;
+
+extern "C" pb_status pb_op_debug_gemm(void* trace, int32_t pdl) {
+    g_gemm_trace = static_cast<unsigned long long*>(trace);
+    g_gemm_pdl = pdl != 0;
+    return PB_OK;
 }
 
 static pb_status gemm_op(const void* X, int32_t x_rows, int32_t m_begin, int32_t m_end, int32_t K, const void* W,
@@ -73,6 +107,8 @@ static pb_status gemm_op(const void* X, int32_t x_rows, int32_t m_begin, int32_t
     a.ldo = ldo;
     a.up_row0 = N;
     a.split_k = split_k;
+    a.trace = g_gemm_trace;
+    a.pdl = g_gemm_pdl;
     a.M_total = m_end - m_begin;
     CUtensorMap mw64;
     if (epi != EPI_SILU_MUL) {

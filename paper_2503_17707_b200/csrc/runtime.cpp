@@ -429,6 +429,8 @@ extern "C" pb_status pb_ctx_create(const pb_plan* plan, int32_t rank, const void
         mk(&c->ready_recv) || mk(&c->stage_begin) || mk(&c->stage_end) ||
         cudaEventCreateWithFlags(&c->tok_ev, cudaEventDisableTiming))
         return cleanup(fail(PB_ECUDA, "cudaEventCreate failed"));
+    for (auto& e : c->trial_fence)
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming)) return cleanup(fail(PB_ECUDA, "cudaEventCreate failed"));
     if (const char* lt = getenv("PB_LANDED_TIMING")) c->landed_timing = atoi(lt) != 0;
     if (mk(&c->load_end)) return cleanup(fail(PB_ECUDA, "cudaEventCreate failed"));
     for (int32_t id : plan->load[rank]) {
@@ -519,6 +521,7 @@ extern "C" void pb_ctx_free(pb_ctx* c) {
     }
     auto d = [](cudaEvent_t e) { if (e) cudaEventDestroy(e); };
     d(c->t0); d(c->merge_done); d(c->gather_done); d(c->done); d(c->ready_merge); d(c->ready_recv); d(c->tok_ev);
+    for (auto e : c->trial_fence) d(e);
     d(c->load_end); d(c->stage_begin); d(c->stage_end);
     for (auto e : c->merged_ev) d(e);
     for (auto e : c->budget_events) d(e);
@@ -735,13 +738,21 @@ extern "C" pb_status pb_trial_begin(pb_ctx* c, uint32_t epoch) {
     for (int r = 0; r < c->n; ++r)
         if (!c->peers[r].linked) return fail(PB_EPROTOCOL, "peer %d not wired (import/link)", r);
     c->epoch = epoch;
+    c->cold_epoch = epoch;
     c->n_launches = 0;
     c->prof_n = 0;
     c->load_bytes = c->recv_bytes = 0;
     std::fill(c->tl_landed.begin(), c->tl_landed.end(), -1.0);
     std::fill(c->tl_gathered.begin(), c->tl_gathered.end(), -1.0);
-    CU(cudaEventRecord(c->t0, c->h2d[0]));
+    // Every stream of the previous trial drains before this one starts: a trial armed and then left without a
+    // prompt (a refused pb_prefill_enqueue) keeps loading / merging; its in-place merges must not run after this
+    // trial's copies of the same bytes.
     cudaStream_t others[] = {c->h2d[1], c->merge, c->nv, c->comp};
+    for (int i = 0; i < 4; ++i) {
+        CU(cudaEventRecord(c->trial_fence[i], others[i]));
+        CU(cudaStreamWaitEvent(c->h2d[0], c->trial_fence[i], 0));
+    }
+    CU(cudaEventRecord(c->t0, c->h2d[0]));
     for (auto s : others) CU(cudaStreamWaitEvent(s, c->t0, 0));
     // re-plan resume: chunks this rank already holds are ready for the peers that receive them from it
     for (int r = 0; r < c->n && c->n_held_src > 0; ++r)
@@ -1120,12 +1131,18 @@ pb_status issue_group(Issuer& I, size_t gi) {
     for (int r = 0; r < c->n; ++r)
         if (r != c->rank) others.push_back(r);
     long mops = 0;
+    static thread_local std::vector<int32_t> group_jobs;
+    group_jobs.clear();
+    cudaEvent_t last_wait = nullptr;
     for (int32_t i = g.first; i < g.first + g.count; ++i) {
         const int32_t id = ld[i];
         const ChunkRec& ch = p->chunks[id];
         if (ch.is_adapter) continue;
-        CU(cudaStreamWaitEvent(c->merge, landed_ev(c, id), 0));
-        ++mops;
+        if (landed_ev(c, id) != last_wait) {   // the chunks of a group share its landed event
+            last_wait = landed_ev(c, id);
+            CU(cudaStreamWaitEvent(c->merge, last_wait, 0));
+            ++mops;
+        }
         const bool all = c->merge_adapter == PB_MERGE_ALL;
         if (c->backup && !all && p->backup_off[ch.tensor] >= 0) {   // f2: keep the pristine base of the chunk
             CU(launch_copy(c->backup + p->backup_off[ch.tensor] + (int64_t)ch.r0 * p->tensors[ch.tensor].row_bytes(),
@@ -1167,18 +1184,43 @@ pb_status issue_group(Issuer& I, size_t gi) {
                     I.adapter_waited[a] = 1;
                     ++mops;
                 }
+            group_jobs.push_back(j);
+        }
+    }
+    // The adapted chunks of the group (they landed together) merge in as few launches as possible: up to
+    // kMaxMergeJobs jobs of one padded rank per persistent launch.
+    for (size_t k = 0; k < group_jobs.size();) {
+        if (p->f32()) {
+            const MergeJob& job = c->jobs[group_jobs[k++]];
             const int pi = prof_begin(c, K_MERGE, c->merge);
-            if (p->f32()) {
-                CU(launch_merge_f32(job.W, job.Wout, job.ldw, job.rows, job.cols, job.Bp, job.Ap, job.rank, job.scale,
-                                    c->merge));
-            } else {
-                CU(launch_merge(job.maps, job.rows, job.cols, job.rank, job.scale, c->merge));
-            }
+            CU(launch_merge_f32(job.W, job.Wout, job.ldw, job.rows, job.cols, job.Bp, job.Ap, job.rank, job.scale,
+                                c->merge));
             prof_end(c, pi, c->merge, 2.0 * job.rows * job.cols * job.rank,
                      p->es() * (2.0 * job.rows * job.cols + (double)job.rank * (job.rows + job.cols)));
             ++c->n_launches;
             mops += 1 + prof_ops(c);
+            continue;
         }
+        MergeJobDesc batch[kMaxMergeJobs];
+        int nb = 0;
+        double flops = 0, bytes = 0;
+        const int rk = merge_rk(c->jobs[group_jobs[k]].rank);
+        while (k < group_jobs.size() && nb < kMaxMergeJobs && merge_rk(c->jobs[group_jobs[k]].rank) == rk) {
+            const MergeJob& job = c->jobs[group_jobs[k++]];
+            batch[nb++] = MergeJobDesc{&job.maps, job.rows, job.cols, job.rank, job.scale};
+            flops += 2.0 * job.rows * job.cols * job.rank;
+            bytes += p->es() * (2.0 * job.rows * job.cols + (double)job.rank * (job.rows + job.cols));
+        }
+        const int pi = prof_begin(c, K_MERGE, c->merge);
+        CU(launch_merge_batch(batch, nb, c->merge));
+        prof_end(c, pi, c->merge, flops, bytes);
+        ++c->n_launches;
+        mops += 1 + prof_ops(c);
+    }
+    for (int32_t i = g.first; i < g.first + g.count; ++i) {
+        const int32_t id = ld[i];
+        const ChunkRec& ch = p->chunks[id];
+        if (ch.is_adapter) continue;
         if (c->merged_ev[id]) {   // timing mode (PB_LANDED_TIMING=1): per-chunk merged timestamp
             CU(cudaEventRecord(c->merged_ev[id], c->merge));
             ++mops;
@@ -1997,8 +2039,9 @@ extern "C" pb_status pb_switch_adapter(pb_ctx* c, int32_t adapter_id) {
     cudaStream_t s = c->comp;
     // the stage is rewritten in place: every peer must have finished copying it first (device-side wait on the
     // peers' gather-complete words, so the switch cannot tear a copy still in flight)
+    // (peers signal it in their cold start's epoch; replays and decode steps gather nothing and do not signal)
     for (int r = 0; r < c->n; ++r)
-        if (r != c->rank) CU(wait_word(c, c->L.f_gdone + r, s));
+        if (r != c->rank) CU(stream_wait_geq(s, flag_ptr(c->ws, c->L, c->L.f_gdone + r), c->cold_epoch));
     const auto stage = p->stages[c->rank];
     const char* hb = static_cast<const char*>(c->host_base);
     const char* ha = static_cast<const char*>(c->host_adapters);

@@ -107,6 +107,7 @@ struct pb_ctx {
     bool landed_timing = false;
     cudaEvent_t ready_merge = nullptr, ready_recv = nullptr;   // timing: last stage chunk merged / received
     cudaEvent_t tok_ev = nullptr;                               // prompt tokens landed (copy lane)
+    cudaEvent_t trial_fence[4] = {};                            // previous trial's streams drained (trial begin)
     int32_t last_own_stage_chunk = -1, last_recv_stage_chunk = -1;
     std::vector<cudaEvent_t> landed, gathered;
     std::vector<cudaEvent_t> merged_ev;          // per own chunk, after its merges (timing mode only)
@@ -141,6 +142,7 @@ struct pb_ctx {
 
     // trial state
     uint32_t epoch = 0;
+    uint32_t cold_epoch = 0;   // epoch of the last cold start (pb_trial_begin): the trial whose gather peers signal
     pb::Phase phase = pb::Phase::Idle;
     int32_t cur_batch = 0, cur_seq = 0;
     int32_t n_launches = 0;

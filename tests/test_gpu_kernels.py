@@ -52,6 +52,36 @@ def test_merge_within_one_ulp_of_correct_rounding(rows, cols, rank):
     assert (g == w).mean() > 0.95
 
 
+@pytest.mark.parametrize("rank", [16, 64])
+def test_merge_batch_jobs_in_one_launch(rank):
+    """pb_op_merge_batch: several tensors of different (ragged) shapes merged by one persistent launch whose CTAs walk
+    all jobs' tiles as one list; each job must equal the correctly rounded merge like a single-job launch."""
+    need_gpu()
+    rng = np.random.default_rng(rank)
+    shapes = [(256, 384), (130, 1000), (2048, 2048), (64, 136), (1024, 512)]
+    Ws, Bs, As, want, devs = [], [], [], [], []
+    for (rows, cols) in shapes:
+        W = rbits(rng, (rows, cols), 0.035)
+        Bm = rbits(rng, (rows, rank), 0.08)
+        Am = rbits(rng, (rank, cols), 1 / np.sqrt(cols))
+        d = (dev_bf16(W), dev_bf16(Bm), dev_bf16(Am))
+        devs.append(d)
+        Ws.append(W)
+        want.append(merge_bf16_bits(W, Bm, Am, 2.0))
+        Bs.append(Bm)
+        As.append(Am)
+    B.pb_op_merge_batch([ptr(d[0]) for d in devs], [c for _, c in shapes], [r for r, _ in shapes],
+                        [c for _, c in shapes], [ptr(d[1]) for d in devs], [ptr(d[2]) for d in devs], rank,
+                        [2.0] * len(shapes), stream())
+    torch.cuda.synchronize()
+    for (rows, cols), d, W, Bm, Am, wnt in zip(shapes, devs, Ws, Bs, As, want):
+        g = bf16_bits_to_f64(host_bits(d[0]))
+        w = bf16_bits_to_f64(wnt)
+        mag = np.abs(bf16_bits_to_f64(W)) + 2.0 * (np.abs(bf16_bits_to_f64(Bm)) @ np.abs(bf16_bits_to_f64(Am)))
+        assert np.all(np.abs(g - w) <= bf16_ulp(w) + (rank + 2) * 2.0 ** -24 * mag), (rows, cols)
+        assert (g == w).mean() > 0.95
+
+
 def test_merge_zero_B_is_identity():
     need_gpu()
     rng = np.random.default_rng(5)
@@ -151,6 +181,32 @@ def test_norm(rms, d):
         OF.layer_norm(hf, bf16_bits_to_f64(g), bf16_bits_to_f64(b), 1e-5)
     err = np.abs(bf16_bits_to_f64(host_bits(out)) - ref)
     assert np.all(err <= bf16_ulp(ref) + 1e-6), err.max()
+
+
+@pytest.mark.parametrize("rms", [False, True])
+@pytest.mark.parametrize("d,rows", [(256, 7), (1024, 128), (2048, 128), (2000, 300)])
+def test_norm_warp_kernel_bit_identical_to_cta_kernel(rms, d, rows):
+    """Small-M rows take the warp-per-row kernel; it replays the CTA kernel's virtual-thread sums and butterflies
+    in the same order, so both give the same bits (prefill and decode paths stay consistent)."""
+    import os
+    need_gpu()
+    rng = np.random.default_rng(d + rows)
+    h = (rng.standard_normal((rows, d)) * 2 + 0.3).astype(np.float32)
+    g = f64_to_bf16_bits(1 + rng.uniform(-0.1, 0.1, d))
+    b = f64_to_bf16_bits(rng.uniform(-0.02, 0.02, d))
+    hd_, gd, bd = dev_f32(h), dev_bf16(g), dev_bf16(b)
+    outs = []
+    for cta in (False, True):
+        out = torch.zeros((rows, d), dtype=torch.bfloat16, device="cuda")
+        if cta:
+            os.environ["PB_NORM_CTA"] = "1"
+        try:
+            B.pb_op_norm(ptr(hd_), rows, d, ptr(gd), 0 if rms else ptr(bd), 1e-5, ptr(out), stream())
+            torch.cuda.synchronize()
+        finally:
+            os.environ.pop("PB_NORM_CTA", None)
+        outs.append(host_bits(out))
+    assert np.array_equal(outs[0], outs[1])
 
 
 @pytest.mark.parametrize("T,Bsz,H,KVH,hd,t0,t1", [(16, 1, 4, 4, 64, 0, 16), (77, 2, 4, 2, 128, 0, 77),

@@ -67,6 +67,54 @@ def main():
                           "w_copies": ncp, "timing": "CUDA graph of the launches, one event pair"}), flush=True)
         del g, W, Ws, Bf, Af
         torch.cuda.empty_cache()
+    bench_batches(args.reps, hbm)
+
+
+BATCHES = [  # one launch merging a layer's adapted tensors (pb_op_merge_batch), as the cold start does per DMA group
+    ("C2 layer q+v 2 x 2048x2048 r16", [(2048, 2048)] * 2, 16),
+    ("C3 layer q+v 2 x 4096x4096 r16", [(4096, 4096)] * 2, 16),
+    ("C4 layer q,k,v,o,fc1,fc2 r64", [(5120, 5120)] * 4 + [(20480, 5120), (5120, 20480)], 64),
+]
+
+
+def bench_batches(reps, hbm):
+    s = torch.cuda.current_stream()
+    for label, shapes, rank in BATCHES:
+        tot = sum(r * c * 2 for r, c in shapes)
+        ncp = max(1, -(-300_000_000 // tot))
+        sets = [[torch.randn(r, c, device="cuda").mul_(0.02).to(torch.bfloat16) for r, c in shapes] for _ in range(ncp)]
+        Bs = [torch.randn(r, rank, device="cuda").mul_(0.01).to(torch.bfloat16) for r, _ in shapes]
+        As = [torch.randn(rank, c, device="cuda").mul_(0.01).to(torch.bfloat16) for _, c in shapes]
+
+        def go(i, st):
+            Ws = sets[i % ncp]
+            B.pb_op_merge_batch([w.data_ptr() for w in Ws], [c for _, c in shapes], [r for r, _ in shapes],
+                                [c for _, c in shapes], [b.data_ptr() for b in Bs], [a.data_ptr() for a in As], rank,
+                                [2.0] * len(shapes), st)
+
+        for i in range(ncp):
+            go(i, s.cuda_stream)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            cs = torch.cuda.current_stream().cuda_stream
+            for i in range(reps):
+                go(i, cs)
+        g.replay()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(s)
+        g.replay()
+        e1.record(s)
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / reps
+        nbytes = sum(4.0 * r * c + 2.0 * rank * (r + c) for r, c in shapes)
+        gbs = nbytes / (us * 1e-6) / 1e9
+        print(json.dumps({"batch": label, "jobs": len(shapes), "rank": rank, "us_per_launch": round(us, 2),
+                          "bytes": int(nbytes), "gbs": round(gbs, 1), "frac_hbm": round(gbs / hbm, 3),
+                          "timing": "CUDA graph of the launches, one event pair"}), flush=True)
+        del g, sets, Bs, As
+        torch.cuda.empty_cache()
 
 
 if __name__ == "__main__":
