@@ -128,98 +128,6 @@ __global__ void __launch_bounds__(256) norm_kernel(const float* __restrict__ h, 
     }
 }
 
-// One WARP per row (d <= 2048: the row is 64 fp32 per lane in registers) — the latency-bound small-M regime (C2:
-// 128 rows), with no block barrier on the row's path. Lane l plays virtual threads l + 32 j (j = 0..7) of the CTA
-// kernel above and performs exactly its operations in exactly its order (per-virtual-thread sums in element order,
-// the xor butterfly of each group of 32, the combine of the 8 group sums), so both kernels give the same bits.
-__global__ void __launch_bounds__(128) norm_warp_kernel(const float* __restrict__ h, int ldh,
-                                                        __nv_bfloat16* __restrict__ out, int ldo, int rows, int d,
-                                                        const __nv_bfloat16* __restrict__ gamma,
-                                                        const __nv_bfloat16* __restrict__ beta, float eps,
-                                                        const int* dyn, int dyn_in, int dyn_out) {
-    pdl_launch_dependents();
-    const int lane = threadIdx.x & 31;
-    const int r = blockIdx.x * 4 + (threadIdx.x >> 5);
-    const int ng = d >> 3;
-    uint4 gm[8], bt[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const int g = lane + 32 * j;
-        gm[j] = g < ng ? __ldg(reinterpret_cast<const uint4*>(gamma) + g) : make_uint4(0, 0, 0, 0);
-        bt[j] = g < ng && beta ? __ldg(reinterpret_cast<const uint4*>(beta) + g) : make_uint4(0, 0, 0, 0);
-    }
-    pdl_wait();
-    if (r >= rows) return;
-    long long row = r, orow = r;
-    if (dyn != nullptr) {
-        const long long t = *dyn;
-        row += t * dyn_in;
-        orow += t * dyn_out;
-    }
-    const float4* x = reinterpret_cast<const float4*>(h + row * (long long)ldh);
-    float v[8][8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const int g = lane + 32 * j;
-        float4 lo = make_float4(0.f, 0.f, 0.f, 0.f), hi = lo;
-        if (g < ng) {
-            lo = x[2 * g];
-            hi = x[2 * g + 1];
-        }
-        v[j][0] = lo.x; v[j][1] = lo.y; v[j][2] = lo.z; v[j][3] = lo.w;
-        v[j][4] = hi.x; v[j][5] = hi.y; v[j][6] = hi.z; v[j][7] = hi.w;
-    }
-    auto combine = [&](float (&gs)[8]) {   // rownorm::combine8 of the 8 group sums (red[lane], lane < 8)
-        float sel = 0.f;
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-            if (lane == j) sel = gs[j];
-        return rownorm::warp_sum(sel);
-    };
-    float mean = 0.f;
-    if (beta) {
-        float gs[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            float s = 0.f;
-            if (lane + 32 * j < ng) {
-#pragma unroll
-                for (int e = 0; e < 8; ++e) s = rownorm::acc_sum(s, v[j][e]);
-            }
-            gs[j] = rownorm::warp_sum(s);
-        }
-        mean = rownorm::mean_of(combine(gs), d);
-    }
-    float gq[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        float q = 0.f;
-        if (lane + 32 * j < ng) {
-#pragma unroll
-            for (int e = 0; e < 8; ++e) q = rownorm::acc_sq(q, v[j][e], mean);
-        }
-        gq[j] = rownorm::warp_sum(q);
-    }
-    const float rstd = rownorm::rstd_of(combine(gq), d, eps);
-    uint4* o = reinterpret_cast<uint4*>(out + orow * (long long)ldo);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const int g = lane + 32 * j;
-        if (g >= ng) continue;
-        const __nv_bfloat16* gp = reinterpret_cast<const __nv_bfloat16*>(&gm[j]);
-        const __nv_bfloat16* bp = reinterpret_cast<const __nv_bfloat16*>(&bt[j]);
-        uint4 w;
-        uint16_t* wp = reinterpret_cast<uint16_t*>(&w);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            const __nv_bfloat16 y = rownorm::out_f(v[j][e], mean, rstd, __bfloat162float(gp[e]),
-                                                   __bfloat162float(bp[e]), beta != nullptr);
-            wp[e] = *reinterpret_cast<const uint16_t*>(&y);
-        }
-        o[g] = w;
-    }
-}
-
 // ------------------------------------------------------------------ embedding (+ OPT learned positions)
 __global__ void embed_kernel(EmbedSrc E, const __nv_bfloat16* __restrict__ pos, const int32_t* __restrict__ tok,
                              float* __restrict__ h, int d, int r0, int B, const int* dyn) {
@@ -552,7 +460,7 @@ cudaError_t launch_set_words(uint32_t* base, const int32_t* idx, int n, uint32_t
 cudaError_t warm_simt_kernels() {
     cudaFuncAttributes a;
     const void* fns[] = {(const void*)norm_kernel<1>, (const void*)norm_kernel<2>, (const void*)norm_kernel<3>,
-                         (const void*)norm_kernel<4>, (const void*)norm_kernel<5>, (const void*)norm_warp_kernel, (const void*)embed_kernel,
+                         (const void*)norm_kernel<4>, (const void*)norm_kernel<5>, (const void*)embed_kernel,
                          (const void*)rope_table_kernel, (const void*)rope_kernel, (const void*)attention_kernel<32>,
                          (const void*)attention_kernel<64>, (const void*)attention_kernel<128>,
                          (const void*)logits_kernel, (const void*)argmax_kernel, (const void*)signal_kernel,
@@ -573,9 +481,6 @@ cudaError_t launch_norm(const float* h, int ldh, __nv_bfloat16* out, int ldo, in
         (reinterpret_cast<uintptr_t>(gamma) & 15) || (reinterpret_cast<uintptr_t>(beta) & 15))
         return cudaErrorInvalidValue;
     const int groups = (d / 8 + 255) / 256;
-    if (groups == 1 && rows <= 512 && !getenv("PB_NORM_CTA"))   // small-M rows: one warp per row, no block barrier
-        return launch_pdl(norm_warp_kernel, (rows + 3) / 4, 128, 0, s, pdl, h, ldh, out, ldo, rows, d, gamma, beta,
-                          eps, dyn, dyn_in, dyn_out);
 #define PB_NORM_CASE(G)                                                                                                \
     case G:                                                                                                            \
         return launch_pdl(norm_kernel<G>, rows, 256, 0, s, pdl, h, ldh, out, ldo, d, gamma, beta, eps, dyn, dyn_in,   \
