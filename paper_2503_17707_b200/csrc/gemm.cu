@@ -82,25 +82,13 @@ __device__ __forceinline__ uint32_t map_cluster(uint32_t smem_addr, uint32_t ran
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
     return r;
 }
-__device__ __forceinline__ void st_cluster_u4(uint32_t addr, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
-    asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(x), "r"(y), "r"(z), "r"(w)
+__device__ __forceinline__ float4 ld_cluster_f4(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(addr)
                  : "memory");
-}
-// Arrive on an mbarrier of any CTA of the cluster, releasing this thread's prior (distributed) shared-memory writes.
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
-}
-// Wait for phase `phase` of a local mbarrier with cluster-scope acquire (writes released by other CTAs are visible).
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAITC_%=:\n"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAITC_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(phase)
-        : "memory");
+    return v;
 }
 
 // Partial tile: [128 rows][TBN/4 float4 chunks], chunk c of row r stored at slot c ^ (r % (TBN/4)) (row-per-thread
@@ -137,7 +125,6 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
     uint64_t* empty = full + kMaxStagesAny;
     uint64_t* done = empty + kMaxStagesAny;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
-    uint64_t* recv = done + 2;   // split-K exchange: 128 row arrivals (one per row of the tile, from all S CTAs)
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int split = S > 1 ? (int)cluster_rank() : 0;
@@ -160,7 +147,6 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
             mbar_init(&empty[s], 1);
         }
         mbar_init(done, 1);
-        mbar_init(recv, BM);
         fence_mbar_init();
     }
     if (warp == 0) tmem_alloc<TBN>(tmem_slot);
@@ -225,43 +211,11 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
     tc_fence_after();
     if (tid == 0) PB_GEMM_STAMP(5);
 
-    // ---------------- split-K exchange, PUSHED (no remote reads): CTA `split` owns rows [split*RPO, (split+1)*RPO) of the
-    // tile. Every thread holds one accumulator row (TMEM lane = row); once every CTA of the cluster has finished its
-    // mainloop (cluster barrier: the rings are free) it stores that row into its owner's ring, slot `split`
-    // (st.shared::cluster), and arrives on the owner's receive barrier with release.cluster semantics. The owner
-    // waits for its 128 arrivals, sums its rows over the S slots in the FIXED order 0..S-1 from local shared memory
-    // and applies the fused epilogue. Global operands of the epilogue (fp32 residual, bias) are requested before
-    // the exchange so their latency overlaps it.
-    constexpr int RPO = BM / S;                                   // rows per owner
-    constexpr int chunks = EPI == EPI_SILU_MUL ? 16 : TBN / 4;    // output float4 chunks per row
-    constexpr int ITEMS = RPO * chunks / 128;                     // epilogue items per thread
-    static_assert(RPO * chunks % 128 == 0, "whole items per thread");
-    constexpr bool kPre = ITEMS <= 8;                             // registers: prefetch up to 8 items per thread
-    constexpr int NPRE = kPre ? ITEMS : 1;
-    const int r_lo = RPO * split;
-    float4 pre_h[NPRE];
-    uint2 pre_b[NPRE];
-#pragma unroll
-    for (int k = 0; k < (kPre ? ITEMS : 0); ++k) {
-        const int idx = tid + 128 * k, r = r_lo + idx / chunks, n = n_out0 + (idx % chunks) * 4;
-        const int row = m0 + r;
-        const bool full4 = row < m_end && n + 4 <= a.N;
-        pre_h[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-        pre_b[k] = make_uint2(0u, 0u);
-        if (EPI == EPI_RESID && full4)
-            pre_h[k] = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(a.out) + (size_t)row * a.ldo + n);
-        if (EPI != EPI_SILU_MUL && a.bias && full4) pre_b[k] = *reinterpret_cast<const uint2*>(a.bias + n);
-    }
-    const uint32_t recv_bar = smem_u32(recv);
-    if (S > 1) cluster_sync();
-    else __syncthreads();
+    // ---------------- stage the fp32 tile (this CTA's K-partial) in shared memory; all MMAs and TMA loads
+    // have completed, so the stage ring is free. Two batches of 64 columns (4 loads in flight, one wait).
     {
         const int row = warp * 32 + lane;
-        const int owner = row / RPO, orow = row % RPO;
-        const uint32_t slot_row = smem_u32(smem) + (uint32_t)((split * RPO + orow) * (TBN * 4));
-        const uint32_t dst_row = S > 1 ? map_cluster(slot_row, owner) : slot_row;
         const uint32_t t_row = tmem + ((uint32_t)(warp * 32) << 16);
-        const int sw = (split * RPO + orow) & (TBN / 4 - 1);
 #pragma unroll
         for (int half = 0; half < TBN / 64; ++half) {
             uint32_t r0[32], r1[32];
@@ -270,40 +224,48 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
             tmem_wait_ld();
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-                st_cluster_u4(dst_row + (((half * 16 + q) ^ sw) << 4), r0[4 * q], r0[4 * q + 1], r0[4 * q + 2], r0[4 * q + 3]);
-                st_cluster_u4(dst_row + (((half * 16 + 8 + q) ^ sw) << 4), r1[4 * q], r1[4 * q + 1], r1[4 * q + 2],
-                              r1[4 * q + 3]);
+                *reinterpret_cast<uint4*>(smem + part_off<TBN>(row, half * 16 + q)) =
+                    make_uint4(r0[4 * q], r0[4 * q + 1], r0[4 * q + 2], r0[4 * q + 3]);
+                *reinterpret_cast<uint4*>(smem + part_off<TBN>(row, half * 16 + 8 + q)) =
+                    make_uint4(r1[4 * q], r1[4 * q + 1], r1[4 * q + 2], r1[4 * q + 3]);
             }
         }
-        mbar_arrive_cluster(S > 1 ? map_cluster(recv_bar, owner) : recv_bar);
     }
-    mbar_wait_cluster(recv, 0);
     tc_fence_before();
+    if (S > 1) cluster_sync();
+    else __syncthreads();
     if (tid == 0) PB_GEMM_STAMP(6);
 
-    // ---------------- reduce this CTA's rows over the S slots (fixed order 0..S-1) + fused epilogue
-    auto sum_chunk = [&](int rr, int c) {   // rr = row within the owner's range
-        float4 acc = *reinterpret_cast<const float4*>(smem + part_off<TBN>(rr, c));
+    // ---------------- reduce rows [r_lo, r_hi) over the S partials (fixed order 0..S-1) + fused epilogue
+    const int r_lo = BM * split / S, r_hi = BM * (split + 1) / S;
+    const uint32_t base = smem_u32(smem);
+    const int chunks = EPI == EPI_SILU_MUL ? 16 : TBN / 4;
+    auto sum_chunk = [&](int r, int c) {
+        if constexpr (S == 1) {
+            return *reinterpret_cast<const float4*>(smem + part_off<TBN>(r, c));
+        } else {
+            float4 p[S];
 #pragma unroll
-        for (int s2 = 1; s2 < S; ++s2) {
-            const float4 p = *reinterpret_cast<const float4*>(smem + part_off<TBN>(s2 * RPO + rr, c));
-            acc.x += p.x;
-            acc.y += p.y;
-            acc.z += p.z;
-            acc.w += p.w;
+            for (int s2 = 0; s2 < S; ++s2) p[s2] = ld_cluster_f4(map_cluster(base + part_off<TBN>(r, c), s2));
+            float4 acc = p[0];
+#pragma unroll
+            for (int s2 = 1; s2 < S; ++s2) {
+                acc.x += p[s2].x;
+                acc.y += p[s2].y;
+                acc.z += p[s2].z;
+                acc.w += p[s2].w;
+            }
+            return acc;
         }
-        return acc;
     };
-#pragma unroll
-    for (int k = 0; k < ITEMS; ++k) {
-        const int idx = tid + 128 * k;
-        const int rr = idx / chunks, ch = idx % chunks;
-        const int row = m0 + r_lo + rr;
+    for (int idx = tid; idx < (r_hi - r_lo) * chunks; idx += 128) {
+        const int r = r_lo + idx / chunks, ch = idx % chunks;
+        const int row = m0 + r;
         if (row >= m_end) continue;
         if (EPI == EPI_SILU_MUL) {
             const int n = n_out0 + ch * 4;
             if (n >= a.N) continue;
-            const float4 g = sum_chunk(rr, ch), u = sum_chunk(rr, ch + 16);
+            const float4 g = sum_chunk(r, ch), u = sum_chunk(r, ch + 16);
             const float o[4] = {silu(g.x) * u.x, silu(g.y) * u.y, silu(g.z) * u.z, silu(g.w) * u.w};
             __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(a.out) + (size_t)row * a.ldo + n;
             if (n + 4 <= a.N) {
@@ -323,7 +285,7 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
             // thread owning the first half rotates and writes both, from the fp32 sums
             const int half = a.rope_hd >> 1, ci = n % a.rope_hd;
             if (ci >= half) continue;
-            const float4 p1 = sum_chunk(rr, ch), p2 = sum_chunk(rr, ch + (half >> 2));
+            const float4 p1 = sum_chunk(r, ch), p2 = sum_chunk(r, ch + (half >> 2));
             float x1[4] = {p1.x, p1.y, p1.z, p1.w}, x2[4] = {p2.x, p2.y, p2.z, p2.w};
             rope_rotate4(a, row, ci, x1, x2);
             __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(a.out) + (size_t)row * a.ldo + n;
@@ -336,22 +298,12 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
             *reinterpret_cast<uint2*>(out + half) = w2;
             continue;
         }
-        const float4 acc = sum_chunk(rr, ch);
+        const float4 acc = sum_chunk(r, ch);
         float v[4] = {acc.x, acc.y, acc.z, acc.w};
         const int nv = min(4, a.N - n);
         if (a.bias) {
-            if (nv == 4) {
-                const uint2 bb = kPre ? pre_b[kPre ? k : 0] : *reinterpret_cast<const uint2*>(a.bias + n);
-                const __nv_bfloat162* bp = reinterpret_cast<const __nv_bfloat162*>(&bb);
-                const float2 b01 = __bfloat1622float2(bp[0]), b23 = __bfloat1622float2(bp[1]);
-                v[0] += b01.x;
-                v[1] += b01.y;
-                v[2] += b23.x;
-                v[3] += b23.y;
-            } else {
 #pragma unroll
-                for (int c = 0; c < 4; ++c) v[c] += c < nv ? __bfloat162float(a.bias[n + c]) : 0.f;
-            }
+            for (int c = 0; c < 4; ++c) v[c] += c < nv ? __bfloat162float(a.bias[n + c]) : 0.f;
         }
         if (EPI == EPI_BF16) {
             if (n < a.scale_cols) {
@@ -374,7 +326,7 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
         } else {  // EPI_RESID: h += acc + bias (fp32)
             float* h = reinterpret_cast<float*>(a.out) + (size_t)row * a.ldo + n;
             if (nv == 4) {
-                float4 x = kPre ? pre_h[kPre ? k : 0] : *reinterpret_cast<const float4*>(h);
+                float4 x = *reinterpret_cast<float4*>(h);
                 x.x += v[0];
                 x.y += v[1];
                 x.z += v[2];
@@ -385,6 +337,7 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
             }
         }
     }
+    if (S > 1) cluster_sync();   // keep this CTA's partial alive until every peer has read it
     if (tid == 0) PB_GEMM_STAMP(7);
     tc_fence_before();
     __syncthreads();

@@ -1,0 +1,9 @@
+export CUDA_DEVICE_MAX_CONNECTIONS=32
+O=gpurun_out/${TAG:-r02j}; mkdir -p $O
+timeout 600 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
+timeout 300 python -m pytest tests/test_gpu_kernels.py -q -x -p no:cacheprovider -k gemm > $O/pytest_kernels.log 2>&1; echo "exit $?" >> $O/pytest_kernels.log
+timeout 300 python tools/gemm_phases.py > $O/gemm_phases.txt 2>&1
+timeout 600 python bench.py > $O/bench_C2.json 2> $O/bench_C2.err; echo "bench exit $?" >> $O/bench_C2.err
+free -g > $O/free.txt
+timeout 1200 python bench.py --workload C5a --host-alias 8 --steps 2 --warmup 1 --no-cpu-baseline > $O/bench_C5a.json 2> $O/bench_C5a.err; echo "bench exit $?" >> $O/bench_C5a.err
+ls -la $O
