@@ -39,6 +39,23 @@ __device__ __forceinline__ float fast_exp2(float x) {
     return y;
 }
 
+// Row max / sum of exp2 over the 128 scores a thread holds, in 8 independent chains (one softmax warp per SMSP has
+// no other warp to hide a 128-long dependent FMNMX / FADD chain behind); the chains combine in a fixed tree, so
+// the result is deterministic (the max is exact in any order).
+__device__ __forceinline__ float row_max128(const uint32_t (&sr)[4][32]) {
+    float mk[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) mk[k] = -CUDART_INF_F;
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int e = 0; e < 32; ++e) mk[e & 7] = fmaxf(mk[e & 7], __uint_as_float(sr[c][e]));
+    return fmaxf(fmaxf(fmaxf(mk[0], mk[1]), fmaxf(mk[2], mk[3])), fmaxf(fmaxf(mk[4], mk[5]), fmaxf(mk[6], mk[7])));
+}
+__device__ __forceinline__ float tree8(const float (&r)[8]) {
+    return ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+}
+
 template <int HD>
 struct AttnSmem {
     static constexpr int kQ = HD / 64 * kAtom, kK = kQ, kV = kQ;   // K and V double-buffered; P lives in TMEM
@@ -207,38 +224,29 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
             }
             if (!pass_b) {
                 // ---- pass A: exact running max (scale > 0: max of raw scores, scaled once) and rescaled sum
-                float mx = -CUDART_INF_F;
+                const float m_new = fmaxf(m, row_max128(sr) * scale_log2);
+                float rk[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                 for (int c = 0; c < 4; ++c)
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(sr[c][e]));
-                const float m_new = fmaxf(m, mx * scale_log2);
-                float rs = 0.f;
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) rs += fast_exp2(fmaf(__uint_as_float(sr[c][e]), scale_log2, -m_new));
+                    for (int e = 0; e < 32; ++e) rk[e & 7] += fast_exp2(fmaf(__uint_as_float(sr[c][e]), scale_log2, -m_new));
+                const float rs = tree8(rk);
                 l = (m == -CUDART_INF_F ? 0.f : l * fast_exp2(m - m_new)) + rs;
                 m = m_new;
                 continue;
             }
             if (single) {   // ---- one key tile: max, then E = exp2(s*c - m) kept in sr, l = sum E (pass A's order)
-                float mx = -CUDART_INF_F;
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(sr[c][e]));
-                m = mx * scale_log2;
-                float rs = 0.f;
+                m = row_max128(sr) * scale_log2;
+                float rk[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                 for (int c = 0; c < 4; ++c)
 #pragma unroll
                     for (int e = 0; e < 32; ++e) {
                         const float ev = fast_exp2(fmaf(__uint_as_float(sr[c][e]), scale_log2, -m));
                         sr[c][e] = __float_as_uint(ev);
-                        rs += ev;
+                        rk[e & 7] += ev;
                     }
-                l = rs;
+                l = tree8(rk);
                 inv_l = 1.f / l;
 #pragma unroll
                 for (int cb = 0; cb < 4; ++cb) {
@@ -257,6 +265,16 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
             }
             // ---- pass B: P = RNE_bf16(exp2(s*c - m) / l) straight into TMEM (the A operand of the PV MMA)
             if (j == 0) inv_l = 1.f / l;   // l >= 1: the row maximum contributes exp2(0)
+            // the probabilities are computed (packed in place into sr[cb][0..15]) while PV_{j-1} still reads the
+            // previous P from TMEM; only the stores wait for it
+#pragma unroll
+            for (int cb = 0; cb < 4; ++cb)
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    const float p0 = fast_exp2(fmaf(__uint_as_float(sr[cb][2 * e]), scale_log2, -m)) * inv_l;
+                    const float p1 = fast_exp2(fmaf(__uint_as_float(sr[cb][2 * e + 1]), scale_log2, -m)) * inv_l;
+                    sr[cb][e] = bf16x2_bits(p0, p1);
+                }
             if (j > 0) {   // P (TMEM) is read by PV_{j-1}
                 mbar_wait(o_full, (j - 1) & 1);
                 tc_fence_after();
@@ -265,11 +283,7 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
             for (int cb = 0; cb < 4; ++cb) {
                 uint32_t w[16];
 #pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                    const float p0 = fast_exp2(fmaf(__uint_as_float(sr[cb][2 * e]), scale_log2, -m)) * inv_l;
-                    const float p1 = fast_exp2(fmaf(__uint_as_float(sr[cb][2 * e + 1]), scale_log2, -m)) * inv_l;
-                    w[e] = bf16x2_bits(p0, p1);
-                }
+                for (int e = 0; e < 16; ++e) w[e] = sr[cb][e];
                 tmem_st16(tP + lane_off + cb * 16, w);
             }
             tmem_wait_st();

@@ -46,7 +46,7 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 // resident before the kernel is enqueued). Two-pass fp32 statistics (rownorm.cuh): mean, then the mean of squared
 // deviations, each summed per thread in element order, then by a warp butterfly and over the 8 warps.
 template <int G>
-__global__ void __launch_bounds__(256) norm_kernel(const float* __restrict__ h, int ldh, __nv_bfloat16* __restrict__ out,
+__global__ void __launch_bounds__(256, G >= 3 ? 4 : 1) norm_kernel(const float* __restrict__ h, int ldh, __nv_bfloat16* __restrict__ out,
                                                    int ldo, int d, const __nv_bfloat16* __restrict__ gamma,
                                                    const __nv_bfloat16* __restrict__ beta, float eps, const int* dyn,
                                                    int dyn_in, int dyn_out) {
@@ -54,12 +54,18 @@ __global__ void __launch_bounds__(256) norm_kernel(const float* __restrict__ h, 
     static_assert(NT == rownorm::kVT, "8 warps per row (rownorm::combine8)");
     pdl_launch_dependents();   // a PDL-launched GEMM may start its weight prefetch
     const int ng = d >> 3;     // 8-element groups in the row
-    uint4 gm[G], bt[G];
+    // Small rows (G <= 2, the latency-bound small-M regime): gamma / beta in registers before the dependency wait.
+    // Large rows (G >= 3, e.g. d = 8192 at M = 2048, bandwidth-bound): fetched at the output (L2-resident, shared by
+    // every row), which frees 8 G registers per thread for 4 resident CTAs per SM (more row loads in flight).
+    constexpr bool kPreGB = G <= 2;
+    uint4 gm[kPreGB ? G : 1], bt[kPreGB ? G : 1];
+    if constexpr (kPreGB) {
 #pragma unroll
-    for (int i = 0; i < G; ++i) {
-        const int g = threadIdx.x + i * NT;
-        gm[i] = g < ng ? __ldg(reinterpret_cast<const uint4*>(gamma) + g) : make_uint4(0, 0, 0, 0);
-        bt[i] = g < ng && beta ? __ldg(reinterpret_cast<const uint4*>(beta) + g) : make_uint4(0, 0, 0, 0);
+        for (int i = 0; i < G; ++i) {
+            const int g = threadIdx.x + i * NT;
+            gm[i] = g < ng ? __ldg(reinterpret_cast<const uint4*>(gamma) + g) : make_uint4(0, 0, 0, 0);
+            bt[i] = g < ng && beta ? __ldg(reinterpret_cast<const uint4*>(beta) + g) : make_uint4(0, 0, 0, 0);
+        }
     }
     pdl_wait();                // PDL-launched: the previous kernel's output is visible from here on
     __shared__ float red[32];
@@ -114,8 +120,16 @@ __global__ void __launch_bounds__(256) norm_kernel(const float* __restrict__ h, 
     for (int i = 0; i < G; ++i) {
         const int g = threadIdx.x + i * NT;
         if (g >= ng) continue;
-        const __nv_bfloat16* gp = reinterpret_cast<const __nv_bfloat16*>(&gm[i]);
-        const __nv_bfloat16* bp = reinterpret_cast<const __nv_bfloat16*>(&bt[i]);
+        uint4 gq, bq;
+        if constexpr (kPreGB) {
+            gq = gm[i];
+            bq = bt[i];
+        } else {
+            gq = __ldg(reinterpret_cast<const uint4*>(gamma) + g);
+            bq = beta ? __ldg(reinterpret_cast<const uint4*>(beta) + g) : make_uint4(0, 0, 0, 0);
+        }
+        const __nv_bfloat16* gp = reinterpret_cast<const __nv_bfloat16*>(&gq);
+        const __nv_bfloat16* bp = reinterpret_cast<const __nv_bfloat16*>(&bq);
         uint4 r;
         uint16_t* rp = reinterpret_cast<uint16_t*>(&r);
 #pragma unroll
