@@ -3,9 +3,10 @@
 //   a_t = sum_{j <= t} softmax_j(q_t . k_j * score_scale) v_j        (per head; GQA: kv head = h / group)
 //   (the attention of every decoder layer in the first-token prefill; HF conventions G14)
 //
-// CTA = (128 query positions, head, sequence); 160 threads:
-//   warps 0-3 : softmax + epilogue, one query row per thread = one TMEM lane
-//   warp 4    : TMA producer and single-thread MMA issuer
+// CTA = (128 query positions, head, sequence); 288 threads:
+//   warps 0-7 : softmax + epilogue, two threads per query row (TMEM lane): warp q and warp q + 4 take key columns
+//               [0, 64) and [64, 128) of each S tile (2 softmax warps per SMSP hide each other's stalls)
+//   warp 8    : TMA producer and single-thread MMA issuer
 // Two passes over the 128-key tiles j (keys [0, q_tile_end) only — causal), so that the probabilities are rounded
 // to bf16 after normalisation, at exactly the storage contract's rounding point:
 //   pass A:  S = Q K_j^T   tcgen05.mma M128 N128, K = hd, fp32 accumulator in TMEM columns [0, 128);
@@ -39,19 +40,8 @@ __device__ __forceinline__ float fast_exp2(float x) {
     return y;
 }
 
-// Row max / sum of exp2 over the 128 scores a thread holds, in 8 independent chains (one softmax warp per SMSP has
-// no other warp to hide a 128-long dependent FMNMX / FADD chain behind); the chains combine in a fixed tree, so
-// the result is deterministic (the max is exact in any order).
-__device__ __forceinline__ float row_max128(const uint32_t (&sr)[4][32]) {
-    float mk[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) mk[k] = -CUDART_INF_F;
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-#pragma unroll
-        for (int e = 0; e < 32; ++e) mk[e & 7] = fmaxf(mk[e & 7], __uint_as_float(sr[c][e]));
-    return fmaxf(fmaxf(fmaxf(mk[0], mk[1]), fmaxf(mk[2], mk[3])), fmaxf(fmaxf(mk[4], mk[5]), fmaxf(mk[6], mk[7])));
-}
+// Sums of exp2 over a thread's scores run in 8 independent chains combined in a fixed tree (deterministic); the
+// row max likewise (exact in any order).
 __device__ __forceinline__ float tree8(const float (&r)[8]) {
     return ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
 }
@@ -60,13 +50,14 @@ template <int HD>
 struct AttnSmem {
     static constexpr int kQ = HD / 64 * kAtom, kK = kQ, kV = kQ;   // K and V double-buffered; P lives in TMEM
     static constexpr int offQ = 0, offK = offQ + kQ, offV = offK + 2 * kK, offBar = offV + 2 * kV;
+    static constexpr int offX = offBar + 128;   // half-row exchange: [2 halves][128 rows] float
     // TMEM: S [0, 128) fp32, O [128, 128 + HD) fp32, P [128 + HD, 192 + HD) bf16 pairs (A operand of PV)
     static constexpr uint32_t kTmemCols = HD == 64 ? 256 : 512;
-    static constexpr int kTotal = offBar + 128 + 1024;
+    static constexpr int kTotal = offX + 2 * 128 * 4 + 1024;
 };
 
 template <int HD>
-__global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_constant__ CUtensorMap map, __nv_bfloat16* __restrict__ out,
+__global__ void __launch_bounds__(288, 1) attention_tc_kernel(const __grid_constant__ CUtensorMap map, __nv_bfloat16* __restrict__ out,
                                                         int ldo, int t0, int t1, int group, int k_col0, int v_col0,
                                                         float scale_log2, const int* dyn) {
     using SM = AttnSmem<HD>;
@@ -77,6 +68,7 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
     uint64_t *q_full = bars, *k_full = bars + 1 /* [2] */, *v_full = bars + 3 /* [2] */, *s_full = bars + 5,
              *s_free = bars + 6, *p_full = bars + 7, *o_full = bars + 8;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+    float* xch = reinterpret_cast<float*>(smem + SM::offX);   // [half][row]
 
     pdl_launch_dependents();
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -98,8 +90,8 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
         mbar_init(&v_full[0], 1);
         mbar_init(&v_full[1], 1);
         mbar_init(s_full, 1);
-        mbar_init(s_free, 4);      // one arrive per softmax warp
-        mbar_init(p_full, 4);
+        mbar_init(s_free, 8);      // one arrive per softmax warp
+        mbar_init(p_full, 8);
         mbar_init(o_full, 1);
         fence_mbar_init();
     }
@@ -121,7 +113,7 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
     // values, in the same order, as the two passes would (no second QK^T, no second exponential).
     const bool single = n_kv == 1;
     const int NI = single ? 1 : 2 * n_kv;
-    if (warp == 4) {
+    if (warp == 8) {
         if (lane == 0) {
             constexpr int kBox = kAtom;   // bytes of one 64-col box
             auto load_rows = [&](uint8_t* dst, uint64_t* bar, int col, int t) {
@@ -194,11 +186,24 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
         }
         __syncwarp();
     } else {
-        // ---------------- softmax warps: thread = query row r
-        const int r = warp * 32 + lane;
+        // ---------------- softmax warps: TWO threads per query row r: warps q and q + 4 (TMEM lane quadrant q) hold
+        // key columns [0, 64) and [64, 128) of every S tile — 8 softmax warps, 2 per SMSP, so one's dependency stalls
+        // hide behind the other's issue. Per tile the halves exchange their row maxima (shared memory + a 64-thread
+        // named barrier per quadrant); each keeps the running sum of its own half, combined once after pass A.
+        const int q4 = warp & 3, hf = warp >> 2;
+        const int r = q4 * 32 + lane;
         const int t = q0 + r;
         const bool row_ok = t < q_hi;   // rows past t1 are computed (never masked, always finite) but not stored
-        const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+        const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+        const int bar_id = 1 + q4;      // named barrier of the two warps of quadrant q4
+        auto pair_sync = [&]() { named_bar_sync(bar_id, 64); };
+        auto exchange = [&](float v) {  // the partner half's value of this row
+            xch[hf * 128 + r] = v;
+            pair_sync();
+            const float o = xch[(hf ^ 1) * 128 + r];
+            pair_sync();                 // the slots are rewritten by the next exchange
+            return o;
+        };
         float m = -CUDART_INF_F, l = 0.f, inv_l = 0.f;
         for (int i = 0; i < NI; ++i) {
             const uint32_t ph = i & 1;
@@ -206,56 +211,57 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
             const int j = single ? 0 : (pass_b ? i - n_kv : i);
             mbar_wait(s_full, ph);
             tc_fence_after();
-            uint32_t sr[4][32];
+            uint32_t sr[2][32];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) tmem_ld32_async(tS + lane_off + c * 32, sr[c]);
+            for (int c = 0; c < 2; ++c) tmem_ld32_async(tS + lane_off + hf * 64 + c * 32, sr[c]);
             tmem_wait_ld();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(s_free);
             // causal mask (key > t) only on the tiles that reach past the first query of this query tile
-            const int key0 = j * KT;
-            if (key0 + KT - 1 > q0) {
+            const int key0 = j * KT + hf * 64;
+            if (key0 + 63 > q0) {
 #pragma unroll
-                for (int c = 0; c < 4; ++c)
+                for (int c = 0; c < 2; ++c)
 #pragma unroll
                     for (int e = 0; e < 32; ++e)
                         if (key0 + c * 32 + e > t) sr[c][e] = __float_as_uint(-CUDART_INF_F);
             }
-            if (!pass_b) {
-                // ---- pass A: exact running max (scale > 0: max of raw scores, scaled once) and rescaled sum
-                const float m_new = fmaxf(m, row_max128(sr) * scale_log2);
+            auto half_max = [&]() {
+                float mk[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) mk[k] = -CUDART_INF_F;
+#pragma unroll
+                for (int c = 0; c < 2; ++c)
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) mk[e & 7] = fmaxf(mk[e & 7], __uint_as_float(sr[c][e]));
+                return fmaxf(fmaxf(fmaxf(mk[0], mk[1]), fmaxf(mk[2], mk[3])),
+                             fmaxf(fmaxf(mk[4], mk[5]), fmaxf(mk[6], mk[7])));
+            };
+            if (single) {   // ---- one key tile: max, E = exp2(s*c - m) kept in sr, l = sum E, P = E / l
+                const float hm = half_max();
+                m = fmaxf(hm, exchange(hm)) * scale_log2;
                 float rk[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-                for (int c = 0; c < 4; ++c)
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) rk[e & 7] += fast_exp2(fmaf(__uint_as_float(sr[c][e]), scale_log2, -m_new));
-                const float rs = tree8(rk);
-                l = (m == -CUDART_INF_F ? 0.f : l * fast_exp2(m - m_new)) + rs;
-                m = m_new;
-                continue;
-            }
-            if (single) {   // ---- one key tile: max, then E = exp2(s*c - m) kept in sr, l = sum E (pass A's order)
-                m = row_max128(sr) * scale_log2;
-                float rk[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
+                for (int c = 0; c < 2; ++c)
 #pragma unroll
                     for (int e = 0; e < 32; ++e) {
                         const float ev = fast_exp2(fmaf(__uint_as_float(sr[c][e]), scale_log2, -m));
                         sr[c][e] = __float_as_uint(ev);
                         rk[e & 7] += ev;
                     }
-                l = tree8(rk);
+                const float lh = tree8(rk);
+                const float lo = exchange(lh);
+                l = hf == 0 ? lh + lo : lo + lh;   // the same sum (half 0 first) in both threads
                 inv_l = 1.f / l;
 #pragma unroll
-                for (int cb = 0; cb < 4; ++cb) {
+                for (int cb = 0; cb < 2; ++cb) {
                     uint32_t w[16];
 #pragma unroll
                     for (int e = 0; e < 16; ++e)
                         w[e] = bf16x2_bits(__uint_as_float(sr[cb][2 * e]) * inv_l,
                                            __uint_as_float(sr[cb][2 * e + 1]) * inv_l);
-                    tmem_st16(tP + lane_off + cb * 16, w);
+                    tmem_st16(tP + lane_off + hf * 32 + cb * 16, w);
                 }
                 tmem_wait_st();
                 tc_fence_before();
@@ -263,12 +269,30 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
                 if (lane == 0) mbar_arrive(p_full);
                 continue;
             }
+            if (!pass_b) {
+                // ---- pass A: exact running max of the whole row (halves exchanged) and this half's rescaled sum
+                const float hm = half_max();
+                const float m_new = fmaxf(m, fmaxf(hm, exchange(hm)) * scale_log2);
+                float rk[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int c = 0; c < 2; ++c)
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) rk[e & 7] += fast_exp2(fmaf(__uint_as_float(sr[c][e]), scale_log2, -m_new));
+                const float rs = tree8(rk);
+                l = (m == -CUDART_INF_F ? 0.f : l * fast_exp2(m - m_new)) + rs;
+                m = m_new;
+                continue;
+            }
             // ---- pass B: P = RNE_bf16(exp2(s*c - m) / l) straight into TMEM (the A operand of the PV MMA)
-            if (j == 0) inv_l = 1.f / l;   // l >= 1: the row maximum contributes exp2(0)
+            if (j == 0) {   // the row sum: both halves' running sums at the final max (half 0 first)
+                const float lo = exchange(l);
+                l = hf == 0 ? l + lo : lo + l;
+                inv_l = 1.f / l;   // l >= 1: the row maximum contributes exp2(0)
+            }
             // the probabilities are computed (packed in place into sr[cb][0..15]) while PV_{j-1} still reads the
             // previous P from TMEM; only the stores wait for it
 #pragma unroll
-            for (int cb = 0; cb < 4; ++cb)
+            for (int cb = 0; cb < 2; ++cb)
 #pragma unroll
                 for (int e = 0; e < 16; ++e) {
                     const float p0 = fast_exp2(fmaf(__uint_as_float(sr[cb][2 * e]), scale_log2, -m)) * inv_l;
@@ -280,23 +304,23 @@ __global__ void __launch_bounds__(160, 1) attention_tc_kernel(const __grid_const
                 tc_fence_after();
             }
 #pragma unroll
-            for (int cb = 0; cb < 4; ++cb) {
+            for (int cb = 0; cb < 2; ++cb) {
                 uint32_t w[16];
 #pragma unroll
                 for (int e = 0; e < 16; ++e) w[e] = sr[cb][e];
-                tmem_st16(tP + lane_off + cb * 16, w);
+                tmem_st16(tP + lane_off + hf * 32 + cb * 16, w);
             }
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(p_full);
         }
-        // ---------------- epilogue: out = RNE_bf16(O)
+        // ---------------- epilogue: out = RNE_bf16(O), each half of the row's HD columns by one of the two threads
         mbar_wait(o_full, (n_kv - 1) & 1);
         tc_fence_after();
         __nv_bfloat16* o_row = out + ((size_t)t * gridDim.z + b) * ldo + h * HD;
 #pragma unroll
-        for (int c = 0; c < HD / 32; ++c) {
+        for (int c = hf * (HD / 64); c < (hf + 1) * (HD / 64); ++c) {
             uint32_t o[32];
             tmem_ld32_async(tO + lane_off + c * 32, o);
             tmem_wait_ld();
@@ -340,7 +364,7 @@ cudaError_t launch_tc(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int 
     if (e != cudaSuccess) return e;
     const dim3 grid((t1 - t0 + QT - 1) / QT, H, B);
     const float scale_log2 = score_scale * 1.4426950408889634f;
-    return launch_pdl(attention_tc_kernel<HD>, grid, 160, SM::kTotal, s, pdl, map, out, ldo, t0, t1, group, k_col0,
+    return launch_pdl(attention_tc_kernel<HD>, grid, 288, SM::kTotal, s, pdl, map, out, ldo, t0, t1, group, k_col0,
                       v_col0, scale_log2, dyn);
 }
 
