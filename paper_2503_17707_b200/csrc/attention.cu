@@ -23,6 +23,8 @@
 #include <cuda_bf16.h>
 #include <math_constants.h>
 
+#include <cstdlib>
+
 #include "kernels.hpp"
 #include "sm100.cuh"
 
@@ -46,21 +48,25 @@ __device__ __forceinline__ float tree8(const float (&r)[8]) {
     return ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
 }
 
-template <int HD>
+// TWO = false: one CTA per SM, K and V double-buffered, P in its own TMEM columns (S 128 | O HD | P 64 -> 512).
+// TWO = true : two CTAs per SM (the other CTA's work hides this one's load and handshake latency): K and V single-
+//              buffered (Q + K + V = 96 KB at hd 128), P written over the S columns it came from (S/P 128 | O HD
+//              -> 256 TMEM columns per CTA), so S_{i+1} of pass B waits for PV_i.
+template <int HD, bool TWO>
 struct AttnSmem {
-    static constexpr int kQ = HD / 64 * kAtom, kK = kQ, kV = kQ;   // K and V double-buffered; P lives in TMEM
-    static constexpr int offQ = 0, offK = offQ + kQ, offV = offK + 2 * kK, offBar = offV + 2 * kV;
+    static constexpr int kQ = HD / 64 * kAtom, kK = kQ, kV = kQ;
+    static constexpr int NBUF = TWO ? 1 : 2;
+    static constexpr int offQ = 0, offK = offQ + kQ, offV = offK + NBUF * kK, offBar = offV + NBUF * kV;
     static constexpr int offX = offBar + 128;   // half-row exchange: [2 halves][128 rows] float
-    // TMEM: S [0, 128) fp32, O [128, 128 + HD) fp32, P [128 + HD, 192 + HD) bf16 pairs (A operand of PV)
-    static constexpr uint32_t kTmemCols = HD == 64 ? 256 : 512;
+    static constexpr uint32_t kTmemCols = TWO || HD == 64 ? 256 : 512;
     static constexpr int kTotal = offX + 2 * 128 * 4 + 1024;
 };
 
-template <int HD>
-__global__ void __launch_bounds__(288, 1) attention_tc_kernel(const __grid_constant__ CUtensorMap map, __nv_bfloat16* __restrict__ out,
+template <int HD, bool TWO>
+__global__ void __launch_bounds__(288, TWO ? 2 : 1) attention_tc_kernel(const __grid_constant__ CUtensorMap map, __nv_bfloat16* __restrict__ out,
                                                         int ldo, int t0, int t1, int group, int k_col0, int v_col0,
                                                         float scale_log2, const int* dyn) {
-    using SM = AttnSmem<HD>;
+    using SM = AttnSmem<HD, TWO>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *sQ = smem + SM::offQ, *sK = smem + SM::offK, *sV = smem + SM::offV;
@@ -100,7 +106,11 @@ __global__ void __launch_bounds__(288, 1) attention_tc_kernel(const __grid_const
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t tS = tmem, tO = tmem + 128, tP = tmem + 128 + HD;
+    const uint32_t tS = tmem, tO = tmem + 128, tP = TWO ? tmem : tmem + 128 + HD;
+    // packed P of key half hf (keys hf*64 .. hf*64+63, 32 columns) starts at tP + hf * kPHalf: with P written over S
+    // (TWO) each half writes into ITS OWN S columns [hf*64, hf*64+32), never into columns its partner thread may
+    // not have read yet
+    constexpr uint32_t kPHalf = TWO ? 64 : 32;
     pdl_wait();   // q/k/v are the previous kernel's output
 
     // Two passes over the key tiles, so the probabilities are rounded to bf16 AFTER normalisation, exactly where the
@@ -123,11 +133,12 @@ __global__ void __launch_bounds__(288, 1) attention_tc_kernel(const __grid_const
             auto kv_of = [&](int i) { return single ? 0 : (i < n_kv ? i : i - n_kv); };
             mbar_arrive_expect_tx(q_full, SM::kQ);
             load_rows(sQ, q_full, h * HD, q0);
-            for (int i = 0; i < 2 && i < NI; ++i) {   // K of iterations 0 and 1
+            constexpr int NB = SM::NBUF;
+            for (int i = 0; i < NB && i < NI; ++i) {   // K of the first iteration(s)
                 mbar_arrive_expect_tx(&k_full[i], SM::kK);
                 load_rows(sK + i * SM::kK, &k_full[i], k_col0 + kvh * HD, kv_of(i) * KT);
             }
-            for (int j = 0; j < 2 && j < n_kv; ++j) {   // V_0, V_1 (read in pass B)
+            for (int j = 0; j < NB && j < n_kv; ++j) {   // V of the first pass-B iteration(s)
                 mbar_arrive_expect_tx(&v_full[j], SM::kV);
                 load_rows(sV + j * SM::kV, &v_full[j], v_col0 + kvh * HD, j * KT);
             }
@@ -135,9 +146,10 @@ __global__ void __launch_bounds__(288, 1) attention_tc_kernel(const __grid_const
             constexpr uint32_t idO = idesc_bf16_f32(128, HD, 0, 1);
             mbar_wait(q_full, 0);
             auto issue_S = [&](int i) {   // S = Q K^T into the (single) S columns
-                mbar_wait(&k_full[i & 1], (i >> 1) & 1);
+                const int kb = i % NB;
+                mbar_wait(&k_full[kb], (i / NB) & 1);
                 tc_fence_after();
-                const uint32_t kbase = smem_u32(sK + (i & 1) * SM::kK);
+                const uint32_t kbase = smem_u32(sK + kb * SM::kK);
 #pragma unroll
                 for (int kk = 0; kk < HD / 16; ++kk) {
                     const uint32_t off = (kk >> 2) * kBox + (kk & 3) * 32;
@@ -149,21 +161,23 @@ __global__ void __launch_bounds__(288, 1) attention_tc_kernel(const __grid_const
             issue_S(0);
             for (int i = 0; i < NI; ++i) {
                 const uint32_t ph = i & 1;
-                // ---- S_i done: its K buffer takes the K of iteration i + 2
+                // ---- S_i done: its K buffer takes the K of iteration i + NB
                 mbar_wait(s_full, ph);
-                if (i + 2 < NI) {
-                    mbar_arrive_expect_tx(&k_full[i & 1], SM::kK);
-                    load_rows(sK + (i & 1) * SM::kK, &k_full[i & 1], k_col0 + kvh * HD, kv_of(i + 2) * KT);
+                if (i + NB < NI) {
+                    const int kb = i % NB;
+                    mbar_arrive_expect_tx(&k_full[kb], SM::kK);
+                    load_rows(sK + kb * SM::kK, &k_full[kb], k_col0 + kvh * HD, kv_of(i + NB) * KT);
                 }
-                // ---- S_{i+1} as soon as the softmax has read S_i out of TMEM
+                const bool pass_a = i < n_kv && !single;
+                // ---- S_{i+1} as soon as the softmax has read S_i out of TMEM (pass A, or P in its own columns)
                 if (i + 1 < NI) {
                     mbar_wait(s_free, ph);
-                    issue_S(i + 1);
+                    if (pass_a || !TWO) issue_S(i + 1);
                 }
-                if (i < n_kv && !single) continue;
+                if (pass_a) continue;
                 const int j = single ? 0 : i - n_kv;
-                // ---- V_{j+1} into the buffer PV_{j-1} has finished reading
-                if (j >= 1 && j + 1 < n_kv) {
+                // ---- V_{j+NB} into the buffer PV_{j+NB-2} has finished reading (double-buffered V)
+                if (!TWO && j >= 1 && j + 1 < n_kv) {
                     mbar_wait(o_full, (j - 1) & 1);
                     const int vb = (j + 1) & 1;
                     mbar_arrive_expect_tx(&v_full[vb], SM::kV);
@@ -171,17 +185,25 @@ __global__ void __launch_bounds__(288, 1) attention_tc_kernel(const __grid_const
                 }
                 // ---- O += P_j V_j
                 mbar_wait(p_full, j & 1);
-                mbar_wait(&v_full[j & 1], (j >> 1) & 1);
+                mbar_wait(&v_full[j % NB], (j / NB) & 1);
                 tc_fence_after();
-                const uint32_t vbase = smem_u32(sV + (j & 1) * SM::kV);
+                const uint32_t vbase = smem_u32(sV + (j % NB) * SM::kV);
 #pragma unroll
                 for (int kk = 0; kk < KT / 16; ++kk) {
                     // A = P from TMEM: 16 keys = 8 packed columns. B = V tile [128 keys x hd], hd contiguous
                     // (MN-major): 64-col boxes kBox apart (LBO), 8-key groups 1024 B apart (SBO); 16 keys = 2048 B.
                     const uint64_t bd = smem_desc(vbase + kk * 2048, kBox, 1024, kSw128);
-                    umma_bf16_ts(tO, tP + kk * 8, bd, idO, (j > 0 || kk > 0) ? 1u : 0u);
+                    umma_bf16_ts(tO, tP + (kk >> 2) * kPHalf + (kk & 3) * 8, bd, idO, (j > 0 || kk > 0) ? 1u : 0u);
                 }
                 umma_commit(o_full);
+                if (TWO && i + 1 < NI) {   // P_j lives in S's columns and V_j in the only V buffer: both free after PV_j
+                    mbar_wait(o_full, j & 1);
+                    if (j + 1 < n_kv) {
+                        mbar_arrive_expect_tx(&v_full[0], SM::kV);
+                        load_rows(sV, &v_full[0], v_col0 + kvh * HD, (j + 1) * KT);
+                    }
+                    issue_S(i + 1);
+                }
             }
         }
         __syncwarp();
@@ -261,7 +283,7 @@ __global__ void __launch_bounds__(288, 1) attention_tc_kernel(const __grid_const
                     for (int e = 0; e < 16; ++e)
                         w[e] = bf16x2_bits(__uint_as_float(sr[cb][2 * e]) * inv_l,
                                            __uint_as_float(sr[cb][2 * e + 1]) * inv_l);
-                    tmem_st16(tP + lane_off + hf * 32 + cb * 16, w);
+                    tmem_st16(tP + lane_off + hf * kPHalf + cb * 16, w);
                 }
                 tmem_wait_st();
                 tc_fence_before();
@@ -308,7 +330,7 @@ __global__ void __launch_bounds__(288, 1) attention_tc_kernel(const __grid_const
                 uint32_t w[16];
 #pragma unroll
                 for (int e = 0; e < 16; ++e) w[e] = sr[cb][e];
-                tmem_st16(tP + lane_off + hf * 32 + cb * 16, w);
+                tmem_st16(tP + lane_off + hf * kPHalf + cb * 16, w);
             }
             tmem_wait_st();
             tc_fence_before();
@@ -346,7 +368,7 @@ __global__ void __launch_bounds__(288, 1) attention_tc_kernel(const __grid_const
     }
 }
 
-template <int HD>
+template <int HD, bool TWO>
 cudaError_t launch_tc(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int ldo, int t0, int t1, int B, int H,
                       int group, int k_col0, int v_col0, float score_scale, cudaStream_t s, bool pdl,
                       const int* dyn, int t_extent) {
@@ -359,12 +381,12 @@ cudaError_t launch_tc(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int 
     CUtensorMap map;
     char err[256];
     if (!make_map_bf16_3d(&map, qkv, dims, strides, box, 128, err, sizeof err)) return cudaErrorInvalidValue;
-    using SM = AttnSmem<HD>;
-    cudaError_t e = smem_attr_once<attention_tc_kernel<HD>>(SM::kTotal);
+    using SM = AttnSmem<HD, TWO>;
+    cudaError_t e = smem_attr_once<attention_tc_kernel<HD, TWO>>(SM::kTotal);
     if (e != cudaSuccess) return e;
     const dim3 grid((t1 - t0 + QT - 1) / QT, H, B);
     const float scale_log2 = score_scale * 1.4426950408889634f;
-    return launch_pdl(attention_tc_kernel<HD>, grid, 288, SM::kTotal, s, pdl, map, out, ldo, t0, t1, group, k_col0,
+    return launch_pdl(attention_tc_kernel<HD, TWO>, grid, 288, SM::kTotal, s, pdl, map, out, ldo, t0, t1, group, k_col0,
                       v_col0, scale_log2, dyn);
 }
 
@@ -372,8 +394,10 @@ cudaError_t launch_tc(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int 
 
 cudaError_t warm_attention_kernels() {
     cudaFuncAttributes a;
-    cudaError_t e = cudaFuncGetAttributes(&a, attention_tc_kernel<64>);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, attention_tc_kernel<128>);
+    cudaError_t e = cudaFuncGetAttributes(&a, attention_tc_kernel<64, false>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, attention_tc_kernel<128, false>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, attention_tc_kernel<64, true>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, attention_tc_kernel<128, true>);
     return e;
 }
 
@@ -384,11 +408,18 @@ cudaError_t launch_attention(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* ou
     const bool tma_ok = (ld % 8) == 0 && (reinterpret_cast<uintptr_t>(qkv) & 15) == 0 && (ldo % 8) == 0 &&
                         (k_col0 % 8) == 0 && (v_col0 % 8) == 0;
     const int group = n_heads / n_kv_heads;
+    static const bool two = !getenv("PB_ATTN_ONE") ;   // two CTAs per SM unless PB_ATTN_ONE (A/B measurement)
+    if (tma_ok && hd == 64 && two)
+        return launch_tc<64, true>(qkv, ld, out, ldo, t0, t1, B, n_heads, group, k_col0, v_col0, score_scale, s, pdl,
+                                   dyn, t_extent);
+    if (tma_ok && hd == 128 && two)
+        return launch_tc<128, true>(qkv, ld, out, ldo, t0, t1, B, n_heads, group, k_col0, v_col0, score_scale, s, pdl,
+                                    dyn, t_extent);
     if (tma_ok && hd == 64)
-        return launch_tc<64>(qkv, ld, out, ldo, t0, t1, B, n_heads, group, k_col0, v_col0, score_scale, s, pdl, dyn,
+        return launch_tc<64, false>(qkv, ld, out, ldo, t0, t1, B, n_heads, group, k_col0, v_col0, score_scale, s, pdl, dyn,
                              t_extent);
     if (tma_ok && hd == 128)
-        return launch_tc<128>(qkv, ld, out, ldo, t0, t1, B, n_heads, group, k_col0, v_col0, score_scale, s, pdl, dyn,
+        return launch_tc<128, false>(qkv, ld, out, ldo, t0, t1, B, n_heads, group, k_col0, v_col0, score_scale, s, pdl, dyn,
                               t_extent);
     if (dyn) return cudaErrorNotSupported;   // decode graphs run on the tensor-core kernel only (hd 64 / 128)
     return launch_attention_simt(qkv, ld, out, ldo, t0, t1, B, n_heads, n_kv_heads, hd, k_col0, v_col0, score_scale,

@@ -325,7 +325,8 @@ __global__ void __launch_bounds__(128, 1) gemm_kernel(const __grid_constant__ CU
             }
         } else {  // EPI_RESID: h += acc + bias (fp32)
             float* h = reinterpret_cast<float*>(a.out) + (size_t)row * a.ldo + n;
-            if (nv == 4) {
+            // 16-byte vectors where aligned (every residual stream; a vocab slice of the logits may start anywhere)
+            if (nv == 4 && (reinterpret_cast<uintptr_t>(h) & 15) == 0) {
                 float4 x = *reinterpret_cast<float4*>(h);
                 x.x += v[0];
                 x.y += v[1];
@@ -912,6 +913,33 @@ cudaError_t warm_gemm_kernels() {
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
+}
+
+// Vocabulary logits of a large batch on the tensor cores: logits[b, v0:v1] = y[b] . E[v0:v1]^T (fp32), as the
+// split-K kernel's fp32 epilogue over a zeroed slice. S = 1 (each output's K sum in one CTA, in k order), so a
+// vocab slice of any width gives the same bits as the whole head (pipelined equals sequential).
+cudaError_t launch_logits_tc(const __nv_bfloat16* y, int B, int d, const __nv_bfloat16* E, int v0, int v1, float* logits,
+                             int ldl, cudaStream_t s) {
+    if (v1 <= v0 || B <= 0) return cudaSuccess;
+    CUtensorMap mx, mw;
+    char err[256];
+    if (!make_map_bf16(&mx, y, B, d, d, 128, 64, 128, err, sizeof err) ||
+        !make_map_bf16(&mw, E + (size_t)v0 * d, v1 - v0, d, d, 128, 64, 128, err, sizeof err))
+        return cudaErrorInvalidValue;
+    cudaError_t e = cudaMemset2DAsync(logits + v0, (size_t)ldl * 4, 0, (size_t)(v1 - v0) * 4, B, s);
+    if (e != cudaSuccess) return e;
+    GemmArgs a{};
+    a.M_begin = 0;
+    a.M_end = B;
+    a.N = v1 - v0;
+    a.K = d;
+    a.epi = EPI_RESID;
+    a.scale = 1.f;
+    a.out = logits + v0;
+    a.ldo = ldl;
+    a.split_k = 1;
+    a.M_total = B;
+    return launch_gemm(mx, mw, a, s);
 }
 
 cudaError_t launch_gemm(const CUtensorMap& mapX, const CUtensorMap& mapW, const GemmArgs& a, cudaStream_t s) {

@@ -558,6 +558,9 @@ cudaError_t launch_logits(const __nv_bfloat16* y, int B, int d, const __nv_bfloa
                           int ldl, cudaStream_t s, bool pdl) {
     if (v1 <= v0) return cudaSuccess;
     if (d % 8) return cudaErrorInvalidValue;
+    // a large batch (the paper's 64 x 64 workload) is a GEMM: the tensor cores read the head once
+    // (C2p: 1.3 ms on the CUDA cores, 8 sequences per pass)
+    if (B >= 16 && d % 64 == 0) return launch_logits_tc(y, B, d, E, v0, v1, logits, ldl, s);
     // up to 8 sequences per launch (the warp's accumulators); larger batches (the paper's 64 x 64 workload)
     // stream the head once per group of 8
     for (int b0 = 0; b0 < B; b0 += 8) {

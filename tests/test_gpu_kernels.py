@@ -311,6 +311,30 @@ def test_argmax_large_vocab_ties_across_slices():
     assert nan.item() == 1
 
 
+@pytest.mark.parametrize("Bsz,V", [(16, 1000), (64, 5000), (100, 777)])
+def test_logits_large_batch_tensor_cores(Bsz, V):
+    """B >= 16 takes the tcgen05 GEMM (S = 1): within fp32-accumulation error of the exact product, and vocab
+    slices of any width give the same bits as the whole head (pipelined equals sequential)."""
+    need_gpu()
+    rng = np.random.default_rng(Bsz + V)
+    d = 1024
+    y = rbits(rng, (Bsz, d), 1.0)
+    E = rbits(rng, (V, d), 0.035)
+    Ed, yd = dev_bf16(E), dev_bf16(y)
+    whole = torch.full((Bsz, V), float("nan"), device="cuda")
+    B.pb_op_logits(ptr(yd), Bsz, d, ptr(Ed), 0, V, ptr(whole), V, stream())
+    sliced = torch.full((Bsz, V), float("nan"), device="cuda")
+    cut = V // 3 + 5
+    B.pb_op_logits(ptr(yd), Bsz, d, ptr(Ed), cut, V, ptr(sliced), V, stream())
+    B.pb_op_logits(ptr(yd), Bsz, d, ptr(Ed), 0, cut, ptr(sliced), V, stream())
+    torch.cuda.synchronize()
+    ref = bf16_bits_to_f64(y) @ bf16_bits_to_f64(E).T
+    mag = np.abs(bf16_bits_to_f64(y)) @ np.abs(bf16_bits_to_f64(E)).T
+    got = whole.cpu().numpy().astype(np.float64)
+    assert np.all(np.abs(got - ref) <= 4 * np.sqrt(d) * 2.0 ** -24 * mag + 1e-30)
+    assert np.array_equal(whole.cpu().numpy().view(np.uint32), sliced.cpu().numpy().view(np.uint32))
+
+
 def test_logits_argmax_embed():
     need_gpu()
     rng = np.random.default_rng(9)
