@@ -225,6 +225,25 @@ def test_attention(T, Bsz, H, KVH, hd, t0, t1):
             assert np.all(e2 <= 2 * bf16_ulp(con) + 2.0 ** -6 * np.abs(v).max() + 1e-6), e2.max()
 
 
+@pytest.mark.parametrize("T,H,KVH,hd", [(1024, 40, 40, 128), (640, 16, 4, 64), (128, 32, 32, 64)])
+def test_attention_deterministic_under_load(T, H, KVH, hd):
+    """Two CTAs per SM share the tensor pipe and TMEM, and P is written over S in TMEM: repeated launches (with
+    another launch in flight) must give the same bits every time — a race between the two softmax threads of a row,
+    or between a CTA's PV and its next QK^T, would show up as run-to-run differences."""
+    need_gpu()
+    rng = np.random.default_rng(T + H)
+    qd, kvd = H * hd, KVH * hd
+    ld = qd + 2 * kvd
+    qkv = dev_bf16(f64_to_bf16_bits(rng.standard_normal((T, ld)) * 1.3))
+    outs = [torch.zeros((T, qd), dtype=torch.bfloat16, device="cuda") for _ in range(6)]
+    for o in outs:
+        B.pb_op_attention(ptr(qkv), ld, ptr(o), qd, 0, T, 1, H, KVH, hd, qd, qd + kvd, hd ** -0.5, stream())
+    torch.cuda.synchronize()
+    ref = host_bits(outs[0])
+    for o in outs[1:]:
+        assert np.array_equal(host_bits(o), ref)
+
+
 @pytest.mark.parametrize("M,K,H,KVH,hd,B_,row0,split", [
     (2048, 1024, 8, 2, 128, 1, 0, 0),      # persistent 256-column tiles (C5a-like GQA), rope + plain v columns
     (600, 512, 4, 4, 128, 2, 0, 0),        # persistent, 2 sequences token-major, ragged last row tile
