@@ -400,7 +400,6 @@ cudaError_t launch_epi(const CUtensorMap& mapX, const CUtensorMap& mapW, const G
     switch (S) {
         case 1: return launch_es<EPI, 1>(mapX, mapW, a, s);
         case 2: return launch_es<EPI, 2>(mapX, mapW, a, s);
-        case 3: return launch_es<EPI, 3>(mapX, mapW, a, s);
         case 4: return launch_es<EPI, 4>(mapX, mapW, a, s);
         case 8: return launch_es<EPI, 8>(mapX, mapW, a, s);
     }

@@ -76,7 +76,7 @@ extern "C" pb_status pb_op_gemm_split(const void* X, int32_t x_rows, int32_t m_b
                                       const void* W, int32_t n_rows, int32_t N, int32_t epi, const void* bias,
                                       int32_t relu, float scale, int32_t scale_cols, void* out, int32_t ldo,
                                       int32_t split_k, void* stream) {
-    if (split_k < 0 || split_k > 8 || (split_k != 3 && (split_k & (split_k - 1))) || (split_k > 0 && split_k > (K + 63) / 64))
+    if (split_k < 0 || split_k > 8 || (split_k & (split_k - 1)) || (split_k > 0 && split_k > (K + 63) / 64))
         return fail(PB_EINVAL, "pb_op_gemm_split: split_k %d out of range", split_k);
     return gemm_op(X, x_rows, m_begin, m_end, K, W, n_rows, N, epi, bias, relu, scale, scale_cols, out, ldo, split_k,
                    stream);

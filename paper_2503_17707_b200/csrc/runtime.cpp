@@ -853,7 +853,7 @@ pb_status run_layer_f32(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B,
                         int adapter);
 
 pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, bool first_chunk, int row_base,
-                    int adapter) {
+                    int adapter, int parts = 7) {
     const pb_plan* p = c->plan;
     if (p->f32()) return run_layer_f32(c, l, r0, r1, ta, tb, B, first_chunk, row_base, adapter);
     const auto& m = p->model;
@@ -914,11 +914,17 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, boo
         return e;
     };
     auto need = [&](const char* sfx) -> cudaError_t { return first_chunk ? wait_tensor(c, l, sfx) : cudaSuccess; };
-    // --- attention block
-    CU(need(opt ? "ln1_b" : "ln1_g"));
-    CU(norm("ln1_g", "ln1_b"));
+    // --- attention block. parts: 1 = norm 1, 2 = QKV + attention, 4 = O, norm 2, MLP (a multi-adapter batch runs
+    // 1 and 4 once over every sequence's rows and 2 per sequence with its adapter's weights)
+    if (parts & 1) {
+        CU(need(opt ? "ln1_b" : "ln1_g"));
+        CU(norm("ln1_g", "ln1_b"));
+        ++c->n_launches;
+    }
+    GemmArgs a{};
+    if (parts & 2) {
     CU(need(opt ? "qkv_b" : "qkv"));
-    GemmArgs a = G(r0, qdim, d, EPI_BF16, opt ? wt(c, l, "qkv_b") : nullptr, 0, opt ? 1.0f / sqrtf((float)hd) : 1.0f,
+    a = G(r0, qdim, d, EPI_BF16, opt ? wt(c, l, "qkv_b") : nullptr, 0, opt ? 1.0f / sqrtf((float)hd) : 1.0f,
                    opt ? d : 0, qkv, qdim);
     if (!opt) {   // Llama: RoPE on the fp32 accumulator inside the QKV epilogue, one rounding (storage contract)
         a.rope = reinterpret_cast<const float2*>(c->ws + L.rope);
@@ -937,6 +943,9 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, boo
         const double pairs = (double)B * ((double)tb * (tb + 1) / 2 - (double)ta * (ta + 1) / 2);
         prof_end(c, pi, s, 4.0 * pairs * H * hd, 2.0 * rows * qd * 2 + 2.0 * B * tb * 2 * kvd);
     }
+    c->n_launches += 2;
+    }
+    if (!(parts & 4)) return PB_OK;
     CU(need(opt ? "o_b" : "o"));
     a = G(r0, d, qd, EPI_RESID, opt ? wt(c, l, "o_b") : nullptr, 0, 1.f, 0, h, d);
     CU(gemm(c->map_attn, lm.o, a, d, attn, qd, 1));
@@ -958,7 +967,7 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, boo
         a = G(r0, d, f, EPI_RESID, nullptr, 0, 1.f, 0, h, d);
         CU(gemm(c->map_mlp, lm.down, a, d, mlp, f, 3));
     }
-    c->n_launches += 7;   // norm, qkv (+ RoPE for Llama), attention, o, norm, fc1|gate_up, fc2|down
+    c->n_launches += 4;   // o, norm, fc1|gate_up, fc2|down
     return PB_OK;
 }
 
@@ -1081,7 +1090,7 @@ struct Budget {
     }
 };
 
-enum ItemKind { I_PROLOGUE, I_EMBED, I_WAITACT, I_LAYER, I_PUSH, I_FINAL, I_HEAD, I_ARGMAX, I_DONE };
+enum ItemKind { I_PROLOGUE, I_EMBED, I_WAITACT, I_LAYER, I_PUSH, I_FINAL, I_HEAD, I_ARGMAX, I_DONE, I_LAYER_ALL };
 struct Item {
     int kind, mb, j, l;
     std::vector<int32_t> prereq;   // tensors whose readiness-word writer must already be issued
@@ -1290,6 +1299,24 @@ pb_status issue_recv(Issuer& I, size_t ri) {
     return PB_OK;
 }
 
+// Multi-adapter microbatches (PB_MERGE_ALL: each sequence on its adapter's out-of-place copies) at the last stage:
+// when no adapter of the batch touches layer l's O / MLP weights (every microbatch's maps point at the same base
+// tensors), norm 1, O, norm 2 and the MLP of all sequences run as ONE launch each over all rows (weights read once
+// instead of once per sequence; the M_total that picks the kernel and the split stays one sequence's rows, so the
+// sums are the same as per sequence); QKV + attention stay per sequence. PB_NO_MB_BATCH=1 disables it.
+static bool shared_weight_batch(const Issuer& I, int l) {
+    const pb_ctx* c = I.c;
+    static const bool off = getenv("PB_NO_MB_BATCH") != nullptr;
+    if (off || !I.mb_mode || I.k != 1 || I.n_mb < 2 || I.dec_t >= 0 || c->plan->f32() || c->dyn_pos) return false;
+    for (int mb = 0; mb < I.n_mb; ++mb) {
+        const int a = c->seq_adapter[mb];
+        if (a < 0) return false;
+        for (int wi = 1; wi < 4; ++wi)
+            if (c->lmaps_ad[a][l].w[wi] != c->lmaps[l].w[wi]) return false;
+    }
+    return true;
+}
+
 void build_items(Issuer& I) {
     pb_ctx* c = I.c;
     const pb_plan* p = c->plan;
@@ -1329,12 +1356,19 @@ void build_items(Issuer& I) {
     if (last && (I.n_mb > 1 || I.k > 1)) {
         // Last stage (no downstream consumer): layer-major, so every microbatch / prompt chunk advances as each
         // layer lands instead of all but the first waiting for the whole stage.
-        for (int l = stage.first; l < stage.second; ++l)
+        for (int l = stage.first; l < stage.second; ++l) {
+            if (shared_weight_batch(I, l)) {   // the sequences' shared projections as one GEMM each
+                if (l == stage.first)
+                    for (int mb = 0; mb < I.n_mb; ++mb) head_item(mb, 0);
+                add(I_LAYER_ALL, 0, 0, l, layer_pre(l));
+                continue;
+            }
             for (int mb = 0; mb < I.n_mb; ++mb)
                 for (int j = 0; j < I.k; ++j) {
                     if (l == stage.first) head_item(mb, j);
                     add(I_LAYER, mb, j, l, mb == 0 && j == 0 ? layer_pre(l) : std::vector<int32_t>{});
                 }
+        }
     } else {
         // Intermediate stage: chunk-major, so chunk 0 reaches the next stage as early as possible.
         for (int mb = 0; mb < I.n_mb; ++mb)
@@ -1360,6 +1394,7 @@ long item_ops(Issuer& I, const Item& it) {
     const int po = prof_ops(I.c);
     switch (it.kind) {
         case I_LAYER: return 16 + 8 * po;
+        case I_LAYER_ALL: return (16 + 8 * po) * (I.n_mb + 1);
         case I_EMBED: return 8 + po;
         default: return 8 + po;
     }
@@ -1476,6 +1511,18 @@ pb_status issue_item(Issuer& I, const Item& it, bool late_tokens) {
                                      row_base, adapter);
             if (st) return st;
             if (it.l == stage.second - 1 && it.mb == I.n_mb - 1 && j == I.k - 1) CU(record_ev(c, c->stage_end, s));
+            break;
+        }
+        case I_LAYER_ALL: {   // shared_weight_batch(): sequence mb occupies rows [mb*T, (mb+1)*T)
+            const auto stage = rep ? std::make_pair(0, m.n_layers) : p->stages[g];
+            const bool first_chunk = !I.replay;
+            if (it.l == stage.first) CU(record_ev(c, c->stage_begin, s));
+            pb_status st = run_layer(c, it.l, 0, I.n_mb * T, 0, T, 1, first_chunk, 0, -1, 1);
+            for (int mb = 0; mb < I.n_mb && st == PB_OK; ++mb)
+                st = run_layer(c, it.l, mb * T, (mb + 1) * T, 0, T, 1, first_chunk, mb * T, c->seq_adapter[mb], 2);
+            if (st == PB_OK) st = run_layer(c, it.l, 0, I.n_mb * T, 0, T, 1, first_chunk, 0, -1, 4);
+            if (st) return st;
+            if (it.l == stage.second - 1) CU(record_ev(c, c->stage_end, s));
             break;
         }
         case I_PUSH:

@@ -217,13 +217,14 @@ def test_replay_bitwise_equals_cold_start():
         assert np.array_equal(res[0][1].view(np.uint32), l1.view(np.uint32)) and np.array_equal(res[0][0], t1)
 
 
-@pytest.mark.parametrize("model", [TINY_OPT, TINY_LLAMA], ids=["opt", "llama"])
-def test_multi_adapter_batch(model):
+@pytest.mark.parametrize("model,tg", [(TINY_OPT, ("q", "v")), (TINY_LLAMA, ("q", "v", "gate")), (TINY_LLAMA, ("q", "v"))],
+                         ids=["opt", "llama-gate", "llama-qv"])
+def test_multi_adapter_batch(model, tg):
     """C3-style: several adapters share the base; each sequence uses its own adapter (out-of-place merged
     copies, one pipeline microbatch per sequence). Checked per sequence against the oracle, and bit-identical
-    between 1 and 2 stages."""
+    between 1 and 2 stages. With q / v adapters only, one stage runs the sequences' shared projections (O, MLP) as
+    one launch over all rows while two stages with 2 prompt chunks run them per sequence — the same bits."""
     need_gpu()
-    tg = ("q", "v") if model.arch == "opt" else ("q", "v", "gate")
     ads = tuple(lora(8, tg) for _ in range(3))
     toks = synth.tokens(4, 20, model.vocab)
     aos = [2, 0, 1, 2]
