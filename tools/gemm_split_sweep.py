@@ -48,7 +48,7 @@ def bench(M, K, N, epi, split, reps=30):
 
 for name, K, N, epi in SHAPES:
     res = {}
-    for S in (0, 2, 3, 4, 8):
+    for S in (0, 2, 4, 8):
         if S and K // 64 < 2 * S:
             continue
         us, gbs = bench(128, K, N, epi, S)
