@@ -65,7 +65,7 @@ struct AttnSmem {
 template <int HD, bool TWO>
 __global__ void __launch_bounds__(288, TWO ? 2 : 1) attention_tc_kernel(const __grid_constant__ CUtensorMap map, __nv_bfloat16* __restrict__ out,
                                                         int ldo, int t0, int t1, int group, int k_col0, int v_col0,
-                                                        float scale_log2, const int* dyn) {
+                                                        float scale_log2, const int* dyn, int seq_stride) {
     using SM = AttnSmem<HD, TWO>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -128,7 +128,10 @@ __global__ void __launch_bounds__(288, TWO ? 2 : 1) attention_tc_kernel(const __
             constexpr int kBox = kAtom;   // bytes of one 64-col box
             auto load_rows = [&](uint8_t* dst, uint64_t* bar, int col, int t) {
 #pragma unroll
-                for (int a = 0; a < HD / 64; ++a) tma_load_3d(dst + a * kBox, &map, bar, col + a * 64, b, t);
+                for (int a = 0; a < HD / 64; ++a) {
+                    if (seq_stride) tma_load_3d(dst + a * kBox, &map, bar, col + a * 64, t, b);   // (col, t, b)
+                    else tma_load_3d(dst + a * kBox, &map, bar, col + a * 64, b, t);              // (col, b, t)
+                }
             };
             auto kv_of = [&](int i) { return single ? 0 : (i < n_kv ? i : i - n_kv); };
             mbar_arrive_expect_tx(q_full, SM::kQ);
@@ -340,7 +343,8 @@ __global__ void __launch_bounds__(288, TWO ? 2 : 1) attention_tc_kernel(const __
         // ---------------- epilogue: out = RNE_bf16(O), each half of the row's HD columns by one of the two threads
         mbar_wait(o_full, (n_kv - 1) & 1);
         tc_fence_after();
-        __nv_bfloat16* o_row = out + ((size_t)t * gridDim.z + b) * ldo + h * HD;
+        __nv_bfloat16* o_row =
+            out + (seq_stride ? (size_t)b * seq_stride + t : (size_t)t * gridDim.z + b) * ldo + h * HD;
 #pragma unroll
         for (int c = hf * (HD / 64); c < (hf + 1) * (HD / 64); ++c) {
             uint32_t o[32];
@@ -371,13 +375,18 @@ __global__ void __launch_bounds__(288, TWO ? 2 : 1) attention_tc_kernel(const __
 template <int HD, bool TWO>
 cudaError_t launch_tc(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int ldo, int t0, int t1, int B, int H,
                       int group, int k_col0, int v_col0, float score_scale, cudaStream_t s, bool pdl,
-                      const int* dyn, int t_extent) {
+                      const int* dyn, int t_extent, int seq_stride) {
     // 3-D view of the token-major rows: (col, sequence b, position t), t extent = t1 (keys >= t1 zero-filled);
     // a decode graph's positions are only known on the device: the view then spans t_extent positions and the
     // causal mask (key <= query) keeps later rows out.
-    const uint64_t dims[3] = {(uint64_t)ld, (uint64_t)B, (uint64_t)(dyn ? t_extent : t1)};
-    const uint64_t strides[2] = {(uint64_t)ld * 2, (uint64_t)ld * 2 * B};
-    const uint32_t box[3] = {64, 1, 128};
+    const uint64_t T_ext = (uint64_t)(dyn ? t_extent : t1);
+    const uint64_t dims_tm[3] = {(uint64_t)ld, (uint64_t)B, T_ext}, dims_sm[3] = {(uint64_t)ld, T_ext, (uint64_t)B};
+    const uint64_t str_tm[2] = {(uint64_t)ld * 2, (uint64_t)ld * 2 * B};
+    const uint64_t str_sm[2] = {(uint64_t)ld * 2, (uint64_t)ld * 2 * (uint64_t)seq_stride};
+    const uint32_t box_tm[3] = {64, 1, 128}, box_sm[3] = {64, 128, 1};
+    const uint64_t* dims = seq_stride ? dims_sm : dims_tm;
+    const uint64_t* strides = seq_stride ? str_sm : str_tm;
+    const uint32_t* box = seq_stride ? box_sm : box_tm;
     CUtensorMap map;
     char err[256];
     if (!make_map_bf16_3d(&map, qkv, dims, strides, box, 128, err, sizeof err)) return cudaErrorInvalidValue;
@@ -387,7 +396,7 @@ cudaError_t launch_tc(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int 
     const dim3 grid((t1 - t0 + QT - 1) / QT, H, B);
     const float scale_log2 = score_scale * 1.4426950408889634f;
     return launch_pdl(attention_tc_kernel<HD, TWO>, grid, 288, SM::kTotal, s, pdl, map, out, ldo, t0, t1, group, k_col0,
-                      v_col0, scale_log2, dyn);
+                      v_col0, scale_log2, dyn, seq_stride);
 }
 
 }  // namespace
@@ -403,7 +412,7 @@ cudaError_t warm_attention_kernels() {
 
 cudaError_t launch_attention(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int ldo, int t0, int t1, int B,
                              int n_heads, int n_kv_heads, int hd, int k_col0, int v_col0, float score_scale,
-                             cudaStream_t s, bool pdl, const int* dyn, int t_extent) {
+                             cudaStream_t s, bool pdl, const int* dyn, int t_extent, int seq_stride) {
     if (t1 <= t0) return cudaSuccess;
     const bool tma_ok = (ld % 8) == 0 && (reinterpret_cast<uintptr_t>(qkv) & 15) == 0 && (ldo % 8) == 0 &&
                         (k_col0 % 8) == 0 && (v_col0 % 8) == 0;
@@ -411,17 +420,17 @@ cudaError_t launch_attention(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* ou
     static const bool two = !getenv("PB_ATTN_ONE") ;   // two CTAs per SM unless PB_ATTN_ONE (A/B measurement)
     if (tma_ok && hd == 64 && two)
         return launch_tc<64, true>(qkv, ld, out, ldo, t0, t1, B, n_heads, group, k_col0, v_col0, score_scale, s, pdl,
-                                   dyn, t_extent);
+                                   dyn, t_extent, seq_stride);
     if (tma_ok && hd == 128 && two)
         return launch_tc<128, true>(qkv, ld, out, ldo, t0, t1, B, n_heads, group, k_col0, v_col0, score_scale, s, pdl,
-                                    dyn, t_extent);
+                                    dyn, t_extent, seq_stride);
     if (tma_ok && hd == 64)
         return launch_tc<64, false>(qkv, ld, out, ldo, t0, t1, B, n_heads, group, k_col0, v_col0, score_scale, s, pdl, dyn,
-                             t_extent);
+                                    t_extent, seq_stride);
     if (tma_ok && hd == 128)
         return launch_tc<128, false>(qkv, ld, out, ldo, t0, t1, B, n_heads, group, k_col0, v_col0, score_scale, s, pdl, dyn,
-                              t_extent);
-    if (dyn) return cudaErrorNotSupported;   // decode graphs run on the tensor-core kernel only (hd 64 / 128)
+                                     t_extent, seq_stride);
+    if (dyn || seq_stride) return cudaErrorNotSupported;   // decode graphs / sequence-major: tensor-core kernel only
     return launch_attention_simt(qkv, ld, out, ldo, t0, t1, B, n_heads, n_kv_heads, hd, k_col0, v_col0, score_scale,
                                  s);
 }

@@ -167,7 +167,10 @@ cudaError_t launch_rope(__nv_bfloat16* qkv, int ld, int r0, int r1, int B, int n
 // dyn (f3 decode graphs): positions shift by *dyn; t_extent then bounds the keys' TMA view (>= every t1 + *dyn).
 cudaError_t launch_attention(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int ldo, int t0, int t1, int B,
                              int n_heads, int n_kv_heads, int hd, int k_col0, int v_col0, float score_scale,
-                             cudaStream_t s, bool pdl = false, const int* dyn = nullptr, int t_extent = 0);
+                             cudaStream_t s, bool pdl = false, const int* dyn = nullptr, int t_extent = 0,
+                             int seq_stride = 0);
+// seq_stride > 0: sequence-major rows (sequence b at rows b * seq_stride + t: the multi-adapter microbatches, all of
+// them in one launch); 0: token-major rows t * B + b.
 cudaError_t launch_attention_simt(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int ldo, int t0, int t1,
                                   int B, int n_heads, int n_kv_heads, int hd, int k_col0, int v_col0,
                                   float score_scale, cudaStream_t s);

@@ -853,7 +853,7 @@ pb_status run_layer_f32(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B,
                         int adapter);
 
 pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, bool first_chunk, int row_base,
-                    int adapter, int parts = 7) {
+                    int adapter, int parts = 15) {
     const pb_plan* p = c->plan;
     if (p->f32()) return run_layer_f32(c, l, r0, r1, ta, tb, B, first_chunk, row_base, adapter);
     const auto& m = p->model;
@@ -914,8 +914,9 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, boo
         return e;
     };
     auto need = [&](const char* sfx) -> cudaError_t { return first_chunk ? wait_tensor(c, l, sfx) : cudaSuccess; };
-    // --- attention block. parts: 1 = norm 1, 2 = QKV + attention, 4 = O, norm 2, MLP (a multi-adapter batch runs
-    // 1 and 4 once over every sequence's rows and 2 per sequence with its adapter's weights)
+    // --- attention block. parts: 1 = norm 1, 2 = QKV, 8 = attention, 4 = O, norm 2, MLP (a multi-adapter batch runs 1
+    // and 4 once over every sequence's rows, 2 per sequence with its adapter's weights, and the attention of all
+    // sequences as one sequence-major launch)
     if (parts & 1) {
         CU(need(opt ? "ln1_b" : "ln1_g"));
         CU(norm("ln1_g", "ln1_b"));
@@ -934,7 +935,7 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, boo
         a.rope_B = B;
     }
     CU(gemm(c->map_x, lm.qkv, a, qdim, x, d, 0));
-    {
+    if (parts & 8) {
         const int pi = prof_begin(c, K_ATTN, s);
         CU(launch_attention(qkv + (size_t)row_base * qdim, qdim, attn + (size_t)row_base * qd, qd, ta, tb, B, H, KVH,
                             hd, qd, qd + kvd, opt ? 1.0f : 1.0f / sqrtf((float)hd), s, !c->profiling, c->dyn_pos,
@@ -943,7 +944,7 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, boo
         const double pairs = (double)B * ((double)tb * (tb + 1) / 2 - (double)ta * (ta + 1) / 2);
         prof_end(c, pi, s, 4.0 * pairs * H * hd, 2.0 * rows * qd * 2 + 2.0 * B * tb * 2 * kvd);
     }
-    c->n_launches += 2;
+    c->n_launches += (parts & 8) ? 2 : 1;
     }
     if (!(parts & 4)) return PB_OK;
     CU(need(opt ? "o_b" : "o"));
@@ -1520,7 +1521,19 @@ pb_status issue_item(Issuer& I, const Item& it, bool late_tokens) {
             pb_status st = run_layer(c, it.l, 0, I.n_mb * T, 0, T, 1, first_chunk, 0, -1, 1);
             for (int mb = 0; mb < I.n_mb && st == PB_OK; ++mb)
                 st = run_layer(c, it.l, mb * T, (mb + 1) * T, 0, T, 1, first_chunk, mb * T, c->seq_adapter[mb], 2);
-            if (st == PB_OK) st = run_layer(c, it.l, 0, I.n_mb * T, 0, T, 1, first_chunk, 0, -1, 4);
+            if (st) return st;
+            {   // the attention of every sequence in one launch (sequence-major rows b*T + t)
+                const int H = m.n_heads, KVH = m.n_kv_heads, qd = H * hd, kvd = KVH * hd, qdim = qkv_dim(p);
+                const __nv_bfloat16* qkv = reinterpret_cast<const __nv_bfloat16*>(c->ws + L.qkv + L.qkv_stride * it.l);
+                __nv_bfloat16* attn = reinterpret_cast<__nv_bfloat16*>(c->ws + L.attn);
+                const int pi = prof_begin(c, K_ATTN, s);
+                CU(launch_attention(qkv, qdim, attn, qd, 0, T, I.n_mb, H, KVH, hd, qd, qd + kvd,
+                                    opt ? 1.0f : 1.0f / sqrtf((float)hd), s, !c->profiling, nullptr, 0, T));
+                const double pairs = (double)I.n_mb * ((double)T * (T + 1) / 2);
+                prof_end(c, pi, s, 4.0 * pairs * H * hd, 2.0 * I.n_mb * T * qd * 2 + 2.0 * I.n_mb * T * 2 * kvd);
+                ++c->n_launches;
+            }
+            st = run_layer(c, it.l, 0, I.n_mb * T, 0, T, 1, first_chunk, 0, -1, 4);
             if (st) return st;
             if (it.l == stage.second - 1) CU(record_ev(c, c->stage_end, s));
             break;
