@@ -10,7 +10,9 @@ NVLink gather -> pipelined first-token prefill, until the first token is in host
   value      = TTFT ms, device clock (t0 event before the first DMA -> token D2H complete), max over ranks
   e2e        = the same cold start timed by the host around the public API call (RankEngine.cold_start),
                barrier -> token in host memory; bytes moved H2D/D2H per step stated
-  roofline   = dominant SM kernel class (per-launch CUDA events on its stream) vs MEASURED_PEAKS.json
+  roofline   = dominant SM kernel class vs MEASURED_PEAKS.json: the GEMM class timed back to back as one CUDA graph
+               of the step's projections (one event pair per replay; roofline.event_timed_frac = the same class
+               with a CUDA-event pair around every launch of the warm prefill), other classes per-launch events
   pcie_roofline = the path's own bound: S / sum of measured concurrent H2D GB/s (TTFT >= that)
 The CPU oracle (oracle/, the only other place it runs) is timed on rank 0 on a bounded sample.
 Inputs (2.6 GB of weights at C2) are far larger than the 126 MB L2; weights are re-invalidated each step.
@@ -317,13 +319,13 @@ def measure_h2d(nbytes=2 << 30, chunk=128 << 20):
     return best
 
 
-def ncu_traffic(kernel_class):
-    """dram bytes (read + write) per launch of the kernel class, from the committed ncu --set full capture."""
+def ncu_traffic(kernel_class, workload):
+    """dram bytes (read + write) per launch of the kernel class at this workload, from the committed ncu --set full
+    capture of that workload (None when there is none)."""
     p = os.path.join(HERE, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
-    d = json.load(open(p))
-    return d.get(kernel_class)
+    return json.load(open(p)).get(workload, {}).get(kernel_class)
 
 
 def load_peaks():
@@ -404,6 +406,75 @@ def time_merges(eng, plan, w, reps=3):
                       "one pb_op_merge_batch launch per layer (its adapted tensors), one CUDA graph, one event pair "
                       "per replay (mean of 3); not inside the cold start, where merges overlap the PCIe load on "
                       "their own stream"}
+
+
+def time_gemms(eng, plan, w, stage, reps=3):
+    """The GEMM class without per-launch timing events: the step's projections of this rank's stage (QKV, O, FC1 |
+    gate_up, FC2 | down of every layer, in prefill order, on the resident weights, M = B*T rows, the prefill's kernel
+    choice, epilogue and programmatic dependent launch) replayed back to back as one CUDA graph, one CUDA-event pair
+    per replay on the capture stream; the launch's activations come from scratch buffers (the values do not change
+    the work). A per-launch event pair in the warm replay adds ~5 us of event overhead per launch and cancels the
+    programmatic-dependent-launch overlap the prefill runs with; both numbers are reported.
+    Algorithmic work per launch as pb_kernel_stats counts it: 2*M*N_w*K flop; X + W + output bytes."""
+    import torch
+    from paper_2503_17707_b200 import _binding as B
+    m = w.model
+    opt = m.arch == "opt"
+    M = w.batch * w.seq
+    d, f, hd = m.d_model, m.d_ffn, m.head_dim
+    tens = {t[0]: t for t in plan.tensors()}
+    wp = eng.weights.data_ptr()
+    kmax = max(d, f)
+    X = torch.zeros((M, kmax), dtype=torch.bfloat16, device="cuda")
+    nmax = max(tens["L0.qkv"][1], tens["L0." + ("fc1" if opt else "gate_up")][1], d)
+    out = torch.zeros((M, nmax), dtype=torch.float32, device="cuda")
+    table = torch.zeros(max(1, w.seq * hd // 2 * 8), dtype=torch.uint8, device="cuda") if not opt else None
+    flops = nbytes = 0.0
+    launches = 0
+    g = torch.cuda.CUDAGraph()
+    torch.cuda.synchronize()
+    B.pb_op_debug_gemm(None, 1)   # programmatic dependent launch, as the prefill launches them
+    try:
+        with torch.cuda.graph(g):
+            cs = torch.cuda.current_stream().cuda_stream
+            for l in range(stage[0], stage[1]):
+                L = f"L{l}."
+                projs = [("qkv", 0), ("o", 1), ("fc1" if opt else "gate_up", 0 if opt else 2), ("fc2" if opt else "down", 1)]
+                for name, epi in projs:
+                    _, rows, K, _, _, off = tens[L + name]
+                    N = rows // 2 if epi == 2 else rows
+                    bias = wp + tens[L + name + "_b"][5] if opt and (L + name + "_b") in tens else 0
+                    if name == "qkv" and not opt:
+                        qd = m.n_heads * hd
+                        B.pb_op_gemm_rope(X.data_ptr(), M, 0, M, K, wp + off, N, out.data_ptr(), N,
+                                          qd + m.n_kv_heads * hd, hd, 0, w.batch, w.seq, m.rope_theta,
+                                          table.data_ptr(), 0, cs)
+                    else:
+                        B.pb_op_gemm(X.data_ptr(), M, 0, M, K, wp + off, rows, N, epi, bias,
+                                     1 if name == "fc1" else 0, 1.0 / hd ** 0.5 if name == "qkv" else 1.0,
+                                     d if name == "qkv" else 0, out.data_ptr(), N, cs)
+                    launches += 1
+                    flops += 2.0 * M * rows * K
+                    nbytes += 2.0 * M * K + 2.0 * rows * K + (8.0 if epi == 1 else 2.0) * M * N
+    finally:
+        B.pb_op_debug_gemm(None, 0)
+    g.replay()
+    torch.cuda.synchronize()
+    ms = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st = torch.cuda.current_stream()
+        e0.record(st)
+        g.replay()
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    t = statistics.mean(ms)
+    del g, X, out
+    torch.cuda.empty_cache()
+    return {"launches": launches, "avg_us": 1e3 * t / launches, "ms_per_step": t, "bytes": nbytes, "flops": flops,
+            "timing": "the stage's projections back to back as one CUDA graph (PDL, the prefill's kernels and "
+                      "shapes, resident weights), one event pair per replay (mean of 3)"}
 
 
 def self_launch(args):
@@ -584,6 +655,10 @@ def main():
         if rank == 0:
             out_tokens, out_logits = chk
     merge_k = time_merges(eng, plan, w) if (rank == 0 and not args.no_profile) else None
+    # rank 0's stage: contiguous balanced stages, remainder to the lower ranks
+    L_, base_, rem_ = w.model.n_layers, w.model.n_layers // world, w.model.n_layers % world
+    gemm_k = time_gemms(eng, plan, w, (0, base_ + (1 if rem_ > 0 else 0)) if world > 1 else (0, L_)) \
+        if (rank == 0 and not args.no_profile) else None
     # prefill tensor-core FLOPs per step over all ranks (each rank profiles its own stage) for T_comp
     my_flops = sum(kstats.get(k, {}).get("flops", 0.0) for k in ("gemm", "attention")) / max(1, args.steps)
     all_flops = allsum(my_flops)
@@ -615,6 +690,19 @@ def main():
                              "ms_per_step": merge_k["ms_per_step"], "achieved": ach, "unit": "GB/s",
                              "frac": ach / hbm, "tflops": merge_k["flops"] / t / 1e12, "gbs": ach,
                              "timing": merge_k["timing"]}
+        if gemm_k is not None and "gemm" in kern:
+            # the GEMM class timed back to back (no per-launch events): the same tensor-core / HBM choice as above
+            t = gemm_k["ms_per_step"] * 1e-3
+            gk = kern["gemm"]
+            tensor_bound = gemm_k["flops"] / (bf16_sus * 1e12) > gemm_k["bytes"] / (hbm * 1e9)
+            ach = gemm_k["flops"] / t / 1e12 if tensor_bound else gemm_k["bytes"] / t / 1e9
+            gk["event_timed"] = {"avg_us": gk["avg_us"], "achieved": gk["achieved"], "frac": gk["frac"],
+                                 "timing": "CUDA events per launch on the launching stream, warm re-run of the "
+                                           "step's prefill (pb_prefill_replay) after each timed cold start"}
+            gk.update({"avg_us": gemm_k["avg_us"], "ms_per_step": gemm_k["ms_per_step"] * gk["launches"] / max(1, gemm_k["launches"]),
+                       "achieved": ach, "unit": "TFLOP/s" if tensor_bound else "GB/s",
+                       "frac": ach / (bf16_sus if tensor_bound else hbm), "tflops": gemm_k["flops"] / t / 1e12,
+                       "gbs": gemm_k["bytes"] / t / 1e9, "timing": gemm_k["timing"]})
         # the dominant kernel of the step's critical path: the prefill classes (the merge overlaps the load)
         sm_kernels = {k: v for k, v in kern.items() if k not in ("signal", "merge")}
         if sm_kernels:
@@ -622,10 +710,12 @@ def main():
             d = sm_kernels[dom]
             roof = {"kernel": dom, "bound": "tensor" if d["unit"] == "TFLOP/s" else "hbm", "achieved": d["achieved"],
                     "peak": bf16_sus if d["unit"] == "TFLOP/s" else hbm, "unit": d["unit"], "frac": d["frac"],
-                    "traffic": ncu_traffic(dom),
+                    "traffic": ncu_traffic(dom, w.tag),
                     "peak_source": f"{peak_src} ({'sustained bf16' if d['unit'] == 'TFLOP/s' else 'HBM copy'})",
-                    "timing": "CUDA events per launch on the launching stream, warm re-run of the step's prefill "
-                              "(pb_prefill_replay) after each timed cold start"}
+                    "timing": d.get("timing", "CUDA events per launch on the launching stream, warm re-run of the "
+                                              "step's prefill (pb_prefill_replay) after each timed cold start")}
+            if "event_timed" in d:
+                roof["event_timed_frac"] = d["event_timed"]["frac"]
         t_pcie = S / (agg_h2d * 1e9) * 1e3
         load_gbs = S / (statistics.mean(load_done) * 1e-3) / 1e9
         # roofline = max(T_pcie, T_nv, T_comp). T_nv: every GPU ingests (N-1)/N of S over NVLink

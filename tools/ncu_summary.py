@@ -69,7 +69,7 @@ def launches(src, dst):
     print("\n".join(lines))
 
 
-def full(src, dst):
+def full(src, dst, workload="C2"):
     out = subprocess.run(["ncu", "-i", src, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     h, units = rows[0], rows[1]
@@ -92,15 +92,18 @@ def full(src, dst):
         except (ValueError, IndexError):
             pass
     json.dump(res, open(dst, "w"), indent=1)
+    # per workload (the bench line of that workload reads its own entry): {workload: {class: bytes per launch}}
     tpath = os.path.join(os.path.dirname(dst), "ncu_traffic.json")
+    allw = json.load(open(tpath)) if os.path.exists(tpath) else {}
     tr = {k: sum(v) / len(v) for k, v in traffic.items()}
     tr["_source"] = os.path.basename(dst)
     tr["_note"] = "mean dram__bytes_read.sum + dram__bytes_write.sum per captured launch (ncu --set full)"
-    json.dump(tr, open(tpath, "w"), indent=1)
+    allw[workload] = tr
+    json.dump(allw, open(tpath, "w"), indent=1)
     for k, v in res.items():
         for d in v:
             print(k, {a: b for a, b in d.items() if a != "Kernel Name"})
 
 
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2], sys.argv[3])
+    {"launches": launches, "full": full}[sys.argv[1]](*sys.argv[2:])
