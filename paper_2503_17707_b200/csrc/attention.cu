@@ -78,12 +78,15 @@ __global__ void __launch_bounds__(288, TWO ? 2 : 1) attention_tc_kernel(const __
 
     pdl_launch_dependents();
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int h = blockIdx.y, b = blockIdx.z, kvh = h / group;
+    // grid (head, sequence, query tile): the block scheduler hands out CTAs with x fastest, so every head's and
+    // sequence's LATEST query tile (the most key tiles) starts first and the one-tile CTAs fill the tail (longest
+    // processing time first; with (tile, head) order the last wave was a few long CTAs on otherwise idle SMs)
+    const int h = blockIdx.x, b = blockIdx.y, kvh = h / group;
     if (dyn) {   // f3 decode graph: the position is read on the device
         t0 += *dyn;
         t1 += *dyn;
     }
-    const int qtile = gridDim.x - 1 - blockIdx.x;          // longest (latest) query tiles first
+    const int qtile = gridDim.z - 1 - blockIdx.z;          // longest (latest) query tiles first
     const int q0 = t0 + qtile * QT;
     const int q_hi = min(q0 + QT, t1);
     const int n_kv = (q_hi + KT - 1) / KT;                  // key tiles [0, n_kv)
@@ -344,7 +347,7 @@ __global__ void __launch_bounds__(288, TWO ? 2 : 1) attention_tc_kernel(const __
         mbar_wait(o_full, (n_kv - 1) & 1);
         tc_fence_after();
         __nv_bfloat16* o_row =
-            out + (seq_stride ? (size_t)b * seq_stride + t : (size_t)t * gridDim.z + b) * ldo + h * HD;
+            out + (seq_stride ? (size_t)b * seq_stride + t : (size_t)t * gridDim.y + b) * ldo + h * HD;
 #pragma unroll
         for (int c = hf * (HD / 64); c < (hf + 1) * (HD / 64); ++c) {
             uint32_t o[32];
@@ -393,7 +396,7 @@ cudaError_t launch_tc(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int 
     using SM = AttnSmem<HD, TWO>;
     cudaError_t e = smem_attr_once<attention_tc_kernel<HD, TWO>>(SM::kTotal);
     if (e != cudaSuccess) return e;
-    const dim3 grid((t1 - t0 + QT - 1) / QT, H, B);
+    const dim3 grid(H, B, (t1 - t0 + QT - 1) / QT);
     const float scale_log2 = score_scale * 1.4426950408889634f;
     return launch_pdl(attention_tc_kernel<HD, TWO>, grid, 288, SM::kTotal, s, pdl, map, out, ldo, t0, t1, group, k_col0,
                       v_col0, scale_log2, dyn, seq_stride);
