@@ -418,9 +418,12 @@ cudaError_t launch_epi(const CUtensorMap& mapX, const CUtensorMap& mapW, const G
 // ------------------------------------------------------------------------------------------------------------
 constexpr int BIG_BN = 256, BIG_STAGES = 4;
 constexpr int kBigA = BM * BK * 2, kBigB = BIG_BN * BK * 2;   // 16 KB activation box, 32 KB weight boxes per stage
-// The same kernel with TBN = 192-column tiles (bias / residual epilogues) where 256-column tiles fill the last wave
-// badly (gemm_big_tile_n): W arrives as a 128-row box + a 64-row box (mapW64), 5 stages of 40 KB.
-template <int TBN> __host__ __device__ constexpr int big_stages() { return TBN == 256 ? BIG_STAGES : TBN == 192 ? 5 : 6; }
+// The same kernel with 128- to 224-column tiles (bias / residual epilogues) where 256-column tiles fill the last wave
+// badly (gemm_big_tile_n): W arrives as a 128-row box plus 64- (mapW64) and 32-row (mapW32) boxes for the rest
+// (160 = 128 + 32, 192 = 128 + 64, 224 = 128 + 64 + 32); as many stages as fit in 227 KB (4 to 6).
+template <int TBN> __host__ __device__ constexpr int big_stages() {
+    return TBN == 256 ? BIG_STAGES : TBN >= 192 ? 5 : 6;
+}
 template <int TBN> __host__ __device__ constexpr int big_stage_bytes() { return kBigA + TBN * BK * 2; }
 template <int TBN> __host__ __device__ constexpr int big_smem() {
     return big_stages<TBN>() * big_stage_bytes<TBN>() + 256 + 1024;
@@ -429,9 +432,10 @@ template <int TBN> __host__ __device__ constexpr int big_smem() {
 template <int EPI, int TBN = BIG_BN>
 __global__ void __launch_bounds__(192, 1) gemm_big_kernel(const __grid_constant__ CUtensorMap mapX,
                                                           const __grid_constant__ CUtensorMap mapW,
-                                                          const __grid_constant__ CUtensorMap mapW64, const GemmArgs a) {
-    static_assert(TBN == BIG_BN || ((TBN == 192 || TBN == 128) && EPI != EPI_SILU_MUL),
-                  "192- / 128-column tiles: bias / residual epilogues");
+                                                          const __grid_constant__ CUtensorMap mapW64,
+                                                          const __grid_constant__ CUtensorMap mapW32, const GemmArgs a) {
+    static_assert(TBN == BIG_BN || (TBN % 32 == 0 && TBN >= 128 && TBN < 256 && EPI != EPI_SILU_MUL),
+                  "128- to 224-column tiles: bias / residual epilogues");
     constexpr int NST = big_stages<TBN>(), kStg = big_stage_bytes<TBN>();
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -452,7 +456,8 @@ __global__ void __launch_bounds__(192, 1) gemm_big_kernel(const __grid_constant_
     if (tid == 0) {
         tma_prefetch_desc(&mapX);
         tma_prefetch_desc(&mapW);
-        if (TBN == 192) tma_prefetch_desc(&mapW64);
+        if (TBN == 192 || TBN == 224) tma_prefetch_desc(&mapW64);
+        if (TBN == 160 || TBN == 224) tma_prefetch_desc(&mapW32);
         for (int s = 0; s < NST; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
@@ -488,9 +493,11 @@ __global__ void __launch_bounds__(192, 1) gemm_big_kernel(const __grid_constant_
                         tma_load_2d(sB + kBigB / 2, &mapW, &full[s], kc, a.up_row0 + n0);
                         tma_load_2d(sB + 3 * kBigB / 4, &mapW, &full[s], kc, a.up_row0 + n0 + 64);
                     } else {
-                        tma_load_2d(sB, &mapW, &full[s], kc, n0);
-                        if (TBN == 192) tma_load_2d(sB + kBigB / 2, &mapW64, &full[s], kc, n0 + 128);
-                        else if (TBN == 256) tma_load_2d(sB + kBigB / 2, &mapW, &full[s], kc, n0 + 128);
+                        tma_load_2d(sB, &mapW, &full[s], kc, n0);   // rows 128 B apart: row r at sB + 128 r
+                        if (TBN == 256) tma_load_2d(sB + 128 * 128, &mapW, &full[s], kc, n0 + 128);
+                        if (TBN == 192 || TBN == 224) tma_load_2d(sB + 128 * 128, &mapW64, &full[s], kc, n0 + 128);
+                        if (TBN == 160) tma_load_2d(sB + 128 * 128, &mapW32, &full[s], kc, n0 + 128);
+                        if (TBN == 224) tma_load_2d(sB + 192 * 128, &mapW32, &full[s], kc, n0 + 192);
                     }
                 }
             }
@@ -659,23 +666,23 @@ __global__ void __launch_bounds__(192, 1) gemm_big_kernel(const __grid_constant_
 }
 
 template <int EPI, int TBN = BIG_BN>
-cudaError_t launch_big(const CUtensorMap& mapX, const CUtensorMap& mapW, const CUtensorMap& mapW64, const GemmArgs& a,
-                       cudaStream_t s) {
+cudaError_t launch_big(const CUtensorMap& mapX, const CUtensorMap& mapW, const CUtensorMap& mapW64,
+                       const CUtensorMap& mapW32, const GemmArgs& a, cudaStream_t s) {
     cudaError_t e = smem_attr_once<gemm_big_kernel<EPI, TBN>>(big_smem<TBN>());
     if (e != cudaSuccess) return e;
     const int per = EPI == EPI_SILU_MUL ? BIG_BN / 2 : TBN;
     const int tiles = ((a.N + per - 1) / per) * ((a.M_end - a.M_begin + BM - 1) / BM);
     const int grid = tiles < 148 ? tiles : 148;
     return launch_pdl(gemm_big_kernel<EPI, TBN>, dim3(grid), dim3(192), big_smem<TBN>(), s, a.pdl != 0, mapX, mapW,
-                      mapW64, a);
+                      mapW64, mapW32, a);
 }
 
-// Tile width of the persistent kernel: 256, 192 or 128 columns, whichever minimises waves x (width + 32) (the +32
-// charges narrower tiles for their extra activation traffic and per-tile overhead); 256 unless another width is
-// more than 5 % better. C3: QKV 192, O / down 128 (one wave); C4: O / FC1 / FC2 192, QKV 256; C5a: QKV 192, O / down
-// 256; C5b 256 (measured: C4 GEMM class 0.71 -> 0.81 of the sustained peak, C5a 0.93 -> 0.94).
+// Tile width of the persistent kernel: 256, 224, 192, 160 or 128 columns, whichever minimises waves x (width + 32)
+// (the +32 charges narrower tiles for their extra activation traffic and per-tile overhead); 256 unless another width
+// is more than 5 % better. 160 / 224 need the 32-row weight boxes (fine = false: 256 / 192 / 128 only). C4: QKV and
+// FC1 224, O / FC2 160; C3: QKV 192, O / down 128 (one wave); C5a: QKV 192, O / down 256.
 // Depends on (N, epi, rows of the whole prompt) only.
-int gemm_big_tile_n(int N, int epi, int M_total) {
+int gemm_big_tile_n(int N, int epi, int M_total, bool fine) {
     if (epi == EPI_SILU_MUL) return BIG_BN;
     const long m_tiles = (M_total + BM - 1) / BM;
     auto cost = [&](int w) {
@@ -684,8 +691,8 @@ int gemm_big_tile_n(int N, int epi, int M_total) {
     };
     int best = BIG_BN;
     double best_cost = cost(BIG_BN) * 0.95;
-    for (int w : {192, 128})
-        if (cost(w) < best_cost) {
+    for (int w : {224, 192, 160, 128})
+        if ((fine || (w != 224 && w != 160)) && cost(w) < best_cost) {
             best = w;
             best_cost = cost(w);
         }
@@ -905,6 +912,8 @@ cudaError_t warm_gemm_kernels() {
                          (const void*)gemm_big_kernel<EPI_SILU_MUL>,
                          (const void*)gemm_big_kernel<EPI_BF16, 192>, (const void*)gemm_big_kernel<EPI_RESID, 192>,
                          (const void*)gemm_big_kernel<EPI_BF16, 128>, (const void*)gemm_big_kernel<EPI_RESID, 128>,
+                         (const void*)gemm_big_kernel<EPI_BF16, 160>, (const void*)gemm_big_kernel<EPI_RESID, 160>,
+                         (const void*)gemm_big_kernel<EPI_BF16, 224>, (const void*)gemm_big_kernel<EPI_RESID, 224>,
                          (const void*)gemv_kernel<EPI_BF16, 1>,  (const void*)gemv_kernel<EPI_BF16, 2>,
                          (const void*)gemv_kernel<EPI_RESID, 1>, (const void*)gemv_kernel<EPI_RESID, 2>,
                          (const void*)gemv_kernel<EPI_SILU_MUL, 1>, (const void*)gemv_kernel<EPI_SILU_MUL, 2>};
@@ -963,18 +972,25 @@ cudaError_t launch_gemm(const CUtensorMap& mapX, const CUtensorMap& mapW, const 
     // The kernel is chosen from the WHOLE prompt (M_total), never from the rows of this launch, so a prompt split
     // into chunks runs every output through the same kernel and the same summation order.
     if (S == 1 && a.split_k <= 0 && a.M_total > BM && !a.m_dyn) {
-        int tw = a.mapW64 ? gemm_big_tile_n(a.N, a.epi, a.M_total) : BIG_BN;
-        if (a.rope && tw == 192) tw = BIG_BN;   // rotary pairs need head-aligned tiles
+        static const bool fine_off = getenv("PB_GEMM_FINE_TILES") && atoi(getenv("PB_GEMM_FINE_TILES")) == 0;   // A/B
+        int tw = a.mapW64 ? gemm_big_tile_n(a.N, a.epi, a.M_total, a.mapW32 != nullptr && !fine_off) : BIG_BN;
+        if (a.rope && tw % 128) tw = BIG_BN;   // rotary pairs need head-aligned tiles
+        const CUtensorMap& m64 = a.mapW64 ? *a.mapW64 : mapW;
+        const CUtensorMap& m32 = a.mapW32 ? *a.mapW32 : mapW;
         switch (a.epi) {
             case EPI_BF16:
-                if (tw == 192) return launch_big<EPI_BF16, 192>(mapX, mapW, *a.mapW64, a, s);
-                if (tw == 128) return launch_big<EPI_BF16, 128>(mapX, mapW, mapW, a, s);
-                return launch_big<EPI_BF16>(mapX, mapW, mapW, a, s);
+                if (tw == 224) return launch_big<EPI_BF16, 224>(mapX, mapW, m64, m32, a, s);
+                if (tw == 192) return launch_big<EPI_BF16, 192>(mapX, mapW, m64, m32, a, s);
+                if (tw == 160) return launch_big<EPI_BF16, 160>(mapX, mapW, m64, m32, a, s);
+                if (tw == 128) return launch_big<EPI_BF16, 128>(mapX, mapW, m64, m32, a, s);
+                return launch_big<EPI_BF16>(mapX, mapW, m64, m32, a, s);
             case EPI_RESID:
-                if (tw == 192) return launch_big<EPI_RESID, 192>(mapX, mapW, *a.mapW64, a, s);
-                if (tw == 128) return launch_big<EPI_RESID, 128>(mapX, mapW, mapW, a, s);
-                return launch_big<EPI_RESID>(mapX, mapW, mapW, a, s);
-            case EPI_SILU_MUL: return launch_big<EPI_SILU_MUL>(mapX, mapW, mapW, a, s);
+                if (tw == 224) return launch_big<EPI_RESID, 224>(mapX, mapW, m64, m32, a, s);
+                if (tw == 192) return launch_big<EPI_RESID, 192>(mapX, mapW, m64, m32, a, s);
+                if (tw == 160) return launch_big<EPI_RESID, 160>(mapX, mapW, m64, m32, a, s);
+                if (tw == 128) return launch_big<EPI_RESID, 128>(mapX, mapW, m64, m32, a, s);
+                return launch_big<EPI_RESID>(mapX, mapW, m64, m32, a, s);
+            case EPI_SILU_MUL: return launch_big<EPI_SILU_MUL>(mapX, mapW, m64, m32, a, s);
         }
     }
     const int tbn = a.split_k <= 0 && a.mapW64 && !a.rope ? gemm_tile_n(a.N, a.K, a.epi, a.M_total) : BN;

@@ -121,6 +121,8 @@ struct GemmArgs {
     const __nv_bfloat16* W;     // [rows x K] row-major (rows as for mapW)
     // the same weights with 64-row boxes (64-column tiles, gemm_tile_n); null = 128-column tiles only (host pointer)
     const CUtensorMap* mapW64;
+    // ... and with 32-row boxes (the persistent kernel's 160- / 224-column tiles); null = not used (host pointer)
+    const CUtensorMap* mapW32;
     // Llama QKV (EPI_BF16): rotary embedding applied to the fp32 accumulator BEFORE the one bf16 rounding, so
     // q/k = RNE_bf16(rope(x Wqk^T)) exactly as the storage contract says. Columns [0, rope_cols)
     // are q and k heads of rope_hd columns each (head-aligned); output row r is at position

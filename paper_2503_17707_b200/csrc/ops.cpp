@@ -110,10 +110,13 @@ static pb_status gemm_op(const void* X, int32_t x_rows, int32_t m_begin, int32_t
     a.trace = g_gemm_trace;
     a.pdl = g_gemm_pdl;
     a.M_total = m_end - m_begin;
-    CUtensorMap mw64;
+    CUtensorMap mw64, mw32;
     if (epi != EPI_SILU_MUL) {
-        if (!make_map_bf16(&mw64, W, n_rows, K, K, 64, 64, 128, err, sizeof err)) return fail(PB_EINVAL, "%s", err);
+        if (!make_map_bf16(&mw64, W, n_rows, K, K, 64, 64, 128, err, sizeof err) ||
+            !make_map_bf16(&mw32, W, n_rows, K, K, 32, 64, 128, err, sizeof err))
+            return fail(PB_EINVAL, "%s", err);
         a.mapW64 = &mw64;   // 64-column tiles where gemm_tile_n picks them
+        a.mapW32 = &mw32;   // the persistent kernel's 160- / 224-column tiles where gemm_big_tile_n picks them
     }
     a.X = static_cast<const __nv_bfloat16*>(X);   // M <= 2 with split_k == 0: the weight-streaming GEMV
     a.ldx = K;

@@ -324,7 +324,8 @@ static pb_status build_prefill_maps(pb_ctx* c) {
                     return fail(PB_EINVAL, "weight map layer %d: %s", l, err);
                 lm.w[i] = reinterpret_cast<const __nv_bfloat16*>(base);
                 if (!(i == 2 && !opt) &&
-                    !make_map_bf16(&lm.w64[i], base, t.rows, t.cols, t.cols, 64, 64, 128, err, sizeof err))
+                    (!make_map_bf16(&lm.w64[i], base, t.rows, t.cols, t.cols, 64, 64, 128, err, sizeof err) ||
+                     !make_map_bf16(&lm.w32[i], base, t.rows, t.cols, t.cols, 32, 64, 128, err, sizeof err)))
                     return fail(PB_EINVAL, "weight map layer %d: %s", l, err);
             }
         }
@@ -899,6 +900,7 @@ pb_status run_layer(pb_ctx* c, int l, int r0, int r1, int ta, int tb, int B, boo
         a.ldx = ldx;
         a.W = lm.w[wi];
         a.mapW64 = (wi == 2 && !opt) ? nullptr : &lm.w64[wi];
+        a.mapW32 = (wi == 2 && !opt) ? nullptr : &lm.w32[wi];
         const int pi = prof_begin(c, K_GEMM, s);
         cudaError_t e = launch_gemm(mx, mw, a, s);
         const double M = rows, N = a.N, K = a.K;

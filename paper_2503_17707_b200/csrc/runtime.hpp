@@ -61,6 +61,7 @@ struct LayerMaps {
     CUtensorMap qkv, o, up, down;   // up = fc1 (OPT) or [gate; up] with 64-row boxes (Llama)
     const __nv_bfloat16* w[4];      // the same four weights as plain pointers (GEMV path)
     CUtensorMap w64[4];             // 64-row boxes for 64-column tiles (not for [gate; up])
+    CUtensorMap w32[4];             // 32-row boxes for the persistent kernel's 160- / 224-column tiles (idem)
 };
 
 struct Peer {

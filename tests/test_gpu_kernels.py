@@ -107,6 +107,9 @@ def _gemm_case(rng, M, K, N):
                                          (700, 1536, 1000, 100, 700),
                                          # persistent kernel with 192-column tiles and a ragged last tile
                                          (1024, 512, 3000, 0, 1024),
+                                         # 224-column tiles (128 + 64 + 32-row weight boxes; the last tile's 64- and
+                                         # 32-row boxes wholly past N) and 160-column tiles (128 + 32), ragged M
+                                         (1500, 256, 2328, 0, 1500), (1100, 512, 2300, 100, 1100),
                                          # M <= 2: the weight-streaming GEMV (decode sizes), ragged N and K
                                          (1, 2048, 640, 0, 1), (2, 512, 136, 0, 2), (3, 688, 258, 1, 3)])
 def test_gemm_bf16_epilogue(M, K, N, m0, m1):
@@ -128,11 +131,12 @@ def test_gemm_bf16_epilogue(M, K, N, m0, m1):
 
 
 @pytest.mark.parametrize("M,K,N,f", [(192, 320, 256, 136), (1536, 1024, 2560, 2752), (2, 320, 256, 136),
-                                     (1, 2048, 512, 330), (1024, 512, 3000, 136), (600, 256, 1000, 136)])
+                                     (1, 2048, 512, 330), (1024, 512, 3000, 136), (600, 256, 1000, 136),
+                                     (1024, 512, 3464, 136), (1024, 512, 2600, 136)])
 def test_gemm_relu_and_resid_and_silu(M, K, N, f):
     """Small shapes take the split-K kernel or the persistent 128x256 kernel at S = 1; the second case runs the
     persistent kernel over more tiles than SMs (both TMEM accumulators cycle); M <= 2 takes the GEMV; the last two
-    take the persistent kernel's 192- and 128-column tiles (ragged N)."""
+    take the persistent kernel's 192- and 128-column tiles (ragged N), the last two its 224- and 160-column tiles."""
     need_gpu()
     rng = np.random.default_rng(11 + M)
     X, W, bias = _gemm_case(rng, M, K, N)
