@@ -420,13 +420,63 @@ constexpr int BIG_BN = 256, BIG_STAGES = 4;
 constexpr int kBigA = BM * BK * 2, kBigB = BIG_BN * BK * 2;   // 16 KB activation box, 32 KB weight boxes per stage
 // The same kernel with 128- to 224-column tiles (bias / residual epilogues) where 256-column tiles fill the last wave
 // badly (gemm_big_tile_n): W arrives as a 128-row box plus 64- (mapW64) and 32-row (mapW32) boxes for the rest
-// (160 = 128 + 32, 192 = 128 + 64, 224 = 128 + 64 + 32); as many stages as fit in 227 KB (4 to 6).
+// (160 = 128 + 32, 192 = 128 + 64, 224 = 128 + 64 + 32); as many stages as fit in 227 KB (4 to 6). (144 / 208 columns
+// with 16-row boxes measured slower at the C4 shapes than the wave count predicts.)
 template <int TBN> __host__ __device__ constexpr int big_stages() {
     return TBN == 256 ? BIG_STAGES : TBN >= 192 ? 5 : 6;
 }
 template <int TBN> __host__ __device__ constexpr int big_stage_bytes() { return kBigA + TBN * BK * 2; }
 template <int TBN> __host__ __device__ constexpr int big_smem() {
     return big_stages<TBN>() * big_stage_bytes<TBN>() + 256 + 1024;
+}
+
+// Epilogue of CW accumulator columns [n, n + CW) of one output row: + bias, then (EPI_BF16) q-scale / ReLU and one
+// RNE rounding to bf16, or (EPI_RESID) the fp32 residual add h += acc + bias.
+template <int EPI, int CW>
+__device__ __forceinline__ void big_epi_chunk(const GemmArgs& a, int row, int n, const uint32_t (&r)[CW]) {
+    float v[CW];
+#pragma unroll
+    for (int e = 0; e < CW; ++e) {
+        v[e] = __uint_as_float(r[e]);
+        if (a.bias && n + e < a.N) v[e] += __bfloat162float(a.bias[n + e]);
+    }
+    const int nv = min(CW, a.N - n);
+    if (EPI == EPI_BF16) {
+#pragma unroll
+        for (int e = 0; e < CW; ++e) {
+            if (n + e < a.scale_cols) v[e] *= a.scale;
+            if (a.relu) v[e] = fmaxf(v[e], 0.f);
+        }
+        __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(a.out) + (size_t)row * a.ldo + n;
+        if (nv == CW) {
+#pragma unroll
+            for (int q = 0; q < CW / 8; ++q)
+                *reinterpret_cast<uint4*>(out + 8 * q) =
+                    make_uint4(bf16x2_bits(v[8 * q], v[8 * q + 1]), bf16x2_bits(v[8 * q + 2], v[8 * q + 3]),
+                               bf16x2_bits(v[8 * q + 4], v[8 * q + 5]), bf16x2_bits(v[8 * q + 6], v[8 * q + 7]));
+        } else {
+#pragma unroll
+            for (int e = 0; e < CW; ++e)
+                if (e < nv) out[e] = __float2bfloat16_rn(v[e]);
+        }
+    } else {   // EPI_RESID: h += acc + bias
+        float* h = reinterpret_cast<float*>(a.out) + (size_t)row * a.ldo + n;
+        if (nv == CW) {
+#pragma unroll
+            for (int q = 0; q < CW / 4; ++q) {
+                float4 x = *reinterpret_cast<float4*>(h + 4 * q);
+                x.x += v[4 * q];
+                x.y += v[4 * q + 1];
+                x.z += v[4 * q + 2];
+                x.w += v[4 * q + 3];
+                *reinterpret_cast<float4*>(h + 4 * q) = x;
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < CW; ++e)
+                if (e < nv) h[e] += v[e];
+        }
+    }
 }
 
 template <int EPI, int TBN = BIG_BN>
@@ -606,50 +656,7 @@ __global__ void __launch_bounds__(192, 1) gemm_big_kernel(const __grid_constant_
                     tmem_ld32_async(acc + cb * 32, r);
                     tmem_wait_ld();
                     if (!row_ok || n >= a.N) continue;
-                    float v[32];
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) {
-                        v[e] = __uint_as_float(r[e]);
-                        if (a.bias && n + e < a.N) v[e] += __bfloat162float(a.bias[n + e]);
-                    }
-                    const int nv = min(32, a.N - n);
-                    if (EPI == EPI_BF16) {
-#pragma unroll
-                        for (int e = 0; e < 32; ++e) {
-                            if (n + e < a.scale_cols) v[e] *= a.scale;
-                            if (a.relu) v[e] = fmaxf(v[e], 0.f);
-                        }
-                        __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(a.out) + (size_t)row * a.ldo + n;
-                        if (nv == 32) {
-#pragma unroll
-                            for (int q = 0; q < 4; ++q)
-                                *reinterpret_cast<uint4*>(out + 8 * q) =
-                                    make_uint4(bf16x2_bits(v[8 * q], v[8 * q + 1]), bf16x2_bits(v[8 * q + 2], v[8 * q + 3]),
-                                               bf16x2_bits(v[8 * q + 4], v[8 * q + 5]),
-                                               bf16x2_bits(v[8 * q + 6], v[8 * q + 7]));
-                        } else {
-#pragma unroll
-                            for (int e = 0; e < 32; ++e)
-                                if (e < nv) out[e] = __float2bfloat16_rn(v[e]);
-                        }
-                    } else {   // EPI_RESID: h += acc + bias
-                        float* h = reinterpret_cast<float*>(a.out) + (size_t)row * a.ldo + n;
-                        if (nv == 32) {
-#pragma unroll
-                            for (int q = 0; q < 8; ++q) {
-                                float4 x = *reinterpret_cast<float4*>(h + 4 * q);
-                                x.x += v[4 * q];
-                                x.y += v[4 * q + 1];
-                                x.z += v[4 * q + 2];
-                                x.w += v[4 * q + 3];
-                                *reinterpret_cast<float4*>(h + 4 * q) = x;
-                            }
-                        } else {
-#pragma unroll
-                            for (int e = 0; e < 32; ++e)
-                                if (e < nv) h[e] += v[e];
-                        }
-                    }
+                    big_epi_chunk<EPI, 32>(a, row, n, r);
                 }
             }
             tc_fence_before();
@@ -680,7 +687,7 @@ cudaError_t launch_big(const CUtensorMap& mapX, const CUtensorMap& mapW, const C
 // Tile width of the persistent kernel: 256, 224, 192, 160 or 128 columns, whichever minimises waves x (width + 32)
 // (the +32 charges narrower tiles for their extra activation traffic and per-tile overhead); 256 unless another width
 // is more than 5 % better. 160 / 224 need the 32-row weight boxes (fine = false: 256 / 192 / 128 only). C4: QKV and
-// FC1 224, O / FC2 160; C3: QKV 192, O / down 128 (one wave); C5a: QKV 192, O / down 256.
+// FC1 224, O / FC2 160; C3: QKV 192, O / down 128 (one wave); C5a: O / down 224 (QKV: rotary, 256).
 // Depends on (N, epi, rows of the whole prompt) only.
 int gemm_big_tile_n(int N, int epi, int M_total, bool fine) {
     if (epi == EPI_SILU_MUL) return BIG_BN;
@@ -692,7 +699,7 @@ int gemm_big_tile_n(int N, int epi, int M_total, bool fine) {
     int best = BIG_BN;
     double best_cost = cost(BIG_BN) * 0.95;
     for (int w : {224, 192, 160, 128})
-        if ((fine || (w != 224 && w != 160)) && cost(w) < best_cost) {
+        if ((fine || w == 192 || w == 128) && cost(w) < best_cost) {
             best = w;
             best_cost = cost(w);
         }
@@ -924,6 +931,32 @@ cudaError_t warm_gemm_kernels() {
     return cudaSuccess;
 }
 
+// Vocabulary logits of one or two sequences as the weight-streaming GEMV (the head is a pure stream of V x d bf16 at
+// M <= 2): logits[b, v0:v1] = y[b] . E[v0:v1]^T accumulated into a zeroed fp32 slice (EPI_RESID). Each output's sum
+// is taken in the same order whatever rows a launch covers, so vocab slices give the same bits as the whole head.
+cudaError_t launch_logits_gemv(const __nv_bfloat16* y, int B, int d, const __nv_bfloat16* E, int v0, int v1,
+                               float* logits, int ldl, cudaStream_t s, bool pdl) {
+    if (v1 <= v0 || B <= 0) return cudaSuccess;
+    if (B > kGemvAutoRows || d % 8) return cudaErrorInvalidValue;
+    cudaError_t e = cudaMemset2DAsync(logits + v0, (size_t)ldl * 4, 0, (size_t)(v1 - v0) * 4, B, s);
+    if (e != cudaSuccess) return e;
+    GemmArgs a{};
+    a.M_begin = 0;
+    a.M_end = B;
+    a.N = v1 - v0;
+    a.K = d;
+    a.epi = EPI_RESID;
+    a.scale = 1.f;
+    a.out = logits + v0;
+    a.ldo = ldl;
+    a.M_total = B;
+    a.pdl = pdl ? 1 : 0;
+    a.X = y;
+    a.ldx = d;
+    a.W = E + (size_t)v0 * d;
+    return launch_gemv_epi<EPI_RESID>(a, s);
+}
+
 // Vocabulary logits of a large batch on the tensor cores: logits[b, v0:v1] = y[b] . E[v0:v1]^T (fp32), as the
 // split-K kernel's fp32 epilogue over a zeroed slice. S = 1 (each output's K sum in one CTA, in k order), so a
 // vocab slice of any width gives the same bits as the whole head (pipelined equals sequential).
@@ -973,25 +1006,23 @@ cudaError_t launch_gemm(const CUtensorMap& mapX, const CUtensorMap& mapW, const 
     // into chunks runs every output through the same kernel and the same summation order.
     if (S == 1 && a.split_k <= 0 && a.M_total > BM && !a.m_dyn) {
         static const bool fine_off = getenv("PB_GEMM_FINE_TILES") && atoi(getenv("PB_GEMM_FINE_TILES")) == 0;   // A/B
-        int tw = a.mapW64 ? gemm_big_tile_n(a.N, a.epi, a.M_total, a.mapW32 != nullptr && !fine_off) : BIG_BN;
+        const bool fine = a.mapW32 != nullptr && !fine_off;
+        int tw = a.mapW64 ? gemm_big_tile_n(a.N, a.epi, a.M_total, fine) : BIG_BN;
         if (a.rope && tw % 128) tw = BIG_BN;   // rotary pairs need head-aligned tiles
         const CUtensorMap& m64 = a.mapW64 ? *a.mapW64 : mapW;
         const CUtensorMap& m32 = a.mapW32 ? *a.mapW32 : mapW;
+#define PB_BIG(E, W) \
+    if (tw == W) return launch_big<E, W>(mapX, mapW, m64, m32, a, s);
         switch (a.epi) {
             case EPI_BF16:
-                if (tw == 224) return launch_big<EPI_BF16, 224>(mapX, mapW, m64, m32, a, s);
-                if (tw == 192) return launch_big<EPI_BF16, 192>(mapX, mapW, m64, m32, a, s);
-                if (tw == 160) return launch_big<EPI_BF16, 160>(mapX, mapW, m64, m32, a, s);
-                if (tw == 128) return launch_big<EPI_BF16, 128>(mapX, mapW, m64, m32, a, s);
+                PB_BIG(EPI_BF16, 224) PB_BIG(EPI_BF16, 192) PB_BIG(EPI_BF16, 160) PB_BIG(EPI_BF16, 128)
                 return launch_big<EPI_BF16>(mapX, mapW, m64, m32, a, s);
             case EPI_RESID:
-                if (tw == 224) return launch_big<EPI_RESID, 224>(mapX, mapW, m64, m32, a, s);
-                if (tw == 192) return launch_big<EPI_RESID, 192>(mapX, mapW, m64, m32, a, s);
-                if (tw == 160) return launch_big<EPI_RESID, 160>(mapX, mapW, m64, m32, a, s);
-                if (tw == 128) return launch_big<EPI_RESID, 128>(mapX, mapW, m64, m32, a, s);
+                PB_BIG(EPI_RESID, 224) PB_BIG(EPI_RESID, 192) PB_BIG(EPI_RESID, 160) PB_BIG(EPI_RESID, 128)
                 return launch_big<EPI_RESID>(mapX, mapW, m64, m32, a, s);
             case EPI_SILU_MUL: return launch_big<EPI_SILU_MUL>(mapX, mapW, m64, m32, a, s);
         }
+#undef PB_BIG
     }
     const int tbn = a.split_k <= 0 && a.mapW64 && !a.rope ? gemm_tile_n(a.N, a.K, a.epi, a.M_total) : BN;
     switch (a.epi) {

@@ -137,6 +137,9 @@ int gemm_split_k(int N, int K, int epi, int M_total);
 // Maps: X box {64, 128} SW128 over [max_rows x K]; W box {64, 128} (EPI_SILU_MUL: {64, 64}) SW128 over [rows x K].
 cudaError_t launch_gemm(const CUtensorMap& mapX, const CUtensorMap& mapW, const GemmArgs& a, cudaStream_t s);
 // logits[b, v0:v1] (fp32, row pitch ldl) = y[b] . E[v0:v1]^T for large batches (tcgen05, S = 1)
+// logits[b, v0:v1] for B <= 2 sequences through the weight-streaming GEMV (zeroed fp32 slice, then y . E^T)
+cudaError_t launch_logits_gemv(const __nv_bfloat16* y, int B, int d, const __nv_bfloat16* E, int v0, int v1,
+                               float* logits, int ldl, cudaStream_t s, bool pdl);
 cudaError_t launch_logits_tc(const __nv_bfloat16* y, int B, int d, const __nv_bfloat16* E, int v0, int v1, float* logits,
                              int ldl, cudaStream_t s);
 

@@ -561,6 +561,9 @@ cudaError_t launch_logits(const __nv_bfloat16* y, int B, int d, const __nv_bfloa
     // a large batch (the paper's 64 x 64 workload) is a GEMM: the tensor cores read the head once
     // (C2p: 1.3 ms on the CUDA cores, 8 sequences per pass)
     if (B >= 16 && d % 64 == 0) return launch_logits_tc(y, B, d, E, v0, v1, logits, ldl, s);
+    // one or two sequences (the cold start's first token, decode steps): the weight-streaming GEMV
+    static const bool gemv_off = getenv("PB_LOGITS_GEMV") && atoi(getenv("PB_LOGITS_GEMV")) == 0;   // A/B
+    if (B <= kGemvAutoRows && !gemv_off) return launch_logits_gemv(y, B, d, E, v0, v1, logits, ldl, s, pdl);
     // up to 8 sequences per launch (the warp's accumulators); larger batches (the paper's 64 x 64 workload)
     // stream the head once per group of 8
     for (int b0 = 0; b0 < B; b0 += 8) {

@@ -358,6 +358,27 @@ def test_logits_large_batch_tensor_cores(Bsz, V):
     assert np.array_equal(whole.cpu().numpy().view(np.uint32), sliced.cpu().numpy().view(np.uint32))
 
 
+@pytest.mark.parametrize("Bsz", [1, 2])
+def test_logits_small_batch_gemv_vocab_slices(Bsz):
+    """One or two sequences: the head as the weight-streaming GEMV; vocab slices give the bits of the whole head
+    (pipelined equals sequential) and the values of y . E^T."""
+    need_gpu()
+    rng = np.random.default_rng(40 + Bsz)
+    d, V = 2048, 5003
+    y = rbits(rng, (Bsz, d), 1.0)
+    E = rbits(rng, (V, d), 0.035)
+    Ed, yd = dev_bf16(E), dev_bf16(y)
+    whole = torch.full((Bsz, V), float("nan"), device="cuda")
+    B.pb_op_logits(ptr(yd), Bsz, d, ptr(Ed), 0, V, ptr(whole), V, stream())
+    sliced = torch.full((Bsz, V), float("nan"), device="cuda")
+    for v0, v1 in ((0, 1237), (1237, 4000), (4000, V)):
+        B.pb_op_logits(ptr(yd), Bsz, d, ptr(Ed), v0, v1, ptr(sliced), V, stream())
+    torch.cuda.synchronize()
+    assert torch.equal(whole, sliced)
+    ref = bf16_bits_to_f64(y) @ bf16_bits_to_f64(E).T
+    assert np.allclose(whole.cpu().numpy(), ref, rtol=1e-5, atol=1e-5)
+
+
 def test_logits_argmax_embed():
     need_gpu()
     rng = np.random.default_rng(9)
