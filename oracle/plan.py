@@ -297,6 +297,20 @@ def rows_per_chunk(row_bytes: int, chunk_bytes: int) -> int:
     return rpc
 
 
+def canonical_order(plan: Plan, base_chunks, ad_chunks):
+    """Chunk ids in the canonical load order (G8): non-layer tensors before the first layer, then every adapter
+    chunk (atensor order = host layout order), then the layers' base tensors and the remaining non-layer tensors,
+    each tensor's chunks in row order. base_chunks / ad_chunks: tensor id -> chunk ids."""
+    order, adapters_done = [], False
+    for t in plan.tensors:
+        if t.layer >= 0 and not adapters_done:
+            for at in plan.atensors:
+                order += [c if isinstance(c, int) else c.id for c in ad_chunks.get(at.id, [])]
+            adapters_done = True
+        order += [c if isinstance(c, int) else c.id for c in base_chunks.get(t.id, [])]
+    return order
+
+
 def build_chunks(plan: Plan) -> None:
     cb = plan.opts.chunk_bytes
     cid = 0
@@ -330,34 +344,16 @@ def build_chunks(plan: Plan) -> None:
         per_atensor[at.id] = lst
         plan.chunks += lst
 
-    # Per-GPU load list: the GPU's pieces in canonical table order; a layer's
-    # adapter parts (adapter order, then target order, A then B) come right
-    # BEFORE that layer's base tensors (G8: the paper is silent; the factors are
-    # tiny, and having them first lets each adapted tensor merge as soon as it lands).
+    # Per-GPU load list: the GPU's pieces in canonical table order, with ALL of
+    # its adapter parts (in host layout order: adapter, layer, target, A then B)
+    # right before the first layer tensor (G8: the paper is silent; the factors
+    # are tiny, a GPU's parts of one adapter are contiguous in host and device
+    # memory, so they cross PCIe as one DMA instead of one small DMA per layer,
+    # and every adapted tensor can merge the moment its base rows land).
     N = plan.n_gpus
     plan.load = [[] for _ in range(N)]
-    ad_by_layer = {}
-    for at in plan.atensors:
-        ad_by_layer.setdefault(at.layer, []).append(at)
-    ts = plan.tensors
-    i = 0
-    while i < len(ts):
-        t = ts[i]
-        if t.layer < 0:
-            for c in per_tensor[t.id]:
-                plan.load[c.loader].append(c.id)
-            i += 1
-            continue
-        l = t.layer
-        for at in ad_by_layer.get(l, []):
-            for c in per_atensor[at.id]:
-                plan.load[c.loader].append(c.id)
-        j = i
-        while j < len(ts) and ts[j].layer == l:
-            for c in per_tensor[ts[j].id]:
-                plan.load[c.loader].append(c.id)
-            j += 1
-        i = j
+    for cid in canonical_order(plan, per_tensor, per_atensor):
+        plan.load[plan.chunks[cid].loader].append(cid)
 
 
 # ---------------------------------------------------------------------------
@@ -501,28 +497,12 @@ def replan(plan: Plan, alive: Sequence[int], resident: Sequence[Sequence[int]]) 
             holders = [r for r in range(m) if c.id in rank_held[r]]
             src[c.id] = loaders[0] if loaders else (min(holders) if holders else home_rank(c))
     new.chunks = [replace(c, loader=src[c.id]) for c in chunks]
-    # R5: load lists in the canonical order of build_chunks (per layer: adapter parts, then base tensors)
-    order = []
-    ad_by_layer = {}
-    for at in plan.atensors:
-        ad_by_layer.setdefault(at.layer, []).append(at.id)
+    # R5: load lists in the canonical order of build_chunks (G8: adapter parts, then the layers' base tensors)
     base_by_tensor = {}
     ad_chunks = {}
     for c in chunks:
         (base_by_tensor if c.kind == "base" else ad_chunks).setdefault(c.tensor, []).append(c.id)
-    i = 0
-    while i < len(tens):
-        t = tens[i]
-        if t.layer < 0:
-            order += base_by_tensor[t.id]
-            i += 1
-            continue
-        l = t.layer
-        for aid in ad_by_layer.get(l, []):
-            order += ad_chunks[aid]
-        while i < len(tens) and tens[i].layer == l:
-            order += base_by_tensor[tens[i].id]
-            i += 1
+    order = canonical_order(plan, base_by_tensor, ad_chunks)
     new.load = [[] for _ in range(m)]
     for cid in order:
         c = chunks[cid]

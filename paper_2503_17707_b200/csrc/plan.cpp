@@ -117,6 +117,24 @@ static int32_t layer_loader(const pb_plan* p, int32_t l) {
     return p->opts.policy == PB_LOAD_STAGE ? p->stage_of_layer(l) : l % p->n_gpus;
 }
 
+// Chunk ids in the canonical load order (G8): the non-layer tensors before the first layer, then every adapter
+// chunk in atensor order (= host layout order: adapter, layer, target, A then B), then the layers' base tensors and
+// the remaining non-layer tensors, each tensor's chunks in row order. base_chunks / ad_chunks: per (a)tensor.
+static std::vector<int32_t> canonical_order(const pb_plan* p, const std::vector<std::vector<int32_t>>& base_chunks,
+                                            const std::vector<std::vector<int32_t>>& ad_chunks) {
+    std::vector<int32_t> order;
+    bool adapters_done = false;
+    for (size_t ti = 0; ti < p->tensors.size(); ++ti) {
+        if (p->tensors[ti].layer >= 0 && !adapters_done) {
+            for (size_t ai = 0; ai < p->atensors.size(); ++ai)
+                order.insert(order.end(), ad_chunks[ai].begin(), ad_chunks[ai].end());
+            adapters_done = true;
+        }
+        order.insert(order.end(), base_chunks[ti].begin(), base_chunks[ti].end());
+    }
+    return order;
+}
+
 extern "C" pb_status pb_plan_create(const pb_model_desc* model, const pb_adapter_desc* adapters,
                                     int32_t n_adapters, int32_t n_gpus, const pb_plan_opts* opts,
                                     pb_plan** out) {
@@ -292,25 +310,11 @@ extern "C" pb_status pb_plan_create(const pb_model_desc* model, const pb_adapter
         }
     }
 
-    // Per-GPU load lists: canonical table order; a layer's adapter factors right before its base tensors
-    // (tiny, and then every adapted tensor can merge the moment it lands).
+    // Per-GPU load lists: canonical table order with every adapter factor right before the first layer tensor, in
+    // host layout order (G8: a GPU's parts of one adapter are contiguous in host and device memory, so they cross
+    // PCIe as one DMA instead of one small DMA per layer, and every adapted tensor can merge the moment it lands).
     p->load.assign(N, {});
-    std::vector<std::vector<int32_t>> ad_of_layer(L);
-    for (size_t ai = 0; ai < p->atensors.size(); ++ai) ad_of_layer[p->atensors[ai].layer].push_back((int32_t)ai);
-    for (size_t ti = 0; ti < p->tensors.size();) {
-        const int32_t l = p->tensors[ti].layer;
-        if (l < 0) {
-            for (int32_t c : base_chunks[ti]) p->load[p->chunks[c].loader].push_back(c);
-            ++ti;
-            continue;
-        }
-        for (int32_t ai : ad_of_layer[l])
-            for (int32_t c : ad_chunks[ai]) p->load[p->chunks[c].loader].push_back(c);
-        size_t tj = ti;
-        for (; tj < p->tensors.size() && p->tensors[tj].layer == l; ++tj)
-            for (int32_t c : base_chunks[tj]) p->load[p->chunks[c].loader].push_back(c);
-        ti = tj;
-    }
+    for (int32_t c : canonical_order(p, base_chunks, ad_chunks)) p->load[p->chunks[c].loader].push_back(c);
 
     // Step 4: receive lists. (1) base chunks of my stage's layers loaded elsewhere, in id order;
     // (2) for i = 1..N-1, loader (g+i) mod N's base chunks in its load order.
@@ -435,20 +439,7 @@ extern "C" pb_status pb_plan_replan(const pb_plan* plan, const int32_t* alive, c
     // canonical order (pb_plan_create's load order): per layer, adapter parts then base tensors
     std::vector<std::vector<int32_t>> base_chunks(p->tensors.size()), ad_chunks(p->atensors.size());
     for (const ChunkRec& c : p->chunks) (c.is_adapter ? ad_chunks : base_chunks)[c.tensor].push_back(c.id);
-    std::vector<std::vector<int32_t>> ad_of_layer(L);
-    for (size_t ai = 0; ai < p->atensors.size(); ++ai) ad_of_layer[p->atensors[ai].layer].push_back((int32_t)ai);
-    std::vector<int32_t> order;
-    for (size_t ti = 0; ti < p->tensors.size();) {
-        const int32_t l = p->tensors[ti].layer;
-        if (l < 0) {
-            order.insert(order.end(), base_chunks[ti].begin(), base_chunks[ti].end());
-            ++ti;
-            continue;
-        }
-        for (int32_t ai : ad_of_layer[l]) order.insert(order.end(), ad_chunks[ai].begin(), ad_chunks[ai].end());
-        for (; ti < p->tensors.size() && p->tensors[ti].layer == l; ++ti)
-            order.insert(order.end(), base_chunks[ti].begin(), base_chunks[ti].end());
-    }
+    const std::vector<int32_t> order = canonical_order(p, base_chunks, ad_chunks);
     // R5: load lists
     p->load.assign(m, {});
     for (int32_t cid : order) {
