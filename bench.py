@@ -113,6 +113,16 @@ class OracleSample:
         self.fac_bits = {at.name: ow.adapter_bits(at) for at in self.facs}
         self.toks = synth.tokens(w.batch, w.seq, m.vocab)
         self.ow = ow
+        # fp64 copies of the weights no merge touches: the oracle's resident input data, widened once (untimed);
+        # a merged tensor is widened again every step (part of the timed work)
+        from oracle.numerics import bf16_bits_to_f64
+        id2name = {t.id: n for n, t in ow.tensors.items()}
+        self.touched = {id2name[at.base] for at in self.facs}
+        self.base64 = {}
+        for n, bits in self.base.items():
+            if n not in self.touched:
+                x = bf16_bits_to_f64(bits)
+                self.base64[n] = x.reshape(-1) if ow.tensors[n].rows == 1 else x
         return self
 
     def run(self):
@@ -143,15 +153,20 @@ class OracleSample:
 
         def getter(a):
             def Wget(n):
+                if n in self.base64:
+                    return self.base64[n]
                 if (a, n) not in wf:
                     x = bf16_bits_to_f64(merged[a][n])
                     wf[(a, n)] = x.reshape(-1) if ow.tensors[n].rows == 1 else x
                 return wf[(a, n)]
             return Wget
 
-        for a in merged:   # fp64 views are part of the oracle's data, not its compute
+        tc = time.perf_counter()
+        for a in merged:   # the oracle computes in fp64: widening the merged tensors is part of its work
             for n in merged[a]:
-                getter(a)(n)
+                if n not in self.base64:
+                    getter(a)(n)
+        t_conv = time.perf_counter() - tc
         t1 = time.perf_counter()
         for b in range(w.batch):
             OF.forward_logits(m, getter(self.aos[b]), self.toks[b], "bf16", layers=[])
@@ -162,21 +177,33 @@ class OracleSample:
         t_all = time.perf_counter() - t2
         nls = len(self.ls)
         if nls == L:   # the whole model: the measured time itself
-            total_s = t_merge + t_all
+            total_s = t_merge + t_conv + t_all
             per_layer = max(t_all - t_head, 0.0) / nls
         else:
             per_layer = max(t_all - t_head, 0.0) / nls
-            total_s = t_head + L * (per_layer + t_merge / nls)
+            total_s = t_head + L * (per_layer + (t_merge + t_conv) / nls)
         detail = {"sample_layers": nls, "layers": L, "merge_s_per_layer": t_merge / nls,
-                  "forward_s_per_layer": per_layer, "embed_head_s": t_head, "measured_s": t_merge + t_head + t_all}
+                  "fp64_widen_s_per_layer": t_conv / nls, "forward_s_per_layer": per_layer, "embed_head_s": t_head,
+                  "measured_s": t_merge + t_conv + t_head + t_all}
         return total_s * 1e3, detail
 
 
-def default_sample_layers(w):
-    """The whole model when one oracle pass is ~30 s of CPU work at most (C1, C2: ~0.3 TFLOP of fp64), else 4."""
-    flops = 2.0 * w.batch * w.seq * 2.0 * w.model.n_layers * (4 * w.model.d_model ** 2 + 3 * w.model.d_model *
+def _forward_flops(w):
+    return 2.0 * w.batch * w.seq * 2.0 * w.model.n_layers * (4 * w.model.d_model ** 2 + 3 * w.model.d_model *
                                                                w.model.d_ffn)
-    return w.model.n_layers if flops < 1.2e12 else 4
+
+
+def default_sample_layers(w):
+    """cpu_baseline (one run): the whole model when one oracle pass is ~30 s of CPU work at most (C1, C2: ~0.3 TFLOP
+    of fp64), else 4 layers (extrapolated, labelled)."""
+    return w.model.n_layers if _forward_flops(w) < 1.2e12 else 4
+
+
+def reference_sample_layers(w):
+    """--impl reference runs K + W steps (the driver's 20 + 5): each step a bounded sample, ~3-5 s of CPU work at C2
+    (6 of 24 layers + embed/head, extrapolated linearly in layers and labelled), the whole model only when it is
+    tiny (C1)."""
+    return w.model.n_layers if _forward_flops(w) < 5e10 else min(6, w.model.n_layers)
 
 
 def oracle_sample(w, sample_layers: int):
@@ -198,7 +225,7 @@ def run_reference(args):
         return
     from synth.configs import WORKLOADS
     w = WORKLOADS[args.workload]
-    sample = OracleSample(w, args.ref_sample_layers or default_sample_layers(w)).prepare()
+    sample = OracleSample(w, args.ref_sample_layers or reference_sample_layers(w)).prepare()
     vals, walls = [], []
     det = None
     for i in range(args.warmup + args.steps):
