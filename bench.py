@@ -589,17 +589,19 @@ def main():
     if world == 1:
         base, ada = harness.build_host_images(plan)
     else:
-        tag = f"/dev/shm/pipeboost_{args.workload}_{os.getppid()}"
-        sizes = [("base", plan.sizes.host_base_bytes), ("ada", plan.sizes.host_adapter_bytes)]
+        # base image and (4 KiB-aligned after it) the adapter image in ONE shared file, registered once: the copy
+        # lane then streams from one registered host range (as harness.build_host_images does in one process)
+        path = f"/dev/shm/pipeboost_{args.workload}_{os.getppid()}_img"
+        off = (plan.sizes.host_base_bytes + 4095) // 4096 * 4096
+        total = off + max(plan.sizes.host_adapter_bytes, 1)
         if local == 0:
-            bufs = {k: torch.from_file(f"{tag}_{k}", shared=True, size=max(n, 1), dtype=torch.uint8) for k, n in sizes}
-            harness.fill_host_images(plan, bufs["base"].data_ptr(), bufs["ada"].data_ptr())
+            img = torch.from_file(path, shared=True, size=total, dtype=torch.uint8)
+            harness.fill_host_images(plan, img.data_ptr(), img.data_ptr() + off)
         barrier()
-        bufs = {k: torch.from_file(f"{tag}_{k}", shared=True, size=max(n, 1), dtype=torch.uint8) for k, n in sizes}
-        for k, n in sizes:
-            torch.cuda.cudart().cudaHostRegister(bufs[k].data_ptr(), max(n, 1), 0)
-        shm_paths = [f"{tag}_{k}" for k, _ in sizes]
-        base, ada = bufs["base"], bufs["ada"]
+        img = torch.from_file(path, shared=True, size=total, dtype=torch.uint8)
+        torch.cuda.cudart().cudaHostRegister(img.data_ptr(), total, 0)
+        shm_paths = [path]
+        base, ada = img[:plan.sizes.host_base_bytes], img[off:off + max(plan.sizes.host_adapter_bytes, 1)]
 
     init["host_image_pin_fill"] = (time.perf_counter() - ti) * 1e3
     multi = len(w.adapters) > 1   # C3: several adapters share the base, one sequence per adapter (PB_MERGE_ALL)
