@@ -76,7 +76,10 @@ PB_API pb_status pb_op_attention(const void* qkv, int32_t ld, void* out, int32_t
 PB_API pb_status pb_op_rope(void* qkv, int32_t ld, int32_t r0, int32_t r1, int32_t B, int32_t T, int32_t n_q,
                             int32_t n_k, int32_t hd, int32_t k_col0, float theta, void* table, void* stream);
 
-/* logits[b, v] (fp32, pitch ldl) = y[b] . E[v] for v in [v0, v1); y bf16 [B x d] (8 sequences per launch). */
+/* logits[b, v] (fp32, pitch ldl) = y[b] . E[v] for v in [v0, v1); y bf16 [B x d], E bf16 [V x d] (the LM head,
+ * P:L99-107 final projection). B <= 2: the weight-streaming GEMV into a zeroed slice; 3-15: warp-per-row kernel, 8
+ * sequences per launch; >= 16: the tensor-core GEMM. Each output is summed in an order independent of [v0, v1), so
+ * vocab slices reproduce the whole head bit for bit. Errors: PB_EINVAL (d % 8), PB_ECUDA. */
 PB_API pb_status pb_op_logits(const void* y, int32_t B, int32_t d, const void* E, int32_t v0, int32_t v1,
                               float* logits, int32_t ldl, void* stream);
 
