@@ -176,6 +176,11 @@ cudaError_t launch_attention(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* ou
                              int seq_stride = 0);
 // seq_stride > 0: sequence-major rows (sequence b at rows b * seq_stride + t: the multi-adapter microbatches, all of
 // them in one launch); 0: token-major rows t * B + b.
+// One query position per sequence (decode): keys [0, t1 - 1 (+ *dyn)] of (head, sequence), contract-exact P rounding;
+// max_keys bounds the keys (shared memory for the scores).
+cudaError_t launch_decode_attention(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int ldo, int t1, int B,
+                                    int n_heads, int n_kv_heads, int hd, int k_col0, int v_col0, float score_scale,
+                                    cudaStream_t s, bool pdl, const int* dyn, int max_keys);
 cudaError_t launch_attention_simt(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int ldo, int t0, int t1,
                                   int B, int n_heads, int n_kv_heads, int hd, int k_col0, int v_col0,
                                   float score_scale, cudaStream_t s);

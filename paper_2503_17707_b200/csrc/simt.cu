@@ -530,6 +530,149 @@ cudaError_t launch_rope(__nv_bfloat16* qkv, int ld, int r0, int r1, int B, int n
     return launch_pdl(rope_kernel, r1 - r0, 256, 0, s, pdl, qkv, ld, r0, B, n_q, n_k, hd, k_col0, table, dyn);
 }
 
+// ------------------------------------------------------------------ decode attention (one query position)
+// One new position per sequence (f3 decode steps): a 128-query tensor-core tile would be 127/128 padding and
+// its two passes over the key tiles are a chain of MMA / softmax handshakes per tile. Here a CTA of 16 warps serves
+// one (head, sequence) with the storage contract's exact normalised-P rounding:
+//   scores  s_j = q . k_j (fp32, one thread per key, the key's vectors all requested before the FMAs), kept in smem;
+//   m = max s, E_j = exp2(s_j c - m c), l = sum E (block reductions in a fixed order);
+//   O = sum_j RNE_bf16(E_j / l) v_j (warps take keys j = w, w + 16, ..., lanes the head dims; the 16 warp partials
+//   added in warp order); out = RNE_bf16(O).
+// dyn (decode graphs): positions read on the device. Keys [0, t] of the query position t = t1 - 1.
+constexpr int DA_WARPS = 16, kDecodeMaxKeys = 12288;
+
+template <int HD>
+__global__ void __launch_bounds__(DA_WARPS * 32) decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv, int ld,
+                                                                         __nv_bfloat16* __restrict__ out, int ldo,
+                                                                         int t1, int B, int group, int k_col0,
+                                                                         int v_col0, float scale_log2, const int* dyn) {
+    pdl_launch_dependents();
+    extern __shared__ float da_smem[];
+    constexpr int NT = DA_WARPS * 32, VPR = HD / 8, DPL = HD / 32;   // 16-B vectors per row, dims per lane
+    float* red = da_smem;                        // [DA_WARPS]
+    float* opart = da_smem + 32;                 // [DA_WARPS][HD]
+    float* sq = opart + DA_WARPS * HD;           // [HD] query
+    float* sc = sq + HD;                         // [keys]
+    const int h = blockIdx.x, b = blockIdx.y, kvh = h / group;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (dyn) t1 += *dyn;
+    pdl_wait();
+    const int t = t1 - 1, nk = t + 1;
+    const __nv_bfloat16* qrow = qkv + ((size_t)t * B + b) * ld + h * HD;
+    for (int d = tid; d < HD; d += NT) sq[d] = __bfloat162float(qrow[d]);
+    __syncthreads();
+    // ---- scores: thread per key
+    for (int j = tid; j < nk; j += NT) {
+        const uint4* krow = reinterpret_cast<const uint4*>(qkv + ((size_t)j * B + b) * ld + k_col0 + kvh * HD);
+        uint4 kv[VPR];
+#pragma unroll
+        for (int v = 0; v < VPR; ++v) kv[v] = __ldg(krow + v);
+        float acc = 0.f;
+#pragma unroll
+        for (int v = 0; v < VPR; ++v) {
+            const __nv_bfloat16* kb = reinterpret_cast<const __nv_bfloat16*>(&kv[v]);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc = fmaf(sq[v * 8 + e], __bfloat162float(kb[e]), acc);
+        }
+        sc[j] = acc;
+    }
+    __syncthreads();
+    // ---- m = max s (exact in any order), then E and l = sum E in a fixed order
+    float mx = -CUDART_INF_F;
+    for (int j = tid; j < nk; j += NT) mx = fmaxf(mx, sc[j]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) red[warp] = mx;
+    __syncthreads();
+    mx = red[0];
+#pragma unroll
+    for (int w = 1; w < DA_WARPS; ++w) mx = fmaxf(mx, red[w]);
+    const float m = mx * scale_log2;
+    __syncthreads();
+    float ls = 0.f;
+    for (int j = tid; j < nk; j += NT) {
+        const float e = exp2f(fmaf(sc[j], scale_log2, -m));
+        sc[j] = e;
+        ls += e;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, o);
+    if (lane == 0) red[warp] = ls;
+    __syncthreads();
+    float l = red[0];
+#pragma unroll
+    for (int w = 1; w < DA_WARPS; ++w) l += red[w];
+    const float inv_l = 1.f / l;
+    // ---- O = sum_j RNE_bf16(E_j / l) v_j: warp w takes keys w, w + 16, ...; lane the dims lane*DPL ..
+    float o[DPL];
+#pragma unroll
+    for (int d = 0; d < DPL; ++d) o[d] = 0.f;
+    constexpr int U = 4;
+    for (int j0 = warp; j0 < nk; j0 += DA_WARPS * U) {
+        float vv[U][DPL], pp[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int j = j0 + u * DA_WARPS;
+            pp[u] = 0.f;
+#pragma unroll
+            for (int d = 0; d < DPL; ++d) vv[u][d] = 0.f;
+            if (j < nk) {
+                const __nv_bfloat16* vrow = qkv + ((size_t)j * B + b) * ld + v_col0 + kvh * HD + lane * DPL;
+                if (DPL == 4) {
+                    const uint2 w2 = __ldg(reinterpret_cast<const uint2*>(vrow));
+                    const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(&w2);
+#pragma unroll
+                    for (int d = 0; d < 4; ++d) vv[u][d] = __bfloat162float(vb[d]);
+                } else {
+                    const uint32_t w1 = __ldg(reinterpret_cast<const uint32_t*>(vrow));
+                    const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(&w1);
+#pragma unroll
+                    for (int d = 0; d < DPL; ++d) vv[u][d] = __bfloat162float(vb[d]);
+                }
+                pp[u] = __bfloat162float(__float2bfloat16_rn(sc[j] * inv_l));   // P rounded after normalisation
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int d = 0; d < DPL; ++d) o[d] = fmaf(pp[u], vv[u][d], o[d]);
+    }
+#pragma unroll
+    for (int d = 0; d < DPL; ++d) opart[warp * HD + lane * DPL + d] = o[d];
+    __syncthreads();
+    __nv_bfloat16* orow = out + ((size_t)t * B + b) * ldo + h * HD;
+    for (int d = tid; d < HD; d += NT) {
+        float acc = opart[d];
+#pragma unroll
+        for (int w = 1; w < DA_WARPS; ++w) acc += opart[w * HD + d];
+        orow[d] = __float2bfloat16_rn(acc);
+    }
+}
+
+cudaError_t launch_decode_attention(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int ldo, int t1, int B,
+                                    int n_heads, int n_kv_heads, int hd, int k_col0, int v_col0, float score_scale,
+                                    cudaStream_t s, bool pdl, const int* dyn, int max_keys) {
+    const dim3 grid(n_heads, B);
+    const int group = n_heads / n_kv_heads;
+    const float scale_log2 = score_scale * 1.4426950408889634f;
+    if (max_keys > kDecodeMaxKeys) return cudaErrorInvalidValue;
+    const int sm = (32 + DA_WARPS * hd + hd + max_keys) * (int)sizeof(float);
+    const int sm_max = (32 + DA_WARPS * hd + hd + kDecodeMaxKeys) * (int)sizeof(float);   // the attribute, set once
+    if (hd == 64) {
+        cudaError_t e = smem_attr_once<decode_attention_kernel<64>>(sm_max);
+        if (e != cudaSuccess) return e;
+        return launch_pdl(decode_attention_kernel<64>, grid, dim3(DA_WARPS * 32), sm, s, pdl, qkv, ld, out, ldo, t1, B,
+                          group, k_col0, v_col0, scale_log2, dyn);
+    }
+    if (hd == 128) {
+        cudaError_t e = smem_attr_once<decode_attention_kernel<128>>(sm_max);
+        if (e != cudaSuccess) return e;
+        return launch_pdl(decode_attention_kernel<128>, grid, dim3(DA_WARPS * 32), sm, s, pdl, qkv, ld, out, ldo, t1,
+                          B, group, k_col0, v_col0, scale_log2, dyn);
+    }
+    return cudaErrorNotSupported;
+}
+
 cudaError_t launch_attention_simt(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int ldo, int t0, int t1,
                                   int B, int n_heads, int n_kv_heads, int hd, int k_col0, int v_col0,
                                   float score_scale, cudaStream_t s) {
