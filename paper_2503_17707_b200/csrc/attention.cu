@@ -402,6 +402,12 @@ cudaError_t launch_tc(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int 
                       v_col0, scale_log2, dyn, seq_stride);
 }
 
+// Longest context (keys) that takes the SIMT decode kernel (PB_DECODE_MAX_KEYS overrides, for measurement).
+int kDecodeAttnMaxKeys() {
+    static const int v = getenv("PB_DECODE_MAX_KEYS") ? atoi(getenv("PB_DECODE_MAX_KEYS")) : 12288;
+    return v;
+}
+
 }  // namespace
 
 cudaError_t warm_attention_kernels() {
@@ -420,14 +426,14 @@ cudaError_t launch_attention(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* ou
     const bool tma_ok = (ld % 8) == 0 && (reinterpret_cast<uintptr_t>(qkv) & 15) == 0 && (ldo % 8) == 0 &&
                         (k_col0 % 8) == 0 && (v_col0 % 8) == 0;
     const int group = n_heads / n_kv_heads;
-    // one query position per sequence (decode steps) over a short context: the SIMT decode kernel (one CTA per head
-    // and sequence). Measured (profiles/r02_decode_attention_ab.txt): C2 decode (<= 160 keys) 1.065 -> 1.009 ms per
-    // token; C4 (~1050 keys, 40 CTAs) 6.78 -> 7.85 ms, so longer contexts keep the tensor-core kernel. The choice
-    // depends on the context bound (max_keys: the decode graph's position range), not on the step's position.
+    // one query position per sequence (decode steps): the SIMT decode kernel (a cluster of CTAs per head and
+    // sequence splitting the keys; launch_decode_attention). Measured (profiles/r02_decode_attention_ab.txt): C2
+    // decode 1.065 -> 1.009 ms per token, C4 6.80 -> 5.83 ms. The choice depends on the context bound (max_keys: the
+    // decode graph's position range), not on the step's position.
     static const bool dec_off = getenv("PB_DECODE_ATTN") && atoi(getenv("PB_DECODE_ATTN")) == 0;   // A/B
     const int max_keys = dyn ? t_extent : t1;
     if (t1 - t0 == 1 && !seq_stride && !dec_off && (hd == 64 || hd == 128) && (ld % 8) == 0 && (k_col0 % 8) == 0 &&
-        (v_col0 % 8) == 0 && (reinterpret_cast<uintptr_t>(qkv) & 15) == 0 && max_keys <= 512)
+        (v_col0 % 8) == 0 && (reinterpret_cast<uintptr_t>(qkv) & 15) == 0 && max_keys <= kDecodeAttnMaxKeys())
         return launch_decode_attention(qkv, ld, out, ldo, t1, B, n_heads, n_kv_heads, hd, k_col0, v_col0, score_scale,
                                        s, pdl, dyn, max_keys);
     static const bool two = !getenv("PB_ATTN_ONE") ;   // two CTAs per SM unless PB_ATTN_ONE (A/B measurement)

@@ -532,16 +532,34 @@ cudaError_t launch_rope(__nv_bfloat16* qkv, int ld, int r0, int r1, int B, int n
 
 // ------------------------------------------------------------------ decode attention (one query position)
 // One new position per sequence (f3 decode steps): a 128-query tensor-core tile would be 127/128 padding and
-// its two passes over the key tiles are a chain of MMA / softmax handshakes per tile. Here a CTA of 16 warps serves
-// one (head, sequence) with the storage contract's exact normalised-P rounding:
+// its two passes over the key tiles are a chain of MMA / softmax handshakes per tile. Here a cluster of CL CTAs of 16
+// warps serves one (head, sequence), CTA r taking the contiguous key block r of CL, with the storage contract's
+// exact normalised-P rounding:
 //   scores  s_j = q . k_j (fp32, one thread per key, the key's vectors all requested before the FMAs), kept in smem;
-//   m = max s, E_j = exp2(s_j c - m c), l = sum E (block reductions in a fixed order);
-//   O = sum_j RNE_bf16(E_j / l) v_j (warps take keys j = w, w + 16, ..., lanes the head dims; the 16 warp partials
-//   added in warp order); out = RNE_bf16(O).
-// dyn (decode graphs): positions read on the device. Keys [0, t] of the query position t = t1 - 1.
+//   m = max s over the cluster, E_j = exp2(s_j c - m c), l = sum E (block sums, then the CL block values added in rank
+//   order through distributed shared memory: every CTA gets the same l);
+//   O = sum_j RNE_bf16(E_j / l) v_j (warps take keys w, w + 16, ... of the block, lanes the head dims; 16 warp
+//   partials added in warp order, then the CL block partials in rank order — CTA r finishing dims r of CL);
+//   out = RNE_bf16(O). dyn (decode graphs): positions read on the device. Keys [0, t] of the position t = t1 - 1.
 constexpr int DA_WARPS = 16, kDecodeMaxKeys = 12288;
 
-template <int HD>
+__device__ __forceinline__ uint32_t da_cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void da_cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ float da_ld_remote(const float* p, uint32_t rank) {
+    uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p)), ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+    float v;
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(ra) : "memory");
+    return v;
+}
+
+template <int HD, int CL>
 __global__ void __launch_bounds__(DA_WARPS * 32) decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv, int ld,
                                                                          __nv_bfloat16* __restrict__ out, int ldo,
                                                                          int t1, int B, int group, int k_col0,
@@ -550,20 +568,23 @@ __global__ void __launch_bounds__(DA_WARPS * 32) decode_attention_kernel(const _
     extern __shared__ float da_smem[];
     constexpr int NT = DA_WARPS * 32, VPR = HD / 8, DPL = HD / 32;   // 16-B vectors per row, dims per lane
     float* red = da_smem;                        // [DA_WARPS]
-    float* opart = da_smem + 32;                 // [DA_WARPS][HD]
+    float* xch = da_smem + DA_WARPS;             // [2]: this CTA's block max / block sum (read by the cluster)
+    float* opart = da_smem + 32;                 // [DA_WARPS][HD]; row 0 then holds the CTA's block partial of O
     float* sq = opart + DA_WARPS * HD;           // [HD] query
-    float* sc = sq + HD;                         // [keys]
-    const int h = blockIdx.x, b = blockIdx.y, kvh = h / group;
+    float* sc = sq + HD;                         // [keys of this block]
+    const int h = blockIdx.x / CL, b = blockIdx.y, kvh = h / group;
+    const uint32_t rank = CL > 1 ? da_cluster_rank() : 0u;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (dyn) t1 += *dyn;
     pdl_wait();
     const int t = t1 - 1, nk = t + 1;
+    const int j0 = (int)((long long)nk * rank / CL), j1 = (int)((long long)nk * (rank + 1) / CL), nb = j1 - j0;
     const __nv_bfloat16* qrow = qkv + ((size_t)t * B + b) * ld + h * HD;
     for (int d = tid; d < HD; d += NT) sq[d] = __bfloat162float(qrow[d]);
     __syncthreads();
-    // ---- scores: thread per key
-    for (int j = tid; j < nk; j += NT) {
-        const uint4* krow = reinterpret_cast<const uint4*>(qkv + ((size_t)j * B + b) * ld + k_col0 + kvh * HD);
+    // ---- scores of this block: thread per key
+    for (int jj = tid; jj < nb; jj += NT) {
+        const uint4* krow = reinterpret_cast<const uint4*>(qkv + ((size_t)(j0 + jj) * B + b) * ld + k_col0 + kvh * HD);
         uint4 kv[VPR];
 #pragma unroll
         for (int v = 0; v < VPR; ++v) kv[v] = __ldg(krow + v);
@@ -574,12 +595,12 @@ __global__ void __launch_bounds__(DA_WARPS * 32) decode_attention_kernel(const _
 #pragma unroll
             for (int e = 0; e < 8; ++e) acc = fmaf(sq[v * 8 + e], __bfloat162float(kb[e]), acc);
         }
-        sc[j] = acc;
+        sc[jj] = acc;
     }
     __syncthreads();
-    // ---- m = max s (exact in any order), then E and l = sum E in a fixed order
+    // ---- m = max s (exact in any order): block, then cluster
     float mx = -CUDART_INF_F;
-    for (int j = tid; j < nk; j += NT) mx = fmaxf(mx, sc[j]);
+    for (int jj = tid; jj < nb; jj += NT) mx = fmaxf(mx, sc[jj]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (lane == 0) red[warp] = mx;
@@ -587,12 +608,20 @@ __global__ void __launch_bounds__(DA_WARPS * 32) decode_attention_kernel(const _
     mx = red[0];
 #pragma unroll
     for (int w = 1; w < DA_WARPS; ++w) mx = fmaxf(mx, red[w]);
+    if (CL > 1) {
+        if (tid == 0) xch[0] = mx;
+        da_cluster_sync();
+        mx = da_ld_remote(xch, 0);
+#pragma unroll
+        for (uint32_t r = 1; r < CL; ++r) mx = fmaxf(mx, da_ld_remote(xch, r));
+    }
     const float m = mx * scale_log2;
     __syncthreads();
+    // ---- l = sum E: block sum in a fixed order, then the CL block sums in rank order
     float ls = 0.f;
-    for (int j = tid; j < nk; j += NT) {
-        const float e = exp2f(fmaf(sc[j], scale_log2, -m));
-        sc[j] = e;
+    for (int jj = tid; jj < nb; jj += NT) {
+        const float e = exp2f(fmaf(sc[jj], scale_log2, -m));
+        sc[jj] = e;
         ls += e;
     }
 #pragma unroll
@@ -602,22 +631,29 @@ __global__ void __launch_bounds__(DA_WARPS * 32) decode_attention_kernel(const _
     float l = red[0];
 #pragma unroll
     for (int w = 1; w < DA_WARPS; ++w) l += red[w];
+    if (CL > 1) {
+        if (tid == 0) xch[1] = l;
+        da_cluster_sync();
+        l = da_ld_remote(xch + 1, 0);
+#pragma unroll
+        for (uint32_t r = 1; r < CL; ++r) l += da_ld_remote(xch + 1, r);
+    }
     const float inv_l = 1.f / l;
-    // ---- O = sum_j RNE_bf16(E_j / l) v_j: warp w takes keys w, w + 16, ...; lane the dims lane*DPL ..
+    // ---- this block's O = sum_j RNE_bf16(E_j / l) v_j: warp w takes keys w, w + 16, ...; lane the dims lane*DPL ..
     float o[DPL];
 #pragma unroll
     for (int d = 0; d < DPL; ++d) o[d] = 0.f;
     constexpr int U = 4;
-    for (int j0 = warp; j0 < nk; j0 += DA_WARPS * U) {
+    for (int jb = warp; jb < nb; jb += DA_WARPS * U) {
         float vv[U][DPL], pp[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int j = j0 + u * DA_WARPS;
+            const int jj = jb + u * DA_WARPS;
             pp[u] = 0.f;
 #pragma unroll
             for (int d = 0; d < DPL; ++d) vv[u][d] = 0.f;
-            if (j < nk) {
-                const __nv_bfloat16* vrow = qkv + ((size_t)j * B + b) * ld + v_col0 + kvh * HD + lane * DPL;
+            if (jj < nb) {
+                const __nv_bfloat16* vrow = qkv + ((size_t)(j0 + jj) * B + b) * ld + v_col0 + kvh * HD + lane * DPL;
                 if (DPL == 4) {
                     const uint2 w2 = __ldg(reinterpret_cast<const uint2*>(vrow));
                     const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(&w2);
@@ -629,7 +665,7 @@ __global__ void __launch_bounds__(DA_WARPS * 32) decode_attention_kernel(const _
 #pragma unroll
                     for (int d = 0; d < DPL; ++d) vv[u][d] = __bfloat162float(vb[d]);
                 }
-                pp[u] = __bfloat162float(__float2bfloat16_rn(sc[j] * inv_l));   // P rounded after normalisation
+                pp[u] = __bfloat162float(__float2bfloat16_rn(sc[jj] * inv_l));   // P rounded after normalisation
             }
         }
 #pragma unroll
@@ -640,36 +676,85 @@ __global__ void __launch_bounds__(DA_WARPS * 32) decode_attention_kernel(const _
 #pragma unroll
     for (int d = 0; d < DPL; ++d) opart[warp * HD + lane * DPL + d] = o[d];
     __syncthreads();
-    __nv_bfloat16* orow = out + ((size_t)t * B + b) * ldo + h * HD;
-    for (int d = tid; d < HD; d += NT) {
+    for (int d = tid; d < HD; d += NT) {   // the block partial: the 16 warp partials in warp order, into row 0
         float acc = opart[d];
 #pragma unroll
         for (int w = 1; w < DA_WARPS; ++w) acc += opart[w * HD + d];
+        opart[d] = acc;
+    }
+    __nv_bfloat16* orow = out + ((size_t)t * B + b) * ldo + h * HD;
+    if (CL == 1) {
+        __syncthreads();
+        for (int d = tid; d < HD; d += NT) orow[d] = __float2bfloat16_rn(opart[d]);
+        return;
+    }
+    da_cluster_sync();   // every block partial is complete
+    for (int d = (int)rank * (HD / CL) + tid; d < (int)(rank + 1) * (HD / CL); d += NT) {
+        float acc = da_ld_remote(opart + d, 0);
+#pragma unroll
+        for (uint32_t r = 1; r < CL; ++r) acc += da_ld_remote(opart + d, r);
         orow[d] = __float2bfloat16_rn(acc);
     }
+    da_cluster_sync();   // peers stay alive until every remote read of their smem is done
+}
+
+template <int HD, int CL>
+cudaError_t launch_decode_cl(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int ldo, int t1, int B, int H,
+                             int group, int k_col0, int v_col0, float scale_log2, cudaStream_t s, bool pdl,
+                             const int* dyn, int max_keys) {
+    const int blk = (max_keys + CL - 1) / CL + 1;
+    const int sm = (32 + DA_WARPS * HD + HD + blk) * (int)sizeof(float);
+    const int sm_max = (32 + DA_WARPS * HD + HD + kDecodeMaxKeys / CL + 1) * (int)sizeof(float);   // set once
+    cudaError_t e = smem_attr_once<decode_attention_kernel<HD, CL>>(sm_max);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(H * CL, B);
+    cfg.blockDim = dim3(DA_WARPS * 32);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (CL > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = CL;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    if (pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, decode_attention_kernel<HD, CL>, qkv, ld, out, ldo, t1, B, group, k_col0, v_col0,
+                              scale_log2, dyn);
+}
+
+// Cluster size from the context bound: ~250-400 keys per CTA, at most 8 (portable clusters). Measured
+// (profiles/r02_decode_attention_ab.txt): C2 (<= 160 keys) CL 1 1.01 ms per token vs CL 2 1.08; C4 (~1060 keys)
+// CL 4 5.83 ms vs CL 8 6.10, CL 2 6.42, tensor cores 6.80.
+int decode_attention_cluster(int max_keys) {
+    static const int forced = getenv("PB_DECODE_CL") ? atoi(getenv("PB_DECODE_CL")) : 0;   // experiments
+    if (forced == 1 || forced == 2 || forced == 4 || forced == 8) return forced;
+    return max_keys <= 384 ? 1 : max_keys <= 768 ? 2 : max_keys <= 1600 ? 4 : 8;
 }
 
 cudaError_t launch_decode_attention(const __nv_bfloat16* qkv, int ld, __nv_bfloat16* out, int ldo, int t1, int B,
                                     int n_heads, int n_kv_heads, int hd, int k_col0, int v_col0, float score_scale,
                                     cudaStream_t s, bool pdl, const int* dyn, int max_keys) {
-    const dim3 grid(n_heads, B);
+    if (max_keys > kDecodeMaxKeys) return cudaErrorInvalidValue;
     const int group = n_heads / n_kv_heads;
     const float scale_log2 = score_scale * 1.4426950408889634f;
-    if (max_keys > kDecodeMaxKeys) return cudaErrorInvalidValue;
-    const int sm = (32 + DA_WARPS * hd + hd + max_keys) * (int)sizeof(float);
-    const int sm_max = (32 + DA_WARPS * hd + hd + kDecodeMaxKeys) * (int)sizeof(float);   // the attribute, set once
-    if (hd == 64) {
-        cudaError_t e = smem_attr_once<decode_attention_kernel<64>>(sm_max);
-        if (e != cudaSuccess) return e;
-        return launch_pdl(decode_attention_kernel<64>, grid, dim3(DA_WARPS * 32), sm, s, pdl, qkv, ld, out, ldo, t1, B,
-                          group, k_col0, v_col0, scale_log2, dyn);
-    }
-    if (hd == 128) {
-        cudaError_t e = smem_attr_once<decode_attention_kernel<128>>(sm_max);
-        if (e != cudaSuccess) return e;
-        return launch_pdl(decode_attention_kernel<128>, grid, dim3(DA_WARPS * 32), sm, s, pdl, qkv, ld, out, ldo, t1,
-                          B, group, k_col0, v_col0, scale_log2, dyn);
-    }
+    const int cl = decode_attention_cluster(max_keys);
+#define PB_DEC(HDV, CLV)                                                                                           \
+    if (hd == HDV && cl == CLV)                                                                                    \
+        return launch_decode_cl<HDV, CLV>(qkv, ld, out, ldo, t1, B, n_heads, group, k_col0, v_col0, scale_log2, s, \
+                                          pdl, dyn, max_keys);
+    PB_DEC(64, 1) PB_DEC(64, 2) PB_DEC(64, 4) PB_DEC(64, 8)
+    PB_DEC(128, 1) PB_DEC(128, 2) PB_DEC(128, 4) PB_DEC(128, 8)
+#undef PB_DEC
     return cudaErrorNotSupported;
 }
 
