@@ -194,7 +194,8 @@ def test_norm(rms, d):
                                                   # one query position (decode steps): the SIMT decode kernel
                                                   (300, 2, 4, 2, 128, 299, 300), (129, 3, 4, 4, 64, 128, 129),
                                                   (1, 1, 2, 1, 128, 0, 1), (500, 1, 8, 2, 128, 499, 500),
-                                                  (2000, 1, 8, 2, 128, 1999, 2000)])   # (> 512 keys: tensor cores)
+                                                  (1000, 2, 4, 2, 64, 999, 1000),
+                                                  (2000, 1, 8, 2, 128, 1999, 2000)])   # clusters of 1, 2, 4, 8 CTAs
 def test_attention(T, Bsz, H, KVH, hd, t0, t1):
     """Tensor-core kernel for hd 64/128 (SIMT for 32) vs the oracle's exact causal attention. Bound: the final
     bf16 rounding (1 ulp, 2 allowed) plus the bf16 rounding of the probabilities fed to the PV product (relative
