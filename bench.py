@@ -545,6 +545,9 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {world}"
     dev = 0 if args.same_gpu else local
+    if dev >= torch.cuda.device_count():
+        sys.exit(f"bench.py: rank {rank} needs cuda:{dev} but {torch.cuda.device_count()} GPU(s) are visible "
+                 f"(--same-gpu runs every rank on cuda:0 for testing)")
     init = {}   # init breakdown, excluded from t0 ("Load Model Ckpt" / "Init Meta")
     ti = time.perf_counter()
     torch.cuda.set_device(dev)
